@@ -1,0 +1,1050 @@
+/* oracle.c -- plain, slow, obviously-correct fp64 CPU oracle.
+ *
+ * TEST INFRASTRUCTURE ONLY (see oracle.h).  Everything here is IEEE fp64,
+ * no fast-math, no blocking or fusion beyond the definitions it cites.
+ * Readings of the paper where it is silent are those of SURVEY.md §8(c)
+ * (R1..R24) and are listed in DESIGN.md §3.
+ */
+#include "oracle.h"
+
+#include <math.h>
+#include <stdlib.h>
+#include <string.h>
+#ifdef _OPENMP
+#include <omp.h>
+#endif
+
+#define EPS_AMBIG 1e-6   /* epsilon = 1e-6 world units      */
+#define TAU_OV    1e-12  /* oracle overlap tolerance          */
+#define MAXL 18
+
+/* ======================================================================
+ * Segment algebra.  PAPER.md:386-394 (Eq. aggregate), 398-404 (Eq.
+ * identityinverse), 506-516 (Eq. segsplit), 529-538 (Eq. segaverage),
+ * 364-375 (Eq. ABconstant), 481-488 (background).
+ * Orientation: "near" is the segment closer to the camera =
+ * (A2,B2) of Eq. aggregate; "far" is (A1,B1).
+ * ==================================================================== */
+void orc_combine(double an, double bn, double af, double bf, double* a, double* b) {
+  *a = an * af;          /* A2 A1      */
+  *b = bn + an * bf;     /* B2 + A2 B1 */
+}
+
+int orc_inverse(double a, double b, double* ai, double* bi) {
+  if (!(a > 0.0)) return -1;         /* opaque segments have no inverse */
+  *ai = 1.0 / a;
+  *bi = -b / a;
+  return 0;
+}
+
+/* Split (A,B) of length dx1+dx2 into pieces of lengths dx1, dx2 (Eq. segsplit). */
+int orc_split(double a, double b, double dx1, double dx2, double out[4]) {
+  if (dx1 < 0.0 || dx2 < 0.0 || !(dx1 + dx2 > 0.0)) return -1;
+  double dx = dx1 + dx2;
+  double d[2] = {dx1, dx2};
+  for (int i = 0; i < 2; ++i) {
+    double ai = pow(a, d[i] / dx);
+    double bi = (a == 1.0) ? b * d[i] / dx            /* special case A = 1 */
+                           : b * (1.0 - ai) / (1.0 - a);
+    out[2 * i] = ai;
+    out[2 * i + 1] = bi;
+  }
+  return 0;
+}
+
+void orc_average(double a1, double b1, double a2, double b2, double* a, double* b) {
+  *a = sqrt(a1 * a2);
+  *b = 0.5 * (b1 + b2);
+}
+
+void orc_from_constant(double beta, double gamma, double dx, double* a, double* b) {
+  *a = exp(-beta * dx);
+  *b = (beta == 0.0) ? gamma * dx : gamma / beta * (1.0 - *a);   /* beta -> 0 limit */
+}
+
+double orc_background(double a, double b, double Ib) { return a * Ib + b; }
+
+/* ======================================================================
+ * Quadrature.  Gauss-Legendre on [0,1] (textbook Newton on P_N) and the
+ * Lagrange-basis integral table S_jk = int_0^{u_j} l_k(u) du.
+ * ==================================================================== */
+void orc_gauss_legendre(int N, double* u, double* w) {
+  for (int i = 0; i < N; ++i) {
+    double x = cos(M_PI * (i + 0.75) / (N + 0.5));
+    double dp = 1.0;
+    for (int it = 0; it < 100; ++it) {
+      double p0 = 1.0, p1 = x;
+      for (int k = 2; k <= N; ++k) {
+        double p2 = ((2.0 * k - 1.0) * x * p1 - (k - 1.0) * p0) / k;
+        p0 = p1;
+        p1 = p2;
+      }
+      if (N == 1) { p1 = x; p0 = 1.0; }
+      dp = N * (x * p1 - p0) / (x * x - 1.0);
+      double dx = p1 / dp;
+      x -= dx;
+      if (fabs(dx) < 1e-16) break;
+    }
+    /* recompute derivative at the converged root */
+    {
+      double p0 = 1.0, p1 = x;
+      for (int k = 2; k <= N; ++k) {
+        double p2 = ((2.0 * k - 1.0) * x * p1 - (k - 1.0) * p0) / k;
+        p0 = p1;
+        p1 = p2;
+      }
+      if (N == 1) { p1 = x; p0 = 1.0; }
+      dp = N * (x * p1 - p0) / (x * x - 1.0);
+    }
+    /* x descending in i -> u ascending */
+    u[i] = 0.5 * (1.0 - x);
+    w[i] = 1.0 / ((1.0 - x * x) * dp * dp);   /* (2/((1-x^2)P'^2)) / 2 */
+  }
+}
+
+static double lagrange_basis_at(int N, const double* u, int k, double t) {
+  double v = 1.0;
+  for (int m = 0; m < N; ++m)
+    if (m != k) v *= (t - u[m]) / (u[k] - u[m]);
+  return v;
+}
+
+void orc_lagrange_integrals(int N, const double* u, double* S) {
+  double gu[64], gw[64];
+  orc_gauss_legendre(N, gu, gw);   /* N-point GL is exact for degree N-1 basis polys */
+  for (int j = 0; j < N; ++j)
+    for (int k = 0; k < N; ++k) {
+      double s = 0.0;
+      for (int q = 0; q < N; ++q) s += gw[q] * u[j] * lagrange_basis_at(N, u, k, u[j] * gu[q]);
+      S[j * N + k] = s;
+    }
+}
+
+/* Eq. ABgeneral with s measured from the near (downstream,
+ * camera-side) end x2: a = exp(-int_0^L kappa),
+ * b_c = int_0^L q_c(s) exp(-int_0^s kappa) ds.  Composite 16-point
+ * Gauss-Legendre panels, panel count doubled until two successive estimates
+ * agree to 1e-13 (the "exact mode" of SURVEY §8(c) step 5). */
+#define EX_NQ 16
+static void composite_eval(orc_medium_fn fn, void* ctx, double L, int M, const double* u,
+                           const double* w, const double* S, double* a, double b[3]) {
+  double tau0 = 0.0, bb[3] = {0, 0, 0};
+  double h = L / M;
+  for (int m = 0; m < M; ++m) {
+    double kap[EX_NQ], q[EX_NQ][3];
+    for (int j = 0; j < EX_NQ; ++j) fn(ctx, (m + u[j]) * h, &kap[j], q[j]);
+    double panel = 0.0;
+    for (int j = 0; j < EX_NQ; ++j) panel += w[j] * kap[j];
+    panel *= h;
+    for (int j = 0; j < EX_NQ; ++j) {
+      double part = 0.0;
+      for (int k = 0; k < EX_NQ; ++k) part += S[j * EX_NQ + k] * kap[k];
+      double tau = tau0 + h * part;
+      double att = exp(-tau);
+      for (int c = 0; c < 3; ++c) bb[c] += h * w[j] * q[j][c] * att;
+    }
+    tau0 += panel;
+  }
+  *a = exp(-tau0);
+  for (int c = 0; c < 3; ++c) b[c] = bb[c];
+}
+
+int orc_segment_exact(orc_medium_fn fn, void* ctx, double L, double* a, double b[3]) {
+  double u[EX_NQ], w[EX_NQ], S[EX_NQ * EX_NQ];
+  orc_gauss_legendre(EX_NQ, u, w);
+  orc_lagrange_integrals(EX_NQ, u, S);
+  if (!(L > 0.0)) {
+    *a = 1.0;
+    b[0] = b[1] = b[2] = 0.0;
+    return 0;
+  }
+  double ap, bp[3];
+  composite_eval(fn, ctx, L, 1, u, w, S, &ap, bp);
+  for (int M = 2; M <= 1024; M *= 2) {
+    double ac, bc[3];
+    composite_eval(fn, ctx, L, M, u, w, S, &ac, bc);
+    int ok = fabs(ac - ap) <= 1e-13;
+    for (int c = 0; c < 3; ++c) ok = ok && fabs(bc[c] - bp[c]) <= 1e-13 * fmax(1.0, fabs(bc[c]));
+    ap = ac;
+    memcpy(bp, bc, sizeof bp);
+    if (ok) {
+      *a = ap;
+      memcpy(b, bp, sizeof bp);
+      return M;
+    }
+  }
+  *a = ap;
+  memcpy(b, bp, sizeof bp);
+  return -1;
+}
+
+/* SURVEY §8(c) R13, written out step by step in fp64 ("rule mode"). */
+void orc_segment_rule(int N, orc_medium_fn fn, void* ctx, double L, double* a, double b[3]) {
+  double u[64], w[64], S[64 * 64], kap[64], q[64][3];
+  orc_gauss_legendre(N, u, w);
+  orc_lagrange_integrals(N, u, S);
+  for (int j = 0; j < N; ++j) fn(ctx, u[j] * L, &kap[j], q[j]);
+  double sum = 0.0;
+  for (int j = 0; j < N; ++j) sum += w[j] * kap[j];
+  *a = exp(-L * sum);
+  double bb[3] = {0, 0, 0};
+  for (int j = 0; j < N; ++j) {
+    double tau = 0.0;
+    for (int k = 0; k < N; ++k) tau += S[j * N + k] * kap[k];
+    tau *= L;
+    for (int c = 0; c < 3; ++c) bb[c] += w[j] * q[j][c] * exp(-tau);
+  }
+  for (int c = 0; c < 3; ++c) b[c] = L * bb[c];
+}
+
+/* ======================================================================
+ * Geometry.  Gauss-Lobatto nodes, Lagrange
+ * basis (Eq. nodal), tensor-product map (Eq. tensorgeom),
+ * element = subcube of the tree.
+ * ==================================================================== */
+void orc_gll(int R, double* eta) {
+  if (R == 1) { eta[0] = 0.0; eta[1] = 1.0; }
+  else { eta[0] = 0.0; eta[1] = 0.5; eta[2] = 1.0; }   /* R = 2 */
+}
+
+void orc_lagrange(int R, const double* eta, double t, double* psi, double* dpsi) {
+  for (int m = 0; m <= R; ++m) {
+    double v = 1.0, dv = 0.0;
+    for (int q = 0; q <= R; ++q) {
+      if (q == m) continue;
+      double f = (t - eta[q]) / (eta[m] - eta[q]);
+      double df = 1.0 / (eta[m] - eta[q]);
+      dv = dv * f + v * df;
+      v *= f;
+    }
+    psi[m] = v;
+    if (dpsi) dpsi[m] = dv;
+  }
+}
+
+static void tree_map_jac(const orc_scene* sc, int k, const double t[3], double x[3], double dxdt[9]) {
+  int R = sc->R, n1 = R + 1;
+  double eta[3], p[3][3], dp[3][3];
+  orc_gll(R, eta);
+  for (int d = 0; d < 3; ++d) orc_lagrange(R, eta, t[d], p[d], dp[d]);
+  for (int c = 0; c < 3; ++c) x[c] = 0.0;
+  if (dxdt) for (int c = 0; c < 9; ++c) dxdt[c] = 0.0;
+  const double* z = sc->tree_ctrl + (size_t)k * n1 * n1 * n1 * 3;
+  for (int m3 = 0; m3 < n1; ++m3)
+    for (int m2 = 0; m2 < n1; ++m2)
+      for (int m1 = 0; m1 < n1; ++m1) {
+        const double* zz = z + ((m3 * n1 + m2) * n1 + m1) * 3;
+        double s = p[0][m1] * p[1][m2] * p[2][m3];
+        double s1 = dp[0][m1] * p[1][m2] * p[2][m3];
+        double s2 = p[0][m1] * dp[1][m2] * p[2][m3];
+        double s3 = p[0][m1] * p[1][m2] * dp[2][m3];
+        for (int c = 0; c < 3; ++c) {
+          x[c] += zz[c] * s;
+          if (dxdt) {
+            dxdt[c * 3 + 0] += zz[c] * s1;
+            dxdt[c * 3 + 1] += zz[c] * s2;
+            dxdt[c * 3 + 2] += zz[c] * s3;
+          }
+        }
+      }
+}
+
+void orc_tree_map(const orc_scene* sc, int k, const double t[3], double x[3]) {
+  tree_map_jac(sc, k, t, x, NULL);
+}
+
+static double elem_h(const orc_scene* sc, int64_t e) { return ldexp(1.0, -(int)sc->level[e]); }
+
+/* X_E(xi) = J_k(a 2^-18 + 2^-l xi); J = dX_E/dxi (row c, column d). */
+void orc_element_map(const orc_scene* sc, int64_t e, const double xi[3], double x[3], double J[9]) {
+  double h = elem_h(sc, e), t[3], dt[9];
+  for (int d = 0; d < 3; ++d) t[d] = ldexp((double)sc->anchor[3 * e + d], -MAXL) + h * xi[d];
+  tree_map_jac(sc, sc->tree[e], t, x, J ? dt : NULL);
+  if (J) for (int c = 0; c < 9; ++c) J[c] = h * dt[c];
+}
+
+/* Eq. camerageometry; orthographic per SURVEY R4. */
+void orc_camera_transform(const orc_camera* cam, const double x[3], double X[3]) {
+  double d[3] = {x[0] - cam->origin[0], x[1] - cam->origin[1], x[2] - cam->origin[2]};
+  double n = sqrt(cam->view[0] * cam->view[0] + cam->view[1] * cam->view[1] + cam->view[2] * cam->view[2]);
+  X[0] = cam->right[0] * d[0] + cam->right[1] * d[1] + cam->right[2] * d[2];
+  X[1] = cam->up[0] * d[0] + cam->up[1] * d[1] + cam->up[2] * d[2];
+  X[2] = (cam->view[0] * d[0] + cam->view[1] * d[1] + cam->view[2] * d[2]) / n;
+}
+
+/* Eq. ray: o + alpha r, r = v + l((i-(w-1)/2) t + (j-(h-1)/2) u).
+ * Orthographic: origin P0 + l(...), direction d. */
+void orc_ray(const orc_camera* cam, int i, int j, double o[3], double r[3]) {
+  double di = cam->pixel_size * (i - 0.5 * (cam->width - 1));
+  double dj = cam->pixel_size * (j - 0.5 * (cam->height - 1));
+  for (int c = 0; c < 3; ++c) {
+    double off = di * cam->right[c] + dj * cam->up[c];
+    if (cam->projection == 0) {
+      o[c] = cam->origin[c];
+      r[c] = cam->view[c] + off;
+    } else {
+      o[c] = cam->origin[c] + off;
+      r[c] = cam->view[c];
+    }
+  }
+}
+
+static double cam_n(const orc_camera* cam) {
+  return sqrt(cam->view[0] * cam->view[0] + cam->view[1] * cam->view[1] + cam->view[2] * cam->view[2]);
+}
+static void alpha_range(const orc_camera* cam, double* amin, double* amax) {
+  if (cam->projection == 0) { *amin = 1.0; *amax = cam->far_dist / cam_n(cam); }   /* Z in [n,f] */
+  else { *amin = 0.0; *amax = cam->far_dist; }
+}
+
+/* Bernstein-Bezier control points of the element map restricted to the
+ * parameter box [lo,hi]^3 (for R=2 per axis b1 = 2 y(1/2) - (y0+y2)/2;
+ * SURVEY R6).  Lagrange values are plain evaluations of X_E. */
+static void element_bezier(const orc_scene* sc, int64_t e, const double lo[3], const double hi[3],
+                           double B[27][3]) {
+  int R = sc->R, n1 = R + 1;
+  double eta[3];
+  orc_gll(R, eta);
+  double Y[27][3];
+  for (int m3 = 0; m3 < n1; ++m3)
+    for (int m2 = 0; m2 < n1; ++m2)
+      for (int m1 = 0; m1 < n1; ++m1) {
+        double xi[3] = {lo[0] + (hi[0] - lo[0]) * eta[m1], lo[1] + (hi[1] - lo[1]) * eta[m2],
+                        lo[2] + (hi[2] - lo[2]) * eta[m3]};
+        orc_element_map(sc, e, xi, Y[(m3 * n1 + m2) * n1 + m1], NULL);
+      }
+  memcpy(B, Y, sizeof(double) * 3 * n1 * n1 * n1);
+  if (R == 2) {
+    /* apply the 1D Lagrange->Bernstein conversion along each axis */
+    for (int ax = 0; ax < 3; ++ax)
+      for (int a = 0; a < 3; ++a)
+        for (int b = 0; b < 3; ++b) {
+          int idx[3];
+          for (int m = 0; m < 3; ++m) {
+            int c3[3];
+            c3[ax] = m;
+            c3[(ax + 1) % 3] = a;
+            c3[(ax + 2) % 3] = b;
+            idx[m] = (c3[2] * 3 + c3[1]) * 3 + c3[0];
+          }
+          for (int c = 0; c < 3; ++c)
+            B[idx[1]][c] = 2.0 * B[idx[1]][c] - 0.5 * (B[idx[0]][c] + B[idx[2]][c]);
+        }
+  }
+}
+
+/* Camera-space AABB of the element's Bezier points. */
+int orc_element_aabb(const orc_scene* sc, const orc_camera* cam, int64_t e, double lo[3], double hi[3]) {
+  double B[27][3], plo[3] = {0, 0, 0}, phi[3] = {1, 1, 1};
+  element_bezier(sc, e, plo, phi, B);
+  int np = (sc->R + 1) * (sc->R + 1) * (sc->R + 1);
+  for (int c = 0; c < 3; ++c) { lo[c] = INFINITY; hi[c] = -INFINITY; }
+  for (int m = 0; m < np; ++m) {
+    double X[3];
+    orc_camera_transform(cam, B[m], X);
+    for (int c = 0; c < 3; ++c) { lo[c] = fmin(lo[c], X[c]); hi[c] = fmax(hi[c], X[c]); }
+  }
+  return 0;
+}
+
+/* Pixel-centre rectangle of a camera-space AABB:
+ * p = (n/l) X/Z + (w-1)/2 with Z clamped >= n (perspective), p = X/l + (w-1)/2
+ * (orthographic); rect = [ceil pmin, floor pmax] clipped to the image.
+ * Returns 1 if non-empty. */
+int orc_pixel_rect(const orc_camera* cam, const double lo[3], const double hi[3], int32_t rect[4]) {
+  double n = cam_n(cam), l = cam->pixel_size;
+  double pmin[2], pmax[2];
+  int dims[2] = {cam->width, cam->height};
+  rect[0] = 0; rect[1] = -1; rect[2] = 0; rect[3] = -1;
+  if (cam->projection == 0) {
+    if (hi[2] < n || lo[2] > cam->far_dist) return 0;
+    double Z[2] = {fmax(lo[2], n), fmax(hi[2], n)};
+    for (int d = 0; d < 2; ++d) {
+      double X[2] = {lo[d], hi[d]};
+      pmin[d] = INFINITY; pmax[d] = -INFINITY;
+      for (int a = 0; a < 2; ++a)
+        for (int b = 0; b < 2; ++b) {
+          double p = (n / l) * X[a] / Z[b] + 0.5 * (dims[d] - 1);
+          pmin[d] = fmin(pmin[d], p);
+          pmax[d] = fmax(pmax[d], p);
+        }
+    }
+  } else {
+    if (hi[2] < 0.0 || lo[2] > cam->far_dist) return 0;
+    for (int d = 0; d < 2; ++d) {
+      pmin[d] = lo[d] / l + 0.5 * (dims[d] - 1);
+      pmax[d] = hi[d] / l + 0.5 * (dims[d] - 1);
+    }
+  }
+  for (int d = 0; d < 2; ++d) {
+    double a = ceil(pmin[d]), b = floor(pmax[d]);
+    if (a < 0) a = 0;
+    if (b > dims[d] - 1) b = dims[d] - 1;
+    if (a > b) return 0;
+    rect[2 * d] = (int32_t)a;
+    rect[2 * d + 1] = (int32_t)b;
+  }
+  return 1;
+}
+
+/* Culled list: visible iff the pixel-centre rect is
+ * non-empty; ambiguous iff the decision differs for the AABB inflated and
+ * deflated by EPS_AMBIG.  rects[4n] receives the EPS-inflated rect (superset
+ * used for candidate pairs). */
+void orc_cull(const orc_scene* sc, const orc_camera* cam, int8_t* visible, int8_t* ambiguous,
+              int32_t* rects) {
+#pragma omp parallel for schedule(static)
+  for (int64_t e = 0; e < sc->n; ++e) {
+    double lo[3], hi[3], lp[3], hp[3], lm[3], hm[3];
+    int32_t r0[4], rp[4], rm[4];
+    orc_element_aabb(sc, cam, e, lo, hi);
+    for (int c = 0; c < 3; ++c) {
+      lp[c] = lo[c] - EPS_AMBIG; hp[c] = hi[c] + EPS_AMBIG;
+      lm[c] = lo[c] + EPS_AMBIG; hm[c] = hi[c] - EPS_AMBIG;
+    }
+    int v0 = orc_pixel_rect(cam, lo, hi, r0);
+    int vp = orc_pixel_rect(cam, lp, hp, rp);
+    int vm = orc_pixel_rect(cam, lm, hm, rm);
+    visible[e] = (int8_t)v0;
+    ambiguous[e] = (int8_t)(vp != vm);
+    if (rects) {
+      if (vp) memcpy(rects + 4 * e, rp, sizeof rp);
+      else { rects[4 * e] = 0; rects[4 * e + 1] = -1; rects[4 * e + 2] = 0; rects[4 * e + 3] = -1; }
+    }
+  }
+}
+
+/* Nodal field interpolation at element-local GLL nodes. */
+double orc_field(const orc_scene* sc, int64_t e, const double xi[3]) {
+  int P = sc->P, n1 = P + 1;
+  double eta[3], p[3][3];
+  orc_gll(P, eta);
+  for (int d = 0; d < 3; ++d) orc_lagrange(P, eta, xi[d], p[d], NULL);
+  const float* f = sc->field + (size_t)e * n1 * n1 * n1;
+  double v = 0.0;
+  for (int k3 = 0; k3 < n1; ++k3)
+    for (int k2 = 0; k2 < n1; ++k2)
+      for (int k1 = 0; k1 < n1; ++k1) v += (double)f[(k3 * n1 + k2) * n1 + k1] * p[0][k1] * p[1][k2] * p[2][k3];
+  return v;
+}
+
+static int solve3(const double A[9], const double b[3], double x[3]) {
+  double det = A[0] * (A[4] * A[8] - A[5] * A[7]) - A[1] * (A[3] * A[8] - A[5] * A[6]) +
+               A[2] * (A[3] * A[7] - A[4] * A[6]);
+  if (det == 0.0 || !isfinite(det)) return -1;
+  double inv[9];
+  inv[0] = (A[4] * A[8] - A[5] * A[7]) / det;
+  inv[1] = (A[2] * A[7] - A[1] * A[8]) / det;
+  inv[2] = (A[1] * A[5] - A[2] * A[4]) / det;
+  inv[3] = (A[5] * A[6] - A[3] * A[8]) / det;
+  inv[4] = (A[0] * A[8] - A[2] * A[6]) / det;
+  inv[5] = (A[2] * A[3] - A[0] * A[5]) / det;
+  inv[6] = (A[3] * A[7] - A[4] * A[6]) / det;
+  inv[7] = (A[1] * A[6] - A[0] * A[7]) / det;
+  inv[8] = (A[0] * A[4] - A[1] * A[3]) / det;
+  for (int r = 0; r < 3; ++r) x[r] = inv[3 * r] * b[0] + inv[3 * r + 1] * b[1] + inv[3 * r + 2] * b[2];
+  return 0;
+}
+
+/* xi with X_E(xi) = x by Newton in fp64, started from the
+ * affine model at the element centre.  Returns 0 on convergence. */
+int orc_inverse_map(const orc_scene* sc, int64_t e, const double x[3], double xi[3]) {
+  double c[3] = {0.5, 0.5, 0.5}, X[3], J[9], rhs[3], d[3];
+  orc_element_map(sc, e, c, X, J);
+  for (int k = 0; k < 3; ++k) rhs[k] = x[k] - X[k];
+  if (solve3(J, rhs, d)) return -1;
+  for (int k = 0; k < 3; ++k) xi[k] = 0.5 + d[k];
+  for (int it = 0; it < 80; ++it) {
+    orc_element_map(sc, e, xi, X, J);
+    for (int k = 0; k < 3; ++k) rhs[k] = x[k] - X[k];
+    if (solve3(J, rhs, d)) return -1;
+    for (int k = 0; k < 3; ++k) xi[k] += d[k];
+    if (fabs(d[0]) < 1e-14 && fabs(d[1]) < 1e-14 && fabs(d[2]) < 1e-14) return 0;
+    if (!(fabs(xi[0]) < 1e6 && fabs(xi[1]) < 1e6 && fabs(xi[2]) < 1e6)) return -1;
+  }
+  return -2;
+}
+
+/* ======================================================================
+ * Intersection (App. A.1).
+ * Affine trees: slab test in reference coordinates.  General trees: all
+ * roots on each face by Bezier subdivision of the projected patch (Eq.
+ * intersectiontwod, d1,d2 perpendicular to r) + fp64 Newton; inside/outside
+ * of each interval between consecutive roots decided by the inverse map.
+ * ==================================================================== */
+static int g_force_general = 0;
+/* test hook: route affine trees through the general face-root path */
+void orc_set_force_general(int on) { g_force_general = on; }
+
+static int tree_affine(const orc_scene* sc, int k, double c[3], double M[9]) {
+  if (g_force_general) return 0;
+  double t0[3] = {0, 0, 0}, x[3];
+  orc_tree_map(sc, k, t0, c);
+  for (int d = 0; d < 3; ++d) {
+    double t[3] = {0, 0, 0};
+    t[d] = 1.0;
+    orc_tree_map(sc, k, t, x);
+    for (int q = 0; q < 3; ++q) M[q * 3 + d] = x[q] - c[q];
+  }
+  int R = sc->R, n1 = R + 1;
+  double eta[3];
+  orc_gll(R, eta);
+  const double* z = sc->tree_ctrl + (size_t)k * n1 * n1 * n1 * 3;
+  for (int m3 = 0; m3 < n1; ++m3)
+    for (int m2 = 0; m2 < n1; ++m2)
+      for (int m1 = 0; m1 < n1; ++m1) {
+        const double* zz = z + ((m3 * n1 + m2) * n1 + m1) * 3;
+        double et[3] = {eta[m1], eta[m2], eta[m3]};
+        for (int q = 0; q < 3; ++q) {
+          double v = c[q] + M[q * 3] * et[0] + M[q * 3 + 1] * et[1] + M[q * 3 + 2] * et[2];
+          if (fabs(v - zz[q]) > 1e-13 * (1.0 + fabs(zz[q]))) return 0;
+        }
+      }
+  return 1;
+}
+
+static void inv3(const double A[9], double inv[9]) {
+  double e[3], x[3];
+  for (int col = 0; col < 3; ++col) {
+    e[0] = e[1] = e[2] = 0.0;
+    e[col] = 1.0;
+    solve3(A, e, x);
+    for (int r = 0; r < 3; ++r) inv[r * 3 + col] = x[r];
+  }
+}
+
+/* slab test of the ray against xi in [lo_k, hi_k]; returns 1 and [a0,a1] on hit */
+static int slab(const double xi0[3], const double dxi[3], const double lo[3], const double hi[3],
+                double amin, double amax, double* a0, double* a1) {
+  double enter = amin, exit_ = amax;
+  for (int k = 0; k < 3; ++k) {
+    if (dxi[k] == 0.0) {
+      if (xi0[k] < lo[k] || xi0[k] > hi[k]) return 0;
+      continue;
+    }
+    double t0 = (lo[k] - xi0[k]) / dxi[k], t1 = (hi[k] - xi0[k]) / dxi[k];
+    if (t0 > t1) { double tt = t0; t0 = t1; t1 = tt; }
+    if (t0 > enter) enter = t0;
+    if (t1 < exit_) exit_ = t1;
+  }
+  if (exit_ > enter) { *a0 = enter; *a1 = exit_; return 1; }
+  return 0;
+}
+
+typedef struct { double alpha, cosphi, xi[3]; } froot;
+
+typedef struct {
+  const orc_scene* sc; int64_t e; int fixk; double fixv; int ax, bx;
+  double lo_a, hi_a, lo_b, hi_b;
+  double o[3], r[3], d1[3], d2[3];
+  froot* roots; int nroots, cap, boxes, fail;
+} face_ctx;
+
+static double dot3(const double* a, const double* b) { return a[0] * b[0] + a[1] * b[1] + a[2] * b[2]; }
+static void cross3(const double* a, const double* b, double* c) {
+  c[0] = a[1] * b[2] - a[2] * b[1];
+  c[1] = a[2] * b[0] - a[0] * b[2];
+  c[2] = a[0] * b[1] - a[1] * b[0];
+}
+
+static void face_point(face_ctx* f, double s1, double s2, double xi[3]) {
+  xi[f->fixk] = f->fixv;
+  xi[f->ax] = f->lo_a + (f->hi_a - f->lo_a) * s1;
+  xi[f->bx] = f->lo_b + (f->hi_b - f->lo_b) * s2;
+}
+
+/* Newton on the projected system G(xi_a, xi_b) = (d1.(X-o), d2.(X-o)) = 0 */
+static int face_newton(face_ctx* f, double s1, double s2, froot* out, double* so1, double* so2) {
+  double xi[3], X[3], J[9];
+  face_point(f, s1, s2, xi);
+  for (int it = 0; it < 60; ++it) {
+    orc_element_map(f->sc, f->e, xi, X, J);
+    double dx[3] = {X[0] - f->o[0], X[1] - f->o[1], X[2] - f->o[2]};
+    double g1 = dot3(f->d1, dx), g2 = dot3(f->d2, dx);
+    double Xa[3] = {J[f->ax], J[3 + f->ax], J[6 + f->ax]};
+    double Xb[3] = {J[f->bx], J[3 + f->bx], J[6 + f->bx]};
+    double j11 = dot3(f->d1, Xa), j12 = dot3(f->d1, Xb), j21 = dot3(f->d2, Xa), j22 = dot3(f->d2, Xb);
+    double det = j11 * j22 - j12 * j21;
+    if (det == 0.0 || !isfinite(det)) return -1;
+    double da = (g1 * j22 - g2 * j12) / det, db = (j11 * g2 - j21 * g1) / det;
+    xi[f->ax] -= da;
+    xi[f->bx] -= db;
+    if (!(fabs(xi[f->ax]) < 10 && fabs(xi[f->bx]) < 10)) return -1;
+    if (fabs(da) < 1e-14 && fabs(db) < 1e-14) {
+      orc_element_map(f->sc, f->e, xi, X, J);
+      double Xa2[3] = {J[f->ax], J[3 + f->ax], J[6 + f->ax]};
+      double Xb2[3] = {J[f->bx], J[3 + f->bx], J[6 + f->bx]};
+      double nrm[3];
+      cross3(Xa2, Xb2, nrm);
+      double rr = dot3(f->r, f->r);
+      out->alpha = dot3(f->r, (double[3]){X[0] - f->o[0], X[1] - f->o[1], X[2] - f->o[2]}) / rr;
+      out->cosphi = fabs(dot3(nrm, f->r)) / (sqrt(dot3(nrm, nrm)) * sqrt(rr));
+      memcpy(out->xi, xi, sizeof xi);
+      *so1 = (xi[f->ax] - f->lo_a) / (f->hi_a - f->lo_a);
+      *so2 = (xi[f->bx] - f->lo_b) / (f->hi_b - f->lo_b);
+      return 0;
+    }
+  }
+  return -2;
+}
+
+/* de Casteljau split of a degree-R Bernstein patch g[(R+1)^2][2] along s1
+ * (dir 0) or s2 (dir 1) at 1/2. */
+static void bz_split(int R, const double g[9][2], int dir, double L[9][2], double H[9][2]) {
+  int n1 = R + 1;
+  for (int o = 0; o < n1; ++o) {
+    double row[3][2];
+    for (int m = 0; m < n1; ++m) {
+      int idx = dir == 0 ? o * n1 + m : m * n1 + o;
+      row[m][0] = g[idx][0];
+      row[m][1] = g[idx][1];
+    }
+    double lo[3][2], hi[3][2];
+    if (R == 1) {
+      double mid[2] = {0.5 * (row[0][0] + row[1][0]), 0.5 * (row[0][1] + row[1][1])};
+      lo[0][0] = row[0][0]; lo[0][1] = row[0][1]; lo[1][0] = mid[0]; lo[1][1] = mid[1];
+      hi[0][0] = mid[0]; hi[0][1] = mid[1]; hi[1][0] = row[1][0]; hi[1][1] = row[1][1];
+    } else {
+      for (int c = 0; c < 2; ++c) {
+        double a01 = 0.5 * (row[0][c] + row[1][c]), a12 = 0.5 * (row[1][c] + row[2][c]);
+        double a = 0.5 * (a01 + a12);
+        lo[0][c] = row[0][c]; lo[1][c] = a01; lo[2][c] = a;
+        hi[0][c] = a; hi[1][c] = a12; hi[2][c] = row[2][c];
+      }
+    }
+    for (int m = 0; m < n1; ++m) {
+      int idx = dir == 0 ? o * n1 + m : m * n1 + o;
+      L[idx][0] = lo[m][0]; L[idx][1] = lo[m][1];
+      H[idx][0] = hi[m][0]; H[idx][1] = hi[m][1];
+    }
+  }
+}
+
+static void face_subdiv(face_ctx* f, const double g[9][2], double s1a, double s1b, double s2a,
+                        double s2b) {
+  int R = f->sc->R, np = (R + 1) * (R + 1);
+  if (++f->boxes > 200000) { f->fail = 1; return; }
+  double mn[2] = {INFINITY, INFINITY}, mx[2] = {-INFINITY, -INFINITY};
+  for (int m = 0; m < np; ++m)
+    for (int c = 0; c < 2; ++c) { mn[c] = fmin(mn[c], g[m][c]); mx[c] = fmax(mx[c], g[m][c]); }
+  if (mn[0] > 0 || mx[0] < 0 || mn[1] > 0 || mx[1] < 0) return;   /* hull excludes the ray */
+  if (fmax(s1b - s1a, s2b - s2a) < 1e-3) {
+    froot rt;
+    double so1, so2;
+    if (face_newton(f, 0.5 * (s1a + s1b), 0.5 * (s2a + s2b), &rt, &so1, &so2) == 0) {
+      double tol = 1e-7;
+      if (so1 >= s1a - tol && so1 <= s1b + tol && so2 >= s2a - tol && so2 <= s2b + tol &&
+          so1 >= -1e-12 && so1 <= 1 + 1e-12 && so2 >= -1e-12 && so2 <= 1 + 1e-12) {
+        if (f->nroots < f->cap) f->roots[f->nroots++] = rt;
+        else f->fail = 1;
+      }
+    }
+    return;
+  }
+  double L[9][2], H[9][2];
+  if (s1b - s1a >= s2b - s2a) {
+    bz_split(R, g, 0, L, H);
+    double sm = 0.5 * (s1a + s1b);
+    face_subdiv(f, L, s1a, sm, s2a, s2b);
+    face_subdiv(f, H, sm, s1b, s2a, s2b);
+  } else {
+    bz_split(R, g, 1, L, H);
+    double sm = 0.5 * (s2a + s2b);
+    face_subdiv(f, L, s1a, s1b, s2a, sm);
+    face_subdiv(f, H, s1a, s1b, sm, s2b);
+  }
+}
+
+static int cmp_froot(const void* a, const void* b) {
+  double x = ((const froot*)a)->alpha, y = ((const froot*)b)->alpha;
+  return (x > y) - (x < y);
+}
+
+static int inside_elem(const orc_scene* sc, int64_t e, const double lo[3], const double hi[3],
+                       const double wlo[3], const double whi[3], const double p[3], int* fail) {
+  for (int c = 0; c < 3; ++c)
+    if (p[c] < wlo[c] || p[c] > whi[c]) return 0;
+  double xi[3];
+  if (orc_inverse_map(sc, e, p, xi) != 0) { *fail = 1; return 0; }
+  for (int k = 0; k < 3; ++k)
+    if (xi[k] < lo[k] || xi[k] > hi[k]) return 0;
+  return 1;
+}
+
+/* general-geometry intersection with parameter domain [lo,hi]^3 */
+static int general_segments(const orc_scene* sc, int64_t e, const double o[3], const double r[3],
+                            double amin, double amax, const double lo[3], const double hi[3], int max_seg,
+                            double* seg, int* flags) {
+  froot roots[96];
+  int nr = 0, fail = 0;
+  double d1[3], d2[3], ax[3] = {0, 0, 0};
+  /* d1, d2 orthonormal, perpendicular to r */
+  int im = 0;
+  for (int c = 1; c < 3; ++c)
+    if (fabs(r[c]) < fabs(r[im])) im = c;
+  ax[im] = 1.0;
+  cross3(r, ax, d1);
+  double nd = sqrt(dot3(d1, d1));
+  for (int c = 0; c < 3; ++c) d1[c] /= nd;
+  cross3(r, d1, d2);
+  nd = sqrt(dot3(d2, d2));
+  for (int c = 0; c < 3; ++c) d2[c] /= nd;
+
+  int R = sc->R, n1 = R + 1;
+  double eta[3];
+  orc_gll(R, eta);
+  for (int fidx = 0; fidx < 6; ++fidx) {
+    face_ctx f;
+    memset(&f, 0, sizeof f);
+    f.sc = sc; f.e = e; f.fixk = fidx / 2;
+    f.fixv = (fidx % 2) ? hi[f.fixk] : lo[f.fixk];
+    f.ax = (f.fixk + 1) % 3; f.bx = (f.fixk + 2) % 3;
+    f.lo_a = lo[f.ax]; f.hi_a = hi[f.ax]; f.lo_b = lo[f.bx]; f.hi_b = hi[f.bx];
+    memcpy(f.o, o, sizeof f.o); memcpy(f.r, r, sizeof f.r);
+    memcpy(f.d1, d1, sizeof d1); memcpy(f.d2, d2, sizeof d2);
+    f.roots = roots + nr;
+    f.cap = 96 - nr;
+    /* projected face polynomial in Bernstein form (affine projection commutes) */
+    double g[9][2];
+    for (int m2 = 0; m2 < n1; ++m2)
+      for (int m1 = 0; m1 < n1; ++m1) {
+        double xi[3], X[3];
+        face_point(&f, eta[m1], eta[m2], xi);
+        orc_element_map(sc, e, xi, X, NULL);
+        double dx[3] = {X[0] - o[0], X[1] - o[1], X[2] - o[2]};
+        g[m2 * n1 + m1][0] = dot3(d1, dx);
+        g[m2 * n1 + m1][1] = dot3(d2, dx);
+      }
+    if (R == 2) {
+      for (int row = 0; row < 3; ++row)
+        for (int c = 0; c < 2; ++c) {
+          g[row * 3 + 1][c] = 2 * g[row * 3 + 1][c] - 0.5 * (g[row * 3][c] + g[row * 3 + 2][c]);
+        }
+      for (int col = 0; col < 3; ++col)
+        for (int c = 0; c < 2; ++c) {
+          g[3 + col][c] = 2 * g[3 + col][c] - 0.5 * (g[col][c] + g[6 + col][c]);
+        }
+    }
+    face_subdiv(&f, g, 0.0, 1.0, 0.0, 1.0);
+    nr += f.nroots;
+    fail |= f.fail;
+  }
+  qsort(roots, nr, sizeof(froot), cmp_froot);
+  /* dedupe roots found on several faces / sub-boxes */
+  double rn = sqrt(dot3(r, r));
+  int m = 0;
+  for (int q = 0; q < nr; ++q) {
+    if (m > 0 && fabs(roots[q].alpha - roots[m - 1].alpha) * rn < 1e-10) continue;
+    roots[m++] = roots[q];
+  }
+  nr = m;
+  for (int q = 0; q < nr; ++q)
+    if (roots[q].cosphi < 1e-6) *flags |= ORC_AMBIGUOUS;   /* tangent */
+  /* world AABB of the element restricted to [lo,hi] for a cheap outside test */
+  double B[27][3], wlo[3], whi[3];
+  element_bezier(sc, e, lo, hi, B);
+  int np = n1 * n1 * n1;
+  for (int c = 0; c < 3; ++c) { wlo[c] = INFINITY; whi[c] = -INFINITY; }
+  for (int q = 0; q < np; ++q)
+    for (int c = 0; c < 3; ++c) { wlo[c] = fmin(wlo[c], B[q][c]); whi[c] = fmax(whi[c], B[q][c]); }
+  for (int c = 0; c < 3; ++c) { wlo[c] -= 1e-12; whi[c] += 1e-12; }
+  /* breakpoints */
+  double bp[100];
+  int nb = 0;
+  bp[nb++] = amin;
+  for (int q = 0; q < nr; ++q)
+    if (roots[q].alpha > amin && roots[q].alpha < amax) bp[nb++] = roots[q].alpha;
+  bp[nb++] = amax;
+  int nseg = 0, open = 0;
+  double start = 0;
+  for (int q = 0; q + 1 < nb; ++q) {
+    double am = 0.5 * (bp[q] + bp[q + 1]);
+    double p[3] = {o[0] + am * r[0], o[1] + am * r[1], o[2] + am * r[2]};
+    int in = inside_elem(sc, e, lo, hi, wlo, whi, p, &fail);
+    if (in && !open) { open = 1; start = bp[q]; }
+    if (!in && open) {
+      open = 0;
+      if (nseg < max_seg) { seg[2 * nseg] = start; seg[2 * nseg + 1] = bp[q]; }
+      nseg++;
+    }
+  }
+  if (open) {
+    if (nseg < max_seg) { seg[2 * nseg] = start; seg[2 * nseg + 1] = bp[nb - 1]; }
+    nseg++;
+  }
+  if (fail) *flags |= ORC_NEWTON_FAIL | ORC_AMBIGUOUS;
+  if (nseg > max_seg) { *flags |= ORC_OVERFLOW; nseg = max_seg; }
+  return nseg;
+}
+
+static double min_edge(const orc_scene* sc, int64_t e, int k) {
+  /* minimum length of the 4 element edges parallel to xi_k (corner chords) */
+  double best = INFINITY;
+  for (int a = 0; a < 2; ++a)
+    for (int b = 0; b < 2; ++b) {
+      double x0[3], x1[3], p0[3], p1[3];
+      p0[k] = 0; p1[k] = 1;
+      p0[(k + 1) % 3] = p1[(k + 1) % 3] = a;
+      p0[(k + 2) % 3] = p1[(k + 2) % 3] = b;
+      orc_element_map(sc, e, p0, x0, NULL);
+      orc_element_map(sc, e, p1, x1, NULL);
+      double d[3] = {x1[0] - x0[0], x1[1] - x0[1], x1[2] - x0[2]};
+      best = fmin(best, sqrt(dot3(d, d)));
+    }
+  return best;
+}
+
+/* Segments of the ray of pixel (i,j) inside element e (E0), with the
+ * ambiguity classification of SURVEY R7: hit(E+) != hit(E-) where E+/- is
+ * the element with its boundary pushed out/in by EPS_AMBIG, or a chord
+ * < EPS_AMBIG, or a tangent root. */
+int orc_intersect(const orc_scene* sc, const orc_camera* cam, int64_t e, int i, int j, int max_seg,
+                  double* seg, int* flags) {
+  double o[3], r[3], amin, amax;
+  orc_ray(cam, i, j, o, r);
+  alpha_range(cam, &amin, &amax);
+  *flags = 0;
+  double rn = sqrt(dot3(r, r));
+  double c[3], M[9];
+  int nseg;
+  int hitp, hitm;
+  if (tree_affine(sc, sc->tree[e], c, M)) {
+    double Mi[9], h = elem_h(sc, e), q0[3], dq[3], xi0[3], dxi[3];
+    inv3(M, Mi);
+    for (int k = 0; k < 3; ++k) {
+      q0[k] = Mi[3 * k] * (o[0] - c[0]) + Mi[3 * k + 1] * (o[1] - c[1]) + Mi[3 * k + 2] * (o[2] - c[2]);
+      dq[k] = Mi[3 * k] * r[0] + Mi[3 * k + 1] * r[1] + Mi[3 * k + 2] * r[2];
+      xi0[k] = (q0[k] - ldexp((double)sc->anchor[3 * e + k], -MAXL)) / h;
+      dxi[k] = dq[k] / h;
+    }
+    double lo[3] = {0, 0, 0}, hi[3] = {1, 1, 1}, lp[3], hp[3], lm[3], hm[3], a0, a1;
+    for (int k = 0; k < 3; ++k) {
+      double rowk = sqrt(Mi[3 * k] * Mi[3 * k] + Mi[3 * k + 1] * Mi[3 * k + 1] + Mi[3 * k + 2] * Mi[3 * k + 2]);
+      double dk = EPS_AMBIG * rowk / h;
+      lp[k] = -dk; hp[k] = 1 + dk; lm[k] = dk; hm[k] = 1 - dk;
+    }
+    nseg = slab(xi0, dxi, lo, hi, amin, amax, &a0, &a1);
+    if (nseg && max_seg > 0) { seg[0] = a0; seg[1] = a1; }
+    if (nseg && (a1 - a0) * rn < EPS_AMBIG) *flags |= ORC_AMBIGUOUS;
+    hitp = slab(xi0, dxi, lp, hp, amin, amax, &a0, &a1);
+    hitm = slab(xi0, dxi, lm, hm, amin, amax, &a0, &a1);
+  } else {
+    double lo[3] = {0, 0, 0}, hi[3] = {1, 1, 1}, lp[3], hp[3], lm[3], hm[3], tmp[16];
+    for (int k = 0; k < 3; ++k) {
+      double dk = EPS_AMBIG / min_edge(sc, e, k);
+      lp[k] = -dk; hp[k] = 1 + dk; lm[k] = dk; hm[k] = 1 - dk;
+    }
+    int fl = 0;
+    nseg = general_segments(sc, e, o, r, amin, amax, lo, hi, max_seg, seg, &fl);
+    *flags |= fl;
+    for (int q = 0; q < nseg && q < max_seg; ++q)
+      if ((seg[2 * q + 1] - seg[2 * q]) * rn < EPS_AMBIG) *flags |= ORC_AMBIGUOUS;
+    fl = 0;
+    hitp = general_segments(sc, e, o, r, amin, amax, lp, hp, 8, tmp, &fl) > 0;
+    *flags |= fl & (ORC_AMBIGUOUS | ORC_NEWTON_FAIL);
+    fl = 0;
+    hitm = general_segments(sc, e, o, r, amin, amax, lm, hm, 8, tmp, &fl) > 0;
+    *flags |= fl & (ORC_AMBIGUOUS | ORC_NEWTON_FAIL);
+  }
+  if (hitp != hitm) *flags |= ORC_AMBIGUOUS;
+  if (nseg > 0) *flags |= ORC_HIT;
+  return nseg;
+}
+
+/* ======================================================================
+ * Medium along a segment: kappa = kappa0 (f/F)^2,
+ * q = q0 ((1+f~)/2, (1-f~)/2, 1/2); s measured from the near end.
+ * ==================================================================== */
+typedef struct {
+  const orc_scene* sc; int64_t e; double o[3], r[3], alpha_near, rn;
+} medium_ctx;
+
+static void medium_eval(void* vctx, double s, double* kappa, double* q3) {
+  medium_ctx* m = (medium_ctx*)vctx;
+  double al = m->alpha_near + s / m->rn;
+  double p[3] = {m->o[0] + al * m->r[0], m->o[1] + al * m->r[1], m->o[2] + al * m->r[2]};
+  double xi[3];
+  orc_inverse_map(m->sc, m->e, p, xi);
+  double ft = orc_field(m->sc, m->e, xi) * m->sc->inv_F;
+  *kappa = m->sc->kappa0 * ft * ft;
+  q3[0] = m->sc->q0 * 0.5 * (1.0 + ft);
+  q3[1] = m->sc->q0 * 0.5 * (1.0 - ft);
+  q3[2] = m->sc->q0 * 0.5;
+}
+
+/* ======================================================================
+ * Per-pixel fold: sort by (alpha_near, elem), cut + average
+ * overlaps, then the sequential
+ * back-to-front composite I <- A_k I + B_k.
+ * ==================================================================== */
+static int cmp_hit(const void* x, const void* y) {
+  const orc_hit* a = (const orc_hit*)x;
+  const orc_hit* b = (const orc_hit*)y;
+  if (a->alpha_near != b->alpha_near) return (a->alpha_near > b->alpha_near) - (a->alpha_near < b->alpha_near);
+  return (a->elem > b->elem) - (a->elem < b->elem);
+}
+
+static void split_hit(const orc_hit* s, double at, orc_hit* lo, orc_hit* hi) {
+  double d1 = at - s->alpha_near, d2 = s->alpha_far - at, out[4];
+  *lo = *s; *hi = *s;
+  lo->alpha_far = at; hi->alpha_near = at;
+  orc_split(s->a, 0.0, d1, d2, out);
+  lo->a = out[0]; hi->a = out[2];
+  for (int c = 0; c < 3; ++c) {
+    orc_split(s->a, s->b[c], d1, d2, out);
+    lo->b[c] = out[1]; hi->b[c] = out[3];
+  }
+}
+
+static void avg_hit(const orc_hit* x, const orc_hit* y, orc_hit* out) {
+  *out = *x;
+  double bb;
+  orc_average(x->a, 0.0, y->a, 0.0, &out->a, &bb);
+  for (int c = 0; c < 3; ++c) out->b[c] = 0.5 * (x->b[c] + y->b[c]);
+}
+
+void orc_fold_pixel(int n, orc_hit* segs, double tau, const double background[3], double rgba[4],
+                    double ab[4]) {
+  qsort(segs, n, sizeof(orc_hit), cmp_hit);
+  orc_hit* out = (orc_hit*)malloc(sizeof(orc_hit) * (3 * n + 4));
+  int m = 0;
+  if (n > 0) {
+    orc_hit cur = segs[0];
+    for (int k = 1; k < n; ++k) {
+      orc_hit nx = segs[k];
+      double tol = tau * fmax(1.0, fabs(nx.alpha_near));
+      if (nx.alpha_near >= cur.alpha_far - tol) { out[m++] = cur; cur = nx; continue; }
+      /* overlap: cut cur at nx.alpha_near */
+      orc_hit A, Bp;
+      if (nx.alpha_near - cur.alpha_near > 0) { split_hit(&cur, nx.alpha_near, &A, &Bp); out[m++] = A; }
+      else Bp = cur;
+      if (nx.alpha_far < Bp.alpha_far) {
+        orc_hit B1, B2, av;
+        split_hit(&Bp, nx.alpha_far, &B1, &B2);
+        avg_hit(&B1, &nx, &av);
+        out[m++] = av;
+        cur = B2;
+      } else {
+        orc_hit C1, C2, av;
+        if (nx.alpha_far - Bp.alpha_far > 0) split_hit(&nx, Bp.alpha_far, &C1, &C2);
+        else { C1 = nx; C2 = nx; C2.alpha_near = C2.alpha_far; C2.a = 1; C2.b[0] = C2.b[1] = C2.b[2] = 0; }
+        avg_hit(&Bp, &C1, &av);
+        out[m++] = av;
+        cur = C2;
+      }
+    }
+    out[m++] = cur;
+  }
+  /* back to front */
+  double I[3] = {background[0], background[1], background[2]}, B[3] = {0, 0, 0}, T = 1.0;
+  for (int k = m - 1; k >= 0; --k) {
+    for (int c = 0; c < 3; ++c) {
+      I[c] = out[k].a * I[c] + out[k].b[c];
+      B[c] = out[k].a * B[c] + out[k].b[c];
+    }
+    T = out[k].a * T;
+  }
+  rgba[0] = I[0]; rgba[1] = I[1]; rgba[2] = I[2]; rgba[3] = 1.0 - T;
+  if (ab) { ab[0] = T; ab[1] = B[0]; ab[2] = B[1]; ab[3] = B[2]; }
+  free(out);
+}
+
+/* ======================================================================
+ * Render a subset of pixels: brute force over every leaf whose EPS-inflated
+ * rect contains the pixel (SURVEY §8(c) oracle steps 1-7).
+ * ==================================================================== */
+int64_t orc_render(const orc_scene* sc, const orc_camera* cam, int mode, int N, const double background[3],
+                   int64_t npix, const int32_t* pixels, double* rgba, int32_t* nhits, int32_t* namb,
+                   int32_t cap, orc_hit* hits, int nthreads) {
+#ifdef _OPENMP
+  if (nthreads > 0) omp_set_num_threads(nthreads);
+#endif
+  int W = cam->width, H = cam->height;
+  int64_t npx = (int64_t)W * H;
+  int8_t* vis = (int8_t*)malloc(sc->n);
+  int8_t* amb = (int8_t*)malloc(sc->n);
+  int32_t* rects = (int32_t*)malloc(sizeof(int32_t) * 4 * sc->n);
+  orc_cull(sc, cam, vis, amb, rects);
+  int64_t* slot = (int64_t*)malloc(sizeof(int64_t) * npx);
+  for (int64_t p = 0; p < npx; ++p) slot[p] = -1;
+  for (int64_t q = 0; q < npix; ++q) slot[pixels[q]] = q;
+  int64_t* cnt = (int64_t*)calloc(npix + 1, sizeof(int64_t));
+  for (int64_t e = 0; e < sc->n; ++e) {
+    int32_t* rc = rects + 4 * e;
+    for (int jj = rc[2]; jj <= rc[3]; ++jj)
+      for (int ii = rc[0]; ii <= rc[1]; ++ii) {
+        int64_t s = slot[(int64_t)jj * W + ii];
+        if (s >= 0) cnt[s + 1]++;
+      }
+  }
+  for (int64_t q = 0; q < npix; ++q) cnt[q + 1] += cnt[q];
+  int64_t* cand = (int64_t*)malloc(sizeof(int64_t) * (cnt[npix] + 1));
+  int64_t* fillp = (int64_t*)malloc(sizeof(int64_t) * (npix + 1));
+  memcpy(fillp, cnt, sizeof(int64_t) * (npix + 1));
+  for (int64_t e = 0; e < sc->n; ++e) {   /* SFC order within each pixel list */
+    int32_t* rc = rects + 4 * e;
+    for (int jj = rc[2]; jj <= rc[3]; ++jj)
+      for (int ii = rc[0]; ii <= rc[1]; ++ii) {
+        int64_t s = slot[(int64_t)jj * W + ii];
+        if (s >= 0) cand[fillp[s]++] = e;
+      }
+  }
+  int64_t total_hits = 0;
+#pragma omp parallel for schedule(dynamic, 4) reduction(+ : total_hits)
+  for (int64_t q = 0; q < npix; ++q) {
+    int pix = pixels[q], i = pix % W, j = pix / W;
+    int64_t nc = cnt[q + 1] - cnt[q];
+    orc_hit* list = (orc_hit*)malloc(sizeof(orc_hit) * (8 * nc + 1));
+    orc_hit* fold = (orc_hit*)malloc(sizeof(orc_hit) * (8 * nc + 1));
+    int nl = 0, nf = 0, na = 0, nh = 0;
+    double o[3], r[3];
+    orc_ray(cam, i, j, o, r);
+    double rn = sqrt(dot3(r, r));
+    for (int64_t t = cnt[q]; t < cnt[q + 1]; ++t) {
+      int64_t e = cand[t];
+      double seg[16];
+      int flags = 0;
+      int ns = orc_intersect(sc, cam, e, i, j, 8, seg, &flags);
+      if (flags & ORC_AMBIGUOUS) na++;
+      if (ns > 0) nh++;
+      if (ns == 0 && (flags & ORC_AMBIGUOUS)) {
+        orc_hit hh;
+        memset(&hh, 0, sizeof hh);
+        hh.elem = e; hh.pixel = pix; hh.flags = flags; hh.a = 1.0;
+        list[nl++] = hh;
+      }
+      for (int s = 0; s < ns; ++s) {
+        orc_hit hh;
+        memset(&hh, 0, sizeof hh);
+        hh.elem = e; hh.pixel = pix; hh.flags = flags;
+        hh.alpha_near = seg[2 * s]; hh.alpha_far = seg[2 * s + 1];
+        medium_ctx mc;
+        mc.sc = sc; mc.e = e; memcpy(mc.o, o, sizeof o); memcpy(mc.r, r, sizeof r);
+        mc.alpha_near = hh.alpha_near; mc.rn = rn;
+        double L = (hh.alpha_far - hh.alpha_near) * rn;   /* s = alpha |r| */
+        if (mode == 0) {
+          if (orc_segment_exact(medium_eval, &mc, L, &hh.a, hh.b) < 0) hh.flags |= ORC_NEWTON_FAIL;
+        } else {
+          orc_segment_rule(N, medium_eval, &mc, L, &hh.a, hh.b);
+        }
+        list[nl++] = hh;
+        fold[nf++] = hh;
+      }
+    }
+    orc_fold_pixel(nf, fold, TAU_OV, background, rgba + 4 * q, NULL);
+    nhits[q] = nh;
+    namb[q] = na;
+    if (hits) {
+      qsort(list, nl, sizeof(orc_hit), cmp_hit);
+      int nn = nl < cap ? nl : cap;
+      memcpy(hits + q * cap, list, sizeof(orc_hit) * nn);
+      for (int t = nn; t < cap; ++t) { memset(hits + q * cap + t, 0, sizeof(orc_hit)); hits[q * cap + t].elem = -1; }
+      if (nl > cap) hits[q * cap + cap - 1].flags |= ORC_OVERFLOW;
+    }
+    total_hits += nh;
+    free(list);
+    free(fold);
+  }
+  free(vis); free(amb); free(rects); free(slot); free(cnt); free(cand); free(fillp);
+  return total_hits;
+}
