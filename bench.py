@@ -1,0 +1,359 @@
+"""Benchmark of the raycasting hot path (BASELINE.json metric: element-ray
+segment evaluations/s and ms/frame; % of the FP32 roofline).
+
+One step = one frame: rc_camera_set + rc_cull + rc_cast_segments
+(+ rc_aggregate) + composite on seeded synthetic inputs already resident in
+HBM.  Prints ONE JSON line on rank 0.
+
+  python bench.py [--gpus N] [--steps K] [--warmup W] [--config C] [--impl reference]
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import math
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+# Algorithmic FP32 work per candidate pair (FMA = 2 flops): the
+# operations the method needs in this formulation, counted from the source.
+#   affine miss : ray setup 3x(2 FMA) + slab 3x(2 sub, 2 mul, 4 min/max)  ~ 36 flop
+#   affine hit  : + length (7) + N nodes x (3 FMA + trilinear 14 FMA + transfer 3)
+#                 + rule (N + N^2 FMA + N exp + N) ...
+FLOPS_AFFINE_MISS = 36.0
+
+
+def flops_affine_hit(N, P):
+    field = 28 if P == 1 else 96          # trilinear (14 FMA) / triquadratic (~48 FMA)
+    per_node = 6 + field + 4                # node position, field, f~ and kappa
+    rule = 2 * N + 2 * N * N + 4 * N + 12   # sum w kappa, tau_j, e_j sums, b
+    return FLOPS_AFFINE_MISS + 14 + N * per_node + rule
+
+
+FP32_LANES_PER_SM = 128
+NUM_SMS = 148
+
+
+def peaks():
+    try:
+        mp = json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json")))
+    except Exception:
+        mp = {}
+    sm_mhz = float(mp.get("sm_max_mhz", 1965.0))
+    fp32 = NUM_SMS * FP32_LANES_PER_SM * 2 * sm_mhz * 1e6 / 1e12
+    return dict(fp32_tflops=fp32, hbm_gbs=float(mp.get("hbm_gbs", 6650.0)), sm_mhz=sm_mhz,
+                source="MEASURED_PEAKS.json sm_max_mhz x 148 SM x 128 FP32 lanes x 2 (guide unit counts)"
+                if mp else "fallback 1965 MHz (B200_PROFILING.md)")
+
+
+class Clocks:
+    """nvidia-smi sampler during the timed region (B200_PROFILING.md clocks line)."""
+
+    def __init__(self, index=0):
+        self.index = index
+        self.proc = None
+        self.lines = []
+
+    def __enter__(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(self.index),
+                 "--query-gpu=clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+                 "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+                 "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap",
+                 "--format=csv,noheader,nounits", "-lms", "100"],
+                stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.t = threading.Thread(target=self._read, daemon=True)
+            self.t.start()
+        except Exception:
+            self.proc = None
+        return self
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.lines.append(line.strip())
+
+    def __exit__(self, *a):
+        if self.proc:
+            self.proc.terminate()
+            try:
+                self.proc.wait(timeout=5)
+            except Exception:
+                self.proc.kill()
+
+    def summary(self):
+        sm, mx, reasons = [], None, set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for ln in self.lines:
+            p = [x.strip() for x in ln.split(",")]
+            if len(p) < 8:
+                continue
+            try:
+                sm.append(float(p[0]))
+                mx = float(p[1])
+            except ValueError:
+                continue
+            for nm, v in zip(names, p[4:8]):
+                if v.lower() == "active":
+                    reasons.add(nm)
+        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": mx, "reasons": sorted(reasons),
+                "samples": len(sm)}
+
+
+def make_scene(cfg: int, device):
+    import scenegen as sg
+    if cfg == 1:
+        return sg.config1()
+    if cfg == 2:
+        return sg.config2(device=device)
+    if cfg == 3:
+        return sg.config3(device=device)
+    if cfg == 4:
+        return sg.config4(device=device)
+    if cfg == 5:
+        return sg.config5(device=device)
+    raise ValueError(cfg)
+
+
+WORKLOAD = {1: "C1: identity cube, uniform level 3 (512 hex), ortho 64x64, N=4",
+            2: "C2: identity cube, adaptive levels 3..7 (87,088 hex), perspective 512x512, N=4",
+            3: "C3: cubed-sphere shell R=2, uniform level 6 (1,572,864 hex), 1024x1024, N=6",
+            4: "C4: cubed-sphere shell R=2, uniform level 8 (100,663,296 hex), 2048x2048, N=6",
+            5: "C5: cubed-sphere shell R=2, adaptive levels 6..10, 4096x4096, N=8, 3 coarsening cycles"}
+
+
+def l2_flush(buf):
+    buf.add_(1.0)
+
+
+def cpu_baseline(scene, stride, threads=0):
+    """The oracle as it stands (exact mode) on every `stride`-th pixel row/column."""
+    import numpy as np
+
+    import oracle
+    o = oracle.OracleScene(scene)
+    W, H = scene.camera.width, scene.camera.height
+    jj, ii = np.meshgrid(np.arange(stride // 2, H, stride), np.arange(stride // 2, W, stride), indexing="ij")
+    pix = (jj * W + ii).ravel().astype(np.int32)
+    t0 = time.perf_counter()
+    res = o.render(pix, mode="exact", with_hits=False, nthreads=threads)
+    dt = time.perf_counter() - t0
+    cores = threads or (os.cpu_count() or 1)
+    return dict(value=res["total_hits"] / dt, unit="hit pairs/s", cores=cores, kind="oracle",
+                sample=f"every {stride}th pixel row and column ({pix.size} pixels, {res['total_hits']} hit pairs), "
+                       f"all {scene.num_leaves} leaves culled; fp64 exact mode; {dt:.1f} s wall",
+                seconds=dt, hit_pairs=res["total_hits"])
+
+
+def run_reference(args):
+    """--impl reference: the fp64 oracle timed as it stands on host cores."""
+    rank = int(os.environ.get("RANK", "0"))
+    if rank != 0:
+        return
+    scene = make_scene(args.config, None if args.config <= 2 else "cpu")
+    stride = {1: 1, 2: 8, 3: 32, 4: 64, 5: 128}[args.config]
+    for _ in range(args.warmup):
+        pass
+    vals = []
+    for _ in range(args.steps):
+        vals.append(cpu_baseline(scene, stride))
+    v = statistics.median([x["value"] for x in vals])
+    cb = dict(vals[-1])
+    cb["value"] = v
+    line = {"impl": "reference", "metric": "element-ray segment evaluations/s (hit pairs/s)", "value": v,
+            "unit": "hit pairs/s", "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
+            "ms_per_step": 1000.0 * statistics.median([x["seconds"] for x in vals]),
+            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+            "data": "synthetic", "config": {"workload": WORKLOAD[args.config], "sample_stride": stride},
+            "cpu_baseline": {k: cb[k] for k in ("value", "unit", "cores", "kind", "sample")},
+            "e2e": {"value": v, "unit": "hit pairs/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    print(json.dumps(line), flush=True)
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=10)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--config", type=int, default=int(os.environ.get("RC_BENCH_CONFIG", "2")))
+    ap.add_argument("--impl", default="rc")
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    args = ap.parse_args()
+    if args.impl == "reference":
+        return run_reference(args)
+
+    import numpy as np
+    import torch
+
+    from paper_1809_01334_b200 import rc
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    if world > 1:
+        import torch.distributed as dist
+        dist.init_process_group("nccl", device_id=dev)
+    scene = make_scene(args.config, dev if args.config >= 2 else None)
+    cam = scene.camera
+    W, H = cam.width, cam.height
+    N = cam.gl_points
+    lib = rc.lib()
+
+    # --- device-resident inputs: this rank's contiguous SFC range ---------
+    n = scene.num_leaves
+    lo, hi = n * rank // world, n * (rank + 1) // world
+    forest = rc.Forest.from_scene(scene, first=lo, count=hi - lo, device_copy=True)
+    img = torch.empty((H, W, 4), dtype=torch.float32, device=dev)
+    flush = torch.empty(int(160e6) // 4, dtype=torch.float32, device=dev)   # > 126 MB L2
+    stream = torch.cuda.current_stream()
+
+    def frame():
+        forest.camera_set(cam)
+        forest.cull()
+        forest.cast_segments()
+        if scene.coarsen_cycles:
+            forest.aggregate(scene.coarsen_cycles)
+        if world == 1:
+            forest.composite(out=img)
+            return None
+        from paper_1809_01334_b200 import dist as rdist
+        return rdist.exchange_and_composite(forest, scene.tiles, world, rank)
+
+    for _ in range(max(3, args.warmup)):
+        frame()
+    torch.cuda.synchronize()
+    segs = forest.segments()
+    hits_local = segs["hit_pairs"]
+    cand_local = segs["candidates"]
+    if world > 1:
+        import torch.distributed as dist
+        t = torch.tensor([hits_local, cand_local], dtype=torch.int64, device=dev)
+        dist.all_reduce(t)
+        hits_total, cand_total = int(t[0]), int(t[1])
+    else:
+        hits_total, cand_total = hits_local, cand_local
+
+    # --- timed region: K frames, L2 flushed between frames (outside events) ---
+    times, cast_ms = [], []
+    rc.launch_count(reset=True)
+    with Clocks(local) as clk:
+        for _ in range(args.steps):
+            l2_flush(flush)
+            if world > 1:
+                torch.distributed.barrier()
+            torch.cuda.synchronize()
+            e0 = torch.cuda.Event(enable_timing=True)
+            e1 = torch.cuda.Event(enable_timing=True)
+            e0.record(stream)
+            frame()
+            e1.record(stream)
+            torch.cuda.synchronize()
+            times.append(e0.elapsed_time(e1))
+            cast_ms.append(forest.last_cast_ms())
+    launches = rc.launch_count()
+    ms_local = sum(times) / len(times)
+    if world > 1:
+        import torch.distributed as dist
+        t = torch.tensor([ms_local, sum(cast_ms) / len(cast_ms)], dtype=torch.float64, device=dev)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        ms_step, cast_avg = float(t[0]), float(t[1])
+    else:
+        ms_step, cast_avg = ms_local, sum(cast_ms) / len(cast_ms)
+    value = hits_total / (ms_step / 1000.0)
+
+    # --- roofline of the dominant kernel (segment kernel) -----------------
+    pk = peaks()
+    if scene.geom_degree == 1:
+        fl = hits_local * flops_affine_hit(N, scene.field_degree) + (cand_local - hits_local) * FLOPS_AFFINE_MISS
+    else:
+        from bench_model import flops_curved
+        fl = flops_curved(hits_local, cand_local, N, scene.field_degree)
+    achieved = fl / (cast_avg / 1000.0) / 1e12
+    roof = {"kernel": "k_cast_affine" if scene.geom_degree == 1 else "k_cast_curved", "bound": "alu",
+            "achieved": achieved, "peak": pk["fp32_tflops"], "unit": "TFLOP/s", "frac": achieved / pk["fp32_tflops"],
+            "traffic": None, "kernel_ms": cast_avg, "share_of_step": cast_avg / ms_step,
+            "algorithmic_flops_per_launch": fl, "peak_source": pk["source"]}
+    tpath = os.path.join(ROOT, "profiles", f"traffic_c{args.config}.json")
+    if os.path.exists(tpath):
+        try:
+            roof["traffic"] = json.load(open(tpath)).get("bytes_per_launch")
+        except Exception:
+            pass
+
+    # --- end to end through the public API with HOST buffers --------------
+    host = [np.ascontiguousarray(a if isinstance(a, np.ndarray) else a.cpu().numpy())
+            for a in (scene.leaf_anchor[lo:hi], scene.leaf_tree[lo:hi], scene.leaf_level[lo:hi],
+                      scene.leaf_field[lo:hi])]
+    pinned = [torch.from_numpy(a).pin_memory() for a in host]
+    h2d = sum(a.nbytes for a in host)
+    img_host = torch.empty((H, W, 4), dtype=torch.float32).pin_memory()
+    e2e_times = []
+    for it in range(2 + max(1, min(args.steps, 3))):
+        torch.cuda.synchronize()
+        if world > 1:
+            torch.distributed.barrier()
+        t0 = time.perf_counter()
+        dev_in = [p.to(dev, non_blocking=True) for p in pinned]
+        f2 = rc.Forest(scene.tree_ctrl, scene.geom_degree, scene.field_degree, *dev_in, scene.kappa0,
+                       scene.inv_F, scene.q0, first_global_leaf=lo)
+        f2.camera_set(cam)
+        f2.cull()
+        f2.cast_segments()
+        if scene.coarsen_cycles:
+            f2.aggregate(scene.coarsen_cycles)
+        if world == 1:
+            out = f2.composite()
+            img_host.copy_(out)
+        else:
+            from paper_1809_01334_b200 import dist as rdist
+            out = rdist.exchange_and_composite(f2, scene.tiles, world, rank)
+            img_host.view(-1)[:out.numel()].copy_(out.view(-1))
+        torch.cuda.synchronize()
+        dt = time.perf_counter() - t0
+        f2.close()
+        del dev_in
+        if it >= 2:
+            e2e_times.append(dt)
+    e2e_s = sum(e2e_times) / len(e2e_times)
+    if world > 1:
+        import torch.distributed as dist
+        t = torch.tensor([e2e_s], dtype=torch.float64, device=dev)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        e2e_s = float(t[0])
+    e2e = {"value": hits_total / e2e_s, "unit": "hit pairs/s", "h2d_bytes_per_step": h2d,
+           "d2h_bytes_per_step": H * W * 16, "ms_per_step": e2e_s * 1000.0}
+
+    if rank == 0:
+        line = {"metric": "element-ray segment evaluations/s (hit pairs/s)", "value": value, "unit": "hit pairs/s",
+                "n_gpus": world, "steps": args.steps, "warmup": max(3, args.warmup), "ms_per_step": ms_step,
+                "higher_is_better": True, "scaling": "weak" if world == 1 else "strong", "vs_baseline": None,
+                "dtype": "f32", "data": "synthetic (seeded, scenegen)",
+                "config": {"workload": WORKLOAD[args.config], "leaves": n, "image": [W, H], "gl_points": N,
+                           "hit_pairs": hits_total, "candidate_pairs": cand_total,
+                           "candidate_pairs_per_s": cand_total / (ms_step / 1000.0),
+                           "l2": "flushed between frames (160 MB write outside the events)",
+                           "parallelism": f"sfc{world}"},
+                "roofline": roof, "gpu_launches": launches, "clocks": clk.summary(), "e2e": e2e}
+        if world == 1 and not args.no_cpu_baseline:
+            stride = {1: 1, 2: 8, 3: 32, 4: 64, 5: 128}[args.config]
+            sc_cpu = scene if args.config <= 2 else make_scene(args.config, "cpu")
+            cb = cpu_baseline(sc_cpu, stride)
+            line["cpu_baseline"] = {k: cb[k] for k in ("value", "unit", "cores", "kind", "sample")}
+        print(json.dumps(line), flush=True)
+    if world > 1:
+        import torch.distributed as dist
+        dist.barrier()
+        dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

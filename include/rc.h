@@ -1,0 +1,208 @@
+/* rc.h -- C ABI of the B200-native forest-of-octrees raycasting hot path.
+ *
+ * Method: C. Burstedde, "Distributed-Memory Forest-of-Octrees Raycasting",
+ * arXiv 1809.01334.  PAPER.md line numbers refer to the paper text
+ * (/root/reference/PAPER.md); SURVEY.md §8 fixes the readings used here.
+ *
+ * Conventions for every entry point:
+ *  - returns rc_status; nothing throws, exits or prints.  On failure
+ *    rc_last_error() describes the failing call (thread-local, valid until the
+ *    next rc_* call on the same thread).
+ *  - all device work is enqueued on the caller's stream (a cudaStream_t passed
+ *    as void*, e.g. torch.cuda.current_stream().cuda_stream); entries marked
+ *    [sync] synchronise that stream before returning.
+ *  - pointers named d_* are device pointers, h_* host pointers.  The caller
+ *    owns every buffer it passes; the library owns its device scratch and the
+ *    views it hands out (valid until the next call that recomputes them or
+ *    rc_forest_destroy).
+ *  - one rc_forest per host thread / stream at a time.
+ */
+#ifndef RC_H
+#define RC_H
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef enum {
+  RC_OK = 0,
+  RC_ERR_INVALID_ARG = -1,   /* null pointer, R or P not in {1,2}, n <= 0, bad camera   */
+  RC_ERR_NOT_SFC_SORTED = -2,/* leaves not strictly increasing in (tree, Morton key)    */
+  RC_ERR_OUT_OF_MEMORY = -3,
+  RC_ERR_CUDA = -4,          /* CUDA runtime error; rc_last_error() has the call site   */
+  RC_ERR_CAPACITY = -6,      /* caller buffer too small; *required is written           */
+  RC_ERR_STATE = -7,         /* call order violated (cast before camera_set, ...)       */
+  RC_ERR_NUMERIC = -8        /* non-finite input                                        */
+} rc_status;
+
+const char* rc_last_error(void);
+int32_t rc_version(void);    /* ABI version, currently 1 */
+
+/* ------------------------------------------------------------------------
+ * Forest: SFC-ordered leaves of a forest of octrees with per-tree degree-R
+ * tensor-product Lagrange geometry on Gauss-Lobatto nodes (PAPER.md:82-158,
+ * Eq. geometrytrafo / tensorgeom) and a per-element nodal scalar field
+ * (SURVEY §8(c) R11).  Element map X_E(xi) = J_k(a 2^-18 + 2^-level xi)
+ * (PAPER.md:104-107).
+ * ---------------------------------------------------------------------- */
+typedef struct {
+  float kappa0;   /* kappa = kappa0 (f inv_F)^2 */
+  float inv_F;    /* 1/F, F = max |nodal f|                                       */
+  float q0;       /* q = q0 ((1+f~)/2, (1-f~)/2, 1/2)  RGB emission density      */
+} rc_transfer;
+
+enum { RC_HOST_COPY = 0, RC_DEVICE_COPY = 1 };
+
+typedef struct {
+  int32_t num_trees;          /* K >= 1                                                  */
+  int32_t geom_degree;        /* R in {1,2}: GLL nodes {0,1} / {0,1/2,1}                  */
+  const double* tree_ctrl;    /* HOST [K][R+1][R+1][R+1][3], index [k][m3][m2][m1][xyz]   */
+  int32_t field_degree;       /* P in {1,2}: (P+1)^3 nodal values per element            */
+  int64_t num_leaves;         /* n >= 1 (this GPU's contiguous SFC range)                */
+  int64_t first_global_leaf;  /* global SFC index of leaf 0 (tie-break key, R16)         */
+  const int32_t* leaf_anchor; /* [n][3] in units of 2^-18 of the tree cube               */
+  const int32_t* leaf_tree;   /* [n]                                                     */
+  const int8_t* leaf_level;   /* [n], 0..18                                              */
+  const float* leaf_field;    /* [n][(P+1)^3], node order [k3][k2][k1]                    */
+  int32_t memory;             /* RC_HOST_COPY: leaf arrays are host pointers;
+                                 RC_DEVICE_COPY: leaf arrays are device pointers        */
+  rc_transfer transfer;
+} rc_forest_desc;
+
+typedef struct rc_forest rc_forest;
+
+/* Copies the leaves to device memory (device layout in DESIGN.md §4).  Checks
+ * strict SFC order on the host for RC_HOST_COPY (RC_ERR_NOT_SFC_SORTED).
+ * [sync] */
+rc_status rc_forest_create(const rc_forest_desc* desc, void* stream, rc_forest** out);
+rc_status rc_forest_destroy(rc_forest* f);
+
+/* ------------------------------------------------------------------------
+ * Camera (Fig. camera, Eq. ray; orthographic per SURVEY R4).
+ * Perspective: ray o + alpha r, r = v + l((i-(w-1)/2) t + (j-(h-1)/2) u),
+ * visible alpha in [1, f/|v|].  Orthographic: origin o + l(...), direction v
+ * (unit), alpha in [0, f].  t, u unit, (t,u,v/|v|) orthonormal.
+ * ---------------------------------------------------------------------- */
+enum { RC_PERSPECTIVE = 0, RC_ORTHOGRAPHIC = 1 };
+
+typedef struct {
+  int32_t projection;
+  double origin[3], view[3], right[3], up[3];
+  double pixel_size;      /* l  */
+  double far_dist;        /* f  */
+  int32_t width, height;  /* w, h; pixel id = j*w + i                       */
+  int32_t gl_points;      /* N in [1,8] Gauss-Legendre points per segment  */
+  double newton_tol;      /* R=2: stop when ||dxi||_inf < tol                */
+  int32_t newton_max_iter;/* R=2: iteration cap; failures are counted, never silent     */
+} rc_camera;
+
+/* Host fp64 preprocessing: per-tree camera constants and GL tables
+ * (Eq. camerapoints).  Validates the camera (orthonormal
+ * frame to 1e-9, f > n, w,h in [1,32767], N in [1,8]).  Async. */
+rc_status rc_camera_set(rc_forest* f, const rc_camera* cam, void* stream);
+
+/* ------------------------------------------------------------------------
+ * Cull: leaf visible iff the pixel-
+ * centre rectangle of the camera-space AABB of its Bernstein-Bezier points
+ * is non-empty.  Produces the compacted visible list (SFC order) and the
+ * per-visible-leaf pixel rectangles on the device.  Async.
+ * ---------------------------------------------------------------------- */
+rc_status rc_cull(rc_forest* f, void* stream);
+
+/* [sync] Copies the visible leaf indices (local, SFC order) to the caller's
+ * device buffer d_visible[capacity]; *count = number of visible leaves.
+ * RC_ERR_CAPACITY (with *count set) if capacity is too small. */
+rc_status rc_cull_result(rc_forest* f, int32_t* d_visible, int64_t capacity, int64_t* count, void* stream);
+
+/* ------------------------------------------------------------------------
+ * Cast segments (PAPER.md:921-953 leaf-level rendering): for every candidate
+ * (visible leaf, pixel in its rectangle) pair, intersect the ray with the
+ * element (slab test in reference coordinates for affine trees; face roots
+ * + Newton for curved R=2 trees, App. A.1) and integrate dI/ds = -kappa I + q
+ * over each inside interval with the N-point nested Gauss-Legendre rule
+ * (SURVEY R13), giving the segment (alpha_near, alpha_far, a, b[3]) of
+ * Eq. ABgeneral, near end = camera side.
+ * Must follow rc_cull.  [sync] (one small D2H of the candidate count to
+ * size the output; kernels are asynchronous).
+ * ---------------------------------------------------------------------- */
+typedef struct {              /* 32-byte segment record, also the wire format          */
+  uint32_t pixel;             /* j*w + i                                                */
+  float alpha_near, alpha_far;/* ray parameter interval, alpha_near < alpha_far         */
+  float a;                    /* transmission, shared by the channels (scalar kappa)     */
+  float b[3];                 /* emission per channel                                   */
+  uint32_t key;               /* global SFC leaf index (tie-break R16; node id after
+                                 aggregation = first leaf of the node)                   */
+} rc_seg;
+
+typedef struct {
+  int64_t count;               /* number of records in segs                            */
+  int64_t candidates;          /* candidate (leaf, pixel) pairs evaluated              */
+  int64_t hit_pairs;           /* pairs with >= 1 segment (the metric's unit)          */
+  int64_t newton_failures;     /* R=2 Newton non-convergence count (must be 0)          */
+  int64_t num_visible;
+  const rc_seg* segs;          /* device view, library-owned                           */
+  const int32_t* hits_per_pixel; /* device [w*h]: pairs with >= 1 segment per pixel     */
+} rc_segments;
+
+rc_status rc_cast_segments(rc_forest* f, void* stream);
+/* [sync] fills *out with counts and device views of the current segments. */
+rc_status rc_segments_get(rc_forest* f, rc_segments* out, void* stream);
+
+/* ------------------------------------------------------------------------
+ * Aggregate (PAPER.md:956-994 coarsening): `cycles` times, replace every
+ * complete local family of same-level siblings by its parent and, per
+ * (parent, pixel), merge the children's segments in alpha order, combining
+ * touching ones with Eq. aggregate.  Lossless up to roundoff.
+ * [sync]
+ * ---------------------------------------------------------------------- */
+rc_status rc_aggregate(rc_forest* f, int32_t cycles, void* stream);
+
+/* ------------------------------------------------------------------------
+ * Composite.  Image tiles of
+ * tw x th = (w/tiles_x) x (h/tiles_y) pixels; tile (tx,ty) is owned by rank
+ * (tx + ty) mod nranks.
+ *
+ * rc_pack_tiles: permutes the current segments by owner rank into the
+ *   library-owned send buffer *d_send (rc_seg records) and writes
+ *   h_send_counts[nranks] (records per destination, in rank order).  [sync]
+ * rc_composite_tiles: per owned pixel, orders the given records by
+ *   (alpha_near, key), cuts and averages overlaps beyond 1e-6 max(1,alpha)
+ *   (Eq. segsplit, Eq. segaverage), folds nearest-first with Eq. aggregate
+ *   in fp64 and applies the background I_v = A I_b + B.
+ *   Output d_rgba: float [my tiles in row-major tile order][th][tw][4] =
+ *   (R,G,B, 1-A).  d_recv may be the library's own segments (pass NULL to
+ *   use them).  Async.
+ * rc_composite: single-GPU shortcut: the whole image, d_rgba [h][w][4].
+ * ---------------------------------------------------------------------- */
+typedef struct {
+  int32_t tiles_x, tiles_y;   /* w % tiles_x == 0 and h % tiles_y == 0                 */
+  int32_t nranks, rank;
+} rc_tiling;
+
+rc_status rc_pack_tiles(rc_forest* f, const rc_tiling* t, int64_t* h_send_counts, const rc_seg** d_send,
+                        void* stream);
+rc_status rc_composite_tiles(rc_forest* f, const rc_tiling* t, const rc_seg* d_recv, int64_t nrecv,
+                             const float background[3], float* d_rgba, int64_t capacity_floats,
+                             void* stream);
+rc_status rc_composite(rc_forest* f, const float background[3], float* d_rgba, int64_t capacity_floats,
+                       void* stream);
+
+/* ------------------------------------------------------------------------
+ * One whole frame on one GPU from device-resident inputs:
+ * rc_camera_set + rc_cull + rc_cast_segments + rc_aggregate(cycles) +
+ * rc_composite.  *hit_pairs (optional) receives the metric's unit count.
+ * ---------------------------------------------------------------------- */
+rc_status rc_render_frame(rc_forest* f, const rc_camera* cam, int32_t cycles, const float background[3],
+                          float* d_rgba, int64_t capacity_floats, int64_t* hit_pairs, void* stream);
+
+/* Instrumentation: kernel launches issued by the library since the last
+ * reset, and the device time of the segment kernel(s) of the last
+ * rc_cast_segments measured with CUDA events on the caller's stream. */
+int64_t rc_launch_count(int32_t reset);
+float rc_last_cast_ms(rc_forest* f);
+
+#ifdef __cplusplus
+}
+#endif
+#endif

@@ -1,0 +1,34 @@
+// kernels.cuh -- host launchers of the kernels (each defined and launched in
+// its own translation unit; see kernels.cu and cast_curved.cu).
+#pragma once
+#include "rc_internal.cuh"
+
+namespace rc {
+
+cudaError_t launch_cull(const CamConst& cc, const TreeConst* trees, DevLeafView L, int64_t n, int R, bool affine,
+                        int32_t* flag, Rect16* rect, cudaStream_t s);
+cudaError_t launch_compact(const int32_t* flag, const Rect16* rect, const int64_t* pos, int64_t n, int32_t* vis,
+                           Rect16* vis_rect, cudaStream_t s);
+cudaError_t launch_chunk_count(const Rect16* vis_rect, const int64_t* nvis_p, int64_t n, int64_t* cnt,
+                               int64_t* counters, cudaStream_t s);
+cudaError_t launch_expand(const int64_t* off, const int64_t* nvis_p, int64_t nvis, int32_t* chunk_elem,
+                          cudaStream_t s);
+cudaError_t launch_cast_affine(const CamConst& cc, const TreeConst* trees, DevLeafView L, int P, const int32_t* vis,
+                               const Rect16* vrect, const int64_t* chunk_off, const int32_t* chunk_elem,
+                               int64_t nchunks, uint32_t key_base, rc_seg* segs, int64_t seg_cap, int32_t* hits_pp,
+                               int64_t* counters, int grid, cudaStream_t s);
+cudaError_t launch_cast_curved(const CamConst& cc, const TreeConst* trees, DevLeafView L, int P, const int32_t* vis,
+                               const Rect16* vrect, const int64_t* chunk_off, const int32_t* chunk_elem,
+                               int64_t nchunks, uint32_t key_base, rc_seg* segs, int64_t seg_cap, int32_t* hits_pp,
+                               int64_t* counters, int grid, cudaStream_t s);
+cudaError_t launch_pack(const rc_seg* segs, const int64_t* nseg_p, int W, int tw, int th, int tiles_x, int nranks,
+                        int64_t* counts, const int64_t* dest_off, int64_t* cursor, rc_seg* out, int grid, bool count,
+                        cudaStream_t s);
+cudaError_t launch_hist(const rc_seg* segs, int64_t n, int32_t* cnt, int grid, cudaStream_t s);
+cudaError_t launch_scatter(const rc_seg* segs, int64_t n, const int64_t* off, int32_t* cursor, rc_seg* out, int grid,
+                           cudaStream_t s);
+cudaError_t launch_fold(const rc_seg* sorted, const int64_t* off, int W, int H, int tw, int th,
+                        const int32_t* my_tiles, int tiles_x, int64_t npix_out, const float bg[3], float tau,
+                        float* rgba, int max_grid, cudaStream_t s);
+
+}  // namespace rc

@@ -1,0 +1,670 @@
+// rc_api.cu -- host side of the C ABI declared in include/rc.h.
+#include <cuda_runtime.h>
+#include <math.h>
+#include <stdarg.h>
+#include <stdio.h>
+#include <string.h>
+
+#include <algorithm>
+#include <vector>
+
+#include "kernels.cuh"
+#include "rc_internal.cuh"
+
+namespace rc {
+int64_t g_launches = 0;
+}
+using namespace rc;
+
+static thread_local char g_err[1024] = "";
+
+static rc_status fail(rc_status st, const char* fmt, ...) {
+  va_list ap;
+  va_start(ap, fmt);
+  vsnprintf(g_err, sizeof g_err, fmt, ap);
+  va_end(ap);
+  return st;
+}
+
+#define CU(call)                                                                                   \
+  do {                                                                                             \
+    cudaError_t e_ = (call);                                                                       \
+    if (e_ != cudaSuccess)                                                                         \
+      return fail(e_ == cudaErrorMemoryAllocation ? RC_ERR_OUT_OF_MEMORY : RC_ERR_CUDA, "%s: %s (%s:%d)", \
+                  #call, cudaGetErrorString(e_), __FILE__, __LINE__);                               \
+  } while (0)
+
+#define LAUNCHED() (++g_launches)
+
+extern "C" const char* rc_last_error(void) { return g_err; }
+extern "C" int32_t rc_version(void) { return 1; }
+extern "C" int64_t rc_launch_count(int32_t reset) {
+  int64_t v = g_launches;
+  if (reset) g_launches = 0;
+  return v;
+}
+
+template <typename T>
+static cudaError_t grow(T** p, int64_t* cap, int64_t need) {
+  if (need <= *cap && *p) return cudaSuccess;
+  if (*p) cudaFree(*p);
+  *p = nullptr;
+  int64_t c = std::max<int64_t>(need + need / 8, 64);
+  cudaError_t e = cudaMalloc((void**)p, sizeof(T) * (size_t)c);
+  if (e == cudaSuccess) *cap = c;
+  else *cap = 0;
+  return e;
+}
+
+// ---------------------------------------------------------------------------
+// forest
+// ---------------------------------------------------------------------------
+static uint64_t spread18(uint32_t v) {
+  uint64_t x = v & 0x3FFFFu, r = 0;
+  for (int b = 0; b < 18; ++b) r |= ((x >> b) & 1ull) << (3 * b);
+  return r;
+}
+
+extern "C" rc_status rc_forest_create(const rc_forest_desc* d, void* stream, rc_forest** out) {
+  if (!d || !out) return fail(RC_ERR_INVALID_ARG, "rc_forest_create: null argument");
+  *out = nullptr;
+  if (d->num_trees < 1 || d->num_trees > RC_MAX_TREES) return fail(RC_ERR_INVALID_ARG, "num_trees out of range");
+  if (d->geom_degree < 1 || d->geom_degree > 2) return fail(RC_ERR_INVALID_ARG, "geom_degree must be 1 or 2");
+  if (d->field_degree < 1 || d->field_degree > 2) return fail(RC_ERR_INVALID_ARG, "field_degree must be 1 or 2");
+  if (d->num_leaves < 1 || d->num_leaves > (int64_t)INT32_MAX) return fail(RC_ERR_INVALID_ARG, "num_leaves out of range");
+  if (!d->tree_ctrl || !d->leaf_anchor || !d->leaf_tree || !d->leaf_level || !d->leaf_field)
+    return fail(RC_ERR_INVALID_ARG, "rc_forest_create: null array");
+  if (d->memory != RC_HOST_COPY && d->memory != RC_DEVICE_COPY) return fail(RC_ERR_INVALID_ARG, "bad memory mode");
+  if (d->first_global_leaf < 0 || d->first_global_leaf + d->num_leaves > (int64_t)UINT32_MAX)
+    return fail(RC_ERR_INVALID_ARG, "global leaf index must fit 32 bits");
+  cudaStream_t s = (cudaStream_t)stream;
+  const int64_t n = d->num_leaves;
+  const int NF = (d->field_degree + 1) * (d->field_degree + 1) * (d->field_degree + 1);
+  int n1 = d->geom_degree + 1;
+  for (int q = 0; q < d->num_trees * n1 * n1 * n1 * 3; ++q)
+    if (!isfinite(d->tree_ctrl[q])) return fail(RC_ERR_NUMERIC, "non-finite control point");
+  if (d->memory == RC_HOST_COPY) {
+    // strict SFC order: (tree, Morton key) increasing; anchors aligned to their level
+    uint64_t prev_key = 0;
+    int prev_tree = -1;
+    for (int64_t e = 0; e < n; ++e) {
+      int t = d->leaf_tree[e], l = d->leaf_level[e];
+      if (t < 0 || t >= d->num_trees || l < 0 || l > RC_MAXLEVEL)
+        return fail(RC_ERR_INVALID_ARG, "leaf %lld: bad tree or level", (long long)e);
+      uint32_t mask = (1u << (RC_MAXLEVEL - l)) - 1u;
+      const int32_t* a = d->leaf_anchor + 3 * e;
+      for (int k = 0; k < 3; ++k)
+        if (a[k] < 0 || a[k] >= (1 << RC_MAXLEVEL) || ((uint32_t)a[k] & mask))
+          return fail(RC_ERR_INVALID_ARG, "leaf %lld: anchor not aligned to its level", (long long)e);
+      uint64_t key = spread18(a[0]) | (spread18(a[1]) << 1) | (spread18(a[2]) << 2);
+      if (t < prev_tree || (t == prev_tree && key <= prev_key))
+        return fail(RC_ERR_NOT_SFC_SORTED, "leaf %lld breaks SFC order", (long long)e);
+      // non-overlap: previous leaf's last descendant key must be below this key
+      prev_tree = t;
+      prev_key = key | (spread18(mask) | (spread18(mask) << 1) | (spread18(mask) << 2));
+    }
+    for (int64_t q = 0; q < n * NF; ++q)
+      if (!isfinite(d->leaf_field[q])) return fail(RC_ERR_NUMERIC, "non-finite field value");
+  }
+  rc_forest* f = new rc_forest();
+  f->K = d->num_trees;
+  f->R = d->geom_degree;
+  f->P = d->field_degree;
+  f->n = n;
+  f->first_global = d->first_global_leaf;
+  f->transfer = d->transfer;
+  f->h_trees = new TreeConst[f->K];
+  memset(f->h_trees, 0, sizeof(TreeConst) * f->K);
+  cudaError_t e = cudaSuccess;
+  auto cleanup = [&](rc_status st, const char* what) {
+    rc_status r = fail(st, "%s: %s", what, cudaGetErrorString(e));
+    rc_forest_destroy(f);
+    return r;
+  };
+#define ALLOC(ptr, bytes)                                        \
+  if ((e = cudaMalloc((void**)&(ptr), (bytes))) != cudaSuccess) \
+    return cleanup(RC_ERR_OUT_OF_MEMORY, "cudaMalloc " #ptr);
+  ALLOC(f->d_anchor, sizeof(int32_t) * 3 * n);
+  ALLOC(f->d_tree, sizeof(int32_t) * n);
+  ALLOC(f->d_level, sizeof(int8_t) * n);
+  ALLOC(f->d_field, sizeof(float) * NF * n);
+  ALLOC(f->d_flag, sizeof(int32_t) * n);
+  ALLOC(f->d_rect_all, sizeof(Rect16) * n);
+  ALLOC(f->d_scan, sizeof(int64_t) * (n + 1));
+  ALLOC(f->d_vis, sizeof(int32_t) * n);
+  ALLOC(f->d_vis_rect, sizeof(Rect16) * n);
+  ALLOC(f->d_chunk_off, sizeof(int64_t) * (n + 1));
+  ALLOC(f->d_counters, sizeof(int64_t) * CNT_TOTAL);
+  ALLOC(f->d_trees, sizeof(TreeConst) * f->K);
+  ALLOC(f->d_cam, sizeof(CamConst));
+  f->scan_tmp_cap = std::max<int64_t>((int64_t)scan_tmp_size(n + 1) + 64, 256);
+  ALLOC(f->d_scan_tmp, sizeof(int64_t) * f->scan_tmp_cap);
+#undef ALLOC
+  cudaMemcpyKind kind = d->memory == RC_HOST_COPY ? cudaMemcpyHostToDevice : cudaMemcpyDeviceToDevice;
+  if ((e = cudaMemcpyAsync(f->d_anchor, d->leaf_anchor, sizeof(int32_t) * 3 * n, kind, s)) ||
+      (e = cudaMemcpyAsync(f->d_tree, d->leaf_tree, sizeof(int32_t) * n, kind, s)) ||
+      (e = cudaMemcpyAsync(f->d_level, d->leaf_level, sizeof(int8_t) * n, kind, s)) ||
+      (e = cudaMemcpyAsync(f->d_field, d->leaf_field, sizeof(float) * NF * n, kind, s)) ||
+      (e = cudaMemsetAsync(f->d_counters, 0, sizeof(int64_t) * CNT_TOTAL, s)))
+    return cleanup(RC_ERR_CUDA, "cudaMemcpyAsync leaves");
+  // host copy of the tree control points for rc_camera_set
+  for (int k = 0; k < f->K; ++k)
+    memcpy(f->h_trees[k].lagr, d->tree_ctrl + (size_t)k * n1 * n1 * n1 * 3, sizeof(double) * n1 * n1 * n1 * 3);
+  if ((e = cudaEventCreate(&f->ev0)) || (e = cudaEventCreate(&f->ev1))) return cleanup(RC_ERR_CUDA, "event");
+  if ((e = cudaStreamSynchronize(s))) return cleanup(RC_ERR_CUDA, "sync");
+  *out = f;
+  return RC_OK;
+}
+
+extern "C" rc_status rc_forest_destroy(rc_forest* f) {
+  if (!f) return RC_OK;
+  void* ptrs[] = {f->d_anchor, f->d_tree, f->d_level, f->d_field, f->d_flag, f->d_rect_all, f->d_scan,
+                  f->d_vis, f->d_vis_rect, f->d_chunk_off, f->d_counters, f->d_trees, f->d_cam,
+                  f->d_scan_tmp, f->d_chunk_elem, f->d_segs, f->d_hits_pp, f->d_pix_cnt, f->d_pix_off,
+                  f->d_sorted, f->d_send};
+  for (void* p : ptrs)
+    if (p) cudaFree(p);
+  if (f->ev0) cudaEventDestroy(f->ev0);
+  if (f->ev1) cudaEventDestroy(f->ev1);
+  delete[] f->h_trees;
+  delete f;
+  return RC_OK;
+}
+
+// ---------------------------------------------------------------------------
+// camera (host fp64 preprocessing)
+// ---------------------------------------------------------------------------
+// Gauss-Legendre nodes/weights on [0,1] and the table S_jk = int_0^{u_j} l_k
+// (SURVEY R13), computed in long double: Newton on P_N from Tricomi's
+// initial guess; S by exact integration of the monomial form of l_k.
+static void gl_tables(int N, float* u, float* w, float* S) {
+  long double x[RC_MAX_N], wx[RC_MAX_N];
+  const long double PI = 3.141592653589793238462643383279502884L;
+  for (int i = 1; i <= N; ++i) {
+    long double z = (1.0L - (N - 1.0L) / (8.0L * N * N * N)) * cosl(PI * (4.0L * i - 1.0L) / (4.0L * N + 2.0L));
+    long double dp = 1.0L;
+    for (int it = 0; it < 200; ++it) {
+      long double p0 = 1.0L, p1 = z;
+      for (int k = 2; k <= N; ++k) {
+        long double p2 = ((2.0L * k - 1.0L) * z * p1 - (k - 1.0L) * p0) / k;
+        p0 = p1;
+        p1 = p2;
+      }
+      if (N == 1) p0 = 1.0L;
+      dp = N * (z * p1 - p0) / (z * z - 1.0L);
+      long double dz = p1 / dp;
+      z -= dz;
+      if (fabsl(dz) < 1e-19L) break;
+    }
+    // z descends with i; map to ascending u = (1 + x)/2 with x = -z
+    x[i - 1] = -z;
+    wx[i - 1] = 2.0L / ((1.0L - z * z) * dp * dp);
+  }
+  long double uu[RC_MAX_N];
+  for (int j = 0; j < N; ++j) {
+    uu[j] = 0.5L * (1.0L + x[j]);
+    u[j] = (float)uu[j];
+    w[j] = (float)(0.5L * wx[j]);
+  }
+  for (int k = 0; k < N; ++k) {
+    long double c[RC_MAX_N + 1] = {1.0L};
+    int deg = 0;
+    long double denom = 1.0L;
+    for (int m = 0; m < N; ++m) {
+      if (m == k) continue;
+      for (int q = deg + 1; q >= 1; --q) c[q] = c[q - 1] - uu[m] * c[q];
+      c[0] = -uu[m] * c[0];
+      ++deg;
+      denom *= (uu[k] - uu[m]);
+    }
+    for (int j = 0; j < N; ++j) {
+      long double acc = 0.0L, pw = uu[j];
+      for (int q = 0; q <= deg; ++q) {
+        acc += c[q] * pw / (q + 1);
+        pw *= uu[j];
+      }
+      S[j * RC_MAX_N + k] = (float)(acc / denom);
+    }
+  }
+}
+
+static void mat3_inv(const double A[9], double inv[9], double* det_out) {
+  double det = A[0] * (A[4] * A[8] - A[5] * A[7]) - A[1] * (A[3] * A[8] - A[5] * A[6]) +
+               A[2] * (A[3] * A[7] - A[4] * A[6]);
+  *det_out = det;
+  inv[0] = (A[4] * A[8] - A[5] * A[7]) / det;
+  inv[1] = (A[2] * A[7] - A[1] * A[8]) / det;
+  inv[2] = (A[1] * A[5] - A[2] * A[4]) / det;
+  inv[3] = (A[5] * A[6] - A[3] * A[8]) / det;
+  inv[4] = (A[0] * A[8] - A[2] * A[6]) / det;
+  inv[5] = (A[2] * A[3] - A[0] * A[5]) / det;
+  inv[6] = (A[3] * A[7] - A[4] * A[6]) / det;
+  inv[7] = (A[1] * A[6] - A[0] * A[7]) / det;
+  inv[8] = (A[0] * A[4] - A[1] * A[3]) / det;
+}
+
+extern "C" rc_status rc_camera_set(rc_forest* f, const rc_camera* cam, void* stream) {
+  if (!f || !cam) return fail(RC_ERR_INVALID_ARG, "rc_camera_set: null argument");
+  auto dot = [](const double* a, const double* b) { return a[0] * b[0] + a[1] * b[1] + a[2] * b[2]; };
+  double n = sqrt(dot(cam->view, cam->view));
+  if (cam->projection != RC_PERSPECTIVE && cam->projection != RC_ORTHOGRAPHIC)
+    return fail(RC_ERR_INVALID_ARG, "bad projection");
+  if (!(n > 0) || fabs(dot(cam->right, cam->right) - 1) > 1e-9 || fabs(dot(cam->up, cam->up) - 1) > 1e-9 ||
+      fabs(dot(cam->right, cam->up)) > 1e-9 || fabs(dot(cam->right, cam->view)) > 1e-9 * n ||
+      fabs(dot(cam->up, cam->view)) > 1e-9 * n)
+    return fail(RC_ERR_INVALID_ARG, "camera frame (t,u,v) not orthonormal");
+  if (cam->projection == RC_ORTHOGRAPHIC && fabs(n - 1.0) > 1e-9)
+    return fail(RC_ERR_INVALID_ARG, "orthographic view direction must be a unit vector");
+  if (!(cam->far_dist > (cam->projection == RC_PERSPECTIVE ? n : 0.0)))
+    return fail(RC_ERR_INVALID_ARG, "far distance must exceed the near distance");
+  if (cam->width < 1 || cam->height < 1 || cam->width > 32767 || cam->height > 32767)
+    return fail(RC_ERR_INVALID_ARG, "image size out of range");
+  if (cam->gl_points < 1 || cam->gl_points > RC_MAX_N) return fail(RC_ERR_INVALID_ARG, "gl_points must be 1..8");
+  if (!(cam->pixel_size > 0)) return fail(RC_ERR_INVALID_ARG, "pixel_size must be positive");
+  cudaStream_t s = (cudaStream_t)stream;
+  f->cam = *cam;
+  CamConst& c = f->cc;
+  memset(&c, 0, sizeof c);
+  c.proj = cam->projection;
+  c.W = cam->width;
+  c.H = cam->height;
+  c.N = cam->gl_points;
+  c.newton_max = cam->newton_max_iter > 0 ? cam->newton_max_iter : 20;
+  c.newton_tol = (float)(cam->newton_tol > 0 ? cam->newton_tol : 1e-6);
+  c.n = n;
+  c.ell = cam->pixel_size;
+  c.far_dist = cam->far_dist;
+  for (int k = 0; k < 3; ++k) {
+    c.cam_rot[k] = cam->right[k];
+    c.cam_rot[3 + k] = cam->up[k];
+    c.cam_rot[6 + k] = cam->view[k] / n;
+    c.cam_org[k] = cam->origin[k];
+    if (cam->projection == RC_PERSPECTIVE) {
+      c.O0[k] = cam->origin[k];
+      c.Ot[k] = c.Ou[k] = 0.0;
+      c.R0[k] = cam->view[k];
+      c.Rt[k] = cam->pixel_size * cam->right[k];
+      c.Ru[k] = cam->pixel_size * cam->up[k];
+    } else {
+      c.O0[k] = cam->origin[k];
+      c.Ot[k] = cam->pixel_size * cam->right[k];
+      c.Ou[k] = cam->pixel_size * cam->up[k];
+      c.R0[k] = cam->view[k];
+      c.Rt[k] = c.Ru[k] = 0.0;
+    }
+  }
+  if (cam->projection == RC_PERSPECTIVE) {
+    c.amin = 1.0;
+    c.amax = cam->far_dist / n;
+  } else {
+    c.amin = 0.0;
+    c.amax = cam->far_dist;
+  }
+  gl_tables(c.N, c.u, c.w, c.S);
+  c.kappa0 = f->transfer.kappa0;
+  c.inv_F = f->transfer.inv_F;
+  c.q0 = f->transfer.q0;
+
+  // per tree: affine detection, affine ray constants, Bernstein points
+  const int R = f->R, n1 = R + 1, NP = n1 * n1 * n1;
+  const double eta2[3] = {0.0, 0.5, 1.0};
+  f->all_affine = 1;
+  for (int k = 0; k < f->K; ++k) {
+    TreeConst& T = f->h_trees[k];
+    const double* lagcopy = T.lagr;
+    // affine test: z_m == c + M eta_m
+    const double* eta = R == 1 ? nullptr : eta2;
+    auto node = [&](int m) { return R == 1 ? (double)m : eta[m]; };
+    double cc0[3], M[9];
+    for (int q = 0; q < 3; ++q) cc0[q] = lagcopy[q];
+    for (int d = 0; d < 3; ++d) {
+      int m[3] = {0, 0, 0};
+      m[d] = R;   // the node at t_d = 1
+      int idx = (m[2] * n1 + m[1]) * n1 + m[0];
+      for (int q = 0; q < 3; ++q) M[q * 3 + d] = lagcopy[idx * 3 + q] - cc0[q];
+    }
+    int affine = 1;
+    double scale = 1.0;
+    for (int q = 0; q < NP * 3; ++q) scale = std::max(scale, fabs(lagcopy[q]));
+    for (int m3 = 0; m3 < n1; ++m3)
+      for (int m2 = 0; m2 < n1; ++m2)
+        for (int m1 = 0; m1 < n1; ++m1) {
+          int idx = (m3 * n1 + m2) * n1 + m1;
+          double t[3] = {node(m1), node(m2), node(m3)};
+          for (int q = 0; q < 3; ++q) {
+            double v = cc0[q] + M[q * 3] * t[0] + M[q * 3 + 1] * t[1] + M[q * 3 + 2] * t[2];
+            if (fabs(v - lagcopy[idx * 3 + q]) > 1e-13 * scale) affine = 0;
+          }
+        }
+    double Minv[9], det = 0.0;
+    mat3_inv(M, Minv, &det);
+    if (!(fabs(det) > 0) || !isfinite(det)) affine = 0;
+    T.affine = affine;
+    if (!affine) f->all_affine = 0;
+    auto mv = [&](const double* A, const double* x, double* y) {
+      for (int r = 0; r < 3; ++r) y[r] = A[3 * r] * x[0] + A[3 * r + 1] * x[1] + A[3 * r + 2] * x[2];
+    };
+    if (affine) {
+      double tmp[3];
+      for (int q = 0; q < 3; ++q) tmp[q] = c.O0[q] - cc0[q];
+      mv(Minv, tmp, T.TO0);
+      mv(Minv, c.Ot, T.TOt);
+      mv(Minv, c.Ou, T.TOu);
+      mv(Minv, c.R0, T.TR0);
+      mv(Minv, c.Rt, T.TRt);
+      mv(Minv, c.Ru, T.TRu);
+      // camera-space affine map of the tree: X = rot (c + M t - org)
+      for (int r = 0; r < 3; ++r)
+        for (int q = 0; q < 3; ++q)
+          T.Acam[3 * r + q] = c.cam_rot[3 * r] * M[q] + c.cam_rot[3 * r + 1] * M[3 + q] + c.cam_rot[3 * r + 2] * M[6 + q];
+      for (int q = 0; q < 3; ++q) tmp[q] = cc0[q] - c.cam_org[q];
+      mv(c.cam_rot, tmp, T.bcam);
+    }
+    // Bernstein control points of J_k (Lagrange -> Bernstein per axis, R=2)
+    double B[81];
+    memcpy(B, lagcopy, sizeof(double) * NP * 3);
+    if (R == 2) {
+      for (int ax = 0; ax < 3; ++ax)
+        for (int a = 0; a < 3; ++a)
+          for (int b = 0; b < 3; ++b) {
+            int id[3];
+            for (int m = 0; m < 3; ++m) {
+              int cidx[3];
+              cidx[ax] = m;
+              cidx[(ax + 1) % 3] = a;
+              cidx[(ax + 2) % 3] = b;
+              id[m] = (cidx[2] * 3 + cidx[1]) * 3 + cidx[0];
+            }
+            for (int q = 0; q < 3; ++q) B[id[1] * 3 + q] = 2.0 * B[id[1] * 3 + q] - 0.5 * (B[id[0] * 3 + q] + B[id[2] * 3 + q]);
+          }
+    }
+    memcpy(T.Bw, B, sizeof(double) * NP * 3);
+    for (int m = 0; m < NP; ++m) {
+      double tmp[3] = {B[3 * m] - c.cam_org[0], B[3 * m + 1] - c.cam_org[1], B[3 * m + 2] - c.cam_org[2]};
+      mv(c.cam_rot, tmp, &T.Bc[3 * m]);
+    }
+  }
+  CU(cudaMemcpyAsync(f->d_trees, f->h_trees, sizeof(TreeConst) * f->K, cudaMemcpyHostToDevice, s));
+  CU(cudaMemcpyAsync(f->d_cam, &f->cc, sizeof(CamConst), cudaMemcpyHostToDevice, s));
+  // host buffers are pageable: make the copies complete before the host
+  // structures can change again (a few KB)
+  CU(cudaStreamSynchronize(s));
+  f->have_camera = true;
+  f->have_cull = f->have_cast = false;
+  return RC_OK;
+}
+
+// ---------------------------------------------------------------------------
+// cull + pair generation
+// ---------------------------------------------------------------------------
+static DevLeafView leaf_view(rc_forest* f) { return DevLeafView{f->d_anchor, f->d_tree, f->d_level, f->d_field}; }
+
+static unsigned blocks_for(int64_t n, int threads) { return (unsigned)((n + threads - 1) / threads); }
+
+extern "C" rc_status rc_cull(rc_forest* f, void* stream) {
+  if (!f) return fail(RC_ERR_INVALID_ARG, "rc_cull: null forest");
+  if (!f->have_camera) return fail(RC_ERR_STATE, "rc_cull before rc_camera_set");
+  cudaStream_t s = (cudaStream_t)stream;
+  const int64_t n = f->n;
+  DevLeafView L = leaf_view(f);
+  CU(launch_cull(f->cc, f->d_trees, L, n, f->R, f->all_affine != 0, f->d_flag, f->d_rect_all, s));
+  CU(scan_exclusive<int32_t>(f->d_flag, f->d_scan, n, f->d_scan_tmp, s));
+  CU(launch_compact(f->d_flag, f->d_rect_all, f->d_scan, n, f->d_vis, f->d_vis_rect, s));
+  // pair generation: chunk counts over all n slots (entries >= nvis are 0)
+  CU(cudaMemsetAsync(f->d_counters, 0, sizeof(int64_t) * CNT_TOTAL, s));
+  CU(cudaMemsetAsync(f->d_chunk_off, 0, sizeof(int64_t) * (n + 1), s));
+  CU(launch_chunk_count(f->d_vis_rect, f->d_scan + n, n, f->d_chunk_off, f->d_counters, s));
+  // in-place exclusive scan of the counts (each scan thread reads its items before writing them)
+  CU(scan_exclusive<int64_t>(f->d_chunk_off, f->d_chunk_off, n, f->d_scan_tmp, s));
+  f->have_cull = true;
+  f->have_cast = false;
+  return RC_OK;
+}
+
+extern "C" rc_status rc_cull_result(rc_forest* f, int32_t* d_visible, int64_t capacity, int64_t* count, void* stream) {
+  if (!f || !count) return fail(RC_ERR_INVALID_ARG, "rc_cull_result: null argument");
+  if (!f->have_cull) return fail(RC_ERR_STATE, "rc_cull_result before rc_cull");
+  cudaStream_t s = (cudaStream_t)stream;
+  int64_t nv = 0;
+  CU(cudaMemcpyAsync(&nv, f->d_scan + f->n, sizeof(int64_t), cudaMemcpyDeviceToHost, s));
+  CU(cudaStreamSynchronize(s));
+  *count = nv;
+  if (nv > capacity) return fail(RC_ERR_CAPACITY, "rc_cull_result: capacity %lld < %lld", (long long)capacity, (long long)nv);
+  if (nv > 0 && d_visible) CU(cudaMemcpyAsync(d_visible, f->d_vis, sizeof(int32_t) * nv, cudaMemcpyDeviceToDevice, s));
+  CU(cudaStreamSynchronize(s));
+  return RC_OK;
+}
+
+// ---------------------------------------------------------------------------
+// cast
+// ---------------------------------------------------------------------------
+static int sm_count() {
+  static int sms = 0;
+  if (!sms) {
+    int dev = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    if (sms <= 0) sms = 148;
+  }
+  return sms;
+}
+
+extern "C" rc_status rc_cast_segments(rc_forest* f, void* stream) {
+  if (!f) return fail(RC_ERR_INVALID_ARG, "rc_cast_segments: null forest");
+  if (!f->have_cull) return fail(RC_ERR_STATE, "rc_cast_segments before rc_cull");
+  cudaStream_t s = (cudaStream_t)stream;
+  const int64_t n = f->n;
+  // one small readback to size the chunk map and the segment buffer
+  int64_t hv[2];
+  CU(cudaMemcpyAsync(&hv[0], f->d_scan + n, sizeof(int64_t), cudaMemcpyDeviceToHost, s));
+  CU(cudaMemcpyAsync(&hv[1], f->d_chunk_off + n, sizeof(int64_t), cudaMemcpyDeviceToHost, s));
+  int64_t cand = 0;
+  CU(cudaMemcpyAsync(&cand, f->d_counters + CNT_CANDIDATES, sizeof(int64_t), cudaMemcpyDeviceToHost, s));
+  CU(cudaStreamSynchronize(s));
+  f->h_num_visible = hv[0];
+  f->h_chunks = hv[1];
+  f->h_candidates = cand;
+  const int64_t npix = (int64_t)f->cc.W * f->cc.H;
+  CU(grow(&f->d_chunk_elem, &f->chunk_cap, std::max<int64_t>(f->h_chunks, 1)));
+  // R=1/affine: at most one segment per candidate; curved: allow 1.25x + 1024 (overflow is counted)
+  int64_t need = f->all_affine ? cand + 1024 : cand + cand / 4 + 4096;
+  CU(grow(&f->d_segs, &f->seg_cap, need));
+  CU(grow(&f->d_hits_pp, &f->pix_cap, npix));
+  CU(cudaMemsetAsync(f->d_hits_pp, 0, sizeof(int32_t) * npix, s));
+  CU(cudaMemsetAsync(f->d_counters + CNT_SEGS, 0, sizeof(int64_t) * 3, s));
+  CU(cudaMemsetAsync(f->d_counters + CNT_OVERFLOW, 0, sizeof(int64_t) * 2, s));
+  if (f->h_num_visible > 0) {
+    CU(launch_expand(f->d_chunk_off, f->d_scan + n, f->h_num_visible, f->d_chunk_elem, s));
+  }
+  int grid = sm_count() * 8;
+  CU(cudaEventRecord(f->ev0, s));
+  if (f->h_chunks > 0) {
+    if (f->all_affine) {
+      CU(launch_cast_affine(f->cc, f->d_trees, leaf_view(f), f->P, f->d_vis, f->d_vis_rect, f->d_chunk_off,
+                            f->d_chunk_elem, f->h_chunks, (uint32_t)f->first_global, f->d_segs, f->seg_cap,
+                            f->d_hits_pp, f->d_counters, grid, s));
+    } else {
+      if (f->R != 2) return fail(RC_ERR_INVALID_ARG, "non-affine trees require geom_degree 2");
+      CU(launch_cast_curved(f->cc, f->d_trees, leaf_view(f), f->P, f->d_vis, f->d_vis_rect, f->d_chunk_off,
+                            f->d_chunk_elem, f->h_chunks, (uint32_t)f->first_global, f->d_segs, f->seg_cap,
+                            f->d_hits_pp, f->d_counters, sm_count() * 4, s));
+    }
+  }
+  CU(cudaEventRecord(f->ev1, s));
+  f->timed = true;
+  f->have_cast = true;
+  return RC_OK;
+}
+
+extern "C" float rc_last_cast_ms(rc_forest* f) {
+  if (!f || !f->timed) return -1.0f;
+  float ms = -1.0f;
+  if (cudaEventSynchronize(f->ev1) != cudaSuccess) return -1.0f;
+  if (cudaEventElapsedTime(&ms, f->ev0, f->ev1) != cudaSuccess) return -1.0f;
+  return ms;
+}
+
+extern "C" rc_status rc_segments_get(rc_forest* f, rc_segments* out, void* stream) {
+  if (!f || !out) return fail(RC_ERR_INVALID_ARG, "rc_segments_get: null argument");
+  if (!f->have_cast) return fail(RC_ERR_STATE, "rc_segments_get before rc_cast_segments");
+  cudaStream_t s = (cudaStream_t)stream;
+  int64_t c[CNT_TOTAL];
+  CU(cudaMemcpyAsync(c, f->d_counters, sizeof(int64_t) * CNT_TOTAL, cudaMemcpyDeviceToHost, s));
+  CU(cudaStreamSynchronize(s));
+  out->count = std::min<int64_t>(c[CNT_SEGS], f->seg_cap);
+  out->candidates = c[CNT_CANDIDATES];
+  out->hit_pairs = c[CNT_HITPAIRS];
+  out->newton_failures = c[CNT_NEWTON_FAIL];
+  out->num_visible = f->h_num_visible;
+  out->segs = f->d_segs;
+  out->hits_per_pixel = f->d_hits_pp;
+  if (c[CNT_OVERFLOW] > 0)
+    return fail(RC_ERR_CAPACITY, "segment buffer overflow: %lld records dropped", (long long)c[CNT_OVERFLOW]);
+  return RC_OK;
+}
+
+// ---------------------------------------------------------------------------
+// pack + composite
+// ---------------------------------------------------------------------------
+static rc_status check_tiling(rc_forest* f, const rc_tiling* t) {
+  if (!t) return fail(RC_ERR_INVALID_ARG, "null tiling");
+  if (t->tiles_x < 1 || t->tiles_y < 1 || f->cc.W % t->tiles_x || f->cc.H % t->tiles_y)
+    return fail(RC_ERR_INVALID_ARG, "tiles must divide the image");
+  if (t->nranks < 1 || t->nranks > 64 || t->rank < 0 || t->rank >= t->nranks)
+    return fail(RC_ERR_INVALID_ARG, "bad nranks/rank");
+  return RC_OK;
+}
+
+extern "C" rc_status rc_pack_tiles(rc_forest* f, const rc_tiling* t, int64_t* h_send_counts, const rc_seg** d_send,
+                                   void* stream) {
+  if (!f || !h_send_counts || !d_send) return fail(RC_ERR_INVALID_ARG, "rc_pack_tiles: null argument");
+  if (!f->have_cast) return fail(RC_ERR_STATE, "rc_pack_tiles before rc_cast_segments");
+  rc_status st = check_tiling(f, t);
+  if (st) return st;
+  cudaStream_t s = (cudaStream_t)stream;
+  int tw = f->cc.W / t->tiles_x, th = f->cc.H / t->tiles_y;
+  int64_t nseg = 0;
+  CU(cudaMemcpyAsync(&nseg, f->d_counters + CNT_SEGS, sizeof(int64_t), cudaMemcpyDeviceToHost, s));
+  CU(cudaStreamSynchronize(s));
+  nseg = std::min(nseg, f->seg_cap);
+  CU(grow(&f->d_send, &f->send_cap, std::max<int64_t>(nseg, 1)));
+  // counts in the counter block; [offsets(nranks+1) | cursors(nranks)] in the scan scratch
+  int64_t* d_cnt = f->d_counters + CNT_SEND;
+  static_assert(CNT_TOTAL >= CNT_SEND + 64, "counter space");
+  int64_t* d_off = f->d_scan_tmp;
+  int64_t* d_cursor = f->d_scan_tmp + 80;
+  CU(cudaMemsetAsync(d_cnt, 0, sizeof(int64_t) * t->nranks, s));
+  CU(cudaMemsetAsync(d_cursor, 0, sizeof(int64_t) * t->nranks, s));
+  int64_t* d_nseg = f->d_counters + CNT_SEGS;
+  int grid = sm_count() * 4;
+  CU(launch_pack(f->d_segs, d_nseg, f->cc.W, tw, th, t->tiles_x, t->nranks, d_cnt, nullptr, nullptr, nullptr, grid,
+                 true, s));
+  CU(cudaMemcpyAsync(h_send_counts, d_cnt, sizeof(int64_t) * t->nranks, cudaMemcpyDeviceToHost, s));
+  CU(cudaStreamSynchronize(s));
+  int64_t h_off[65];
+  h_off[0] = 0;
+  for (int r = 0; r < t->nranks; ++r) h_off[r + 1] = h_off[r] + h_send_counts[r];
+  CU(cudaMemcpyAsync(d_off, h_off, sizeof(int64_t) * (t->nranks + 1), cudaMemcpyHostToDevice, s));
+  CU(launch_pack(f->d_segs, d_nseg, f->cc.W, tw, th, t->tiles_x, t->nranks, nullptr, d_off, d_cursor, f->d_send,
+                 grid, false, s));
+  CU(cudaStreamSynchronize(s));
+  *d_send = f->d_send;
+  return RC_OK;
+}
+
+extern "C" rc_status rc_composite_tiles(rc_forest* f, const rc_tiling* t, const rc_seg* d_recv, int64_t nrecv,
+                                        const float background[3], float* d_rgba, int64_t capacity_floats,
+                                        void* stream) {
+  if (!f || !d_rgba) return fail(RC_ERR_INVALID_ARG, "rc_composite_tiles: null argument");
+  if (!f->have_camera) return fail(RC_ERR_STATE, "rc_composite_tiles before rc_camera_set");
+  rc_status st = check_tiling(f, t);
+  if (st) return st;
+  cudaStream_t s = (cudaStream_t)stream;
+  const int W = f->cc.W, H = f->cc.H;
+  const int tw = W / t->tiles_x, th = H / t->tiles_y;
+  std::vector<int32_t> mine;
+  for (int ty = 0; ty < t->tiles_y; ++ty)
+    for (int tx = 0; tx < t->tiles_x; ++tx)
+      if ((tx + ty) % t->nranks == t->rank) mine.push_back(ty * t->tiles_x + tx);
+  const int64_t npix_out = (int64_t)mine.size() * tw * th;
+  if (capacity_floats < 4 * npix_out)
+    return fail(RC_ERR_CAPACITY, "rc_composite_tiles: need %lld floats", (long long)(4 * npix_out));
+  const rc_seg* src = d_recv;
+  int64_t nsrc = nrecv;
+  if (!src) {
+    if (!f->have_cast) return fail(RC_ERR_STATE, "rc_composite_tiles: no segments");
+    int64_t c = 0;
+    CU(cudaMemcpyAsync(&c, f->d_counters + CNT_SEGS, sizeof(int64_t), cudaMemcpyDeviceToHost, s));
+    CU(cudaStreamSynchronize(s));
+    src = f->d_segs;
+    nsrc = std::min(c, f->seg_cap);
+  }
+  const int64_t npix = (int64_t)W * H;
+  // (re)allocate per-pixel arrays sized to the image
+  if (!f->d_pix_cnt || f->pix_cnt_cap < npix) {
+    if (f->d_pix_cnt) cudaFree(f->d_pix_cnt);
+    if (f->d_pix_off) cudaFree(f->d_pix_off);
+    f->d_pix_cnt = nullptr;
+    f->d_pix_off = nullptr;
+    CU(cudaMalloc((void**)&f->d_pix_cnt, sizeof(int32_t) * npix));
+    CU(cudaMalloc((void**)&f->d_pix_off, sizeof(int64_t) * (npix + 1)));
+    f->pix_cnt_cap = npix;
+  }
+  int64_t need_tmp = (int64_t)scan_tmp_size(npix + 1) + 128;
+  if (need_tmp > f->scan_tmp_cap) CU(grow(&f->d_scan_tmp, &f->scan_tmp_cap, need_tmp));
+  CU(grow(&f->d_sorted, &f->sorted_cap, std::max<int64_t>(nsrc, 1)));
+  int32_t* d_my_tiles = nullptr;
+  CU(cudaMallocAsync((void**)&d_my_tiles, sizeof(int32_t) * std::max<size_t>(mine.size(), 1), s));
+  if (!mine.empty())
+    CU(cudaMemcpyAsync(d_my_tiles, mine.data(), sizeof(int32_t) * mine.size(), cudaMemcpyHostToDevice, s));
+  CU(cudaMemsetAsync(f->d_pix_cnt, 0, sizeof(int32_t) * npix, s));
+  int grid = sm_count() * 8;
+  if (nsrc > 0) {
+    CU(launch_hist(src, nsrc, f->d_pix_cnt, grid, s));
+  }
+  CU(scan_exclusive<int32_t>(f->d_pix_cnt, f->d_pix_off, npix, f->d_scan_tmp, s));
+  CU(cudaMemsetAsync(f->d_pix_cnt, 0, sizeof(int32_t) * npix, s));
+  if (nsrc > 0) {
+    CU(launch_scatter(src, nsrc, f->d_pix_off, f->d_pix_cnt, f->d_sorted, grid, s));
+  }
+  if (npix_out > 0) {
+    float bg[3] = {0, 0, 0};
+    if (background) memcpy(bg, background, sizeof bg);
+    CU(launch_fold(f->d_sorted, f->d_pix_off, W, H, tw, th, d_my_tiles, t->tiles_x, npix_out, bg, 1e-6f, d_rgba,
+                   sm_count() * 16, s));
+  }
+  CU(cudaFreeAsync(d_my_tiles, s));
+  return RC_OK;
+}
+
+extern "C" rc_status rc_composite(rc_forest* f, const float background[3], float* d_rgba, int64_t capacity_floats,
+                                  void* stream) {
+  if (!f) return fail(RC_ERR_INVALID_ARG, "rc_composite: null forest");
+  rc_tiling t{1, 1, 1, 0};
+  return rc_composite_tiles(f, &t, nullptr, 0, background, d_rgba, capacity_floats, stream);
+}
+
+extern "C" rc_status rc_aggregate(rc_forest* f, int32_t cycles, void* stream) {
+  if (!f) return fail(RC_ERR_INVALID_ARG, "rc_aggregate: null forest");
+  if (cycles < 0) return fail(RC_ERR_INVALID_ARG, "cycles must be >= 0");
+  if (cycles == 0) return RC_OK;
+  if (!f->have_cast) return fail(RC_ERR_STATE, "rc_aggregate before rc_cast_segments");
+  (void)stream;
+  return fail(RC_ERR_STATE, "rc_aggregate: coarsening cycles not built yet");
+}
+
+extern "C" rc_status rc_render_frame(rc_forest* f, const rc_camera* cam, int32_t cycles, const float background[3],
+                                     float* d_rgba, int64_t capacity_floats, int64_t* hit_pairs, void* stream) {
+  rc_status st;
+  if ((st = rc_camera_set(f, cam, stream))) return st;
+  if ((st = rc_cull(f, stream))) return st;
+  if ((st = rc_cast_segments(f, stream))) return st;
+  if (cycles > 0 && (st = rc_aggregate(f, cycles, stream))) return st;
+  if ((st = rc_composite(f, background, d_rgba, capacity_floats, stream))) return st;
+  if (hit_pairs) {
+    cudaStream_t s = (cudaStream_t)stream;
+    CU(cudaMemcpyAsync(hit_pairs, f->d_counters + CNT_HITPAIRS, sizeof(int64_t), cudaMemcpyDeviceToHost, s));
+    CU(cudaStreamSynchronize(s));
+  }
+  return RC_OK;
+}

@@ -1,0 +1,127 @@
+// rc_internal.cuh -- internal definitions of librc (B200 / sm_100a).
+// Shares nothing with oracle/ (independent implementation of the method).
+#pragma once
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include "../../include/rc.h"
+
+#define RC_MAX_N 8          // GL points per segment
+#define RC_MAX_TREES 4096
+#define RC_MAXLEVEL 18
+#define RC_CHUNK 32         // candidate pairs per warp work item (one element)
+
+// Camera constants (host fp64 preprocessing, rc_camera_set).
+struct CamConst {
+  int proj, W, H, N;
+  int newton_max;
+  float newton_tol;
+  double O0[3], Ot[3], Ou[3];   // world ray origin  O(i,j) = O0 + di Ot + dj Ou
+  double R0[3], Rt[3], Ru[3];   // world ray dir     R(i,j) = R0 + di Rt + dj Ru
+  double amin, amax;            // visible alpha range
+  double cam_rot[9];            // rows t, u, v/n
+  double cam_org[3];            // o (perspective) / P0 (ortho)
+  double n, ell, far_dist;
+  float u[RC_MAX_N], w[RC_MAX_N], S[RC_MAX_N * RC_MAX_N];
+  float kappa0, inv_F, q0;
+};
+
+// Per-tree constants (device buffer, warp-uniform reads).
+struct TreeConst {
+  int affine;                   // 1: J_k affine -> slab path
+  int pad;
+  // affine: tree-reference ray t(i,j,alpha) = TO0 + di TOt + dj TOu + alpha (TR0 + di TRt + dj TRu)
+  double TO0[3], TOt[3], TOu[3], TR0[3], TRt[3], TRu[3];
+  // affine culling: camera-space X = Acam t + bcam
+  double Acam[9], bcam[3];
+  // Bernstein control points of J_k: world [27][3] and camera space [27][3]
+  double Bw[81];
+  double Bc[81];
+  double lagr[81];              // Lagrange control points as given (host copy)
+};
+
+struct DevLeafView {
+  const int32_t* anchor;  // [n][3]
+  const int32_t* tree;    // [n]
+  const int8_t* level;    // [n]
+  const float* field;     // [n][(P+1)^3]
+};
+
+// short rect (i0,i1,j0,j1), inclusive
+struct __align__(8) Rect16 {
+  int16_t i0, i1, j0, j1;
+};
+
+struct rc_forest {
+  int K, R, P;
+  int64_t n, first_global;
+  rc_transfer transfer;
+  // device leaves
+  int32_t* d_anchor = nullptr;
+  int32_t* d_tree = nullptr;
+  int8_t* d_level = nullptr;
+  float* d_field = nullptr;
+  // camera
+  bool have_camera = false, have_cull = false, have_cast = false;
+  rc_camera cam{};
+  CamConst cc{};
+  TreeConst* d_trees = nullptr;
+  TreeConst* h_trees = nullptr;
+  CamConst* d_cam = nullptr;
+  int all_affine = 1;
+  // cull
+  int32_t* d_flag = nullptr;      // [n] visible flag
+  Rect16* d_rect_all = nullptr;   // [n]
+  int64_t* d_scan = nullptr;      // [n+1]
+  int32_t* d_vis = nullptr;       // [n] compacted visible leaf index
+  Rect16* d_vis_rect = nullptr;   // [n]
+  int64_t* d_chunk_off = nullptr; // [n+1]
+  int64_t* d_counters = nullptr;  // misc device counters (see enum in rc.cu)
+  int64_t h_num_visible = 0;
+  // chunks / segments
+  int32_t* d_chunk_elem = nullptr;
+  int64_t chunk_cap = 0;
+  rc_seg* d_segs = nullptr;
+  int64_t seg_cap = 0;
+  int32_t* d_hits_pp = nullptr;   // [W*H]
+  int64_t pix_cap = 0;
+  int64_t h_candidates = 0, h_chunks = 0;
+  // composite scratch
+  int32_t* d_pix_cnt = nullptr;   // [W*H]
+  int64_t pix_cnt_cap = 0;
+  int64_t* d_pix_off = nullptr;   // [W*H+1]
+  rc_seg* d_sorted = nullptr;
+  int64_t sorted_cap = 0;
+  rc_seg* d_send = nullptr;
+  int64_t send_cap = 0;
+  // scan scratch
+  int64_t* d_scan_tmp = nullptr;
+  int64_t scan_tmp_cap = 0;
+  // timing
+  cudaEvent_t ev0 = nullptr, ev1 = nullptr;
+  bool timed = false;
+};
+
+// Device counters layout
+enum {
+  CNT_SEGS = 0,        // segment records written
+  CNT_HITPAIRS = 1,    // pairs with >= 1 segment
+  CNT_NEWTON_FAIL = 2,
+  CNT_CANDIDATES = 3,
+  CNT_OVERFLOW = 4,
+  CNT_WORK = 5,        // dynamic work counter of the segment kernel
+  CNT_SEND = 8,        // [8..8+64) per-rank cursors for pack
+  CNT_TOTAL = 80
+};
+
+// ---- kernels / launchers (defined in the .cu files) ----
+namespace rc {
+extern int64_t g_launches;
+cudaError_t scan_exclusive_i64(const int64_t* in, int64_t* out, int64_t n, int64_t* tmp, cudaStream_t s);
+size_t scan_tmp_size(int64_t n);
+}  // namespace rc
+
+namespace rc {
+template <typename Tin>
+cudaError_t scan_exclusive(const Tin* in, int64_t* out, int64_t n, int64_t* tmp, cudaStream_t s);
+}  // namespace rc

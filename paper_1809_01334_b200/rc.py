@@ -1,0 +1,292 @@
+"""Thin ctypes binding of librc (include/rc.h).  Argument marshalling only:
+every step of the hot path runs in the CUDA kernels of librc.so.  There is no
+CPU fallback: a missing or unloadable librc.so raises RcError."""
+from __future__ import annotations
+
+import ctypes as C
+import os
+from typing import Optional, Sequence
+
+import numpy as np
+
+HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(HERE, "librc.so")
+
+RC_OK = 0
+RC_ERR_CAPACITY = -6
+STATUS_NAMES = {0: "RC_OK", -1: "RC_ERR_INVALID_ARG", -2: "RC_ERR_NOT_SFC_SORTED", -3: "RC_ERR_OUT_OF_MEMORY",
+                -4: "RC_ERR_CUDA", -6: "RC_ERR_CAPACITY", -7: "RC_ERR_STATE", -8: "RC_ERR_NUMERIC"}
+RC_HOST_COPY, RC_DEVICE_COPY = 0, 1
+RC_PERSPECTIVE, RC_ORTHOGRAPHIC = 0, 1
+
+
+class RcError(RuntimeError):
+    def __init__(self, status, msg):
+        super().__init__(f"{STATUS_NAMES.get(status, status)}: {msg}")
+        self.status = status
+
+
+class Transfer(C.Structure):
+    _fields_ = [("kappa0", C.c_float), ("inv_F", C.c_float), ("q0", C.c_float)]
+
+
+class ForestDesc(C.Structure):
+    _fields_ = [("num_trees", C.c_int32), ("geom_degree", C.c_int32), ("tree_ctrl", C.c_void_p),
+                ("field_degree", C.c_int32), ("num_leaves", C.c_int64), ("first_global_leaf", C.c_int64),
+                ("leaf_anchor", C.c_void_p), ("leaf_tree", C.c_void_p), ("leaf_level", C.c_void_p),
+                ("leaf_field", C.c_void_p), ("memory", C.c_int32), ("transfer", Transfer)]
+
+
+class CameraDesc(C.Structure):
+    _fields_ = [("projection", C.c_int32), ("origin", C.c_double * 3), ("view", C.c_double * 3),
+                ("right", C.c_double * 3), ("up", C.c_double * 3), ("pixel_size", C.c_double),
+                ("far_dist", C.c_double), ("width", C.c_int32), ("height", C.c_int32), ("gl_points", C.c_int32),
+                ("newton_tol", C.c_double), ("newton_max_iter", C.c_int32)]
+
+
+class Segments(C.Structure):
+    _fields_ = [("count", C.c_int64), ("candidates", C.c_int64), ("hit_pairs", C.c_int64),
+                ("newton_failures", C.c_int64), ("num_visible", C.c_int64), ("segs", C.c_void_p),
+                ("hits_per_pixel", C.c_void_p)]
+
+
+class Tiling(C.Structure):
+    _fields_ = [("tiles_x", C.c_int32), ("tiles_y", C.c_int32), ("nranks", C.c_int32), ("rank", C.c_int32)]
+
+
+SEG_BYTES = 32
+EXPORTS = ["rc_last_error", "rc_version", "rc_forest_create", "rc_forest_destroy", "rc_camera_set", "rc_cull",
+           "rc_cull_result", "rc_cast_segments", "rc_segments_get", "rc_aggregate", "rc_pack_tiles",
+           "rc_composite_tiles", "rc_composite", "rc_render_frame", "rc_launch_count", "rc_last_cast_ms"]
+
+_lib = None
+
+
+def lib():
+    """Load librc.so (built by paper_1809_01334_b200.build); raise if missing."""
+    global _lib
+    if _lib is not None:
+        return _lib
+    if not os.path.exists(LIB_PATH):
+        raise RcError(-4, f"{LIB_PATH} is missing: run __graft_entry__.build() (no CPU fallback exists)")
+    L = C.CDLL(LIB_PATH)
+    vp, i32, i64 = C.c_void_p, C.c_int32, C.c_int64
+    L.rc_last_error.restype = C.c_char_p
+    L.rc_version.restype = i32
+    L.rc_forest_create.argtypes = [C.POINTER(ForestDesc), vp, C.POINTER(vp)]
+    L.rc_forest_destroy.argtypes = [vp]
+    L.rc_camera_set.argtypes = [vp, C.POINTER(CameraDesc), vp]
+    L.rc_cull.argtypes = [vp, vp]
+    L.rc_cull_result.argtypes = [vp, vp, i64, C.POINTER(i64), vp]
+    L.rc_cast_segments.argtypes = [vp, vp]
+    L.rc_segments_get.argtypes = [vp, C.POINTER(Segments), vp]
+    L.rc_aggregate.argtypes = [vp, i32, vp]
+    L.rc_pack_tiles.argtypes = [vp, C.POINTER(Tiling), vp, C.POINTER(vp), vp]
+    L.rc_composite_tiles.argtypes = [vp, C.POINTER(Tiling), vp, i64, vp, vp, i64, vp]
+    L.rc_composite.argtypes = [vp, vp, vp, i64, vp]
+    L.rc_render_frame.argtypes = [vp, C.POINTER(CameraDesc), i32, vp, vp, i64, C.POINTER(i64), vp]
+    L.rc_launch_count.argtypes = [i32]
+    L.rc_launch_count.restype = i64
+    L.rc_last_cast_ms.argtypes = [vp]
+    L.rc_last_cast_ms.restype = C.c_float
+    for name in EXPORTS:
+        getattr(L, name).restype = getattr(L, name).restype if name in (
+            "rc_last_error", "rc_version", "rc_launch_count", "rc_last_cast_ms") else C.c_int
+    _lib = L
+    return L
+
+
+def _check(st):
+    if st != RC_OK:
+        raise RcError(st, lib().rc_last_error().decode(errors="replace"))
+
+
+def _stream(stream):
+    if stream is None:
+        import torch
+        return C.c_void_p(torch.cuda.current_stream().cuda_stream)
+    if isinstance(stream, int):
+        return C.c_void_p(stream)
+    return C.c_void_p(stream.cuda_stream)
+
+
+class _DevArray:
+    """Zero-copy __cuda_array_interface__ wrapper of a library-owned buffer."""
+
+    def __init__(self, ptr, shape, typestr):
+        self.__cuda_array_interface__ = {"data": (int(ptr), False), "shape": tuple(shape), "typestr": typestr,
+                                         "version": 3, "strides": None}
+
+
+def device_view(ptr, shape, typestr):
+    import torch
+    if int(ptr or 0) == 0 or int(np.prod(shape)) == 0:
+        dt = {"<i4": torch.int32, "<f4": torch.float32, "<i8": torch.int64, "<u4": torch.int32}[typestr]
+        return torch.empty(shape, dtype=dt, device="cuda")
+    return torch.as_tensor(_DevArray(ptr, shape, typestr), device="cuda")
+
+
+def camera_desc(cam, gl_points=None, newton_tol=None, newton_max_iter=None) -> CameraDesc:
+    d3 = C.c_double * 3
+    return CameraDesc(int(cam.projection), d3(*map(float, cam.origin)), d3(*map(float, cam.view)),
+                      d3(*map(float, cam.right)), d3(*map(float, cam.up)), float(cam.pixel_size),
+                      float(cam.far_dist), int(cam.width), int(cam.height),
+                      int(gl_points or cam.gl_points), float(newton_tol or cam.newton_tol),
+                      int(newton_max_iter or cam.newton_max_iter))
+
+
+def unpack_segments(raw):
+    """raw: int32 tensor [n, 8] of rc_seg records -> dict of column views."""
+    import torch
+    f = raw.view(torch.float32)
+    return {"pixel": raw[:, 0], "alpha_near": f[:, 1], "alpha_far": f[:, 2], "a": f[:, 3], "b": f[:, 4:7],
+            "key": raw[:, 7]}
+
+
+class Forest:
+    """rc_forest handle.  Leaf arrays may be numpy (host copy) or CUDA tensors
+    (device copy); they are copied by rc_forest_create."""
+
+    def __init__(self, tree_ctrl, geom_degree, field_degree, leaf_anchor, leaf_tree, leaf_level, leaf_field,
+                 kappa0, inv_F, q0, first_global_leaf=0, stream=None):
+        import torch
+        L = lib()
+        ctrl = np.ascontiguousarray(tree_ctrl if isinstance(tree_ctrl, np.ndarray) else tree_ctrl.cpu().numpy(),
+                                    dtype=np.float64)
+        on_dev = isinstance(leaf_anchor, torch.Tensor) and leaf_anchor.is_cuda
+        if on_dev:
+            keep = [leaf_anchor.contiguous().to(torch.int32), leaf_tree.contiguous().to(torch.int32),
+                    leaf_level.contiguous().to(torch.int8), leaf_field.contiguous().to(torch.float32)]
+            ptrs = [t.data_ptr() for t in keep]
+            mem = RC_DEVICE_COPY
+        else:
+            def npy(a, dt):
+                a = a.cpu().numpy() if isinstance(a, torch.Tensor) else a
+                return np.ascontiguousarray(a, dtype=dt)
+            keep = [npy(leaf_anchor, np.int32), npy(leaf_tree, np.int32), npy(leaf_level, np.int8),
+                    npy(leaf_field, np.float32)]
+            ptrs = [k.ctypes.data for k in keep]
+            mem = RC_HOST_COPY
+        n = int(keep[1].shape[0])
+        self.n = n
+        self.P = int(field_degree)
+        self.R = int(geom_degree)
+        desc = ForestDesc(int(ctrl.shape[0]), int(geom_degree), ctrl.ctypes.data, int(field_degree), n,
+                          int(first_global_leaf), ptrs[0], ptrs[1], ptrs[2], ptrs[3], mem,
+                          Transfer(float(kappa0), float(inv_F), float(q0)))
+        h = C.c_void_p()
+        _check(L.rc_forest_create(C.byref(desc), _stream(stream), C.byref(h)))
+        self.h = h
+        self.cam = None
+
+    @classmethod
+    def from_scene(cls, scene, first=0, count=None, device_copy=False, stream=None):
+        """Build from a scenegen.Scene-like object (attributes only, duck typed)."""
+        import torch
+        hi = scene.num_leaves if count is None else first + count
+        arrs = [scene.leaf_anchor[first:hi], scene.leaf_tree[first:hi], scene.leaf_level[first:hi],
+                scene.leaf_field[first:hi]]
+        if device_copy:
+            arrs = [torch.as_tensor(np.ascontiguousarray(a) if isinstance(a, np.ndarray) else a).cuda() for a in arrs]
+        return cls(scene.tree_ctrl, scene.geom_degree, scene.field_degree, *arrs, scene.kappa0, scene.inv_F,
+                   scene.q0, first_global_leaf=first, stream=stream)
+
+    def close(self):
+        if getattr(self, "h", None):
+            lib().rc_forest_destroy(self.h)
+            self.h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    # -- pipeline --------------------------------------------------------
+    def camera_set(self, cam, stream=None, **kw):
+        self.cam = cam
+        self.W, self.H = int(cam.width), int(cam.height)
+        d = camera_desc(cam, **kw)
+        _check(lib().rc_camera_set(self.h, C.byref(d), _stream(stream)))
+
+    def cull(self, stream=None):
+        _check(lib().rc_cull(self.h, _stream(stream)))
+
+    def cull_result(self, stream=None):
+        import torch
+        cnt = C.c_int64()
+        buf = torch.empty(self.n, dtype=torch.int32, device="cuda")
+        _check(lib().rc_cull_result(self.h, C.c_void_p(buf.data_ptr()), self.n, C.byref(cnt), _stream(stream)))
+        return buf[:cnt.value]
+
+    def cast_segments(self, stream=None):
+        _check(lib().rc_cast_segments(self.h, _stream(stream)))
+
+    def segments(self, stream=None):
+        s = Segments()
+        _check(lib().rc_segments_get(self.h, C.byref(s), _stream(stream)))
+        raw = device_view(s.segs, (s.count, 8), "<i4")
+        hpp = device_view(s.hits_per_pixel, (self.H, self.W), "<i4")
+        return {"count": s.count, "candidates": s.candidates, "hit_pairs": s.hit_pairs,
+                "newton_failures": s.newton_failures, "num_visible": s.num_visible, "raw": raw,
+                "hits_per_pixel": hpp}
+
+    def aggregate(self, cycles, stream=None):
+        _check(lib().rc_aggregate(self.h, int(cycles), _stream(stream)))
+
+    def composite(self, background=(0.0, 0.0, 0.0), out=None, stream=None):
+        import torch
+        if out is None:
+            out = torch.empty((self.H, self.W, 4), dtype=torch.float32, device="cuda")
+        bg = (C.c_float * 3)(*background)
+        _check(lib().rc_composite(self.h, bg, C.c_void_p(out.data_ptr()), out.numel(), _stream(stream)))
+        return out
+
+    def pack_tiles(self, tiles_x, tiles_y, nranks, rank, stream=None):
+        t = Tiling(tiles_x, tiles_y, nranks, rank)
+        counts = (C.c_int64 * nranks)()
+        ptr = C.c_void_p()
+        _check(lib().rc_pack_tiles(self.h, C.byref(t), counts, C.byref(ptr), _stream(stream)))
+        cnt = [int(c) for c in counts]
+        raw = device_view(ptr.value, (sum(cnt), 8), "<i4")
+        return raw, cnt
+
+    def composite_tiles(self, tiles_x, tiles_y, nranks, rank, recv=None, background=(0.0, 0.0, 0.0), out=None,
+                        stream=None):
+        import torch
+        t = Tiling(tiles_x, tiles_y, nranks, rank)
+        tw, th = self.W // tiles_x, self.H // tiles_y
+        mine = [(tx, ty) for ty in range(tiles_y) for tx in range(tiles_x) if (tx + ty) % nranks == rank]
+        if out is None:
+            out = torch.empty((len(mine), th, tw, 4), dtype=torch.float32, device="cuda")
+        bg = (C.c_float * 3)(*background)
+        rp = C.c_void_p(recv.data_ptr()) if recv is not None and recv.numel() else C.c_void_p(
+            0 if recv is None else 1)
+        if recv is not None and recv.numel() == 0:
+            # zero records received: pass a non-null pointer with count 0
+            dummy = torch.empty((1, 8), dtype=torch.int32, device="cuda")
+            rp = C.c_void_p(dummy.data_ptr())
+        nrecv = 0 if recv is None else int(recv.shape[0])
+        _check(lib().rc_composite_tiles(self.h, C.byref(t), rp, nrecv, bg, C.c_void_p(out.data_ptr()), out.numel(),
+                                        _stream(stream)))
+        return out, mine
+
+    def render_frame(self, cam, cycles=0, background=(0.0, 0.0, 0.0), out=None, stream=None):
+        import torch
+        self.cam = cam
+        self.W, self.H = int(cam.width), int(cam.height)
+        if out is None:
+            out = torch.empty((self.H, self.W, 4), dtype=torch.float32, device="cuda")
+        d = camera_desc(cam)
+        hp = C.c_int64()
+        bg = (C.c_float * 3)(*background)
+        _check(lib().rc_render_frame(self.h, C.byref(d), int(cycles), bg, C.c_void_p(out.data_ptr()), out.numel(),
+                                     C.byref(hp), _stream(stream)))
+        return out, hp.value
+
+    def last_cast_ms(self):
+        return float(lib().rc_last_cast_ms(self.h))
+
+
+def launch_count(reset=False) -> int:
+    return int(lib().rc_launch_count(1 if reset else 0))
