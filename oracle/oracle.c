@@ -10,6 +10,7 @@
 #include <math.h>
 #include <stdlib.h>
 #include <string.h>
+#include <stdio.h>
 #ifdef _OPENMP
 #include <omp.h>
 #endif
@@ -623,23 +624,47 @@ static void bz_split(int R, const double g[9][2], int dir, double L[9][2], doubl
 static void face_subdiv(face_ctx* f, const double g[9][2], double s1a, double s1b, double s2a,
                         double s2b) {
   int R = f->sc->R, np = (R + 1) * (R + 1);
-  if (++f->boxes > 200000) { f->fail = 1; return; }
+  if (++f->boxes > 400000) { f->fail = 1; return; }
   double mn[2] = {INFINITY, INFINITY}, mx[2] = {-INFINITY, -INFINITY};
   for (int m = 0; m < np; ++m)
     for (int c = 0; c < 2; ++c) { mn[c] = fmin(mn[c], g[m][c]); mx[c] = fmax(mx[c], g[m][c]); }
   if (mn[0] > 0 || mx[0] < 0 || mn[1] > 0 || mx[1] < 0) return;   /* hull excludes the ray */
-  if (fmax(s1b - s1a, s2b - s2a) < 1e-3) {
+  double width = fmax(s1b - s1a, s2b - s2a);
+  if (width < 1e-3) {
+    /* Newton from the box centre; a root it lands on inside this box is
+     * accepted.  If it leaves the box (ill-conditioned grazing rays can jump
+     * to another root), keep subdividing: the hull test alone converges to
+     * every root (exhaustive Bezier subdivision). */
     froot rt;
     double so1, so2;
     if (face_newton(f, 0.5 * (s1a + s1b), 0.5 * (s2a + s2b), &rt, &so1, &so2) == 0) {
-      double tol = 1e-7;
-      if (so1 >= s1a - tol && so1 <= s1b + tol && so2 >= s2a - tol && so2 <= s2b + tol &&
-          so1 >= -1e-12 && so1 <= 1 + 1e-12 && so2 >= -1e-12 && so2 <= 1 + 1e-12) {
-        if (f->nroots < f->cap) f->roots[f->nroots++] = rt;
-        else f->fail = 1;
+      double tol = 1e-9;
+      if (so1 >= s1a - tol && so1 <= s1b + tol && so2 >= s2a - tol && so2 <= s2b + tol) {
+        if (so1 >= -1e-12 && so1 <= 1 + 1e-12 && so2 >= -1e-12 && so2 <= 1 + 1e-12) {
+          if (f->nroots < f->cap) f->roots[f->nroots++] = rt;
+          else f->fail = 1;
+        }
+        return;
       }
     }
-    return;
+    if (width < 1e-11) {   /* converged by subdivision alone: accept the box centre */
+      double xi[3], X[3], J[9], nrm[3];
+      face_point(f, 0.5 * (s1a + s1b), 0.5 * (s2a + s2b), xi);
+      orc_element_map(f->sc, f->e, xi, X, J);
+      double Xa[3] = {J[f->ax], J[3 + f->ax], J[6 + f->ax]}, Xb[3] = {J[f->bx], J[3 + f->bx], J[6 + f->bx]};
+      cross3(Xa, Xb, nrm);
+      double rr = dot3(f->r, f->r);
+      froot rt2;
+      rt2.alpha = dot3(f->r, (double[3]){X[0] - f->o[0], X[1] - f->o[1], X[2] - f->o[2]}) / rr;
+      rt2.cosphi = fabs(dot3(nrm, f->r)) / (sqrt(dot3(nrm, nrm)) * sqrt(rr));
+      memcpy(rt2.xi, xi, sizeof xi);
+      double m1 = 0.5 * (s1a + s1b), m2 = 0.5 * (s2a + s2b);
+      if (m1 >= 0 && m1 <= 1 && m2 >= 0 && m2 <= 1) {
+        if (f->nroots < f->cap) f->roots[f->nroots++] = rt2;
+        else f->fail = 1;
+      }
+      return;
+    }
   }
   double L[9][2], H[9][2];
   if (s1b - s1a >= s2b - s2a) {
@@ -730,6 +755,11 @@ static int general_segments(const orc_scene* sc, int64_t e, const double o[3], c
     fail |= f.fail;
   }
   qsort(roots, nr, sizeof(froot), cmp_froot);
+  if (getenv("ORC_DEBUG")) {
+    fprintf(stderr, "roots %d:", nr);
+    for (int q = 0; q < nr; ++q) fprintf(stderr, " (%.9f c%.2e xi %.4f %.4f %.4f)", roots[q].alpha, roots[q].cosphi, roots[q].xi[0], roots[q].xi[1], roots[q].xi[2]);
+    fprintf(stderr, "\n");
+  }
   /* dedupe roots found on several faces / sub-boxes */
   double rn = sqrt(dot3(r, r));
   int m = 0;
@@ -792,6 +822,18 @@ static double min_edge(const orc_scene* sc, int64_t e, int k) {
       best = fmin(best, sqrt(dot3(d, d)));
     }
   return best;
+}
+
+/* debug/test export: general-path segments with the parameter domain
+ * [-delta, 1+delta]^3 (E+ for delta > 0, E- for delta < 0). */
+int orc_intersect_domain(const orc_scene* sc, const orc_camera* cam, int64_t e, int i, int j, double delta,
+                         int max_seg, double* seg, int* flags) {
+  double o[3], r[3], amin, amax, lo[3], hi[3];
+  orc_ray(cam, i, j, o, r);
+  alpha_range(cam, &amin, &amax);
+  for (int k = 0; k < 3; ++k) { lo[k] = -delta; hi[k] = 1 + delta; }
+  *flags = 0;
+  return general_segments(sc, e, o, r, amin, amax, lo, hi, max_seg, seg, flags);
 }
 
 /* Segments of the ray of pixel (i,j) inside element e (E0), with the

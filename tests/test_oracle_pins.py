@@ -611,3 +611,44 @@ def test_generator_pins():
     r = np.linalg.norm(sh.tree_ctrl, axis=-1)
     for m3, rr in enumerate((0.55, 0.775, 1.0)):
         np.testing.assert_allclose(r[:, m3], rr, atol=1e-15)
+
+
+def test_skimming_rays_two_roots_one_face_P11():
+    """Rays grazing the outer sphere face enter and exit through the SAME
+    curved face (<= 8 roots per biquadratic face).  For
+    every candidate pair of coarse level-1 elements near the silhouette the
+    segments must equal the inside-intervals found by dense sampling of the
+    inverse map (brute force), ambiguous or not, away from 1e-6 of an end."""
+    sh = sg.shell_uniform(1, 48, 4)
+    o = oracle.OracleScene(sh)
+    vis, amb, rects = o.cull()
+    W = sh.camera.width
+    checked, skims = 0, 0
+    for e in range(sh.num_leaves):
+        if not vis[e]:
+            continue
+        rc = rects[e]
+        for j in range(rc[2], rc[3] + 1, 2):
+            for i in range(rc[0], rc[1] + 1, 2):
+                ro, rd = o.ray(i, j)
+                if abs(np.linalg.norm(np.cross(ro, rd)) / np.linalg.norm(rd) - 1.0) > 0.08:
+                    continue          # keep rays passing near the outer silhouette only
+                seg, fl = o.intersect(e, i, j)
+                lo, hi = o.aabb(e)
+                al = np.linspace(lo[2] * 0.999, hi[2] * 1.001, 3000)
+                inside = []
+                for a in al:
+                    st, xi = o.inverse_map(e, ro + a * rd)
+                    inside.append(st == 0 and np.all(xi >= 0) and np.all(xi <= 1))
+                for a, ins in zip(al, inside):
+                    inseg = any(a0 <= a <= a1 for a0, a1 in seg)
+                    near = any(min(abs(a - a0), abs(a - a1)) * np.linalg.norm(rd) < 2e-6 for a0, a1 in seg)
+                    if not near:
+                        assert ins == inseg, (e, i, j, a, seg)
+                checked += 1
+                if len(seg) and np.sum(np.diff(np.r_[False, inside, False].astype(int)) == 1) >= 1:
+                    st0, x0 = o.inverse_map(e, ro + seg[0][0] * rd)
+                    st1, x1 = o.inverse_map(e, ro + seg[-1][1] * rd)
+                    if abs(x0[2] - 1) < 1e-9 and abs(x1[2] - 1) < 1e-9:
+                        skims += 1       # entry and exit on the outer face
+    assert checked > 50 and skims > 3
