@@ -455,12 +455,17 @@ int orc_inverse_map(const orc_scene* sc, int64_t e, const double x[3], double xi
   for (int k = 0; k < 3; ++k) rhs[k] = x[k] - X[k];
   if (solve3(J, rhs, d)) return -1;
   for (int k = 0; k < 3; ++k) xi[k] = 0.5 + d[k];
+  double prev = INFINITY;
   for (int it = 0; it < 80; ++it) {
     orc_element_map(sc, e, xi, X, J);
     for (int k = 0; k < 3; ++k) rhs[k] = x[k] - X[k];
     if (solve3(J, rhs, d)) return -1;
     for (int k = 0; k < 3; ++k) xi[k] += d[k];
-    if (fabs(d[0]) < 1e-14 && fabs(d[1]) < 1e-14 && fabs(d[2]) < 1e-14) return 0;
+    double st = fmax(fabs(d[0]), fmax(fabs(d[1]), fabs(d[2])));
+    /* converged: step below 1e-12, or stagnating at the fp64 rounding floor
+     * (|x| ~ 1 against elements of size h gives ~1e-16/h noise in xi) */
+    if (st < 1e-12 || (st < 1e-9 && st >= 0.5 * prev)) return 0;
+    prev = st;
     if (!(fabs(xi[0]) < 1e6 && fabs(xi[1]) < 1e6 && fabs(xi[2]) < 1e6)) return -1;
   }
   return -2;
@@ -558,6 +563,7 @@ static void face_point(face_ctx* f, double s1, double s2, double xi[3]) {
 static int face_newton(face_ctx* f, double s1, double s2, froot* out, double* so1, double* so2) {
   double xi[3], X[3], J[9];
   face_point(f, s1, s2, xi);
+  double prev = INFINITY;
   for (int it = 0; it < 60; ++it) {
     orc_element_map(f->sc, f->e, xi, X, J);
     double dx[3] = {X[0] - f->o[0], X[1] - f->o[1], X[2] - f->o[2]};
@@ -571,7 +577,8 @@ static int face_newton(face_ctx* f, double s1, double s2, froot* out, double* so
     xi[f->ax] -= da;
     xi[f->bx] -= db;
     if (!(fabs(xi[f->ax]) < 10 && fabs(xi[f->bx]) < 10)) return -1;
-    if (fabs(da) < 1e-14 && fabs(db) < 1e-14) {
+    double st = fmax(fabs(da), fabs(db));
+    if (st < 1e-12 || (st < 1e-9 && st >= 0.5 * prev)) {   /* see orc_inverse_map */
       orc_element_map(f->sc, f->e, xi, X, J);
       double Xa2[3] = {J[f->ax], J[3 + f->ax], J[6 + f->ax]};
       double Xb2[3] = {J[f->bx], J[3 + f->bx], J[6 + f->bx]};
@@ -585,6 +592,7 @@ static int face_newton(face_ctx* f, double s1, double s2, froot* out, double* so
       *so2 = (xi[f->bx] - f->lo_b) / (f->hi_b - f->lo_b);
       return 0;
     }
+    prev = st;
   }
   return -2;
 }
@@ -624,7 +632,7 @@ static void bz_split(int R, const double g[9][2], int dir, double L[9][2], doubl
 static void face_subdiv(face_ctx* f, const double g[9][2], double s1a, double s1b, double s2a,
                         double s2b) {
   int R = f->sc->R, np = (R + 1) * (R + 1);
-  if (++f->boxes > 400000) { f->fail = 1; return; }
+  if (++f->boxes > 400000) { if (getenv("ORC_DEBUG")) fprintf(stderr, "box limit face %d\n", f->fixk); f->fail = 1; return; }
   double mn[2] = {INFINITY, INFINITY}, mx[2] = {-INFINITY, -INFINITY};
   for (int m = 0; m < np; ++m)
     for (int c = 0; c < 2; ++c) { mn[c] = fmin(mn[c], g[m][c]); mx[c] = fmax(mx[c], g[m][c]); }
@@ -690,7 +698,7 @@ static int inside_elem(const orc_scene* sc, int64_t e, const double lo[3], const
   for (int c = 0; c < 3; ++c)
     if (p[c] < wlo[c] || p[c] > whi[c]) return 0;
   double xi[3];
-  if (orc_inverse_map(sc, e, p, xi) != 0) { *fail = 1; return 0; }
+  if (orc_inverse_map(sc, e, p, xi) != 0) { if (getenv("ORC_DEBUG")) fprintf(stderr, "inverse map fail\n"); *fail = 1; return 0; }
   for (int k = 0; k < 3; ++k)
     if (xi[k] < lo[k] || xi[k] > hi[k]) return 0;
   return 1;
