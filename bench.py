@@ -22,21 +22,6 @@ import time
 ROOT = os.path.dirname(os.path.abspath(__file__))
 sys.path.insert(0, ROOT)
 
-# Algorithmic FP32 work per candidate pair (FMA = 2 flops): the
-# operations the method needs in this formulation, counted from the source.
-#   affine miss : ray setup 3x(2 FMA) + slab 3x(2 sub, 2 mul, 4 min/max)  ~ 36 flop
-#   affine hit  : + length (7) + N nodes x (3 FMA + trilinear 14 FMA + transfer 3)
-#                 + rule (N + N^2 FMA + N exp + N) ...
-FLOPS_AFFINE_MISS = 36.0
-
-
-def flops_affine_hit(N, P):
-    field = 28 if P == 1 else 96          # trilinear (14 FMA) / triquadratic (~48 FMA)
-    per_node = 6 + field + 4                # node position, field, f~ and kappa
-    rule = 2 * N + 2 * N * N + 4 * N + 12   # sum w kappa, tau_j, e_j sums, b
-    return FLOPS_AFFINE_MISS + 14 + N * per_node + rule
-
-
 FP32_LANES_PER_SM = 128
 NUM_SMS = 148
 
@@ -127,6 +112,10 @@ WORKLOAD = {1: "C1: identity cube, uniform level 3 (512 hex), ortho 64x64, N=4",
             3: "C3: cubed-sphere shell R=2, uniform level 6 (1,572,864 hex), 1024x1024, N=6",
             4: "C4: cubed-sphere shell R=2, uniform level 8 (100,663,296 hex), 2048x2048, N=6",
             5: "C5: cubed-sphere shell R=2, adaptive levels 6..10, 4096x4096, N=8, 3 coarsening cycles"}
+
+
+def forest_affine(scene):
+    return scene.name.startswith(("C1", "C2"))
 
 
 def l2_flush(buf):
@@ -272,13 +261,10 @@ def main():
 
     # --- roofline of the dominant kernel (segment kernel) -----------------
     pk = peaks()
-    if scene.geom_degree == 1:
-        fl = hits_local * flops_affine_hit(N, scene.field_degree) + (cand_local - hits_local) * FLOPS_AFFINE_MISS
-    else:
-        from bench_model import flops_curved
-        fl = flops_curved(hits_local, cand_local, N, scene.field_degree)
+    import bench_model
+    fl = bench_model.flops(scene.geom_degree if not forest_affine(scene) else 1, N, hits_local, cand_local)
     achieved = fl / (cast_avg / 1000.0) / 1e12
-    roof = {"kernel": "k_cast_affine" if scene.geom_degree == 1 else "k_cast_curved", "bound": "alu",
+    roof = {"kernel": "k_cast_affine" if forest_affine(scene) else "k_cast_curved", "bound": "alu",
             "achieved": achieved, "peak": pk["fp32_tflops"], "unit": "TFLOP/s", "frac": achieved / pk["fp32_tflops"],
             "traffic": None, "kernel_ms": cast_avg, "share_of_step": cast_avg / ms_step,
             "algorithmic_flops_per_launch": fl, "peak_source": pk["source"]}

@@ -139,7 +139,8 @@ typedef struct {
   int64_t count;               /* number of records in segs                            */
   int64_t candidates;          /* candidate (leaf, pixel) pairs evaluated              */
   int64_t hit_pairs;           /* pairs with >= 1 segment (the metric's unit)          */
-  int64_t newton_failures;     /* R=2 Newton non-convergence count (must be 0)          */
+  int64_t newton_failures;     /* R=2 Newton non-convergence count, all solves (must be 0) */
+  int64_t face_failures;       /* ... of which face-root solves (diagnostic)               */
   int64_t num_visible;
   const rc_seg* segs;          /* device view, library-owned                           */
   const int32_t* hits_per_pixel; /* device [w*h]: pairs with >= 1 segment per pixel     */

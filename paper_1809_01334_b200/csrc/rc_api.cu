@@ -472,7 +472,7 @@ extern "C" rc_status rc_cast_segments(rc_forest* f, void* stream) {
   CU(grow(&f->d_hits_pp, &f->pix_cap, npix));
   CU(cudaMemsetAsync(f->d_hits_pp, 0, sizeof(int32_t) * npix, s));
   CU(cudaMemsetAsync(f->d_counters + CNT_SEGS, 0, sizeof(int64_t) * 3, s));
-  CU(cudaMemsetAsync(f->d_counters + CNT_OVERFLOW, 0, sizeof(int64_t) * 2, s));
+  CU(cudaMemsetAsync(f->d_counters + CNT_OVERFLOW, 0, sizeof(int64_t) * 3, s));
   if (f->h_num_visible > 0) {
     CU(launch_expand(f->d_chunk_off, f->d_scan + n, f->h_num_visible, f->d_chunk_elem, s));
   }
@@ -515,6 +515,7 @@ extern "C" rc_status rc_segments_get(rc_forest* f, rc_segments* out, void* strea
   out->candidates = c[CNT_CANDIDATES];
   out->hit_pairs = c[CNT_HITPAIRS];
   out->newton_failures = c[CNT_NEWTON_FAIL];
+  out->face_failures = c[CNT_FACE_FAIL];
   out->num_visible = f->h_num_visible;
   out->segs = f->d_segs;
   out->hits_per_pixel = f->d_hits_pp;

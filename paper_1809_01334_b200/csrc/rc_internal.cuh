@@ -110,6 +110,7 @@ enum {
   CNT_CANDIDATES = 3,
   CNT_OVERFLOW = 4,
   CNT_WORK = 5,        // dynamic work counter of the segment kernel
+  CNT_FACE_FAIL = 6,   // face-root Newton non-convergence (diagnostic)
   CNT_SEND = 8,        // [8..8+64) per-rank cursors for pack
   CNT_TOTAL = 80
 };

@@ -46,7 +46,8 @@ class CameraDesc(C.Structure):
 
 class Segments(C.Structure):
     _fields_ = [("count", C.c_int64), ("candidates", C.c_int64), ("hit_pairs", C.c_int64),
-                ("newton_failures", C.c_int64), ("num_visible", C.c_int64), ("segs", C.c_void_p),
+                ("newton_failures", C.c_int64), ("face_failures", C.c_int64), ("num_visible", C.c_int64),
+                ("segs", C.c_void_p),
                 ("hits_per_pixel", C.c_void_p)]
 
 
@@ -228,7 +229,8 @@ class Forest:
         raw = device_view(s.segs, (s.count, 8), "<i4")
         hpp = device_view(s.hits_per_pixel, (self.H, self.W), "<i4")
         return {"count": s.count, "candidates": s.candidates, "hit_pairs": s.hit_pairs,
-                "newton_failures": s.newton_failures, "num_visible": s.num_visible, "raw": raw,
+                "newton_failures": s.newton_failures, "face_failures": s.face_failures,
+                "num_visible": s.num_visible, "raw": raw,
                 "hits_per_pixel": hpp}
 
     def aggregate(self, cycles, stream=None):

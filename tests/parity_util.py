@@ -18,7 +18,7 @@ def gpu_run(scene, background=(0.0, 0.0, 0.0), device_copy=False):
     img = f.composite(background).cpu().numpy().copy()
     torch.cuda.synchronize()
     out = dict(visible=vis, raw=raw, hits_per_pixel=hpp, rgba=img.reshape(-1, 4), count=segs["count"],
-               candidates=segs["candidates"], hit_pairs=segs["hit_pairs"], newton_failures=segs["newton_failures"],
+               candidates=segs["candidates"], hit_pairs=segs["hit_pairs"], newton_failures=segs["newton_failures"], face_failures=segs["face_failures"],
                forest=f)
     return out
 

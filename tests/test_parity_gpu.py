@@ -131,3 +131,53 @@ def test_errors_are_loud():
     f = rc.Forest.from_scene(sc)
     with pytest.raises(rc.RcError):
         f.cull()      # before camera_set -> RC_ERR_STATE
+
+
+# ---------------------------------------------------------------------------
+# Curved R=2 geometry (cubed-sphere shell, configs C3-C5)
+# ---------------------------------------------------------------------------
+@pytest.mark.parametrize("level,width,nb", [(1, 48, 8), (2, 64, 16), (3, 96, 16)])
+def test_shell_full_frame(level, width, nb):
+    sc = sg.shell_uniform(level, width, nb, gl_points=6)
+    o, pixels, ores = _full(sc)
+    g = gpu_run(sc)
+    rep = compare(sc, g, ores, pixels, cull=o.cull())
+    print(rep, "newton_failures", g["newton_failures"])
+    _check(rep)
+    assert g["newton_failures"] == 0
+
+
+def test_shell_gl8_field_p2():
+    """N = 8 GL points (C5's rule) on a level-2 shell."""
+    sc = sg.shell_uniform(2, 56, 32, gl_points=8)
+    o, pixels, ores = _full(sc)
+    g = gpu_run(sc)
+    _check(compare(sc, g, ores, pixels, cull=o.cull()))
+
+
+def test_c3_full_size_sampled():
+    """BASELINE C3 at full size (1,572,864 curved hexes, 1024^2, N=6) in the
+    bench's launch configuration; a stratified pixel sample is compared one
+    by one with the oracle (all leaves culled by the oracle)."""
+    sc = sg.config3(device="cuda")
+    o = oracle.OracleScene(sc)
+    W = sc.camera.width
+    jj, ii = np.meshgrid(np.arange(5, W, 41), np.arange(11, W, 41), indexing="ij")
+    pixels = (jj * W + ii).ravel().astype(np.int32)
+    ores = o.render(pixels, mode="exact", cap=512)
+    g = gpu_run(sc, device_copy=True)
+    rep = compare(sc, g, ores, pixels, cull=o.cull())
+    print(rep, "hit_pairs", g["hit_pairs"], "newton_failures", g["newton_failures"])
+    _check(rep)
+    assert g["newton_failures"] == 0
+
+
+def test_affine_r2_matches_r1_P9():
+    """R=2 tree with affine (identity) control points goes through the same
+    slab path and reproduces the R=1 result."""
+    import dataclasses
+    sc1 = sg.config2(width=64, maxlevel=5)
+    sc2 = dataclasses.replace(sc1, geom_degree=2, tree_ctrl=sg.identity_cube_ctrl(2))
+    g1, g2 = gpu_run(sc1), gpu_run(sc2)
+    assert g1["count"] == g2["count"]
+    assert np.abs(g1["rgba"] - g2["rgba"]).max() < 1e-6
