@@ -202,6 +202,11 @@ rc_status rc_render_frame(rc_forest* f, const rc_camera* cam, int32_t cycles, co
  * rc_cast_segments measured with CUDA events on the caller's stream. */
 int64_t rc_launch_count(int32_t reset);
 float rc_last_cast_ms(rc_forest* f);
+/* [sync] device time of one phase of the last rc_cast_segments (CUDA events on
+ * the caller's stream, summed over chunk batches): 0 = whole cast,
+ * 1 = intersection kernel(s), 2 = integration kernel(s) (curved path; the
+ * affine path fuses both into phase 1). */
+float rc_last_phase_ms(rc_forest* f, int32_t phase);
 
 #ifdef __cplusplus
 }

@@ -72,6 +72,24 @@ __device__ __forceinline__ void eval_X(const float* __restrict__ sB, const float
   }
 }
 
+// X_E on face (axis k fixed): 9 Bernstein points m = base + ia*sa + jb*sb.
+__device__ __forceinline__ void eval_face(const float* __restrict__ sB, int base, int sa, int sb, float s1, float s2,
+                                          float X[3]) {
+  float a0, a1, a2, b0, b1, b2;
+  bern(s1, a0, a1, a2);
+  bern(s2, b0, b1, b2);
+  const float bb[3] = {b0, b1, b2};
+  X[0] = X[1] = X[2] = 0.0f;
+#pragma unroll
+  for (int jb = 0; jb < 3; ++jb) {
+    const float* p0 = sB + 3 * (base + jb * sb);
+    const float* p1 = p0 + 3 * sa;
+    const float* p2 = p1 + 3 * sa;
+#pragma unroll
+    for (int c = 0; c < 3; ++c) X[c] = fmaf(bb[jb], fmaf(a2, p2[c], fmaf(a1, p1[c], a0 * p0[c])), X[c]);
+  }
+}
+
 // X and J = dX/dxi (J[c][d]).
 __device__ __forceinline__ void eval_XJ(const float* __restrict__ sB, const float xi[3], float X[3], float J[3][3]) {
   float a[3], b[3], c[3], da[3], db[3], dc[3];
@@ -270,18 +288,37 @@ __device__ __forceinline__ int chord_root(const Patch& pt, float A11, float A12,
 // Roots of one face patch in face coordinates [0,1]^2.  Common case: hull
 // test + injectivity + Newton.  Rare case: subdivision with a small stack.
 // Returns the number of roots written to (u1[], u2[]).
-__device__ __noinline__ int face_roots_subdiv(const Patch& root, float tol, int max_it, float* u1, float* u2,
-                                              int cap, int* fails) {
+__device__ __forceinline__ void load_patch(const float* __restrict__ sp, int f, Patch& pt) {
+  const int k = f >> 1, side = f & 1;
+  const int ka = (k + 1) % 3, kb = (k + 2) % 3;
+  const int str[3] = {1, 3, 9};
+  const int base = 2 * side * str[k], sa = str[ka], sbb = str[kb];
+#pragma unroll
+  for (int jb = 0; jb < 3; ++jb)
+#pragma unroll
+    for (int ia = 0; ia < 3; ++ia) {
+      const int m = base + ia * sa + jb * sbb;
+      pt.gx[3 * jb + ia] = sp[(2 * m) * 32];
+      pt.gy[3 * jb + ia] = sp[(2 * m + 1) * 32];
+    }
+}
+
+// sp: this lane's projected control points ([m*2+c] with stride 32), f: face.
+// Roots are written to u[2*t], u[2*t+1] (shared-memory scratch of the lane).
+__device__ __noinline__ int face_roots_subdiv(const float* __restrict__ sp, int f, float tol, int max_it,
+                                              float* u, int stride, int cap, int* fails) {
+  Patch root;
+  load_patch(sp, f, root);
   struct Item {
     Patch p;
     float s1a, s2a, w;
   };
   Item stack[32];
-  int sp = 0, nr = 0;
-  stack[sp++] = Item{root, 0.0f, 0.0f, 1.0f};
+  int top = 0, nr = 0;
+  stack[top++] = Item{root, 0.0f, 0.0f, 1.0f};
   int visited = 0;
-  while (sp > 0) {
-    Item it = stack[--sp];
+  while (top > 0) {
+    Item it = stack[--top];
     if (hull_excludes_origin(it.p)) continue;
     ++visited;
     float A11, A12, A21, A22, gcx, gcy;
@@ -292,25 +329,25 @@ __device__ __noinline__ int face_roots_subdiv(const Patch& root, float tol, int 
       if (st == 1) {
         float lt = FACE_TOL / it.w;
         if (s1 >= -lt && s1 <= 1.0f + lt && s2 >= -lt && s2 <= 1.0f + lt && nr < cap) {
-          u1[nr] = it.s1a + it.w * s1;
-          u2[nr] = it.s2a + it.w * s2;
+          u[(2 * nr) * stride] = it.s1a + it.w * s1;
+          u[(2 * nr + 1) * stride] = it.s2a + it.w * s2;
           ++nr;
         }
         continue;
       } else if (st == -1) {
         continue;
-      } else if (it.w < 1.0f / 1024.0f || sp > 28 || visited > 1024) {
+      } else if (it.w < 1.0f / 1024.0f || top > 28 || visited > 1024) {
         ++*fails;
         continue;
       }
       // not converged: split further (sub-patches have smaller q)
-    } else if (it.w < 1.0f / 1024.0f || sp > 28 || visited > 1024) {
+    } else if (it.w < 1.0f / 1024.0f || top > 28 || visited > 1024) {
       // depth limit without an injectivity proof (tangency): Newton from the centre
       float s1 = 0.5f, s2 = 0.5f;
       if (patch_newton(it.p, s1, s2, tol / it.w, max_it) && s1 >= -1e-3f && s1 <= 1.001f && s2 >= -1e-3f &&
           s2 <= 1.001f && nr < cap) {
-        u1[nr] = it.s1a + it.w * s1;
-        u2[nr] = it.s2a + it.w * s2;
+        u[(2 * nr) * stride] = it.s1a + it.w * s1;
+        u[(2 * nr + 1) * stride] = it.s2a + it.w * s2;
         ++nr;
       }
       continue;
@@ -320,349 +357,735 @@ __device__ __noinline__ int face_roots_subdiv(const Patch& root, float tol, int 
     patch_split(a, 1, aa, ab);
     patch_split(b, 1, ba, bb);
     float h = 0.5f * it.w;
-    stack[sp++] = Item{aa, it.s1a, it.s2a, h};
-    stack[sp++] = Item{ab, it.s1a, it.s2a + h, h};
-    stack[sp++] = Item{ba, it.s1a + h, it.s2a, h};
-    stack[sp++] = Item{bb, it.s1a + h, it.s2a + h, h};
+    stack[top++] = Item{aa, it.s1a, it.s2a, h};
+    stack[top++] = Item{ab, it.s1a, it.s2a + h, h};
+    stack[top++] = Item{ba, it.s1a + h, it.s2a, h};
+    stack[top++] = Item{bb, it.s1a + h, it.s2a + h, h};
   }
   return nr;
 }
 
-}  // namespace
 
-template <int P, int N>
-__global__ void __launch_bounds__(WARPS * 32, 4) k_cast_curved(CamConst cc, const TreeConst* __restrict__ trees,
-                                                               DevLeafView L, const int32_t* __restrict__ vis,
-                                                               const Rect16* __restrict__ vrect,
-                                                               const int64_t* __restrict__ chunk_off,
-                                                               const int32_t* __restrict__ chunk_elem, int64_t nchunks,
-                                                               uint32_t key_base, rc_seg* __restrict__ segs,
-                                                               int64_t seg_cap, int32_t* __restrict__ hits_pp,
-                                                               int64_t* __restrict__ counters) {
-  constexpr int NF = (P + 1) * (P + 1) * (P + 1);
-  __shared__ double sD[WARPS][2][81];
-  __shared__ __align__(16) float sBall[WARPS][84];
-  __shared__ float sFall[WARPS][28];
-  __shared__ double sOrg[WARPS][3];
-  __shared__ float sProj[WARPS][54 * 32];   // projected control points, [m*2+c][lane]
+// X_E(xi) - C_E with the Bernstein points in registers (G[m*3+c]).
+__device__ __forceinline__ void eval_Xr(const float (&G)[81], const float xi[3], float X[3]) {
+  float a0, a1, a2, b0, b1, b2, c0, c1, c2;
+  bern(xi[0], a0, a1, a2);
+  bern(xi[1], b0, b1, b2);
+  bern(xi[2], c0, c1, c2);
+  const float bb[3] = {b0, b1, b2}, cc[3] = {c0, c1, c2};
+  X[0] = X[1] = X[2] = 0.0f;
+#pragma unroll
+  for (int m3 = 0; m3 < 3; ++m3) {
+    float y[3] = {0.f, 0.f, 0.f};
+#pragma unroll
+    for (int m2 = 0; m2 < 3; ++m2) {
+      const int o = ((m3 * 3 + m2) * 3) * 3;
+#pragma unroll
+      for (int c = 0; c < 3; ++c) y[c] = fmaf(bb[m2], fmaf(a2, G[o + 6 + c], fmaf(a1, G[o + 3 + c], a0 * G[o + c])), y[c]);
+    }
+#pragma unroll
+    for (int c = 0; c < 3; ++c) X[c] = fmaf(cc[m3], y[c], X[c]);
+  }
+}
+
+__device__ __forceinline__ void eval_XJr(const float (&G)[81], const float xi[3], float X[3], float J[3][3]) {
+  float a[3], b[3], c[3], da[3], db[3], dc[3];
+  bern(xi[0], a[0], a[1], a[2]);
+  bern(xi[1], b[0], b[1], b[2]);
+  bern(xi[2], c[0], c[1], c[2]);
+  dbern(xi[0], da[0], da[1], da[2]);
+  dbern(xi[1], db[0], db[1], db[2]);
+  dbern(xi[2], dc[0], dc[1], dc[2]);
+#pragma unroll
+  for (int q = 0; q < 3; ++q) X[q] = J[q][0] = J[q][1] = J[q][2] = 0.0f;
+#pragma unroll
+  for (int m3 = 0; m3 < 3; ++m3) {
+    float y[3] = {0, 0, 0}, y1[3] = {0, 0, 0}, y2[3] = {0, 0, 0};
+#pragma unroll
+    for (int m2 = 0; m2 < 3; ++m2) {
+      const int o = ((m3 * 3 + m2) * 3) * 3;
+#pragma unroll
+      for (int q = 0; q < 3; ++q) {
+        float v = fmaf(a[2], G[o + 6 + q], fmaf(a[1], G[o + 3 + q], a[0] * G[o + q]));
+        float dv = fmaf(da[2], G[o + 6 + q], fmaf(da[1], G[o + 3 + q], da[0] * G[o + q]));
+        y[q] = fmaf(b[m2], v, y[q]);
+        y1[q] = fmaf(b[m2], dv, y1[q]);
+        y2[q] = fmaf(db[m2], v, y2[q]);
+      }
+    }
+#pragma unroll
+    for (int q = 0; q < 3; ++q) {
+      X[q] = fmaf(c[m3], y[q], X[q]);
+      J[q][0] = fmaf(c[m3], y1[q], J[q][0]);
+      J[q][1] = fmaf(c[m3], y2[q], J[q][1]);
+      J[q][2] = fmaf(dc[m3], y[q], J[q][2]);
+    }
+  }
+}
+
+// ---------------------------------------------------------------------------
+// Element preparation (warp-cooperative, 27 lanes): Bernstein control points
+// of X_E by restriction of the tree's (fp64, three sum-factorised blossom
+// passes), stored fp32 relative to the local origin org = B_(1,1,1) in
+// sl[0..80]; optional nodal field in sl[84..110]; the affine model and its
+// nonlinearity bounds in sl[SLOT_AFF..+15].
+// ---------------------------------------------------------------------------
+constexpr int SLOT_STRIDE = 132;   // 84 geometry + 28 field + 16 affine model (+4); 132 mod 32 = 4 spreads slot banks
+constexpr int SLOT_AFF = 112;      // Xc[3], J0inv[9], dp[3], eta
+
+__device__ __forceinline__ void prep_element(float* __restrict__ sl, double* __restrict__ org,
+                                             double (*__restrict__ prep)[81], const TreeConst* __restrict__ trees,
+                                             const DevLeafView& L, int e, unsigned lane, int NF, bool with_field) {
+  const double h = ldexp(1.0, -(int)L.level[e]);
+  if (lane < 27) {
+    const TreeConst& T = trees[L.tree[e]];
+    const int m1 = lane % 3, m2 = (lane / 3) % 3, m3 = lane / 9;
+    const int mm[3] = {m1, m2, m3};
+    double M[3][3];
+#pragma unroll
+    for (int k = 0; k < 3; ++k) {
+      const double u = ldexp((double)L.anchor[3 * (int64_t)e + k], -RC_MAXLEVEL);
+      const double w = u + h;
+      const double x = mm[k] == 2 ? w : u, y = mm[k] == 0 ? u : w;
+      M[k][0] = (1 - x) * (1 - y);
+      M[k][1] = (1 - x) * y + x * (1 - y);
+      M[k][2] = x * y;
+    }
+    double o[3];
+#pragma unroll
+    for (int q3 = 0; q3 < 3; ++q3) {
+      double acc = 0.0;
+#pragma unroll
+      for (int q = 0; q < 3; ++q) acc = fma(M[0][q], T.Bw[((m3 * 3 + m2) * 3 + q) * 3 + q3], acc);
+      prep[0][lane * 3 + q3] = acc;
+    }
+    __syncwarp(0x07ffffffu);
+#pragma unroll
+    for (int q3 = 0; q3 < 3; ++q3) {
+      double acc = 0.0;
+#pragma unroll
+      for (int q = 0; q < 3; ++q) acc = fma(M[1][q], prep[0][((m3 * 3 + q) * 3 + m1) * 3 + q3], acc);
+      o[q3] = acc;
+    }
+    __syncwarp(0x07ffffffu);
+#pragma unroll
+    for (int q3 = 0; q3 < 3; ++q3) prep[1][lane * 3 + q3] = o[q3];
+    __syncwarp(0x07ffffffu);
+#pragma unroll
+    for (int q3 = 0; q3 < 3; ++q3) {
+      double acc = 0.0;
+#pragma unroll
+      for (int q = 0; q < 3; ++q) acc = fma(M[2][q], prep[1][((q * 3 + m2) * 3 + m1) * 3 + q3], acc);
+      o[q3] = acc;
+    }
+    if (lane == 13) {
+      org[0] = o[0];
+      org[1] = o[1];
+      org[2] = o[2];
+    }
+    __syncwarp(0x07ffffffu);
+#pragma unroll
+    for (int q3 = 0; q3 < 3; ++q3) sl[lane * 3 + q3] = (float)(o[q3] - org[q3]);
+    if (with_field && (int)lane < NF) sl[84 + lane] = __ldg(&L.field[(int64_t)e * NF + lane]);
+  }
+  __syncwarp();
+        {
+          // affine model A(xi) = Xc + J0 (xi - 1/2) at the centre and the bound
+          // dp_k = max_m |(J0^-1 (B_m - A(m/2)))_k| of the nonlinear remainder
+          // (Bernstein coefficients of X - A; convex hull property).
+          const int m1 = lane % 3, m2 = (lane / 3) % 3, m3 = lane / 9;
+          const float wq[3] = {0.25f, 0.5f, 0.25f}, dq[3] = {-1.0f, 0.0f, 1.0f};
+          float B0 = 0.f, B1 = 0.f, B2 = 0.f;
+          if (lane < 27) { B0 = sl[3 * lane]; B1 = sl[3 * lane + 1]; B2 = sl[3 * lane + 2]; }
+          const float w3 = lane < 27 ? wq[m1] * wq[m2] * wq[m3] : 0.0f;
+          const float g1 = lane < 27 ? dq[m1] * wq[m2] * wq[m3] : 0.0f;
+          const float g2 = lane < 27 ? wq[m1] * dq[m2] * wq[m3] : 0.0f;
+          const float g3 = lane < 27 ? wq[m1] * wq[m2] * dq[m3] : 0.0f;
+          float acc[12] = {w3 * B0, w3 * B1, w3 * B2, g1 * B0, g1 * B1, g1 * B2,
+                           g2 * B0, g2 * B1, g2 * B2, g3 * B0, g3 * B1, g3 * B2};
+#pragma unroll
+          for (int off = 16; off > 0; off >>= 1)
+#pragma unroll
+            for (int t = 0; t < 12; ++t) acc[t] += __shfl_xor_sync(0xffffffffu, acc[t], off);
+          float J[3][3] = {{acc[3], acc[6], acc[9]}, {acc[4], acc[7], acc[10]}, {acc[5], acc[8], acc[11]}};
+          float Ji[3][3];
+          if (!inv3(J, Ji)) {
+#pragma unroll
+            for (int a = 0; a < 3; ++a)
+#pragma unroll
+              for (int b = 0; b < 3; ++b) Ji[a][b] = 0.0f;
+          }
+          float dp0 = 0.f, dp1 = 0.f, dp2 = 0.f;
+          if (lane < 27) {
+            const float x0 = 0.5f * m1 - 0.5f, x1 = 0.5f * m2 - 0.5f, x2 = 0.5f * m3 - 0.5f;
+            const float r0 = B0 - (acc[0] + J[0][0] * x0 + J[0][1] * x1 + J[0][2] * x2);
+            const float r1 = B1 - (acc[1] + J[1][0] * x0 + J[1][1] * x1 + J[1][2] * x2);
+            const float r2 = B2 - (acc[2] + J[2][0] * x0 + J[2][1] * x1 + J[2][2] * x2);
+            dp0 = fabsf(Ji[0][0] * r0 + Ji[0][1] * r1 + Ji[0][2] * r2);
+            dp1 = fabsf(Ji[1][0] * r0 + Ji[1][1] * r1 + Ji[1][2] * r2);
+            dp2 = fabsf(Ji[2][0] * r0 + Ji[2][1] * r1 + Ji[2][2] * r2);
+          }
+          // eta = max over the Bernstein coefficients of dE/dxi_a (E = J0^-1 (X - Xc) - (xi - 1/2)):
+          // 2 J0^-1 (B_{m+e_a} - B_m) - e_a, vector inf-norm (bounds |dE/dxi_a| on the element)
+          float eta = 0.0f;
+          if (lane < 27) {
+            const int mmv[3] = {m1, m2, m3}, str[3] = {1, 3, 9};
+#pragma unroll
+            for (int ax = 0; ax < 3; ++ax) {
+              if (mmv[ax] < 2) {
+                const int n2 = lane + str[ax];
+                const float e0 = 2.0f * (sl[3 * n2] - B0), e1 = 2.0f * (sl[3 * n2 + 1] - B1), e2 = 2.0f * (sl[3 * n2 + 2] - B2);
+                const float t0 = Ji[0][0] * e0 + Ji[0][1] * e1 + Ji[0][2] * e2 - (ax == 0 ? 1.0f : 0.0f);
+                const float t1 = Ji[1][0] * e0 + Ji[1][1] * e1 + Ji[1][2] * e2 - (ax == 1 ? 1.0f : 0.0f);
+                const float t2 = Ji[2][0] * e0 + Ji[2][1] * e1 + Ji[2][2] * e2 - (ax == 2 ? 1.0f : 0.0f);
+                eta = fmaxf(eta, fmaxf(fabsf(t0), fmaxf(fabsf(t1), fabsf(t2))));
+              }
+            }
+          }
+#pragma unroll
+          for (int off = 16; off > 0; off >>= 1) {
+            dp0 = fmaxf(dp0, __shfl_xor_sync(0xffffffffu, dp0, off));
+            dp1 = fmaxf(dp1, __shfl_xor_sync(0xffffffffu, dp1, off));
+            dp2 = fmaxf(dp2, __shfl_xor_sync(0xffffffffu, dp2, off));
+            eta = fmaxf(eta, __shfl_xor_sync(0xffffffffu, eta, off));
+          }
+          if (lane == 0) {
+            float* af = sl + SLOT_AFF;
+            af[0] = acc[0]; af[1] = acc[1]; af[2] = acc[2];
+#pragma unroll
+            for (int a = 0; a < 3; ++a)
+#pragma unroll
+              for (int b = 0; b < 3; ++b) af[3 + 3 * a + b] = Ji[a][b];
+            // inflate by a rounding margin relative to the element (fp32)
+            af[12] = dp0 * 1.001f + 1e-5f;
+            af[13] = dp1 * 1.001f + 1e-5f;
+            af[14] = dp2 * 1.001f + 1e-5f;
+            af[15] = eta * 1.001f + 1e-5f;
+          }
+        }
+  __syncwarp();
+}
+
+// ---------------------------------------------------------------------------
+// Kernel 1: intersection.  One warp = one 32-pixel chunk of one element;
+// writes one 64-byte item per (pair, segment):
+//   float xin[3], xout[3]  entry / exit point relative to the element origin
+//   float xiin[3], xiout[3] reference coordinates of entry / exit
+//   float alpha_near, alpha_far; uint32 pixel; int32 visible index
+// ---------------------------------------------------------------------------
+constexpr int IWARPS = 4;
+struct IsectSmem {
+  float slot[SLOT_STRIDE];
+  double prep[2][81];
+  double org[3];
+  float proj[54][32];
+  float roots[4][4][32];
+  float sub[8][32];
+};
+
+__global__ void __launch_bounds__(IWARPS * 32, 4) k_isect_curved(CamConst cc, const TreeConst* __restrict__ trees,
+                                                                 DevLeafView L, const int32_t* __restrict__ vis,
+                                                                 const Rect16* __restrict__ vrect,
+                                                                 const int64_t* __restrict__ chunk_off,
+                                                                 const int32_t* __restrict__ chunk_elem,
+                                                                 int64_t c_begin, int64_t c_end,
+                                                                 float4* __restrict__ items, int64_t item_cap,
+                                                                 int32_t* __restrict__ hits_pp,
+                                                                 int64_t* __restrict__ counters) {
+  extern __shared__ __align__(16) unsigned char smem_raw[];
   const int warp = threadIdx.x >> 5;
   const unsigned lane = threadIdx.x & 31;
-  float* sB = sBall[warp];
-  float* sF = sFall[warp];
-  int local_hits = 0, local_fail = 0, face_fail = 0;
+  IsectSmem& W = reinterpret_cast<IsectSmem*>(smem_raw)[warp];
   const float tol = cc.newton_tol;
   const int max_it = cc.newton_max;
-
+  int local_hits = 0, face_fail = 0;
+  int cur_v = -1, e = 0;
+  const float* sB = W.slot;
   for (;;) {
     int64_t c = 0;
-    if (lane == 0) c = (int64_t)atomicAdd((unsigned long long*)&counters[CNT_WORK], 1ull);
+    if (lane == 0) c = c_begin + (int64_t)atomicAdd((unsigned long long*)&counters[CNT_WORK], 1ull);
     c = __shfl_sync(0xffffffffu, c, 0);
-    if (c >= nchunks) break;
+    if (c >= c_end) break;
     const int v = chunk_elem[c];
-    const int e = vis[v];
+    if (v != cur_v) {
+      e = vis[v];
+      __syncwarp();
+      prep_element(W.slot, W.org, W.prep, trees, L, e, lane, 0, false);
+      cur_v = v;
+    }
     const Rect16 r = vrect[v];
     const int rw = r.i1 - r.i0 + 1, rh = r.j1 - r.j0 + 1;
     const int p = (int)(c - chunk_off[v]) * RC_CHUNK + (int)lane;
     const bool active = p < rw * rh;
     const int i = r.i0 + p % rw, j = r.j0 + p / rw;
-    const int lvl = L.level[e];
-    const double h = ldexp(1.0, -lvl);
-
-    // ---- 1. element prep: Bernstein restriction, 27 lanes, fp64 ----------
-    __syncwarp();
-    if (lane < 27) {
-      const TreeConst& T = trees[L.tree[e]];
-      const int m1 = lane % 3, m2 = (lane / 3) % 3, m3 = lane / 9;
-      const int mm[3] = {m1, m2, m3};
-      double M[3][3];   // blossom weights of output index mm[k] along axis k
+      // ---- ray of pixel (i,j), re-based near the element (fp64) ----------
+      const double di = (double)i - 0.5 * (cc.W - 1), dj = (double)j - 0.5 * (cc.H - 1);
+      double Rw[3], D[3];
 #pragma unroll
       for (int k = 0; k < 3; ++k) {
-        double u = ldexp((double)L.anchor[3 * (int64_t)e + k], -RC_MAXLEVEL);
-        double w = u + h;
-        double x = mm[k] == 2 ? w : u, y = mm[k] == 0 ? u : w;
-        M[k][0] = (1 - x) * (1 - y);
-        M[k][1] = (1 - x) * y + x * (1 - y);
-        M[k][2] = x * y;
+        Rw[k] = fma(dj, cc.Ru[k], fma(di, cc.Rt[k], cc.R0[k]));
+        const double O = fma(dj, cc.Ou[k], fma(di, cc.Ot[k], cc.O0[k]));
+        D[k] = W.org[k] - O;
       }
-      double o[3];
-      // axis 1: in[m3][m2][q]
+      const float rf[3] = {(float)Rw[0], (float)Rw[1], (float)Rw[2]};
+      const float rr = rf[0] * rf[0] + rf[1] * rf[1] + rf[2] * rf[2];
+      const float alpha0 = ((float)D[0] * rf[0] + (float)D[1] * rf[1] + (float)D[2] * rf[2]) / rr;
+      float P0[3];
 #pragma unroll
-      for (int q3 = 0; q3 < 3; ++q3) {
-        double acc = 0.0;
-#pragma unroll
-        for (int q = 0; q < 3; ++q) acc = fma(M[0][q], T.Bw[((m3 * 3 + m2) * 3 + q) * 3 + q3], acc);
-        o[q3] = acc;
-      }
-#pragma unroll
-      for (int q3 = 0; q3 < 3; ++q3) sD[warp][0][lane * 3 + q3] = o[q3];
-      __syncwarp(0x07ffffffu);
-#pragma unroll
-      for (int q3 = 0; q3 < 3; ++q3) {
-        double acc = 0.0;
-#pragma unroll
-        for (int q = 0; q < 3; ++q) acc = fma(M[1][q], sD[warp][0][((m3 * 3 + q) * 3 + m1) * 3 + q3], acc);
-        o[q3] = acc;
-      }
-#pragma unroll
-      for (int q3 = 0; q3 < 3; ++q3) sD[warp][1][lane * 3 + q3] = o[q3];
-      __syncwarp(0x07ffffffu);
-#pragma unroll
-      for (int q3 = 0; q3 < 3; ++q3) {
-        double acc = 0.0;
-#pragma unroll
-        for (int q = 0; q < 3; ++q) acc = fma(M[2][q], sD[warp][1][((q * 3 + m2) * 3 + m1) * 3 + q3], acc);
-        o[q3] = acc;
-      }
-      if (lane == 13) {
-        sOrg[warp][0] = o[0];
-        sOrg[warp][1] = o[1];
-        sOrg[warp][2] = o[2];
-      }
-      __syncwarp(0x07ffffffu);
-#pragma unroll
-      for (int q3 = 0; q3 < 3; ++q3) sB[lane * 3 + q3] = (float)(o[q3] - sOrg[warp][q3]);
-      if (lane < NF) sF[lane] = __ldg(&L.field[(int64_t)e * NF + lane]);
-    }
-    __syncwarp();
-    const double org0 = sOrg[warp][0], org1 = sOrg[warp][1], org2 = sOrg[warp][2];
+      for (int k = 0; k < 3; ++k) P0[k] = (float)fma((double)alpha0, Rw[k], -D[k]);
+      const float rn = sqrtf(rr);
 
-    // ---- 2. ray of pixel (i,j), re-based near the element (fp64) ---------
-    const double di = (double)i - 0.5 * (cc.W - 1), dj = (double)j - 0.5 * (cc.H - 1);
-    double Rw[3], D[3];
-    const double orgv[3] = {org0, org1, org2};
+      // roots (beta, xi) go to per-lane shared scratch, sorted by beta afterwards
+      int nroots = 0;
+      float rb0 = 3.4e38f, rb1 = 3.4e38f, rb2 = 3.4e38f, rb3 = 3.4e38f;
+      int ri0 = 0, ri1 = 1, ri2 = 2, ri3 = 3;
+      if (active) {
+        float ax[3] = {0.f, 0.f, 0.f};
+        {
+          const float a0 = fabsf(rf[0]), a1 = fabsf(rf[1]), a2 = fabsf(rf[2]);
+          ax[(a0 <= a1 && a0 <= a2) ? 0 : (a1 <= a2 ? 1 : 2)] = 1.0f;
+        }
+        float d1[3] = {rf[1] * ax[2] - rf[2] * ax[1], rf[2] * ax[0] - rf[0] * ax[2], rf[0] * ax[1] - rf[1] * ax[0]};
+        const float n1 = rsqrtf(d1[0] * d1[0] + d1[1] * d1[1] + d1[2] * d1[2]);
+        d1[0] *= n1; d1[1] *= n1; d1[2] *= n1;
+        float d2[3] = {rf[1] * d1[2] - rf[2] * d1[1], rf[2] * d1[0] - rf[0] * d1[2], rf[0] * d1[1] - rf[1] * d1[0]};
+        const float n2 = rsqrtf(d2[0] * d2[0] + d2[1] * d2[1] + d2[2] * d2[2]);
+        d2[0] *= n2; d2[1] *= n2; d2[2] *= n2;
+        const float o1 = d1[0] * P0[0] + d1[1] * P0[1] + d1[2] * P0[2];
+        const float o2 = d2[0] * P0[0] + d2[1] * P0[1] + d2[2] * P0[2];
+        // affine prefilter in xi~ = J0^-1 coordinates: line xl(beta) = xl0 + beta dl
+        const float* af = sB + SLOT_AFF;
+        const float q0 = P0[0] - af[0], q1 = P0[1] - af[1], q2 = P0[2] - af[2];
+        const float xl0[3] = {0.5f + af[3] * q0 + af[4] * q1 + af[5] * q2, 0.5f + af[6] * q0 + af[7] * q1 + af[8] * q2,
+                              0.5f + af[9] * q0 + af[10] * q1 + af[11] * q2};
+        const float dl[3] = {af[3] * rf[0] + af[4] * rf[1] + af[5] * rf[2], af[6] * rf[0] + af[7] * rf[1] + af[8] * rf[2],
+                             af[9] * rf[0] + af[10] * rf[1] + af[11] * rf[2]};
+        const float dpv[3] = {af[12], af[13], af[14]};
+        float tin[3], tout[3], inv[3];
 #pragma unroll
-    for (int k = 0; k < 3; ++k) {
-      Rw[k] = fma(dj, cc.Ru[k], fma(di, cc.Rt[k], cc.R0[k]));
-      double O = fma(dj, cc.Ou[k], fma(di, cc.Ot[k], cc.O0[k]));
-      D[k] = orgv[k] - O;
-    }
-    float rf[3] = {(float)Rw[0], (float)Rw[1], (float)Rw[2]};
-    const float rr = rf[0] * rf[0] + rf[1] * rf[1] + rf[2] * rf[2];
-    const float alpha0 = ((float)D[0] * rf[0] + (float)D[1] * rf[1] + (float)D[2] * rf[2]) / rr;
-    float P0[3];
+        for (int k = 0; k < 3; ++k) {
+          inv[k] = 1.0f / dl[k];
+          const float ta = (-dpv[k] - xl0[k]) * inv[k], tb = (1.0f + dpv[k] - xl0[k]) * inv[k];
+          tin[k] = fminf(ta, tb);
+          tout[k] = fmaxf(ta, tb);
+        }
+        const float ben = fmaxf(tin[0], fmaxf(tin[1], tin[2])), bex = fminf(tout[0], fminf(tout[1], tout[2]));
+        unsigned face_mask = 0;
+        if (bex >= ben) {
 #pragma unroll
-    for (int k = 0; k < 3; ++k) P0[k] = (float)fma((double)alpha0, Rw[k], -D[k]);
-    const float rn = sqrtf(rr);
-
-    int nroots = 0;
-    RootRec roots[MAX_ROOTS];
-    if (active) {
-      // projection basis d1, d2 perpendicular to r
-      float ax[3] = {0.f, 0.f, 0.f};
-      {
-        float a0 = fabsf(rf[0]), a1 = fabsf(rf[1]), a2 = fabsf(rf[2]);
-        int im = (a0 <= a1 && a0 <= a2) ? 0 : (a1 <= a2 ? 1 : 2);
-        ax[im] = 1.0f;
-      }
-      float d1[3] = {rf[1] * ax[2] - rf[2] * ax[1], rf[2] * ax[0] - rf[0] * ax[2], rf[0] * ax[1] - rf[1] * ax[0]};
-      float n1 = rsqrtf(d1[0] * d1[0] + d1[1] * d1[1] + d1[2] * d1[2]);
-      d1[0] *= n1; d1[1] *= n1; d1[2] *= n1;
-      float d2[3] = {rf[1] * d1[2] - rf[2] * d1[1], rf[2] * d1[0] - rf[0] * d1[2], rf[0] * d1[1] - rf[1] * d1[0]};
-      float n2 = rsqrtf(d2[0] * d2[0] + d2[1] * d2[1] + d2[2] * d2[2]);
-      d2[0] *= n2; d2[1] *= n2; d2[2] *= n2;
-      const float o1 = d1[0] * P0[0] + d1[1] * P0[1] + d1[2] * P0[2];
-      const float o2 = d2[0] * P0[0] + d2[1] * P0[1] + d2[2] * P0[2];
-      float* sp = sProj[warp] + lane;
-#pragma unroll 9
-      for (int m = 0; m < 27; ++m) {
-        float bx = sB[3 * m], by = sB[3 * m + 1], bz = sB[3 * m + 2];
-        sp[(2 * m) * 32] = fmaf(d1[0], bx, fmaf(d1[1], by, fmaf(d1[2], bz, -o1)));
-        sp[(2 * m + 1) * 32] = fmaf(d2[0], bx, fmaf(d2[1], by, fmaf(d2[2], bz, -o2)));
-      }
-      // ---- 3. face roots ------------------------------------------------
-#pragma unroll 1
-      for (int f = 0; f < 6; ++f) {
-        const int k = f >> 1, side = f & 1;
-        const int a = (k + 1) % 3, b = (k + 2) % 3;
-        Patch pt;
-#pragma unroll
-        for (int jb = 0; jb < 3; ++jb)
-#pragma unroll
-          for (int ia = 0; ia < 3; ++ia) {
-            int mm[3];
-            mm[k] = 2 * side;
-            mm[a] = ia;
-            mm[b] = jb;
-            int m = (mm[2] * 3 + mm[1]) * 3 + mm[0];
-            pt.gx[3 * jb + ia] = sp[(2 * m) * 32];
-            pt.gy[3 * jb + ia] = sp[(2 * m + 1) * 32];
+          for (int f = 0; f < 6; ++f) {
+            const int k = f >> 1;
+            const float side = (float)(f & 1);
+            // face slab |xl_k - side| <= dp_k within the inflated box
+            const float ta = (side - dpv[k] - xl0[k]) * inv[k], tb = (side + dpv[k] - xl0[k]) * inv[k];
+            const float lo = fmaxf(ben, fminf(ta, tb)), hi = fminf(bex, fmaxf(ta, tb));
+            if (hi >= lo) face_mask |= 1u << f;
           }
-        if (hull_excludes_origin(pt)) continue;
-        float u1[4], u2[4];
-        int nf = 0;
-        float A11, A12, A21, A22, gcx, gcy;
-        float q = injectivity_bound(pt, A11, A12, A21, A22, gcx, gcy);
-        if (q < 1.0f) {
-          float s1, s2;
-          int st = chord_root(pt, A11, A12, A21, A22, gcx, gcy, q, tol, max_it, s1, s2);
+        }
+        float* sp = &W.proj[0][lane];
+        float* su = &W.sub[0][lane];
+        const float dpm = fmaxf(dpv[0], fmaxf(dpv[1], dpv[2])), eta2 = 2.0f * af[15];
+#pragma unroll 1
+        for (int f = 0; f < 6; ++f) {
+          if (!(face_mask & (1u << f))) continue;
+          const int fk = f >> 1, fside = f & 1;
+          const int fa = (fk + 1) % 3, fb = (fk + 2) % 3;
+          {
+            // Certified fast path.  In xi~ coordinates the face is
+            // (s_a, s_b, side) + E(s) and the ray xl0 + beta dl, so the root
+            // x = (s_a, s_b, beta) solves x = x0 - M0^-1 E(s) with M0 = [e_a, e_b, -dl]:
+            // |x* - x0|_inf <= ||M0^-1|| max|E| (exclusion) and the map contracts
+            // with q = ||M0^-1|| 2 eta (uniqueness + convergence) when q < 1.
+            const float dk = dl[fk];
+            const float rk = 1.0f / dk;
+            const float ga = dl[fa] * rk, gb = dl[fb] * rk;
+            const float mnorm = fmaxf(fabsf(rk), 1.0f + fabsf(ga) + fabsf(gb));
+            const float qf = mnorm * eta2;
+            if (qf < 0.25f) {
+              const float b0 = ((float)fside - xl0[fk]) * rk;
+              const float sa0 = xl0[fa] + b0 * dl[fa], sb0 = xl0[fb] + b0 * dl[fb];
+              const float rho = mnorm * dpm + FACE_TOL;
+              if (sa0 < -rho || sa0 > 1.0f + rho || sb0 < -rho || sb0 > 1.0f + rho) continue;   // proof: no root
+              float sa = sa0, sb = sb0, bt = b0;
+              bool conv = false;
+#pragma unroll 1
+              const int str3[3] = {1, 3, 9};
+              const int fbase = 2 * fside * str3[fk], fsa = str3[fa], fsb = str3[fb];
+              for (int it = 0; it < max_it; ++it) {
+                float xi[3];
+                xi[fk] = (float)fside;
+                xi[fa] = sa;
+                xi[fb] = sb;
+                float X[3];
+                eval_face(sB, fbase, fsa, fsb, sa, sb, X);
+                // E(s) = J0^-1 (X - Xc) + 1/2 - xi
+                const float y0 = X[0] - af[0], y1 = X[1] - af[1], y2 = X[2] - af[2];
+                float Ev[3];
+                Ev[0] = af[3] * y0 + af[4] * y1 + af[5] * y2 + 0.5f - xi[0];
+                Ev[1] = af[6] * y0 + af[7] * y1 + af[8] * y2 + 0.5f - xi[1];
+                Ev[2] = af[9] * y0 + af[10] * y1 + af[11] * y2 + 0.5f - xi[2];
+                // M0^-1 y: beta = -y_k/dl_k, s_a = y_a + beta dl_a, s_b = y_b + beta dl_b
+                const float db = -Ev[fk] * rk;
+                const float nbt = b0 - db;
+                const float nsa = sa0 - (Ev[fa] + db * dl[fa]);
+                const float nsb = sb0 - (Ev[fb] + db * dl[fb]);
+                const float step = fmaxf(fabsf(nsa - sa), fmaxf(fabsf(nsb - sb), fabsf((nbt - bt) * dk)));
+                sa = nsa;
+                sb = nsb;
+                bt = nbt;
+                if (step < tol) {
+                  conv = true;
+                  break;
+                }
+              }
+              if (conv) {
+              if (sa < -FACE_TOL || sa > 1.0f + FACE_TOL || sb < -FACE_TOL || sb > 1.0f + FACE_TOL) continue;
+              if (nroots >= 4) {
+                ++face_fail;
+                continue;
+              }
+              float xi[3];
+              xi[fk] = (float)fside;
+              xi[fa] = fminf(fmaxf(sa, 0.0f), 1.0f);
+              xi[fb] = fminf(fmaxf(sb, 0.0f), 1.0f);
+              W.roots[nroots][0][lane] = bt;
+              W.roots[nroots][1][lane] = xi[0];
+              W.roots[nroots][2][lane] = xi[1];
+              W.roots[nroots][3][lane] = xi[2];
+              ++nroots;
+              continue;
+              }   // not converged (rounding floor for grazing rays): rigorous 2D path below
+            }
+          }
+          {
+            // project this face's 9 Bernstein points on d1, d2
+            const int k = f >> 1, side = f & 1;
+            const int ka = (k + 1) % 3, kb = (k + 2) % 3;
+            const int str[3] = {1, 3, 9};
+            const int base = 2 * side * str[k], sa = str[ka], sbb = str[kb];
+#pragma unroll
+            for (int jb = 0; jb < 3; ++jb)
+#pragma unroll
+              for (int ia = 0; ia < 3; ++ia) {
+                const int m = base + ia * sa + jb * sbb;
+                const float bx = sB[3 * m], by = sB[3 * m + 1], bz = sB[3 * m + 2];
+                sp[(2 * m) * 32] = fmaf(d1[0], bx, fmaf(d1[1], by, fmaf(d1[2], bz, -o1)));
+                sp[(2 * m + 1) * 32] = fmaf(d2[0], bx, fmaf(d2[1], by, fmaf(d2[2], bz, -o2)));
+              }
+          }
+          Patch pt;
+          load_patch(sp, f, pt);
+          if (hull_excludes_origin(pt)) continue;
+          int nf = 0;
+          float A11, A12, A21, A22, gcx, gcy;
+          const float q = injectivity_bound(pt, A11, A12, A21, A22, gcx, gcy);
+          int st = 0;
+          float s1 = 0.f, s2 = 0.f;
+          if (q < 1.0f) st = chord_root(pt, A11, A12, A21, A22, gcx, gcy, q, tol, max_it, s1, s2);
           if (st == 1) {
             if (s1 >= -FACE_TOL && s1 <= 1.0f + FACE_TOL && s2 >= -FACE_TOL && s2 <= 1.0f + FACE_TOL) {
-              u1[0] = s1;
-              u2[0] = s2;
+              su[0] = s1;
+              su[32] = s2;
               nf = 1;
             }
           } else if (st == 0) {
-            nf = face_roots_subdiv(pt, tol, max_it, u1, u2, 4, &face_fail);   // Newton wandered: split
+            nf = face_roots_subdiv(sp, f, tol, max_it, su, 32, 4, &face_fail);
           }
-        } else {
-          nf = face_roots_subdiv(pt, tol, max_it, u1, u2, 4, &face_fail);
-        }
-        if (nroots + nf > MAX_ROOTS) ++face_fail;
-        for (int t = 0; t < nf && nroots < MAX_ROOTS; ++t) {
-          float xi[3];
-          xi[k] = (float)side;
-          xi[a] = fminf(fmaxf(u1[t], 0.0f), 1.0f);
-          xi[b] = fminf(fmaxf(u2[t], 0.0f), 1.0f);
-          float X[3];
-          eval_X(sB, xi, X);
-          float beta = ((X[0] - P0[0]) * rf[0] + (X[1] - P0[1]) * rf[1] + (X[2] - P0[2]) * rf[2]) / rr;
-          // insertion by beta
-          int pos = nroots;
-          while (pos > 0 && roots[pos - 1].beta > beta) {
-            roots[pos] = roots[pos - 1];
-            --pos;
-          }
-          roots[pos].beta = beta;
-          roots[pos].xi[0] = xi[0];
-          roots[pos].xi[1] = xi[1];
-          roots[pos].xi[2] = xi[2];
-          ++nroots;
-        }
-      }
-      // dedupe roots found on two faces at a shared edge / vertex
-      const float hw = fabsf(sB[3 * 26] - sB[0]) + fabsf(sB[3 * 26 + 1] - sB[1]) + fabsf(sB[3 * 26 + 2] - sB[2]);
-      const float dtol = 4e-6f * hw / rn;   // edge roots found on two faces (>= 2x FACE_TOL)
-      int m = 0;
-      for (int t = 0; t < nroots; ++t) {
-        if (m > 0 && roots[t].beta - roots[m - 1].beta < dtol) continue;
-        roots[m++] = roots[t];
-      }
-      nroots = m & ~1;   // entry/exit pairs; an odd leftover is a tangency
-    }
-
-    // ---- 4. segments: GL rule with the inverse map per node ---------------
-    const int nseg = nroots / 2;
-    const float bmin = (float)(cc.amin - (double)alpha0), bmax = (float)(cc.amax - (double)alpha0);
-    const int wseg = __reduce_max_sync(0xffffffffu, (unsigned)nseg);
-    bool any_out = false;
-    const uint32_t pix = (uint32_t)(j * cc.W + i);
-    for (int s = 0; s < wseg; ++s) {
-      bool have = false;
-      float a = 1.0f, bb[3] = {0.f, 0.f, 0.f}, an = 0.f, af = 0.f;
-      if (s < nseg) {
-        const RootRec& ra = roots[2 * s];
-        const RootRec& rb = roots[2 * s + 1];
-        float b0 = fmaxf(ra.beta, bmin), b1 = fminf(rb.beta, bmax);
-        if (b1 > b0) {
-          have = true;
-          const float db = b1 - b0;
-          const float Lseg = db * rn;
-          float xin[3] = {ra.xi[0], ra.xi[1], ra.xi[2]};
-          float dxi[3] = {rb.xi[0] - ra.xi[0], rb.xi[1] - ra.xi[1], rb.xi[2] - ra.xi[2]};
-          float xm[3] = {xin[0] + 0.5f * dxi[0], xin[1] + 0.5f * dxi[1], xin[2] + 0.5f * dxi[2]};
-          float Xm[3], Jm[3][3], Ji[3][3];
-          eval_XJ(sB, xm, Xm, Jm);
-          bool okJ = inv3(Jm, Ji);
-          float ft[N];
-#pragma unroll
-          for (int q = 0; q < N; ++q) {
-            const float bq = fmaf(cc.u[q], db, b0);
-            const float tx = fmaf(bq, rf[0], P0[0]), ty = fmaf(bq, rf[1], P0[1]), tz = fmaf(bq, rf[2], P0[2]);
-            float xi[3] = {fmaf(cc.u[q], dxi[0], xin[0]), fmaf(cc.u[q], dxi[1], xin[1]),
-                           fmaf(cc.u[q], dxi[2], xin[2])};
-            bool conv = false;
-            float last = 3.4e38f;
-            for (int it = 0; okJ && it < max_it; ++it) {
-              float X[3];
-              float Jc[3][3], Jci[3][3];
-              const bool full = it >= 3;   // simplified Newton first, full Newton if it stalls
-              if (full) {
-                eval_XJ(sB, xi, X, Jc);
-                if (!inv3(Jc, Jci)) break;
-              } else {
-                eval_X(sB, xi, X);
-              }
-              const float(*A)[3] = full ? Jci : Ji;
-              float rx = tx - X[0], ry = ty - X[1], rz = tz - X[2];
-              float s0 = A[0][0] * rx + A[0][1] * ry + A[0][2] * rz;
-              float s1 = A[1][0] * rx + A[1][1] * ry + A[1][2] * rz;
-              float s2 = A[2][0] * rx + A[2][1] * ry + A[2][2] * rz;
-              xi[0] += s0;
-              xi[1] += s1;
-              xi[2] += s2;
-              float step = fmaxf(fabsf(s0), fmaxf(fabsf(s1), fabsf(s2)));
-              if (step < tol) {
-                conv = true;
-                break;
-              }
-              last = step;
+          const int k = f >> 1, side = f & 1;
+          const int ka = (k + 1) % 3, kb = (k + 2) % 3;
+          for (int t = 0; t < nf; ++t) {
+            float xi[3];
+            xi[k] = (float)side;
+            xi[ka] = fminf(fmaxf(su[(2 * t) * 32], 0.0f), 1.0f);
+            xi[kb] = fminf(fmaxf(su[(2 * t + 1) * 32], 0.0f), 1.0f);
+            float X[3];
+            eval_X(sB, xi, X);
+            const float beta = ((X[0] - P0[0]) * rf[0] + (X[1] - P0[1]) * rf[1] + (X[2] - P0[2]) * rf[2]) / rr;
+            if (nroots >= 4) {
+              ++face_fail;
+              continue;
             }
-            (void)last;
-            if (!conv) ++local_fail;
-            // the node lies inside the element: clamp against rounding (and
-            // against divergence, which is counted above)
-            xi[0] = fminf(fmaxf(xi[0], 0.0f), 1.0f);
-            xi[1] = fminf(fmaxf(xi[1], 0.0f), 1.0f);
-            xi[2] = fminf(fmaxf(xi[2], 0.0f), 1.0f);
-            ft[q] = field_at<P>(sF, xi[0], xi[1], xi[2]) * cc.inv_F;
+            W.roots[nroots][0][lane] = beta;
+            W.roots[nroots][1][lane] = xi[0];
+            W.roots[nroots][2][lane] = xi[1];
+            W.roots[nroots][3][lane] = xi[2];
+            ++nroots;
           }
-          gl_rule<N>(cc, ft, Lseg, a, bb);
-          an = alpha0 + b0;
-          af = alpha0 + b1;
         }
+        // sort (beta, index) with a 4-element network
+        if (nroots > 0) rb0 = W.roots[0][0][lane];
+        if (nroots > 1) rb1 = W.roots[1][0][lane];
+        if (nroots > 2) rb2 = W.roots[2][0][lane];
+        if (nroots > 3) rb3 = W.roots[3][0][lane];
+#define CSWAP(a, b, ia, ib)                            \
+  if (b < a) {                                        \
+    float tf = a; a = b; b = tf;                      \
+    int ti = ia; ia = ib; ib = ti;                    \
+  }
+        CSWAP(rb0, rb1, ri0, ri1) CSWAP(rb2, rb3, ri2, ri3) CSWAP(rb0, rb2, ri0, ri2) CSWAP(rb1, rb3, ri1, ri3)
+        CSWAP(rb1, rb2, ri1, ri2)
+#undef CSWAP
+        // dedupe roots found on two faces at a shared edge / vertex
+        const float hw = fabsf(sB[3 * 26] - sB[0]) + fabsf(sB[3 * 26 + 1] - sB[1]) + fabsf(sB[3 * 26 + 2] - sB[2]);
+        const float dtol = 4e-6f * hw / rn;
+        if (nroots > 1 && rb1 - rb0 < dtol) { rb1 = rb2; ri1 = ri2; rb2 = rb3; ri2 = ri3; rb3 = 3.4e38f; --nroots; }
+        if (nroots > 2 && rb2 - rb1 < dtol) { rb2 = rb3; ri2 = ri3; rb3 = 3.4e38f; --nroots; }
+        if (nroots > 3 && rb3 - rb2 < dtol) { rb3 = 3.4e38f; --nroots; }
+        nroots &= ~1;   // entry/exit pairs
       }
-      int64_t slot = warp_append(&counters[CNT_SEGS], have ? 1 : 0);
-      if (have) {
-        any_out = true;
-        if (slot < seg_cap) store_seg(segs + slot, pix, an, af, a, bb, key_base + (uint32_t)e);
-        else atomicAdd((unsigned long long*)&counters[CNT_OVERFLOW], 1ull);
+      const float bmin = (float)(cc.amin - (double)alpha0), bmax = (float)(cc.amax - (double)alpha0);
+      bool s0ok = false, s1ok = false;
+      if (nroots >= 2) s0ok = fminf(rb1, bmax) > fmaxf(rb0, bmin);
+      if (nroots >= 4) s1ok = fminf(rb3, bmax) > fmaxf(rb2, bmin);
+      const int nseg = (int)s0ok + (int)s1ok;
+      const uint32_t pix = (uint32_t)(j * cc.W + i);
+      if (nseg > 0) {
+        ++local_hits;
+        atomicAdd(&hits_pp[pix], 1);
       }
-    }
-    if (any_out) {
-      ++local_hits;
-      atomicAdd(&hits_pp[pix], 1);
-    }
+      int64_t slot = warp_append(&counters[CNT_ITEMS], nseg);
+#pragma unroll 1
+      for (int z = 0; z < 2; ++z) {
+        const bool ok = z == 0 ? s0ok : s1ok;
+        if (!ok) continue;
+        const float ba = z == 0 ? rb0 : rb2, bz = z == 0 ? rb1 : rb3;
+        const int ia = z == 0 ? ri0 : ri2, ib = z == 0 ? ri1 : ri3;
+        const float b0 = fmaxf(ba, bmin), b1 = fminf(bz, bmax);
+        if (slot < item_cap) {
+          float4* it = items + 4 * slot;
+          it[0] = make_float4(fmaf(b0, rf[0], P0[0]), fmaf(b0, rf[1], P0[1]), fmaf(b0, rf[2], P0[2]),
+                              fmaf(b1, rf[0], P0[0]));
+          it[1] = make_float4(fmaf(b1, rf[1], P0[1]), fmaf(b1, rf[2], P0[2]), W.roots[ia][1][lane],
+                              W.roots[ia][2][lane]);
+          it[2] = make_float4(W.roots[ia][3][lane], W.roots[ib][1][lane], W.roots[ib][2][lane],
+                              W.roots[ib][3][lane]);
+          it[3] = make_float4(alpha0 + b0, alpha0 + b1, __uint_as_float(pix), __int_as_float(v));
+        } else {
+          atomicAdd((unsigned long long*)&counters[CNT_OVERFLOW], 1ull);
+        }
+        ++slot;
+      }
   }
 #pragma unroll
   for (int off = 16; off > 0; off >>= 1) {
     local_hits += __shfl_down_sync(0xffffffffu, local_hits, off);
-    local_fail += __shfl_down_sync(0xffffffffu, local_fail, off);
     face_fail += __shfl_down_sync(0xffffffffu, face_fail, off);
   }
   if (lane == 0) {
     if (local_hits) atomicAdd((unsigned long long*)&counters[CNT_HITPAIRS], (unsigned long long)local_hits);
-    if (local_fail + face_fail)
-      atomicAdd((unsigned long long*)&counters[CNT_NEWTON_FAIL], (unsigned long long)(local_fail + face_fail));
-    if (face_fail) atomicAdd((unsigned long long*)&counters[CNT_FACE_FAIL], (unsigned long long)face_fail);
+    if (face_fail) {
+      atomicAdd((unsigned long long*)&counters[CNT_NEWTON_FAIL], (unsigned long long)face_fail);
+      atomicAdd((unsigned long long*)&counters[CNT_FACE_FAIL], (unsigned long long)face_fail);
+    }
   }
 }
 
-template <int P>
-static void curved_P(const CamConst& cc, const TreeConst* trees, DevLeafView L, const int32_t* vis,
-                     const Rect16* vrect, const int64_t* chunk_off, const int32_t* chunk_elem, int64_t nchunks,
-                     uint32_t key_base, rc_seg* segs, int64_t seg_cap, int32_t* hits_pp, int64_t* counters, int grid,
-                     cudaStream_t s) {
-#define CASE(N)                                                                                                     \
-  case N:                                                                                                           \
-    k_cast_curved<P, N><<<grid, WARPS * 32, 0, s>>>(cc, trees, L, vis, vrect, chunk_off, chunk_elem, nchunks,      \
-                                                    key_base, segs, seg_cap, hits_pp, counters);                    \
-    break;
-  switch (cc.N) { CASE(1) CASE(2) CASE(3) CASE(4) CASE(5) CASE(6) CASE(7) CASE(8) }
-#undef CASE
+// ---------------------------------------------------------------------------
+// Kernel 2: integration of the items, one per lane, full warps.  The field
+// at each GL node needs xi(x): chord iteration with the
+// element's J0^-1 at the midpoint, quadratic prediction through
+// (entry, midpoint, exit) for the nodes, then chord steps to the tolerance.
+// The elements of a 32-item block (usually 1-3) are prepared once each.
+// ---------------------------------------------------------------------------
+constexpr int GWARPS = 4;
+constexpr int GSLOTS = 4;
+struct IntegSmem {
+  float slot[GSLOTS][SLOT_STRIDE];
+  double prep[2][81];
+  double org[3];
+};
+
+template <int P, int N>
+__global__ void __launch_bounds__(GWARPS * 32, 3) k_integ_curved(CamConst cc, const TreeConst* __restrict__ trees,
+                                                                 DevLeafView L, const int32_t* __restrict__ vis,
+                                                                 const float4* __restrict__ items, int64_t nitems,
+                                                                 uint32_t key_base, rc_seg* __restrict__ segs,
+                                                                 int64_t seg_base, int64_t* __restrict__ counters) {
+  constexpr int NF = (P + 1) * (P + 1) * (P + 1);
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  const int warp = threadIdx.x >> 5;
+  const unsigned lane = threadIdx.x & 31;
+  IntegSmem& W = reinterpret_cast<IntegSmem*>(smem_raw)[warp];
+  const float tol = cc.newton_tol;
+  const int max_it = cc.newton_max;
+  int fails = 0;
+  const int64_t nblocks = (nitems + 31) / 32;
+  for (int64_t blk = (int64_t)blockIdx.x * GWARPS + warp; blk < nblocks; blk += (int64_t)gridDim.x * GWARPS) {
+    const int64_t idx = blk * 32 + lane;
+    const bool act = idx < nitems;
+    float4 i0 = make_float4(0, 0, 0, 0), i1 = i0, i2 = i0, i3 = i0;
+    if (act) {
+      const float4* it = items + 4 * idx;
+      i0 = it[0];
+      i1 = it[1];
+      i2 = it[2];
+      i3 = it[3];
+    }
+    const int v = act ? __float_as_int(i3.w) : -1;
+    // prepare the distinct elements of this block (GSLOTS at a time)
+    unsigned pending = __ballot_sync(0xffffffffu, act);
+    while (pending) {
+      int myslot = -1;
+      int ns = 0;
+      while (pending && ns < GSLOTS) {
+        const int leader = __ffs(pending) - 1;
+        const int vl = __shfl_sync(0xffffffffu, v, leader);
+        prep_element(W.slot[ns], W.org, W.prep, trees, L, vis[vl], lane, NF, true);
+        const unsigned same = __ballot_sync(0xffffffffu, act && v == vl);
+        if (same & (1u << lane)) myslot = ns;
+        pending &= ~same;
+        ++ns;
+      }
+      // integrate the lanes whose element is prepared in this round
+      float a = 1.0f, bb[3] = {0.f, 0.f, 0.f};
+      if (myslot >= 0) {
+        const float* gs = W.slot[myslot];
+        float G[81];
+#pragma unroll
+        for (int m = 0; m < 81; ++m) G[m] = gs[m];
+        const float* fs = gs + 84;
+        const float* afm = gs + SLOT_AFF;
+        float Ji[3][3];
+#pragma unroll
+        for (int aa = 0; aa < 3; ++aa)
+#pragma unroll
+          for (int b = 0; b < 3; ++b) Ji[aa][b] = afm[3 + 3 * aa + b];
+        const float xin[3] = {i0.x, i0.y, i0.z}, xout[3] = {i0.w, i1.x, i1.y};
+        const float xia[3] = {i1.z, i1.w, i2.x}, xib[3] = {i2.y, i2.z, i2.w};
+        const float dX[3] = {xout[0] - xin[0], xout[1] - xin[1], xout[2] - xin[2]};
+        const float Lseg = sqrtf(dX[0] * dX[0] + dX[1] * dX[1] + dX[2] * dX[2]);   // physical length (R2)
+        float xm[3] = {0.5f * (xia[0] + xib[0]), 0.5f * (xia[1] + xib[1]), 0.5f * (xia[2] + xib[2])};
+        const float tm[3] = {xin[0] + 0.5f * dX[0], xin[1] + 0.5f * dX[1], xin[2] + 0.5f * dX[2]};
+        bool ok = false;
+#pragma unroll 1
+        for (int it = 0; it < 2 * max_it; ++it) {
+          float X[3];
+          eval_Xr(G, xm, X);
+          const float r0 = tm[0] - X[0], r1 = tm[1] - X[1], r2 = tm[2] - X[2];
+          const float s0 = Ji[0][0] * r0 + Ji[0][1] * r1 + Ji[0][2] * r2;
+          const float s1 = Ji[1][0] * r0 + Ji[1][1] * r1 + Ji[1][2] * r2;
+          const float s2 = Ji[2][0] * r0 + Ji[2][1] * r1 + Ji[2][2] * r2;
+          xm[0] += s0;
+          xm[1] += s1;
+          xm[2] += s2;
+          if (fmaxf(fabsf(s0), fmaxf(fabsf(s1), fabsf(s2))) < tol) {
+            ok = true;
+            break;
+          }
+        }
+        if (!ok) ++fails;
+        float tau[N], ftv[N];
+#pragma unroll
+        for (int jj = 0; jj < N; ++jj) tau[jj] = ftv[jj] = 0.0f;
+        float sumk = 0.0f;
+#pragma unroll 1
+        for (int q = 0; q < N; ++q) {
+          const float u = cc.u[q];
+          const float l0 = (1.0f - u) * (1.0f - 2.0f * u), l1 = 4.0f * u * (1.0f - u), l2 = u * (2.0f * u - 1.0f);
+          float xi[3] = {l0 * xia[0] + l1 * xm[0] + l2 * xib[0], l0 * xia[1] + l1 * xm[1] + l2 * xib[1],
+                         l0 * xia[2] + l1 * xm[2] + l2 * xib[2]};
+          const float t0 = fmaf(u, dX[0], xin[0]), t1 = fmaf(u, dX[1], xin[1]), t2 = fmaf(u, dX[2], xin[2]);
+          bool conv = false;
+#pragma unroll 1
+          for (int it = 0; it < 2 * max_it; ++it) {
+            float X[3];
+            eval_Xr(G, xi, X);
+            const float r0 = t0 - X[0], r1 = t1 - X[1], r2 = t2 - X[2];
+            const float s0 = Ji[0][0] * r0 + Ji[0][1] * r1 + Ji[0][2] * r2;
+            const float s1 = Ji[1][0] * r0 + Ji[1][1] * r1 + Ji[1][2] * r2;
+            const float s2 = Ji[2][0] * r0 + Ji[2][1] * r1 + Ji[2][2] * r2;
+            xi[0] += s0;
+            xi[1] += s1;
+            xi[2] += s2;
+            if (fmaxf(fabsf(s0), fmaxf(fabsf(s1), fabsf(s2))) < tol) {
+              conv = true;
+              break;
+            }
+          }
+          if (!conv) ++fails;
+          xi[0] = fminf(fmaxf(xi[0], 0.0f), 1.0f);   // nodes lie inside the element
+          xi[1] = fminf(fmaxf(xi[1], 0.0f), 1.0f);
+          xi[2] = fminf(fmaxf(xi[2], 0.0f), 1.0f);
+          const float ft = field_at<P>(fs, xi[0], xi[1], xi[2]) * cc.inv_F;
+          const float kap = cc.kappa0 * ft * ft;
+          sumk = fmaf(cc.w[q], kap, sumk);
+#pragma unroll
+          for (int jj = 0; jj < N; ++jj) {
+            tau[jj] = fmaf(cc.S[jj * RC_MAX_N + q], kap, tau[jj]);
+            ftv[jj] = (jj == q) ? ft : ftv[jj];
+          }
+        }
+        // a = exp(-L sum w kappa); b_c = L sum w_j q_cj exp(-tau_j)
+        a = __expf(-Lseg * sumk);
+        float E0 = 0.0f, E1 = 0.0f;
+#pragma unroll
+        for (int jj = 0; jj < N; ++jj) {
+          const float ee = cc.w[jj] * __expf(-Lseg * tau[jj]);
+          E0 += ee;
+          E1 = fmaf(ee, ftv[jj], E1);
+        }
+        const float sc = 0.5f * Lseg * cc.q0;
+        bb[0] = sc * (E0 + E1);
+        bb[1] = sc * (E0 - E1);
+        bb[2] = sc * E0;
+        store_seg(segs + seg_base + idx, __float_as_uint(i3.z), i3.x, i3.y, a, bb, key_base + (uint32_t)vis[v]);
+      }
+      __syncwarp();
+    }
+  }
+#pragma unroll
+  for (int off = 16; off > 0; off >>= 1) fails += __shfl_down_sync(0xffffffffu, fails, off);
+  if (lane == 0 && fails) atomicAdd((unsigned long long*)&counters[CNT_NEWTON_FAIL], (unsigned long long)fails);
 }
 
-cudaError_t launch_cast_curved(const CamConst& cc, const TreeConst* trees, DevLeafView L, int P, const int32_t* vis,
-                               const Rect16* vrect, const int64_t* chunk_off, const int32_t* chunk_elem,
-                               int64_t nchunks, uint32_t key_base, rc_seg* segs, int64_t seg_cap, int32_t* hits_pp,
-                               int64_t* counters, int grid, cudaStream_t s) {
-  if (P == 1)
-    curved_P<1>(cc, trees, L, vis, vrect, chunk_off, chunk_elem, nchunks, key_base, segs, seg_cap, hits_pp, counters,
-                grid, s);
-  else
-    curved_P<2>(cc, trees, L, vis, vrect, chunk_off, chunk_elem, nchunks, key_base, segs, seg_cap, hits_pp, counters,
-                grid, s);
+}  // namespace
+
+size_t curved_item_bytes() { return 64; }
+
+cudaError_t launch_isect_curved(const CamConst& cc, const TreeConst* trees, DevLeafView L, const int32_t* vis,
+                                const Rect16* vrect, const int64_t* chunk_off, const int32_t* chunk_elem,
+                                int64_t c_begin, int64_t c_end, void* items, int64_t item_cap, int32_t* hits_pp,
+                                int64_t* counters, int grid, cudaStream_t s) {
+  const size_t smem = sizeof(IsectSmem) * IWARPS;
+  static bool attr = false;
+  if (!attr) {
+    cudaError_t e = cudaFuncSetAttribute(k_isect_curved, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    if (e != cudaSuccess) return e;
+    attr = true;
+  }
+  k_isect_curved<<<grid, IWARPS * 32, smem, s>>>(cc, trees, L, vis, vrect, chunk_off, chunk_elem, c_begin, c_end,
+                                                 (float4*)items, item_cap, hits_pp, counters);
   ++g_launches;
   return cudaGetLastError();
+}
+
+template <int P, int N>
+static cudaError_t integ_PN(const CamConst& cc, const TreeConst* trees, DevLeafView L, const int32_t* vis,
+                            const void* items, int64_t nitems, uint32_t key_base, rc_seg* segs, int64_t seg_base,
+                            int64_t* counters, int grid, cudaStream_t s) {
+  const size_t smem = sizeof(IntegSmem) * GWARPS;
+  static bool attr = false;
+  if (!attr) {
+    cudaError_t e = cudaFuncSetAttribute(k_integ_curved<P, N>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    if (e != cudaSuccess) return e;
+    attr = true;
+  }
+  k_integ_curved<P, N><<<grid, GWARPS * 32, smem, s>>>(cc, trees, L, vis, (const float4*)items, nitems, key_base,
+                                                       segs, seg_base, counters);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_integ_curved(const CamConst& cc, const TreeConst* trees, DevLeafView L, int P, const int32_t* vis,
+                                const void* items, int64_t nitems, uint32_t key_base, rc_seg* segs, int64_t seg_base,
+                                int64_t* counters, int grid, cudaStream_t s) {
+  ++g_launches;
+#define CASE(PP, NN)                                                                                              \
+  if (P == PP && cc.N == NN) return integ_PN<PP, NN>(cc, trees, L, vis, items, nitems, key_base, segs, seg_base, \
+                                                     counters, grid, s);
+  CASE(1, 1) CASE(1, 2) CASE(1, 3) CASE(1, 4) CASE(1, 5) CASE(1, 6) CASE(1, 7) CASE(1, 8)
+  CASE(2, 1) CASE(2, 2) CASE(2, 3) CASE(2, 4) CASE(2, 5) CASE(2, 6) CASE(2, 7) CASE(2, 8)
+#undef CASE
+  return cudaErrorInvalidValue;
 }
 
 }  // namespace rc

@@ -17,10 +17,13 @@ cudaError_t launch_cast_affine(const CamConst& cc, const TreeConst* trees, DevLe
                                const Rect16* vrect, const int64_t* chunk_off, const int32_t* chunk_elem,
                                int64_t nchunks, uint32_t key_base, rc_seg* segs, int64_t seg_cap, int32_t* hits_pp,
                                int64_t* counters, int grid, cudaStream_t s);
-cudaError_t launch_cast_curved(const CamConst& cc, const TreeConst* trees, DevLeafView L, int P, const int32_t* vis,
-                               const Rect16* vrect, const int64_t* chunk_off, const int32_t* chunk_elem,
-                               int64_t nchunks, uint32_t key_base, rc_seg* segs, int64_t seg_cap, int32_t* hits_pp,
-                               int64_t* counters, int grid, cudaStream_t s);
+cudaError_t launch_isect_curved(const CamConst& cc, const TreeConst* trees, DevLeafView L, const int32_t* vis,
+                                const Rect16* vrect, const int64_t* chunk_off, const int32_t* chunk_elem,
+                                int64_t c_begin, int64_t c_end, void* items, int64_t item_cap, int32_t* hits_pp,
+                                int64_t* counters, int grid, cudaStream_t s);
+cudaError_t launch_integ_curved(const CamConst& cc, const TreeConst* trees, DevLeafView L, int P, const int32_t* vis,
+                                const void* items, int64_t nitems, uint32_t key_base, rc_seg* segs, int64_t seg_base,
+                                int64_t* counters, int grid, cudaStream_t s);
 cudaError_t launch_pack(const rc_seg* segs, const int64_t* nseg_p, int W, int tw, int th, int tiles_x, int nranks,
                         int64_t* counts, const int64_t* dest_off, int64_t* cursor, rc_seg* out, int grid, bool count,
                         cudaStream_t s);

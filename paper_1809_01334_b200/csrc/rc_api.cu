@@ -161,11 +161,13 @@ extern "C" rc_status rc_forest_destroy(rc_forest* f) {
   void* ptrs[] = {f->d_anchor, f->d_tree, f->d_level, f->d_field, f->d_flag, f->d_rect_all, f->d_scan,
                   f->d_vis, f->d_vis_rect, f->d_chunk_off, f->d_counters, f->d_trees, f->d_cam,
                   f->d_scan_tmp, f->d_chunk_elem, f->d_segs, f->d_hits_pp, f->d_pix_cnt, f->d_pix_off,
-                  f->d_sorted, f->d_send};
+                  f->d_sorted, f->d_send, f->d_items};
   for (void* p : ptrs)
     if (p) cudaFree(p);
   if (f->ev0) cudaEventDestroy(f->ev0);
   if (f->ev1) cudaEventDestroy(f->ev1);
+  for (int k = 0; k < 4; ++k)
+    if (f->evb[k]) cudaEventDestroy(f->evb[k]);
   delete[] f->h_trees;
   delete f;
   return RC_OK;
@@ -466,8 +468,9 @@ extern "C" rc_status rc_cast_segments(rc_forest* f, void* stream) {
   f->h_candidates = cand;
   const int64_t npix = (int64_t)f->cc.W * f->cc.H;
   CU(grow(&f->d_chunk_elem, &f->chunk_cap, std::max<int64_t>(f->h_chunks, 1)));
-  // R=1/affine: at most one segment per candidate; curved: allow 1.25x + 1024 (overflow is counted)
-  int64_t need = f->all_affine ? cand + 1024 : cand + cand / 4 + 4096;
+  // R=1/affine: at most one segment per candidate; curved: start at half the candidates,
+  // grown between chunk batches when needed
+  int64_t need = f->all_affine ? cand + 1024 : std::max<int64_t>(f->h_seg_total, cand / 2) + 4096;
   CU(grow(&f->d_segs, &f->seg_cap, need));
   CU(grow(&f->d_hits_pp, &f->pix_cap, npix));
   CU(cudaMemsetAsync(f->d_hits_pp, 0, sizeof(int32_t) * npix, s));
@@ -485,9 +488,61 @@ extern "C" rc_status rc_cast_segments(rc_forest* f, void* stream) {
                             f->d_hits_pp, f->d_counters, grid, s));
     } else {
       if (f->R != 2) return fail(RC_ERR_INVALID_ARG, "non-affine trees require geom_degree 2");
-      CU(launch_cast_curved(f->cc, f->d_trees, leaf_view(f), f->P, f->d_vis, f->d_vis_rect, f->d_chunk_off,
-                            f->d_chunk_elem, f->h_chunks, (uint32_t)f->first_global, f->d_segs, f->seg_cap,
-                            f->d_hits_pp, f->d_counters, sm_count() * 4, s));
+      // curved path: chunk batches of intersection -> items -> integration
+      const int64_t batch = 1 << 20;
+      const int64_t nb = std::min<int64_t>(f->h_chunks, batch);
+      const int64_t icap = nb * RC_CHUNK * 2;   // at most two segments per pair
+      if (f->items_cap < icap) {
+        if (f->d_items) cudaFree(f->d_items);
+        f->d_items = nullptr;
+        f->items_cap = 0;
+        CU(cudaMalloc(&f->d_items, (size_t)icap * 64));
+        f->items_cap = icap;
+      }
+      for (int k = 0; k < 4; ++k)
+        if (!f->evb[k]) CU(cudaEventCreate(&f->evb[k]));
+      f->phase_ms[1] = f->phase_ms[2] = 0.0f;
+      int64_t seg_total = 0;
+      for (int64_t c0 = 0; c0 < f->h_chunks; c0 += batch) {
+        const int64_t c1 = std::min(c0 + batch, f->h_chunks);
+        CU(cudaMemsetAsync(f->d_counters + CNT_WORK, 0, sizeof(int64_t), s));
+        CU(cudaMemsetAsync(f->d_counters + CNT_ITEMS, 0, sizeof(int64_t), s));
+        CU(cudaEventRecord(f->evb[0], s));
+        CU(launch_isect_curved(f->cc, f->d_trees, leaf_view(f), f->d_vis, f->d_vis_rect, f->d_chunk_off,
+                               f->d_chunk_elem, c0, c1, f->d_items, f->items_cap, f->d_hits_pp, f->d_counters,
+                               sm_count() * 4, s));
+        CU(cudaEventRecord(f->evb[1], s));
+        int64_t ni = 0;
+        CU(cudaMemcpyAsync(&ni, f->d_counters + CNT_ITEMS, sizeof(int64_t), cudaMemcpyDeviceToHost, s));
+        CU(cudaStreamSynchronize(s));
+        float ms = 0.0f;
+        CU(cudaEventElapsedTime(&ms, f->evb[0], f->evb[1]));
+        f->phase_ms[1] += ms;
+        if (ni > f->items_cap) return fail(RC_ERR_CAPACITY, "intersection items overflow");
+        if (seg_total + ni > f->seg_cap) {   // grow, keeping the records of earlier batches
+          int64_t ncap = std::max<int64_t>(seg_total + ni + (seg_total + ni) / 4, 1024);
+          rc_seg* nseg = nullptr;
+          CU(cudaMalloc((void**)&nseg, sizeof(rc_seg) * (size_t)ncap));
+          if (seg_total > 0)
+            CU(cudaMemcpyAsync(nseg, f->d_segs, sizeof(rc_seg) * (size_t)seg_total, cudaMemcpyDeviceToDevice, s));
+          CU(cudaStreamSynchronize(s));
+          if (f->d_segs) cudaFree(f->d_segs);
+          f->d_segs = nseg;
+          f->seg_cap = ncap;
+        }
+        if (ni > 0) {
+          CU(cudaEventRecord(f->evb[2], s));
+          CU(launch_integ_curved(f->cc, f->d_trees, leaf_view(f), f->P, f->d_vis, f->d_items, ni,
+                                 (uint32_t)f->first_global, f->d_segs, seg_total, f->d_counters, sm_count() * 3, s));
+          CU(cudaEventRecord(f->evb[3], s));
+          CU(cudaEventSynchronize(f->evb[3]));
+          CU(cudaEventElapsedTime(&ms, f->evb[2], f->evb[3]));
+          f->phase_ms[2] += ms;
+        }
+        seg_total += ni;
+      }
+      f->h_seg_total = seg_total;
+      CU(cudaMemcpyAsync(f->d_counters + CNT_SEGS, &f->h_seg_total, sizeof(int64_t), cudaMemcpyHostToDevice, s));
     }
   }
   CU(cudaEventRecord(f->ev1, s));
@@ -502,6 +557,14 @@ extern "C" float rc_last_cast_ms(rc_forest* f) {
   if (cudaEventSynchronize(f->ev1) != cudaSuccess) return -1.0f;
   if (cudaEventElapsedTime(&ms, f->ev0, f->ev1) != cudaSuccess) return -1.0f;
   return ms;
+}
+
+extern "C" float rc_last_phase_ms(rc_forest* f, int32_t phase) {
+  if (!f || !f->timed) return -1.0f;
+  if (phase == 0) return rc_last_cast_ms(f);
+  if (f->all_affine) return phase == 1 ? rc_last_cast_ms(f) : 0.0f;
+  if (phase == 1 || phase == 2) return f->phase_ms[phase];
+  return -1.0f;
 }
 
 extern "C" rc_status rc_segments_get(rc_forest* f, rc_segments* out, void* stream) {

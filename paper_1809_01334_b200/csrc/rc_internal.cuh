@@ -97,8 +97,14 @@ struct rc_forest {
   // scan scratch
   int64_t* d_scan_tmp = nullptr;
   int64_t scan_tmp_cap = 0;
+  // curved path: intersection items of one chunk batch (64 B each)
+  void* d_items = nullptr;
+  int64_t items_cap = 0;
+  int64_t h_seg_total = 0;
   // timing
   cudaEvent_t ev0 = nullptr, ev1 = nullptr;
+  cudaEvent_t evb[4] = {nullptr, nullptr, nullptr, nullptr};
+  float phase_ms[3] = {0, 0, 0};
   bool timed = false;
 };
 
@@ -111,6 +117,7 @@ enum {
   CNT_OVERFLOW = 4,
   CNT_WORK = 5,        // dynamic work counter of the segment kernel
   CNT_FACE_FAIL = 6,   // face-root Newton non-convergence (diagnostic)
+  CNT_ITEMS = 7,       // curved path: (pair, segment) items of the current batch
   CNT_SEND = 8,        // [8..8+64) per-rank cursors for pack
   CNT_TOTAL = 80
 };

@@ -58,7 +58,8 @@ class Tiling(C.Structure):
 SEG_BYTES = 32
 EXPORTS = ["rc_last_error", "rc_version", "rc_forest_create", "rc_forest_destroy", "rc_camera_set", "rc_cull",
            "rc_cull_result", "rc_cast_segments", "rc_segments_get", "rc_aggregate", "rc_pack_tiles",
-           "rc_composite_tiles", "rc_composite", "rc_render_frame", "rc_launch_count", "rc_last_cast_ms"]
+           "rc_composite_tiles", "rc_composite", "rc_render_frame", "rc_launch_count", "rc_last_cast_ms",
+           "rc_last_phase_ms"]
 
 _lib = None
 
@@ -90,9 +91,11 @@ def lib():
     L.rc_launch_count.restype = i64
     L.rc_last_cast_ms.argtypes = [vp]
     L.rc_last_cast_ms.restype = C.c_float
+    L.rc_last_phase_ms.argtypes = [vp, i32]
+    L.rc_last_phase_ms.restype = C.c_float
     for name in EXPORTS:
         getattr(L, name).restype = getattr(L, name).restype if name in (
-            "rc_last_error", "rc_version", "rc_launch_count", "rc_last_cast_ms") else C.c_int
+            "rc_last_error", "rc_version", "rc_launch_count", "rc_last_cast_ms", "rc_last_phase_ms") else C.c_int
     _lib = L
     return L
 
@@ -288,6 +291,9 @@ class Forest:
 
     def last_cast_ms(self):
         return float(lib().rc_last_cast_ms(self.h))
+
+    def last_phase_ms(self, phase):
+        return float(lib().rc_last_phase_ms(self.h, int(phase)))
 
 
 def launch_count(reset=False) -> int:

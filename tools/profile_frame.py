@@ -1,0 +1,24 @@
+"""Minimal frame driver for ncu: build the scene, run `--frames` frames."""
+import argparse
+import os
+import sys
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+sys.path.insert(0, ROOT)
+
+if __name__ == "__main__":
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--config", type=int, default=3)
+    ap.add_argument("--frames", type=int, default=2)
+    a = ap.parse_args()
+    import torch
+    import bench
+    from paper_1809_01334_b200 import rc
+    sc = bench.make_scene(a.config, torch.device("cuda"))
+    f = rc.Forest.from_scene(sc, device_copy=True)
+    for _ in range(a.frames):
+        img, hits = f.render_frame(sc.camera)
+    torch.cuda.synchronize()
+    s = f.segments()
+    print("hit_pairs", hits, "candidates", s["candidates"], "segments", s["count"], "newton_failures",
+          s["newton_failures"], "cast_ms", f.last_cast_ms(), "isect_ms", f.last_phase_ms(1), "integ_ms", f.last_phase_ms(2))
