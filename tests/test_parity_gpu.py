@@ -181,3 +181,35 @@ def test_affine_r2_matches_r1_P9():
     g1, g2 = gpu_run(sc1), gpu_run(sc2)
     assert g1["count"] == g2["count"]
     assert np.abs(g1["rgba"] - g2["rgba"]).max() < 1e-6
+
+
+@pytest.mark.parametrize("which,nranks", [("c2", 2), ("c2", 3), ("shell", 4)])
+def test_virtual_ranks_tile_exchange(which, nranks):
+    """Multi-GPU path on one GPU: P forests over contiguous SFC
+    ranges, rc_pack_tiles by tile owner, the per-owner concatenation stands in
+    for the NCCL all-to-all, rc_composite_tiles per owner.  Equals the
+    single-forest image (partition invariance)."""
+    import torch
+    from paper_1809_01334_b200 import dist as rdist
+    from paper_1809_01334_b200 import rc
+    sc = sg.config2(width=96, maxlevel=5) if which == "c2" else sg.shell_uniform(3, 96, 16, gl_points=6)
+    tiles = (4, 4)
+    full = gpu_run(sc)["rgba"].reshape(96, 96, 4)
+    ranges = rdist.weighted_ranges(torch.ones(sc.num_leaves), nranks)
+    forests, packed = [], []
+    for lo, hi in ranges:
+        f = rc.Forest.from_scene(sc, first=lo, count=hi - lo)
+        f.camera_set(sc.camera)
+        f.cull()
+        f.cast_segments()
+        raw, counts = f.pack_tiles(*tiles, nranks, 0)
+        offs = np.r_[0, np.cumsum(counts)]
+        packed.append([raw[offs[d]:offs[d + 1]].clone() for d in range(nranks)])
+        forests.append(f)
+    out = {}
+    for d in range(nranks):
+        recv = torch.cat([packed[s][d] for s in range(nranks)])
+        img, mine = forests[d].composite_tiles(*tiles, nranks, d, recv=recv)
+        out[d] = (img, mine)
+    merged = rdist.assemble_image(out, *tiles, 96, 96).numpy()
+    assert np.abs(merged - full).max() < 1e-6
