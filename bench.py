@@ -118,6 +118,15 @@ def forest_affine(scene):
     return scene.name.startswith(("C1", "C2"))
 
 
+def scene_to_host(scene):
+    import dataclasses
+    import numpy as np
+    def h(a):
+        return a if isinstance(a, np.ndarray) else a.detach().cpu().numpy()
+    return dataclasses.replace(scene, leaf_anchor=h(scene.leaf_anchor), leaf_tree=h(scene.leaf_tree),
+                               leaf_level=h(scene.leaf_level), leaf_field=h(scene.leaf_field))
+
+
 def l2_flush(buf):
     buf.add_(1.0)
 
@@ -146,7 +155,9 @@ def run_reference(args):
     rank = int(os.environ.get("RANK", "0"))
     if rank != 0:
         return
-    scene = make_scene(args.config, None if args.config <= 2 else "cpu")
+    import torch
+    dev = "cuda" if (args.config >= 3 and torch.cuda.is_available()) else None
+    scene = scene_to_host(make_scene(args.config, dev))
     stride = {1: 1, 2: 8, 3: 32, 4: 64, 5: 128}[args.config]
     for _ in range(args.warmup):
         pass
@@ -232,7 +243,7 @@ def main():
         hits_total, cand_total = hits_local, cand_local
 
     # --- timed region: K frames, L2 flushed between frames (outside events) ---
-    times, cast_ms = [], []
+    times, cast_ms, phase_ms = [], [], []
     rc.launch_count(reset=True)
     with Clocks(local) as clk:
         for _ in range(args.steps):
@@ -247,7 +258,8 @@ def main():
             e1.record(stream)
             torch.cuda.synchronize()
             times.append(e0.elapsed_time(e1))
-            cast_ms.append(forest.last_cast_ms())
+            cast_ms.append(forest.last_phase_ms(1) + forest.last_phase_ms(2))
+            phase_ms.append((forest.last_phase_ms(1), forest.last_phase_ms(2), forest.last_cast_ms()))
     launches = rc.launch_count()
     ms_local = sum(times) / len(times)
     if world > 1:
@@ -264,9 +276,13 @@ def main():
     import bench_model
     fl = bench_model.flops(scene.geom_degree if not forest_affine(scene) else 1, N, hits_local, cand_local)
     achieved = fl / (cast_avg / 1000.0) / 1e12
-    roof = {"kernel": "k_cast_affine" if forest_affine(scene) else "k_cast_curved", "bound": "alu",
+    kname = "k_cast_affine" if forest_affine(scene) else "k_isect_curved + k_integ_curved"
+    roof = {"kernel": kname, "bound": "alu",
             "achieved": achieved, "peak": pk["fp32_tflops"], "unit": "TFLOP/s", "frac": achieved / pk["fp32_tflops"],
             "traffic": None, "kernel_ms": cast_avg, "share_of_step": cast_avg / ms_step,
+            "phase_ms": {"intersection": sum(p[0] for p in phase_ms) / len(phase_ms),
+                         "integration": sum(p[1] for p in phase_ms) / len(phase_ms),
+                         "cast_call_wall_on_stream": sum(p[2] for p in phase_ms) / len(phase_ms)},
             "algorithmic_flops_per_launch": fl, "peak_source": pk["source"]}
     tpath = os.path.join(ROOT, "profiles", f"traffic_c{args.config}.json")
     if os.path.exists(tpath):
@@ -276,6 +292,11 @@ def main():
             pass
 
     # --- end to end through the public API with HOST buffers --------------
+    seg_info = forest.segments()
+    newton_failures = seg_info["newton_failures"]
+    forest.close()          # release the device-resident forest before the e2e forests
+    del forest
+    torch.cuda.empty_cache()
     host = [np.ascontiguousarray(a if isinstance(a, np.ndarray) else a.cpu().numpy())
             for a in (scene.leaf_anchor[lo:hi], scene.leaf_tree[lo:hi], scene.leaf_level[lo:hi],
                       scene.leaf_field[lo:hi])]
@@ -283,7 +304,8 @@ def main():
     h2d = sum(a.nbytes for a in host)
     img_host = torch.empty((H, W, 4), dtype=torch.float32).pin_memory()
     e2e_times = []
-    for it in range(2 + max(1, min(args.steps, 3))):
+    n_e2e = 2 + (1 if args.config >= 4 else max(1, min(args.steps, 3)))
+    for it in range(n_e2e):
         torch.cuda.synchronize()
         if world > 1:
             torch.distributed.barrier()
@@ -328,10 +350,11 @@ def main():
                            "candidate_pairs_per_s": cand_total / (ms_step / 1000.0),
                            "l2": "flushed between frames (160 MB write outside the events)",
                            "parallelism": f"sfc{world}"},
-                "roofline": roof, "gpu_launches": launches, "clocks": clk.summary(), "e2e": e2e}
+                "roofline": roof, "gpu_launches": launches, "clocks": clk.summary(), "e2e": e2e,
+                "newton_failures": newton_failures}
         if world == 1 and not args.no_cpu_baseline:
             stride = {1: 1, 2: 8, 3: 32, 4: 64, 5: 128}[args.config]
-            sc_cpu = scene if args.config <= 2 else make_scene(args.config, "cpu")
+            sc_cpu = scene_to_host(scene)
             cb = cpu_baseline(sc_cpu, stride)
             line["cpu_baseline"] = {k: cb[k] for k in ("value", "unit", "cores", "kind", "sample")}
         print(json.dumps(line), flush=True)

@@ -383,12 +383,14 @@ __global__ void k_hist(const rc_seg* __restrict__ segs, int64_t n, int32_t* __re
     atomicAdd(&cnt[segs[s].pixel], 1);
 }
 
+// bucket by pixel as a permutation (record indices, 4 bytes each) instead of
+// a sorted copy of the 32-byte records
 __global__ void k_scatter(const rc_seg* __restrict__ segs, int64_t n, const int64_t* __restrict__ off,
-                          int32_t* __restrict__ cursor, rc_seg* __restrict__ out) {
+                          int32_t* __restrict__ cursor, uint32_t* __restrict__ out) {
   for (int64_t s = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; s < n; s += (int64_t)gridDim.x * blockDim.x) {
-    rc_seg rec = segs[s];
-    int k = atomicAdd(&cursor[rec.pixel], 1);
-    out[off[rec.pixel] + k] = rec;
+    const uint32_t pix = segs[s].pixel;
+    int k = atomicAdd(&cursor[pix], 1);
+    out[off[pix] + k] = (uint32_t)s;
   }
 }
 
@@ -473,7 +475,8 @@ struct Sweep {
 constexpr int FOLD_WARPS = 4;
 constexpr int FOLD_CAP = 2048;   // records per pixel sorted in shared memory
 
-__global__ void __launch_bounds__(FOLD_WARPS * 32) k_fold(const rc_seg* __restrict__ sorted,
+__global__ void __launch_bounds__(FOLD_WARPS * 32) k_fold(const rc_seg* __restrict__ recs,
+                                                          const uint32_t* __restrict__ perm,
                                                           const int64_t* __restrict__ off, int W, int H, int tw,
                                                           int th, const int32_t* __restrict__ my_tiles,
                                                           int tiles_x, int64_t npix_out, float bg0, float bg1,
@@ -494,13 +497,13 @@ __global__ void __launch_bounds__(FOLD_WARPS * 32) k_fold(const rc_seg* __restri
     int64_t pix = (int64_t)j * W + i;
     int64_t base = off[pix];
     int n = (int)(off[pix + 1] - base);
-    const rc_seg* S = sorted + base;
+    const uint32_t* S = perm + base;   // S[k] = index of the pixel's k-th record
     Acc acc{1.0, 0.0, 0.0, 0.0};
     if (n <= FOLD_CAP) {
       int m = 1;
       while (m < n) m <<= 1;
       for (int k = lane; k < m; k += 32) {
-        keys[k] = k < n ? sort_key(S[k]) : ~0ull;
+        keys[k] = k < n ? sort_key(recs[S[k]]) : ~0ull;
         idxs[k] = (uint16_t)k;
       }
       __syncwarp();
@@ -524,8 +527,8 @@ __global__ void __launch_bounds__(FOLD_WARPS * 32) k_fold(const rc_seg* __restri
       // overlap detection between consecutive records
       bool ovl = false;
       for (int k = lane; k + 1 < n; k += 32) {
-        const rc_seg& x = S[idxs[k]];
-        const rc_seg& y = S[idxs[k + 1]];
+        const rc_seg& x = recs[S[idxs[k]]];
+        const rc_seg& y = recs[S[idxs[k + 1]]];
         float tol = tau * fmaxf(1.0f, fabsf(y.alpha_near));
         ovl |= (x.alpha_far - y.alpha_near) > tol;
       }
@@ -534,7 +537,7 @@ __global__ void __launch_bounds__(FOLD_WARPS * 32) k_fold(const rc_seg* __restri
           Sweep sw;
           sw.acc = acc;
           sw.tau = tau;
-          for (int k = 0; k < n; ++k) sw.push(piece_of(S[idxs[k]]));
+          for (int k = 0; k < n; ++k) sw.push(piece_of(recs[S[idxs[k]]]));
           sw.finish();
           acc = sw.acc;
         }
@@ -543,7 +546,7 @@ __global__ void __launch_bounds__(FOLD_WARPS * 32) k_fold(const rc_seg* __restri
         int per = (n + 31) / 32;
         int lo = min(n, (int)lane * per), hi = min(n, lo + per);
         for (int k = lo; k < hi; ++k) {
-          const rc_seg& s = S[idxs[k]];
+          const rc_seg& s = recs[S[idxs[k]]];
           acc_push(acc, s.a, s.b[0], s.b[1], s.b[2]);
         }
 #pragma unroll
@@ -567,13 +570,13 @@ __global__ void __launch_bounds__(FOLD_WARPS * 32) k_fold(const rc_seg* __restri
         uint64_t best = ~0ull;
         int bi = -1;
         for (int k = 0; k < n; ++k) {
-          uint64_t kk = sort_key(S[k]);
+          uint64_t kk = sort_key(recs[S[k]]);
           if ((first || kk > last) && kk < best) { best = kk; bi = k; }
         }
         if (bi < 0) break;
         first = false;
         last = best;
-        sw.push(piece_of(S[bi]));
+        sw.push(piece_of(recs[S[bi]]));
       }
       sw.finish();
       acc = sw.acc;
@@ -663,14 +666,14 @@ cudaError_t launch_hist(const rc_seg* segs, int64_t n, int32_t* cnt, int grid, c
   return cudaGetLastError();
 }
 
-cudaError_t launch_scatter(const rc_seg* segs, int64_t n, const int64_t* off, int32_t* cursor, rc_seg* out, int grid,
-                           cudaStream_t s) {
+cudaError_t launch_scatter(const rc_seg* segs, int64_t n, const int64_t* off, int32_t* cursor, uint32_t* out,
+                           int grid, cudaStream_t s) {
   k_scatter<<<grid, 256, 0, s>>>(segs, n, off, cursor, out);
   ++g_launches;
   return cudaGetLastError();
 }
 
-cudaError_t launch_fold(const rc_seg* sorted, const int64_t* off, int W, int H, int tw, int th,
+cudaError_t launch_fold(const rc_seg* recs, const uint32_t* perm, const int64_t* off, int W, int H, int tw, int th,
                         const int32_t* my_tiles, int tiles_x, int64_t npix_out, const float bg[3], float tau,
                         float* rgba, int max_grid, cudaStream_t s) {
   static bool attr = false;
@@ -681,7 +684,7 @@ cudaError_t launch_fold(const rc_seg* sorted, const int64_t* off, int W, int H, 
     attr = true;
   }
   int grid = (int)std::min<int64_t>((npix_out + FOLD_WARPS - 1) / FOLD_WARPS, (int64_t)max_grid);
-  k_fold<<<grid, FOLD_WARPS * 32, smem, s>>>(sorted, off, W, H, tw, th, my_tiles, tiles_x, npix_out, bg[0], bg[1],
+  k_fold<<<grid, FOLD_WARPS * 32, smem, s>>>(recs, perm, off, W, H, tw, th, my_tiles, tiles_x, npix_out, bg[0], bg[1],
                                              bg[2], tau, rgba);
   ++g_launches;
   return cudaGetLastError();

@@ -161,7 +161,7 @@ extern "C" rc_status rc_forest_destroy(rc_forest* f) {
   void* ptrs[] = {f->d_anchor, f->d_tree, f->d_level, f->d_field, f->d_flag, f->d_rect_all, f->d_scan,
                   f->d_vis, f->d_vis_rect, f->d_chunk_off, f->d_counters, f->d_trees, f->d_cam,
                   f->d_scan_tmp, f->d_chunk_elem, f->d_segs, f->d_hits_pp, f->d_pix_cnt, f->d_pix_off,
-                  f->d_sorted, f->d_send, f->d_items};
+                  f->d_perm, f->d_send, f->d_items};
   for (void* p : ptrs)
     if (p) cudaFree(p);
   if (f->ev0) cudaEventDestroy(f->ev0);
@@ -676,7 +676,8 @@ extern "C" rc_status rc_composite_tiles(rc_forest* f, const rc_tiling* t, const 
   }
   int64_t need_tmp = (int64_t)scan_tmp_size(npix + 1) + 128;
   if (need_tmp > f->scan_tmp_cap) CU(grow(&f->d_scan_tmp, &f->scan_tmp_cap, need_tmp));
-  CU(grow(&f->d_sorted, &f->sorted_cap, std::max<int64_t>(nsrc, 1)));
+  if (nsrc >= (int64_t)UINT32_MAX) return fail(RC_ERR_CAPACITY, "more than 2^32 records in one composite");
+  CU(grow(&f->d_perm, &f->perm_cap, std::max<int64_t>(nsrc, 1)));
   int32_t* d_my_tiles = nullptr;
   CU(cudaMallocAsync((void**)&d_my_tiles, sizeof(int32_t) * std::max<size_t>(mine.size(), 1), s));
   if (!mine.empty())
@@ -689,12 +690,12 @@ extern "C" rc_status rc_composite_tiles(rc_forest* f, const rc_tiling* t, const 
   CU(scan_exclusive<int32_t>(f->d_pix_cnt, f->d_pix_off, npix, f->d_scan_tmp, s));
   CU(cudaMemsetAsync(f->d_pix_cnt, 0, sizeof(int32_t) * npix, s));
   if (nsrc > 0) {
-    CU(launch_scatter(src, nsrc, f->d_pix_off, f->d_pix_cnt, f->d_sorted, grid, s));
+    CU(launch_scatter(src, nsrc, f->d_pix_off, f->d_pix_cnt, f->d_perm, grid, s));
   }
   if (npix_out > 0) {
     float bg[3] = {0, 0, 0};
     if (background) memcpy(bg, background, sizeof bg);
-    CU(launch_fold(f->d_sorted, f->d_pix_off, W, H, tw, th, d_my_tiles, t->tiles_x, npix_out, bg, 1e-6f, d_rgba,
+    CU(launch_fold(src, f->d_perm, f->d_pix_off, W, H, tw, th, d_my_tiles, t->tiles_x, npix_out, bg, 1e-6f, d_rgba,
                    sm_count() * 16, s));
   }
   CU(cudaFreeAsync(d_my_tiles, s));

@@ -90,8 +90,8 @@ struct rc_forest {
   int32_t* d_pix_cnt = nullptr;   // [W*H]
   int64_t pix_cnt_cap = 0;
   int64_t* d_pix_off = nullptr;   // [W*H+1]
-  rc_seg* d_sorted = nullptr;
-  int64_t sorted_cap = 0;
+  uint32_t* d_perm = nullptr;     // pixel-bucketed permutation of the records
+  int64_t perm_cap = 0;
   rc_seg* d_send = nullptr;
   int64_t send_cap = 0;
   // scan scratch

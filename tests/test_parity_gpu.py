@@ -213,3 +213,21 @@ def test_virtual_ranks_tile_exchange(which, nranks):
         out[d] = (img, mine)
     merged = rdist.assemble_image(out, *tiles, 96, 96).numpy()
     assert np.abs(merged - full).max() < 1e-6
+
+
+def test_c4_full_size_sampled():
+    """BASELINE C4 at full size on one GPU (100,663,296 curved hexes, 2048^2,
+    N = 6) in the bench's launch configuration; 256 stratified pixels compared
+    one by one with the oracle (which culls all 1e8 leaves in fp64)."""
+    sc = sg.config4(device="cuda")
+    g = gpu_run(sc, device_copy=True)
+    assert g["newton_failures"] == 0
+    import bench
+    o = oracle.OracleScene(bench.scene_to_host(sc))
+    W = sc.camera.width
+    jj, ii = np.meshgrid(np.arange(37, W, 128), np.arange(61, W, 128), indexing="ij")
+    pixels = (jj * W + ii).ravel().astype(np.int32)
+    ores = o.render(pixels, mode="exact", cap=1536)
+    rep = compare(sc, g, ores, pixels)
+    print(rep, "hit_pairs", g["hit_pairs"], "segments", g["count"])
+    _check(rep)
