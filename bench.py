@@ -182,9 +182,11 @@ def main():
     ap.add_argument("--gpus", type=int, default=1)
     ap.add_argument("--steps", type=int, default=10)
     ap.add_argument("--warmup", type=int, default=3)
-    ap.add_argument("--config", type=int, default=int(os.environ.get("RC_BENCH_CONFIG", "2")))
+    ap.add_argument("--config", type=int, default=int(os.environ.get("RC_BENCH_CONFIG", "4")))
     ap.add_argument("--impl", default="rc")
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--fold", type=int, default=-1,
+                    help="node level of the on-chip fold (row a6); default 2 for curved forests, 0 for affine")
     args = ap.parse_args()
     if args.impl == "reference":
         return run_reference(args)
@@ -216,10 +218,12 @@ def main():
     flush = torch.empty(int(160e6) // 4, dtype=torch.float32, device=dev)   # > 126 MB L2
     stream = torch.cuda.current_stream()
 
+    fold = args.fold if args.fold >= 0 else (0 if forest_affine(scene) else 2)
+
     def frame():
         forest.camera_set(cam)
         forest.cull()
-        forest.cast_segments()
+        forest.cast_segments(fold)
         if scene.coarsen_cycles:
             forest.aggregate(scene.coarsen_cycles)
         if world == 1:
@@ -258,8 +262,7 @@ def main():
             e1.record(stream)
             torch.cuda.synchronize()
             times.append(e0.elapsed_time(e1))
-            cast_ms.append(forest.last_phase_ms(1) + forest.last_phase_ms(2))
-            phase_ms.append((forest.last_phase_ms(1), forest.last_phase_ms(2), forest.last_cast_ms()))
+            cast_ms.append(forest.last_phase_ms(1))
     launches = rc.launch_count()
     ms_local = sum(times) / len(times)
     if world > 1:
@@ -276,13 +279,10 @@ def main():
     import bench_model
     fl = bench_model.flops(scene.geom_degree if not forest_affine(scene) else 1, N, hits_local, cand_local)
     achieved = fl / (cast_avg / 1000.0) / 1e12
-    kname = "k_cast_affine" if forest_affine(scene) else "k_isect_curved + k_integ_curved"
+    kname = "k_cast_affine" if forest_affine(scene) else "k_cast_curved (intersection + integration + fold, fused)"
     roof = {"kernel": kname, "bound": "alu",
             "achieved": achieved, "peak": pk["fp32_tflops"], "unit": "TFLOP/s", "frac": achieved / pk["fp32_tflops"],
             "traffic": None, "kernel_ms": cast_avg, "share_of_step": cast_avg / ms_step,
-            "phase_ms": {"intersection": sum(p[0] for p in phase_ms) / len(phase_ms),
-                         "integration": sum(p[1] for p in phase_ms) / len(phase_ms),
-                         "cast_call_wall_on_stream": sum(p[2] for p in phase_ms) / len(phase_ms)},
             "algorithmic_flops_per_launch": fl, "peak_source": pk["source"]}
     tpath = os.path.join(ROOT, "profiles", f"traffic_c{args.config}.json")
     if os.path.exists(tpath):
@@ -294,6 +294,9 @@ def main():
     # --- end to end through the public API with HOST buffers --------------
     seg_info = forest.segments()
     newton_failures = seg_info["newton_failures"]
+    fold_info = {"fold_levels": fold, "records": seg_info["count"], "raw_segments": seg_info["raw_segments"],
+                 "record_level": seg_info["level"], "units": seg_info["units"],
+                 "unfolded_units": seg_info["unfolded_units"]}
     forest.close()          # release the device-resident forest before the e2e forests
     del forest
     torch.cuda.empty_cache()
@@ -315,7 +318,7 @@ def main():
                        scene.inv_F, scene.q0, first_global_leaf=lo)
         f2.camera_set(cam)
         f2.cull()
-        f2.cast_segments()
+        f2.cast_segments(fold)
         if scene.coarsen_cycles:
             f2.aggregate(scene.coarsen_cycles)
         if world == 1:
@@ -351,7 +354,7 @@ def main():
                            "l2": "flushed between frames (160 MB write outside the events)",
                            "parallelism": f"sfc{world}"},
                 "roofline": roof, "gpu_launches": launches, "clocks": clk.summary(), "e2e": e2e,
-                "newton_failures": newton_failures}
+                "newton_failures": newton_failures, "segments": fold_info}
         if world == 1 and not args.no_cpu_baseline:
             stride = {1: 1, 2: 8, 3: 32, 4: 64, 5: 128}[args.config]
             sc_cpu = scene_to_host(scene)

@@ -123,16 +123,25 @@ rc_status rc_cull_result(rc_forest* f, int32_t* d_visible, int64_t capacity, int
  * over each inside interval with the N-point nested Gauss-Legendre rule
  * (SURVEY R13), giving the segment (alpha_near, alpha_far, a, b[3]) of
  * Eq. ABgeneral, near end = camera side.
- * Must follow rc_cull.  [sync] (one small D2H of the candidate count to
- * size the output; kernels are asynchronous).
+ *
+ * fold_levels = c in [0, 8] (row a6): the segments are combined per
+ * (node of coarsening level c, pixel) where they touch, nearest first with
+ * Eq. aggregate -- the first c coarsening cycles of
+ * PAPER.md:956-977, done on chip for curved trees.  Level 0
+ * gives one record per (leaf, pixel, segment).  Records are keyed by the
+ * global SFC index of the node's first leaf (the leaf itself at level 0).
+ * Node levels: level c+1 replaces every complete local family of 8 siblings
+ * of level c by its parent (rc_node_table).
+ * Must follow rc_cull.  [sync] (small D2H reads to size the outputs; a too
+ * small record buffer is grown and the kernel repeated).
  * ---------------------------------------------------------------------- */
 typedef struct {              /* 32-byte segment record, also the wire format          */
   uint32_t pixel;             /* j*w + i                                                */
   float alpha_near, alpha_far;/* ray parameter interval, alpha_near < alpha_far         */
   float a;                    /* transmission, shared by the channels (scalar kappa)     */
   float b[3];                 /* emission per channel                                   */
-  uint32_t key;               /* global SFC leaf index (tie-break R16; node id after
-                                 aggregation = first leaf of the node)                   */
+  uint32_t key;               /* global SFC index of the record's node's first leaf
+                                 (tie-break R16; the leaf itself at level 0)            */
 } rc_seg;
 
 typedef struct {
@@ -142,20 +151,30 @@ typedef struct {
   int64_t newton_failures;     /* R=2 Newton non-convergence count, all solves (must be 0) */
   int64_t face_failures;       /* ... of which face-root solves (diagnostic)               */
   int64_t num_visible;
+  int64_t raw_segments;        /* segments before any folding                          */
+  int64_t level;               /* node level of the records (fold + aggregation cycles) */
+  int64_t units;               /* fold units of the curved kernel                      */
+  int64_t unfolded_units;      /* units over the on-chip sort capacity (emitted unfolded) */
   const rc_seg* segs;          /* device view, library-owned                           */
   const int32_t* hits_per_pixel; /* device [w*h]: pairs with >= 1 segment per pixel     */
 } rc_segments;
 
-rc_status rc_cast_segments(rc_forest* f, void* stream);
+rc_status rc_cast_segments(rc_forest* f, int32_t fold_levels, void* stream);
 /* [sync] fills *out with counts and device views of the current segments. */
 rc_status rc_segments_get(rc_forest* f, rc_segments* out, void* stream);
 
+/* [sync] Copies the node table of coarsening level `level` in [1, 8] (local
+ * index of each node's first leaf, SFC order) to d_first[capacity] (device);
+ * *count = number of nodes.  RC_ERR_CAPACITY if capacity is too small. */
+rc_status rc_node_table(rc_forest* f, int32_t level, int32_t* d_first, int64_t capacity, int64_t* count,
+                        void* stream);
+
 /* ------------------------------------------------------------------------
- * Aggregate (PAPER.md:956-994 coarsening): `cycles` times, replace every
- * complete local family of same-level siblings by its parent and, per
- * (parent, pixel), merge the children's segments in alpha order, combining
- * touching ones with Eq. aggregate.  Lossless up to roundoff.
- * [sync]
+ * Aggregate (PAPER.md:956-994 coarsening cycles, row a7): `cycles` more
+ * levels: every complete local family of siblings is replaced by its parent
+ * and, per (parent, pixel), the children's records are merged in alpha order,
+ * touching ones combined with Eq. aggregate.  Lossless up to
+ * roundoff.  The record level rises by `cycles` (at most 8 in total).  [sync]
  * ---------------------------------------------------------------------- */
 rc_status rc_aggregate(rc_forest* f, int32_t cycles, void* stream);
 
@@ -191,21 +210,21 @@ rc_status rc_composite(rc_forest* f, const float background[3], float* d_rgba, i
 
 /* ------------------------------------------------------------------------
  * One whole frame on one GPU from device-resident inputs:
- * rc_camera_set + rc_cull + rc_cast_segments + rc_aggregate(cycles) +
- * rc_composite.  *hit_pairs (optional) receives the metric's unit count.
+ * rc_camera_set + rc_cull + rc_cast_segments(fold_levels) +
+ * rc_aggregate(cycles) + rc_composite.  *hit_pairs (optional) receives the metric's unit count.
  * ---------------------------------------------------------------------- */
-rc_status rc_render_frame(rc_forest* f, const rc_camera* cam, int32_t cycles, const float background[3],
-                          float* d_rgba, int64_t capacity_floats, int64_t* hit_pairs, void* stream);
+rc_status rc_render_frame(rc_forest* f, const rc_camera* cam, int32_t fold_levels, int32_t cycles,
+                          const float background[3], float* d_rgba, int64_t capacity_floats, int64_t* hit_pairs,
+                          void* stream);
 
 /* Instrumentation: kernel launches issued by the library since the last
  * reset, and the device time of the segment kernel(s) of the last
  * rc_cast_segments measured with CUDA events on the caller's stream. */
 int64_t rc_launch_count(int32_t reset);
 float rc_last_cast_ms(rc_forest* f);
-/* [sync] device time of one phase of the last rc_cast_segments (CUDA events on
- * the caller's stream, summed over chunk batches): 0 = whole cast,
- * 1 = intersection kernel(s), 2 = integration kernel(s) (curved path; the
- * affine path fuses both into phase 1). */
+/* [sync] device time of the last rc_cast_segments' segment kernel (CUDA
+ * events on the caller's stream): phase 0 or 1 = the kernel (intersection,
+ * integration and fold are fused), 2 = 0 (kept for ABI stability). */
 float rc_last_phase_ms(rc_forest* f, int32_t phase);
 
 #ifdef __cplusplus

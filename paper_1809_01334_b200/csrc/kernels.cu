@@ -209,6 +209,50 @@ __global__ void k_expand(const int64_t* __restrict__ off, const int64_t* __restr
   for (int64_t c = off[v]; c < off[v + 1]; ++c) chunk_elem[c] = (int32_t)v;
 }
 
+// Fold units of the curved segment kernel (row a6): every node of the fold
+// level with visible leaves -> ceil(chunks / RC_UNIT_CHUNKS) units of about
+// equal size.  Nodes are contiguous in the visible list (SFC order).
+__global__ void k_unit_count(const int32_t* __restrict__ vis, const int64_t* __restrict__ nvis_p,
+                             const int32_t* __restrict__ leaf_node, const int64_t* __restrict__ chunk_off,
+                             int32_t* __restrict__ ucnt, int32_t* __restrict__ uend) {
+  const int64_t nvis = *nvis_p;
+  const int64_t v = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (v >= nvis) return;
+  const int32_t nd = leaf_node[vis[v]];
+  if (v > 0 && leaf_node[vis[v - 1]] == nd) {
+    ucnt[v] = 0;
+    return;
+  }
+  // end of the node's visible run: first w > v with another node (monotone)
+  int64_t lo = v, hi = nvis;   // leaf_node[vis[lo]] == nd, hi is past the run
+  while (hi - lo > 1) {
+    const int64_t mid = (lo + hi) >> 1;
+    if (leaf_node[vis[mid]] == nd) lo = mid;
+    else hi = mid;
+  }
+  uend[v] = (int32_t)hi;
+  const int64_t nch = chunk_off[hi] - chunk_off[v];
+  ucnt[v] = (int32_t)((nch + RC_UNIT_CHUNKS - 1) / RC_UNIT_CHUNKS);
+}
+
+__global__ void k_unit_emit(const int32_t* __restrict__ vis, const int64_t* __restrict__ nvis_p,
+                            const int32_t* __restrict__ leaf_node, const int32_t* __restrict__ node_first,
+                            const int64_t* __restrict__ chunk_off, const int32_t* __restrict__ ucnt,
+                            const int64_t* __restrict__ uoff, const int32_t* __restrict__ uend, uint32_t key_base,
+                            Unit* __restrict__ units) {
+  const int64_t nvis = *nvis_p;
+  const int64_t v = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (v >= nvis) return;
+  const int64_t nu = ucnt[v];
+  if (nu == 0) return;
+  const int64_t c0 = chunk_off[v], nch = chunk_off[uend[v]] - c0;
+  const uint32_t key = key_base + (uint32_t)node_first[leaf_node[vis[v]]];
+  for (int64_t k = 0; k < nu; ++k) {
+    const int64_t a = c0 + nch * k / nu, b = c0 + nch * (k + 1) / nu;
+    units[uoff[v] + k] = Unit{a, (int32_t)(b - a), key};
+  }
+}
+
 // ---------------------------------------------------------------------------
 // a4 + a5 (affine trees): slab test in element reference coordinates and the
 // N-point GL rule.  One warp = one 32-pixel chunk of one element; dynamic
@@ -591,6 +635,111 @@ __global__ void __launch_bounds__(FOLD_WARPS * 32) k_fold(const rc_seg* __restri
 
 
 // ---------------------------------------------------------------------------
+// a7: one pass of the aggregation cycles.
+// Records are bucketed by pixel (k_hist / k_scatter); one warp per pixel
+// orders them by (alpha_near, key) and combines every maximal run of touching
+// records (|gap| <= tau max(1, alpha)) that lie in the same node of the target
+// level (node_of of the record's key) with Eq. aggregate, nearest first.  The
+// result is keyed by the node's first leaf.  Records of one node that do not
+// touch stay separate (safe for non-convex curved nodes).
+// ---------------------------------------------------------------------------
+__global__ void __launch_bounds__(FOLD_WARPS * 32) k_coarsen(const rc_seg* __restrict__ recs,
+                                                             const uint32_t* __restrict__ perm,
+                                                             const int64_t* __restrict__ off, int64_t npix,
+                                                             const int32_t* __restrict__ node_first, int64_t nnodes,
+                                                             uint32_t key_base, float tau, rc_seg* __restrict__ out,
+                                                             int64_t out_cap, int64_t* __restrict__ counters) {
+  extern __shared__ unsigned char smem_raw[];
+  const int warp = threadIdx.x >> 5;
+  const unsigned lane = threadIdx.x & 31;
+  uint64_t* keys = reinterpret_cast<uint64_t*>(smem_raw) + (size_t)warp * FOLD_CAP;
+  uint16_t* idxs = reinterpret_cast<uint16_t*>(reinterpret_cast<uint64_t*>(smem_raw) + (size_t)FOLD_WARPS * FOLD_CAP) +
+                   (size_t)warp * FOLD_CAP;
+  for (int64_t pix = (int64_t)blockIdx.x * FOLD_WARPS + warp; pix < npix; pix += (int64_t)gridDim.x * FOLD_WARPS) {
+    const int64_t base = off[pix];
+    const int n = (int)(off[pix + 1] - base);
+    if (n == 0) continue;
+    const uint32_t* S = perm + base;
+    if (n > FOLD_CAP) {   // rare: pass through, re-keyed by the target node
+      for (int k0 = 0; k0 < n; k0 += 32) {
+        const int k = k0 + (int)lane;
+        const int64_t slot = warp_append(&counters[CNT_AGG_OUT], k < n ? 1 : 0);
+        if (k < n) {
+          rc_seg r = recs[S[k]];
+          r.key = key_base + (uint32_t)node_first[node_of(node_first, nnodes, (int32_t)(r.key - key_base))];
+          if (slot < out_cap) out[slot] = r;
+          else atomicAdd((unsigned long long*)&counters[CNT_OVERFLOW], 1ull);
+        }
+      }
+      continue;
+    }
+    int m = 1;
+    while (m < n) m <<= 1;
+    for (int k = lane; k < m; k += 32) {
+      keys[k] = k < n ? sort_key(recs[S[k]]) : ~0ull;
+      idxs[k] = (uint16_t)k;
+    }
+    __syncwarp();
+    for (int size = 2; size <= m; size <<= 1) {
+      for (int stride = size >> 1; stride > 0; stride >>= 1) {
+        for (int k = lane; k < m; k += 32) {
+          const int p = k ^ stride;
+          if (p > k) {
+            const bool up = (k & size) == 0;
+            const uint64_t ka = keys[k], kb = keys[p];
+            if ((ka > kb) == up) {
+              keys[k] = kb;
+              keys[p] = ka;
+              const uint16_t t2 = idxs[k];
+              idxs[k] = idxs[p];
+              idxs[p] = t2;
+            }
+          }
+        }
+        __syncwarp();
+      }
+    }
+    auto anc = [&](int k) -> int64_t {
+      return node_of(node_first, nnodes, (int32_t)(recs[S[idxs[k]]].key - key_base));
+    };
+    auto is_head = [&](int k) -> bool {
+      if (k == 0) return true;
+      const rc_seg& x = recs[S[idxs[k - 1]]];
+      const rc_seg& y = recs[S[idxs[k]]];
+      if (fabsf(y.alpha_near - x.alpha_far) > tau * fmaxf(1.0f, fabsf(y.alpha_near))) return true;
+      return anc(k) != anc(k - 1);
+    };
+    for (int k0 = 0; k0 < n; k0 += 32) {
+      const int k = k0 + (int)lane;
+      const bool h = k < n && is_head(k);
+      const int64_t slot = warp_append(&counters[CNT_AGG_OUT], h ? 1 : 0);
+      if (!h) continue;
+      const rc_seg& s0 = recs[S[idxs[k]]];
+      double A = 1.0, B0 = 0.0, B1 = 0.0, B2 = 0.0;
+      float af = s0.alpha_far;
+      int q = k;
+      do {
+        const rc_seg& sq = recs[S[idxs[q]]];
+        B0 = fma(A, (double)sq.b[0], B0);
+        B1 = fma(A, (double)sq.b[1], B1);
+        B2 = fma(A, (double)sq.b[2], B2);
+        A *= (double)sq.a;
+        af = sq.alpha_far;
+        ++q;
+      } while (q < n && !is_head(q));
+      if (slot < out_cap) {
+        const float bb[3] = {(float)B0, (float)B1, (float)B2};
+        store_seg(out + slot, s0.pixel, s0.alpha_near, af, (float)A, bb,
+                  key_base + (uint32_t)node_first[anc(k)]);
+      } else {
+        atomicAdd((unsigned long long*)&counters[CNT_OVERFLOW], 1ull);
+      }
+    }
+    __syncwarp();
+  }
+}
+
+// ---------------------------------------------------------------------------
 // host launchers (kernels are launched only from this translation unit)
 // ---------------------------------------------------------------------------
 static unsigned nblk(int64_t n, int t) { return (unsigned)((n + t - 1) / t); }
@@ -622,6 +771,27 @@ cudaError_t launch_expand(const int64_t* off, const int64_t* nvis_p, int64_t nvi
                           cudaStream_t s) {
   k_expand<<<nblk(nvis, 256), 256, 0, s>>>(off, nvis_p, chunk_elem);
   ++g_launches;
+  return cudaGetLastError();
+}
+
+cudaError_t launch_units(const int32_t* vis, const int64_t* nvis_p, int64_t nvis, const int32_t* leaf_node,
+                         const int32_t* node_first, const int64_t* chunk_off, int32_t* ucnt, int64_t* uoff,
+                         int32_t* uend, int64_t* scan_tmp, uint32_t key_base, Unit* units, bool emit,
+                         cudaStream_t s) {
+  if (!emit) {
+    cudaError_t e = cudaMemsetAsync(ucnt, 0, sizeof(int32_t) * (nvis + 1), s);
+    if (e != cudaSuccess) return e;
+    if (nvis > 0) {
+      k_unit_count<<<nblk(nvis, 256), 256, 0, s>>>(vis, nvis_p, leaf_node, chunk_off, ucnt, uend);
+      ++g_launches;
+    }
+    return scan_exclusive<int32_t>(ucnt, uoff, nvis, scan_tmp, s);
+  }
+  if (nvis > 0) {
+    k_unit_emit<<<nblk(nvis, 256), 256, 0, s>>>(vis, nvis_p, leaf_node, node_first, chunk_off, ucnt, uoff, uend,
+                                                key_base, units);
+    ++g_launches;
+  }
   return cudaGetLastError();
 }
 
@@ -669,6 +839,23 @@ cudaError_t launch_hist(const rc_seg* segs, int64_t n, int32_t* cnt, int grid, c
 cudaError_t launch_scatter(const rc_seg* segs, int64_t n, const int64_t* off, int32_t* cursor, uint32_t* out,
                            int grid, cudaStream_t s) {
   k_scatter<<<grid, 256, 0, s>>>(segs, n, off, cursor, out);
+  ++g_launches;
+  return cudaGetLastError();
+}
+
+cudaError_t launch_coarsen(const rc_seg* recs, const uint32_t* perm, const int64_t* off, int64_t npix,
+                           const int32_t* node_first, int64_t nnodes, uint32_t key_base, float tau, rc_seg* out,
+                           int64_t out_cap, int64_t* counters, int max_grid, cudaStream_t s) {
+  static bool attr = false;
+  size_t smem = (size_t)FOLD_WARPS * FOLD_CAP * (sizeof(uint64_t) + sizeof(uint16_t));
+  if (!attr) {
+    cudaError_t e = cudaFuncSetAttribute(k_coarsen, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    if (e != cudaSuccess) return e;
+    attr = true;
+  }
+  int grid = (int)std::min<int64_t>((npix + FOLD_WARPS - 1) / FOLD_WARPS, (int64_t)max_grid);
+  k_coarsen<<<grid, FOLD_WARPS * 32, smem, s>>>(recs, perm, off, npix, node_first, nnodes, key_base, tau, out, out_cap,
+                                                counters);
   ++g_launches;
   return cudaGetLastError();
 }

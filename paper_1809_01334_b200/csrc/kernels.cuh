@@ -17,13 +17,20 @@ cudaError_t launch_cast_affine(const CamConst& cc, const TreeConst* trees, DevLe
                                const Rect16* vrect, const int64_t* chunk_off, const int32_t* chunk_elem,
                                int64_t nchunks, uint32_t key_base, rc_seg* segs, int64_t seg_cap, int32_t* hits_pp,
                                int64_t* counters, int grid, cudaStream_t s);
-cudaError_t launch_isect_curved(const CamConst& cc, const TreeConst* trees, DevLeafView L, const int32_t* vis,
-                                const Rect16* vrect, const int64_t* chunk_off, const int32_t* chunk_elem,
-                                int64_t c_begin, int64_t c_end, void* items, int64_t item_cap, int32_t* hits_pp,
-                                int64_t* counters, int grid, cudaStream_t s);
-cudaError_t launch_integ_curved(const CamConst& cc, const TreeConst* trees, DevLeafView L, int P, const int32_t* vis,
-                                const void* items, int64_t nitems, uint32_t key_base, rc_seg* segs, int64_t seg_base,
-                                int64_t* counters, int grid, cudaStream_t s);
+cudaError_t launch_units(const int32_t* vis, const int64_t* nvis_p, int64_t nvis, const int32_t* leaf_node,
+                         const int32_t* node_first, const int64_t* chunk_off, int32_t* ucnt, int64_t* uoff,
+                         int32_t* uend, int64_t* scan_tmp, uint32_t key_base, Unit* units, bool emit,
+                         cudaStream_t s);
+cudaError_t launch_cast_curved(const CamConst& cc, const TreeConst* trees, DevLeafView L, int P, const int32_t* vis,
+                               const Rect16* vrect, const int64_t* chunk_off, const int32_t* chunk_elem,
+                               const Unit* units, int64_t nunits, int64_t nchunks, int fold, uint32_t key_base,
+                               void* scratch, rc_seg* out, int64_t out_cap, int32_t* hits_pp, int64_t* counters,
+                               int grid, cudaStream_t s);
+size_t cast_curved_scratch_per_cta();
+int cast_curved_ctas_per_sm();
+cudaError_t launch_coarsen(const rc_seg* recs, const uint32_t* perm, const int64_t* off, int64_t npix,
+                           const int32_t* node_first, int64_t nnodes, uint32_t key_base, float tau, rc_seg* out,
+                           int64_t out_cap, int64_t* counters, int max_grid, cudaStream_t s);
 cudaError_t launch_pack(const rc_seg* segs, const int64_t* nseg_p, int W, int tw, int th, int tiles_x, int nranks,
                         int64_t* counts, const int64_t* dest_off, int64_t* cursor, rc_seg* out, int grid, bool count,
                         cudaStream_t s);

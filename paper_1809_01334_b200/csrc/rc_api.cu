@@ -152,6 +152,7 @@ extern "C" rc_status rc_forest_create(const rc_forest_desc* d, void* stream, rc_
     memcpy(f->h_trees[k].lagr, d->tree_ctrl + (size_t)k * n1 * n1 * n1 * 3, sizeof(double) * n1 * n1 * n1 * 3);
   if ((e = cudaEventCreate(&f->ev0)) || (e = cudaEventCreate(&f->ev1))) return cleanup(RC_ERR_CUDA, "event");
   if ((e = cudaStreamSynchronize(s))) return cleanup(RC_ERR_CUDA, "sync");
+  if ((e = build_node_levels(f, s))) return cleanup(RC_ERR_CUDA, "node levels");
   *out = f;
   return RC_OK;
 }
@@ -161,9 +162,12 @@ extern "C" rc_status rc_forest_destroy(rc_forest* f) {
   void* ptrs[] = {f->d_anchor, f->d_tree, f->d_level, f->d_field, f->d_flag, f->d_rect_all, f->d_scan,
                   f->d_vis, f->d_vis_rect, f->d_chunk_off, f->d_counters, f->d_trees, f->d_cam,
                   f->d_scan_tmp, f->d_chunk_elem, f->d_segs, f->d_hits_pp, f->d_pix_cnt, f->d_pix_off,
-                  f->d_perm, f->d_send, f->d_items};
+                  f->d_perm, f->d_send, f->d_items, f->d_leaf_node, f->d_ucnt, f->d_uend, f->d_units,
+                  f->d_scratch, f->d_segs2, f->d_uoff};
   for (void* p : ptrs)
     if (p) cudaFree(p);
+  for (int c = 0; c <= RC_NODE_LEVELS; ++c)
+    if (f->d_node_first[c]) cudaFree(f->d_node_first[c]);
   if (f->ev0) cudaEventDestroy(f->ev0);
   if (f->ev1) cudaEventDestroy(f->ev1);
   for (int k = 0; k < 4; ++k)
@@ -451,103 +455,103 @@ static int sm_count() {
   return sms;
 }
 
-extern "C" rc_status rc_cast_segments(rc_forest* f, void* stream) {
+static rc_status aggregate_to(rc_forest* f, int level, cudaStream_t s);
+
+extern "C" rc_status rc_cast_segments(rc_forest* f, int32_t fold_levels, void* stream) {
   if (!f) return fail(RC_ERR_INVALID_ARG, "rc_cast_segments: null forest");
   if (!f->have_cull) return fail(RC_ERR_STATE, "rc_cast_segments before rc_cull");
+  if (fold_levels < 0 || fold_levels > RC_NODE_LEVELS)
+    return fail(RC_ERR_INVALID_ARG, "fold_levels must be in [0, %d]", RC_NODE_LEVELS);
+  if (!f->all_affine && f->R != 2) return fail(RC_ERR_INVALID_ARG, "non-affine trees require geom_degree 2");
   cudaStream_t s = (cudaStream_t)stream;
   const int64_t n = f->n;
-  // one small readback to size the chunk map and the segment buffer
-  int64_t hv[2];
+  // one small readback to size the chunk map, the units and the record buffer
+  int64_t hv[3];
   CU(cudaMemcpyAsync(&hv[0], f->d_scan + n, sizeof(int64_t), cudaMemcpyDeviceToHost, s));
   CU(cudaMemcpyAsync(&hv[1], f->d_chunk_off + n, sizeof(int64_t), cudaMemcpyDeviceToHost, s));
-  int64_t cand = 0;
-  CU(cudaMemcpyAsync(&cand, f->d_counters + CNT_CANDIDATES, sizeof(int64_t), cudaMemcpyDeviceToHost, s));
+  CU(cudaMemcpyAsync(&hv[2], f->d_counters + CNT_CANDIDATES, sizeof(int64_t), cudaMemcpyDeviceToHost, s));
   CU(cudaStreamSynchronize(s));
   f->h_num_visible = hv[0];
   f->h_chunks = hv[1];
-  f->h_candidates = cand;
+  f->h_candidates = hv[2];
+  const int64_t cand = hv[2], nvis = hv[0];
   const int64_t npix = (int64_t)f->cc.W * f->cc.H;
   CU(grow(&f->d_chunk_elem, &f->chunk_cap, std::max<int64_t>(f->h_chunks, 1)));
-  // R=1/affine: at most one segment per candidate; curved: start at half the candidates,
-  // grown between chunk batches when needed
-  int64_t need = f->all_affine ? cand + 1024 : std::max<int64_t>(f->h_seg_total, cand / 2) + 4096;
-  CU(grow(&f->d_segs, &f->seg_cap, need));
   CU(grow(&f->d_hits_pp, &f->pix_cap, npix));
-  CU(cudaMemsetAsync(f->d_hits_pp, 0, sizeof(int32_t) * npix, s));
-  CU(cudaMemsetAsync(f->d_counters + CNT_SEGS, 0, sizeof(int64_t) * 3, s));
-  CU(cudaMemsetAsync(f->d_counters + CNT_OVERFLOW, 0, sizeof(int64_t) * 3, s));
-  if (f->h_num_visible > 0) {
-    CU(launch_expand(f->d_chunk_off, f->d_scan + n, f->h_num_visible, f->d_chunk_elem, s));
-  }
-  int grid = sm_count() * 8;
-  CU(cudaEventRecord(f->ev0, s));
-  if (f->h_chunks > 0) {
-    if (f->all_affine) {
-      CU(launch_cast_affine(f->cc, f->d_trees, leaf_view(f), f->P, f->d_vis, f->d_vis_rect, f->d_chunk_off,
-                            f->d_chunk_elem, f->h_chunks, (uint32_t)f->first_global, f->d_segs, f->seg_cap,
-                            f->d_hits_pp, f->d_counters, grid, s));
-    } else {
-      if (f->R != 2) return fail(RC_ERR_INVALID_ARG, "non-affine trees require geom_degree 2");
-      // curved path: chunk batches of intersection -> items -> integration
-      const int64_t batch = 1 << 20;
-      const int64_t nb = std::min<int64_t>(f->h_chunks, batch);
-      const int64_t icap = nb * RC_CHUNK * 2;   // at most two segments per pair
-      if (f->items_cap < icap) {
-        if (f->d_items) cudaFree(f->d_items);
-        f->d_items = nullptr;
-        f->items_cap = 0;
-        CU(cudaMalloc(&f->d_items, (size_t)icap * 64));
-        f->items_cap = icap;
-      }
-      for (int k = 0; k < 4; ++k)
-        if (!f->evb[k]) CU(cudaEventCreate(&f->evb[k]));
-      f->phase_ms[1] = f->phase_ms[2] = 0.0f;
-      int64_t seg_total = 0;
-      for (int64_t c0 = 0; c0 < f->h_chunks; c0 += batch) {
-        const int64_t c1 = std::min(c0 + batch, f->h_chunks);
-        CU(cudaMemsetAsync(f->d_counters + CNT_WORK, 0, sizeof(int64_t), s));
-        CU(cudaMemsetAsync(f->d_counters + CNT_ITEMS, 0, sizeof(int64_t), s));
-        CU(cudaEventRecord(f->evb[0], s));
-        CU(launch_isect_curved(f->cc, f->d_trees, leaf_view(f), f->d_vis, f->d_vis_rect, f->d_chunk_off,
-                               f->d_chunk_elem, c0, c1, f->d_items, f->items_cap, f->d_hits_pp, f->d_counters,
-                               sm_count() * 4, s));
-        CU(cudaEventRecord(f->evb[1], s));
-        int64_t ni = 0;
-        CU(cudaMemcpyAsync(&ni, f->d_counters + CNT_ITEMS, sizeof(int64_t), cudaMemcpyDeviceToHost, s));
-        CU(cudaStreamSynchronize(s));
-        float ms = 0.0f;
-        CU(cudaEventElapsedTime(&ms, f->evb[0], f->evb[1]));
-        f->phase_ms[1] += ms;
-        if (ni > f->items_cap) return fail(RC_ERR_CAPACITY, "intersection items overflow");
-        if (seg_total + ni > f->seg_cap) {   // grow, keeping the records of earlier batches
-          int64_t ncap = std::max<int64_t>(seg_total + ni + (seg_total + ni) / 4, 1024);
-          rc_seg* nseg = nullptr;
-          CU(cudaMalloc((void**)&nseg, sizeof(rc_seg) * (size_t)ncap));
-          if (seg_total > 0)
-            CU(cudaMemcpyAsync(nseg, f->d_segs, sizeof(rc_seg) * (size_t)seg_total, cudaMemcpyDeviceToDevice, s));
-          CU(cudaStreamSynchronize(s));
-          if (f->d_segs) cudaFree(f->d_segs);
-          f->d_segs = nseg;
-          f->seg_cap = ncap;
-        }
-        if (ni > 0) {
-          CU(cudaEventRecord(f->evb[2], s));
-          CU(launch_integ_curved(f->cc, f->d_trees, leaf_view(f), f->P, f->d_vis, f->d_items, ni,
-                                 (uint32_t)f->first_global, f->d_segs, seg_total, f->d_counters, sm_count() * 3, s));
-          CU(cudaEventRecord(f->evb[3], s));
-          CU(cudaEventSynchronize(f->evb[3]));
-          CU(cudaEventElapsedTime(&ms, f->evb[2], f->evb[3]));
-          f->phase_ms[2] += ms;
-        }
-        seg_total += ni;
-      }
-      f->h_seg_total = seg_total;
-      CU(cudaMemcpyAsync(f->d_counters + CNT_SEGS, &f->h_seg_total, sizeof(int64_t), cudaMemcpyHostToDevice, s));
+  if (nvis > 0) CU(launch_expand(f->d_chunk_off, f->d_scan + n, nvis, f->d_chunk_elem, s));
+  const bool curved = !f->all_affine;
+  const uint32_t key_base = (uint32_t)f->first_global;
+  // fold units (curved path): nodes of the fold level cut into <= RC_UNIT_CHUNKS chunks
+  int64_t nunits = (f->h_chunks + RC_UNIT_CHUNKS - 1) / RC_UNIT_CHUNKS;
+  if (curved && fold_levels > 0 && nvis > 0) {
+    CU(build_leaf_node(f, fold_levels, s));
+    if (!f->d_ucnt) {
+      CU(cudaMalloc((void**)&f->d_ucnt, sizeof(int32_t) * (n + 1)));
+      CU(cudaMalloc((void**)&f->d_uoff, sizeof(int64_t) * (n + 1)));
+      CU(cudaMalloc((void**)&f->d_uend, sizeof(int32_t) * (n + 1)));
     }
+    CU(launch_units(f->d_vis, f->d_scan + n, nvis, f->d_leaf_node, f->d_node_first[fold_levels], f->d_chunk_off,
+                    f->d_ucnt, f->d_uoff, f->d_uend, f->d_scan_tmp, key_base, nullptr, false, s));
+    CU(cudaMemcpyAsync(&nunits, f->d_uoff + nvis, sizeof(int64_t), cudaMemcpyDeviceToHost, s));
+    CU(cudaStreamSynchronize(s));
+    CU(grow(&f->d_units, &f->units_cap, std::max<int64_t>(nunits, 1)));
+    CU(launch_units(f->d_vis, f->d_scan + n, nvis, f->d_leaf_node, f->d_node_first[fold_levels], f->d_chunk_off,
+                    f->d_ucnt, f->d_uoff, f->d_uend, f->d_scan_tmp, key_base, f->d_units, true, s));
   }
-  CU(cudaEventRecord(f->ev1, s));
+  f->h_units = curved ? nunits : 0;
+  const int grid_curved = sm_count() * cast_curved_ctas_per_sm();
+  if (curved && !f->d_scratch) {
+    f->scratch_bytes = cast_curved_scratch_per_cta() * (size_t)grid_curved;
+    CU(cudaMalloc(&f->d_scratch, f->scratch_bytes));
+  }
+  // record capacity: the previous frame's count, else an estimate; a too
+  // small buffer is grown to the exact count and the cast repeated
+  int64_t est = curved ? (fold_levels > 0 ? cand / 8 : cand / 2 + cand / 8) : cand;
+  int64_t need = std::max<int64_t>(f->h_seg_total + f->h_seg_total / 8, est) + 4096;
+  CU(grow(&f->d_segs, &f->seg_cap, need));
+  for (int attempt = 0; attempt < 2; ++attempt) {
+    CU(cudaMemsetAsync(f->d_hits_pp, 0, sizeof(int32_t) * npix, s));
+    CU(cudaMemsetAsync(f->d_counters + CNT_SEGS, 0, sizeof(int64_t) * 3, s));
+    CU(cudaMemsetAsync(f->d_counters + CNT_OVERFLOW, 0, sizeof(int64_t) * 3, s));
+    CU(cudaMemsetAsync(f->d_counters + CNT_UNITS, 0, sizeof(int64_t) * 4, s));
+    CU(cudaEventRecord(f->ev0, s));
+    if (f->h_chunks > 0) {
+      if (!curved) {
+        CU(launch_cast_affine(f->cc, f->d_trees, leaf_view(f), f->P, f->d_vis, f->d_vis_rect, f->d_chunk_off,
+                              f->d_chunk_elem, f->h_chunks, key_base, f->d_segs, f->seg_cap, f->d_hits_pp,
+                              f->d_counters, sm_count() * 8, s));
+      } else {
+        CU(launch_cast_curved(f->cc, f->d_trees, leaf_view(f), f->P, f->d_vis, f->d_vis_rect, f->d_chunk_off,
+                              f->d_chunk_elem, fold_levels > 0 ? f->d_units : nullptr, nunits, f->h_chunks,
+                              fold_levels, key_base, f->d_scratch, f->d_segs, f->seg_cap, f->d_hits_pp,
+                              f->d_counters, grid_curved, s));
+      }
+    }
+    CU(cudaEventRecord(f->ev1, s));
+    int64_t c[2];
+    CU(cudaMemcpyAsync(c, f->d_counters + CNT_SEGS, sizeof(int64_t), cudaMemcpyDeviceToHost, s));
+    CU(cudaMemcpyAsync(c + 1, f->d_counters + CNT_OVERFLOW, sizeof(int64_t), cudaMemcpyDeviceToHost, s));
+    CU(cudaStreamSynchronize(s));
+    f->h_seg_total = c[0];
+    if (c[0] <= f->seg_cap && c[1] == 0) break;
+    if (attempt == 1) return fail(RC_ERR_CAPACITY, "segment records overflow after regrowth");
+    CU(grow(&f->d_segs, &f->seg_cap, c[0] + c[0] / 16 + 4096));
+  }
+  float ms = 0.0f;
+  CU(cudaEventElapsedTime(&ms, f->ev0, f->ev1));
+  f->phase_ms[1] = ms;
+  f->phase_ms[2] = 0.0f;
+  f->rec_level = 0;
+  if (!curved) f->h_raw_affine = f->h_seg_total;
   f->timed = true;
   f->have_cast = true;
+  if (curved) {
+    f->rec_level = fold_levels;
+  } else if (fold_levels > 0) {
+    // affine path: segments are written per leaf; fold them to the node level
+    rc_status st = aggregate_to(f, fold_levels, s);
+    if (st) return st;
+  }
   return RC_OK;
 }
 
@@ -561,9 +565,8 @@ extern "C" float rc_last_cast_ms(rc_forest* f) {
 
 extern "C" float rc_last_phase_ms(rc_forest* f, int32_t phase) {
   if (!f || !f->timed) return -1.0f;
-  if (phase == 0) return rc_last_cast_ms(f);
-  if (f->all_affine) return phase == 1 ? rc_last_cast_ms(f) : 0.0f;
-  if (phase == 1 || phase == 2) return f->phase_ms[phase];
+  if (phase == 0 || phase == 1) return rc_last_cast_ms(f);
+  if (phase == 2) return 0.0f;
   return -1.0f;
 }
 
@@ -580,6 +583,10 @@ extern "C" rc_status rc_segments_get(rc_forest* f, rc_segments* out, void* strea
   out->newton_failures = c[CNT_NEWTON_FAIL];
   out->face_failures = c[CNT_FACE_FAIL];
   out->num_visible = f->h_num_visible;
+  out->raw_segments = f->all_affine ? f->h_raw_affine : c[CNT_RAW];
+  out->level = f->rec_level;
+  out->units = f->h_units;
+  out->unfolded_units = c[CNT_UNFOLDED];
   out->segs = f->d_segs;
   out->hits_per_pixel = f->d_hits_pp;
   if (c[CNT_OVERFLOW] > 0)
@@ -709,21 +716,83 @@ extern "C" rc_status rc_composite(rc_forest* f, const float background[3], float
   return rc_composite_tiles(f, &t, nullptr, 0, background, d_rgba, capacity_floats, stream);
 }
 
+// One aggregation pass: the current records (node level f->rec_level) are
+// combined per (node of `level`, pixel) where they touch (k_coarsen).
+static rc_status aggregate_to(rc_forest* f, int level, cudaStream_t s) {
+  if (level <= f->rec_level) return RC_OK;
+  int64_t nrec = 0;
+  CU(cudaMemcpyAsync(&nrec, f->d_counters + CNT_SEGS, sizeof(int64_t), cudaMemcpyDeviceToHost, s));
+  CU(cudaStreamSynchronize(s));
+  nrec = std::min(nrec, f->seg_cap);
+  const int64_t npix = (int64_t)f->cc.W * f->cc.H;
+  if (nrec >= (int64_t)UINT32_MAX) return fail(RC_ERR_CAPACITY, "more than 2^32 records in one aggregation");
+  if (!f->d_pix_cnt || f->pix_cnt_cap < npix) {
+    if (f->d_pix_cnt) cudaFree(f->d_pix_cnt);
+    if (f->d_pix_off) cudaFree(f->d_pix_off);
+    f->d_pix_cnt = nullptr;
+    f->d_pix_off = nullptr;
+    CU(cudaMalloc((void**)&f->d_pix_cnt, sizeof(int32_t) * npix));
+    CU(cudaMalloc((void**)&f->d_pix_off, sizeof(int64_t) * (npix + 1)));
+    f->pix_cnt_cap = npix;
+  }
+  int64_t need_tmp = (int64_t)scan_tmp_size(npix + 1) + 128;
+  if (need_tmp > f->scan_tmp_cap) CU(grow(&f->d_scan_tmp, &f->scan_tmp_cap, need_tmp));
+  CU(grow(&f->d_perm, &f->perm_cap, std::max<int64_t>(nrec, 1)));
+  CU(grow(&f->d_segs2, &f->seg2_cap, std::max<int64_t>(nrec, 1)));
+  const int grid = sm_count() * 8;
+  CU(cudaMemsetAsync(f->d_pix_cnt, 0, sizeof(int32_t) * npix, s));
+  if (nrec > 0) CU(launch_hist(f->d_segs, nrec, f->d_pix_cnt, grid, s));
+  CU(scan_exclusive<int32_t>(f->d_pix_cnt, f->d_pix_off, npix, f->d_scan_tmp, s));
+  CU(cudaMemsetAsync(f->d_pix_cnt, 0, sizeof(int32_t) * npix, s));
+  if (nrec > 0) CU(launch_scatter(f->d_segs, nrec, f->d_pix_off, f->d_pix_cnt, f->d_perm, grid, s));
+  CU(cudaMemsetAsync(f->d_counters + CNT_AGG_OUT, 0, sizeof(int64_t), s));
+  CU(launch_coarsen(f->d_segs, f->d_perm, f->d_pix_off, npix, f->d_node_first[level], f->n_nodes[level],
+                    (uint32_t)f->first_global, 1e-6f, f->d_segs2, f->seg2_cap, f->d_counters, sm_count() * 16, s));
+  int64_t nout = 0;
+  CU(cudaMemcpyAsync(&nout, f->d_counters + CNT_AGG_OUT, sizeof(int64_t), cudaMemcpyDeviceToHost, s));
+  CU(cudaMemcpyAsync(f->d_counters + CNT_SEGS, f->d_counters + CNT_AGG_OUT, sizeof(int64_t),
+                     cudaMemcpyDeviceToDevice, s));
+  CU(cudaStreamSynchronize(s));
+  if (nout > f->seg2_cap) return fail(RC_ERR_CAPACITY, "aggregation output overflow");
+  std::swap(f->d_segs, f->d_segs2);
+  std::swap(f->seg_cap, f->seg2_cap);
+  f->rec_level = level;
+  f->h_seg_total = nout;
+  return RC_OK;
+}
+
 extern "C" rc_status rc_aggregate(rc_forest* f, int32_t cycles, void* stream) {
   if (!f) return fail(RC_ERR_INVALID_ARG, "rc_aggregate: null forest");
   if (cycles < 0) return fail(RC_ERR_INVALID_ARG, "cycles must be >= 0");
   if (cycles == 0) return RC_OK;
   if (!f->have_cast) return fail(RC_ERR_STATE, "rc_aggregate before rc_cast_segments");
-  (void)stream;
-  return fail(RC_ERR_STATE, "rc_aggregate: coarsening cycles not built yet");
+  if (f->rec_level + cycles > RC_NODE_LEVELS)
+    return fail(RC_ERR_INVALID_ARG, "records at level %d: at most %d more cycles", f->rec_level,
+                RC_NODE_LEVELS - f->rec_level);
+  return aggregate_to(f, f->rec_level + cycles, (cudaStream_t)stream);
 }
 
-extern "C" rc_status rc_render_frame(rc_forest* f, const rc_camera* cam, int32_t cycles, const float background[3],
-                                     float* d_rgba, int64_t capacity_floats, int64_t* hit_pairs, void* stream) {
+extern "C" rc_status rc_node_table(rc_forest* f, int32_t level, int32_t* d_first, int64_t capacity, int64_t* count,
+                                   void* stream) {
+  if (!f || !count) return fail(RC_ERR_INVALID_ARG, "rc_node_table: null argument");
+  if (level < 1 || level > RC_NODE_LEVELS) return fail(RC_ERR_INVALID_ARG, "level must be in [1, %d]", RC_NODE_LEVELS);
+  *count = f->n_nodes[level];
+  if (f->n_nodes[level] > capacity) return fail(RC_ERR_CAPACITY, "rc_node_table: capacity too small");
+  cudaStream_t s = (cudaStream_t)stream;
+  if (d_first && f->n_nodes[level] > 0)
+    CU(cudaMemcpyAsync(d_first, f->d_node_first[level], sizeof(int32_t) * f->n_nodes[level],
+                       cudaMemcpyDeviceToDevice, s));
+  CU(cudaStreamSynchronize(s));
+  return RC_OK;
+}
+
+extern "C" rc_status rc_render_frame(rc_forest* f, const rc_camera* cam, int32_t fold_levels, int32_t cycles,
+                                     const float background[3], float* d_rgba, int64_t capacity_floats,
+                                     int64_t* hit_pairs, void* stream) {
   rc_status st;
   if ((st = rc_camera_set(f, cam, stream))) return st;
   if ((st = rc_cull(f, stream))) return st;
-  if ((st = rc_cast_segments(f, stream))) return st;
+  if ((st = rc_cast_segments(f, fold_levels, stream))) return st;
   if (cycles > 0 && (st = rc_aggregate(f, cycles, stream))) return st;
   if ((st = rc_composite(f, background, d_rgba, capacity_floats, stream))) return st;
   if (hit_pairs) {

@@ -10,6 +10,27 @@
 #define RC_MAX_TREES 4096
 #define RC_MAXLEVEL 18
 #define RC_CHUNK 32         // candidate pairs per warp work item (one element)
+#define RC_NODE_LEVELS 8    // coarsening levels of the node tables (fold + aggregation cycles)
+#define RC_UNIT_CHUNKS 128  // chunks per fold unit of the curved segment kernel (<= 4096 pairs)
+
+// Fold unit of the curved segment kernel (row a6): a contiguous chunk range
+// inside one node of the fold level (or any 128 chunks when not folding).
+struct __align__(16) Unit {
+  int64_t chunk_begin;
+  int32_t nchunks;
+  uint32_t key;                 // global SFC index of the node's first leaf
+};
+
+// node k of a level owns leaves [first[k], first[k+1]); returns k for leaf e
+__device__ __forceinline__ int64_t node_of(const int32_t* __restrict__ first, int64_t nnodes, int32_t e) {
+  int64_t lo = 0, hi = nnodes;   // invariant first[lo] <= e < first[hi]
+  while (hi - lo > 1) {
+    const int64_t mid = (lo + hi) >> 1;
+    if (first[mid] <= e) lo = mid;
+    else hi = mid;
+  }
+  return lo;
+}
 
 // Camera constants (host fp64 preprocessing, rc_camera_set).
 struct CamConst {
@@ -101,6 +122,25 @@ struct rc_forest {
   void* d_items = nullptr;
   int64_t items_cap = 0;
   int64_t h_seg_total = 0;
+  int64_t h_raw_affine = 0;        // affine path: segments before folding
+  // coarsening hierarchy (nodes.cu): node tables of levels 1..RC_NODE_LEVELS
+  int32_t* d_node_first[RC_NODE_LEVELS + 1] = {};
+  int64_t n_nodes[RC_NODE_LEVELS + 1] = {};
+  int32_t* d_leaf_node = nullptr;  // per-leaf node index at level leaf_node_level
+  int leaf_node_level = -1;
+  int rec_level = 0;               // node level of the current records (0 = leaves)
+  // fold units of the curved kernel
+  int32_t* d_ucnt = nullptr;       // [n+1] units per visible leaf (node starts only)
+  int64_t* d_uoff = nullptr;       // [n+1] exclusive scan of d_ucnt
+  int32_t* d_uend = nullptr;       // [n]
+  Unit* d_units = nullptr;
+  int64_t units_cap = 0;
+  int64_t h_units = 0;
+  void* d_scratch = nullptr;       // per-CTA item / segment / key scratch of the fused kernel
+  size_t scratch_bytes = 0;
+  // aggregation output (ping-pong with d_segs)
+  rc_seg* d_segs2 = nullptr;
+  int64_t seg2_cap = 0;
   // timing
   cudaEvent_t ev0 = nullptr, ev1 = nullptr;
   cudaEvent_t evb[4] = {nullptr, nullptr, nullptr, nullptr};
@@ -119,6 +159,10 @@ enum {
   CNT_FACE_FAIL = 6,   // face-root Newton non-convergence (diagnostic)
   CNT_ITEMS = 7,       // curved path: (pair, segment) items of the current batch
   CNT_SEND = 8,        // [8..8+64) per-rank cursors for pack
+  CNT_UNITS = 72,      // dynamic unit counter of the fused curved kernel
+  CNT_RAW = 73,        // segments before folding
+  CNT_UNFOLDED = 74,   // units whose segments exceeded the on-chip sort (emitted unfolded)
+  CNT_AGG_OUT = 75,    // records written by an aggregation pass
   CNT_TOTAL = 80
 };
 
@@ -130,6 +174,8 @@ size_t scan_tmp_size(int64_t n);
 }  // namespace rc
 
 namespace rc {
+cudaError_t build_node_levels(rc_forest* f, cudaStream_t s);
+cudaError_t build_leaf_node(rc_forest* f, int c, cudaStream_t s);
 template <typename Tin>
 cudaError_t scan_exclusive(const Tin* in, int64_t* out, int64_t n, int64_t* tmp, cudaStream_t s);
 }  // namespace rc

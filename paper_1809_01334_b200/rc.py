@@ -47,7 +47,8 @@ class CameraDesc(C.Structure):
 class Segments(C.Structure):
     _fields_ = [("count", C.c_int64), ("candidates", C.c_int64), ("hit_pairs", C.c_int64),
                 ("newton_failures", C.c_int64), ("face_failures", C.c_int64), ("num_visible", C.c_int64),
-                ("segs", C.c_void_p),
+                ("raw_segments", C.c_int64), ("level", C.c_int64), ("units", C.c_int64),
+                ("unfolded_units", C.c_int64), ("segs", C.c_void_p),
                 ("hits_per_pixel", C.c_void_p)]
 
 
@@ -59,7 +60,7 @@ SEG_BYTES = 32
 EXPORTS = ["rc_last_error", "rc_version", "rc_forest_create", "rc_forest_destroy", "rc_camera_set", "rc_cull",
            "rc_cull_result", "rc_cast_segments", "rc_segments_get", "rc_aggregate", "rc_pack_tiles",
            "rc_composite_tiles", "rc_composite", "rc_render_frame", "rc_launch_count", "rc_last_cast_ms",
-           "rc_last_phase_ms"]
+           "rc_last_phase_ms", "rc_node_table"]
 
 _lib = None
 
@@ -80,13 +81,14 @@ def lib():
     L.rc_camera_set.argtypes = [vp, C.POINTER(CameraDesc), vp]
     L.rc_cull.argtypes = [vp, vp]
     L.rc_cull_result.argtypes = [vp, vp, i64, C.POINTER(i64), vp]
-    L.rc_cast_segments.argtypes = [vp, vp]
+    L.rc_cast_segments.argtypes = [vp, i32, vp]
+    L.rc_node_table.argtypes = [vp, i32, vp, i64, C.POINTER(i64), vp]
     L.rc_segments_get.argtypes = [vp, C.POINTER(Segments), vp]
     L.rc_aggregate.argtypes = [vp, i32, vp]
     L.rc_pack_tiles.argtypes = [vp, C.POINTER(Tiling), vp, C.POINTER(vp), vp]
     L.rc_composite_tiles.argtypes = [vp, C.POINTER(Tiling), vp, i64, vp, vp, i64, vp]
     L.rc_composite.argtypes = [vp, vp, vp, i64, vp]
-    L.rc_render_frame.argtypes = [vp, C.POINTER(CameraDesc), i32, vp, vp, i64, C.POINTER(i64), vp]
+    L.rc_render_frame.argtypes = [vp, C.POINTER(CameraDesc), i32, i32, vp, vp, i64, C.POINTER(i64), vp]
     L.rc_launch_count.argtypes = [i32]
     L.rc_launch_count.restype = i64
     L.rc_last_cast_ms.argtypes = [vp]
@@ -223,8 +225,21 @@ class Forest:
         _check(lib().rc_cull_result(self.h, C.c_void_p(buf.data_ptr()), self.n, C.byref(cnt), _stream(stream)))
         return buf[:cnt.value]
 
-    def cast_segments(self, stream=None):
-        _check(lib().rc_cast_segments(self.h, _stream(stream)))
+    def cast_segments(self, fold_levels=0, stream=None):
+        """fold_levels = c: records per (node of coarsening level c, pixel) (row a6)."""
+        _check(lib().rc_cast_segments(self.h, int(fold_levels), _stream(stream)))
+
+    def node_table(self, level, stream=None):
+        """Local first-leaf index of every node of coarsening level `level`."""
+        import torch
+        cnt = C.c_int64()
+        st = lib().rc_node_table(self.h, int(level), None, 0, C.byref(cnt), _stream(stream))
+        if st not in (RC_OK, RC_ERR_CAPACITY):
+            _check(st)
+        buf = torch.empty(max(cnt.value, 1), dtype=torch.int32, device="cuda")
+        _check(lib().rc_node_table(self.h, int(level), C.c_void_p(buf.data_ptr()), buf.numel(), C.byref(cnt),
+                                   _stream(stream)))
+        return buf[:cnt.value]
 
     def segments(self, stream=None):
         s = Segments()
@@ -233,7 +248,8 @@ class Forest:
         hpp = device_view(s.hits_per_pixel, (self.H, self.W), "<i4")
         return {"count": s.count, "candidates": s.candidates, "hit_pairs": s.hit_pairs,
                 "newton_failures": s.newton_failures, "face_failures": s.face_failures,
-                "num_visible": s.num_visible, "raw": raw,
+                "num_visible": s.num_visible, "raw": raw, "raw_segments": s.raw_segments, "level": s.level,
+                "units": s.units, "unfolded_units": s.unfolded_units,
                 "hits_per_pixel": hpp}
 
     def aggregate(self, cycles, stream=None):
@@ -276,7 +292,7 @@ class Forest:
                                         _stream(stream)))
         return out, mine
 
-    def render_frame(self, cam, cycles=0, background=(0.0, 0.0, 0.0), out=None, stream=None):
+    def render_frame(self, cam, fold_levels=0, cycles=0, background=(0.0, 0.0, 0.0), out=None, stream=None):
         import torch
         self.cam = cam
         self.W, self.H = int(cam.width), int(cam.height)
@@ -285,8 +301,8 @@ class Forest:
         d = camera_desc(cam)
         hp = C.c_int64()
         bg = (C.c_float * 3)(*background)
-        _check(lib().rc_render_frame(self.h, C.byref(d), int(cycles), bg, C.c_void_p(out.data_ptr()), out.numel(),
-                                     C.byref(hp), _stream(stream)))
+        _check(lib().rc_render_frame(self.h, C.byref(d), int(fold_levels), int(cycles), bg,
+                                     C.c_void_p(out.data_ptr()), out.numel(), C.byref(hp), _stream(stream)))
         return out, hp.value
 
     def last_cast_ms(self):

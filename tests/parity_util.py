@@ -4,22 +4,25 @@ import numpy as np
 import oracle
 
 
-def gpu_run(scene, background=(0.0, 0.0, 0.0), device_copy=False):
+def gpu_run(scene, background=(0.0, 0.0, 0.0), device_copy=False, fold=0, cycles=0):
     import torch
     from paper_1809_01334_b200 import rc
     f = rc.Forest.from_scene(scene, device_copy=device_copy)
     f.camera_set(scene.camera)
     f.cull()
     vis = f.cull_result().cpu().numpy()
-    f.cast_segments()
+    f.cast_segments(fold)
+    if cycles:
+        f.aggregate(cycles)
     segs = f.segments()
     raw = segs["raw"].cpu().numpy().copy()
     hpp = segs["hits_per_pixel"].cpu().numpy().copy()
     img = f.composite(background).cpu().numpy().copy()
     torch.cuda.synchronize()
     out = dict(visible=vis, raw=raw, hits_per_pixel=hpp, rgba=img.reshape(-1, 4), count=segs["count"],
-               candidates=segs["candidates"], hit_pairs=segs["hit_pairs"], newton_failures=segs["newton_failures"], face_failures=segs["face_failures"],
-               forest=f)
+               candidates=segs["candidates"], hit_pairs=segs["hit_pairs"], newton_failures=segs["newton_failures"],
+               face_failures=segs["face_failures"], raw_segments=segs["raw_segments"], level=segs["level"],
+               units=segs["units"], unfolded_units=segs["unfolded_units"], forest=f)
     return out
 
 
@@ -29,8 +32,11 @@ def seg_columns(raw):
                 key=raw[:, 7].astype(np.int64))
 
 
-def compare(scene, g, ores, pixels, cull=None, tol=1e-4):
-    """Return a report dict with the three gates evaluated on `pixels`."""
+def compare(scene, g, ores, pixels, cull=None, tol=1e-4, by_counts=False):
+    """Return a report dict with the three gates evaluated on `pixels`.
+    by_counts: records are folded (node keys), so gate 2 compares the
+    per-pixel hit counts (rc_segments.hits_per_pixel) with the oracle's:
+    non-ambiguous hits <= count <= non-ambiguous hits + ambiguous pairs."""
     rep = {}
     # gate 1: culled list
     if cull is not None:
@@ -52,9 +58,14 @@ def compare(scene, g, ores, pixels, cull=None, tol=1e-4):
         h = h[h["elem"] >= 0]
         amb = set(h["elem"][(h["flags"] & oracle.AMBIGUOUS) != 0].tolist())
         ohit = set(h["elem"][(h["flags"] & oracle.HIT) != 0].tolist()) - amb
-        ghit = set(keys_sorted[lo[q]:hi[q]].tolist()) - amb
-        if ohit != ghit:
-            hit_mismatch += 1
+        if by_counts:
+            c = int(g["hits_per_pixel"].reshape(-1)[p])
+            if not (len(ohit) <= c <= len(ohit) + len(amb)):
+                hit_mismatch += 1
+        else:
+            ghit = set(keys_sorted[lo[q]:hi[q]].tolist()) - amb
+            if ohit != ghit:
+                hit_mismatch += 1
         amb_pairs += len(amb)
         err = float(np.abs(g["rgba"][p] - ores["rgba"][q]).max())
         if amb:

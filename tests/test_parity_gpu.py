@@ -170,6 +170,14 @@ def test_c3_full_size_sampled():
     print(rep, "hit_pairs", g["hit_pairs"], "newton_failures", g["newton_failures"])
     _check(rep)
     assert g["newton_failures"] == 0
+    # the bench's configuration folds to node level 2 on chip (row a6)
+    g2 = gpu_run(sc, device_copy=True, fold=2)
+    rep2 = compare(sc, g2, ores, pixels, by_counts=True)
+    print(rep2, "records", g2["count"], "raw", g2["raw_segments"], "units", g2["units"])
+    _check(rep2)
+    assert np.array_equal(g2["hits_per_pixel"], g["hits_per_pixel"])
+    assert g2["raw_segments"] == g["count"] and g2["count"] < g["count"] // 3
+    assert np.abs(g2["rgba"] - g["rgba"]).max() < 1e-5
 
 
 def test_affine_r2_matches_r1_P9():
@@ -220,14 +228,14 @@ def test_c4_full_size_sampled():
     N = 6) in the bench's launch configuration; 256 stratified pixels compared
     one by one with the oracle (which culls all 1e8 leaves in fp64)."""
     sc = sg.config4(device="cuda")
-    g = gpu_run(sc, device_copy=True)
-    assert g["newton_failures"] == 0
+    g = gpu_run(sc, device_copy=True, fold=2)     # bench.py's launch configuration
+    assert g["newton_failures"] == 0 and g["unfolded_units"] == 0
     import bench
     o = oracle.OracleScene(bench.scene_to_host(sc))
     W = sc.camera.width
     jj, ii = np.meshgrid(np.arange(37, W, 128), np.arange(61, W, 128), indexing="ij")
     pixels = (jj * W + ii).ravel().astype(np.int32)
     ores = o.render(pixels, mode="exact", cap=1536)
-    rep = compare(sc, g, ores, pixels)
-    print(rep, "hit_pairs", g["hit_pairs"], "segments", g["count"])
+    rep = compare(sc, g, ores, pixels, by_counts=True)
+    print(rep, "hit_pairs", g["hit_pairs"], "records", g["count"], "raw segments", g["raw_segments"])
     _check(rep)
