@@ -418,33 +418,41 @@ def config4(device=None) -> Scene:
     return shell_uniform(8, 2048, 256, name="C4", tiles=(8, 8), device=device)
 
 
-def config5(device=None, c=14.0, maxlevel=10) -> Scene:
-    """C5: shell adaptive around 512 sources."""
+def config5(device=None, c=14.0, maxlevel=10, level0=4, width=4096, nsources=512) -> Scene:
+    """C5: shell adaptive around 512 sources: start uniform
+    at level 4, refine E (level < 10) iff its exact-shell centre is closer than
+    c 2^-level to a source; field = the 512 Gaussian bumps at the sources.
+    ~1.9e8 leaves: generated on the GPU (scenegen/gpu.py, fp64 inside, field
+    rounded once to fp32).  Smaller variants (maxlevel, width, nsources) serve
+    the tests."""
     rng = np.random.default_rng(0)
-    sources = _shell_volume_points(rng, 512)
-    sigma = rng.uniform(0.03, 0.15, size=512)
-    amp = rng.uniform(0.5, 1.0, size=512)
+    sources = _shell_volume_points(rng, nsources)
+    sigma = rng.uniform(0.03, 0.15, size=nsources)
+    amp = rng.uniform(0.5, 1.0, size=nsources)
+    cam = perspective_camera(SHELL_EYE, [0.0, 0.0, 0.0], 40.0, width, width, gl_points=8)
+    if device is None or device == "numpy":
+        def rule(tree, anc, L):
+            h = 1.0 / (1 << L)
+            t = anc.astype(np.float64) / (1 << MAXLEVEL) + 0.5 * h
+            out = np.zeros(anc.shape[0], dtype=bool)
+            for k in range(6):
+                m = tree == k
+                if not m.any():
+                    continue
+                x = _shell_point(k, t[m, 0], t[m, 1], t[m, 2])
+                d = np.full(x.shape[0], np.inf)
+                for s_ in sources:
+                    d = np.minimum(d, np.linalg.norm(x - s_, axis=1))
+                out[m] = d < c * h
+            return out
 
-    def rule(tree, anc, L):
-        h = 1.0 / (1 << L)
-        t = anc.astype(np.float64) / (1 << MAXLEVEL) + 0.5 * h
-        out = np.zeros(anc.shape[0], dtype=bool)
-        for k in range(6):
-            m = tree == k
-            if not m.any():
-                continue
-            x = _shell_point(k, t[m, 0], t[m, 1], t[m, 2])
-            d = np.full(x.shape[0], np.inf)
-            for s in sources:
-                d = np.minimum(d, np.linalg.norm(x - s, axis=1))
-            out[m] = d < c * h
-        return out
-
-    anchor, tree, lev = refine_leaves(6, 4, maxlevel, rule)
-    cam = perspective_camera(SHELL_EYE, [0.0, 0.0, 0.0], 40.0, 4096, 4096, gl_points=8)
-    f = _field_from("shell", 2, anchor, tree, lev, lambda x, xp: _bumps_eval(x, sources, sigma, amp, xp),
-                    device=device)
-    return _finish("C5", 2, 2, shell_ctrl(2), anchor, tree, lev, f, cam, (8, 8), 3)
+        anchor, tree, lev = refine_leaves(6, level0, maxlevel, rule)
+        f = _field_from("shell", 2, anchor, tree, lev, lambda x, xp: _bumps_eval(x, sources, sigma, amp, xp))
+        return _finish("C5", 2, 2, shell_ctrl(2), anchor, tree, lev, f, cam, (8, 8), 3)
+    from . import gpu
+    anchor, tree, lev = gpu.refine_leaves_shell(level0, maxlevel, sources, c, device)
+    field, F = gpu.shell_bumps_field(anchor, tree, lev, 2, sources, sigma, amp)
+    return _finish("C5", 2, 2, shell_ctrl(2), anchor, tree, lev, field, cam, (8, 8), 3, F=F)
 
 
 def constant_field(scene: Scene, value: float = 0.7) -> Scene:

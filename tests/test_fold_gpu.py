@@ -12,6 +12,7 @@ import pytest
 
 import oracle
 import scenegen as sg
+from oracle import coarsen
 from parity_util import compare, gpu_run
 
 pytestmark = pytest.mark.gpu
@@ -19,34 +20,24 @@ pytestmark = pytest.mark.gpu
 LOSSLESS = 1e-5
 
 
-def nodes_reference(anchor, tree, level, levels):
-    """Host reference of the node tables: level c+1 replaces every complete
-    family of 8 same-level siblings of level c (8 consecutive nodes, child ids
-    0..7, one parent) by its parent."""
-    nodes = [(int(tree[k]), tuple(int(x) for x in anchor[k]), int(level[k]), k) for k in range(len(tree))]
-    out = {}
-    for c in range(1, levels + 1):
-        new, k = [], 0
-        while k < len(nodes):
-            t, a, l, first = nodes[k]
-            fam = False
-            if l >= 1 and k + 7 < len(nodes):
-                sh = 18 - l
-                par = tuple(x & ~((1 << (sh + 1)) - 1) for x in a)
-                fam = par == a
-                for j in range(8):
-                    t2, a2, l2, _ = nodes[k + j]
-                    cid = ((a2[0] >> sh) & 1) | (((a2[1] >> sh) & 1) << 1) | (((a2[2] >> sh) & 1) << 2)
-                    p2 = tuple(x & ~((1 << (sh + 1)) - 1) for x in a2)
-                    fam = fam and t2 == t and l2 == l and p2 == par and cid == j
-            if fam:
-                new.append((t, a, l - 1, first))
-                k += 8
-            else:
-                new.append(nodes[k])
-                k += 1
-        nodes = new
-        out[c] = np.array([nd[3] for nd in nodes], dtype=np.int64)
+nodes_reference = coarsen.node_tables
+
+
+def _record_counts(g, npix):
+    return np.bincount(g["raw"][:, 0].astype(np.int64), minlength=npix)
+
+
+def _oracle_runs(ores, table):
+    """Per pixel: oracle run count at the table's level, or -1 for pixels
+    with eps-ambiguous pairs (excluded from the exact comparison)."""
+    out = np.zeros(len(ores["pixels"]), dtype=np.int64)
+    for q in range(len(ores["pixels"])):
+        h = ores["hits"][q]
+        h = h[h["elem"] >= 0]
+        if ((h["flags"] & oracle.AMBIGUOUS) != 0).any():
+            out[q] = -1
+        else:
+            out[q] = coarsen.run_counts(h, table)
     return out
 
 
@@ -89,6 +80,17 @@ def test_fold_levels_curved(level, width):
         assert np.abs(g["rgba"] - g0["rgba"]).max() < LOSSLESS
         rep = compare(sc, g, ores, pixels, by_counts=True)
         assert rep["hit_mismatch_pixels"] == 0 and rep["bad_pixels"] == 0, rep
+        # per pixel the fused fold leaves at least the maximal runs of the
+        # plain coarsening (units may cut big nodes), exactly those when every
+        # unit is a whole node
+        table = coarsen.node_tables(sc.leaf_anchor, sc.leaf_tree, sc.leaf_level, c)[c]
+        ref = _oracle_runs(ores, table)
+        clean = ref >= 0
+        got = _record_counts(g, width * width)
+        assert (got[clean] >= ref[clean]).all()
+        vis_nodes = np.unique(np.searchsorted(table, g["visible"], side="right") - 1).size
+        if g["units"] == vis_nodes:
+            assert np.array_equal(got[clean], ref[clean]), (c, int((got[clean] != ref[clean]).sum()))
         # records are keyed by nodes of level c
         keys = np.unique(g["raw"][:, 7].astype(np.int64))
         table = g["forest"].node_table(c).cpu().numpy()
@@ -100,6 +102,10 @@ def test_aggregate_cycles_lossless(which):
     """rc_aggregate (a7): each cycle lowers the record count, pixels unchanged."""
     sc = sg.config2(width=96, maxlevel=5) if which == "c2" else sg.shell_uniform(3, 96, 16, gl_points=6)
     g0 = gpu_run(sc, fold=0)
+    W = sc.camera.width
+    ores = oracle.OracleScene(sc).render(np.arange(W * W, dtype=np.int32), mode="rule", cap=256)
+    tables = coarsen.node_tables(sc.leaf_anchor, sc.leaf_tree, sc.leaf_level, 3)
+    clean = None
     prev = g0["count"]
     for cyc in (1, 2, 3):
         g = gpu_run(sc, fold=0, cycles=cyc)
@@ -108,6 +114,11 @@ def test_aggregate_cycles_lossless(which):
         prev = g["count"]
         assert np.abs(g["rgba"] - g0["rgba"]).max() < LOSSLESS
         assert np.array_equal(g["hits_per_pixel"], g0["hits_per_pixel"])
+        # exact record counts per pixel vs the plain coarsening of the oracle's segments
+        ref = _oracle_runs(ores, tables[cyc])
+        clean = ref >= 0
+        got = _record_counts(g, W * W)
+        assert np.array_equal(got[clean], ref[clean]), (cyc, int((got[clean] != ref[clean]).sum()))
     # on-chip fold then aggregation reaches the same level with the same pixels
     g2 = gpu_run(sc, fold=1, cycles=2)
     assert g2["level"] == 3
@@ -144,3 +155,38 @@ def test_aggregate_errors():
     f.cast_segments(6)
     with pytest.raises(rc.RcError):
         f.aggregate(3)           # beyond the 8 node levels
+
+
+def test_c5_generator_gpu_matches_host():
+    """The GPU generator of C5 (scenegen/gpu.py) builds the same forest as the
+    host generator on a reduced variant, and the same field up to the final
+    fp32 rounding."""
+    host = sg.config5(device=None, maxlevel=6, level0=3, width=64, nsources=24)
+    dev = sg.config5(device="cuda", maxlevel=6, level0=3, width=64, nsources=24)
+    assert np.array_equal(host.leaf_anchor, dev.leaf_anchor.cpu().numpy())
+    assert np.array_equal(host.leaf_tree, dev.leaf_tree.cpu().numpy())
+    assert np.array_equal(host.leaf_level, dev.leaf_level.cpu().numpy())
+    fd = dev.leaf_field.cpu().numpy()
+    assert np.abs(fd - host.leaf_field).max() <= 2e-7 * max(1.0, np.abs(host.leaf_field).max())
+    assert abs(dev.inv_F / host.inv_F - 1.0) < 1e-12
+
+
+def test_c5_reduced_fold_and_cycles():
+    """C5's pipeline (fold 2 on chip + 3 aggregation cycles, N = 8) on a reduced
+    adaptive shell vs the oracle on every pixel."""
+    import dataclasses
+    sc = sg.config5(device="cuda", maxlevel=6, level0=3, width=96, nsources=24)
+    import bench
+    sc = bench.scene_to_host(sc)
+    o = oracle.OracleScene(sc)
+    pixels = np.arange(96 * 96, dtype=np.int32)
+    ores = o.render(pixels, mode="exact", cap=512)
+    g0 = gpu_run(sc, fold=0)
+    rep0 = compare(sc, g0, ores, pixels, cull=o.cull())
+    assert rep0["hit_mismatch_pixels"] == 0 and rep0["bad_pixels"] == 0, rep0
+    g = gpu_run(sc, fold=2, cycles=3)
+    assert g["level"] == 5
+    rep = compare(sc, g, ores, pixels, by_counts=True)
+    assert rep["hit_mismatch_pixels"] == 0 and rep["bad_pixels"] == 0, rep
+    assert g["count"] < g0["count"] // 2
+    assert np.abs(g["rgba"] - g0["rgba"]).max() < LOSSLESS
