@@ -767,6 +767,7 @@ __device__ __forceinline__ void isect_chunk(IsectSmem& W, const CamConst& cc, co
           if (sa0 < -rho || sa0 > 1.0f + rho || sb0 < -rho || sb0 > 1.0f + rho) continue;   // proof: no root
           float sa = sa0, sb = sb0, bt = b0;
           bool conv = false;
+          const float qfac = qf / (1.0f - qf) * 1.01f;
           const int str3[3] = {1, 3, 9};
           const int fbase = 2 * fside * str3[fk], fsa = str3[fa], fsb = str3[fb];
 #pragma unroll 1
@@ -792,7 +793,8 @@ __device__ __forceinline__ void isect_chunk(IsectSmem& W, const CamConst& cc, co
             sa = nsa;
             sb = nsb;
             bt = nbt;
-            if (step < tol) {
+            // contraction q = qf < 1/4: |x_{k+1} - x*| <= q/(1-q) |x_{k+1} - x_k|
+            if (step * qfac < tol) {
               conv = true;
               break;
             }
@@ -989,6 +991,11 @@ __device__ __forceinline__ bool integ_group(IntegSmem& W, const CamConst& cc, co
       for (int aa = 0; aa < 3; ++aa)
 #pragma unroll
         for (int b = 0; b < 3; ++b) Ji[aa][b] = afm[3 + 3 * aa + b];
+      // chord map T(xi) = xi + J0^-1 (t - X(xi)): |DT|_inf = |I - J0^-1 J|_inf <= 3 eta on the
+      // element, so after a step s the error is <= q/(1-q) s (q = 3 eta); stop when that is
+      // below tol (the plain rule s < tol when q/(1-q) >= 1)
+      const float q3 = 3.0f * afm[15] * 1.1f;
+      const float qfac = q3 < 0.5f ? q3 / (1.0f - q3) : 1.0f;
       const float xin[3] = {i0.x, i0.y, i0.z}, xout[3] = {i0.w, i1.x, i1.y};
       const float xia[3] = {i1.z, i1.w, i2.x}, xib[3] = {i2.y, i2.z, i2.w};
       const float dX[3] = {xout[0] - xin[0], xout[1] - xin[1], xout[2] - xin[2]};
@@ -1007,7 +1014,7 @@ __device__ __forceinline__ bool integ_group(IntegSmem& W, const CamConst& cc, co
         xm[0] += s0;
         xm[1] += s1;
         xm[2] += s2;
-        if (fmaxf(fabsf(s0), fmaxf(fabsf(s1), fabsf(s2))) < tol) {
+        if (fmaxf(fabsf(s0), fmaxf(fabsf(s1), fabsf(s2))) * qfac < tol) {
           ok = true;
           break;
         }
@@ -1036,7 +1043,7 @@ __device__ __forceinline__ bool integ_group(IntegSmem& W, const CamConst& cc, co
           xi[0] += s0;
           xi[1] += s1;
           xi[2] += s2;
-          if (fmaxf(fabsf(s0), fmaxf(fabsf(s1), fabsf(s2))) < tol) {
+          if (fmaxf(fabsf(s0), fmaxf(fabsf(s1), fabsf(s2))) * qfac < tol) {
             conv = true;
             break;
           }

@@ -405,8 +405,14 @@ def shell_uniform(level, width, nbumps, seed=0, gl_points=6, name=None, tiles=(1
     anchor, tree, lev = uniform_leaves(6, level)
     centers, sigma, amp = shell_bumps(nbumps, seed)
     cam = perspective_camera(SHELL_EYE, [0.0, 0.0, 0.0], fov, width, width, gl_points=gl_points)
-    f = _field_from("shell", 2, anchor, tree, lev, lambda x, xp: _bumps_eval(x, centers, sigma, amp, xp),
-                    device=device)
+    if device is not None and device != "numpy":
+        # same bump sum in fp64 by the generator's CUDA helper (scenegen/gpu.py)
+        import torch
+        from . import gpu
+        A, T, Lv = (torch.as_tensor(x, device=device) for x in (anchor, tree, lev))
+        f, F = gpu.shell_bumps_field(A, T, Lv, 2, centers, sigma, amp)
+        return _finish(name or f"shell-L{level}", 2, 2, shell_ctrl(2), A, T, Lv, f, cam, tiles, F=F)
+    f = _field_from("shell", 2, anchor, tree, lev, lambda x, xp: _bumps_eval(x, centers, sigma, amp, xp))
     return _finish(name or f"shell-L{level}", 2, 2, shell_ctrl(2), anchor, tree, lev, f, cam, tiles)
 
 

@@ -190,3 +190,13 @@ def test_c5_reduced_fold_and_cycles():
     assert rep["hit_mismatch_pixels"] == 0 and rep["bad_pixels"] == 0, rep
     assert g["count"] < g0["count"] // 2
     assert np.abs(g["rgba"] - g0["rgba"]).max() < LOSSLESS
+
+
+def test_shell_generator_gpu_matches_host():
+    """shell_uniform(device=cuda) (generator CUDA helper) vs the host generator."""
+    host = sg.shell_uniform(3, 64, 16)
+    dev = sg.shell_uniform(3, 64, 16, device="cuda")
+    assert np.array_equal(host.leaf_anchor, dev.leaf_anchor.cpu().numpy())
+    fd = dev.leaf_field.cpu().numpy()
+    assert np.abs(fd - host.leaf_field).max() <= 2e-7 * max(1.0, np.abs(host.leaf_field).max())
+    assert abs(dev.inv_F / host.inv_F - 1.0) < 1e-12

@@ -17,7 +17,7 @@ if __name__ == "__main__":
     sc = bench.make_scene(a.config, torch.device("cuda"))
     f = rc.Forest.from_scene(sc, device_copy=True)
     for _ in range(a.frames):
-        img, hits = f.render_frame(sc.camera)
+        img, hits = f.render_frame(sc.camera, fold_levels=(0 if a.config <= 2 else 2))
     torch.cuda.synchronize()
     s = f.segments()
     print("hit_pairs", hits, "candidates", s["candidates"], "segments", s["count"], "newton_failures",
