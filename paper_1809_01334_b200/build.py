@@ -20,7 +20,11 @@ def _stale(out, deps):
     return not os.path.exists(out) or os.path.getmtime(out) < max(os.path.getmtime(d) for d in deps)
 
 
-def build(force: bool = False, verbose: bool = False) -> str:
+def build(force: bool = False, verbose: bool = False, defines=(), tag: str = "") -> str:
+    """Compile csrc/*.cu into librc.so; `defines` + `tag` build an experiment
+    variant into build_<tag>/ and librc_<tag>.so (same sources)."""
+    BUILD = os.path.join(HERE, "build" + (f"_{tag}" if tag else ""))
+    OUT = os.path.join(HERE, f"librc_{tag}.so" if tag else "librc.so")
     os.makedirs(BUILD, exist_ok=True)
     srcs = sorted(glob.glob(os.path.join(CSRC, "*.cu")))
     hdrs = sorted(glob.glob(os.path.join(CSRC, "*.cuh"))) + [os.path.join(HERE, "..", "include", "rc.h")]
@@ -34,7 +38,7 @@ def build(force: bool = False, verbose: bool = False) -> str:
 
     def compile_one(job):
         src, obj = job
-        cmd = [NVCC] + FLAGS + ["-c", src, "-o", obj]
+        cmd = [NVCC] + FLAGS + [f"-D{d}" for d in defines] + ["-c", src, "-o", obj]
         r = subprocess.run(cmd, capture_output=True, text=True)
         log = os.path.join(BUILD, os.path.basename(src) + ".ptxas.log")
         with open(log, "w") as fh:
@@ -56,4 +60,6 @@ def build(force: bool = False, verbose: bool = False) -> str:
 
 
 if __name__ == "__main__":
-    print(build(force="--force" in sys.argv, verbose=True))
+    defs = [a[2:] for a in sys.argv[1:] if a.startswith("-D")]
+    tags = [a[6:] for a in sys.argv[1:] if a.startswith("--tag=")]
+    print(build(force="--force" in sys.argv, verbose=True, defines=defs, tag=tags[0] if tags else ""))

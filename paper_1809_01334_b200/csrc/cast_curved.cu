@@ -285,10 +285,11 @@ __device__ __forceinline__ int chord_root(const Patch& pt, float A11, float A12,
   return 0;
 }
 
-// Roots of one face patch in face coordinates [0,1]^2.  Common case: hull
-// test + injectivity + Newton.  Rare case: subdivision with a small stack.
-// Returns the number of roots written to (u1[], u2[]).
-__device__ __forceinline__ void load_patch(const float* __restrict__ sp, int f, Patch& pt) {
+// Face f's 9 Bernstein points (relative to the element origin) projected on
+// the plane spanned by d1, d2 perpendicular to the ray, origin at the ray
+// (Eq. intersectiontwod).
+__device__ __forceinline__ void project_face(const float* __restrict__ sB, int f, const float d1[3],
+                                             const float d2[3], float o1, float o2, Patch& pt) {
   const int k = f >> 1, side = f & 1;
   const int ka = (k + 1) % 3, kb = (k + 2) % 3;
   const int str[3] = {1, 3, 9};
@@ -298,17 +299,16 @@ __device__ __forceinline__ void load_patch(const float* __restrict__ sp, int f, 
 #pragma unroll
     for (int ia = 0; ia < 3; ++ia) {
       const int m = base + ia * sa + jb * sbb;
-      pt.gx[3 * jb + ia] = sp[(2 * m) * 32];
-      pt.gy[3 * jb + ia] = sp[(2 * m + 1) * 32];
+      const float bx = sB[3 * m], by = sB[3 * m + 1], bz = sB[3 * m + 2];
+      pt.gx[3 * jb + ia] = fmaf(d1[0], bx, fmaf(d1[1], by, fmaf(d1[2], bz, -o1)));
+      pt.gy[3 * jb + ia] = fmaf(d2[0], bx, fmaf(d2[1], by, fmaf(d2[2], bz, -o2)));
     }
 }
 
-// sp: this lane's projected control points ([m*2+c] with stride 32), f: face.
-// Roots are written to u[2*t], u[2*t+1] (shared-memory scratch of the lane).
-__device__ __noinline__ int face_roots_subdiv(const float* __restrict__ sp, int f, float tol, int max_it,
-                                              float* u, int stride, int cap, int* fails) {
-  Patch root;
-  load_patch(sp, f, root);
+// All roots of a projected face patch by Bezier subdivision (App. A.1,
+// PAPER.md:1481-1514).  Roots are written to u[2*t], u[2*t+1].
+__device__ __noinline__ int face_roots_subdiv(const Patch& root, float tol, int max_it, float* u, int stride,
+                                              int cap, int* fails) {
   struct Item {
     Patch p;
     float s1a, s2a, w;
@@ -569,53 +569,66 @@ __device__ __forceinline__ void prep_element(float* __restrict__ sl, double* __r
 // ---------------------------------------------------------------------------
 // The fused segment kernel (rows a4 + a5 + a6 of SURVEY §8(a)).  Persistent
 // CTAs of CWARPS warps take fold units from a global counter; a unit is a
-// range of <= RC_UNIT_CHUNKS chunks inside one node of the fold level (built
-// by k_unit_* in kernels.cu), or any RC_UNIT_CHUNKS chunks when not folding.
-// Per unit:
-//  phase 1 (intersection): warps take the unit's chunks from a shared
-//    counter; one warp = 32 candidate pixels of one element; every inside
-//    interval becomes a 64-byte item in the CTA's scratch (L2-resident):
-//      float xin[3], xout[3]  entry / exit point relative to the element origin
-//      float xiin[3], xiout[3] reference coordinates of entry / exit
-//      float alpha_near, alpha_far; uint32 pixel; int32 visible index
+// range of <= RC_UNIT_CHUNKS chunks of <= RC_UNIT_LEAVES visible leaves
+// inside one node of the fold level (k_unit_* in kernels.cu).  Per unit:
+//  phase 0: the unit's elements are prepared once into shared memory
+//    (Bernstein points relative to the element origin, nodal field, affine
+//    model and its nonlinearity bounds; warps take elements);
+//  phase 1 (intersection): warps take the unit's chunks from a shared counter;
+//    per chunk (32 candidate pixels of one element):
+//    1a per lane: ray re-based near the element (fp64), affine prefilter and
+//       the proof of "no root" per face -> candidate (pixel, face) tasks;
+//    1b the chunk's face tasks in full warps (one task per lane): certified
+//       affine-model iteration, else the projected-patch method of App. A.1;
+//       roots go to the pixel's list in shared memory;
+//    1c per lane: roots sorted by beta, deduplicated, paired entry/exit; each
+//       inside interval becomes a 64-byte item in the CTA's scratch (L2):
+//         float xin[3], xout[3]  entry / exit point relative to the element origin
+//         float xiin[3], xiout[3] reference coordinates of entry / exit
+//         float alpha_near, alpha_far; uint32 pixel; int32 visible index
 //  phase 2 (integration): warps take 32 items at a time (full warps, no idle
-//    lanes on misses) and integrate them with the N-point GL rule.
+//    lanes on misses) and integrate them with the N-point GL rule;
 //  phase 3 (fold, fold level >= 1): the unit's segments are sorted by
-//    (pixel, alpha_near) in shared memory and every maximal run of touching
-//    segments of one pixel (|gap| <= 1e-6 max(1, alpha)) is
-//    combined nearest-first with Eq. aggregate into one
-//    record keyed by the node: the first levels of the paper's coarsening
-//     done on chip.  Overlapping or separated
-//    segments stay separate records (the composite cuts / orders them).
+//    (pixel, alpha_near) in shared memory (batches of SORT_CAP) and every
+//    maximal run of touching segments of one pixel (|gap| <= 1e-6 max(1,
+//    alpha)) is combined nearest-first with Eq. aggregate
+//     into one record keyed by the node: the first levels of
+//    the paper's coarsening done on chip.
 //    Without folding every segment is a record keyed by its leaf.
 // ---------------------------------------------------------------------------
 constexpr int CWARPS = 4;
+#ifndef CAST_CTAS_PER_SM
+#define CAST_CTAS_PER_SM 4   // resident CTAs per SM (launch bounds; 4 fits the 56 KB of shared memory)
+#endif
 constexpr int ITEM_CAP = 2 * RC_CHUNK * RC_UNIT_CHUNKS;   // <= two segments per pair
-constexpr int SORT_CAP = 4096;
+constexpr int SORT_CAP = 2048;
+constexpr int MAXT = 6 * RC_CHUNK;                        // face tasks of one chunk
 constexpr float FOLD_TAU = 1e-6f;
+constexpr int PS_N = 14;                                  // per-pixel ray state (floats)
 
-struct IsectSmem {
-  float slot[SLOT_STRIDE];
-  double prep[2][81];
-  double org[3];
-  float proj[54][32];
-  float roots[4][4][32];
-  float sub[8][32];
+struct WarpIsect {
+  float ps[PS_N][32];       // P0[3], rf[3], xl0[3], dl[3], alpha0, rr
+  float roots[4][4][32];    // [k][beta, xi0, xi1, xi2][lane]
+  int nroots[32];
+  uint8_t task[MAXT];       // lane << 3 | face
 };
-constexpr int GSLOTS = 4;
-struct IntegSmem {
-  float slot[GSLOTS][SLOT_STRIDE];
+struct PrepScratch {
   double prep[2][81];
-  double org[3];
 };
 struct SortSmem {
   unsigned long long key[SORT_CAP];
   uint16_t idx[SORT_CAP];
 };
-union CastSmem {
-  IsectSmem isect[CWARPS];
-  IntegSmem integ[CWARPS];
+union PhaseSmem {
+  PrepScratch prep[CWARPS];
+  WarpIsect isect[CWARPS];
   SortSmem sort;
+  float scr[RC_MAX_N * CWARPS * 32];   // phase 2: per-thread node values
+};
+struct CastSmem {
+  float slot[RC_UNIT_LEAVES][SLOT_STRIDE];
+  double org[RC_UNIT_LEAVES][3];
+  PhaseSmem ph;
 };
 struct CastCtl {
   int64_t unit;
@@ -654,37 +667,42 @@ __device__ __forceinline__ unsigned long long fold_key(uint32_t pix, float an) {
   return ((unsigned long long)pix << 32) | u;
 }
 
+__device__ __forceinline__ void push_root(WarpIsect& W, int pl, float beta, const float xi[3], int& face_fail) {
+  const int k = atomicAdd(&W.nroots[pl], 1);
+  if (k >= 4) {
+    ++face_fail;
+    return;
+  }
+  W.roots[k][0][pl] = beta;
+  W.roots[k][1][pl] = xi[0];
+  W.roots[k][2][pl] = xi[1];
+  W.roots[k][3][pl] = xi[2];
+}
+
 // ---- phase 1: one chunk (32 candidate pixels of one element) --------------
-__device__ __forceinline__ void isect_chunk(IsectSmem& W, const CamConst& cc, const TreeConst* __restrict__ trees,
-                                            const DevLeafView& L, const int32_t* __restrict__ vis,
-                                            const Rect16* __restrict__ vrect, const int64_t* __restrict__ chunk_off,
-                                            const int32_t* __restrict__ chunk_elem, int64_t c, int& cur_v,
+__device__ __forceinline__ void isect_chunk(WarpIsect& W, const float* __restrict__ sB, const double* __restrict__ org,
+                                            const CamConst& cc, const Rect16 r, int64_t cpos, int v,
                                             float4* __restrict__ items, int* s_nitems,
                                             int32_t* __restrict__ hits_pp, int& local_hits, int& face_fail) {
   const unsigned lane = threadIdx.x & 31;
   const float tol = cc.newton_tol;
   const int max_it = cc.newton_max;
-  const float* sB = W.slot;
-  const int v = chunk_elem[c];
-  if (v != cur_v) {
-    const int e = vis[v];
-    __syncwarp();
-    prep_element(W.slot, W.org, W.prep, trees, L, e, lane, 0, false);
-    cur_v = v;
-  }
-  const Rect16 r = vrect[v];
+  const float* af = sB + SLOT_AFF;
+  const float dpv[3] = {af[12], af[13], af[14]};
+  const float dpm = fmaxf(dpv[0], fmaxf(dpv[1], dpv[2])), eta2 = 2.0f * af[15];
   const int rw = r.i1 - r.i0 + 1, rh = r.j1 - r.j0 + 1;
-  const int p = (int)(c - chunk_off[v]) * RC_CHUNK + (int)lane;
+  const int p = (int)cpos * RC_CHUNK + (int)lane;
   const bool active = p < rw * rh;
   const int i = r.i0 + p % rw, j = r.j0 + p / rw;
-  // ---- ray of pixel (i,j), re-based near the element (fp64) ----------
+
+  // ---- 1a: ray of pixel (i,j), re-based near the element (fp64) -----------
   const double di = (double)i - 0.5 * (cc.W - 1), dj = (double)j - 0.5 * (cc.H - 1);
   double Rw[3], D[3];
 #pragma unroll
   for (int k = 0; k < 3; ++k) {
     Rw[k] = fma(dj, cc.Ru[k], fma(di, cc.Rt[k], cc.R0[k]));
     const double O = fma(dj, cc.Ou[k], fma(di, cc.Ot[k], cc.O0[k]));
-    D[k] = W.org[k] - O;
+    D[k] = org[k] - O;
   }
   const float rf[3] = {(float)Rw[0], (float)Rw[1], (float)Rw[2]};
   const float rr = rf[0] * rf[0] + rf[1] * rf[1] + rf[2] * rf[2];
@@ -692,34 +710,14 @@ __device__ __forceinline__ void isect_chunk(IsectSmem& W, const CamConst& cc, co
   float P0[3];
 #pragma unroll
   for (int k = 0; k < 3; ++k) P0[k] = (float)fma((double)alpha0, Rw[k], -D[k]);
-  const float rn = sqrtf(rr);
-
-  // roots (beta, xi) go to per-lane shared scratch, sorted by beta afterwards
-  int nroots = 0;
-  float rb0 = 3.4e38f, rb1 = 3.4e38f, rb2 = 3.4e38f, rb3 = 3.4e38f;
-  int ri0 = 0, ri1 = 1, ri2 = 2, ri3 = 3;
+  // affine prefilter in xi~ = J0^-1 coordinates: line xl(beta) = xl0 + beta dl
+  const float q0 = P0[0] - af[0], q1 = P0[1] - af[1], q2 = P0[2] - af[2];
+  const float xl0[3] = {0.5f + af[3] * q0 + af[4] * q1 + af[5] * q2, 0.5f + af[6] * q0 + af[7] * q1 + af[8] * q2,
+                        0.5f + af[9] * q0 + af[10] * q1 + af[11] * q2};
+  const float dl[3] = {af[3] * rf[0] + af[4] * rf[1] + af[5] * rf[2], af[6] * rf[0] + af[7] * rf[1] + af[8] * rf[2],
+                       af[9] * rf[0] + af[10] * rf[1] + af[11] * rf[2]};
+  unsigned face_mask = 0;
   if (active) {
-    float ax[3] = {0.f, 0.f, 0.f};
-    {
-      const float a0 = fabsf(rf[0]), a1 = fabsf(rf[1]), a2 = fabsf(rf[2]);
-      ax[(a0 <= a1 && a0 <= a2) ? 0 : (a1 <= a2 ? 1 : 2)] = 1.0f;
-    }
-    float d1[3] = {rf[1] * ax[2] - rf[2] * ax[1], rf[2] * ax[0] - rf[0] * ax[2], rf[0] * ax[1] - rf[1] * ax[0]};
-    const float n1 = rsqrtf(d1[0] * d1[0] + d1[1] * d1[1] + d1[2] * d1[2]);
-    d1[0] *= n1; d1[1] *= n1; d1[2] *= n1;
-    float d2[3] = {rf[1] * d1[2] - rf[2] * d1[1], rf[2] * d1[0] - rf[0] * d1[2], rf[0] * d1[1] - rf[1] * d1[0]};
-    const float n2 = rsqrtf(d2[0] * d2[0] + d2[1] * d2[1] + d2[2] * d2[2]);
-    d2[0] *= n2; d2[1] *= n2; d2[2] *= n2;
-    const float o1 = d1[0] * P0[0] + d1[1] * P0[1] + d1[2] * P0[2];
-    const float o2 = d2[0] * P0[0] + d2[1] * P0[1] + d2[2] * P0[2];
-    // affine prefilter in xi~ = J0^-1 coordinates: line xl(beta) = xl0 + beta dl
-    const float* af = sB + SLOT_AFF;
-    const float q0 = P0[0] - af[0], q1 = P0[1] - af[1], q2 = P0[2] - af[2];
-    const float xl0[3] = {0.5f + af[3] * q0 + af[4] * q1 + af[5] * q2, 0.5f + af[6] * q0 + af[7] * q1 + af[8] * q2,
-                          0.5f + af[9] * q0 + af[10] * q1 + af[11] * q2};
-    const float dl[3] = {af[3] * rf[0] + af[4] * rf[1] + af[5] * rf[2], af[6] * rf[0] + af[7] * rf[1] + af[8] * rf[2],
-                         af[9] * rf[0] + af[10] * rf[1] + af[11] * rf[2]};
-    const float dpv[3] = {af[12], af[13], af[14]};
     float tin[3], tout[3], inv[3];
 #pragma unroll
     for (int k = 0; k < 3; ++k) {
@@ -729,45 +727,79 @@ __device__ __forceinline__ void isect_chunk(IsectSmem& W, const CamConst& cc, co
       tout[k] = fmaxf(ta, tb);
     }
     const float ben = fmaxf(tin[0], fmaxf(tin[1], tin[2])), bex = fminf(tout[0], fminf(tout[1], tout[2]));
-    unsigned face_mask = 0;
     if (bex >= ben) {
 #pragma unroll
       for (int f = 0; f < 6; ++f) {
-        const int k = f >> 1;
+        const int k = f >> 1, fa = (k + 1) % 3, fb = (k + 2) % 3;
         const float side = (float)(f & 1);
         // face slab |xl_k - side| <= dp_k within the inflated box
         const float ta = (side - dpv[k] - xl0[k]) * inv[k], tb = (side + dpv[k] - xl0[k]) * inv[k];
         const float lo = fmaxf(ben, fminf(ta, tb)), hi = fminf(bex, fmaxf(ta, tb));
-        if (hi >= lo) face_mask |= 1u << f;
+        if (!(hi >= lo)) continue;
+        // proof of "no root" of the certified iteration (see 1b): the root
+        // x* = (s_a, s_b, beta) lies within ||M0^-1|| max|E| of x0
+        const float rk = inv[k];
+        const float mnorm = fmaxf(fabsf(rk), 1.0f + fabsf(dl[fa] * rk) + fabsf(dl[fb] * rk));
+        if (mnorm * eta2 < 0.25f) {
+          const float b0 = (side - xl0[k]) * rk;
+          const float sa0 = xl0[fa] + b0 * dl[fa], sb0 = xl0[fb] + b0 * dl[fb];
+          const float rho = mnorm * dpm + FACE_TOL;
+          if (sa0 < -rho || sa0 > 1.0f + rho || sb0 < -rho || sb0 > 1.0f + rho) continue;
+        }
+        face_mask |= 1u << f;
       }
     }
-    float* sp = &W.proj[0][lane];
-    float* su = &W.sub[0][lane];
-    const float dpm = fmaxf(dpv[0], fmaxf(dpv[1], dpv[2])), eta2 = 2.0f * af[15];
-#pragma unroll 1
-    for (int f = 0; f < 6; ++f) {
-      if (!(face_mask & (1u << f))) continue;
+  }
+  W.ps[0][lane] = P0[0]; W.ps[1][lane] = P0[1]; W.ps[2][lane] = P0[2];
+  W.ps[3][lane] = rf[0]; W.ps[4][lane] = rf[1]; W.ps[5][lane] = rf[2];
+  W.ps[6][lane] = xl0[0]; W.ps[7][lane] = xl0[1]; W.ps[8][lane] = xl0[2];
+  W.ps[9][lane] = dl[0]; W.ps[10][lane] = dl[1]; W.ps[11][lane] = dl[2];
+  W.ps[13][lane] = rr;
+  W.nroots[lane] = 0;
+  int ntask;
+  {
+    const int want = __popc(face_mask);
+    int incl = want;
+#pragma unroll
+    for (int off = 1; off < 32; off <<= 1) {
+      const int y = __shfl_up_sync(0xffffffffu, incl, off);
+      if ((int)lane >= off) incl += y;
+    }
+    ntask = __shfl_sync(0xffffffffu, incl, 31);
+    int t = incl - want;
+    for (unsigned m = face_mask; m; m &= m - 1) W.task[t++] = (uint8_t)((lane << 3) | (__ffs(m) - 1));
+  }
+  __syncwarp();
+
+  // ---- 1b: face tasks, one per lane -----------------------------------------
+  for (int t0 = 0; t0 < ntask; t0 += 32) {
+    const int t = t0 + (int)lane;
+    if (t < ntask) {
+      const int code = W.task[t];
+      const int pl = code >> 3, f = code & 7;
+      const float tP0[3] = {W.ps[0][pl], W.ps[1][pl], W.ps[2][pl]};
+      const float trf[3] = {W.ps[3][pl], W.ps[4][pl], W.ps[5][pl]};
+      const float txl0[3] = {W.ps[6][pl], W.ps[7][pl], W.ps[8][pl]};
+      const float tdl[3] = {W.ps[9][pl], W.ps[10][pl], W.ps[11][pl]};
+      const float trr = W.ps[13][pl];
       const int fk = f >> 1, fside = f & 1;
       const int fa = (fk + 1) % 3, fb = (fk + 2) % 3;
+      bool done = false;
       {
         // Certified fast path.  In xi~ coordinates the face is
         // (s_a, s_b, side) + E(s) and the ray xl0 + beta dl, so the root
-        // x = (s_a, s_b, beta) solves x = x0 - M0^-1 E(s) with M0 = [e_a, e_b, -dl]:
-        // |x* - x0|_inf <= ||M0^-1|| max|E| (exclusion) and the map contracts
-        // with q = ||M0^-1|| 2 eta (uniqueness + convergence) when q < 1.
-        const float dk = dl[fk];
+        // x = (s_a, s_b, beta) solves x = x0 - M0^-1 E(s) with M0 = [e_a, e_b, -dl];
+        // the map contracts with q = ||M0^-1|| 2 eta < 1/4 (uniqueness +
+        // convergence; the exclusion was proven in 1a).
+        const float dk = tdl[fk];
         const float rk = 1.0f / dk;
-        const float ga = dl[fa] * rk, gb = dl[fb] * rk;
-        const float mnorm = fmaxf(fabsf(rk), 1.0f + fabsf(ga) + fabsf(gb));
+        const float mnorm = fmaxf(fabsf(rk), 1.0f + fabsf(tdl[fa] * rk) + fabsf(tdl[fb] * rk));
         const float qf = mnorm * eta2;
         if (qf < 0.25f) {
-          const float b0 = ((float)fside - xl0[fk]) * rk;
-          const float sa0 = xl0[fa] + b0 * dl[fa], sb0 = xl0[fb] + b0 * dl[fb];
-          const float rho = mnorm * dpm + FACE_TOL;
-          if (sa0 < -rho || sa0 > 1.0f + rho || sb0 < -rho || sb0 > 1.0f + rho) continue;   // proof: no root
-          float sa = sa0, sb = sb0, bt = b0;
-          bool conv = false;
+          const float b0 = ((float)fside - txl0[fk]) * rk;
+          const float sa0 = txl0[fa] + b0 * tdl[fa], sb0 = txl0[fb] + b0 * tdl[fb];
           const float qfac = qf / (1.0f - qf) * 1.01f;
+          float sa = sa0, sb = sb0, bt = b0;
           const int str3[3] = {1, 3, 9};
           const int fbase = 2 * fside * str3[fk], fsa = str3[fa], fsb = str3[fb];
 #pragma unroll 1
@@ -787,97 +819,88 @@ __device__ __forceinline__ void isect_chunk(IsectSmem& W, const CamConst& cc, co
             // M0^-1 y: beta = -y_k/dl_k, s_a = y_a + beta dl_a, s_b = y_b + beta dl_b
             const float db = -Ev[fk] * rk;
             const float nbt = b0 - db;
-            const float nsa = sa0 - (Ev[fa] + db * dl[fa]);
-            const float nsb = sb0 - (Ev[fb] + db * dl[fb]);
+            const float nsa = sa0 - (Ev[fa] + db * tdl[fa]);
+            const float nsb = sb0 - (Ev[fb] + db * tdl[fb]);
             const float step = fmaxf(fabsf(nsa - sa), fmaxf(fabsf(nsb - sb), fabsf((nbt - bt) * dk)));
             sa = nsa;
             sb = nsb;
             bt = nbt;
-            // contraction q = qf < 1/4: |x_{k+1} - x*| <= q/(1-q) |x_{k+1} - x_k|
+            // |x_{k+1} - x*| <= q/(1-q) |x_{k+1} - x_k|
             if (step * qfac < tol) {
-              conv = true;
+              done = true;
               break;
             }
           }
-          if (conv) {
-            if (sa < -FACE_TOL || sa > 1.0f + FACE_TOL || sb < -FACE_TOL || sb > 1.0f + FACE_TOL) continue;
-            if (nroots >= 4) {
-              ++face_fail;
-              continue;
-            }
+          if (done && sa >= -FACE_TOL && sa <= 1.0f + FACE_TOL && sb >= -FACE_TOL && sb <= 1.0f + FACE_TOL) {
             float xi[3];
             xi[fk] = (float)fside;
             xi[fa] = fminf(fmaxf(sa, 0.0f), 1.0f);
             xi[fb] = fminf(fmaxf(sb, 0.0f), 1.0f);
-            W.roots[nroots][0][lane] = bt;
-            W.roots[nroots][1][lane] = xi[0];
-            W.roots[nroots][2][lane] = xi[1];
-            W.roots[nroots][3][lane] = xi[2];
-            ++nroots;
-            continue;
-          }   // not converged (rounding floor for grazing rays): rigorous 2D path below
-        }
-      }
-      {
-        // project this face's 9 Bernstein points on d1, d2
-        const int k = f >> 1, side = f & 1;
-        const int ka = (k + 1) % 3, kb = (k + 2) % 3;
-        const int str[3] = {1, 3, 9};
-        const int base = 2 * side * str[k], sa = str[ka], sbb = str[kb];
-#pragma unroll
-        for (int jb = 0; jb < 3; ++jb)
-#pragma unroll
-          for (int ia = 0; ia < 3; ++ia) {
-            const int m = base + ia * sa + jb * sbb;
-            const float bx = sB[3 * m], by = sB[3 * m + 1], bz = sB[3 * m + 2];
-            sp[(2 * m) * 32] = fmaf(d1[0], bx, fmaf(d1[1], by, fmaf(d1[2], bz, -o1)));
-            sp[(2 * m + 1) * 32] = fmaf(d2[0], bx, fmaf(d2[1], by, fmaf(d2[2], bz, -o2)));
+            push_root(W, pl, bt, xi, face_fail);
           }
-      }
-      Patch pt;
-      load_patch(sp, f, pt);
-      if (hull_excludes_origin(pt)) continue;
-      int nf = 0;
-      float A11, A12, A21, A22, gcx, gcy;
-      const float q = injectivity_bound(pt, A11, A12, A21, A22, gcx, gcy);
-      int st = 0;
-      float s1 = 0.f, s2 = 0.f;
-      if (q < 1.0f) st = chord_root(pt, A11, A12, A21, A22, gcx, gcy, q, tol, max_it, s1, s2);
-      if (st == 1) {
-        if (s1 >= -FACE_TOL && s1 <= 1.0f + FACE_TOL && s2 >= -FACE_TOL && s2 <= 1.0f + FACE_TOL) {
-          su[0] = s1;
-          su[32] = s2;
-          nf = 1;
         }
-      } else if (st == 0) {
-        nf = face_roots_subdiv(sp, f, tol, max_it, su, 32, 4, &face_fail);
       }
-      const int k = f >> 1, side = f & 1;
-      const int ka = (k + 1) % 3, kb = (k + 2) % 3;
-      for (int t = 0; t < nf; ++t) {
-        float xi[3];
-        xi[k] = (float)side;
-        xi[ka] = fminf(fmaxf(su[(2 * t) * 32], 0.0f), 1.0f);
-        xi[kb] = fminf(fmaxf(su[(2 * t + 1) * 32], 0.0f), 1.0f);
-        float X[3];
-        eval_X(sB, xi, X);
-        const float beta = ((X[0] - P0[0]) * rf[0] + (X[1] - P0[1]) * rf[1] + (X[2] - P0[2]) * rf[2]) / rr;
-        if (nroots >= 4) {
-          ++face_fail;
-          continue;
+      if (!done) {
+        // rigorous 2D path (App. A.1): project the face on d1, d2 perpendicular to r
+        float ax[3] = {0.f, 0.f, 0.f};
+        {
+          const float a0 = fabsf(trf[0]), a1 = fabsf(trf[1]), a2 = fabsf(trf[2]);
+          ax[(a0 <= a1 && a0 <= a2) ? 0 : (a1 <= a2 ? 1 : 2)] = 1.0f;
         }
-        W.roots[nroots][0][lane] = beta;
-        W.roots[nroots][1][lane] = xi[0];
-        W.roots[nroots][2][lane] = xi[1];
-        W.roots[nroots][3][lane] = xi[2];
-        ++nroots;
+        float d1[3] = {trf[1] * ax[2] - trf[2] * ax[1], trf[2] * ax[0] - trf[0] * ax[2],
+                       trf[0] * ax[1] - trf[1] * ax[0]};
+        const float n1 = rsqrtf(d1[0] * d1[0] + d1[1] * d1[1] + d1[2] * d1[2]);
+        d1[0] *= n1; d1[1] *= n1; d1[2] *= n1;
+        float d2[3] = {trf[1] * d1[2] - trf[2] * d1[1], trf[2] * d1[0] - trf[0] * d1[2],
+                       trf[0] * d1[1] - trf[1] * d1[0]};
+        const float n2 = rsqrtf(d2[0] * d2[0] + d2[1] * d2[1] + d2[2] * d2[2]);
+        d2[0] *= n2; d2[1] *= n2; d2[2] *= n2;
+        const float o1 = d1[0] * tP0[0] + d1[1] * tP0[1] + d1[2] * tP0[2];
+        const float o2 = d2[0] * tP0[0] + d2[1] * tP0[1] + d2[2] * tP0[2];
+        Patch pt;
+        project_face(sB, f, d1, d2, o1, o2, pt);
+        if (!hull_excludes_origin(pt)) {
+          float su[8];
+          int nf = 0;
+          float A11, A12, A21, A22, gcx, gcy;
+          const float q = injectivity_bound(pt, A11, A12, A21, A22, gcx, gcy);
+          int st = 0;
+          float s1 = 0.f, s2 = 0.f;
+          if (q < 1.0f) st = chord_root(pt, A11, A12, A21, A22, gcx, gcy, q, tol, max_it, s1, s2);
+          if (st == 1) {
+            if (s1 >= -FACE_TOL && s1 <= 1.0f + FACE_TOL && s2 >= -FACE_TOL && s2 <= 1.0f + FACE_TOL) {
+              su[0] = s1;
+              su[1] = s2;
+              nf = 1;
+            }
+          } else if (st == 0) {
+            nf = face_roots_subdiv(pt, tol, max_it, su, 1, 4, &face_fail);
+          }
+          for (int z = 0; z < nf; ++z) {
+            float xi[3];
+            xi[fk] = (float)fside;
+            xi[fa] = fminf(fmaxf(su[2 * z], 0.0f), 1.0f);
+            xi[fb] = fminf(fmaxf(su[2 * z + 1], 0.0f), 1.0f);
+            float X[3];
+            eval_X(sB, xi, X);
+            const float beta =
+                ((X[0] - tP0[0]) * trf[0] + (X[1] - tP0[1]) * trf[1] + (X[2] - tP0[2]) * trf[2]) / trr;
+            push_root(W, pl, beta, xi, face_fail);
+          }
+        }
       }
     }
-    // sort (beta, index) with a 4-element network
-    if (nroots > 0) rb0 = W.roots[0][0][lane];
-    if (nroots > 1) rb1 = W.roots[1][0][lane];
-    if (nroots > 2) rb2 = W.roots[2][0][lane];
-    if (nroots > 3) rb3 = W.roots[3][0][lane];
+  }
+  __syncwarp();
+
+  // ---- 1c: per pixel: sort roots, pair entry/exit, emit items ---------------
+  int nroots = min(W.nroots[lane], 4);
+  float rb0 = 3.4e38f, rb1 = 3.4e38f, rb2 = 3.4e38f, rb3 = 3.4e38f;
+  int ri0 = 0, ri1 = 1, ri2 = 2, ri3 = 3;
+  if (nroots > 0) rb0 = W.roots[0][0][lane];
+  if (nroots > 1) rb1 = W.roots[1][0][lane];
+  if (nroots > 2) rb2 = W.roots[2][0][lane];
+  if (nroots > 3) rb3 = W.roots[3][0][lane];
 #define CSWAP(a, b, ia, ib) \
   if (b < a) {              \
     float tf = a;           \
@@ -887,10 +910,12 @@ __device__ __forceinline__ void isect_chunk(IsectSmem& W, const CamConst& cc, co
     ia = ib;                \
     ib = ti;                \
   }
-    CSWAP(rb0, rb1, ri0, ri1) CSWAP(rb2, rb3, ri2, ri3) CSWAP(rb0, rb2, ri0, ri2) CSWAP(rb1, rb3, ri1, ri3)
-    CSWAP(rb1, rb2, ri1, ri2)
+  CSWAP(rb0, rb1, ri0, ri1) CSWAP(rb2, rb3, ri2, ri3) CSWAP(rb0, rb2, ri0, ri2) CSWAP(rb1, rb3, ri1, ri3)
+  CSWAP(rb1, rb2, ri1, ri2)
 #undef CSWAP
+  {
     // dedupe roots found on two faces at a shared edge / vertex
+    const float rn = sqrtf(rr);
     const float hw = fabsf(sB[3 * 26] - sB[0]) + fabsf(sB[3 * 26 + 1] - sB[1]) + fabsf(sB[3 * 26 + 2] - sB[2]);
     const float dtol = 4e-6f * hw / rn;
     if (nroots > 1 && rb1 - rb0 < dtol) { rb1 = rb2; ri1 = ri2; rb2 = rb3; ri2 = ri3; rb3 = 3.4e38f; --nroots; }
@@ -927,172 +952,130 @@ __device__ __forceinline__ void isect_chunk(IsectSmem& W, const CamConst& cc, co
     }
     ++slot;
   }
+  __syncwarp();   // W is reused by the warp's next chunk
 }
 
-// ---- phase 2: integrate 32 items (one per lane) ----------------------------
+// ---- phase 2: integrate one item per lane ----------------------------------
 // The field at each GL node needs xi(x): chord iteration with
-// the element's J0^-1 at the midpoint, quadratic prediction through (entry,
-// midpoint, exit) for the nodes, then chord steps to the tolerance.  The
-// distinct elements of the 32 items (usually 1-3) are prepared once each.
-struct SegOut {
-  float an, af, a, b[3];
-  uint32_t pix;
-  int v;
-};
-
+// the element's J0^-1, started from a quadratic prediction through (entry,
+// midpoint, exit) xi (the midpoint solved first).  Chord map
+// T(xi) = xi + J0^-1 (t - X(xi)): |DT|_inf = |I - J0^-1 J|_inf <= 3 eta on the
+// element, so after a step s the error is <= q/(1-q) s (q = 3 eta); the
+// iteration stops when that bound is below tol (plain s < tol when q >= 1/2).
+// scr: this thread's scratch (stride CWARPS*32 floats) for the node values
 template <int P, int N>
-__device__ __forceinline__ bool integ_group(IntegSmem& W, const CamConst& cc, const TreeConst* __restrict__ trees,
-                                            const DevLeafView& L, const int32_t* __restrict__ vis,
-                                            const float4* __restrict__ items, int nitems, int g, int& fails,
-                                            SegOut& out) {
-  constexpr int NF = (P + 1) * (P + 1) * (P + 1);
-  const unsigned lane = threadIdx.x & 31;
+__device__ __forceinline__ void integ_item(const float* __restrict__ gs, const CamConst& cc, float4 i0, float4 i1,
+                                           float4 i2, float* __restrict__ scr, int& fails, float& a_out,
+                                           float b_out[3]) {
+  constexpr int ST = CWARPS * 32;
   const float tol = cc.newton_tol;
   const int max_it = cc.newton_max;
-  const int idx = g * 32 + (int)lane;
-  const bool act = idx < nitems;
-  float4 i0 = make_float4(0, 0, 0, 0), i1 = i0, i2 = i0, i3 = i0;
-  if (act) {
-    const float4* it = items + 4 * idx;
-    i0 = it[0];
-    i1 = it[1];
-    i2 = it[2];
-    i3 = it[3];
-  }
-  const int v = act ? __float_as_int(i3.w) : -1;
-  out.an = i3.x;
-  out.af = i3.y;
-  out.pix = __float_as_uint(i3.z);
-  out.v = v;
-  // prepare the distinct elements of this block (GSLOTS at a time)
-  unsigned pending = __ballot_sync(0xffffffffu, act);
-  while (pending) {
-    int myslot = -1;
-    int ns = 0;
-    while (pending && ns < GSLOTS) {
-      const int leader = __ffs(pending) - 1;
-      const int vl = __shfl_sync(0xffffffffu, v, leader);
-      prep_element(W.slot[ns], W.org, W.prep, trees, L, vis[vl], lane, NF, true);
-      const unsigned same = __ballot_sync(0xffffffffu, act && v == vl);
-      if (same & (1u << lane)) myslot = ns;
-      pending &= ~same;
-      ++ns;
+  const float* fs = gs + 84;
+  const float* afm = gs + SLOT_AFF;
+  float Ji[3][3];
+#pragma unroll
+  for (int aa = 0; aa < 3; ++aa)
+#pragma unroll
+    for (int b = 0; b < 3; ++b) Ji[aa][b] = afm[3 + 3 * aa + b];
+  const float q3 = 3.0f * afm[15] * 1.1f;
+  const float qfac = q3 < 0.5f ? q3 / (1.0f - q3) : 1.0f;
+  const float xin[3] = {i0.x, i0.y, i0.z}, xout[3] = {i0.w, i1.x, i1.y};
+  const float xia[3] = {i1.z, i1.w, i2.x}, xib[3] = {i2.y, i2.z, i2.w};
+  const float dX[3] = {xout[0] - xin[0], xout[1] - xin[1], xout[2] - xin[2]};
+  const float Lseg = sqrtf(dX[0] * dX[0] + dX[1] * dX[1] + dX[2] * dX[2]);   // physical length (R2)
+  float xm[3] = {0.5f * (xia[0] + xib[0]), 0.5f * (xia[1] + xib[1]), 0.5f * (xia[2] + xib[2])};
+  const float tm[3] = {xin[0] + 0.5f * dX[0], xin[1] + 0.5f * dX[1], xin[2] + 0.5f * dX[2]};
+  bool ok = false;
+#pragma unroll 1
+  for (int it = 0; it < 2 * max_it; ++it) {
+    float X[3];
+    eval_X(gs, xm, X);
+    const float r0 = tm[0] - X[0], r1 = tm[1] - X[1], r2 = tm[2] - X[2];
+    const float s0 = Ji[0][0] * r0 + Ji[0][1] * r1 + Ji[0][2] * r2;
+    const float s1 = Ji[1][0] * r0 + Ji[1][1] * r1 + Ji[1][2] * r2;
+    const float s2 = Ji[2][0] * r0 + Ji[2][1] * r1 + Ji[2][2] * r2;
+    xm[0] += s0;
+    xm[1] += s1;
+    xm[2] += s2;
+    if (fmaxf(fabsf(s0), fmaxf(fabsf(s1), fabsf(s2))) * qfac < tol) {
+      ok = true;
+      break;
     }
-    // integrate the lanes whose element is prepared in this round
-    if (myslot >= 0) {
-      const float* gs = W.slot[myslot];
-      float G[81];
-#pragma unroll
-      for (int m = 0; m < 81; ++m) G[m] = gs[m];
-      const float* fs = gs + 84;
-      const float* afm = gs + SLOT_AFF;
-      float Ji[3][3];
-#pragma unroll
-      for (int aa = 0; aa < 3; ++aa)
-#pragma unroll
-        for (int b = 0; b < 3; ++b) Ji[aa][b] = afm[3 + 3 * aa + b];
-      // chord map T(xi) = xi + J0^-1 (t - X(xi)): |DT|_inf = |I - J0^-1 J|_inf <= 3 eta on the
-      // element, so after a step s the error is <= q/(1-q) s (q = 3 eta); stop when that is
-      // below tol (the plain rule s < tol when q/(1-q) >= 1)
-      const float q3 = 3.0f * afm[15] * 1.1f;
-      const float qfac = q3 < 0.5f ? q3 / (1.0f - q3) : 1.0f;
-      const float xin[3] = {i0.x, i0.y, i0.z}, xout[3] = {i0.w, i1.x, i1.y};
-      const float xia[3] = {i1.z, i1.w, i2.x}, xib[3] = {i2.y, i2.z, i2.w};
-      const float dX[3] = {xout[0] - xin[0], xout[1] - xin[1], xout[2] - xin[2]};
-      const float Lseg = sqrtf(dX[0] * dX[0] + dX[1] * dX[1] + dX[2] * dX[2]);   // physical length (R2)
-      float xm[3] = {0.5f * (xia[0] + xib[0]), 0.5f * (xia[1] + xib[1]), 0.5f * (xia[2] + xib[2])};
-      const float tm[3] = {xin[0] + 0.5f * dX[0], xin[1] + 0.5f * dX[1], xin[2] + 0.5f * dX[2]};
-      bool ok = false;
-#pragma unroll 1
-      for (int it = 0; it < 2 * max_it; ++it) {
-        float X[3];
-        eval_Xr(G, xm, X);
-        const float r0 = tm[0] - X[0], r1 = tm[1] - X[1], r2 = tm[2] - X[2];
-        const float s0 = Ji[0][0] * r0 + Ji[0][1] * r1 + Ji[0][2] * r2;
-        const float s1 = Ji[1][0] * r0 + Ji[1][1] * r1 + Ji[1][2] * r2;
-        const float s2 = Ji[2][0] * r0 + Ji[2][1] * r1 + Ji[2][2] * r2;
-        xm[0] += s0;
-        xm[1] += s1;
-        xm[2] += s2;
-        if (fmaxf(fabsf(s0), fmaxf(fabsf(s1), fabsf(s2))) * qfac < tol) {
-          ok = true;
-          break;
-        }
-      }
-      if (!ok) ++fails;
-      float tau[N], ftv[N];
-#pragma unroll
-      for (int jj = 0; jj < N; ++jj) tau[jj] = ftv[jj] = 0.0f;
-      float sumk = 0.0f;
-#pragma unroll 1
-      for (int q = 0; q < N; ++q) {
-        const float u = cc.u[q];
-        const float l0 = (1.0f - u) * (1.0f - 2.0f * u), l1 = 4.0f * u * (1.0f - u), l2 = u * (2.0f * u - 1.0f);
-        float xi[3] = {l0 * xia[0] + l1 * xm[0] + l2 * xib[0], l0 * xia[1] + l1 * xm[1] + l2 * xib[1],
-                       l0 * xia[2] + l1 * xm[2] + l2 * xib[2]};
-        const float t0 = fmaf(u, dX[0], xin[0]), t1 = fmaf(u, dX[1], xin[1]), t2 = fmaf(u, dX[2], xin[2]);
-        bool conv = false;
-#pragma unroll 1
-        for (int it = 0; it < 2 * max_it; ++it) {
-          float X[3];
-          eval_Xr(G, xi, X);
-          const float r0 = t0 - X[0], r1 = t1 - X[1], r2 = t2 - X[2];
-          const float s0 = Ji[0][0] * r0 + Ji[0][1] * r1 + Ji[0][2] * r2;
-          const float s1 = Ji[1][0] * r0 + Ji[1][1] * r1 + Ji[1][2] * r2;
-          const float s2 = Ji[2][0] * r0 + Ji[2][1] * r1 + Ji[2][2] * r2;
-          xi[0] += s0;
-          xi[1] += s1;
-          xi[2] += s2;
-          if (fmaxf(fabsf(s0), fmaxf(fabsf(s1), fabsf(s2))) * qfac < tol) {
-            conv = true;
-            break;
-          }
-        }
-        if (!conv) ++fails;
-        xi[0] = fminf(fmaxf(xi[0], 0.0f), 1.0f);   // nodes lie inside the element
-        xi[1] = fminf(fmaxf(xi[1], 0.0f), 1.0f);
-        xi[2] = fminf(fmaxf(xi[2], 0.0f), 1.0f);
-        const float ft = field_at<P>(fs, xi[0], xi[1], xi[2]) * cc.inv_F;
-        const float kap = cc.kappa0 * ft * ft;
-        sumk = fmaf(cc.w[q], kap, sumk);
-#pragma unroll
-        for (int jj = 0; jj < N; ++jj) {
-          tau[jj] = fmaf(cc.S[jj * RC_MAX_N + q], kap, tau[jj]);
-          ftv[jj] = (jj == q) ? ft : ftv[jj];
-        }
-      }
-      // a = exp(-L sum w kappa); b_c = L sum w_j q_cj exp(-tau_j)
-      out.a = __expf(-Lseg * sumk);
-      float E0 = 0.0f, E1 = 0.0f;
-#pragma unroll
-      for (int jj = 0; jj < N; ++jj) {
-        const float ee = cc.w[jj] * __expf(-Lseg * tau[jj]);
-        E0 += ee;
-        E1 = fmaf(ee, ftv[jj], E1);
-      }
-      const float sc = 0.5f * Lseg * cc.q0;
-      out.b[0] = sc * (E0 + E1);
-      out.b[1] = sc * (E0 - E1);
-      out.b[2] = sc * E0;
-    }
-    __syncwarp();
   }
-  return act;
+  if (!ok) ++fails;
+  float sumk = 0.0f;
+#pragma unroll 1
+  for (int q = 0; q < N; ++q) {
+    const float u = cc.u[q];
+    const float l0 = (1.0f - u) * (1.0f - 2.0f * u), l1 = 4.0f * u * (1.0f - u), l2 = u * (2.0f * u - 1.0f);
+    float xi[3] = {l0 * xia[0] + l1 * xm[0] + l2 * xib[0], l0 * xia[1] + l1 * xm[1] + l2 * xib[1],
+                   l0 * xia[2] + l1 * xm[2] + l2 * xib[2]};
+    const float t0 = fmaf(u, dX[0], xin[0]), t1 = fmaf(u, dX[1], xin[1]), t2 = fmaf(u, dX[2], xin[2]);
+    bool conv = false;
+#pragma unroll 1
+    for (int it = 0; it < 2 * max_it; ++it) {
+      float X[3];
+      eval_X(gs, xi, X);
+      const float r0 = t0 - X[0], r1 = t1 - X[1], r2 = t2 - X[2];
+      const float s0 = Ji[0][0] * r0 + Ji[0][1] * r1 + Ji[0][2] * r2;
+      const float s1 = Ji[1][0] * r0 + Ji[1][1] * r1 + Ji[1][2] * r2;
+      const float s2 = Ji[2][0] * r0 + Ji[2][1] * r1 + Ji[2][2] * r2;
+      xi[0] += s0;
+      xi[1] += s1;
+      xi[2] += s2;
+      if (fmaxf(fabsf(s0), fmaxf(fabsf(s1), fabsf(s2))) * qfac < tol) {
+        conv = true;
+        break;
+      }
+    }
+    if (!conv) ++fails;
+    xi[0] = fminf(fmaxf(xi[0], 0.0f), 1.0f);   // nodes lie inside the element
+    xi[1] = fminf(fmaxf(xi[1], 0.0f), 1.0f);
+    xi[2] = fminf(fmaxf(xi[2], 0.0f), 1.0f);
+    const float ft = field_at<P>(fs, xi[0], xi[1], xi[2]) * cc.inv_F;
+    const float kap = cc.kappa0 * ft * ft;
+    sumk = fmaf(cc.w[q], kap, sumk);
+    scr[q * ST] = ft;
+  }
+  // node optical depths tau_j = L sum_k S_jk kappa_k
+  float tau[N], ftv[N];
+#pragma unroll
+  for (int q = 0; q < N; ++q) ftv[q] = scr[q * ST];
+#pragma unroll
+  for (int jj = 0; jj < N; ++jj) {
+    tau[jj] = 0.0f;
+#pragma unroll
+    for (int q = 0; q < N; ++q) tau[jj] = fmaf(cc.S[jj * RC_MAX_N + q], cc.kappa0 * ftv[q] * ftv[q], tau[jj]);
+  }
+  // a = exp(-L sum w kappa); b_c = L sum w_j q_cj exp(-tau_j)
+  a_out = __expf(-Lseg * sumk);
+  float E0 = 0.0f, E1 = 0.0f;
+#pragma unroll
+  for (int jj = 0; jj < N; ++jj) {
+    const float ee = cc.w[jj] * __expf(-Lseg * tau[jj]);
+    E0 += ee;
+    E1 = fmaf(ee, ftv[jj], E1);
+  }
+  const float sc = 0.5f * Lseg * cc.q0;
+  b_out[0] = sc * (E0 + E1);
+  b_out[1] = sc * (E0 - E1);
+  b_out[2] = sc * E0;
 }
 
 // ---- the kernel --------------------------------------------------------------
 template <int P, int N>
-__global__ void __launch_bounds__(CWARPS * 32, 3) k_cast_curved(CamConst cc, const TreeConst* __restrict__ trees,
+__global__ void __launch_bounds__(CWARPS * 32, CAST_CTAS_PER_SM) k_cast_curved(CamConst cc, const TreeConst* __restrict__ trees,
                                                                 DevLeafView L, const int32_t* __restrict__ vis,
                                                                 const Rect16* __restrict__ vrect,
                                                                 const int64_t* __restrict__ chunk_off,
                                                                 const int32_t* __restrict__ chunk_elem,
                                                                 const Unit* __restrict__ units, int64_t nunits,
-                                                                int64_t nchunks, int fold, uint32_t key_base,
+                                                                int fold, uint32_t key_base,
                                                                 unsigned char* __restrict__ scratch,
                                                                 rc_seg* __restrict__ out, int64_t out_cap,
                                                                 int32_t* __restrict__ hits_pp,
                                                                 int64_t* __restrict__ counters) {
+  constexpr int NF = (P + 1) * (P + 1) * (P + 1);
   extern __shared__ __align__(16) unsigned char smem_raw[];
   CastSmem& S = *reinterpret_cast<CastSmem*>(smem_raw);
   __shared__ CastCtl ctl;
@@ -1115,142 +1098,148 @@ __global__ void __launch_bounds__(CWARPS * 32, 3) k_cast_curved(CamConst cc, con
     __syncthreads();
     const int64_t u = ctl.unit;
     if (u >= nunits) break;
-    int64_t cb;
-    int nch;
-    uint32_t ukey = 0;
-    if (fold > 0) {
-      const Unit U = units[u];
-      cb = U.chunk_begin;
-      nch = U.nchunks;
-      ukey = U.key;
-    } else {
-      cb = u * RC_UNIT_CHUNKS;
-      nch = (int)min((int64_t)RC_UNIT_CHUNKS, nchunks - cb);
-    }
-    // ---- phase 1: intersection ----------------------------------------------
+    const Unit U = units[u];
+    // ---- phase 0: the unit's elements into shared memory ---------------------
+    for (int w = warp; w < U.nvis; w += CWARPS)
+      prep_element(S.slot[w], S.org[w], S.ph.prep[warp].prep, trees, L, vis[U.vfirst + w], lane, NF, true);
+    __syncthreads();
+    // ---- phase 1: intersection -----------------------------------------------
     {
-      IsectSmem& W = S.isect[warp];
-      int cur_v = -1;
+      WarpIsect& W = S.ph.isect[warp];
       for (;;) {
         int k = 0;
         if (lane == 0) k = atomicAdd(&ctl.next_chunk, 1);
         k = __shfl_sync(0xffffffffu, k, 0);
-        if (k >= nch) break;
-        isect_chunk(W, cc, trees, L, vis, vrect, chunk_off, chunk_elem, cb + k, cur_v, items, &ctl.nitems, hits_pp,
+        if (k >= U.nchunks) break;
+        const int64_t c = U.chunk_begin + k;
+        const int v = chunk_elem[c];
+        const int lv = v - U.vfirst;
+        isect_chunk(W, S.slot[lv], S.org[lv], cc, vrect[v], c - chunk_off[v], v, items, &ctl.nitems, hits_pp,
                     local_hits, face_fail);
       }
     }
     __syncthreads();
     const int nitems = min(ctl.nitems, ITEM_CAP);
     raw_local += (tid == 0) ? nitems : 0;
-    const bool do_fold = fold > 0 && nitems <= SORT_CAP;
-    // ---- phase 2: integration -----------------------------------------------
+    // ---- phase 2: integration ---------------------------------------------------
     {
-      IntegSmem& W = S.integ[warp];
       const int ngroups = (nitems + 31) / 32;
       for (int g = warp; g < ngroups; g += CWARPS) {
-        SegOut o;
-        const bool act = integ_group<P, N>(W, cc, trees, L, vis, items, nitems, g, fails, o);
-        if (do_fold) {
+        const int idx = g * 32 + (int)lane;
+        const bool act = idx < nitems;
+        float a = 1.0f, bb[3] = {0.f, 0.f, 0.f};
+        uint32_t pix = 0;
+        float an = 0.f, afar = 0.f;
+        int v = 0;
+        if (act) {
+          const float4* it = items + 4 * idx;
+          const float4 i0 = it[0], i1 = it[1], i2 = it[2], i3 = it[3];
+          v = __float_as_int(i3.w);
+          pix = __float_as_uint(i3.z);
+          an = i3.x;
+          afar = i3.y;
+          integ_item<P, N>(S.slot[v - U.vfirst], cc, i0, i1, i2, S.ph.scr + tid, fails, a, bb);
+        }
+        if (fold > 0) {
           if (act) {
-            const int idx = g * 32 + (int)lane;
-            store_seg(segs + idx, o.pix, o.an, o.af, o.a, o.b, ukey);
-            keys[idx] = fold_key(o.pix, o.an);
+            store_seg(segs + idx, pix, an, afar, a, bb, U.key);
+            keys[idx] = fold_key(pix, an);
           }
         } else {
-          // every segment is a record: leaf key without folding, node key for an
-          // over-full fold unit (SORT_CAP exceeded, counted)
-          const uint32_t k = fold > 0 ? ukey : key_base + (uint32_t)(act ? vis[o.v] : 0);
           const int64_t slot = warp_append(&counters[CNT_SEGS], act ? 1 : 0);
           if (act) {
-            if (slot < out_cap) store_seg(out + slot, o.pix, o.an, o.af, o.a, o.b, k);
+            if (slot < out_cap) store_seg(out + slot, pix, an, afar, a, bb, key_base + (uint32_t)vis[v]);
             else atomicAdd((unsigned long long*)&counters[CNT_OVERFLOW], 1ull);
           }
         }
       }
     }
-    if (fold > 0 && !do_fold && tid == 0) atomicAdd((unsigned long long*)&counters[CNT_UNFOLDED], 1ull);
-    if (!do_fold) continue;   // next unit (the loop head synchronises first)
+    if (fold == 0) continue;   // next unit (the loop head synchronises first)
     __syncthreads();
-    // ---- phase 3: fold -------------------------------------------------------
-    int m = 1;
-    while (m < nitems) m <<= 1;
-    for (int k = tid; k < m; k += CWARPS * 32) {
-      S.sort.key[k] = k < nitems ? keys[k] : ~0ull;
-      S.sort.idx[k] = (uint16_t)k;
-    }
-    __syncthreads();
-    for (int size = 2; size <= m; size <<= 1) {
-      for (int stride = size >> 1; stride > 0; stride >>= 1) {
-        for (int k = tid; k < m; k += CWARPS * 32) {
-          const int p = k ^ stride;
-          if (p > k) {
-            const bool up = (k & size) == 0;
-            const unsigned long long ka = S.sort.key[k], kb = S.sort.key[p];
-            if ((ka > kb) == up) {
-              S.sort.key[k] = kb;
-              S.sort.key[p] = ka;
-              const uint16_t t2 = S.sort.idx[k];
-              S.sort.idx[k] = S.sort.idx[p];
-              S.sort.idx[p] = t2;
+    // ---- phase 3: fold (batches of SORT_CAP segments) ---------------------------
+    for (int b0 = 0; b0 < nitems; b0 += SORT_CAP) {
+      const int n = min(SORT_CAP, nitems - b0);
+      int m = 1;
+      while (m < n) m <<= 1;
+      __syncthreads();
+      for (int k = tid; k < m; k += CWARPS * 32) {
+        S.ph.sort.key[k] = k < n ? keys[b0 + k] : ~0ull;
+        S.ph.sort.idx[k] = (uint16_t)k;
+      }
+      __syncthreads();
+      for (int size = 2; size <= m; size <<= 1) {
+        for (int stride = size >> 1; stride > 0; stride >>= 1) {
+          for (int k = tid; k < m; k += CWARPS * 32) {
+            const int p = k ^ stride;
+            if (p > k) {
+              const bool up = (k & size) == 0;
+              const unsigned long long ka = S.ph.sort.key[k], kb = S.ph.sort.key[p];
+              if ((ka > kb) == up) {
+                S.ph.sort.key[k] = kb;
+                S.ph.sort.key[p] = ka;
+                const uint16_t t2 = S.ph.sort.idx[k];
+                S.ph.sort.idx[k] = S.ph.sort.idx[p];
+                S.ph.sort.idx[p] = t2;
+              }
             }
           }
+          __syncthreads();
         }
-        __syncthreads();
+      }
+      const rc_seg* bs = segs + b0;
+      // run heads: new pixel, or a gap / overlap beyond the tolerance
+      auto is_head = [&](int k) -> bool {
+        if (k == 0) return true;
+        if ((S.ph.sort.key[k] >> 32) != (S.ph.sort.key[k - 1] >> 32)) return true;
+        const float an2 = bs[S.ph.sort.idx[k]].alpha_near, afp = bs[S.ph.sort.idx[k - 1]].alpha_far;
+        return fabsf(an2 - afp) > FOLD_TAU * fmaxf(1.0f, fabsf(an2));
+      };
+      const int per = (n + CWARPS * 32 - 1) / (CWARPS * 32);
+      const int k0 = min(n, tid * per), k1 = min(n, k0 + per);
+      int nh = 0;
+      for (int k = k0; k < k1; ++k) nh += is_head(k) ? 1 : 0;
+      int incl = nh;
+#pragma unroll
+      for (int off = 1; off < 32; off <<= 1) {
+        const int y = __shfl_up_sync(0xffffffffu, incl, off);
+        if ((int)lane >= off) incl += y;
+      }
+      if (lane == 31) ctl.warp_sum[warp] = incl;
+      __syncthreads();
+      int wbase = 0, total = 0;
+#pragma unroll
+      for (int w = 0; w < CWARPS; ++w) {
+        wbase += w < warp ? ctl.warp_sum[w] : 0;
+        total += ctl.warp_sum[w];
+      }
+      if (tid == 0) ctl.base = atomicAdd((unsigned long long*)&counters[CNT_SEGS], (unsigned long long)total);
+      __syncthreads();
+      int64_t pos = (int64_t)ctl.base + wbase + incl - nh;
+      for (int k = k0; k < k1; ++k) {
+        if (!is_head(k)) continue;
+        const rc_seg& s0 = bs[S.ph.sort.idx[k]];
+        double A = 1.0, B0 = 0.0, B1 = 0.0, B2 = 0.0;
+        float afr = s0.alpha_far;
+        int q = k;
+        do {
+          const rc_seg& sq = bs[S.ph.sort.idx[q]];
+          B0 = fma(A, (double)sq.b[0], B0);
+          B1 = fma(A, (double)sq.b[1], B1);
+          B2 = fma(A, (double)sq.b[2], B2);
+          A *= (double)sq.a;
+          afr = sq.alpha_far;
+          ++q;
+        } while (q < n && !is_head(q));
+        if (pos < out_cap) {
+          const float bf[3] = {(float)B0, (float)B1, (float)B2};
+          store_seg(out + pos, s0.pixel, s0.alpha_near, afr, (float)A, bf, U.key);
+        } else {
+          atomicAdd((unsigned long long*)&counters[CNT_OVERFLOW], 1ull);
+        }
+        ++pos;
       }
     }
-    // run heads: new pixel, or a gap / overlap beyond the tolerance
-    auto is_head = [&](int k) -> bool {
-      if (k == 0) return true;
-      if ((S.sort.key[k] >> 32) != (S.sort.key[k - 1] >> 32)) return true;
-      const float an = segs[S.sort.idx[k]].alpha_near, afp = segs[S.sort.idx[k - 1]].alpha_far;
-      return fabsf(an - afp) > FOLD_TAU * fmaxf(1.0f, fabsf(an));
-    };
-    const int per = (nitems + CWARPS * 32 - 1) / (CWARPS * 32);
-    const int k0 = min(nitems, tid * per), k1 = min(nitems, k0 + per);
-    int nh = 0;
-    for (int k = k0; k < k1; ++k) nh += is_head(k) ? 1 : 0;
-    // block exclusive scan of the head counts
-    int incl = nh;
-#pragma unroll
-    for (int off = 1; off < 32; off <<= 1) {
-      const int y = __shfl_up_sync(0xffffffffu, incl, off);
-      if ((int)lane >= off) incl += y;
-    }
-    if (lane == 31) ctl.warp_sum[warp] = incl;
-    __syncthreads();
-    int wbase = 0, total = 0;
-#pragma unroll
-    for (int w = 0; w < CWARPS; ++w) {
-      wbase += w < warp ? ctl.warp_sum[w] : 0;
-      total += ctl.warp_sum[w];
-    }
-    if (tid == 0) ctl.base = atomicAdd((unsigned long long*)&counters[CNT_SEGS], (unsigned long long)total);
-    __syncthreads();
-    int64_t pos = (int64_t)ctl.base + wbase + incl - nh;
-    for (int k = k0; k < k1; ++k) {
-      if (!is_head(k)) continue;
-      const rc_seg& s0 = segs[S.sort.idx[k]];
-      double A = 1.0, B0 = 0.0, B1 = 0.0, B2 = 0.0;
-      float af = s0.alpha_far;
-      int q = k;
-      do {
-        const rc_seg& s = segs[S.sort.idx[q]];
-        B0 = fma(A, (double)s.b[0], B0);
-        B1 = fma(A, (double)s.b[1], B1);
-        B2 = fma(A, (double)s.b[2], B2);
-        A *= (double)s.a;
-        af = s.alpha_far;
-        ++q;
-      } while (q < nitems && !is_head(q));
-      if (pos < out_cap) {
-        const float bb[3] = {(float)B0, (float)B1, (float)B2};
-        store_seg(out + pos, s0.pixel, s0.alpha_near, af, (float)A, bb, ukey);
-      } else {
-        atomicAdd((unsigned long long*)&counters[CNT_OVERFLOW], 1ull);
-      }
-      ++pos;
-    }
+    if (tid == 0 && nitems > SORT_CAP) atomicAdd((unsigned long long*)&counters[CNT_UNFOLDED], 1ull);
   }
 #pragma unroll
   for (int off = 16; off > 0; off >>= 1) {
@@ -1270,13 +1259,13 @@ __global__ void __launch_bounds__(CWARPS * 32, 3) k_cast_curved(CamConst cc, con
 }  // namespace
 
 size_t cast_curved_scratch_per_cta() { return SCR_PER_CTA; }
-int cast_curved_ctas_per_sm() { return 3; }
+int cast_curved_ctas_per_sm() { return CAST_CTAS_PER_SM; }
 
 template <int P, int N>
 static cudaError_t cast_PN(const CamConst& cc, const TreeConst* trees, DevLeafView L, const int32_t* vis,
                            const Rect16* vrect, const int64_t* chunk_off, const int32_t* chunk_elem, const Unit* units,
-                           int64_t nunits, int64_t nchunks, int fold, uint32_t key_base, void* scratch, rc_seg* out,
-                           int64_t out_cap, int32_t* hits_pp, int64_t* counters, int grid, cudaStream_t s) {
+                           int64_t nunits, int fold, uint32_t key_base, void* scratch, rc_seg* out, int64_t out_cap,
+                           int32_t* hits_pp, int64_t* counters, int grid, cudaStream_t s) {
   const size_t smem = sizeof(CastSmem);
   static bool attr = false;
   if (!attr) {
@@ -1285,21 +1274,21 @@ static cudaError_t cast_PN(const CamConst& cc, const TreeConst* trees, DevLeafVi
     attr = true;
   }
   k_cast_curved<P, N><<<grid, CWARPS * 32, smem, s>>>(cc, trees, L, vis, vrect, chunk_off, chunk_elem, units, nunits,
-                                                      nchunks, fold, key_base, (unsigned char*)scratch, out, out_cap,
-                                                      hits_pp, counters);
+                                                      fold, key_base, (unsigned char*)scratch, out, out_cap, hits_pp,
+                                                      counters);
   return cudaGetLastError();
 }
 
 cudaError_t launch_cast_curved(const CamConst& cc, const TreeConst* trees, DevLeafView L, int P, const int32_t* vis,
                                const Rect16* vrect, const int64_t* chunk_off, const int32_t* chunk_elem,
-                               const Unit* units, int64_t nunits, int64_t nchunks, int fold, uint32_t key_base,
-                               void* scratch, rc_seg* out, int64_t out_cap, int32_t* hits_pp, int64_t* counters,
-                               int grid, cudaStream_t s) {
+                               const Unit* units, int64_t nunits, int fold, uint32_t key_base, void* scratch,
+                               rc_seg* out, int64_t out_cap, int32_t* hits_pp, int64_t* counters, int grid,
+                               cudaStream_t s) {
   ++g_launches;
-#define CASE(PP, NN)                                                                                               \
-  if (P == PP && cc.N == NN)                                                                                       \
-    return cast_PN<PP, NN>(cc, trees, L, vis, vrect, chunk_off, chunk_elem, units, nunits, nchunks, fold, key_base, \
-                           scratch, out, out_cap, hits_pp, counters, grid, s);
+#define CASE(PP, NN)                                                                                             \
+  if (P == PP && cc.N == NN)                                                                                     \
+    return cast_PN<PP, NN>(cc, trees, L, vis, vrect, chunk_off, chunk_elem, units, nunits, fold, key_base, scratch, \
+                           out, out_cap, hits_pp, counters, grid, s);
   CASE(1, 1) CASE(1, 2) CASE(1, 3) CASE(1, 4) CASE(1, 5) CASE(1, 6) CASE(1, 7) CASE(1, 8)
   CASE(2, 1) CASE(2, 2) CASE(2, 3) CASE(2, 4) CASE(2, 5) CASE(2, 6) CASE(2, 7) CASE(2, 8)
 #undef CASE

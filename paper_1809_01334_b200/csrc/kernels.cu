@@ -209,30 +209,53 @@ __global__ void k_expand(const int64_t* __restrict__ off, const int64_t* __restr
   for (int64_t c = off[v]; c < off[v + 1]; ++c) chunk_elem[c] = (int32_t)v;
 }
 
-// Fold units of the curved segment kernel (row a6): every node of the fold
-// level with visible leaves -> ceil(chunks / RC_UNIT_CHUNKS) units of about
-// equal size.  Nodes are contiguous in the visible list (SFC order).
-__global__ void k_unit_count(const int32_t* __restrict__ vis, const int64_t* __restrict__ nvis_p,
-                             const int32_t* __restrict__ leaf_node, const int64_t* __restrict__ chunk_off,
-                             int32_t* __restrict__ ucnt, int32_t* __restrict__ uend) {
-  const int64_t nvis = *nvis_p;
-  const int64_t v = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-  if (v >= nvis) return;
-  const int32_t nd = leaf_node[vis[v]];
-  if (v > 0 && leaf_node[vis[v - 1]] == nd) {
-    ucnt[v] = 0;
-    return;
+// Fold units of the curved segment kernel (row a6): the visible leaves of
+// every node of the fold level (contiguous in the visible list, SFC order)
+// are cut into <= RC_UNIT_LEAVES-leaf windows, and each window into
+// <= RC_UNIT_CHUNKS-chunk pieces of about equal size.  Without folding
+// (leaf_node == nullptr) the windows are 64 consecutive visible leaves.
+struct NodeRun {
+  int64_t v0, v1;   // visible range of the node
+};
+
+__device__ __forceinline__ NodeRun node_run(const int32_t* __restrict__ vis, const int32_t* __restrict__ leaf_node,
+                                            int64_t nvis, int64_t v, bool& start) {
+  if (!leaf_node) {
+    start = (v % RC_UNIT_LEAVES) == 0;
+    return NodeRun{v, min(nvis, v + RC_UNIT_LEAVES)};
   }
-  // end of the node's visible run: first w > v with another node (monotone)
+  const int32_t nd = leaf_node[vis[v]];
+  start = v == 0 || leaf_node[vis[v - 1]] != nd;
+  if (!start) return NodeRun{v, v};
   int64_t lo = v, hi = nvis;   // leaf_node[vis[lo]] == nd, hi is past the run
   while (hi - lo > 1) {
     const int64_t mid = (lo + hi) >> 1;
     if (leaf_node[vis[mid]] == nd) lo = mid;
     else hi = mid;
   }
-  uend[v] = (int32_t)hi;
-  const int64_t nch = chunk_off[hi] - chunk_off[v];
-  ucnt[v] = (int32_t)((nch + RC_UNIT_CHUNKS - 1) / RC_UNIT_CHUNKS);
+  return NodeRun{v, hi};
+}
+
+__global__ void k_unit_count(const int32_t* __restrict__ vis, const int64_t* __restrict__ nvis_p,
+                             const int32_t* __restrict__ leaf_node, const int64_t* __restrict__ chunk_off,
+                             int32_t* __restrict__ ucnt, int32_t* __restrict__ uend) {
+  const int64_t nvis = *nvis_p;
+  const int64_t v = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (v >= nvis) return;
+  bool start;
+  const NodeRun r = node_run(vis, leaf_node, nvis, v, start);
+  if (!start) {
+    ucnt[v] = 0;
+    return;
+  }
+  uend[v] = (int32_t)r.v1;
+  const int64_t nl = r.v1 - r.v0, nw = (nl + RC_UNIT_LEAVES - 1) / RC_UNIT_LEAVES;
+  int64_t nu = 0;
+  for (int64_t w = 0; w < nw; ++w) {
+    const int64_t a = r.v0 + nl * w / nw, b = r.v0 + nl * (w + 1) / nw;
+    nu += (chunk_off[b] - chunk_off[a] + RC_UNIT_CHUNKS - 1) / RC_UNIT_CHUNKS;
+  }
+  ucnt[v] = (int32_t)nu;
 }
 
 __global__ void k_unit_emit(const int32_t* __restrict__ vis, const int64_t* __restrict__ nvis_p,
@@ -243,13 +266,18 @@ __global__ void k_unit_emit(const int32_t* __restrict__ vis, const int64_t* __re
   const int64_t nvis = *nvis_p;
   const int64_t v = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (v >= nvis) return;
-  const int64_t nu = ucnt[v];
-  if (nu == 0) return;
-  const int64_t c0 = chunk_off[v], nch = chunk_off[uend[v]] - c0;
-  const uint32_t key = key_base + (uint32_t)node_first[leaf_node[vis[v]]];
-  for (int64_t k = 0; k < nu; ++k) {
-    const int64_t a = c0 + nch * k / nu, b = c0 + nch * (k + 1) / nu;
-    units[uoff[v] + k] = Unit{a, (int32_t)(b - a), key};
+  if (ucnt[v] == 0) return;
+  const int64_t v1 = uend[v], nl = v1 - v, nw = (nl + RC_UNIT_LEAVES - 1) / RC_UNIT_LEAVES;
+  const uint32_t key = leaf_node ? key_base + (uint32_t)node_first[leaf_node[vis[v]]] : 0u;
+  int64_t out = uoff[v];
+  for (int64_t w = 0; w < nw; ++w) {
+    const int64_t a = v + nl * w / nw, b = v + nl * (w + 1) / nw;
+    const int64_t c0 = chunk_off[a], nch = chunk_off[b] - c0;
+    const int64_t nu = (nch + RC_UNIT_CHUNKS - 1) / RC_UNIT_CHUNKS;
+    for (int64_t k = 0; k < nu; ++k) {
+      const int64_t ca = c0 + nch * k / nu, cb = c0 + nch * (k + 1) / nu;
+      units[out++] = Unit{ca, (int32_t)(cb - ca), key, (int32_t)a, (int32_t)(b - a), 0};
+    }
   }
 }
 

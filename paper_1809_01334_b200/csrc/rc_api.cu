@@ -481,22 +481,26 @@ extern "C" rc_status rc_cast_segments(rc_forest* f, int32_t fold_levels, void* s
   if (nvis > 0) CU(launch_expand(f->d_chunk_off, f->d_scan + n, nvis, f->d_chunk_elem, s));
   const bool curved = !f->all_affine;
   const uint32_t key_base = (uint32_t)f->first_global;
-  // fold units (curved path): nodes of the fold level cut into <= RC_UNIT_CHUNKS chunks
-  int64_t nunits = (f->h_chunks + RC_UNIT_CHUNKS - 1) / RC_UNIT_CHUNKS;
-  if (curved && fold_levels > 0 && nvis > 0) {
-    CU(build_leaf_node(f, fold_levels, s));
+  // fold units (curved path): the visible leaves of every node of the fold
+  // level (64-leaf windows without folding) cut into <= 64 leaves and
+  // <= RC_UNIT_CHUNKS chunks
+  int64_t nunits = 0;
+  if (curved && nvis > 0) {
+    if (fold_levels > 0) CU(build_leaf_node(f, fold_levels, s));
+    const int32_t* leaf_node = fold_levels > 0 ? f->d_leaf_node : nullptr;
+    const int32_t* node_first = fold_levels > 0 ? f->d_node_first[fold_levels] : nullptr;
     if (!f->d_ucnt) {
       CU(cudaMalloc((void**)&f->d_ucnt, sizeof(int32_t) * (n + 1)));
       CU(cudaMalloc((void**)&f->d_uoff, sizeof(int64_t) * (n + 1)));
       CU(cudaMalloc((void**)&f->d_uend, sizeof(int32_t) * (n + 1)));
     }
-    CU(launch_units(f->d_vis, f->d_scan + n, nvis, f->d_leaf_node, f->d_node_first[fold_levels], f->d_chunk_off,
-                    f->d_ucnt, f->d_uoff, f->d_uend, f->d_scan_tmp, key_base, nullptr, false, s));
+    CU(launch_units(f->d_vis, f->d_scan + n, nvis, leaf_node, node_first, f->d_chunk_off, f->d_ucnt, f->d_uoff,
+                    f->d_uend, f->d_scan_tmp, key_base, nullptr, false, s));
     CU(cudaMemcpyAsync(&nunits, f->d_uoff + nvis, sizeof(int64_t), cudaMemcpyDeviceToHost, s));
     CU(cudaStreamSynchronize(s));
     CU(grow(&f->d_units, &f->units_cap, std::max<int64_t>(nunits, 1)));
-    CU(launch_units(f->d_vis, f->d_scan + n, nvis, f->d_leaf_node, f->d_node_first[fold_levels], f->d_chunk_off,
-                    f->d_ucnt, f->d_uoff, f->d_uend, f->d_scan_tmp, key_base, f->d_units, true, s));
+    CU(launch_units(f->d_vis, f->d_scan + n, nvis, leaf_node, node_first, f->d_chunk_off, f->d_ucnt, f->d_uoff,
+                    f->d_uend, f->d_scan_tmp, key_base, f->d_units, true, s));
   }
   f->h_units = curved ? nunits : 0;
   const int grid_curved = sm_count() * cast_curved_ctas_per_sm();
@@ -522,9 +526,8 @@ extern "C" rc_status rc_cast_segments(rc_forest* f, int32_t fold_levels, void* s
                               f->d_counters, sm_count() * 8, s));
       } else {
         CU(launch_cast_curved(f->cc, f->d_trees, leaf_view(f), f->P, f->d_vis, f->d_vis_rect, f->d_chunk_off,
-                              f->d_chunk_elem, fold_levels > 0 ? f->d_units : nullptr, nunits, f->h_chunks,
-                              fold_levels, key_base, f->d_scratch, f->d_segs, f->seg_cap, f->d_hits_pp,
-                              f->d_counters, grid_curved, s));
+                              f->d_chunk_elem, f->d_units, nunits, fold_levels, key_base, f->d_scratch,
+                              f->d_segs, f->seg_cap, f->d_hits_pp, f->d_counters, grid_curved, s));
       }
     }
     CU(cudaEventRecord(f->ev1, s));

@@ -12,13 +12,17 @@
 #define RC_CHUNK 32         // candidate pairs per warp work item (one element)
 #define RC_NODE_LEVELS 8    // coarsening levels of the node tables (fold + aggregation cycles)
 #define RC_UNIT_CHUNKS 128  // chunks per fold unit of the curved segment kernel (<= 4096 pairs)
+#define RC_UNIT_LEAVES 64   // visible leaves per fold unit (their geometry is staged in shared memory)
 
 // Fold unit of the curved segment kernel (row a6): a contiguous chunk range
-// inside one node of the fold level (or any 128 chunks when not folding).
+// of at most RC_UNIT_LEAVES visible leaves [vfirst, vfirst+nvis) inside one
+// node of the fold level (64 consecutive visible leaves when not folding).
 struct __align__(16) Unit {
   int64_t chunk_begin;
   int32_t nchunks;
-  uint32_t key;                 // global SFC index of the node's first leaf
+  uint32_t key;                 // global SFC index of the node's first leaf (0 when not folding)
+  int32_t vfirst, nvis;         // visible-leaf window holding the unit's chunks
+  int64_t pad;
 };
 
 // node k of a level owns leaves [first[k], first[k+1]); returns k for leaf e

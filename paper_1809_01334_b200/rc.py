@@ -10,7 +10,7 @@ from typing import Optional, Sequence
 import numpy as np
 
 HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(HERE, "librc.so")
+LIB_PATH = os.environ.get("RC_LIB") or os.path.join(HERE, "librc.so")   # RC_LIB: an in-tree build variant
 
 RC_OK = 0
 RC_ERR_CAPACITY = -6
