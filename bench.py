@@ -296,7 +296,8 @@ def main():
     newton_failures = seg_info["newton_failures"]
     fold_info = {"fold_levels": fold, "records": seg_info["count"], "raw_segments": seg_info["raw_segments"],
                  "record_level": seg_info["level"], "units": seg_info["units"],
-                 "unfolded_units": seg_info["unfolded_units"]}
+                 "unfolded_units": seg_info["unfolded_units"], "face_tasks": seg_info["face_tasks"],
+                 "fallback_tasks": seg_info["fallback_tasks"]}
     forest.close()          # release the device-resident forest before the e2e forests
     del forest
     torch.cuda.empty_cache()

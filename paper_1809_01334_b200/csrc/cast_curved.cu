@@ -72,6 +72,39 @@ __device__ __forceinline__ void eval_X(const float* __restrict__ sB, const float
   }
 }
 
+// Two points at once (independent FMA chains, each control point loaded once).
+__device__ __forceinline__ void eval_X2(const float* __restrict__ sB, const float xa[3], const float xb[3], float XA[3],
+                                        float XB[3]) {
+  float a[3], b[3], c[3], e[3], g[3], h[3];
+  bern(xa[0], a[0], a[1], a[2]);
+  bern(xa[1], b[0], b[1], b[2]);
+  bern(xa[2], c[0], c[1], c[2]);
+  bern(xb[0], e[0], e[1], e[2]);
+  bern(xb[1], g[0], g[1], g[2]);
+  bern(xb[2], h[0], h[1], h[2]);
+#pragma unroll
+  for (int q = 0; q < 3; ++q) XA[q] = XB[q] = 0.0f;
+#pragma unroll
+  for (int m3 = 0; m3 < 3; ++m3) {
+    float ya[3] = {0.f, 0.f, 0.f}, yb[3] = {0.f, 0.f, 0.f};
+#pragma unroll
+    for (int m2 = 0; m2 < 3; ++m2) {
+      const float* p = sB + ((m3 * 3 + m2) * 3) * 3;
+#pragma unroll
+      for (int q = 0; q < 3; ++q) {
+        const float p0 = p[q], p1 = p[3 + q], p2 = p[6 + q];
+        ya[q] = fmaf(b[m2], fmaf(a[2], p2, fmaf(a[1], p1, a[0] * p0)), ya[q]);
+        yb[q] = fmaf(g[m2], fmaf(e[2], p2, fmaf(e[1], p1, e[0] * p0)), yb[q]);
+      }
+    }
+#pragma unroll
+    for (int q = 0; q < 3; ++q) {
+      XA[q] = fmaf(c[m3], ya[q], XA[q]);
+      XB[q] = fmaf(h[m3], yb[q], XB[q]);
+    }
+  }
+}
+
 // X_E on face (axis k fixed): 9 Bernstein points m = base + ia*sa + jb*sb.
 __device__ __forceinline__ void eval_face(const float* __restrict__ sB, int base, int sa, int sb, float s1, float s2,
                                           float X[3]) {
@@ -610,6 +643,7 @@ struct WarpIsect {
   float ps[PS_N][32];       // P0[3], rf[3], xl0[3], dl[3], alpha0, rr
   float roots[4][4][32];    // [k][beta, xi0, xi1, xi2][lane]
   int nroots[32];
+  int stats[2];             // face tasks, 2D-path tasks (flushed per unit)
   uint8_t task[MAXT];       // lane << 3 | face
 };
 struct PrepScratch {
@@ -772,6 +806,7 @@ __device__ __forceinline__ void isect_chunk(WarpIsect& W, const float* __restric
   __syncwarp();
 
   // ---- 1b: face tasks, one per lane -----------------------------------------
+  int nfallback = 0;
   for (int t0 = 0; t0 < ntask; t0 += 32) {
     const int t = t0 + (int)lane;
     if (t < ntask) {
@@ -841,6 +876,7 @@ __device__ __forceinline__ void isect_chunk(WarpIsect& W, const float* __restric
         }
       }
       if (!done) {
+        ++nfallback;
         // rigorous 2D path (App. A.1): project the face on d1, d2 perpendicular to r
         float ax[3] = {0.f, 0.f, 0.f};
         {
@@ -892,6 +928,15 @@ __device__ __forceinline__ void isect_chunk(WarpIsect& W, const float* __restric
     }
   }
   __syncwarp();
+  {
+    // diagnostics: face tasks and those that needed the 2D path
+#pragma unroll
+    for (int off = 16; off > 0; off >>= 1) nfallback += __shfl_xor_sync(0xffffffffu, nfallback, off);
+    if (lane == 0) {
+      atomicAdd(&W.stats[0], ntask);
+      atomicAdd(&W.stats[1], nfallback);
+    }
+  }
 
   // ---- 1c: per pixel: sort roots, pair entry/exit, emit items ---------------
   int nroots = min(W.nroots[lane], 4);
@@ -1004,38 +1049,56 @@ __device__ __forceinline__ void integ_item(const float* __restrict__ gs, const C
   }
   if (!ok) ++fails;
   float sumk = 0.0f;
+  // the GL nodes two at a time: independent chord iterations in lockstep
 #pragma unroll 1
-  for (int q = 0; q < N; ++q) {
-    const float u = cc.u[q];
-    const float l0 = (1.0f - u) * (1.0f - 2.0f * u), l1 = 4.0f * u * (1.0f - u), l2 = u * (2.0f * u - 1.0f);
-    float xi[3] = {l0 * xia[0] + l1 * xm[0] + l2 * xib[0], l0 * xia[1] + l1 * xm[1] + l2 * xib[1],
-                   l0 * xia[2] + l1 * xm[2] + l2 * xib[2]};
-    const float t0 = fmaf(u, dX[0], xin[0]), t1 = fmaf(u, dX[1], xin[1]), t2 = fmaf(u, dX[2], xin[2]);
+  for (int q = 0; q < N; q += 2) {
+    const int qb = q + 1 < N ? q + 1 : q;
+    float xa[3], xb[3], ta[3], tb[3];
+    {
+      const float u = cc.u[q], w = cc.u[qb];
+      const float l0 = (1.0f - u) * (1.0f - 2.0f * u), l1 = 4.0f * u * (1.0f - u), l2 = u * (2.0f * u - 1.0f);
+      const float k0 = (1.0f - w) * (1.0f - 2.0f * w), k1 = 4.0f * w * (1.0f - w), k2 = w * (2.0f * w - 1.0f);
+#pragma unroll
+      for (int d = 0; d < 3; ++d) {
+        xa[d] = l0 * xia[d] + l1 * xm[d] + l2 * xib[d];
+        xb[d] = k0 * xia[d] + k1 * xm[d] + k2 * xib[d];
+        ta[d] = fmaf(u, dX[d], xin[d]);
+        tb[d] = fmaf(w, dX[d], xin[d]);
+      }
+    }
     bool conv = false;
 #pragma unroll 1
     for (int it = 0; it < 2 * max_it; ++it) {
-      float X[3];
-      eval_X(gs, xi, X);
-      const float r0 = t0 - X[0], r1 = t1 - X[1], r2 = t2 - X[2];
-      const float s0 = Ji[0][0] * r0 + Ji[0][1] * r1 + Ji[0][2] * r2;
-      const float s1 = Ji[1][0] * r0 + Ji[1][1] * r1 + Ji[1][2] * r2;
-      const float s2 = Ji[2][0] * r0 + Ji[2][1] * r1 + Ji[2][2] * r2;
-      xi[0] += s0;
-      xi[1] += s1;
-      xi[2] += s2;
-      if (fmaxf(fabsf(s0), fmaxf(fabsf(s1), fabsf(s2))) * qfac < tol) {
+      float XA[3], XB[3];
+      eval_X2(gs, xa, xb, XA, XB);
+      float step = 0.0f;
+#pragma unroll
+      for (int r = 0; r < 3; ++r) {
+        const float sa = Ji[r][0] * (ta[0] - XA[0]) + Ji[r][1] * (ta[1] - XA[1]) + Ji[r][2] * (ta[2] - XA[2]);
+        const float sb = Ji[r][0] * (tb[0] - XB[0]) + Ji[r][1] * (tb[1] - XB[1]) + Ji[r][2] * (tb[2] - XB[2]);
+        xa[r] += sa;
+        xb[r] += sb;
+        step = fmaxf(step, fmaxf(fabsf(sa), fabsf(sb)));
+      }
+      if (step * qfac < tol) {
         conv = true;
         break;
       }
     }
     if (!conv) ++fails;
-    xi[0] = fminf(fmaxf(xi[0], 0.0f), 1.0f);   // nodes lie inside the element
-    xi[1] = fminf(fmaxf(xi[1], 0.0f), 1.0f);
-    xi[2] = fminf(fmaxf(xi[2], 0.0f), 1.0f);
-    const float ft = field_at<P>(fs, xi[0], xi[1], xi[2]) * cc.inv_F;
-    const float kap = cc.kappa0 * ft * ft;
-    sumk = fmaf(cc.w[q], kap, sumk);
-    scr[q * ST] = ft;
+#pragma unroll
+    for (int d = 0; d < 3; ++d) {   // nodes lie inside the element
+      xa[d] = fminf(fmaxf(xa[d], 0.0f), 1.0f);
+      xb[d] = fminf(fmaxf(xb[d], 0.0f), 1.0f);
+    }
+    const float fa = field_at<P>(fs, xa[0], xa[1], xa[2]) * cc.inv_F;
+    sumk = fmaf(cc.w[q], cc.kappa0 * fa * fa, sumk);
+    scr[q * ST] = fa;
+    if (qb != q) {
+      const float fb = field_at<P>(fs, xb[0], xb[1], xb[2]) * cc.inv_F;
+      sumk = fmaf(cc.w[qb], cc.kappa0 * fb * fb, sumk);
+      scr[qb * ST] = fb;
+    }
   }
   // node optical depths tau_j = L sum_k S_jk kappa_k
   float tau[N], ftv[N];
@@ -1087,7 +1150,7 @@ __global__ void __launch_bounds__(CWARPS * 32, CAST_CTAS_PER_SM) k_cast_curved(C
   rc_seg* segs = reinterpret_cast<rc_seg*>(my + SCR_ITEMS);
   unsigned long long* keys = reinterpret_cast<unsigned long long*>(my + SCR_ITEMS + SCR_SEGS);
   int local_hits = 0, face_fail = 0, fails = 0;
-  long long raw_local = 0;
+  long long raw_local = 0, n_tasks = 0, n_fallback = 0;
   for (;;) {
     __syncthreads();   // the previous unit's shared state (ctl, S) is no longer read
     if (tid == 0) {
@@ -1106,6 +1169,8 @@ __global__ void __launch_bounds__(CWARPS * 32, CAST_CTAS_PER_SM) k_cast_curved(C
     // ---- phase 1: intersection -----------------------------------------------
     {
       WarpIsect& W = S.ph.isect[warp];
+      if (lane == 0) W.stats[0] = W.stats[1] = 0;
+      __syncwarp();
       for (;;) {
         int k = 0;
         if (lane == 0) k = atomicAdd(&ctl.next_chunk, 1);
@@ -1116,6 +1181,10 @@ __global__ void __launch_bounds__(CWARPS * 32, CAST_CTAS_PER_SM) k_cast_curved(C
         const int lv = v - U.vfirst;
         isect_chunk(W, S.slot[lv], S.org[lv], cc, vrect[v], c - chunk_off[v], v, items, &ctl.nitems, hits_pp,
                     local_hits, face_fail);
+      }
+      if (lane == 0) {
+        n_tasks += W.stats[0];
+        n_fallback += W.stats[1];
       }
     }
     __syncthreads();
@@ -1254,6 +1323,10 @@ __global__ void __launch_bounds__(CWARPS * 32, CAST_CTAS_PER_SM) k_cast_curved(C
       atomicAdd((unsigned long long*)&counters[CNT_NEWTON_FAIL], (unsigned long long)(face_fail + fails));
   }
   if (tid == 0 && raw_local) atomicAdd((unsigned long long*)&counters[CNT_RAW], (unsigned long long)raw_local);
+  if (lane == 0 && n_tasks) {
+    atomicAdd((unsigned long long*)&counters[CNT_TASKS], (unsigned long long)n_tasks);
+    atomicAdd((unsigned long long*)&counters[CNT_FALLBACK], (unsigned long long)n_fallback);
+  }
 }
 
 }  // namespace

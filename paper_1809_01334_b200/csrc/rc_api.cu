@@ -517,7 +517,7 @@ extern "C" rc_status rc_cast_segments(rc_forest* f, int32_t fold_levels, void* s
     CU(cudaMemsetAsync(f->d_hits_pp, 0, sizeof(int32_t) * npix, s));
     CU(cudaMemsetAsync(f->d_counters + CNT_SEGS, 0, sizeof(int64_t) * 3, s));
     CU(cudaMemsetAsync(f->d_counters + CNT_OVERFLOW, 0, sizeof(int64_t) * 3, s));
-    CU(cudaMemsetAsync(f->d_counters + CNT_UNITS, 0, sizeof(int64_t) * 4, s));
+    CU(cudaMemsetAsync(f->d_counters + CNT_UNITS, 0, sizeof(int64_t) * 6, s));
     CU(cudaEventRecord(f->ev0, s));
     if (f->h_chunks > 0) {
       if (!curved) {
@@ -590,6 +590,8 @@ extern "C" rc_status rc_segments_get(rc_forest* f, rc_segments* out, void* strea
   out->level = f->rec_level;
   out->units = f->h_units;
   out->unfolded_units = c[CNT_UNFOLDED];
+  out->face_tasks = c[CNT_TASKS];
+  out->fallback_tasks = c[CNT_FALLBACK];
   out->segs = f->d_segs;
   out->hits_per_pixel = f->d_hits_pp;
   if (c[CNT_OVERFLOW] > 0)

@@ -167,6 +167,8 @@ enum {
   CNT_RAW = 73,        // segments before folding
   CNT_UNFOLDED = 74,   // units whose segments exceeded the on-chip sort (emitted unfolded)
   CNT_AGG_OUT = 75,    // records written by an aggregation pass
+  CNT_TASKS = 76,      // curved path: (pixel, face) root-finding tasks
+  CNT_FALLBACK = 77,   // ... of which needed the projected-patch (2D) method
   CNT_TOTAL = 80
 };
 

@@ -48,7 +48,8 @@ class Segments(C.Structure):
     _fields_ = [("count", C.c_int64), ("candidates", C.c_int64), ("hit_pairs", C.c_int64),
                 ("newton_failures", C.c_int64), ("face_failures", C.c_int64), ("num_visible", C.c_int64),
                 ("raw_segments", C.c_int64), ("level", C.c_int64), ("units", C.c_int64),
-                ("unfolded_units", C.c_int64), ("segs", C.c_void_p),
+                ("unfolded_units", C.c_int64), ("face_tasks", C.c_int64), ("fallback_tasks", C.c_int64),
+                ("segs", C.c_void_p),
                 ("hits_per_pixel", C.c_void_p)]
 
 
@@ -249,7 +250,8 @@ class Forest:
         return {"count": s.count, "candidates": s.candidates, "hit_pairs": s.hit_pairs,
                 "newton_failures": s.newton_failures, "face_failures": s.face_failures,
                 "num_visible": s.num_visible, "raw": raw, "raw_segments": s.raw_segments, "level": s.level,
-                "units": s.units, "unfolded_units": s.unfolded_units,
+                "units": s.units, "unfolded_units": s.unfolded_units, "face_tasks": s.face_tasks,
+                "fallback_tasks": s.fallback_tasks,
                 "hits_per_pixel": hpp}
 
     def aggregate(self, cycles, stream=None):
