@@ -154,7 +154,7 @@ typedef struct {
   int64_t raw_segments;        /* segments before any folding                          */
   int64_t level;               /* node level of the records (fold + aggregation cycles) */
   int64_t units;               /* fold units of the curved kernel                      */
-  int64_t unfolded_units;      /* units over the on-chip sort capacity (folded in batches) */
+  int64_t unfolded_units;      /* units too large for the bucket fold (bitonic batches instead) */
   int64_t face_tasks;          /* curved path: (pixel, face) root-finding tasks (diagnostic) */
   int64_t fallback_tasks;      /* ... of which needed the projected-patch method (diagnostic) */
   const rc_seg* segs;          /* device view, library-owned                           */

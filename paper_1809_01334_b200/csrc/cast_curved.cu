@@ -466,7 +466,7 @@ __device__ __forceinline__ void eval_XJr(const float (&G)[81], const float xi[3]
 constexpr int SLOT_STRIDE = 132;   // 84 geometry + 28 field + 16 affine model (+4); 132 mod 32 = 4 spreads slot banks
 constexpr int SLOT_AFF = 112;      // Xc[3], J0inv[9], dp[3], eta
 
-__device__ __forceinline__ void prep_element(float* __restrict__ sl, double* __restrict__ org,
+__device__ __noinline__ void prep_element(float* __restrict__ sl, double* __restrict__ org,
                                              double (*__restrict__ prep)[81], const TreeConst* __restrict__ trees,
                                              const DevLeafView& L, int e, unsigned lane, int NF, bool with_field) {
   const double h = ldexp(1.0, -(int)L.level[e]);
@@ -631,7 +631,7 @@ __device__ __forceinline__ void prep_element(float* __restrict__ sl, double* __r
 // ---------------------------------------------------------------------------
 constexpr int CWARPS = 4;
 #ifndef CAST_CTAS_PER_SM
-#define CAST_CTAS_PER_SM 4   // resident CTAs per SM (launch bounds; 4 fits the 56 KB of shared memory)
+#define CAST_CTAS_PER_SM 3   // resident CTAs per SM (launch bounds: 168 registers, ~60 KB shared memory)
 #endif
 constexpr int ITEM_CAP = 2 * RC_CHUNK * RC_UNIT_CHUNKS;   // <= two segments per pair
 constexpr int SORT_CAP = 2048;
@@ -653,10 +653,18 @@ struct SortSmem {
   unsigned long long key[SORT_CAP];
   uint16_t idx[SORT_CAP];
 };
+constexpr int PIXCAP = 2048;   // pixels of a unit's bounding rectangle for the bucket fold
+constexpr int FCAP = 4096;     // segments of a unit for the bucket fold
+struct BucketSmem {
+  int off[PIXCAP + 1];         // per-pixel counts, then offsets
+  uint16_t rank[FCAP];         // segment -> slot within its pixel
+  uint16_t order[FCAP];        // pixel-bucketed segment indices
+};
 union PhaseSmem {
   PrepScratch prep[CWARPS];
   WarpIsect isect[CWARPS];
   SortSmem sort;
+  BucketSmem bucket;
   float scr[RC_MAX_N * CWARPS * 32];   // phase 2: per-thread node values
 };
 struct CastSmem {
@@ -670,6 +678,7 @@ struct CastCtl {
   int nitems;
   unsigned long long base;
   int warp_sum[CWARPS];
+  int bb[4];                   // unit pixel bounding rectangle: -i0, i1, -j0, j1 (atomicMax)
 };
 
 // per-CTA global scratch (bytes)
@@ -711,6 +720,62 @@ __device__ __forceinline__ void push_root(WarpIsect& W, int pl, float beta, cons
   W.roots[k][1][pl] = xi[0];
   W.roots[k][2][pl] = xi[1];
   W.roots[k][3][pl] = xi[2];
+}
+
+// Rigorous 2D path of one (pixel, face) task (App. A.1):
+// project the face on d1, d2 perpendicular to r, reject by the Bezier hull,
+// prove injectivity and iterate, else subdivide.  Out of line: ~1% of tasks.
+__device__ __noinline__ void face_2d(WarpIsect& W, const float* __restrict__ sB, int pl, int f, const float tP0[3],
+                                     const float trf[3], float trr, float tol, int max_it, int& face_fail) {
+  const int fk = f >> 1, fside = f & 1;
+  const int fa = (fk + 1) % 3, fb = (fk + 2) % 3;
+  // rigorous 2D path (App. A.1): project the face on d1, d2 perpendicular to r
+  float ax[3] = {0.f, 0.f, 0.f};
+  {
+    const float a0 = fabsf(trf[0]), a1 = fabsf(trf[1]), a2 = fabsf(trf[2]);
+    ax[(a0 <= a1 && a0 <= a2) ? 0 : (a1 <= a2 ? 1 : 2)] = 1.0f;
+  }
+  float d1[3] = {trf[1] * ax[2] - trf[2] * ax[1], trf[2] * ax[0] - trf[0] * ax[2],
+                 trf[0] * ax[1] - trf[1] * ax[0]};
+  const float n1 = rsqrtf(d1[0] * d1[0] + d1[1] * d1[1] + d1[2] * d1[2]);
+  d1[0] *= n1; d1[1] *= n1; d1[2] *= n1;
+  float d2[3] = {trf[1] * d1[2] - trf[2] * d1[1], trf[2] * d1[0] - trf[0] * d1[2],
+                 trf[0] * d1[1] - trf[1] * d1[0]};
+  const float n2 = rsqrtf(d2[0] * d2[0] + d2[1] * d2[1] + d2[2] * d2[2]);
+  d2[0] *= n2; d2[1] *= n2; d2[2] *= n2;
+  const float o1 = d1[0] * tP0[0] + d1[1] * tP0[1] + d1[2] * tP0[2];
+  const float o2 = d2[0] * tP0[0] + d2[1] * tP0[1] + d2[2] * tP0[2];
+  Patch pt;
+  project_face(sB, f, d1, d2, o1, o2, pt);
+  if (!hull_excludes_origin(pt)) {
+    float su[8];
+    int nf = 0;
+    float A11, A12, A21, A22, gcx, gcy;
+    const float q = injectivity_bound(pt, A11, A12, A21, A22, gcx, gcy);
+    int st = 0;
+    float s1 = 0.f, s2 = 0.f;
+    if (q < 1.0f) st = chord_root(pt, A11, A12, A21, A22, gcx, gcy, q, tol, max_it, s1, s2);
+    if (st == 1) {
+      if (s1 >= -FACE_TOL && s1 <= 1.0f + FACE_TOL && s2 >= -FACE_TOL && s2 <= 1.0f + FACE_TOL) {
+        su[0] = s1;
+        su[1] = s2;
+        nf = 1;
+      }
+    } else if (st == 0) {
+      nf = face_roots_subdiv(pt, tol, max_it, su, 1, 4, &face_fail);
+    }
+    for (int z = 0; z < nf; ++z) {
+      float xi[3];
+      xi[fk] = (float)fside;
+      xi[fa] = fminf(fmaxf(su[2 * z], 0.0f), 1.0f);
+      xi[fb] = fminf(fmaxf(su[2 * z + 1], 0.0f), 1.0f);
+      float X[3];
+      eval_X(sB, xi, X);
+      const float beta =
+          ((X[0] - tP0[0]) * trf[0] + (X[1] - tP0[1]) * trf[1] + (X[2] - tP0[2]) * trf[2]) / trr;
+      push_root(W, pl, beta, xi, face_fail);
+    }
+  }
 }
 
 // ---- phase 1: one chunk (32 candidate pixels of one element) --------------
@@ -877,53 +942,7 @@ __device__ __forceinline__ void isect_chunk(WarpIsect& W, const float* __restric
       }
       if (!done) {
         ++nfallback;
-        // rigorous 2D path (App. A.1): project the face on d1, d2 perpendicular to r
-        float ax[3] = {0.f, 0.f, 0.f};
-        {
-          const float a0 = fabsf(trf[0]), a1 = fabsf(trf[1]), a2 = fabsf(trf[2]);
-          ax[(a0 <= a1 && a0 <= a2) ? 0 : (a1 <= a2 ? 1 : 2)] = 1.0f;
-        }
-        float d1[3] = {trf[1] * ax[2] - trf[2] * ax[1], trf[2] * ax[0] - trf[0] * ax[2],
-                       trf[0] * ax[1] - trf[1] * ax[0]};
-        const float n1 = rsqrtf(d1[0] * d1[0] + d1[1] * d1[1] + d1[2] * d1[2]);
-        d1[0] *= n1; d1[1] *= n1; d1[2] *= n1;
-        float d2[3] = {trf[1] * d1[2] - trf[2] * d1[1], trf[2] * d1[0] - trf[0] * d1[2],
-                       trf[0] * d1[1] - trf[1] * d1[0]};
-        const float n2 = rsqrtf(d2[0] * d2[0] + d2[1] * d2[1] + d2[2] * d2[2]);
-        d2[0] *= n2; d2[1] *= n2; d2[2] *= n2;
-        const float o1 = d1[0] * tP0[0] + d1[1] * tP0[1] + d1[2] * tP0[2];
-        const float o2 = d2[0] * tP0[0] + d2[1] * tP0[1] + d2[2] * tP0[2];
-        Patch pt;
-        project_face(sB, f, d1, d2, o1, o2, pt);
-        if (!hull_excludes_origin(pt)) {
-          float su[8];
-          int nf = 0;
-          float A11, A12, A21, A22, gcx, gcy;
-          const float q = injectivity_bound(pt, A11, A12, A21, A22, gcx, gcy);
-          int st = 0;
-          float s1 = 0.f, s2 = 0.f;
-          if (q < 1.0f) st = chord_root(pt, A11, A12, A21, A22, gcx, gcy, q, tol, max_it, s1, s2);
-          if (st == 1) {
-            if (s1 >= -FACE_TOL && s1 <= 1.0f + FACE_TOL && s2 >= -FACE_TOL && s2 <= 1.0f + FACE_TOL) {
-              su[0] = s1;
-              su[1] = s2;
-              nf = 1;
-            }
-          } else if (st == 0) {
-            nf = face_roots_subdiv(pt, tol, max_it, su, 1, 4, &face_fail);
-          }
-          for (int z = 0; z < nf; ++z) {
-            float xi[3];
-            xi[fk] = (float)fside;
-            xi[fa] = fminf(fmaxf(su[2 * z], 0.0f), 1.0f);
-            xi[fb] = fminf(fmaxf(su[2 * z + 1], 0.0f), 1.0f);
-            float X[3];
-            eval_X(sB, xi, X);
-            const float beta =
-                ((X[0] - tP0[0]) * trf[0] + (X[1] - tP0[1]) * trf[1] + (X[2] - tP0[2]) * trf[2]) / trr;
-            push_root(W, pl, beta, xi, face_fail);
-          }
-        }
+        face_2d(W, sB, pl, f, tP0, trf, trr, tol, max_it, face_fail);
       }
     }
   }
@@ -1125,6 +1144,149 @@ __device__ __forceinline__ void integ_item(const float* __restrict__ gs, const C
   b_out[2] = sc * E0;
 }
 
+// ---- phase 3, common case: bucket fold -------------------------------------
+// The unit's segments are bucketed by pixel over the unit's bounding rectangle
+// (shared-memory counting sort), each pixel's few segments (one per element
+// the ray crosses in the unit) are ordered by alpha_near in registers, and
+// every maximal run of touching segments is combined nearest-first with
+// Eq. aggregate in fp64 and written as one record.
+constexpr int PIXSEG = 16;   // segments of one pixel ordered in registers (more: slow path)
+
+__device__ __forceinline__ int block_excl_scan(CastCtl& ctl, int v, int& total) {
+  const unsigned lane = threadIdx.x & 31;
+  const int warp = threadIdx.x >> 5;
+  int incl = v;
+#pragma unroll
+  for (int off = 1; off < 32; off <<= 1) {
+    const int y = __shfl_up_sync(0xffffffffu, incl, off);
+    if ((int)lane >= off) incl += y;
+  }
+  __syncthreads();
+  if (lane == 31) ctl.warp_sum[warp] = incl;
+  __syncthreads();
+  int base = 0;
+  total = 0;
+#pragma unroll
+  for (int w = 0; w < CWARPS; ++w) {
+    base += w < warp ? ctl.warp_sum[w] : 0;
+    total += ctl.warp_sum[w];
+  }
+  return base + incl - v;
+}
+
+__device__ __forceinline__ bool touching(float an, float af_prev) {
+  return fabsf(an - af_prev) <= FOLD_TAU * fmaxf(1.0f, fabsf(an));
+}
+
+__device__ void fold_bucket(CastSmem& S, CastCtl& ctl, const rc_seg* __restrict__ segs, int nitems, int bi0, int bj0,
+                            int bw, int area, int W, uint32_t ukey, rc_seg* __restrict__ out, int64_t out_cap,
+                            int64_t* __restrict__ counters) {
+  const int tid = threadIdx.x;
+  constexpr int NT = CWARPS * 32;
+  BucketSmem& B = S.ph.bucket;
+  for (int k = tid; k <= area; k += NT) B.off[k] = 0;
+  __syncthreads();
+  for (int k = tid; k < nitems; k += NT) {
+    const uint32_t pix = segs[k].pixel;
+    const int pl = ((int)(pix / (uint32_t)W) - bj0) * bw + ((int)(pix % (uint32_t)W) - bi0);
+    B.rank[k] = (uint16_t)atomicAdd(&B.off[pl], 1);
+  }
+  __syncthreads();
+  // exclusive scan of the counts over the rectangle (each thread a contiguous range)
+  const int per = (area + NT - 1) / NT;
+  const int p0 = min(area, tid * per), p1 = min(area, p0 + per);
+  int sum = 0;
+  for (int k = p0; k < p1; ++k) sum += B.off[k];
+  int total;
+  int run = block_excl_scan(ctl, sum, total);
+  for (int k = p0; k < p1; ++k) {
+    const int c = B.off[k];
+    B.off[k] = run;
+    run += c;
+  }
+  if (tid == 0) B.off[area] = total;
+  __syncthreads();
+  for (int k = tid; k < nitems; k += NT) {
+    const uint32_t pix = segs[k].pixel;
+    const int pl = ((int)(pix / (uint32_t)W) - bj0) * bw + ((int)(pix % (uint32_t)W) - bi0);
+    B.order[B.off[pl] + B.rank[k]] = (uint16_t)k;
+  }
+  __syncthreads();
+  // per pixel: order by (alpha_near, index), count runs, then emit (two passes)
+  int nrun = 0;
+  for (int pass = 0; pass < 2; ++pass) {
+    int64_t pos = 0;
+    if (pass == 1) {
+      int tot;
+      const int ex = block_excl_scan(ctl, nrun, tot);
+      if (tid == 0) ctl.base = atomicAdd((unsigned long long*)&counters[CNT_SEGS], (unsigned long long)tot);
+      __syncthreads();
+      pos = (int64_t)ctl.base + ex;
+    }
+    for (int pl = tid; pl < area; pl += NT) {
+      const int o = B.off[pl], n = B.off[pl + 1] - o;
+      if (n == 0) continue;
+      float key[PIXSEG];
+      int id[PIXSEG];
+      const int m = min(n, PIXSEG);
+      for (int t = 0; t < m; ++t) {   // insertion sort by (alpha_near, index)
+        const int k = B.order[o + t];
+        const float an = segs[k].alpha_near;
+        int z = t;
+        while (z > 0 && (key[z - 1] > an || (key[z - 1] == an && id[z - 1] > k))) {
+          key[z] = key[z - 1];
+          id[z] = id[z - 1];
+          --z;
+        }
+        key[z] = an;
+        id[z] = k;
+      }
+      if (n > PIXSEG) {
+        // rare: too many segments for the registers -> records of single segments
+        if (pass == 0) nrun += n;
+        else
+          for (int t = 0; t < n; ++t) {
+            const rc_seg& sq = segs[B.order[o + t]];
+            if (pos < out_cap) store_seg(out + pos, sq.pixel, sq.alpha_near, sq.alpha_far, sq.a, sq.b, ukey);
+            else atomicAdd((unsigned long long*)&counters[CNT_OVERFLOW], 1ull);
+            ++pos;
+          }
+        continue;
+      }
+      int t = 0;
+      while (t < m) {
+        const rc_seg& s0 = segs[id[t]];
+        double A = (double)s0.a, B0 = (double)s0.b[0], B1 = (double)s0.b[1], B2 = (double)s0.b[2];
+        float afr = s0.alpha_far;
+        int q = t + 1;
+        for (; q < m; ++q) {
+          const rc_seg& sq = segs[id[q]];
+          if (!touching(sq.alpha_near, afr)) break;
+          if (pass == 1) {
+            B0 = fma(A, (double)sq.b[0], B0);
+            B1 = fma(A, (double)sq.b[1], B1);
+            B2 = fma(A, (double)sq.b[2], B2);
+            A *= (double)sq.a;
+          }
+          afr = sq.alpha_far;
+        }
+        if (pass == 0) {
+          ++nrun;
+        } else {
+          if (pos < out_cap) {
+            const float bf[3] = {(float)B0, (float)B1, (float)B2};
+            store_seg(out + pos, s0.pixel, s0.alpha_near, afr, (float)A, bf, ukey);
+          } else {
+            atomicAdd((unsigned long long*)&counters[CNT_OVERFLOW], 1ull);
+          }
+          ++pos;
+        }
+        t = q;
+      }
+    }
+  }
+}
+
 // ---- the kernel --------------------------------------------------------------
 template <int P, int N>
 __global__ void __launch_bounds__(CWARPS * 32, CAST_CTAS_PER_SM) k_cast_curved(CamConst cc, const TreeConst* __restrict__ trees,
@@ -1163,6 +1325,15 @@ __global__ void __launch_bounds__(CWARPS * 32, CAST_CTAS_PER_SM) k_cast_curved(C
     if (u >= nunits) break;
     const Unit U = units[u];
     // ---- phase 0: the unit's elements into shared memory ---------------------
+    if (tid < 4) ctl.bb[tid] = -0x7fffffff;
+    __syncthreads();
+    for (int w = tid; w < U.nvis; w += CWARPS * 32) {
+      const Rect16 r = vrect[U.vfirst + w];
+      atomicMax(&ctl.bb[0], -(int)r.i0);
+      atomicMax(&ctl.bb[1], (int)r.i1);
+      atomicMax(&ctl.bb[2], -(int)r.j0);
+      atomicMax(&ctl.bb[3], (int)r.j1);
+    }
     for (int w = warp; w < U.nvis; w += CWARPS)
       prep_element(S.slot[w], S.org[w], S.ph.prep[warp].prep, trees, L, vis[U.vfirst + w], lane, NF, true);
     __syncthreads();
@@ -1225,7 +1396,16 @@ __global__ void __launch_bounds__(CWARPS * 32, CAST_CTAS_PER_SM) k_cast_curved(C
     }
     if (fold == 0) continue;   // next unit (the loop head synchronises first)
     __syncthreads();
-    // ---- phase 3: fold (batches of SORT_CAP segments) ---------------------------
+    // ---- phase 3: fold -----------------------------------------------------------
+    {
+      const int bi0 = -ctl.bb[0], bi1 = ctl.bb[1], bj0 = -ctl.bb[2], bj1 = ctl.bb[3];
+      const int bw = bi1 - bi0 + 1, area = bw * (bj1 - bj0 + 1);
+      if (area <= PIXCAP && nitems <= FCAP) {
+        fold_bucket(S, ctl, segs, nitems, bi0, bj0, bw, area, cc.W, U.key, out, out_cap, counters);
+        continue;
+      }
+    }
+    // large units: bitonic sort by (pixel, alpha) in batches of SORT_CAP
     for (int b0 = 0; b0 < nitems; b0 += SORT_CAP) {
       const int n = min(SORT_CAP, nitems - b0);
       int m = 1;
@@ -1308,7 +1488,7 @@ __global__ void __launch_bounds__(CWARPS * 32, CAST_CTAS_PER_SM) k_cast_curved(C
         ++pos;
       }
     }
-    if (tid == 0 && nitems > SORT_CAP) atomicAdd((unsigned long long*)&counters[CNT_UNFOLDED], 1ull);
+    if (tid == 0) atomicAdd((unsigned long long*)&counters[CNT_UNFOLDED], 1ull);
   }
 #pragma unroll
   for (int off = 16; off > 0; off >>= 1) {
