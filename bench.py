@@ -104,6 +104,8 @@ def make_scene(cfg: int, device):
         return sg.config4(device=device)
     if cfg == 5:
         return sg.config5(device=device)
+    if cfg == 45:   # profiling stand-in for C4: level 7 at 1024^2 has C4's pixels per element
+        return sg.shell_uniform(7, 1024, 256, name="C4s", device=device)
     raise ValueError(cfg)
 
 
@@ -111,7 +113,8 @@ WORKLOAD = {1: "C1: identity cube, uniform level 3 (512 hex), ortho 64x64, N=4",
             2: "C2: identity cube, adaptive levels 3..7 (87,088 hex), perspective 512x512, N=4",
             3: "C3: cubed-sphere shell R=2, uniform level 6 (1,572,864 hex), 1024x1024, N=6",
             4: "C4: cubed-sphere shell R=2, uniform level 8 (100,663,296 hex), 2048x2048, N=6",
-            5: "C5: cubed-sphere shell R=2, adaptive levels 6..10, 4096x4096, N=8, 3 coarsening cycles"}
+            5: "C5: cubed-sphere shell R=2, adaptive levels 6..10, 4096x4096, N=8, 3 coarsening cycles",
+            45: "C4s (profiling stand-in): shell R=2, uniform level 7 (12,582,912 hex), 1024x1024, N=6"}
 
 
 def forest_affine(scene):
@@ -158,7 +161,7 @@ def run_reference(args):
     import torch
     dev = "cuda" if (args.config >= 3 and torch.cuda.is_available()) else None
     scene = scene_to_host(make_scene(args.config, dev))
-    stride = {1: 1, 2: 8, 3: 32, 4: 64, 5: 128}[args.config]
+    stride = {1: 1, 2: 8, 3: 32, 4: 64, 5: 128, 45: 32}[args.config]
     for _ in range(args.warmup):
         pass
     vals = []
@@ -357,7 +360,7 @@ def main():
                 "roofline": roof, "gpu_launches": launches, "clocks": clk.summary(), "e2e": e2e,
                 "newton_failures": newton_failures, "segments": fold_info}
         if world == 1 and not args.no_cpu_baseline:
-            stride = {1: 1, 2: 8, 3: 32, 4: 64, 5: 128}[args.config]
+            stride = {1: 1, 2: 8, 3: 32, 4: 64, 5: 128, 45: 32}[args.config]
             sc_cpu = scene_to_host(scene)
             cb = cpu_baseline(sc_cpu, stride)
             line["cpu_baseline"] = {k: cb[k] for k in ("value", "unit", "cores", "kind", "sample")}

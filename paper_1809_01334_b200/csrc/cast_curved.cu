@@ -50,7 +50,26 @@ __device__ __forceinline__ void dbern(float t, float& d0, float& d1, float& d2) 
   d2 = 2.0f * t;
 }
 
-// X_E(xi) - C_E from the relative Bernstein points sB[m*3+c], m = (m3*3+m2)*3+m1.
+// Element slot layout in shared memory (floats, 16-byte aligned rows): the
+// 27 Bernstein points relative to the element origin as 9 rows (m3, m2) of
+// 3 points (m1) x 3 coordinates padded to 12 floats; the nodal field (P = 2:
+// 3 rows of 9 values padded to 12; P = 1: 8 values); the affine model.
+__host__ __device__ constexpr int GI(int m) { return (m / 3) * 12 + (m % 3) * 3; }   // point m = (m3*3+m2)*3+m1
+__host__ __device__ constexpr int FI(int q, int NF) { return NF == 27 ? (q / 9) * 12 + q % 9 : q; }
+constexpr int SLOT_FIELD = 108;
+constexpr int SLOT_AFF = 144;      // Xc[3], J0inv[9], dp[3], eta
+constexpr int SLOT_STRIDE = 164;   // 160 used; 164 mod 32 = 4 spreads slot banks, 656 B keeps 16-B alignment
+
+// one row (m3, m2) of 3 points by three 16-byte loads
+__device__ __forceinline__ void load_row(const float* __restrict__ sB, int row, float p0[3], float p1[3], float p2[3]) {
+  const float4* r = reinterpret_cast<const float4*>(sB + row * 12);
+  const float4 v0 = r[0], v1 = r[1], v2 = r[2];
+  p0[0] = v0.x; p0[1] = v0.y; p0[2] = v0.z;
+  p1[0] = v0.w; p1[1] = v1.x; p1[2] = v1.y;
+  p2[0] = v1.z; p2[1] = v1.w; p2[2] = v2.x;
+}
+
+// X_E(xi) - C_E (tensor Bernstein form of the degree-2 element map).
 __device__ __forceinline__ void eval_X(const float* __restrict__ sB, const float xi[3], float X[3]) {
   float a0, a1, a2, b0, b1, b2, c0, c1, c2;
   bern(xi[0], a0, a1, a2);
@@ -63,9 +82,10 @@ __device__ __forceinline__ void eval_X(const float* __restrict__ sB, const float
     float y[3] = {0.f, 0.f, 0.f};
 #pragma unroll
     for (int m2 = 0; m2 < 3; ++m2) {
-      const float* p = sB + ((m3 * 3 + m2) * 3) * 3;
+      float p0[3], p1[3], p2[3];
+      load_row(sB, m3 * 3 + m2, p0, p1, p2);
 #pragma unroll
-      for (int c = 0; c < 3; ++c) y[c] = fmaf(bb[m2], fmaf(a2, p[6 + c], fmaf(a1, p[3 + c], a0 * p[c])), y[c]);
+      for (int c = 0; c < 3; ++c) y[c] = fmaf(bb[m2], fmaf(a2, p2[c], fmaf(a1, p1[c], a0 * p0[c])), y[c]);
     }
 #pragma unroll
     for (int c = 0; c < 3; ++c) X[c] = fmaf(cc[m3], y[c], X[c]);
@@ -89,12 +109,12 @@ __device__ __forceinline__ void eval_X2(const float* __restrict__ sB, const floa
     float ya[3] = {0.f, 0.f, 0.f}, yb[3] = {0.f, 0.f, 0.f};
 #pragma unroll
     for (int m2 = 0; m2 < 3; ++m2) {
-      const float* p = sB + ((m3 * 3 + m2) * 3) * 3;
+      float p0[3], p1[3], p2[3];
+      load_row(sB, m3 * 3 + m2, p0, p1, p2);
 #pragma unroll
       for (int q = 0; q < 3; ++q) {
-        const float p0 = p[q], p1 = p[3 + q], p2 = p[6 + q];
-        ya[q] = fmaf(b[m2], fmaf(a[2], p2, fmaf(a[1], p1, a[0] * p0)), ya[q]);
-        yb[q] = fmaf(g[m2], fmaf(e[2], p2, fmaf(e[1], p1, e[0] * p0)), yb[q]);
+        ya[q] = fmaf(b[m2], fmaf(a[2], p2[q], fmaf(a[1], p1[q], a[0] * p0[q])), ya[q]);
+        yb[q] = fmaf(g[m2], fmaf(e[2], p2[q], fmaf(e[1], p1[q], e[0] * p0[q])), yb[q]);
       }
     }
 #pragma unroll
@@ -103,6 +123,37 @@ __device__ __forceinline__ void eval_X2(const float* __restrict__ sB, const floa
       XB[q] = fmaf(h[m3], yb[q], XB[q]);
     }
   }
+}
+
+// Field at xi from the padded nodal values (node order [k3][k2][k1]).
+template <int P>
+__device__ __forceinline__ float field_pad(const float* __restrict__ f, float x1, float x2, float x3);
+template <>
+__device__ __forceinline__ float field_pad<1>(const float* __restrict__ f, float x1, float x2, float x3) {
+  const float4 lo = reinterpret_cast<const float4*>(f)[0], hi = reinterpret_cast<const float4*>(f)[1];
+  const float a00 = fmaf(x1, lo.y - lo.x, lo.x), a10 = fmaf(x1, lo.w - lo.z, lo.z);
+  const float a01 = fmaf(x1, hi.y - hi.x, hi.x), a11 = fmaf(x1, hi.w - hi.z, hi.z);
+  const float b0 = fmaf(x2, a10 - a00, a00), b1 = fmaf(x2, a11 - a01, a01);
+  return fmaf(x3, b1 - b0, b0);
+}
+template <>
+__device__ __forceinline__ float field_pad<2>(const float* __restrict__ f, float x1, float x2, float x3) {
+  float p0, p1, p2, q0, q1, q2, r0, r1, r2;
+  lag2(x1, p0, p1, p2);
+  lag2(x2, q0, q1, q2);
+  lag2(x3, r0, r1, r2);
+  const float rr[3] = {r0, r1, r2};
+  float out = 0.0f;
+#pragma unroll
+  for (int k3 = 0; k3 < 3; ++k3) {
+    float g[9];
+    load_row(f, k3, g, g + 3, g + 6);
+    const float s0 = fmaf(p2, g[2], fmaf(p1, g[1], p0 * g[0]));
+    const float s1 = fmaf(p2, g[5], fmaf(p1, g[4], p0 * g[3]));
+    const float s2 = fmaf(p2, g[8], fmaf(p1, g[7], p0 * g[6]));
+    out = fmaf(rr[k3], fmaf(q2, s2, fmaf(q1, s1, q0 * s0)), out);
+  }
+  return out;
 }
 
 // X_E on face (axis k fixed): 9 Bernstein points m = base + ia*sa + jb*sb.
@@ -115,49 +166,15 @@ __device__ __forceinline__ void eval_face(const float* __restrict__ sB, int base
   X[0] = X[1] = X[2] = 0.0f;
 #pragma unroll
   for (int jb = 0; jb < 3; ++jb) {
-    const float* p0 = sB + 3 * (base + jb * sb);
-    const float* p1 = p0 + 3 * sa;
-    const float* p2 = p1 + 3 * sa;
+    const int m = base + jb * sb;
+    const float* p0 = sB + GI(m);
+    const float* p1 = sB + GI(m + sa);
+    const float* p2 = sB + GI(m + 2 * sa);
 #pragma unroll
     for (int c = 0; c < 3; ++c) X[c] = fmaf(bb[jb], fmaf(a2, p2[c], fmaf(a1, p1[c], a0 * p0[c])), X[c]);
   }
 }
 
-// X and J = dX/dxi (J[c][d]).
-__device__ __forceinline__ void eval_XJ(const float* __restrict__ sB, const float xi[3], float X[3], float J[3][3]) {
-  float a[3], b[3], c[3], da[3], db[3], dc[3];
-  bern(xi[0], a[0], a[1], a[2]);
-  bern(xi[1], b[0], b[1], b[2]);
-  bern(xi[2], c[0], c[1], c[2]);
-  dbern(xi[0], da[0], da[1], da[2]);
-  dbern(xi[1], db[0], db[1], db[2]);
-  dbern(xi[2], dc[0], dc[1], dc[2]);
-#pragma unroll
-  for (int q = 0; q < 3; ++q) X[q] = J[q][0] = J[q][1] = J[q][2] = 0.0f;
-#pragma unroll
-  for (int m3 = 0; m3 < 3; ++m3) {
-    float y[3] = {0, 0, 0}, y1[3] = {0, 0, 0}, y2[3] = {0, 0, 0};
-#pragma unroll
-    for (int m2 = 0; m2 < 3; ++m2) {
-      const float* p = sB + ((m3 * 3 + m2) * 3) * 3;
-#pragma unroll
-      for (int q = 0; q < 3; ++q) {
-        float v = fmaf(a[2], p[6 + q], fmaf(a[1], p[3 + q], a[0] * p[q]));
-        float dv = fmaf(da[2], p[6 + q], fmaf(da[1], p[3 + q], da[0] * p[q]));
-        y[q] = fmaf(b[m2], v, y[q]);
-        y1[q] = fmaf(b[m2], dv, y1[q]);
-        y2[q] = fmaf(db[m2], v, y2[q]);
-      }
-    }
-#pragma unroll
-    for (int q = 0; q < 3; ++q) {
-      X[q] = fmaf(c[m3], y[q], X[q]);
-      J[q][0] = fmaf(c[m3], y1[q], J[q][0]);
-      J[q][1] = fmaf(c[m3], y2[q], J[q][1]);
-      J[q][2] = fmaf(dc[m3], y[q], J[q][2]);
-    }
-  }
-}
 
 __device__ __forceinline__ bool inv3(const float J[3][3], float I[3][3]) {
   float c00 = J[1][1] * J[2][2] - J[1][2] * J[2][1];
@@ -332,7 +349,7 @@ __device__ __forceinline__ void project_face(const float* __restrict__ sB, int f
 #pragma unroll
     for (int ia = 0; ia < 3; ++ia) {
       const int m = base + ia * sa + jb * sbb;
-      const float bx = sB[3 * m], by = sB[3 * m + 1], bz = sB[3 * m + 2];
+      const float bx = sB[GI(m)], by = sB[GI(m) + 1], bz = sB[GI(m) + 2];
       pt.gx[3 * jb + ia] = fmaf(d1[0], bx, fmaf(d1[1], by, fmaf(d1[2], bz, -o1)));
       pt.gy[3 * jb + ia] = fmaf(d2[0], bx, fmaf(d2[1], by, fmaf(d2[2], bz, -o2)));
     }
@@ -399,72 +416,15 @@ __device__ __noinline__ int face_roots_subdiv(const Patch& root, float tol, int 
 }
 
 
-// X_E(xi) - C_E with the Bernstein points in registers (G[m*3+c]).
-__device__ __forceinline__ void eval_Xr(const float (&G)[81], const float xi[3], float X[3]) {
-  float a0, a1, a2, b0, b1, b2, c0, c1, c2;
-  bern(xi[0], a0, a1, a2);
-  bern(xi[1], b0, b1, b2);
-  bern(xi[2], c0, c1, c2);
-  const float bb[3] = {b0, b1, b2}, cc[3] = {c0, c1, c2};
-  X[0] = X[1] = X[2] = 0.0f;
-#pragma unroll
-  for (int m3 = 0; m3 < 3; ++m3) {
-    float y[3] = {0.f, 0.f, 0.f};
-#pragma unroll
-    for (int m2 = 0; m2 < 3; ++m2) {
-      const int o = ((m3 * 3 + m2) * 3) * 3;
-#pragma unroll
-      for (int c = 0; c < 3; ++c) y[c] = fmaf(bb[m2], fmaf(a2, G[o + 6 + c], fmaf(a1, G[o + 3 + c], a0 * G[o + c])), y[c]);
-    }
-#pragma unroll
-    for (int c = 0; c < 3; ++c) X[c] = fmaf(cc[m3], y[c], X[c]);
-  }
-}
 
-__device__ __forceinline__ void eval_XJr(const float (&G)[81], const float xi[3], float X[3], float J[3][3]) {
-  float a[3], b[3], c[3], da[3], db[3], dc[3];
-  bern(xi[0], a[0], a[1], a[2]);
-  bern(xi[1], b[0], b[1], b[2]);
-  bern(xi[2], c[0], c[1], c[2]);
-  dbern(xi[0], da[0], da[1], da[2]);
-  dbern(xi[1], db[0], db[1], db[2]);
-  dbern(xi[2], dc[0], dc[1], dc[2]);
-#pragma unroll
-  for (int q = 0; q < 3; ++q) X[q] = J[q][0] = J[q][1] = J[q][2] = 0.0f;
-#pragma unroll
-  for (int m3 = 0; m3 < 3; ++m3) {
-    float y[3] = {0, 0, 0}, y1[3] = {0, 0, 0}, y2[3] = {0, 0, 0};
-#pragma unroll
-    for (int m2 = 0; m2 < 3; ++m2) {
-      const int o = ((m3 * 3 + m2) * 3) * 3;
-#pragma unroll
-      for (int q = 0; q < 3; ++q) {
-        float v = fmaf(a[2], G[o + 6 + q], fmaf(a[1], G[o + 3 + q], a[0] * G[o + q]));
-        float dv = fmaf(da[2], G[o + 6 + q], fmaf(da[1], G[o + 3 + q], da[0] * G[o + q]));
-        y[q] = fmaf(b[m2], v, y[q]);
-        y1[q] = fmaf(b[m2], dv, y1[q]);
-        y2[q] = fmaf(db[m2], v, y2[q]);
-      }
-    }
-#pragma unroll
-    for (int q = 0; q < 3; ++q) {
-      X[q] = fmaf(c[m3], y[q], X[q]);
-      J[q][0] = fmaf(c[m3], y1[q], J[q][0]);
-      J[q][1] = fmaf(c[m3], y2[q], J[q][1]);
-      J[q][2] = fmaf(dc[m3], y[q], J[q][2]);
-    }
-  }
-}
 
 // ---------------------------------------------------------------------------
 // Element preparation (warp-cooperative, 27 lanes): Bernstein control points
 // of X_E by restriction of the tree's (fp64, three sum-factorised blossom
 // passes), stored fp32 relative to the local origin org = B_(1,1,1) in
-// sl[0..80]; optional nodal field in sl[84..110]; the affine model and its
-// nonlinearity bounds in sl[SLOT_AFF..+15].
+// sl (layout GI / FI / SLOT_FIELD above); optional nodal field; the affine
+// model and its nonlinearity bounds in sl[SLOT_AFF..+15].
 // ---------------------------------------------------------------------------
-constexpr int SLOT_STRIDE = 132;   // 84 geometry + 28 field + 16 affine model (+4); 132 mod 32 = 4 spreads slot banks
-constexpr int SLOT_AFF = 112;      // Xc[3], J0inv[9], dp[3], eta
 
 __device__ __noinline__ void prep_element(float* __restrict__ sl, double* __restrict__ org,
                                              double (*__restrict__ prep)[81], const TreeConst* __restrict__ trees,
@@ -518,8 +478,8 @@ __device__ __noinline__ void prep_element(float* __restrict__ sl, double* __rest
     }
     __syncwarp(0x07ffffffu);
 #pragma unroll
-    for (int q3 = 0; q3 < 3; ++q3) sl[lane * 3 + q3] = (float)(o[q3] - org[q3]);
-    if (with_field && (int)lane < NF) sl[84 + lane] = __ldg(&L.field[(int64_t)e * NF + lane]);
+    for (int q3 = 0; q3 < 3; ++q3) sl[GI(lane) + q3] = (float)(o[q3] - org[q3]);
+    if (with_field && (int)lane < NF) sl[SLOT_FIELD + FI(lane, NF)] = __ldg(&L.field[(int64_t)e * NF + lane]);
   }
   __syncwarp();
         {
@@ -529,7 +489,7 @@ __device__ __noinline__ void prep_element(float* __restrict__ sl, double* __rest
           const int m1 = lane % 3, m2 = (lane / 3) % 3, m3 = lane / 9;
           const float wq[3] = {0.25f, 0.5f, 0.25f}, dq[3] = {-1.0f, 0.0f, 1.0f};
           float B0 = 0.f, B1 = 0.f, B2 = 0.f;
-          if (lane < 27) { B0 = sl[3 * lane]; B1 = sl[3 * lane + 1]; B2 = sl[3 * lane + 2]; }
+          if (lane < 27) { B0 = sl[GI(lane)]; B1 = sl[GI(lane) + 1]; B2 = sl[GI(lane) + 2]; }
           const float w3 = lane < 27 ? wq[m1] * wq[m2] * wq[m3] : 0.0f;
           const float g1 = lane < 27 ? dq[m1] * wq[m2] * wq[m3] : 0.0f;
           const float g2 = lane < 27 ? wq[m1] * dq[m2] * wq[m3] : 0.0f;
@@ -567,7 +527,7 @@ __device__ __noinline__ void prep_element(float* __restrict__ sl, double* __rest
             for (int ax = 0; ax < 3; ++ax) {
               if (mmv[ax] < 2) {
                 const int n2 = lane + str[ax];
-                const float e0 = 2.0f * (sl[3 * n2] - B0), e1 = 2.0f * (sl[3 * n2 + 1] - B1), e2 = 2.0f * (sl[3 * n2 + 2] - B2);
+                const float e0 = 2.0f * (sl[GI(n2)] - B0), e1 = 2.0f * (sl[GI(n2) + 1] - B1), e2 = 2.0f * (sl[GI(n2) + 2] - B2);
                 const float t0 = Ji[0][0] * e0 + Ji[0][1] * e1 + Ji[0][2] * e2 - (ax == 0 ? 1.0f : 0.0f);
                 const float t1 = Ji[1][0] * e0 + Ji[1][1] * e1 + Ji[1][2] * e2 - (ax == 1 ? 1.0f : 0.0f);
                 const float t2 = Ji[2][0] * e0 + Ji[2][1] * e1 + Ji[2][2] * e2 - (ax == 2 ? 1.0f : 0.0f);
@@ -670,6 +630,9 @@ union PhaseSmem {
 struct CastSmem {
   float slot[RC_UNIT_LEAVES][SLOT_STRIDE];
   double org[RC_UNIT_LEAVES][3];
+  Rect16 rect[RC_UNIT_LEAVES];          // pixel rectangles of the unit's elements
+  int32_t coff[RC_UNIT_LEAVES];         // first chunk of each element relative to the unit's first
+  uint8_t cmap[RC_UNIT_CHUNKS];         // unit chunk -> element
   PhaseSmem ph;
 };
 struct CastCtl {
@@ -980,7 +943,7 @@ __device__ __forceinline__ void isect_chunk(WarpIsect& W, const float* __restric
   {
     // dedupe roots found on two faces at a shared edge / vertex
     const float rn = sqrtf(rr);
-    const float hw = fabsf(sB[3 * 26] - sB[0]) + fabsf(sB[3 * 26 + 1] - sB[1]) + fabsf(sB[3 * 26 + 2] - sB[2]);
+    const float hw = fabsf(sB[GI(26)] - sB[0]) + fabsf(sB[GI(26) + 1] - sB[1]) + fabsf(sB[GI(26) + 2] - sB[2]);
     const float dtol = 4e-6f * hw / rn;
     if (nroots > 1 && rb1 - rb0 < dtol) { rb1 = rb2; ri1 = ri2; rb2 = rb3; ri2 = ri3; rb3 = 3.4e38f; --nroots; }
     if (nroots > 2 && rb2 - rb1 < dtol) { rb2 = rb3; ri2 = ri3; rb3 = 3.4e38f; --nroots; }
@@ -1034,7 +997,7 @@ __device__ __forceinline__ void integ_item(const float* __restrict__ gs, const C
   constexpr int ST = CWARPS * 32;
   const float tol = cc.newton_tol;
   const int max_it = cc.newton_max;
-  const float* fs = gs + 84;
+  const float* fs = gs + SLOT_FIELD;
   const float* afm = gs + SLOT_AFF;
   float Ji[3][3];
 #pragma unroll
@@ -1110,11 +1073,11 @@ __device__ __forceinline__ void integ_item(const float* __restrict__ gs, const C
       xa[d] = fminf(fmaxf(xa[d], 0.0f), 1.0f);
       xb[d] = fminf(fmaxf(xb[d], 0.0f), 1.0f);
     }
-    const float fa = field_at<P>(fs, xa[0], xa[1], xa[2]) * cc.inv_F;
+    const float fa = field_pad<P>(fs, xa[0], xa[1], xa[2]) * cc.inv_F;
     sumk = fmaf(cc.w[q], cc.kappa0 * fa * fa, sumk);
     scr[q * ST] = fa;
     if (qb != q) {
-      const float fb = field_at<P>(fs, xb[0], xb[1], xb[2]) * cc.inv_F;
+      const float fb = field_pad<P>(fs, xb[0], xb[1], xb[2]) * cc.inv_F;
       sumk = fmaf(cc.w[qb], cc.kappa0 * fb * fb, sumk);
       scr[qb * ST] = fb;
     }
@@ -1329,6 +1292,11 @@ __global__ void __launch_bounds__(CWARPS * 32, CAST_CTAS_PER_SM) k_cast_curved(C
     __syncthreads();
     for (int w = tid; w < U.nvis; w += CWARPS * 32) {
       const Rect16 r = vrect[U.vfirst + w];
+      S.rect[w] = r;
+      const int64_t ca = chunk_off[U.vfirst + w], cz = chunk_off[U.vfirst + w + 1];
+      S.coff[w] = (int32_t)(ca - U.chunk_begin);
+      const int k0 = (int)max((int64_t)0, ca - U.chunk_begin), k1 = (int)min((int64_t)U.nchunks, cz - U.chunk_begin);
+      for (int k = k0; k < k1; ++k) S.cmap[k] = (uint8_t)w;
       atomicMax(&ctl.bb[0], -(int)r.i0);
       atomicMax(&ctl.bb[1], (int)r.i1);
       atomicMax(&ctl.bb[2], -(int)r.j0);
@@ -1347,11 +1315,9 @@ __global__ void __launch_bounds__(CWARPS * 32, CAST_CTAS_PER_SM) k_cast_curved(C
         if (lane == 0) k = atomicAdd(&ctl.next_chunk, 1);
         k = __shfl_sync(0xffffffffu, k, 0);
         if (k >= U.nchunks) break;
-        const int64_t c = U.chunk_begin + k;
-        const int v = chunk_elem[c];
-        const int lv = v - U.vfirst;
-        isect_chunk(W, S.slot[lv], S.org[lv], cc, vrect[v], c - chunk_off[v], v, items, &ctl.nitems, hits_pp,
-                    local_hits, face_fail);
+        const int lv = S.cmap[k];
+        isect_chunk(W, S.slot[lv], S.org[lv], cc, S.rect[lv], k - S.coff[lv], U.vfirst + lv, items, &ctl.nitems,
+                    hits_pp, local_hits, face_fail);
       }
       if (lane == 0) {
         n_tasks += W.stats[0];

@@ -14,7 +14,7 @@ for v in $VARIANTS; do
   RC_LIB=$LIB timeout 600 python bench.py --config 4 --steps 5 --no-cpu-baseline > $OUT/bench_$v.json 2> $OUT/bench_$v.err
   echo "bench $v exit $?" >> $OUT/status
 done
-PCMD="python tools/profile_frame.py --config 3 --frames 1"
+PCMD="python tools/profile_frame.py --config ${PROFCFG:-45} --frames 1"
 timeout 300 $PCMD > $OUT/plain_pf.log 2>&1 && \
   timeout 900 ncu --set full --clock-control none --import-source on -k regex:'k_cast_curved' -c 1 -o $OUT/prof $PCMD > $OUT/ncu_full.log 2>&1
 echo "ncu full exit $?" >> $OUT/status
