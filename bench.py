@@ -213,15 +213,23 @@ def main():
     N = cam.gl_points
     lib = rc.lib()
 
+    fold = args.fold if args.fold >= 0 else (0 if forest_affine(scene) else 2)
     # --- device-resident inputs: this rank's contiguous SFC range ---------
+    # equal leaf counts, cuts moved to node starts of the coarsest level the
+    # fold + aggregation cycles reach: every family is local
     n = scene.num_leaves
-    lo, hi = n * rank // world, n * (rank + 1) // world
+    if world > 1:
+        from paper_1809_01334_b200 import dist as rdist
+        A, T, Lv = (torch.as_tensor(x, device=dev) for x in (scene.leaf_anchor, scene.leaf_tree, scene.leaf_level))
+        allowed = rdist.node_starts(A, T, Lv, fold + scene.coarsen_cycles)
+        lo, hi = rdist.aligned_ranges(torch.ones(n, dtype=torch.float64), world, allowed)[rank]
+        del A, T, Lv, allowed
+    else:
+        lo, hi = 0, n
     forest = rc.Forest.from_scene(scene, first=lo, count=hi - lo, device_copy=True)
     img = torch.empty((H, W, 4), dtype=torch.float32, device=dev)
     flush = torch.empty(int(160e6) // 4, dtype=torch.float32, device=dev)   # > 126 MB L2
     stream = torch.cuda.current_stream()
-
-    fold = args.fold if args.fold >= 0 else (0 if forest_affine(scene) else 2)
 
     def frame():
         forest.camera_set(cam)

@@ -156,7 +156,8 @@ __device__ __forceinline__ float field_pad<2>(const float* __restrict__ f, float
   return out;
 }
 
-// X_E on face (axis k fixed): 9 Bernstein points m = base + ia*sa + jb*sb.
+// X_E on face (axis k fixed): 9 Bernstein points at padded float offsets
+// base + ia*sa + jb*sb (offset of point (m1,m2,m3) = 3 m1 + 12 m2 + 36 m3).
 __device__ __forceinline__ void eval_face(const float* __restrict__ sB, int base, int sa, int sb, float s1, float s2,
                                           float X[3]) {
   float a0, a1, a2, b0, b1, b2;
@@ -166,10 +167,9 @@ __device__ __forceinline__ void eval_face(const float* __restrict__ sB, int base
   X[0] = X[1] = X[2] = 0.0f;
 #pragma unroll
   for (int jb = 0; jb < 3; ++jb) {
-    const int m = base + jb * sb;
-    const float* p0 = sB + GI(m);
-    const float* p1 = sB + GI(m + sa);
-    const float* p2 = sB + GI(m + 2 * sa);
+    const float* p0 = sB + base + jb * sb;
+    const float* p1 = p0 + sa;
+    const float* p2 = p1 + sa;
 #pragma unroll
     for (int c = 0; c < 3; ++c) X[c] = fmaf(bb[jb], fmaf(a2, p2[c], fmaf(a1, p1[c], a0 * p0[c])), X[c]);
   }
@@ -615,25 +615,34 @@ struct SortSmem {
 };
 constexpr int PIXCAP = 2048;   // pixels of a unit's bounding rectangle for the bucket fold
 constexpr int FCAP = 4096;     // segments of a unit for the bucket fold
-struct BucketSmem {
+union PhaseSmem {              // per-phase scratch of phases 0-2
+  PrepScratch prep[CWARPS];
+  WarpIsect isect[CWARPS];
+  float scr[RC_MAX_N * CWARPS * 32];   // phase 2: per-thread node values
+};
+struct UnitMeta {
+  double org[RC_UNIT_LEAVES][3];        // element origins (fp64)
+  Rect16 rect[RC_UNIT_LEAVES];          // pixel rectangles of the unit's elements
+  int32_t coff[RC_UNIT_LEAVES];         // first chunk of each element relative to the unit's first
+  uint8_t cmap[RC_UNIT_CHUNKS];         // unit chunk -> element
+};
+struct Phase012 {
+  float slot[RC_UNIT_LEAVES][SLOT_STRIDE];
+  PhaseSmem ph;
+};
+struct FoldSmem {              // phase 3 (the slots are dead by then)
+  float2 alpha[FCAP];          // (alpha_near, alpha_far) of every segment
   int off[PIXCAP + 1];         // per-pixel counts, then offsets
   uint16_t rank[FCAP];         // segment -> slot within its pixel
   uint16_t order[FCAP];        // pixel-bucketed segment indices
 };
-union PhaseSmem {
-  PrepScratch prep[CWARPS];
-  WarpIsect isect[CWARPS];
-  SortSmem sort;
-  BucketSmem bucket;
-  float scr[RC_MAX_N * CWARPS * 32];   // phase 2: per-thread node values
-};
 struct CastSmem {
-  float slot[RC_UNIT_LEAVES][SLOT_STRIDE];
-  double org[RC_UNIT_LEAVES][3];
-  Rect16 rect[RC_UNIT_LEAVES];          // pixel rectangles of the unit's elements
-  int32_t coff[RC_UNIT_LEAVES];         // first chunk of each element relative to the unit's first
-  uint8_t cmap[RC_UNIT_CHUNKS];         // unit chunk -> element
-  PhaseSmem ph;
+  UnitMeta meta;
+  union {
+    Phase012 p;
+    FoldSmem fold;
+    SortSmem sort;
+  } u;
 };
 struct CastCtl {
   int64_t unit;
@@ -863,8 +872,8 @@ __device__ __forceinline__ void isect_chunk(WarpIsect& W, const float* __restric
           const float sa0 = txl0[fa] + b0 * tdl[fa], sb0 = txl0[fb] + b0 * tdl[fb];
           const float qfac = qf / (1.0f - qf) * 1.01f;
           float sa = sa0, sb = sb0, bt = b0;
-          const int str3[3] = {1, 3, 9};
-          const int fbase = 2 * fside * str3[fk], fsa = str3[fa], fsb = str3[fb];
+          const int pstr[3] = {3, 12, 36};   // padded float stride of m1, m2, m3
+          const int fbase = 2 * fside * pstr[fk], fsa = pstr[fa], fsb = pstr[fb];
 #pragma unroll 1
           for (int it = 0; it < max_it; ++it) {
             float xi[3];
@@ -1146,33 +1155,37 @@ __device__ void fold_bucket(CastSmem& S, CastCtl& ctl, const rc_seg* __restrict_
                             int64_t* __restrict__ counters) {
   const int tid = threadIdx.x;
   constexpr int NT = CWARPS * 32;
-  BucketSmem& B = S.ph.bucket;
-  for (int k = tid; k <= area; k += NT) B.off[k] = 0;
+  FoldSmem& F = S.u.fold;
+  for (int k = tid; k <= area; k += NT) F.off[k] = 0;
   __syncthreads();
+  // one coalesced pass over the unit's segments: (alpha_near, alpha_far) to
+  // shared memory, bucket counts per pixel of the rectangle
   for (int k = tid; k < nitems; k += NT) {
-    const uint32_t pix = segs[k].pixel;
+    const float4 h = reinterpret_cast<const float4*>(segs + k)[0];   // pixel, alpha_near, alpha_far, a
+    const uint32_t pix = __float_as_uint(h.x);
     const int pl = ((int)(pix / (uint32_t)W) - bj0) * bw + ((int)(pix % (uint32_t)W) - bi0);
-    B.rank[k] = (uint16_t)atomicAdd(&B.off[pl], 1);
+    F.alpha[k] = make_float2(h.y, h.z);
+    F.rank[k] = (uint16_t)atomicAdd(&F.off[pl], 1);
   }
   __syncthreads();
   // exclusive scan of the counts over the rectangle (each thread a contiguous range)
   const int per = (area + NT - 1) / NT;
   const int p0 = min(area, tid * per), p1 = min(area, p0 + per);
   int sum = 0;
-  for (int k = p0; k < p1; ++k) sum += B.off[k];
+  for (int k = p0; k < p1; ++k) sum += F.off[k];
   int total;
   int run = block_excl_scan(ctl, sum, total);
   for (int k = p0; k < p1; ++k) {
-    const int c = B.off[k];
-    B.off[k] = run;
+    const int c = F.off[k];
+    F.off[k] = run;
     run += c;
   }
-  if (tid == 0) B.off[area] = total;
+  if (tid == 0) F.off[area] = total;
   __syncthreads();
-  for (int k = tid; k < nitems; k += NT) {
+  for (int k = tid; k < nitems; k += NT) {   // pixel-bucketed order
     const uint32_t pix = segs[k].pixel;
     const int pl = ((int)(pix / (uint32_t)W) - bj0) * bw + ((int)(pix % (uint32_t)W) - bi0);
-    B.order[B.off[pl] + B.rank[k]] = (uint16_t)k;
+    F.order[F.off[pl] + F.rank[k]] = (uint16_t)k;
   }
   __syncthreads();
   // per pixel: order by (alpha_near, index), count runs, then emit (two passes)
@@ -1187,14 +1200,25 @@ __device__ void fold_bucket(CastSmem& S, CastCtl& ctl, const rc_seg* __restrict_
       pos = (int64_t)ctl.base + ex;
     }
     for (int pl = tid; pl < area; pl += NT) {
-      const int o = B.off[pl], n = B.off[pl + 1] - o;
+      const int o = F.off[pl], n = F.off[pl + 1] - o;
       if (n == 0) continue;
+      if (n > PIXSEG) {
+        // rare: too many segments for the registers -> records of single segments
+        if (pass == 0) nrun += n;
+        else
+          for (int t = 0; t < n; ++t) {
+            const rc_seg& sq = segs[F.order[o + t]];
+            if (pos < out_cap) store_seg(out + pos, sq.pixel, sq.alpha_near, sq.alpha_far, sq.a, sq.b, ukey);
+            else atomicAdd((unsigned long long*)&counters[CNT_OVERFLOW], 1ull);
+            ++pos;
+          }
+        continue;
+      }
       float key[PIXSEG];
       int id[PIXSEG];
-      const int m = min(n, PIXSEG);
-      for (int t = 0; t < m; ++t) {   // insertion sort by (alpha_near, index)
-        const int k = B.order[o + t];
-        const float an = segs[k].alpha_near;
+      for (int t = 0; t < n; ++t) {   // insertion sort by (alpha_near, index)
+        const int k = F.order[o + t];
+        const float an = F.alpha[k].x;
         int z = t;
         while (z > 0 && (key[z - 1] > an || (key[z - 1] == an && id[z - 1] > k))) {
           key[z] = key[z - 1];
@@ -1204,41 +1228,32 @@ __device__ void fold_bucket(CastSmem& S, CastCtl& ctl, const rc_seg* __restrict_
         key[z] = an;
         id[z] = k;
       }
-      if (n > PIXSEG) {
-        // rare: too many segments for the registers -> records of single segments
-        if (pass == 0) nrun += n;
-        else
-          for (int t = 0; t < n; ++t) {
-            const rc_seg& sq = segs[B.order[o + t]];
-            if (pos < out_cap) store_seg(out + pos, sq.pixel, sq.alpha_near, sq.alpha_far, sq.a, sq.b, ukey);
-            else atomicAdd((unsigned long long*)&counters[CNT_OVERFLOW], 1ull);
-            ++pos;
-          }
-        continue;
-      }
       int t = 0;
-      while (t < m) {
-        const rc_seg& s0 = segs[id[t]];
-        double A = (double)s0.a, B0 = (double)s0.b[0], B1 = (double)s0.b[1], B2 = (double)s0.b[2];
-        float afr = s0.alpha_far;
+      while (t < n) {
+        float afr = F.alpha[id[t]].y;
         int q = t + 1;
-        for (; q < m; ++q) {
-          const rc_seg& sq = segs[id[q]];
-          if (!touching(sq.alpha_near, afr)) break;
-          if (pass == 1) {
-            B0 = fma(A, (double)sq.b[0], B0);
-            B1 = fma(A, (double)sq.b[1], B1);
-            B2 = fma(A, (double)sq.b[2], B2);
-            A *= (double)sq.a;
-          }
-          afr = sq.alpha_far;
+        while (q < n && touching(key[q], afr)) {
+          afr = F.alpha[id[q]].y;
+          ++q;
         }
         if (pass == 0) {
           ++nrun;
         } else {
+          // fold the run [t, q) nearest first (Eq. aggregate) in fp64
+          double A = 1.0, B0 = 0.0, B1 = 0.0, B2 = 0.0;
+          for (int z = t; z < q; ++z) {
+            const rc_seg* sq = segs + id[z];
+            const float a = sq->a;
+            const float4 hb = reinterpret_cast<const float4*>(sq)[1];   // b0, b1, b2, key
+            B0 = fma(A, (double)hb.x, B0);
+            B1 = fma(A, (double)hb.y, B1);
+            B2 = fma(A, (double)hb.z, B2);
+            A *= (double)a;
+          }
+          const uint32_t pix = (uint32_t)((bj0 + pl / bw) * W + bi0 + pl % bw);
           if (pos < out_cap) {
             const float bf[3] = {(float)B0, (float)B1, (float)B2};
-            store_seg(out + pos, s0.pixel, s0.alpha_near, afr, (float)A, bf, ukey);
+            store_seg(out + pos, pix, key[t], afr, (float)A, bf, ukey);
           } else {
             atomicAdd((unsigned long long*)&counters[CNT_OVERFLOW], 1ull);
           }
@@ -1292,22 +1307,22 @@ __global__ void __launch_bounds__(CWARPS * 32, CAST_CTAS_PER_SM) k_cast_curved(C
     __syncthreads();
     for (int w = tid; w < U.nvis; w += CWARPS * 32) {
       const Rect16 r = vrect[U.vfirst + w];
-      S.rect[w] = r;
+      S.meta.rect[w] = r;
       const int64_t ca = chunk_off[U.vfirst + w], cz = chunk_off[U.vfirst + w + 1];
-      S.coff[w] = (int32_t)(ca - U.chunk_begin);
+      S.meta.coff[w] = (int32_t)(ca - U.chunk_begin);
       const int k0 = (int)max((int64_t)0, ca - U.chunk_begin), k1 = (int)min((int64_t)U.nchunks, cz - U.chunk_begin);
-      for (int k = k0; k < k1; ++k) S.cmap[k] = (uint8_t)w;
+      for (int k = k0; k < k1; ++k) S.meta.cmap[k] = (uint8_t)w;
       atomicMax(&ctl.bb[0], -(int)r.i0);
       atomicMax(&ctl.bb[1], (int)r.i1);
       atomicMax(&ctl.bb[2], -(int)r.j0);
       atomicMax(&ctl.bb[3], (int)r.j1);
     }
     for (int w = warp; w < U.nvis; w += CWARPS)
-      prep_element(S.slot[w], S.org[w], S.ph.prep[warp].prep, trees, L, vis[U.vfirst + w], lane, NF, true);
+      prep_element(S.u.p.slot[w], S.meta.org[w], S.u.p.ph.prep[warp].prep, trees, L, vis[U.vfirst + w], lane, NF, true);
     __syncthreads();
     // ---- phase 1: intersection -----------------------------------------------
     {
-      WarpIsect& W = S.ph.isect[warp];
+      WarpIsect& W = S.u.p.ph.isect[warp];
       if (lane == 0) W.stats[0] = W.stats[1] = 0;
       __syncwarp();
       for (;;) {
@@ -1315,8 +1330,8 @@ __global__ void __launch_bounds__(CWARPS * 32, CAST_CTAS_PER_SM) k_cast_curved(C
         if (lane == 0) k = atomicAdd(&ctl.next_chunk, 1);
         k = __shfl_sync(0xffffffffu, k, 0);
         if (k >= U.nchunks) break;
-        const int lv = S.cmap[k];
-        isect_chunk(W, S.slot[lv], S.org[lv], cc, S.rect[lv], k - S.coff[lv], U.vfirst + lv, items, &ctl.nitems,
+        const int lv = S.meta.cmap[k];
+        isect_chunk(W, S.u.p.slot[lv], S.meta.org[lv], cc, S.meta.rect[lv], k - S.meta.coff[lv], U.vfirst + lv, items, &ctl.nitems,
                     hits_pp, local_hits, face_fail);
       }
       if (lane == 0) {
@@ -1344,7 +1359,7 @@ __global__ void __launch_bounds__(CWARPS * 32, CAST_CTAS_PER_SM) k_cast_curved(C
           pix = __float_as_uint(i3.z);
           an = i3.x;
           afar = i3.y;
-          integ_item<P, N>(S.slot[v - U.vfirst], cc, i0, i1, i2, S.ph.scr + tid, fails, a, bb);
+          integ_item<P, N>(S.u.p.slot[v - U.vfirst], cc, i0, i1, i2, S.u.p.ph.scr + tid, fails, a, bb);
         }
         if (fold > 0) {
           if (act) {
@@ -1378,8 +1393,8 @@ __global__ void __launch_bounds__(CWARPS * 32, CAST_CTAS_PER_SM) k_cast_curved(C
       while (m < n) m <<= 1;
       __syncthreads();
       for (int k = tid; k < m; k += CWARPS * 32) {
-        S.ph.sort.key[k] = k < n ? keys[b0 + k] : ~0ull;
-        S.ph.sort.idx[k] = (uint16_t)k;
+        S.u.sort.key[k] = k < n ? keys[b0 + k] : ~0ull;
+        S.u.sort.idx[k] = (uint16_t)k;
       }
       __syncthreads();
       for (int size = 2; size <= m; size <<= 1) {
@@ -1388,13 +1403,13 @@ __global__ void __launch_bounds__(CWARPS * 32, CAST_CTAS_PER_SM) k_cast_curved(C
             const int p = k ^ stride;
             if (p > k) {
               const bool up = (k & size) == 0;
-              const unsigned long long ka = S.ph.sort.key[k], kb = S.ph.sort.key[p];
+              const unsigned long long ka = S.u.sort.key[k], kb = S.u.sort.key[p];
               if ((ka > kb) == up) {
-                S.ph.sort.key[k] = kb;
-                S.ph.sort.key[p] = ka;
-                const uint16_t t2 = S.ph.sort.idx[k];
-                S.ph.sort.idx[k] = S.ph.sort.idx[p];
-                S.ph.sort.idx[p] = t2;
+                S.u.sort.key[k] = kb;
+                S.u.sort.key[p] = ka;
+                const uint16_t t2 = S.u.sort.idx[k];
+                S.u.sort.idx[k] = S.u.sort.idx[p];
+                S.u.sort.idx[p] = t2;
               }
             }
           }
@@ -1405,8 +1420,8 @@ __global__ void __launch_bounds__(CWARPS * 32, CAST_CTAS_PER_SM) k_cast_curved(C
       // run heads: new pixel, or a gap / overlap beyond the tolerance
       auto is_head = [&](int k) -> bool {
         if (k == 0) return true;
-        if ((S.ph.sort.key[k] >> 32) != (S.ph.sort.key[k - 1] >> 32)) return true;
-        const float an2 = bs[S.ph.sort.idx[k]].alpha_near, afp = bs[S.ph.sort.idx[k - 1]].alpha_far;
+        if ((S.u.sort.key[k] >> 32) != (S.u.sort.key[k - 1] >> 32)) return true;
+        const float an2 = bs[S.u.sort.idx[k]].alpha_near, afp = bs[S.u.sort.idx[k - 1]].alpha_far;
         return fabsf(an2 - afp) > FOLD_TAU * fmaxf(1.0f, fabsf(an2));
       };
       const int per = (n + CWARPS * 32 - 1) / (CWARPS * 32);
@@ -1432,12 +1447,12 @@ __global__ void __launch_bounds__(CWARPS * 32, CAST_CTAS_PER_SM) k_cast_curved(C
       int64_t pos = (int64_t)ctl.base + wbase + incl - nh;
       for (int k = k0; k < k1; ++k) {
         if (!is_head(k)) continue;
-        const rc_seg& s0 = bs[S.ph.sort.idx[k]];
+        const rc_seg& s0 = bs[S.u.sort.idx[k]];
         double A = 1.0, B0 = 0.0, B1 = 0.0, B2 = 0.0;
         float afr = s0.alpha_far;
         int q = k;
         do {
-          const rc_seg& sq = bs[S.ph.sort.idx[q]];
+          const rc_seg& sq = bs[S.u.sort.idx[q]];
           B0 = fma(A, (double)sq.b[0], B0);
           B1 = fma(A, (double)sq.b[1], B1);
           B2 = fma(A, (double)sq.b[2], B2);

@@ -46,6 +46,62 @@ def weighted_ranges(weights: torch.Tensor, nranks: int) -> List[Tuple[int, int]]
     return [(cuts[r], cuts[r + 1]) for r in range(nranks)]
 
 
+MAXLEVEL = 18
+
+
+def node_starts(anchor: torch.Tensor, tree: torch.Tensor, level: torch.Tensor, levels: int) -> torch.Tensor:
+    """Bool mask over the SFC-ordered leaves: True where a node of coarsening
+    level `levels` starts (level c+1 replaces every family of 8 consecutive
+    same-level siblings of level c by the parent).  Cutting
+    the SFC ranges only at these leaves keeps every family of the first
+    `levels` coarsening cycles on one rank ("cuts are aligned to
+    family boundaries"), so fold and aggregation never need a neighbour's
+    leaves.  Vectorised torch (any device); host logic, no method arithmetic."""
+    a = anchor.to(torch.int64)
+    t = tree.to(torch.int64)
+    lv = level.to(torch.int64)
+    first = torch.arange(t.numel(), device=t.device)
+    for _ in range(levels):
+        n = t.numel()
+        if n < 8:
+            break
+        m = n - 7
+        sh = (MAXLEVEL - lv[:m]).clamp(min=0)
+        cid = lambda aa, s: ((aa[:, 0] >> s) & 1) | (((aa[:, 1] >> s) & 1) << 1) | (((aa[:, 2] >> s) & 1) << 2)
+        ok = (lv[:m] >= 1) & (cid(a[:m], sh) == 0)
+        par = a[:m] >> (sh + 1)[:, None]
+        for j in range(1, 8):
+            aj = a[j:j + m]
+            ok &= (t[j:j + m] == t[:m]) & (lv[j:j + m] == lv[:m]) & (cid(aj, sh) == j)
+            ok &= ((aj >> (sh + 1)[:, None]) == par).all(dim=1)
+        start = torch.zeros(n, dtype=torch.bool, device=t.device)
+        start[:m] = ok
+        inside = torch.zeros(n, dtype=torch.bool, device=t.device)
+        for j in range(1, 8):
+            inside[j:] |= start[:n - j]
+        keep = ~inside
+        lv = torch.where(start, lv - 1, lv)[keep]
+        a, t, first = a[keep], t[keep], first[keep]
+    mask = torch.zeros(anchor.shape[0], dtype=torch.bool, device=anchor.device)
+    mask[first] = True
+    return mask
+
+
+def aligned_ranges(weights: torch.Tensor, nranks: int, allowed: torch.Tensor) -> List[Tuple[int, int]]:
+    """weighted_ranges with every cut moved to the next allowed leaf (node start)."""
+    rng = weighted_ranges(weights, nranks)
+    idx = torch.nonzero(allowed.to(torch.bool).cpu()).flatten()
+    n = int(weights.numel())
+    cuts = [0]
+    for r in range(1, nranks):
+        c = rng[r][0]
+        k = int(torch.searchsorted(idx, torch.tensor(c)))
+        cut = int(idx[k]) if k < idx.numel() else n
+        cuts.append(max(cut, cuts[-1]))
+    cuts.append(n)
+    return [(cuts[r], cuts[r + 1]) for r in range(nranks)]
+
+
 def exchange_records(send: torch.Tensor, counts: Sequence[int], group=None) -> torch.Tensor:
     """All-to-all(v) of rc_seg records: `send` is [sum(counts), 8] int32 with
     the records for rank d in rows [sum(counts[:d]), sum(counts[:d+1])).

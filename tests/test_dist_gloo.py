@@ -141,3 +141,25 @@ def test_tile_protocol_gloo_matches_single_process():
     for q, p in enumerate(full["pixels"]):
         # records cross the wire as fp32: compare at fp32 resolution
         assert np.abs(merged[int(p)] - full["rgba"][q]).max() < 1e-6
+
+
+def test_node_starts_match_coarsening_reference():
+    """dist.node_starts (vectorised) vs the plain coarsening reference of
+    oracle/coarsen.py on an adaptive forest; aligned cuts fall on node starts."""
+    import scenegen as sg
+    from oracle import coarsen
+    sc = sg.config2(width=32, maxlevel=5)
+    A, T, L = (torch.as_tensor(x) for x in (sc.leaf_anchor, sc.leaf_tree, sc.leaf_level))
+    ref = coarsen.node_tables(sc.leaf_anchor, sc.leaf_tree, sc.leaf_level, 3)
+    for c in (1, 2, 3):
+        m = rdist.node_starts(A, T, L, c)
+        assert np.array_equal(np.nonzero(m.numpy())[0], ref[c])
+    m3 = rdist.node_starts(A, T, L, 3)
+    rng = rdist.aligned_ranges(torch.ones(sc.num_leaves), 4, m3)
+    assert rng[0][0] == 0 and rng[-1][1] == sc.num_leaves
+    for lo, hi in rng[1:]:
+        assert lo == sc.num_leaves or m3[lo]
+    # uniform forest: level-c nodes start at multiples of 8^c
+    a, t, l = sg.uniform_leaves(2, 3)
+    m = rdist.node_starts(torch.as_tensor(a), torch.as_tensor(t), torch.as_tensor(l), 2)
+    assert np.array_equal(np.nonzero(m.numpy())[0], np.arange(0, 2 * 512, 64))
