@@ -560,6 +560,152 @@ __device__ __noinline__ void prep_element(float* __restrict__ sl, double* __rest
 }
 
 // ---------------------------------------------------------------------------
+// Element preparation by ONE thread (phase 0 runs one element per thread):
+// same result as prep_element (Bernstein points of X_E by restriction of the
+// tree's, fp64, stored fp32 relative to the origin B_(1,1,1); nodal field;
+// affine model A(xi) = Xc + J0 (xi - 1/2) and the bounds dp (nonlinear
+// remainder in J0^-1 coordinates) and eta (its derivative)), without warp
+// shuffles.  Restriction to [u, u+h] per axis: blossoms (u,u), (u,u+h),
+// (u+h,u+h) of the degree-2 Bernstein polynomial (de Casteljau).
+// ---------------------------------------------------------------------------
+__device__ __noinline__ void prep_element_t(float* __restrict__ sl, double* __restrict__ org,
+                                            const TreeConst* __restrict__ trees, const DevLeafView& L, int e, int NF,
+                                            bool with_field) {
+  const double h = ldexp(1.0, -(int)L.level[e]);
+  const double* __restrict__ Bw = trees[L.tree[e]].Bw;   // [q3][q2][q1][xyz]
+  double M[3][3][3];                                     // [axis][r][q]
+#pragma unroll
+  for (int k = 0; k < 3; ++k) {
+    const double u = ldexp((double)L.anchor[3 * (int64_t)e + k], -RC_MAXLEVEL), w = u + h;
+#pragma unroll
+    for (int r = 0; r < 3; ++r) {
+      const double x = r == 2 ? w : u, y = r == 0 ? u : w;
+      M[k][r][0] = (1 - x) * (1 - y);
+      M[k][r][1] = (1 - x) * y + x * (1 - y);
+      M[k][r][2] = x * y;
+    }
+  }
+  // origin = point (1,1,1)
+  double o[3] = {0.0, 0.0, 0.0};
+#pragma unroll
+  for (int q3 = 0; q3 < 3; ++q3)
+#pragma unroll
+    for (int q2 = 0; q2 < 3; ++q2) {
+      const double w23 = M[2][1][q3] * M[1][1][q2];
+#pragma unroll
+      for (int q1 = 0; q1 < 3; ++q1) {
+        const double wq = w23 * M[0][1][q1];
+        const double* b = Bw + ((q3 * 3 + q2) * 3 + q1) * 3;
+#pragma unroll
+        for (int c = 0; c < 3; ++c) o[c] = fma(wq, b[c], o[c]);
+      }
+    }
+  org[0] = o[0];
+  org[1] = o[1];
+  org[2] = o[2];
+  // all 27 points, sum-factorised: axis 3, then 2, then 1
+#pragma unroll 1
+  for (int r3 = 0; r3 < 3; ++r3) {
+    double T2[9][3];
+#pragma unroll
+    for (int q21 = 0; q21 < 9; ++q21)
+#pragma unroll
+      for (int c = 0; c < 3; ++c) {
+        double acc = 0.0;
+#pragma unroll
+        for (int q3 = 0; q3 < 3; ++q3) acc = fma(M[2][r3][q3], Bw[(q3 * 9 + q21) * 3 + c], acc);
+        T2[q21][c] = acc;
+      }
+#pragma unroll 1
+    for (int r2 = 0; r2 < 3; ++r2) {
+      double T1[3][3];
+#pragma unroll
+      for (int q1 = 0; q1 < 3; ++q1)
+#pragma unroll
+        for (int c = 0; c < 3; ++c) {
+          double acc = 0.0;
+#pragma unroll
+          for (int q2 = 0; q2 < 3; ++q2) acc = fma(M[1][r2][q2], T2[q2 * 3 + q1][c], acc);
+          T1[q1][c] = acc;
+        }
+#pragma unroll
+      for (int r1 = 0; r1 < 3; ++r1) {
+        float* dst = sl + GI((r3 * 3 + r2) * 3 + r1);
+#pragma unroll
+        for (int c = 0; c < 3; ++c) {
+          double acc = 0.0;
+#pragma unroll
+          for (int q1 = 0; q1 < 3; ++q1) acc = fma(M[0][r1][q1], T1[q1][c], acc);
+          dst[c] = (float)(acc - o[c]);
+        }
+      }
+    }
+  }
+  if (with_field)
+    for (int q = 0; q < NF; ++q) sl[SLOT_FIELD + FI(q, NF)] = __ldg(&L.field[(int64_t)e * NF + q]);
+  // affine model at the centre from the Bernstein coefficients (fp32)
+  const float wq[3] = {0.25f, 0.5f, 0.25f}, dq[3] = {-1.0f, 0.0f, 1.0f};
+  float Xc[3] = {0.f, 0.f, 0.f}, J[3][3] = {{0.f, 0.f, 0.f}, {0.f, 0.f, 0.f}, {0.f, 0.f, 0.f}};
+#pragma unroll 1
+  for (int m = 0; m < 27; ++m) {
+    const int m1 = m % 3, m2 = (m / 3) % 3, m3 = m / 9;
+    const float* b = sl + GI(m);
+    const float w3 = wq[m1] * wq[m2] * wq[m3];
+    const float g[3] = {dq[m1] * wq[m2] * wq[m3], wq[m1] * dq[m2] * wq[m3], wq[m1] * wq[m2] * dq[m3]};
+#pragma unroll
+    for (int c = 0; c < 3; ++c) {
+      Xc[c] = fmaf(w3, b[c], Xc[c]);
+#pragma unroll
+      for (int a = 0; a < 3; ++a) J[c][a] = fmaf(g[a], b[c], J[c][a]);
+    }
+  }
+  float Ji[3][3];
+  if (!inv3(J, Ji)) {
+#pragma unroll
+    for (int a = 0; a < 3; ++a)
+#pragma unroll
+      for (int b = 0; b < 3; ++b) Ji[a][b] = 0.0f;
+  }
+  float dp0 = 0.f, dp1 = 0.f, dp2 = 0.f, eta = 0.0f;
+#pragma unroll 1
+  for (int m = 0; m < 27; ++m) {
+    const int mmv[3] = {m % 3, (m / 3) % 3, m / 9};
+    const float* b = sl + GI(m);
+    const float x0 = 0.5f * mmv[0] - 0.5f, x1 = 0.5f * mmv[1] - 0.5f, x2 = 0.5f * mmv[2] - 0.5f;
+    const float r0 = b[0] - (Xc[0] + J[0][0] * x0 + J[0][1] * x1 + J[0][2] * x2);
+    const float r1 = b[1] - (Xc[1] + J[1][0] * x0 + J[1][1] * x1 + J[1][2] * x2);
+    const float r2 = b[2] - (Xc[2] + J[2][0] * x0 + J[2][1] * x1 + J[2][2] * x2);
+    dp0 = fmaxf(dp0, fabsf(Ji[0][0] * r0 + Ji[0][1] * r1 + Ji[0][2] * r2));
+    dp1 = fmaxf(dp1, fabsf(Ji[1][0] * r0 + Ji[1][1] * r1 + Ji[1][2] * r2));
+    dp2 = fmaxf(dp2, fabsf(Ji[2][0] * r0 + Ji[2][1] * r1 + Ji[2][2] * r2));
+    // eta: Bernstein coefficients of dE/dxi_a = 2 J0^-1 (B_{m+e_a} - B_m) - e_a (inf-norm)
+    const int str[3] = {1, 3, 9};
+#pragma unroll
+    for (int ax = 0; ax < 3; ++ax) {
+      if (mmv[ax] < 2) {
+        const float* b2 = sl + GI(m + str[ax]);
+        const float e0 = 2.0f * (b2[0] - b[0]), e1 = 2.0f * (b2[1] - b[1]), e2 = 2.0f * (b2[2] - b[2]);
+        const float t0 = Ji[0][0] * e0 + Ji[0][1] * e1 + Ji[0][2] * e2 - (ax == 0 ? 1.0f : 0.0f);
+        const float t1 = Ji[1][0] * e0 + Ji[1][1] * e1 + Ji[1][2] * e2 - (ax == 1 ? 1.0f : 0.0f);
+        const float t2 = Ji[2][0] * e0 + Ji[2][1] * e1 + Ji[2][2] * e2 - (ax == 2 ? 1.0f : 0.0f);
+        eta = fmaxf(eta, fmaxf(fabsf(t0), fmaxf(fabsf(t1), fabsf(t2))));
+      }
+    }
+  }
+  float* af = sl + SLOT_AFF;
+  af[0] = Xc[0]; af[1] = Xc[1]; af[2] = Xc[2];
+#pragma unroll
+  for (int a = 0; a < 3; ++a)
+#pragma unroll
+    for (int b = 0; b < 3; ++b) af[3 + 3 * a + b] = Ji[a][b];
+  // inflate by a rounding margin relative to the element (fp32)
+  af[12] = dp0 * 1.001f + 1e-5f;
+  af[13] = dp1 * 1.001f + 1e-5f;
+  af[14] = dp2 * 1.001f + 1e-5f;
+  af[15] = eta * 1.001f + 1e-5f;
+}
+
+// ---------------------------------------------------------------------------
 // The fused segment kernel (rows a4 + a5 + a6 of SURVEY §8(a)).  Persistent
 // CTAs of CWARPS warps take fold units from a global counter; a unit is a
 // range of <= RC_UNIT_CHUNKS chunks of <= RC_UNIT_LEAVES visible leaves
@@ -1317,8 +1463,8 @@ __global__ void __launch_bounds__(CWARPS * 32, CAST_CTAS_PER_SM) k_cast_curved(C
       atomicMax(&ctl.bb[2], -(int)r.j0);
       atomicMax(&ctl.bb[3], (int)r.j1);
     }
-    for (int w = warp; w < U.nvis; w += CWARPS)
-      prep_element(S.u.p.slot[w], S.meta.org[w], S.u.p.ph.prep[warp].prep, trees, L, vis[U.vfirst + w], lane, NF, true);
+    for (int w = tid; w < U.nvis; w += CWARPS * 32)
+      prep_element_t(S.u.p.slot[w], S.meta.org[w], trees, L, vis[U.vfirst + w], NF, true);
     __syncthreads();
     // ---- phase 1: intersection -----------------------------------------------
     {
