@@ -418,150 +418,10 @@ __device__ __noinline__ int face_roots_subdiv(const Patch& root, float tol, int 
 
 
 
-// ---------------------------------------------------------------------------
-// Element preparation (warp-cooperative, 27 lanes): Bernstein control points
-// of X_E by restriction of the tree's (fp64, three sum-factorised blossom
-// passes), stored fp32 relative to the local origin org = B_(1,1,1) in
-// sl (layout GI / FI / SLOT_FIELD above); optional nodal field; the affine
-// model and its nonlinearity bounds in sl[SLOT_AFF..+15].
-// ---------------------------------------------------------------------------
-
-__device__ __noinline__ void prep_element(float* __restrict__ sl, double* __restrict__ org,
-                                             double (*__restrict__ prep)[81], const TreeConst* __restrict__ trees,
-                                             const DevLeafView& L, int e, unsigned lane, int NF, bool with_field) {
-  const double h = ldexp(1.0, -(int)L.level[e]);
-  if (lane < 27) {
-    const TreeConst& T = trees[L.tree[e]];
-    const int m1 = lane % 3, m2 = (lane / 3) % 3, m3 = lane / 9;
-    const int mm[3] = {m1, m2, m3};
-    double M[3][3];
-#pragma unroll
-    for (int k = 0; k < 3; ++k) {
-      const double u = ldexp((double)L.anchor[3 * (int64_t)e + k], -RC_MAXLEVEL);
-      const double w = u + h;
-      const double x = mm[k] == 2 ? w : u, y = mm[k] == 0 ? u : w;
-      M[k][0] = (1 - x) * (1 - y);
-      M[k][1] = (1 - x) * y + x * (1 - y);
-      M[k][2] = x * y;
-    }
-    double o[3];
-#pragma unroll
-    for (int q3 = 0; q3 < 3; ++q3) {
-      double acc = 0.0;
-#pragma unroll
-      for (int q = 0; q < 3; ++q) acc = fma(M[0][q], T.Bw[((m3 * 3 + m2) * 3 + q) * 3 + q3], acc);
-      prep[0][lane * 3 + q3] = acc;
-    }
-    __syncwarp(0x07ffffffu);
-#pragma unroll
-    for (int q3 = 0; q3 < 3; ++q3) {
-      double acc = 0.0;
-#pragma unroll
-      for (int q = 0; q < 3; ++q) acc = fma(M[1][q], prep[0][((m3 * 3 + q) * 3 + m1) * 3 + q3], acc);
-      o[q3] = acc;
-    }
-    __syncwarp(0x07ffffffu);
-#pragma unroll
-    for (int q3 = 0; q3 < 3; ++q3) prep[1][lane * 3 + q3] = o[q3];
-    __syncwarp(0x07ffffffu);
-#pragma unroll
-    for (int q3 = 0; q3 < 3; ++q3) {
-      double acc = 0.0;
-#pragma unroll
-      for (int q = 0; q < 3; ++q) acc = fma(M[2][q], prep[1][((q * 3 + m2) * 3 + m1) * 3 + q3], acc);
-      o[q3] = acc;
-    }
-    if (lane == 13) {
-      org[0] = o[0];
-      org[1] = o[1];
-      org[2] = o[2];
-    }
-    __syncwarp(0x07ffffffu);
-#pragma unroll
-    for (int q3 = 0; q3 < 3; ++q3) sl[GI(lane) + q3] = (float)(o[q3] - org[q3]);
-    if (with_field && (int)lane < NF) sl[SLOT_FIELD + FI(lane, NF)] = __ldg(&L.field[(int64_t)e * NF + lane]);
-  }
-  __syncwarp();
-        {
-          // affine model A(xi) = Xc + J0 (xi - 1/2) at the centre and the bound
-          // dp_k = max_m |(J0^-1 (B_m - A(m/2)))_k| of the nonlinear remainder
-          // (Bernstein coefficients of X - A; convex hull property).
-          const int m1 = lane % 3, m2 = (lane / 3) % 3, m3 = lane / 9;
-          const float wq[3] = {0.25f, 0.5f, 0.25f}, dq[3] = {-1.0f, 0.0f, 1.0f};
-          float B0 = 0.f, B1 = 0.f, B2 = 0.f;
-          if (lane < 27) { B0 = sl[GI(lane)]; B1 = sl[GI(lane) + 1]; B2 = sl[GI(lane) + 2]; }
-          const float w3 = lane < 27 ? wq[m1] * wq[m2] * wq[m3] : 0.0f;
-          const float g1 = lane < 27 ? dq[m1] * wq[m2] * wq[m3] : 0.0f;
-          const float g2 = lane < 27 ? wq[m1] * dq[m2] * wq[m3] : 0.0f;
-          const float g3 = lane < 27 ? wq[m1] * wq[m2] * dq[m3] : 0.0f;
-          float acc[12] = {w3 * B0, w3 * B1, w3 * B2, g1 * B0, g1 * B1, g1 * B2,
-                           g2 * B0, g2 * B1, g2 * B2, g3 * B0, g3 * B1, g3 * B2};
-#pragma unroll
-          for (int off = 16; off > 0; off >>= 1)
-#pragma unroll
-            for (int t = 0; t < 12; ++t) acc[t] += __shfl_xor_sync(0xffffffffu, acc[t], off);
-          float J[3][3] = {{acc[3], acc[6], acc[9]}, {acc[4], acc[7], acc[10]}, {acc[5], acc[8], acc[11]}};
-          float Ji[3][3];
-          if (!inv3(J, Ji)) {
-#pragma unroll
-            for (int a = 0; a < 3; ++a)
-#pragma unroll
-              for (int b = 0; b < 3; ++b) Ji[a][b] = 0.0f;
-          }
-          float dp0 = 0.f, dp1 = 0.f, dp2 = 0.f;
-          if (lane < 27) {
-            const float x0 = 0.5f * m1 - 0.5f, x1 = 0.5f * m2 - 0.5f, x2 = 0.5f * m3 - 0.5f;
-            const float r0 = B0 - (acc[0] + J[0][0] * x0 + J[0][1] * x1 + J[0][2] * x2);
-            const float r1 = B1 - (acc[1] + J[1][0] * x0 + J[1][1] * x1 + J[1][2] * x2);
-            const float r2 = B2 - (acc[2] + J[2][0] * x0 + J[2][1] * x1 + J[2][2] * x2);
-            dp0 = fabsf(Ji[0][0] * r0 + Ji[0][1] * r1 + Ji[0][2] * r2);
-            dp1 = fabsf(Ji[1][0] * r0 + Ji[1][1] * r1 + Ji[1][2] * r2);
-            dp2 = fabsf(Ji[2][0] * r0 + Ji[2][1] * r1 + Ji[2][2] * r2);
-          }
-          // eta = max over the Bernstein coefficients of dE/dxi_a (E = J0^-1 (X - Xc) - (xi - 1/2)):
-          // 2 J0^-1 (B_{m+e_a} - B_m) - e_a, vector inf-norm (bounds |dE/dxi_a| on the element)
-          float eta = 0.0f;
-          if (lane < 27) {
-            const int mmv[3] = {m1, m2, m3}, str[3] = {1, 3, 9};
-#pragma unroll
-            for (int ax = 0; ax < 3; ++ax) {
-              if (mmv[ax] < 2) {
-                const int n2 = lane + str[ax];
-                const float e0 = 2.0f * (sl[GI(n2)] - B0), e1 = 2.0f * (sl[GI(n2) + 1] - B1), e2 = 2.0f * (sl[GI(n2) + 2] - B2);
-                const float t0 = Ji[0][0] * e0 + Ji[0][1] * e1 + Ji[0][2] * e2 - (ax == 0 ? 1.0f : 0.0f);
-                const float t1 = Ji[1][0] * e0 + Ji[1][1] * e1 + Ji[1][2] * e2 - (ax == 1 ? 1.0f : 0.0f);
-                const float t2 = Ji[2][0] * e0 + Ji[2][1] * e1 + Ji[2][2] * e2 - (ax == 2 ? 1.0f : 0.0f);
-                eta = fmaxf(eta, fmaxf(fabsf(t0), fmaxf(fabsf(t1), fabsf(t2))));
-              }
-            }
-          }
-#pragma unroll
-          for (int off = 16; off > 0; off >>= 1) {
-            dp0 = fmaxf(dp0, __shfl_xor_sync(0xffffffffu, dp0, off));
-            dp1 = fmaxf(dp1, __shfl_xor_sync(0xffffffffu, dp1, off));
-            dp2 = fmaxf(dp2, __shfl_xor_sync(0xffffffffu, dp2, off));
-            eta = fmaxf(eta, __shfl_xor_sync(0xffffffffu, eta, off));
-          }
-          if (lane == 0) {
-            float* af = sl + SLOT_AFF;
-            af[0] = acc[0]; af[1] = acc[1]; af[2] = acc[2];
-#pragma unroll
-            for (int a = 0; a < 3; ++a)
-#pragma unroll
-              for (int b = 0; b < 3; ++b) af[3 + 3 * a + b] = Ji[a][b];
-            // inflate by a rounding margin relative to the element (fp32)
-            af[12] = dp0 * 1.001f + 1e-5f;
-            af[13] = dp1 * 1.001f + 1e-5f;
-            af[14] = dp2 * 1.001f + 1e-5f;
-            af[15] = eta * 1.001f + 1e-5f;
-          }
-        }
-  __syncwarp();
-}
 
 // ---------------------------------------------------------------------------
 // Element preparation by ONE thread (phase 0 runs one element per thread):
-// same result as prep_element (Bernstein points of X_E by restriction of the
+// the element slot (Bernstein points of X_E by restriction of the
 // tree's, fp64, stored fp32 relative to the origin B_(1,1,1); nodal field;
 // affine model A(xi) = Xc + J0 (xi - 1/2) and the bounds dp (nonlinear
 // remainder in J0^-1 coordinates) and eta (its derivative)), without warp
@@ -752,9 +612,6 @@ struct WarpIsect {
   int stats[2];             // face tasks, 2D-path tasks (flushed per unit)
   uint8_t task[MAXT];       // lane << 3 | face
 };
-struct PrepScratch {
-  double prep[2][81];
-};
 struct SortSmem {
   unsigned long long key[SORT_CAP];
   uint16_t idx[SORT_CAP];
@@ -762,7 +619,6 @@ struct SortSmem {
 constexpr int PIXCAP = 2048;   // pixels of a unit's bounding rectangle for the bucket fold
 constexpr int FCAP = 4096;     // segments of a unit for the bucket fold
 union PhaseSmem {              // per-phase scratch of phases 0-2
-  PrepScratch prep[CWARPS];
   WarpIsect isect[CWARPS];
   float scr[RC_MAX_N * CWARPS * 32];   // phase 2: per-thread node values
 };
@@ -953,16 +809,15 @@ __device__ __forceinline__ void isect_chunk(WarpIsect& W, const float* __restric
         const float ta = (side - dpv[k] - xl0[k]) * inv[k], tb = (side + dpv[k] - xl0[k]) * inv[k];
         const float lo = fmaxf(ben, fminf(ta, tb)), hi = fminf(bex, fmaxf(ta, tb));
         if (!(hi >= lo)) continue;
-        // proof of "no root" of the certified iteration (see 1b): the root
-        // x* = (s_a, s_b, beta) lies within ||M0^-1|| max|E| of x0
+        // proof of "no root" (see 1b): any root x* = (s_a, s_b, beta) solves
+        // x* = x0 - M0^-1 E(s*), so |x* - x0|_inf <= ||M0^-1|| max|E| -- no
+        // contraction needed; inconclusive (NaN / inf) bounds keep the face
         const float rk = inv[k];
         const float mnorm = fmaxf(fabsf(rk), 1.0f + fabsf(dl[fa] * rk) + fabsf(dl[fb] * rk));
-        if (mnorm * eta2 < 0.25f) {
-          const float b0 = (side - xl0[k]) * rk;
-          const float sa0 = xl0[fa] + b0 * dl[fa], sb0 = xl0[fb] + b0 * dl[fb];
-          const float rho = mnorm * dpm + FACE_TOL;
-          if (sa0 < -rho || sa0 > 1.0f + rho || sb0 < -rho || sb0 > 1.0f + rho) continue;
-        }
+        const float b0 = (side - xl0[k]) * rk;
+        const float sa0 = xl0[fa] + b0 * dl[fa], sb0 = xl0[fb] + b0 * dl[fb];
+        const float rho = mnorm * dpm + FACE_TOL;
+        if (sa0 < -rho || sa0 > 1.0f + rho || sb0 < -rho || sb0 > 1.0f + rho) continue;
         face_mask |= 1u << f;
       }
     }

@@ -18,3 +18,11 @@ PCMD="python tools/profile_frame.py --config ${PROFCFG:-45} --frames 1"
 timeout 300 $PCMD > $OUT/plain_pf.log 2>&1 && \
   timeout 900 ncu --set full --clock-control none --import-source on -k regex:'k_cast_curved' -c 1 -o $OUT/prof $PCMD > $OUT/ncu_full.log 2>&1
 echo "ncu full exit $?" >> $OUT/status
+# DRAM traffic of the segment kernel at the bench's config (one metric pass: no replay of the big buffers)
+if [ -n "${TRAFFIC:-}" ]; then
+  TCMD="python tools/profile_frame.py --config 4 --frames 3"
+  timeout 600 $TCMD > $OUT/plain_traffic.log 2>&1 && \
+    timeout 900 ncu --metrics dram__bytes_read.sum,dram__bytes_write.sum,gpu__time_duration.sum --clock-control none \
+      -k regex:'k_cast_curved' -s 2 -c 1 --csv --log-file $OUT/traffic_c4.csv $TCMD > $OUT/ncu_traffic.log 2>&1
+  echo "traffic exit $?" >> $OUT/status
+fi
