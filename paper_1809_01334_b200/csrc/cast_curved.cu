@@ -595,7 +595,10 @@ __device__ __noinline__ void prep_element_t(float* __restrict__ sl, double* __re
 //    the paper's coarsening done on chip.
 //    Without folding every segment is a record keyed by its leaf.
 // ---------------------------------------------------------------------------
-constexpr int CWARPS = 4;
+#ifndef CAST_WARPS
+#define CAST_WARPS 4        // warps per CTA
+#endif
+constexpr int CWARPS = CAST_WARPS;
 #ifndef CAST_CTAS_PER_SM
 #define CAST_CTAS_PER_SM 3   // resident CTAs per SM (launch bounds: 168 registers, ~60 KB shared memory)
 #endif
@@ -658,8 +661,23 @@ struct CastCtl {
 // per-CTA global scratch (bytes)
 constexpr size_t SCR_ITEMS = (size_t)ITEM_CAP * 64;
 constexpr size_t SCR_SEGS = (size_t)ITEM_CAP * sizeof(rc_seg);
-constexpr size_t SCR_KEYS = (size_t)ITEM_CAP * 8;
-constexpr size_t SCR_PER_CTA = SCR_ITEMS + SCR_SEGS + SCR_KEYS;
+constexpr size_t SCR_PER_CTA = SCR_ITEMS + SCR_SEGS;
+
+// Scratch lines of a finished unit are dead: drop them from L2 without a
+// write-back (they would otherwise reach HBM as ~100 B per segment).
+__device__ __forceinline__ void discard_l2(const void* base, size_t bytes) {
+  const char* p = reinterpret_cast<const char*>(base);
+  for (size_t off = (size_t)threadIdx.x * 128; off < bytes; off += (size_t)blockDim.x * 128)
+    asm volatile("discard.global.L2 [%0], 128;" ::"l"(p + off) : "memory");
+}
+
+// output records: streaming stores (evict-first; they are not re-read by this kernel)
+__device__ __forceinline__ void store_seg_cs(rc_seg* dst, uint32_t pixel, float an, float af, float a,
+                                             const float b[3], uint32_t key) {
+  float4* d = reinterpret_cast<float4*>(dst);
+  __stcs(d, make_float4(__uint_as_float(pixel), an, af, a));
+  __stcs(d + 1, make_float4(b[0], b[1], b[2], __uint_as_float(key)));
+}
 
 // warp-aggregated append on a shared-memory counter
 __device__ __forceinline__ int warp_append_smem(int* counter, int want) {
@@ -1120,10 +1138,9 @@ __device__ __forceinline__ void integ_item(const float* __restrict__ gs, const C
 // ---- phase 3, common case: bucket fold -------------------------------------
 // The unit's segments are bucketed by pixel over the unit's bounding rectangle
 // (shared-memory counting sort), each pixel's few segments (one per element
-// the ray crosses in the unit) are ordered by alpha_near in registers, and
+// the ray crosses in the unit) are ordered by alpha_near in place, and
 // every maximal run of touching segments is combined nearest-first with
 // Eq. aggregate in fp64 and written as one record.
-constexpr int PIXSEG = 16;   // segments of one pixel ordered in registers (more: slow path)
 
 __device__ __forceinline__ int block_excl_scan(CastCtl& ctl, int v, int& total) {
   const unsigned lane = threadIdx.x & 31;
@@ -1203,38 +1220,29 @@ __device__ void fold_bucket(CastSmem& S, CastCtl& ctl, const rc_seg* __restrict_
     for (int pl = tid; pl < area; pl += NT) {
       const int o = F.off[pl], n = F.off[pl + 1] - o;
       if (n == 0) continue;
-      if (n > PIXSEG) {
-        // rare: too many segments for the registers -> records of single segments
-        if (pass == 0) nrun += n;
-        else
-          for (int t = 0; t < n; ++t) {
-            const rc_seg& sq = segs[F.order[o + t]];
-            if (pos < out_cap) store_seg(out + pos, sq.pixel, sq.alpha_near, sq.alpha_far, sq.a, sq.b, ukey);
-            else atomicAdd((unsigned long long*)&counters[CNT_OVERFLOW], 1ull);
-            ++pos;
+      uint16_t* ord = F.order + o;
+      if (pass == 0) {
+        // insertion sort of the pixel's slice by (alpha_near, index), in place
+        for (int t = 1; t < n; ++t) {
+          const int k = ord[t];
+          const float an = F.alpha[k].x;
+          int z = t;
+          while (z > 0) {
+            const int kp = ord[z - 1];
+            const float ap = F.alpha[kp].x;
+            if (!(ap > an || (ap == an && kp > k))) break;
+            ord[z] = (uint16_t)kp;
+            --z;
           }
-        continue;
-      }
-      float key[PIXSEG];
-      int id[PIXSEG];
-      for (int t = 0; t < n; ++t) {   // insertion sort by (alpha_near, index)
-        const int k = F.order[o + t];
-        const float an = F.alpha[k].x;
-        int z = t;
-        while (z > 0 && (key[z - 1] > an || (key[z - 1] == an && id[z - 1] > k))) {
-          key[z] = key[z - 1];
-          id[z] = id[z - 1];
-          --z;
+          ord[z] = (uint16_t)k;
         }
-        key[z] = an;
-        id[z] = k;
       }
       int t = 0;
       while (t < n) {
-        float afr = F.alpha[id[t]].y;
+        float afr = F.alpha[ord[t]].y;
         int q = t + 1;
-        while (q < n && touching(key[q], afr)) {
-          afr = F.alpha[id[q]].y;
+        while (q < n && touching(F.alpha[ord[q]].x, afr)) {
+          afr = F.alpha[ord[q]].y;
           ++q;
         }
         if (pass == 0) {
@@ -1243,7 +1251,7 @@ __device__ void fold_bucket(CastSmem& S, CastCtl& ctl, const rc_seg* __restrict_
           // fold the run [t, q) nearest first (Eq. aggregate) in fp64
           double A = 1.0, B0 = 0.0, B1 = 0.0, B2 = 0.0;
           for (int z = t; z < q; ++z) {
-            const rc_seg* sq = segs + id[z];
+            const rc_seg* sq = segs + ord[z];
             const float a = sq->a;
             const float4 hb = reinterpret_cast<const float4*>(sq)[1];   // b0, b1, b2, key
             B0 = fma(A, (double)hb.x, B0);
@@ -1254,7 +1262,7 @@ __device__ void fold_bucket(CastSmem& S, CastCtl& ctl, const rc_seg* __restrict_
           const uint32_t pix = (uint32_t)((bj0 + pl / bw) * W + bi0 + pl % bw);
           if (pos < out_cap) {
             const float bf[3] = {(float)B0, (float)B1, (float)B2};
-            store_seg(out + pos, pix, key[t], afr, (float)A, bf, ukey);
+            store_seg_cs(out + pos, pix, F.alpha[ord[t]].x, afr, (float)A, bf, ukey);
           } else {
             atomicAdd((unsigned long long*)&counters[CNT_OVERFLOW], 1ull);
           }
@@ -1289,11 +1297,15 @@ __global__ void __launch_bounds__(CWARPS * 32, CAST_CTAS_PER_SM) k_cast_curved(C
   unsigned char* my = scratch + (size_t)blockIdx.x * SCR_PER_CTA;
   float4* items = reinterpret_cast<float4*>(my);
   rc_seg* segs = reinterpret_cast<rc_seg*>(my + SCR_ITEMS);
-  unsigned long long* keys = reinterpret_cast<unsigned long long*>(my + SCR_ITEMS + SCR_SEGS);
   int local_hits = 0, face_fail = 0, fails = 0;
   long long raw_local = 0, n_tasks = 0, n_fallback = 0;
+  int prev_items = 0;
   for (;;) {
-    __syncthreads();   // the previous unit's shared state (ctl, S) is no longer read
+    __syncthreads();   // the previous unit's shared state (ctl, S) and scratch are no longer read
+    if (prev_items > 0) {
+      discard_l2(items, ((size_t)prev_items * 64 + 127) & ~(size_t)127);
+      if (fold > 0) discard_l2(segs, ((size_t)prev_items * sizeof(rc_seg) + 127) & ~(size_t)127);
+    }
     if (tid == 0) {
       ctl.unit = (int64_t)atomicAdd((unsigned long long*)&counters[CNT_UNITS], 1ull);
       ctl.next_chunk = 0;
@@ -1343,6 +1355,7 @@ __global__ void __launch_bounds__(CWARPS * 32, CAST_CTAS_PER_SM) k_cast_curved(C
     __syncthreads();
     const int nitems = min(ctl.nitems, ITEM_CAP);
     raw_local += (tid == 0) ? nitems : 0;
+    prev_items = nitems;
     // ---- phase 2: integration ---------------------------------------------------
     {
       const int ngroups = (nitems + 31) / 32;
@@ -1365,12 +1378,11 @@ __global__ void __launch_bounds__(CWARPS * 32, CAST_CTAS_PER_SM) k_cast_curved(C
         if (fold > 0) {
           if (act) {
             store_seg(segs + idx, pix, an, afar, a, bb, U.key);
-            keys[idx] = fold_key(pix, an);
           }
         } else {
           const int64_t slot = warp_append(&counters[CNT_SEGS], act ? 1 : 0);
           if (act) {
-            if (slot < out_cap) store_seg(out + slot, pix, an, afar, a, bb, key_base + (uint32_t)vis[v]);
+            if (slot < out_cap) store_seg_cs(out + slot, pix, an, afar, a, bb, key_base + (uint32_t)vis[v]);
             else atomicAdd((unsigned long long*)&counters[CNT_OVERFLOW], 1ull);
           }
         }
@@ -1394,7 +1406,7 @@ __global__ void __launch_bounds__(CWARPS * 32, CAST_CTAS_PER_SM) k_cast_curved(C
       while (m < n) m <<= 1;
       __syncthreads();
       for (int k = tid; k < m; k += CWARPS * 32) {
-        S.u.sort.key[k] = k < n ? keys[b0 + k] : ~0ull;
+        S.u.sort.key[k] = k < n ? fold_key(segs[b0 + k].pixel, segs[b0 + k].alpha_near) : ~0ull;
         S.u.sort.idx[k] = (uint16_t)k;
       }
       __syncthreads();

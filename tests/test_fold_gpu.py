@@ -74,8 +74,9 @@ def test_fold_levels_curved(level, width):
         assert g["raw_segments"] == g0["count"]
         assert np.array_equal(g["hits_per_pixel"], g0["hits_per_pixel"])
         assert g["hit_pairs"] == g0["hit_pairs"]
-        # fewer records while the node level stays below the tree roots (level `level`)
-        assert g["count"] < prev if c <= level else g["count"] <= prev, (c, g["count"], prev)
+        # fewer records while the nodes grow (fold units hold <= 64 leaves, so
+        # beyond level 2 the fused fold cannot merge more; rc_aggregate can)
+        assert g["count"] < prev if c <= min(level, 2) else g["count"] <= prev, (c, g["count"], prev)
         prev = g["count"]
         assert np.abs(g["rgba"] - g0["rgba"]).max() < LOSSLESS
         rep = compare(sc, g, ores, pixels, by_counts=True)
