@@ -599,6 +599,9 @@ __device__ __noinline__ void prep_element_t(float* __restrict__ sl, double* __re
 #define CAST_WARPS 4        // warps per CTA
 #endif
 constexpr int CWARPS = CAST_WARPS;
+#ifndef FAST_Q
+#define FAST_Q 0.25f        // contraction bound below which a face root takes the certified fast path
+#endif
 #ifndef CAST_CTAS_PER_SM
 #define CAST_CTAS_PER_SM 3   // resident CTAs per SM (launch bounds: 168 registers, ~60 KB shared memory)
 #endif
@@ -880,13 +883,13 @@ __device__ __forceinline__ void isect_chunk(WarpIsect& W, const float* __restric
         // Certified fast path.  In xi~ coordinates the face is
         // (s_a, s_b, side) + E(s) and the ray xl0 + beta dl, so the root
         // x = (s_a, s_b, beta) solves x = x0 - M0^-1 E(s) with M0 = [e_a, e_b, -dl];
-        // the map contracts with q = ||M0^-1|| 2 eta < 1/4 (uniqueness +
+        // the map contracts with q = ||M0^-1|| 2 eta < FAST_Q < 1 (uniqueness +
         // convergence; the exclusion was proven in 1a).
         const float dk = tdl[fk];
         const float rk = 1.0f / dk;
         const float mnorm = fmaxf(fabsf(rk), 1.0f + fabsf(tdl[fa] * rk) + fabsf(tdl[fb] * rk));
         const float qf = mnorm * eta2;
-        if (qf < 0.25f) {
+        if (qf < FAST_Q) {
           const float b0 = ((float)fside - txl0[fk]) * rk;
           const float sa0 = txl0[fa] + b0 * tdl[fa], sb0 = txl0[fb] + b0 * tdl[fb];
           const float qfac = qf / (1.0f - qf) * 1.01f;

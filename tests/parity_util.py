@@ -4,7 +4,7 @@ import numpy as np
 import oracle
 
 
-def gpu_run(scene, background=(0.0, 0.0, 0.0), device_copy=False, fold=0, cycles=0):
+def gpu_run(scene, background=(0.0, 0.0, 0.0), device_copy=False, fold=0, cycles=0, keep_raw=True):
     import torch
     from paper_1809_01334_b200 import rc
     f = rc.Forest.from_scene(scene, device_copy=device_copy)
@@ -15,7 +15,7 @@ def gpu_run(scene, background=(0.0, 0.0, 0.0), device_copy=False, fold=0, cycles
     if cycles:
         f.aggregate(cycles)
     segs = f.segments()
-    raw = segs["raw"].cpu().numpy().copy()
+    raw = segs["raw"].cpu().numpy().copy() if keep_raw else None
     hpp = segs["hits_per_pixel"].cpu().numpy().copy()
     img = f.composite(background).cpu().numpy().copy()
     torch.cuda.synchronize()
@@ -45,12 +45,13 @@ def compare(scene, g, ores, pixels, cull=None, tol=1e-4, by_counts=False):
         sg_ = set(g["visible"].tolist()) - set(np.nonzero(amb_o)[0].tolist())
         rep["cull_mismatch"] = len(so ^ sg_)
         rep["cull_ambiguous"] = int(amb_o.sum())
-    cols = seg_columns(g["raw"])
-    order = np.argsort(cols["pixel"], kind="stable")
-    pix_sorted = cols["pixel"][order]
-    keys_sorted = cols["key"][order]
-    lo = np.searchsorted(pix_sorted, pixels, side="left")
-    hi = np.searchsorted(pix_sorted, pixels, side="right")
+    if not by_counts:
+        cols = seg_columns(g["raw"])
+        order = np.argsort(cols["pixel"], kind="stable")
+        pix_sorted = cols["pixel"][order]
+        keys_sorted = cols["key"][order]
+        lo = np.searchsorted(pix_sorted, pixels, side="left")
+        hi = np.searchsorted(pix_sorted, pixels, side="right")
     hit_mismatch, amb_pairs, amb_pixels, bad_pix, bad_amb_pix = 0, 0, 0, 0, 0
     maxerr, maxerr_amb = 0.0, 0.0
     for q, p in enumerate(pixels):

