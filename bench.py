@@ -227,6 +227,10 @@ def main():
     else:
         lo, hi = 0, n
     forest = rc.Forest.from_scene(scene, first=lo, count=hi - lo, device_copy=True)
+    # the forest holds its own device copy: keep the scene on the host only
+    # (e2e inputs, CPU baseline) and hand the generator's memory back (C5 needs it)
+    scene = scene_to_host(scene)
+    torch.cuda.empty_cache()
     img = torch.empty((H, W, 4), dtype=torch.float32, device=dev)
     flush = torch.empty(int(160e6) // 4, dtype=torch.float32, device=dev)   # > 126 MB L2
     stream = torch.cuda.current_stream()

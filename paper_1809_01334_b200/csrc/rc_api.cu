@@ -49,7 +49,7 @@ static cudaError_t grow(T** p, int64_t* cap, int64_t need) {
   if (need <= *cap && *p) return cudaSuccess;
   if (*p) cudaFree(*p);
   *p = nullptr;
-  int64_t c = std::max<int64_t>(need + need / 8, 64);
+  int64_t c = std::max<int64_t>(need + std::min<int64_t>(need / 8, (int64_t)1 << 24), 64);   // bounded slack
   cudaError_t e = cudaMalloc((void**)p, sizeof(T) * (size_t)c);
   if (e == cudaSuccess) *cap = c;
   else *cap = 0;
@@ -743,22 +743,31 @@ static rc_status aggregate_to(rc_forest* f, int level, cudaStream_t s) {
   int64_t need_tmp = (int64_t)scan_tmp_size(npix + 1) + 128;
   if (need_tmp > f->scan_tmp_cap) CU(grow(&f->d_scan_tmp, &f->scan_tmp_cap, need_tmp));
   CU(grow(&f->d_perm, &f->perm_cap, std::max<int64_t>(nrec, 1)));
-  CU(grow(&f->d_segs2, &f->seg2_cap, std::max<int64_t>(nrec, 1)));
   const int grid = sm_count() * 8;
   CU(cudaMemsetAsync(f->d_pix_cnt, 0, sizeof(int32_t) * npix, s));
   if (nrec > 0) CU(launch_hist(f->d_segs, nrec, f->d_pix_cnt, grid, s));
   CU(scan_exclusive<int32_t>(f->d_pix_cnt, f->d_pix_off, npix, f->d_scan_tmp, s));
   CU(cudaMemsetAsync(f->d_pix_cnt, 0, sizeof(int32_t) * npix, s));
   if (nrec > 0) CU(launch_scatter(f->d_segs, nrec, f->d_pix_off, f->d_pix_cnt, f->d_perm, grid, s));
-  CU(cudaMemsetAsync(f->d_counters + CNT_AGG_OUT, 0, sizeof(int64_t), s));
-  CU(launch_coarsen(f->d_segs, f->d_perm, f->d_pix_off, npix, f->d_node_first[level], f->n_nodes[level],
-                    (uint32_t)f->first_global, 1e-6f, f->d_segs2, f->seg2_cap, f->d_counters, sm_count() * 16, s));
+  // output buffer: half the input first (a cycle roughly halves the count,
+  // PAPER.md:976-977), grown to the exact count and the pass repeated if short
+  int64_t want = std::max<int64_t>(nrec / 2 + 4096, 1);
   int64_t nout = 0;
-  CU(cudaMemcpyAsync(&nout, f->d_counters + CNT_AGG_OUT, sizeof(int64_t), cudaMemcpyDeviceToHost, s));
+  for (int attempt = 0; attempt < 2; ++attempt) {
+    CU(grow(&f->d_segs2, &f->seg2_cap, want));
+    CU(cudaMemsetAsync(f->d_counters + CNT_AGG_OUT, 0, sizeof(int64_t), s));
+    CU(cudaMemsetAsync(f->d_counters + CNT_OVERFLOW, 0, sizeof(int64_t), s));
+    CU(launch_coarsen(f->d_segs, f->d_perm, f->d_pix_off, npix, f->d_node_first[level], f->n_nodes[level],
+                      (uint32_t)f->first_global, 1e-6f, f->d_segs2, f->seg2_cap, f->d_counters, sm_count() * 16, s));
+    CU(cudaMemcpyAsync(&nout, f->d_counters + CNT_AGG_OUT, sizeof(int64_t), cudaMemcpyDeviceToHost, s));
+    CU(cudaStreamSynchronize(s));
+    if (nout <= f->seg2_cap) break;
+    want = nout;
+  }
+  if (nout > f->seg2_cap) return fail(RC_ERR_CAPACITY, "aggregation output overflow");
+  CU(cudaMemsetAsync(f->d_counters + CNT_OVERFLOW, 0, sizeof(int64_t), s));
   CU(cudaMemcpyAsync(f->d_counters + CNT_SEGS, f->d_counters + CNT_AGG_OUT, sizeof(int64_t),
                      cudaMemcpyDeviceToDevice, s));
-  CU(cudaStreamSynchronize(s));
-  if (nout > f->seg2_cap) return fail(RC_ERR_CAPACITY, "aggregation output overflow");
   std::swap(f->d_segs, f->d_segs2);
   std::swap(f->seg_cap, f->seg2_cap);
   f->rec_level = level;

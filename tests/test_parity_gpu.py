@@ -246,12 +246,14 @@ def test_c5_full_size_sampled():
     6..10, 4096^2, N = 8, fold 2 + 3 aggregation cycles = bench.py's launch
     configuration); 256 stratified pixels compared one by one with the oracle
     (which culls every leaf in fp64)."""
-    sc = sg.config5(device="cuda")
-    g = gpu_run(sc, device_copy=True, fold=2, cycles=3, keep_raw=False)
+    import torch
+    import bench
+    sc = bench.scene_to_host(sg.config5(device="cuda"))   # generated on the GPU, kept on the host
+    torch.cuda.empty_cache()
+    g = gpu_run(sc, fold=2, cycles=3, keep_raw=False)
     assert g["newton_failures"] == 0 and g["level"] == 5
     assert g["count"] < g["raw_segments"] // 4
-    import bench
-    o = oracle.OracleScene(bench.scene_to_host(sc))
+    o = oracle.OracleScene(sc)
     W = sc.camera.width
     jj, ii = np.meshgrid(np.arange(101, W, 256), np.arange(77, W, 256), indexing="ij")
     pixels = (jj * W + ii).ravel().astype(np.int32)
