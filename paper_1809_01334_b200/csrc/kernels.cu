@@ -547,6 +547,85 @@ struct Sweep {
 constexpr int FOLD_WARPS = 4;
 constexpr int FOLD_CAP = 2048;   // records per pixel sorted in shared memory
 
+// Common case of the per-pixel fold: up to 32 E records sorted by
+// (alpha_near, key) in registers (warp bitonic network over the blocked
+// layout i = lane E + e: in-register exchanges for distances < E, shuffles
+// beyond), then each lane folds its E consecutive records and the lanes are
+// combined by an ordered tree reduction (Eq. aggregate is associative,
+// PAPER.md:395-427).  Returns false when consecutive records overlap beyond
+// tau (the caller then cuts and averages in the sequential sweep).
+template <int E>
+__device__ __forceinline__ bool fold_pixel_reg(const rc_seg* __restrict__ recs, const uint32_t* __restrict__ S, int n,
+                                               float tau, Acc& acc) {
+  const unsigned lane = threadIdx.x & 31;
+  constexpr int NN = 32 * E;
+  uint64_t key[E];
+  uint32_t id[E];
+#pragma unroll
+  for (int e = 0; e < E; ++e) {
+    const int i = (int)lane * E + e;
+    id[e] = i < n ? S[i] : 0xffffffffu;
+    key[e] = i < n ? sort_key(recs[id[e]]) : ~0ull;
+  }
+#pragma unroll
+  for (int k = 2; k <= NN; k <<= 1) {
+#pragma unroll
+    for (int j = k >> 1; j > 0; j >>= 1) {
+      if (j < E) {
+#pragma unroll
+        for (int e = 0; e < E; ++e) {
+          const int p = e ^ j;
+          if (p > e) {
+            const bool up = ((((int)lane * E + e) & k) == 0);
+            if ((key[e] > key[p]) == up) {
+              const uint64_t tk = key[e]; key[e] = key[p]; key[p] = tk;
+              const uint32_t ti = id[e]; id[e] = id[p]; id[p] = ti;
+            }
+          }
+        }
+      } else {
+        const int lj = j / E;
+        const bool lower = (lane & lj) == 0;
+#pragma unroll
+        for (int e = 0; e < E; ++e) {
+          const uint64_t ok = __shfl_xor_sync(0xffffffffu, key[e], lj);
+          const uint32_t oi = __shfl_xor_sync(0xffffffffu, id[e], lj);
+          const bool up = ((((int)lane * E + e) & k) == 0);
+          const bool take = (lower == up) ? (ok < key[e]) : (ok > key[e]);
+          if (take) {
+            key[e] = ok;
+            id[e] = oi;
+          }
+        }
+      }
+    }
+  }
+  // overlap check between consecutive records, then the lane's ordered fold
+  float prev_af = __shfl_up_sync(0xffffffffu, id[E - 1] != 0xffffffffu ? recs[id[E - 1]].alpha_far : -3.4e38f, 1);
+  if (lane == 0) prev_af = -3.4e38f;
+  bool ovl = false;
+  Acc a{1.0, 0.0, 0.0, 0.0};
+#pragma unroll
+  for (int e = 0; e < E; ++e) {
+    if (id[e] == 0xffffffffu) continue;
+    const rc_seg& r = recs[id[e]];
+    ovl |= (prev_af - r.alpha_near) > tau * fmaxf(1.0f, fabsf(r.alpha_near));
+    prev_af = r.alpha_far;
+    acc_push(a, r.a, r.b[0], r.b[1], r.b[2]);
+  }
+  if (__any_sync(0xffffffffu, ovl)) return false;
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    const double A = __shfl_down_sync(0xffffffffu, a.A, o);
+    const double B0 = __shfl_down_sync(0xffffffffu, a.B0, o);
+    const double B1 = __shfl_down_sync(0xffffffffu, a.B1, o);
+    const double B2 = __shfl_down_sync(0xffffffffu, a.B2, o);
+    if ((lane & (2 * o - 1)) == 0) acc_push(a, A, B0, B1, B2);
+  }
+  acc = a;
+  return true;
+}
+
 __global__ void __launch_bounds__(FOLD_WARPS * 32) k_fold(const rc_seg* __restrict__ recs,
                                                           const uint32_t* __restrict__ perm,
                                                           const int64_t* __restrict__ off, int W, int H, int tw,
@@ -571,7 +650,15 @@ __global__ void __launch_bounds__(FOLD_WARPS * 32) k_fold(const rc_seg* __restri
     int n = (int)(off[pix + 1] - base);
     const uint32_t* S = perm + base;   // S[k] = index of the pixel's k-th record
     Acc acc{1.0, 0.0, 0.0, 0.0};
-    if (n <= FOLD_CAP) {
+    bool done = false;
+    if (n <= 32) done = fold_pixel_reg<1>(recs, S, n, tau, acc);
+    else if (n <= 64) done = fold_pixel_reg<2>(recs, S, n, tau, acc);
+    else if (n <= 128) done = fold_pixel_reg<4>(recs, S, n, tau, acc);
+    else if (n <= 256) done = fold_pixel_reg<8>(recs, S, n, tau, acc);
+    else if (n <= 512) done = fold_pixel_reg<16>(recs, S, n, tau, acc);
+    if (done) {
+      // lane 0 holds the pixel's fold
+    } else if (n <= FOLD_CAP) {
       int m = 1;
       while (m < n) m <<= 1;
       for (int k = lane; k < m; k += 32) {

@@ -510,6 +510,11 @@ extern "C" rc_status rc_cast_segments(rc_forest* f, int32_t fold_levels, void* s
   }
   // record capacity: the previous frame's count, else an estimate; a too
   // small buffer is grown to the exact count and the cast repeated
+  // reuse the larger of the two record buffers (aggregation swaps them)
+  if (f->seg2_cap > f->seg_cap) {
+    std::swap(f->d_segs, f->d_segs2);
+    std::swap(f->seg_cap, f->seg2_cap);
+  }
   int64_t est = curved ? (fold_levels > 0 ? cand / 8 : cand / 2 + cand / 8) : cand;
   int64_t need = std::max<int64_t>(f->h_seg_total + f->h_seg_total / 8, est) + 4096;
   CU(grow(&f->d_segs, &f->seg_cap, need));
@@ -749,9 +754,10 @@ static rc_status aggregate_to(rc_forest* f, int level, cudaStream_t s) {
   CU(scan_exclusive<int32_t>(f->d_pix_cnt, f->d_pix_off, npix, f->d_scan_tmp, s));
   CU(cudaMemsetAsync(f->d_pix_cnt, 0, sizeof(int32_t) * npix, s));
   if (nrec > 0) CU(launch_scatter(f->d_segs, nrec, f->d_pix_off, f->d_pix_cnt, f->d_perm, grid, s));
-  // output buffer: half the input first (a cycle roughly halves the count,
-  // PAPER.md:976-977), grown to the exact count and the pass repeated if short
-  int64_t want = std::max<int64_t>(nrec / 2 + 4096, 1);
+  // output buffer: half the input first for one cycle, a quarter for several
+  // (a cycle roughly halves the count), grown to the exact
+  // count and the pass repeated if short
+  int64_t want = std::max<int64_t>(nrec / (level - f->rec_level >= 2 ? 4 : 2) + 4096, 1);
   int64_t nout = 0;
   for (int attempt = 0; attempt < 2; ++attempt) {
     CU(grow(&f->d_segs2, &f->seg2_cap, want));
