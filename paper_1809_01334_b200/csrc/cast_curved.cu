@@ -622,7 +622,7 @@ struct SortSmem {
   unsigned long long key[SORT_CAP];
   uint16_t idx[SORT_CAP];
 };
-constexpr int PIXCAP = 2048;   // pixels of a unit's bounding rectangle for the bucket fold
+constexpr int PIXCAP = 4096;   // pixels of a unit's bounding rectangle for the bucket fold
 constexpr int FCAP = 4096;     // segments of a unit for the bucket fold
 union PhaseSmem {              // per-phase scratch of phases 0-2
   WarpIsect isect[CWARPS];
