@@ -332,6 +332,7 @@ def main():
         dev_in = [p.to(dev, non_blocking=True) for p in pinned]
         f2 = rc.Forest(scene.tree_ctrl, scene.geom_degree, scene.field_degree, *dev_in, scene.kappa0,
                        scene.inv_F, scene.q0, first_global_leaf=lo)
+        del dev_in            # the forest owns its device copy (C5 needs the memory back)
         f2.camera_set(cam)
         f2.cull()
         f2.cast_segments(fold)
@@ -347,7 +348,6 @@ def main():
         torch.cuda.synchronize()
         dt = time.perf_counter() - t0
         f2.close()
-        del dev_in
         if it >= 2:
             e2e_times.append(dt)
     e2e_s = sum(e2e_times) / len(e2e_times)

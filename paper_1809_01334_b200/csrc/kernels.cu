@@ -547,6 +547,65 @@ struct Sweep {
 constexpr int FOLD_WARPS = 4;
 constexpr int FOLD_CAP = 2048;   // records per pixel sorted in shared memory
 
+// Warp register bitonic sort of a pixel's n <= 32 E records by (alpha_near,
+// key); the sorted keys and local indices (0..n-1) go to shared memory.
+template <int E>
+__device__ __forceinline__ void sort_pixel_reg(const rc_seg* __restrict__ recs, const uint32_t* __restrict__ S, int n,
+                                               uint64_t* __restrict__ keys_out, uint16_t* __restrict__ idx_out) {
+  const unsigned lane = threadIdx.x & 31;
+  constexpr int NN = 32 * E;
+  uint64_t key[E];
+  uint32_t id[E];
+#pragma unroll
+  for (int e = 0; e < E; ++e) {
+    const int i = (int)lane * E + e;
+    id[e] = (uint32_t)i;
+    key[e] = i < n ? sort_key(recs[S[i]]) : ~0ull;
+  }
+#pragma unroll
+  for (int k = 2; k <= NN; k <<= 1) {
+#pragma unroll
+    for (int j = k >> 1; j > 0; j >>= 1) {
+      if (j < E) {
+#pragma unroll
+        for (int e = 0; e < E; ++e) {
+          const int p = e ^ j;
+          if (p > e) {
+            const bool up = ((((int)lane * E + e) & k) == 0);
+            if ((key[e] > key[p]) == up) {
+              const uint64_t tk = key[e]; key[e] = key[p]; key[p] = tk;
+              const uint32_t ti = id[e]; id[e] = id[p]; id[p] = ti;
+            }
+          }
+        }
+      } else {
+        const int lj = j / E;
+        const bool lower = (lane & lj) == 0;
+#pragma unroll
+        for (int e = 0; e < E; ++e) {
+          const uint64_t ok = __shfl_xor_sync(0xffffffffu, key[e], lj);
+          const uint32_t oi = __shfl_xor_sync(0xffffffffu, id[e], lj);
+          const bool up = ((((int)lane * E + e) & k) == 0);
+          const bool take = (lower == up) ? (ok < key[e]) : (ok > key[e]);
+          if (take) {
+            key[e] = ok;
+            id[e] = oi;
+          }
+        }
+      }
+    }
+  }
+#pragma unroll
+  for (int e = 0; e < E; ++e) {
+    const int i = (int)lane * E + e;
+    if (i < n) {
+      keys_out[i] = key[e];
+      idx_out[i] = (uint16_t)id[e];
+    }
+  }
+  __syncwarp();
+}
+
 // Common case of the per-pixel fold: up to 32 E records sorted by
 // (alpha_near, key) in registers (warp bitonic network over the blocked
 // layout i = lane E + e: in-register exchanges for distances < E, shuffles
@@ -626,20 +685,24 @@ __device__ __forceinline__ bool fold_pixel_reg(const rc_seg* __restrict__ recs, 
   return true;
 }
 
-__global__ void __launch_bounds__(FOLD_WARPS * 32) k_fold(const rc_seg* __restrict__ recs,
-                                                          const uint32_t* __restrict__ perm,
-                                                          const int64_t* __restrict__ off, int W, int H, int tw,
-                                                          int th, const int32_t* __restrict__ my_tiles,
-                                                          int tiles_x, int64_t npix_out, float bg0, float bg1,
-                                                          float bg2, float tau, float* __restrict__ rgba) {
+// Two passes: CAP = 512 over every pixel (registers, 16 warps per SM); the
+// few pixels with more records are deferred to a list that the CAP = 2048
+// pass (shared-memory bitonic, else selection order) works through.
+template <int CAP, bool FROM_LIST>
+__global__ void __launch_bounds__(FOLD_WARPS * 32, CAP <= 512 ? 4 : 1) k_fold(
+    const rc_seg* __restrict__ recs, const uint32_t* __restrict__ perm, const int64_t* __restrict__ off, int W,
+    int H, int tw, int th, const int32_t* __restrict__ my_tiles, int tiles_x, int64_t npix_out, float bg0, float bg1,
+    float bg2, float tau, float* __restrict__ rgba, int32_t* __restrict__ defer, int64_t* __restrict__ counters) {
   extern __shared__ unsigned char smem_raw[];
   const int warp = threadIdx.x >> 5;
   const unsigned lane = threadIdx.x & 31;
-  uint64_t* keys = reinterpret_cast<uint64_t*>(smem_raw) + (size_t)warp * FOLD_CAP;
-  uint16_t* idxs = reinterpret_cast<uint16_t*>(reinterpret_cast<uint64_t*>(smem_raw) + (size_t)FOLD_WARPS * FOLD_CAP) +
-                   (size_t)warp * FOLD_CAP;
+  uint64_t* keys = reinterpret_cast<uint64_t*>(smem_raw) + (size_t)warp * CAP;
+  uint16_t* idxs = reinterpret_cast<uint16_t*>(reinterpret_cast<uint64_t*>(smem_raw) + (size_t)FOLD_WARPS * CAP) +
+                   (size_t)warp * CAP;
   const int64_t tile_px = (int64_t)tw * th;
-  for (int64_t q = (int64_t)blockIdx.x * FOLD_WARPS + warp; q < npix_out; q += (int64_t)gridDim.x * FOLD_WARPS) {
+  const int64_t nq = FROM_LIST ? counters[CNT_DEFER] : npix_out;
+  for (int64_t qi = (int64_t)blockIdx.x * FOLD_WARPS + warp; qi < nq; qi += (int64_t)gridDim.x * FOLD_WARPS) {
+    const int64_t q = FROM_LIST ? (int64_t)defer[qi] : qi;
     int t = (int)(q / tile_px);
     int rem = (int)(q - (int64_t)t * tile_px);
     int tile = my_tiles[t];
@@ -649,6 +712,10 @@ __global__ void __launch_bounds__(FOLD_WARPS * 32) k_fold(const rc_seg* __restri
     int64_t base = off[pix];
     int n = (int)(off[pix + 1] - base);
     const uint32_t* S = perm + base;   // S[k] = index of the pixel's k-th record
+    if (!FROM_LIST && n > CAP && defer) {
+      if (lane == 0) defer[atomicAdd((unsigned long long*)&counters[CNT_DEFER], 1ull)] = (int32_t)q;
+      continue;
+    }
     Acc acc{1.0, 0.0, 0.0, 0.0};
     bool done = false;
     if (n <= 32) done = fold_pixel_reg<1>(recs, S, n, tau, acc);
@@ -658,7 +725,7 @@ __global__ void __launch_bounds__(FOLD_WARPS * 32) k_fold(const rc_seg* __restri
     else if (n <= 512) done = fold_pixel_reg<16>(recs, S, n, tau, acc);
     if (done) {
       // lane 0 holds the pixel's fold
-    } else if (n <= FOLD_CAP) {
+    } else if (n <= CAP) {
       int m = 1;
       while (m < n) m <<= 1;
       for (int k = lane; k < m; k += 32) {
@@ -788,30 +855,37 @@ __global__ void __launch_bounds__(FOLD_WARPS * 32) k_coarsen(const rc_seg* __res
       }
       continue;
     }
-    int m = 1;
-    while (m < n) m <<= 1;
-    for (int k = lane; k < m; k += 32) {
-      keys[k] = k < n ? sort_key(recs[S[k]]) : ~0ull;
-      idxs[k] = (uint16_t)k;
-    }
-    __syncwarp();
-    for (int size = 2; size <= m; size <<= 1) {
-      for (int stride = size >> 1; stride > 0; stride >>= 1) {
-        for (int k = lane; k < m; k += 32) {
-          const int p = k ^ stride;
-          if (p > k) {
-            const bool up = (k & size) == 0;
-            const uint64_t ka = keys[k], kb = keys[p];
-            if ((ka > kb) == up) {
-              keys[k] = kb;
-              keys[p] = ka;
-              const uint16_t t2 = idxs[k];
-              idxs[k] = idxs[p];
-              idxs[p] = t2;
+    if (n <= 32) sort_pixel_reg<1>(recs, S, n, keys, idxs);
+    else if (n <= 64) sort_pixel_reg<2>(recs, S, n, keys, idxs);
+    else if (n <= 128) sort_pixel_reg<4>(recs, S, n, keys, idxs);
+    else if (n <= 256) sort_pixel_reg<8>(recs, S, n, keys, idxs);
+    else if (n <= 512) sort_pixel_reg<16>(recs, S, n, keys, idxs);
+    else {
+      int m = 1;
+      while (m < n) m <<= 1;
+      for (int k = lane; k < m; k += 32) {
+        keys[k] = k < n ? sort_key(recs[S[k]]) : ~0ull;
+        idxs[k] = (uint16_t)k;
+      }
+      __syncwarp();
+      for (int size = 2; size <= m; size <<= 1) {
+        for (int stride = size >> 1; stride > 0; stride >>= 1) {
+          for (int k = lane; k < m; k += 32) {
+            const int p = k ^ stride;
+            if (p > k) {
+              const bool up = (k & size) == 0;
+              const uint64_t ka = keys[k], kb = keys[p];
+              if ((ka > kb) == up) {
+                keys[k] = kb;
+                keys[p] = ka;
+                const uint16_t t2 = idxs[k];
+                idxs[k] = idxs[p];
+                idxs[p] = t2;
+              }
             }
           }
+          __syncwarp();
         }
-        __syncwarp();
       }
     }
     auto anc = [&](int k) -> int64_t {
@@ -975,21 +1049,36 @@ cudaError_t launch_coarsen(const rc_seg* recs, const uint32_t* perm, const int64
   return cudaGetLastError();
 }
 
-cudaError_t launch_fold(const rc_seg* recs, const uint32_t* perm, const int64_t* off, int W, int H, int tw, int th,
-                        const int32_t* my_tiles, int tiles_x, int64_t npix_out, const float bg[3], float tau,
-                        float* rgba, int max_grid, cudaStream_t s) {
+template <int CAP, bool FROM_LIST>
+static cudaError_t fold_pass(const rc_seg* recs, const uint32_t* perm, const int64_t* off, int W, int H, int tw,
+                             int th, const int32_t* my_tiles, int tiles_x, int64_t npix_out, const float bg[3],
+                             float tau, float* rgba, int32_t* defer, int64_t* counters, int grid, cudaStream_t s) {
   static bool attr = false;
-  size_t smem = (size_t)FOLD_WARPS * FOLD_CAP * (sizeof(uint64_t) + sizeof(uint16_t));
+  const size_t smem = (size_t)FOLD_WARPS * CAP * (sizeof(uint64_t) + sizeof(uint16_t));
   if (!attr) {
-    cudaError_t e = cudaFuncSetAttribute(k_fold, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    cudaError_t e = cudaFuncSetAttribute(k_fold<CAP, FROM_LIST>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     if (e != cudaSuccess) return e;
     attr = true;
   }
-  int grid = (int)std::min<int64_t>((npix_out + FOLD_WARPS - 1) / FOLD_WARPS, (int64_t)max_grid);
-  k_fold<<<grid, FOLD_WARPS * 32, smem, s>>>(recs, perm, off, W, H, tw, th, my_tiles, tiles_x, npix_out, bg[0], bg[1],
-                                             bg[2], tau, rgba);
+  k_fold<CAP, FROM_LIST><<<grid, FOLD_WARPS * 32, smem, s>>>(recs, perm, off, W, H, tw, th, my_tiles, tiles_x,
+                                                             npix_out, bg[0], bg[1], bg[2], tau, rgba, defer,
+                                                             counters);
   ++g_launches;
   return cudaGetLastError();
+}
+
+cudaError_t launch_fold(const rc_seg* recs, const uint32_t* perm, const int64_t* off, int W, int H, int tw, int th,
+                        const int32_t* my_tiles, int tiles_x, int64_t npix_out, const float bg[3], float tau,
+                        float* rgba, int32_t* defer, int64_t* counters, int max_grid, cudaStream_t s) {
+  const int grid = (int)std::min<int64_t>((npix_out + FOLD_WARPS - 1) / FOLD_WARPS, (int64_t)max_grid);
+  cudaError_t e = cudaMemsetAsync(counters + CNT_DEFER, 0, sizeof(int64_t), s);
+  if (e != cudaSuccess) return e;
+  e = fold_pass<512, false>(recs, perm, off, W, H, tw, th, my_tiles, tiles_x, npix_out, bg, tau, rgba, defer,
+                            counters, grid, s);
+  if (e != cudaSuccess) return e;
+  // the deferred pixels (n > 512): a fixed grid reading the list length on the device
+  return fold_pass<FOLD_CAP, true>(recs, perm, off, W, H, tw, th, my_tiles, tiles_x, npix_out, bg, tau, rgba, defer,
+                                   counters, std::min(grid, 296), s);
 }
 
 }  // namespace rc

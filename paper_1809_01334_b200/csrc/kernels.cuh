@@ -39,6 +39,6 @@ cudaError_t launch_scatter(const rc_seg* segs, int64_t n, const int64_t* off, in
                            int grid, cudaStream_t s);
 cudaError_t launch_fold(const rc_seg* recs, const uint32_t* perm, const int64_t* off, int W, int H, int tw, int th,
                         const int32_t* my_tiles, int tiles_x, int64_t npix_out, const float bg[3], float tau,
-                        float* rgba, int max_grid, cudaStream_t s);
+                        float* rgba, int32_t* defer, int64_t* counters, int max_grid, cudaStream_t s);
 
 }  // namespace rc

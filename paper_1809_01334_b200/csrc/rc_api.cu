@@ -163,7 +163,7 @@ extern "C" rc_status rc_forest_destroy(rc_forest* f) {
                   f->d_vis, f->d_vis_rect, f->d_chunk_off, f->d_counters, f->d_trees, f->d_cam,
                   f->d_scan_tmp, f->d_chunk_elem, f->d_segs, f->d_hits_pp, f->d_pix_cnt, f->d_pix_off,
                   f->d_perm, f->d_send, f->d_items, f->d_leaf_node, f->d_ucnt, f->d_uend, f->d_units,
-                  f->d_scratch, f->d_segs2, f->d_uoff};
+                  f->d_scratch, f->d_segs2, f->d_uoff, f->d_defer};
   for (void* p : ptrs)
     if (p) cudaFree(p);
   for (int c = 0; c <= RC_NODE_LEVELS; ++c)
@@ -515,7 +515,17 @@ extern "C" rc_status rc_cast_segments(rc_forest* f, int32_t fold_levels, void* s
     std::swap(f->d_segs, f->d_segs2);
     std::swap(f->seg_cap, f->seg2_cap);
   }
-  int64_t est = curved ? (fold_levels > 0 ? cand / 8 : cand / 2 + cand / 8) : cand;
+  // first-frame estimate (C3-C5: fold-2 records are 1/7..1/4 of the candidates,
+  // raw segments ~1/2), capped by the free device memory so that a forest
+  // near the memory limit falls back to the exact regrowth instead of failing
+  int64_t est = curved ? (fold_levels > 0 ? cand / 4 : cand / 2 + cand / 8) : cand;
+  {
+    size_t free_b = 0, total_b = 0;
+    if (cudaMemGetInfo(&free_b, &total_b) == cudaSuccess) {
+      const int64_t cap = (int64_t)(free_b / 2 / sizeof(rc_seg)) + f->seg_cap;
+      est = std::min(est, cap);
+    }
+  }
   int64_t need = std::max<int64_t>(f->h_seg_total + f->h_seg_total / 8, est) + 4096;
   CU(grow(&f->d_segs, &f->seg_cap, need));
   for (int attempt = 0; attempt < 2; ++attempt) {
@@ -712,8 +722,9 @@ extern "C" rc_status rc_composite_tiles(rc_forest* f, const rc_tiling* t, const 
   if (npix_out > 0) {
     float bg[3] = {0, 0, 0};
     if (background) memcpy(bg, background, sizeof bg);
+    CU(grow(&f->d_defer, &f->defer_cap, npix_out));
     CU(launch_fold(src, f->d_perm, f->d_pix_off, W, H, tw, th, d_my_tiles, t->tiles_x, npix_out, bg, 1e-6f, d_rgba,
-                   sm_count() * 16, s));
+                   f->d_defer, f->d_counters, sm_count() * 16, s));
   }
   CU(cudaFreeAsync(d_my_tiles, s));
   return RC_OK;

@@ -143,6 +143,8 @@ struct rc_forest {
   void* d_scratch = nullptr;       // per-CTA item / segment / key scratch of the fused kernel
   size_t scratch_bytes = 0;
   // aggregation output (ping-pong with d_segs)
+  int32_t* d_defer = nullptr;      // composite: deferred pixels [w*h]
+  int64_t defer_cap = 0;
   rc_seg* d_segs2 = nullptr;
   int64_t seg2_cap = 0;
   // timing
@@ -169,6 +171,7 @@ enum {
   CNT_AGG_OUT = 75,    // records written by an aggregation pass
   CNT_TASKS = 76,      // curved path: (pixel, face) root-finding tasks
   CNT_FALLBACK = 77,   // ... of which needed the projected-patch (2D) method
+  CNT_DEFER = 78,      // composite: pixels deferred to the large-pixel pass
   CNT_TOTAL = 80
 };
 
