@@ -52,7 +52,7 @@ typedef struct {
   float q0;       /* q = q0 ((1+f~)/2, (1-f~)/2, 1/2)  RGB emission density      */
 } rc_transfer;
 
-enum { RC_HOST_COPY = 0, RC_DEVICE_COPY = 1 };
+enum { RC_HOST_COPY = 0, RC_DEVICE_COPY = 1, RC_HOST_COPY_TRUSTED = 2 };
 
 typedef struct {
   int32_t num_trees;          /* K >= 1                                                  */
@@ -65,7 +65,10 @@ typedef struct {
   const int32_t* leaf_tree;   /* [n]                                                     */
   const int8_t* leaf_level;   /* [n], 0..18                                              */
   const float* leaf_field;    /* [n][(P+1)^3], node order [k3][k2][k1]                    */
-  int32_t memory;             /* RC_HOST_COPY: leaf arrays are host pointers;
+  int32_t memory;             /* RC_HOST_COPY: leaf arrays are host pointers (checked);
+                                 RC_HOST_COPY_TRUSTED: host pointers, the caller
+                                 guarantees SFC order (no host-side check; pinned
+                                 memory gives asynchronous DMA);
                                  RC_DEVICE_COPY: leaf arrays are device pointers        */
   rc_transfer transfer;
 } rc_forest_desc;

@@ -615,6 +615,7 @@ struct WarpIsect {
   float ps[PS_N][32];       // P0[3], rf[3], xl0[3], dl[3], alpha0, rr
   float roots[4][4][32];    // [k][beta, xi0, xi1, xi2][lane]
   int nroots[32];
+  int pw[32];               // element (unit slot) of each lane's pixel
   int stats[2];             // face tasks, 2D-path tasks (flushed per unit)
   uint8_t task[MAXT];       // lane << 3 | face
 };
@@ -631,8 +632,8 @@ union PhaseSmem {              // per-phase scratch of phases 0-2
 struct UnitMeta {
   double org[RC_UNIT_LEAVES][3];        // element origins (fp64)
   Rect16 rect[RC_UNIT_LEAVES];          // pixel rectangles of the unit's elements
-  int32_t coff[RC_UNIT_LEAVES];         // first chunk of each element relative to the unit's first
-  uint8_t cmap[RC_UNIT_CHUNKS];         // unit chunk -> element
+  int32_t pa[RC_UNIT_LEAVES];           // first pair of each element in this unit (rect raster index)
+  int32_t pstart[RC_UNIT_LEAVES + 1];   // prefix of the elements' pair counts in the unit
 };
 struct Phase012 {
   float slot[RC_UNIT_LEAVES][SLOT_STRIDE];
@@ -774,19 +775,38 @@ __device__ __noinline__ void face_2d(WarpIsect& W, const float* __restrict__ sB,
 }
 
 // ---- phase 1: one chunk (32 candidate pixels of one element) --------------
-__device__ __forceinline__ void isect_chunk(WarpIsect& W, const float* __restrict__ sB, const double* __restrict__ org,
-                                            const CamConst& cc, const Rect16 r, int64_t cpos, int v,
-                                            float4* __restrict__ items, int* s_nitems,
+// The unit's candidate pairs are packed across its elements: pair g of the
+// unit belongs to the element w with pstart[w] <= g < pstart[w+1], pixel
+// pa[w] + g - pstart[w] of its rectangle (row-major).  A warp takes 32
+// consecutive pairs, so small elements (a few pixels each at C4/C5) do not
+// leave most lanes idle.
+__device__ __forceinline__ void isect_chunk(WarpIsect& W, CastSmem& S, const CamConst& cc, int nvis, int vfirst,
+                                            int g0, float4* __restrict__ items, int* s_nitems,
                                             int32_t* __restrict__ hits_pp, int& local_hits, int& face_fail) {
   const unsigned lane = threadIdx.x & 31;
   const float tol = cc.newton_tol;
   const int max_it = cc.newton_max;
+  const int g = g0 + (int)lane;
+  const bool active = g < S.meta.pstart[nvis];
+  int w = 0;
+  if (active) {
+    int lo = 0, hi = nvis;   // pstart[lo] <= g < pstart[hi]
+    while (hi - lo > 1) {
+      const int mid = (lo + hi) >> 1;
+      if (S.meta.pstart[mid] <= g) lo = mid;
+      else hi = mid;
+    }
+    w = lo;
+  }
+  const float* sB = S.u.p.slot[w];
+  const double* org = S.meta.org[w];
+  const Rect16 r = S.meta.rect[w];
+  const int v = vfirst + w;
   const float* af = sB + SLOT_AFF;
   const float dpv[3] = {af[12], af[13], af[14]};
-  const float dpm = fmaxf(dpv[0], fmaxf(dpv[1], dpv[2])), eta2 = 2.0f * af[15];
-  const int rw = r.i1 - r.i0 + 1, rh = r.j1 - r.j0 + 1;
-  const int p = (int)cpos * RC_CHUNK + (int)lane;
-  const bool active = p < rw * rh;
+  const float dpm = fmaxf(dpv[0], fmaxf(dpv[1], dpv[2]));
+  const int rw = r.i1 - r.i0 + 1;
+  const int p = S.meta.pa[w] + g - S.meta.pstart[w];
   const int i = r.i0 + p % rw, j = r.j0 + p / rw;
 
   // ---- 1a: ray of pixel (i,j), re-based near the element (fp64) -----------
@@ -849,6 +869,7 @@ __device__ __forceinline__ void isect_chunk(WarpIsect& W, const float* __restric
   W.ps[9][lane] = dl[0]; W.ps[10][lane] = dl[1]; W.ps[11][lane] = dl[2];
   W.ps[13][lane] = rr;
   W.nroots[lane] = 0;
+  W.pw[lane] = w;
   int ntask;
   {
     const int want = __popc(face_mask);
@@ -871,6 +892,9 @@ __device__ __forceinline__ void isect_chunk(WarpIsect& W, const float* __restric
     if (t < ntask) {
       const int code = W.task[t];
       const int pl = code >> 3, f = code & 7;
+      const float* sB = S.u.p.slot[W.pw[pl]];   // the task's element
+      const float* af = sB + SLOT_AFF;
+      const float eta2 = 2.0f * af[15];
       const float tP0[3] = {W.ps[0][pl], W.ps[1][pl], W.ps[2][pl]};
       const float trf[3] = {W.ps[3][pl], W.ps[4][pl], W.ps[5][pl]};
       const float txl0[3] = {W.ps[6][pl], W.ps[7][pl], W.ps[8][pl]};
@@ -1324,14 +1348,32 @@ __global__ void __launch_bounds__(CWARPS * 32, CAST_CTAS_PER_SM) k_cast_curved(C
     for (int w = tid; w < U.nvis; w += CWARPS * 32) {
       const Rect16 r = vrect[U.vfirst + w];
       S.meta.rect[w] = r;
+      // the element's candidate pairs inside this unit's chunk range
       const int64_t ca = chunk_off[U.vfirst + w], cz = chunk_off[U.vfirst + w + 1];
-      S.meta.coff[w] = (int32_t)(ca - U.chunk_begin);
-      const int k0 = (int)max((int64_t)0, ca - U.chunk_begin), k1 = (int)min((int64_t)U.nchunks, cz - U.chunk_begin);
-      for (int k = k0; k < k1; ++k) S.meta.cmap[k] = (uint8_t)w;
+      const int64_t k0 = max((int64_t)0, U.chunk_begin - ca);
+      const int64_t k1 = min(cz - ca, U.chunk_begin + U.nchunks - ca);
+      const int area = (r.i1 - r.i0 + 1) * (r.j1 - r.j0 + 1);
+      const int pa = (int)(k0 * RC_CHUNK), pb = (int)min((int64_t)area, k1 * RC_CHUNK);
+      S.meta.pa[w] = pa;
+      S.meta.pstart[w + 1] = max(0, pb - pa);   // counts; prefix-summed below
       atomicMax(&ctl.bb[0], -(int)r.i0);
       atomicMax(&ctl.bb[1], (int)r.i1);
       atomicMax(&ctl.bb[2], -(int)r.j0);
       atomicMax(&ctl.bb[3], (int)r.j1);
+    }
+    __syncthreads();
+    if (warp == 0) {   // prefix of the pair counts (<= 64 elements: two per lane)
+      const int a0 = 2 * (int)lane + 1, a1 = a0 + 1;
+      const int c0 = a0 <= U.nvis ? S.meta.pstart[a0] : 0, c1 = a1 <= U.nvis ? S.meta.pstart[a1] : 0;
+      int incl = c0 + c1;
+#pragma unroll
+      for (int off = 1; off < 32; off <<= 1) {
+        const int y = __shfl_up_sync(0xffffffffu, incl, off);
+        if ((int)lane >= off) incl += y;
+      }
+      if (a0 <= U.nvis) S.meta.pstart[a0] = incl - c1;
+      if (a1 <= U.nvis) S.meta.pstart[a1] = incl;
+      if (lane == 0) S.meta.pstart[0] = 0;
     }
     for (int w = tid; w < U.nvis; w += CWARPS * 32)
       prep_element_t(S.u.p.slot[w], S.meta.org[w], trees, L, vis[U.vfirst + w], NF, true);
@@ -1341,14 +1383,13 @@ __global__ void __launch_bounds__(CWARPS * 32, CAST_CTAS_PER_SM) k_cast_curved(C
       WarpIsect& W = S.u.p.ph.isect[warp];
       if (lane == 0) W.stats[0] = W.stats[1] = 0;
       __syncwarp();
+      const int nvchunks = (S.meta.pstart[U.nvis] + RC_CHUNK - 1) / RC_CHUNK;
       for (;;) {
         int k = 0;
         if (lane == 0) k = atomicAdd(&ctl.next_chunk, 1);
         k = __shfl_sync(0xffffffffu, k, 0);
-        if (k >= U.nchunks) break;
-        const int lv = S.meta.cmap[k];
-        isect_chunk(W, S.u.p.slot[lv], S.meta.org[lv], cc, S.meta.rect[lv], k - S.meta.coff[lv], U.vfirst + lv, items, &ctl.nitems,
-                    hits_pp, local_hits, face_fail);
+        if (k >= nvchunks) break;
+        isect_chunk(W, S, cc, U.nvis, U.vfirst, k * RC_CHUNK, items, &ctl.nitems, hits_pp, local_hits, face_fail);
       }
       if (lane == 0) {
         n_tasks += W.stats[0];

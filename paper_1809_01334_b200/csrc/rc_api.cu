@@ -74,7 +74,8 @@ extern "C" rc_status rc_forest_create(const rc_forest_desc* d, void* stream, rc_
   if (d->num_leaves < 1 || d->num_leaves > (int64_t)INT32_MAX) return fail(RC_ERR_INVALID_ARG, "num_leaves out of range");
   if (!d->tree_ctrl || !d->leaf_anchor || !d->leaf_tree || !d->leaf_level || !d->leaf_field)
     return fail(RC_ERR_INVALID_ARG, "rc_forest_create: null array");
-  if (d->memory != RC_HOST_COPY && d->memory != RC_DEVICE_COPY) return fail(RC_ERR_INVALID_ARG, "bad memory mode");
+  if (d->memory != RC_HOST_COPY && d->memory != RC_DEVICE_COPY && d->memory != RC_HOST_COPY_TRUSTED)
+    return fail(RC_ERR_INVALID_ARG, "bad memory mode");
   if (d->first_global_leaf < 0 || d->first_global_leaf + d->num_leaves > (int64_t)UINT32_MAX)
     return fail(RC_ERR_INVALID_ARG, "global leaf index must fit 32 bits");
   cudaStream_t s = (cudaStream_t)stream;
@@ -140,7 +141,7 @@ extern "C" rc_status rc_forest_create(const rc_forest_desc* d, void* stream, rc_
   f->scan_tmp_cap = std::max<int64_t>((int64_t)scan_tmp_size(n + 1) + 64, 256);
   ALLOC(f->d_scan_tmp, sizeof(int64_t) * f->scan_tmp_cap);
 #undef ALLOC
-  cudaMemcpyKind kind = d->memory == RC_HOST_COPY ? cudaMemcpyHostToDevice : cudaMemcpyDeviceToDevice;
+  cudaMemcpyKind kind = d->memory == RC_DEVICE_COPY ? cudaMemcpyDeviceToDevice : cudaMemcpyHostToDevice;
   if ((e = cudaMemcpyAsync(f->d_anchor, d->leaf_anchor, sizeof(int32_t) * 3 * n, kind, s)) ||
       (e = cudaMemcpyAsync(f->d_tree, d->leaf_tree, sizeof(int32_t) * n, kind, s)) ||
       (e = cudaMemcpyAsync(f->d_level, d->leaf_level, sizeof(int8_t) * n, kind, s)) ||

@@ -16,7 +16,7 @@ RC_OK = 0
 RC_ERR_CAPACITY = -6
 STATUS_NAMES = {0: "RC_OK", -1: "RC_ERR_INVALID_ARG", -2: "RC_ERR_NOT_SFC_SORTED", -3: "RC_ERR_OUT_OF_MEMORY",
                 -4: "RC_ERR_CUDA", -6: "RC_ERR_CAPACITY", -7: "RC_ERR_STATE", -8: "RC_ERR_NUMERIC"}
-RC_HOST_COPY, RC_DEVICE_COPY = 0, 1
+RC_HOST_COPY, RC_DEVICE_COPY, RC_HOST_COPY_TRUSTED = 0, 1, 2
 RC_PERSPECTIVE, RC_ORTHOGRAPHIC = 0, 1
 
 
@@ -155,7 +155,7 @@ class Forest:
     (device copy); they are copied by rc_forest_create."""
 
     def __init__(self, tree_ctrl, geom_degree, field_degree, leaf_anchor, leaf_tree, leaf_level, leaf_field,
-                 kappa0, inv_F, q0, first_global_leaf=0, stream=None):
+                 kappa0, inv_F, q0, first_global_leaf=0, stream=None, trusted=False):
         import torch
         L = lib()
         ctrl = np.ascontiguousarray(tree_ctrl if isinstance(tree_ctrl, np.ndarray) else tree_ctrl.cpu().numpy(),
@@ -173,7 +173,7 @@ class Forest:
             keep = [npy(leaf_anchor, np.int32), npy(leaf_tree, np.int32), npy(leaf_level, np.int8),
                     npy(leaf_field, np.float32)]
             ptrs = [k.ctypes.data for k in keep]
-            mem = RC_HOST_COPY
+            mem = RC_HOST_COPY_TRUSTED if trusted else RC_HOST_COPY
         n = int(keep[1].shape[0])
         self.n = n
         self.P = int(field_degree)
