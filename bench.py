@@ -188,6 +188,7 @@ def main():
     ap.add_argument("--config", type=int, default=int(os.environ.get("RC_BENCH_CONFIG", "4")))
     ap.add_argument("--impl", default="rc")
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-e2e", action="store_true", help="skip the end-to-end leg (A/B runs of build variants)")
     ap.add_argument("--fold", type=int, default=-1,
                     help="node level of the on-chip fold (row a6); default 2 for curved forests, 0 for affine")
     args = ap.parse_args()
@@ -324,7 +325,7 @@ def main():
     h2d = sum(a.nbytes for a in host)
     img_host = torch.empty((H, W, 4), dtype=torch.float32).pin_memory()
     e2e_times = []
-    n_e2e = 2 + (1 if args.config >= 4 else max(1, min(args.steps, 3)))
+    n_e2e = 0 if args.no_e2e else 2 + (1 if args.config >= 4 else max(1, min(args.steps, 3)))
     for it in range(n_e2e):
         torch.cuda.synchronize()
         if world > 1:
@@ -351,7 +352,7 @@ def main():
         f2.close()
         if it >= 2:
             e2e_times.append(dt)
-    e2e_s = sum(e2e_times) / len(e2e_times)
+    e2e_s = sum(e2e_times) / len(e2e_times) if e2e_times else float("nan")
     if world > 1:
         import torch.distributed as dist
         t = torch.tensor([e2e_s], dtype=torch.float64, device=dev)

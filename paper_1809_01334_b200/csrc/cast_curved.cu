@@ -647,7 +647,7 @@ struct FoldSmem {              // phase 3 (the slots are dead by then)
 };
 struct CastSmem {
   UnitMeta meta;
-  union {
+  union __align__(16) {   // the slots are read with 16-byte loads
     Phase012 p;
     FoldSmem fold;
     SortSmem sort;
