@@ -310,7 +310,7 @@ def main():
     # --- end to end through the public API with HOST buffers --------------
     seg_info = forest.segments()
     newton_failures = seg_info["newton_failures"]
-    fold_info = {"fold_levels": fold, "records": seg_info["count"], "raw_segments": seg_info["raw_segments"],
+    fold_info = {"face_failures": seg_info["face_failures"], "fold_levels": fold, "records": seg_info["count"], "raw_segments": seg_info["raw_segments"],
                  "record_level": seg_info["level"], "units": seg_info["units"],
                  "unfolded_units": seg_info["unfolded_units"], "face_tasks": seg_info["face_tasks"],
                  "fallback_tasks": seg_info["fallback_tasks"]}

@@ -16,9 +16,12 @@ if __name__ == "__main__":
     from paper_1809_01334_b200 import rc
     sc = bench.make_scene(a.config, torch.device("cuda"))
     f = rc.Forest.from_scene(sc, device_copy=True)
+    sc = bench.scene_to_host(sc)
+    torch.cuda.empty_cache()
     for _ in range(a.frames):
-        img, hits = f.render_frame(sc.camera, fold_levels=(0 if a.config <= 2 else 2))
+        img, hits = f.render_frame(sc.camera, fold_levels=(0 if a.config <= 2 else 2), cycles=sc.coarsen_cycles)
     torch.cuda.synchronize()
     s = f.segments()
-    print("hit_pairs", hits, "candidates", s["candidates"], "segments", s["count"], "newton_failures",
-          s["newton_failures"], "cast_ms", f.last_cast_ms(), "isect_ms", f.last_phase_ms(1), "integ_ms", f.last_phase_ms(2))
+    print("hit_pairs", hits, "candidates", s["candidates"], "records", s["count"], "raw", s["raw_segments"],
+          "newton_failures", s["newton_failures"], "face_failures", s["face_failures"], "fallback_tasks",
+          s["fallback_tasks"], "unfolded_units", s["unfolded_units"], "cast_ms", f.last_cast_ms())
