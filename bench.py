@@ -236,17 +236,32 @@ def main():
     flush = torch.empty(int(160e6) // 4, dtype=torch.float32, device=dev)   # > 126 MB L2
     stream = torch.cuda.current_stream()
 
+    phase_ev = {}
+
+    def mark(name):
+        if phase_ev is not None:
+            ev = torch.cuda.Event(enable_timing=True)
+            ev.record(stream)
+            phase_ev[name] = ev
+
     def frame():
+        mark("start")
         forest.camera_set(cam)
         forest.cull()
+        mark("cull")
         forest.cast_segments(fold)
+        mark("cast")
         if scene.coarsen_cycles:
             forest.aggregate(scene.coarsen_cycles)
+        mark("aggregate")
         if world == 1:
             forest.composite(out=img)
+            mark("composite")
             return None
         from paper_1809_01334_b200 import dist as rdist
-        return rdist.exchange_and_composite(forest, scene.tiles, world, rank)
+        out = rdist.exchange_and_composite(forest, scene.tiles, world, rank)
+        mark("composite")
+        return out
 
     for _ in range(max(3, args.warmup)):
         frame()
@@ -264,6 +279,7 @@ def main():
 
     # --- timed region: K frames, L2 flushed between frames (outside events) ---
     times, cast_ms, phase_ms = [], [], []
+    phase_acc = {}
     rc.launch_count(reset=True)
     with Clocks(local) as clk:
         for _ in range(args.steps):
@@ -279,6 +295,9 @@ def main():
             torch.cuda.synchronize()
             times.append(e0.elapsed_time(e1))
             cast_ms.append(forest.last_phase_ms(1))
+            names = ["start", "cull", "cast", "aggregate", "composite"]
+            for a, b in zip(names, names[1:]):
+                phase_acc[b] = phase_acc.get(b, 0.0) + phase_ev[a].elapsed_time(phase_ev[b]) / args.steps
     launches = rc.launch_count()
     ms_local = sum(times) / len(times)
     if world > 1:
@@ -372,7 +391,8 @@ def main():
                            "l2": "flushed between frames (160 MB write outside the events)",
                            "parallelism": f"sfc{world}"},
                 "roofline": roof, "gpu_launches": launches, "clocks": clk.summary(), "e2e": e2e,
-                "newton_failures": newton_failures, "segments": fold_info}
+                "newton_failures": newton_failures, "segments": fold_info,
+                "phase_ms": {k: round(v, 3) for k, v in phase_acc.items()}}
         if world == 1 and not args.no_cpu_baseline:
             stride = {1: 1, 2: 8, 3: 32, 4: 64, 5: 128, 45: 32}[args.config]
             sc_cpu = scene_to_host(scene)

@@ -30,7 +30,6 @@ namespace rc {
 namespace {
 
 constexpr int WARPS = 4;
-constexpr int MAX_ROOTS = 4;   // two segments per (element, ray); more is counted as a failure
 constexpr float FACE_TOL = 2e-6f;   // accepted face-parameter overshoot (~20x fp32 rounding of s)
 
 struct RootRec {
@@ -605,7 +604,8 @@ constexpr int CWARPS = CAST_WARPS;
 #ifndef CAST_CTAS_PER_SM
 #define CAST_CTAS_PER_SM 3   // resident CTAs per SM (launch bounds: 168 registers, ~60 KB shared memory)
 #endif
-constexpr int ITEM_CAP = 2 * RC_CHUNK * RC_UNIT_CHUNKS;   // <= two segments per pair
+constexpr int MAXR = 8;                                   // face roots per (element, pixel) pair
+constexpr int ITEM_CAP = (MAXR / 2) * RC_CHUNK * RC_UNIT_CHUNKS;   // <= MAXR/2 segments per pair
 constexpr int SORT_CAP = 2048;
 constexpr int MAXT = 6 * RC_CHUNK;                        // face tasks of one chunk
 constexpr float FOLD_TAU = 1e-6f;
@@ -613,7 +613,8 @@ constexpr int PS_N = 14;                                  // per-pixel ray state
 
 struct WarpIsect {
   float ps[PS_N][32];       // P0[3], rf[3], xl0[3], dl[3], alpha0, rr
-  float roots[4][4][32];    // [k][beta, xi0, xi1, xi2][lane]
+  float roots[MAXR][4][32]; // [k][beta, xi0, xi1, xi2][lane]
+  uint8_t rord[MAXR][32];   // per-lane sorted root order (1c)
   int nroots[32];
   int pw[32];               // element (unit slot) of each lane's pixel
   int stats[2];             // face tasks, 2D-path tasks (flushed per unit)
@@ -708,7 +709,7 @@ __device__ __forceinline__ unsigned long long fold_key(uint32_t pix, float an) {
 
 __device__ __forceinline__ void push_root(WarpIsect& W, int pl, float beta, const float xi[3], int& face_fail) {
   const int k = atomicAdd(&W.nroots[pl], 1);
-  if (k >= 4) {
+  if (k >= MAXR) {
     ++face_fail;
     return;
   }
@@ -976,40 +977,35 @@ __device__ __forceinline__ void isect_chunk(WarpIsect& W, CastSmem& S, const Cam
   }
 
   // ---- 1c: per pixel: sort roots, pair entry/exit, emit items ---------------
-  int nroots = min(W.nroots[lane], 4);
-  float rb0 = 3.4e38f, rb1 = 3.4e38f, rb2 = 3.4e38f, rb3 = 3.4e38f;
-  int ri0 = 0, ri1 = 1, ri2 = 2, ri3 = 3;
-  if (nroots > 0) rb0 = W.roots[0][0][lane];
-  if (nroots > 1) rb1 = W.roots[1][0][lane];
-  if (nroots > 2) rb2 = W.roots[2][0][lane];
-  if (nroots > 3) rb3 = W.roots[3][0][lane];
-#define CSWAP(a, b, ia, ib) \
-  if (b < a) {              \
-    float tf = a;           \
-    a = b;                  \
-    b = tf;                 \
-    int ti = ia;            \
-    ia = ib;                \
-    ib = ti;                \
+  int nr = min(W.nroots[lane], MAXR);
+  uint8_t* ord = &W.rord[0][lane];   // this lane's sorted root list (stride 32)
+  for (int t = 0; t < nr; ++t) {      // insertion sort by beta
+    const float bt = W.roots[t][0][lane];
+    int z = t;
+    while (z > 0 && W.roots[ord[(z - 1) * 32]][0][lane] > bt) {
+      ord[z * 32] = ord[(z - 1) * 32];
+      --z;
+    }
+    ord[z * 32] = (uint8_t)t;
   }
-  CSWAP(rb0, rb1, ri0, ri1) CSWAP(rb2, rb3, ri2, ri3) CSWAP(rb0, rb2, ri0, ri2) CSWAP(rb1, rb3, ri1, ri3)
-  CSWAP(rb1, rb2, ri1, ri2)
-#undef CSWAP
   {
     // dedupe roots found on two faces at a shared edge / vertex
     const float rn = sqrtf(rr);
     const float hw = fabsf(sB[GI(26)] - sB[0]) + fabsf(sB[GI(26) + 1] - sB[1]) + fabsf(sB[GI(26) + 2] - sB[2]);
     const float dtol = 4e-6f * hw / rn;
-    if (nroots > 1 && rb1 - rb0 < dtol) { rb1 = rb2; ri1 = ri2; rb2 = rb3; ri2 = ri3; rb3 = 3.4e38f; --nroots; }
-    if (nroots > 2 && rb2 - rb1 < dtol) { rb2 = rb3; ri2 = ri3; rb3 = 3.4e38f; --nroots; }
-    if (nroots > 3 && rb3 - rb2 < dtol) { rb3 = 3.4e38f; --nroots; }
-    nroots &= ~1;   // entry/exit pairs
+    int m = 0;
+    for (int t = 0; t < nr; ++t) {
+      const int o = ord[t * 32];
+      if (m > 0 && W.roots[o][0][lane] - W.roots[ord[(m - 1) * 32]][0][lane] < dtol) continue;
+      ord[m * 32] = (uint8_t)o;
+      ++m;
+    }
+    nr = m & ~1;   // entry/exit pairs
   }
   const float bmin = (float)(cc.amin - (double)alpha0), bmax = (float)(cc.amax - (double)alpha0);
-  bool s0ok = false, s1ok = false;
-  if (nroots >= 2) s0ok = fminf(rb1, bmax) > fmaxf(rb0, bmin);
-  if (nroots >= 4) s1ok = fminf(rb3, bmax) > fmaxf(rb2, bmin);
-  const int nseg = (int)s0ok + (int)s1ok;
+  int nseg = 0;
+  for (int z = 0; z < nr; z += 2)
+    nseg += fminf(W.roots[ord[(z + 1) * 32]][0][lane], bmax) > fmaxf(W.roots[ord[z * 32]][0][lane], bmin) ? 1 : 0;
   const uint32_t pix = (uint32_t)(j * cc.W + i);
   if (nseg > 0) {
     ++local_hits;
@@ -1017,11 +1013,10 @@ __device__ __forceinline__ void isect_chunk(WarpIsect& W, CastSmem& S, const Cam
   }
   int slot = warp_append_smem(s_nitems, nseg);
 #pragma unroll 1
-  for (int z = 0; z < 2; ++z) {
-    const bool ok = z == 0 ? s0ok : s1ok;
-    if (!ok) continue;
-    const float ba = z == 0 ? rb0 : rb2, bz = z == 0 ? rb1 : rb3;
-    const int ia = z == 0 ? ri0 : ri2, ib = z == 0 ? ri1 : ri3;
+  for (int z = 0; z < nr; z += 2) {
+    const int ia = ord[z * 32], ib = ord[(z + 1) * 32];
+    const float ba = W.roots[ia][0][lane], bz = W.roots[ib][0][lane];
+    if (!(fminf(bz, bmax) > fmaxf(ba, bmin))) continue;
     const float b0 = fmaxf(ba, bmin), b1 = fminf(bz, bmax);
     if (slot < ITEM_CAP) {
       float4* it = items + 4 * slot;

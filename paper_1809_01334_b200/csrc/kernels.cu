@@ -828,7 +828,8 @@ __global__ void __launch_bounds__(FOLD_WARPS * 32, CAP <= 512 ? 4 : 1) k_fold(
 __global__ void __launch_bounds__(FOLD_WARPS * 32) k_coarsen(const rc_seg* __restrict__ recs,
                                                              const uint32_t* __restrict__ perm,
                                                              const int64_t* __restrict__ off, int64_t npix,
-                                                             const int32_t* __restrict__ node_first, int64_t nnodes,
+                                                             const int32_t* __restrict__ node_first,
+                                                             const int32_t* __restrict__ leaf_node,
                                                              uint32_t key_base, float tau, rc_seg* __restrict__ out,
                                                              int64_t out_cap, int64_t* __restrict__ counters) {
   extern __shared__ unsigned char smem_raw[];
@@ -848,7 +849,7 @@ __global__ void __launch_bounds__(FOLD_WARPS * 32) k_coarsen(const rc_seg* __res
         const int64_t slot = warp_append(&counters[CNT_AGG_OUT], k < n ? 1 : 0);
         if (k < n) {
           rc_seg r = recs[S[k]];
-          r.key = key_base + (uint32_t)node_first[node_of(node_first, nnodes, (int32_t)(r.key - key_base))];
+          r.key = key_base + (uint32_t)node_first[leaf_node[r.key - key_base]];
           if (slot < out_cap) out[slot] = r;
           else atomicAdd((unsigned long long*)&counters[CNT_OVERFLOW], 1ull);
         }
@@ -889,7 +890,7 @@ __global__ void __launch_bounds__(FOLD_WARPS * 32) k_coarsen(const rc_seg* __res
       }
     }
     auto anc = [&](int k) -> int64_t {
-      return node_of(node_first, nnodes, (int32_t)(recs[S[idxs[k]]].key - key_base));
+      return (int64_t)leaf_node[recs[S[idxs[k]]].key - key_base];
     };
     auto is_head = [&](int k) -> bool {
       if (k == 0) return true;
@@ -1033,7 +1034,7 @@ cudaError_t launch_scatter(const rc_seg* segs, int64_t n, const int64_t* off, in
 }
 
 cudaError_t launch_coarsen(const rc_seg* recs, const uint32_t* perm, const int64_t* off, int64_t npix,
-                           const int32_t* node_first, int64_t nnodes, uint32_t key_base, float tau, rc_seg* out,
+                           const int32_t* node_first, const int32_t* leaf_node, uint32_t key_base, float tau, rc_seg* out,
                            int64_t out_cap, int64_t* counters, int max_grid, cudaStream_t s) {
   static bool attr = false;
   size_t smem = (size_t)FOLD_WARPS * FOLD_CAP * (sizeof(uint64_t) + sizeof(uint16_t));
@@ -1043,8 +1044,8 @@ cudaError_t launch_coarsen(const rc_seg* recs, const uint32_t* perm, const int64
     attr = true;
   }
   int grid = (int)std::min<int64_t>((npix + FOLD_WARPS - 1) / FOLD_WARPS, (int64_t)max_grid);
-  k_coarsen<<<grid, FOLD_WARPS * 32, smem, s>>>(recs, perm, off, npix, node_first, nnodes, key_base, tau, out, out_cap,
-                                                counters);
+  k_coarsen<<<grid, FOLD_WARPS * 32, smem, s>>>(recs, perm, off, npix, node_first, leaf_node, key_base, tau, out,
+                                                out_cap, counters);
   ++g_launches;
   return cudaGetLastError();
 }

@@ -29,7 +29,7 @@ cudaError_t launch_cast_curved(const CamConst& cc, const TreeConst* trees, DevLe
 size_t cast_curved_scratch_per_cta();
 int cast_curved_ctas_per_sm();
 cudaError_t launch_coarsen(const rc_seg* recs, const uint32_t* perm, const int64_t* off, int64_t npix,
-                           const int32_t* node_first, int64_t nnodes, uint32_t key_base, float tau, rc_seg* out,
+                           const int32_t* node_first, const int32_t* leaf_node, uint32_t key_base, float tau, rc_seg* out,
                            int64_t out_cap, int64_t* counters, int max_grid, cudaStream_t s);
 cudaError_t launch_pack(const rc_seg* segs, const int64_t* nseg_p, int W, int tw, int th, int tiles_x, int nranks,
                         int64_t* counts, const int64_t* dest_off, int64_t* cursor, rc_seg* out, int grid, bool count,

@@ -162,17 +162,24 @@ done:
   return e;
 }
 
-// f->d_leaf_node = node index of every leaf at level c (c >= 1).
-cudaError_t build_leaf_node(rc_forest* f, int c, cudaStream_t s) {
-  if (f->leaf_node_level == c && f->d_leaf_node) return cudaSuccess;
-  cudaError_t e = cudaSuccess;
-  if (!f->d_leaf_node) {
-    e = cudaMalloc(&f->d_leaf_node, sizeof(int32_t) * f->n);
+// Per-leaf node index at level c (c >= 1), cached for the last two levels
+// asked for (the fold level of the cast and the target level of rc_aggregate).
+cudaError_t build_leaf_node(rc_forest* f, int c, cudaStream_t s, const int32_t** out) {
+  for (int k = 0; k < 2; ++k)
+    if (f->leaf_node_lv[k] == c && f->d_leaf_nodes[k]) {
+      *out = f->d_leaf_nodes[k];
+      return cudaSuccess;
+    }
+  const int k = f->leaf_node_next;
+  f->leaf_node_next ^= 1;
+  if (!f->d_leaf_nodes[k]) {
+    cudaError_t e = cudaMalloc(&f->d_leaf_nodes[k], sizeof(int32_t) * f->n);
     if (e != cudaSuccess) return e;
   }
-  k_leaf_node<<<nb(f->n, 256), 256, 0, s>>>(f->d_node_first[c], f->n_nodes[c], f->n, f->d_leaf_node);
+  k_leaf_node<<<nb(f->n, 256), 256, 0, s>>>(f->d_node_first[c], f->n_nodes[c], f->n, f->d_leaf_nodes[k]);
   ++g_launches;
-  f->leaf_node_level = c;
+  f->leaf_node_lv[k] = c;
+  *out = f->d_leaf_nodes[k];
   return cudaGetLastError();
 }
 

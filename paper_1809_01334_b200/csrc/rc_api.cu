@@ -163,7 +163,7 @@ extern "C" rc_status rc_forest_destroy(rc_forest* f) {
   void* ptrs[] = {f->d_anchor, f->d_tree, f->d_level, f->d_field, f->d_flag, f->d_rect_all, f->d_scan,
                   f->d_vis, f->d_vis_rect, f->d_chunk_off, f->d_counters, f->d_trees, f->d_cam,
                   f->d_scan_tmp, f->d_chunk_elem, f->d_segs, f->d_hits_pp, f->d_pix_cnt, f->d_pix_off,
-                  f->d_perm, f->d_send, f->d_items, f->d_leaf_node, f->d_ucnt, f->d_uend, f->d_units,
+                  f->d_perm, f->d_send, f->d_items, f->d_leaf_nodes[0], f->d_leaf_nodes[1], f->d_ucnt, f->d_uend, f->d_units,
                   f->d_scratch, f->d_segs2, f->d_uoff, f->d_defer};
   for (void* p : ptrs)
     if (p) cudaFree(p);
@@ -487,8 +487,8 @@ extern "C" rc_status rc_cast_segments(rc_forest* f, int32_t fold_levels, void* s
   // <= RC_UNIT_CHUNKS chunks
   int64_t nunits = 0;
   if (curved && nvis > 0) {
-    if (fold_levels > 0) CU(build_leaf_node(f, fold_levels, s));
-    const int32_t* leaf_node = fold_levels > 0 ? f->d_leaf_node : nullptr;
+    const int32_t* leaf_node = nullptr;
+    if (fold_levels > 0) CU(build_leaf_node(f, fold_levels, s, &leaf_node));
     const int32_t* node_first = fold_levels > 0 ? f->d_node_first[fold_levels] : nullptr;
     if (!f->d_ucnt) {
       CU(cudaMalloc((void**)&f->d_ucnt, sizeof(int32_t) * (n + 1)));
@@ -766,6 +766,8 @@ static rc_status aggregate_to(rc_forest* f, int level, cudaStream_t s) {
   CU(scan_exclusive<int32_t>(f->d_pix_cnt, f->d_pix_off, npix, f->d_scan_tmp, s));
   CU(cudaMemsetAsync(f->d_pix_cnt, 0, sizeof(int32_t) * npix, s));
   if (nrec > 0) CU(launch_scatter(f->d_segs, nrec, f->d_pix_off, f->d_pix_cnt, f->d_perm, grid, s));
+  const int32_t* leaf_node = nullptr;   // node of every leaf at the target level
+  CU(build_leaf_node(f, level, s, &leaf_node));
   // output buffer: half the input first for one cycle, a quarter for several
   // (a cycle roughly halves the count), grown to the exact
   // count and the pass repeated if short
@@ -775,7 +777,7 @@ static rc_status aggregate_to(rc_forest* f, int level, cudaStream_t s) {
     CU(grow(&f->d_segs2, &f->seg2_cap, want));
     CU(cudaMemsetAsync(f->d_counters + CNT_AGG_OUT, 0, sizeof(int64_t), s));
     CU(cudaMemsetAsync(f->d_counters + CNT_OVERFLOW, 0, sizeof(int64_t), s));
-    CU(launch_coarsen(f->d_segs, f->d_perm, f->d_pix_off, npix, f->d_node_first[level], f->n_nodes[level],
+    CU(launch_coarsen(f->d_segs, f->d_perm, f->d_pix_off, npix, f->d_node_first[level], leaf_node,
                       (uint32_t)f->first_global, 1e-6f, f->d_segs2, f->seg2_cap, f->d_counters, sm_count() * 16, s));
     CU(cudaMemcpyAsync(&nout, f->d_counters + CNT_AGG_OUT, sizeof(int64_t), cudaMemcpyDeviceToHost, s));
     CU(cudaStreamSynchronize(s));

@@ -130,8 +130,9 @@ struct rc_forest {
   // coarsening hierarchy (nodes.cu): node tables of levels 1..RC_NODE_LEVELS
   int32_t* d_node_first[RC_NODE_LEVELS + 1] = {};
   int64_t n_nodes[RC_NODE_LEVELS + 1] = {};
-  int32_t* d_leaf_node = nullptr;  // per-leaf node index at level leaf_node_level
-  int leaf_node_level = -1;
+  int32_t* d_leaf_nodes[2] = {nullptr, nullptr};   // per-leaf node index at levels leaf_node_lv[]
+  int leaf_node_lv[2] = {-1, -1};
+  int leaf_node_next = 0;
   int rec_level = 0;               // node level of the current records (0 = leaves)
   // fold units of the curved kernel
   int32_t* d_ucnt = nullptr;       // [n+1] units per visible leaf (node starts only)
@@ -184,7 +185,7 @@ size_t scan_tmp_size(int64_t n);
 
 namespace rc {
 cudaError_t build_node_levels(rc_forest* f, cudaStream_t s);
-cudaError_t build_leaf_node(rc_forest* f, int c, cudaStream_t s);
+cudaError_t build_leaf_node(rc_forest* f, int c, cudaStream_t s, const int32_t** out);
 template <typename Tin>
 cudaError_t scan_exclusive(const Tin* in, int64_t* out, int64_t n, int64_t* tmp, cudaStream_t s);
 }  // namespace rc
