@@ -1190,21 +1190,28 @@ __device__ __forceinline__ bool touching(float an, float af_prev) {
   return fabsf(an - af_prev) <= FOLD_TAU * fmaxf(1.0f, fabsf(an));
 }
 
+// One window of rows [bj0, bj0 + rows) of the unit's pixel rectangle (the
+// caller covers the rectangle with windows of <= PIXCAP pixels); segments of
+// other rows are left to their window.
 __device__ void fold_bucket(CastSmem& S, CastCtl& ctl, const rc_seg* __restrict__ segs, int nitems, int bi0, int bj0,
-                            int bw, int area, int W, uint32_t ukey, rc_seg* __restrict__ out, int64_t out_cap,
+                            int bw, int rows, int W, uint32_t ukey, rc_seg* __restrict__ out, int64_t out_cap,
                             int64_t* __restrict__ counters) {
   const int tid = threadIdx.x;
   constexpr int NT = CWARPS * 32;
   FoldSmem& F = S.u.fold;
+  const int area = bw * rows;
+  __syncthreads();   // the previous window's readers are done
   for (int k = tid; k <= area; k += NT) F.off[k] = 0;
   __syncthreads();
   // one coalesced pass over the unit's segments: (alpha_near, alpha_far) to
-  // shared memory, bucket counts per pixel of the rectangle
+  // shared memory, bucket counts per pixel of the window
   for (int k = tid; k < nitems; k += NT) {
     const float4 h = reinterpret_cast<const float4*>(segs + k)[0];   // pixel, alpha_near, alpha_far, a
     const uint32_t pix = __float_as_uint(h.x);
-    const int pl = ((int)(pix / (uint32_t)W) - bj0) * bw + ((int)(pix % (uint32_t)W) - bi0);
+    const int row = (int)(pix / (uint32_t)W) - bj0;
     F.alpha[k] = make_float2(h.y, h.z);
+    if (row < 0 || row >= rows) continue;
+    const int pl = row * bw + ((int)(pix % (uint32_t)W) - bi0);
     F.rank[k] = (uint16_t)atomicAdd(&F.off[pl], 1);
   }
   __syncthreads();
@@ -1224,7 +1231,9 @@ __device__ void fold_bucket(CastSmem& S, CastCtl& ctl, const rc_seg* __restrict_
   __syncthreads();
   for (int k = tid; k < nitems; k += NT) {   // pixel-bucketed order
     const uint32_t pix = segs[k].pixel;
-    const int pl = ((int)(pix / (uint32_t)W) - bj0) * bw + ((int)(pix % (uint32_t)W) - bi0);
+    const int row = (int)(pix / (uint32_t)W) - bj0;
+    if (row < 0 || row >= rows) continue;
+    const int pl = row * bw + ((int)(pix % (uint32_t)W) - bi0);
     F.order[F.off[pl] + F.rank[k]] = (uint16_t)k;
   }
   __syncthreads();
@@ -1432,9 +1441,12 @@ __global__ void __launch_bounds__(CWARPS * 32, CAST_CTAS_PER_SM) k_cast_curved(C
     // ---- phase 3: fold -----------------------------------------------------------
     {
       const int bi0 = -ctl.bb[0], bi1 = ctl.bb[1], bj0 = -ctl.bb[2], bj1 = ctl.bb[3];
-      const int bw = bi1 - bi0 + 1, area = bw * (bj1 - bj0 + 1);
-      if (area <= PIXCAP && nitems <= FCAP) {
-        fold_bucket(S, ctl, segs, nitems, bi0, bj0, bw, area, cc.W, U.key, out, out_cap, counters);
+      const int bw = bi1 - bi0 + 1, bh = bj1 - bj0 + 1;
+      if (bw <= PIXCAP && nitems <= FCAP) {
+        const int rows = PIXCAP / bw;
+        for (int r0 = 0; r0 < bh; r0 += rows)
+          fold_bucket(S, ctl, segs, nitems, bi0, bj0 + r0, bw, min(rows, bh - r0), cc.W, U.key, out, out_cap,
+                      counters);
         continue;
       }
     }
