@@ -606,6 +606,77 @@ __device__ __forceinline__ void sort_pixel_reg(const rc_seg* __restrict__ recs, 
   __syncwarp();
 }
 
+// Aggregation fast path (n <= 32 E): register sort, then per sorted record
+// its index, alpha_near, alpha_far and target-level node cached in shared
+// memory, so that run detection needs no dependent global loads.
+struct RunCache {
+  uint32_t* rid;
+  float* an;
+  float* af;
+  int32_t* anc;
+};
+
+template <int E>
+__device__ __forceinline__ void sort_pixel_cache(const rc_seg* __restrict__ recs, const uint32_t* __restrict__ S,
+                                                 int n, const int32_t* __restrict__ leaf_node, uint32_t key_base,
+                                                 RunCache C) {
+  const unsigned lane = threadIdx.x & 31;
+  constexpr int NN = 32 * E;
+  uint64_t key[E];
+  uint32_t id[E];
+#pragma unroll
+  for (int e = 0; e < E; ++e) {
+    const int i = (int)lane * E + e;
+    id[e] = i < n ? S[i] : 0u;
+    key[e] = i < n ? sort_key(recs[id[e]]) : ~0ull;
+  }
+#pragma unroll
+  for (int k = 2; k <= NN; k <<= 1) {
+#pragma unroll
+    for (int j = k >> 1; j > 0; j >>= 1) {
+      if (j < E) {
+#pragma unroll
+        for (int e = 0; e < E; ++e) {
+          const int p = e ^ j;
+          if (p > e) {
+            const bool up = ((((int)lane * E + e) & k) == 0);
+            if ((key[e] > key[p]) == up) {
+              const uint64_t tk = key[e]; key[e] = key[p]; key[p] = tk;
+              const uint32_t ti = id[e]; id[e] = id[p]; id[p] = ti;
+            }
+          }
+        }
+      } else {
+        const int lj = j / E;
+        const bool lower = (lane & lj) == 0;
+#pragma unroll
+        for (int e = 0; e < E; ++e) {
+          const uint64_t ok = __shfl_xor_sync(0xffffffffu, key[e], lj);
+          const uint32_t oi = __shfl_xor_sync(0xffffffffu, id[e], lj);
+          const bool up = ((((int)lane * E + e) & k) == 0);
+          const bool take = (lower == up) ? (ok < key[e]) : (ok > key[e]);
+          if (take) {
+            key[e] = ok;
+            id[e] = oi;
+          }
+        }
+      }
+    }
+  }
+#pragma unroll
+  for (int e = 0; e < E; ++e) {
+    const int i = (int)lane * E + e;
+    if (i < n) {
+      const rc_seg& r = recs[id[e]];
+      C.rid[i] = id[e];
+      C.an[i] = r.alpha_near;
+      C.af[i] = r.alpha_far;
+      C.anc[i] = leaf_node[r.key - key_base];
+    }
+  }
+  __syncwarp();
+}
+
 // Common case of the per-pixel fold: up to 32 E records sorted by
 // (alpha_near, key) in registers (warp bitonic network over the blocked
 // layout i = lane E + e: in-register exchanges for distances < E, shuffles
@@ -856,12 +927,46 @@ __global__ void __launch_bounds__(FOLD_WARPS * 32) k_coarsen(const rc_seg* __res
       }
       continue;
     }
-    if (n <= 32) sort_pixel_reg<1>(recs, S, n, keys, idxs);
-    else if (n <= 64) sort_pixel_reg<2>(recs, S, n, keys, idxs);
-    else if (n <= 128) sort_pixel_reg<4>(recs, S, n, keys, idxs);
-    else if (n <= 256) sort_pixel_reg<8>(recs, S, n, keys, idxs);
-    else if (n <= 512) sort_pixel_reg<16>(recs, S, n, keys, idxs);
-    else {
+    if (n <= 512) {
+      RunCache C{reinterpret_cast<uint32_t*>(keys), reinterpret_cast<float*>(keys) + 512,
+                 reinterpret_cast<float*>(keys) + 1024, reinterpret_cast<int32_t*>(keys) + 1536};
+      if (n <= 32) sort_pixel_cache<1>(recs, S, n, leaf_node, key_base, C);
+      else if (n <= 64) sort_pixel_cache<2>(recs, S, n, leaf_node, key_base, C);
+      else if (n <= 128) sort_pixel_cache<4>(recs, S, n, leaf_node, key_base, C);
+      else if (n <= 256) sort_pixel_cache<8>(recs, S, n, leaf_node, key_base, C);
+      else sort_pixel_cache<16>(recs, S, n, leaf_node, key_base, C);
+      auto head = [&](int k) -> bool {
+        return k == 0 || fabsf(C.an[k] - C.af[k - 1]) > tau * fmaxf(1.0f, fabsf(C.an[k])) || C.anc[k] != C.anc[k - 1];
+      };
+      for (int k0 = 0; k0 < n; k0 += 32) {
+        const int k = k0 + (int)lane;
+        const bool h = k < n && head(k);
+        const int64_t slot = warp_append(&counters[CNT_AGG_OUT], h ? 1 : 0);
+        if (!h) continue;
+        double A = 1.0, B0 = 0.0, B1 = 0.0, B2 = 0.0;
+        int q = k;
+        do {
+          const rc_seg* sq = recs + C.rid[q];
+          const float a = sq->a;
+          const float4 hb = reinterpret_cast<const float4*>(sq)[1];   // b0, b1, b2, key
+          B0 = fma(A, (double)hb.x, B0);
+          B1 = fma(A, (double)hb.y, B1);
+          B2 = fma(A, (double)hb.z, B2);
+          A *= (double)a;
+          ++q;
+        } while (q < n && !head(q));
+        if (slot < out_cap) {
+          const float bb[3] = {(float)B0, (float)B1, (float)B2};
+          store_seg(out + slot, (uint32_t)pix, C.an[k], C.af[q - 1], (float)A, bb,
+                    key_base + (uint32_t)node_first[C.anc[k]]);
+        } else {
+          atomicAdd((unsigned long long*)&counters[CNT_OVERFLOW], 1ull);
+        }
+      }
+      __syncwarp();
+      continue;
+    }
+    {
       int m = 1;
       while (m < n) m <<= 1;
       for (int k = lane; k < m; k += 32) {
