@@ -466,6 +466,21 @@ __global__ void k_scatter(const rc_seg* __restrict__ segs, int64_t n, const int6
   }
 }
 
+// pixel-bucketed copy of the records (the composite then reads each pixel's
+// records contiguously instead of gathering them through a permutation)
+__global__ void k_scatter_rec(const rc_seg* __restrict__ segs, int64_t n, const int64_t* __restrict__ off,
+                              int32_t* __restrict__ cursor, rc_seg* __restrict__ out) {
+  for (int64_t s = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; s < n; s += (int64_t)gridDim.x * blockDim.x) {
+    const float4* src = reinterpret_cast<const float4*>(segs + s);
+    const float4 lo = __ldcs(src), hi = __ldcs(src + 1);
+    const uint32_t pix = __float_as_uint(lo.x);
+    const int k = atomicAdd(&cursor[pix], 1);
+    float4* dst = reinterpret_cast<float4*>(out + off[pix] + k);
+    dst[0] = lo;
+    dst[1] = hi;
+  }
+}
+
 struct Acc {
   double A, B0, B1, B2;
 };
@@ -547,26 +562,35 @@ struct Sweep {
 constexpr int FOLD_WARPS = 4;
 constexpr int FOLD_CAP = 2048;   // records per pixel sorted in shared memory
 
-// Warp register bitonic sort of a pixel's n <= 32 E records by (alpha_near,
-// key); the sorted keys and local indices (0..n-1) go to shared memory.
+// Warp bitonic sort of 32 E (key, id) pairs held in registers in the blocked
+// layout i = lane E + e, ascending.  Stage loops are not unrolled (code size:
+// the per-pixel kernels were instruction-cache bound); only the element loops
+// and the in-register distances (j < E) are static.
 template <int E>
-__device__ __forceinline__ void sort_pixel_reg(const rc_seg* __restrict__ recs, const uint32_t* __restrict__ S, int n,
-                                               uint64_t* __restrict__ keys_out, uint16_t* __restrict__ idx_out) {
+__device__ __forceinline__ void warp_sort_blocked(uint64_t (&key)[E], uint32_t (&id)[E]) {
   const unsigned lane = threadIdx.x & 31;
   constexpr int NN = 32 * E;
-  uint64_t key[E];
-  uint32_t id[E];
-#pragma unroll
-  for (int e = 0; e < E; ++e) {
-    const int i = (int)lane * E + e;
-    id[e] = (uint32_t)i;
-    key[e] = i < n ? sort_key(recs[S[i]]) : ~0ull;
-  }
-#pragma unroll
+#pragma unroll 1
   for (int k = 2; k <= NN; k <<= 1) {
+#pragma unroll 1
+    for (int j = k >> 1; j >= E; j >>= 1) {   // partners in other lanes
+      const int lj = j / E;
+      const bool lower = (lane & lj) == 0;
 #pragma unroll
-    for (int j = k >> 1; j > 0; j >>= 1) {
-      if (j < E) {
+      for (int e = 0; e < E; ++e) {
+        const uint64_t ok = __shfl_xor_sync(0xffffffffu, key[e], lj);
+        const uint32_t oi = __shfl_xor_sync(0xffffffffu, id[e], lj);
+        const bool up = ((((int)lane * E + e) & k) == 0);
+        const bool take = (lower == up) ? (ok < key[e]) : (ok > key[e]);
+        if (take) {
+          key[e] = ok;
+          id[e] = oi;
+        }
+      }
+    }
+#pragma unroll
+    for (int j = E >> 1; j > 0; j >>= 1) {     // partners in the same lane
+      if (j < k) {
 #pragma unroll
         for (int e = 0; e < E; ++e) {
           const int p = e ^ j;
@@ -578,33 +602,11 @@ __device__ __forceinline__ void sort_pixel_reg(const rc_seg* __restrict__ recs, 
             }
           }
         }
-      } else {
-        const int lj = j / E;
-        const bool lower = (lane & lj) == 0;
-#pragma unroll
-        for (int e = 0; e < E; ++e) {
-          const uint64_t ok = __shfl_xor_sync(0xffffffffu, key[e], lj);
-          const uint32_t oi = __shfl_xor_sync(0xffffffffu, id[e], lj);
-          const bool up = ((((int)lane * E + e) & k) == 0);
-          const bool take = (lower == up) ? (ok < key[e]) : (ok > key[e]);
-          if (take) {
-            key[e] = ok;
-            id[e] = oi;
-          }
-        }
       }
     }
   }
-#pragma unroll
-  for (int e = 0; e < E; ++e) {
-    const int i = (int)lane * E + e;
-    if (i < n) {
-      keys_out[i] = key[e];
-      idx_out[i] = (uint16_t)id[e];
-    }
-  }
-  __syncwarp();
 }
+
 
 // Aggregation fast path (n <= 32 E): register sort, then per sorted record
 // its index, alpha_near, alpha_far and target-level node cached in shared
@@ -630,39 +632,7 @@ __device__ __forceinline__ void sort_pixel_cache(const rc_seg* __restrict__ recs
     id[e] = i < n ? S[i] : 0u;
     key[e] = i < n ? sort_key(recs[id[e]]) : ~0ull;
   }
-#pragma unroll
-  for (int k = 2; k <= NN; k <<= 1) {
-#pragma unroll
-    for (int j = k >> 1; j > 0; j >>= 1) {
-      if (j < E) {
-#pragma unroll
-        for (int e = 0; e < E; ++e) {
-          const int p = e ^ j;
-          if (p > e) {
-            const bool up = ((((int)lane * E + e) & k) == 0);
-            if ((key[e] > key[p]) == up) {
-              const uint64_t tk = key[e]; key[e] = key[p]; key[p] = tk;
-              const uint32_t ti = id[e]; id[e] = id[p]; id[p] = ti;
-            }
-          }
-        }
-      } else {
-        const int lj = j / E;
-        const bool lower = (lane & lj) == 0;
-#pragma unroll
-        for (int e = 0; e < E; ++e) {
-          const uint64_t ok = __shfl_xor_sync(0xffffffffu, key[e], lj);
-          const uint32_t oi = __shfl_xor_sync(0xffffffffu, id[e], lj);
-          const bool up = ((((int)lane * E + e) & k) == 0);
-          const bool take = (lower == up) ? (ok < key[e]) : (ok > key[e]);
-          if (take) {
-            key[e] = ok;
-            id[e] = oi;
-          }
-        }
-      }
-    }
-  }
+  warp_sort_blocked<E>(key, id);
 #pragma unroll
   for (int e = 0; e < E; ++e) {
     const int i = (int)lane * E + e;
@@ -685,8 +655,8 @@ __device__ __forceinline__ void sort_pixel_cache(const rc_seg* __restrict__ recs
 // PAPER.md:395-427).  Returns false when consecutive records overlap beyond
 // tau (the caller then cuts and averages in the sequential sweep).
 template <int E>
-__device__ __forceinline__ bool fold_pixel_reg(const rc_seg* __restrict__ recs, const uint32_t* __restrict__ S, int n,
-                                               float tau, Acc& acc) {
+__device__ __forceinline__ bool fold_pixel_reg(const rc_seg* __restrict__ recs, const uint32_t* __restrict__ S,
+                                               int64_t base, int n, float tau, Acc& acc) {
   const unsigned lane = threadIdx.x & 31;
   constexpr int NN = 32 * E;
   uint64_t key[E];
@@ -694,42 +664,10 @@ __device__ __forceinline__ bool fold_pixel_reg(const rc_seg* __restrict__ recs, 
 #pragma unroll
   for (int e = 0; e < E; ++e) {
     const int i = (int)lane * E + e;
-    id[e] = i < n ? S[i] : 0xffffffffu;
+    id[e] = i < n ? (S ? S[i] : (uint32_t)(base + i)) : 0xffffffffu;   // S == nullptr: pixel-sorted copy
     key[e] = i < n ? sort_key(recs[id[e]]) : ~0ull;
   }
-#pragma unroll
-  for (int k = 2; k <= NN; k <<= 1) {
-#pragma unroll
-    for (int j = k >> 1; j > 0; j >>= 1) {
-      if (j < E) {
-#pragma unroll
-        for (int e = 0; e < E; ++e) {
-          const int p = e ^ j;
-          if (p > e) {
-            const bool up = ((((int)lane * E + e) & k) == 0);
-            if ((key[e] > key[p]) == up) {
-              const uint64_t tk = key[e]; key[e] = key[p]; key[p] = tk;
-              const uint32_t ti = id[e]; id[e] = id[p]; id[p] = ti;
-            }
-          }
-        }
-      } else {
-        const int lj = j / E;
-        const bool lower = (lane & lj) == 0;
-#pragma unroll
-        for (int e = 0; e < E; ++e) {
-          const uint64_t ok = __shfl_xor_sync(0xffffffffu, key[e], lj);
-          const uint32_t oi = __shfl_xor_sync(0xffffffffu, id[e], lj);
-          const bool up = ((((int)lane * E + e) & k) == 0);
-          const bool take = (lower == up) ? (ok < key[e]) : (ok > key[e]);
-          if (take) {
-            key[e] = ok;
-            id[e] = oi;
-          }
-        }
-      }
-    }
-  }
+  warp_sort_blocked<E>(key, id);
   // overlap check between consecutive records, then the lane's ordered fold
   float prev_af = __shfl_up_sync(0xffffffffu, id[E - 1] != 0xffffffffu ? recs[id[E - 1]].alpha_far : -3.4e38f, 1);
   if (lane == 0) prev_af = -3.4e38f;
@@ -782,25 +720,24 @@ __global__ void __launch_bounds__(FOLD_WARPS * 32, CAP <= 512 ? 4 : 1) k_fold(
     int64_t pix = (int64_t)j * W + i;
     int64_t base = off[pix];
     int n = (int)(off[pix + 1] - base);
-    const uint32_t* S = perm + base;   // S[k] = index of the pixel's k-th record
+    const uint32_t* S = perm ? perm + base : nullptr;   // S[k] = index of the pixel's k-th record
+#define RI(k) (S ? S[(k)] : (uint32_t)(base + (k)))
     if (!FROM_LIST && n > CAP && defer) {
       if (lane == 0) defer[atomicAdd((unsigned long long*)&counters[CNT_DEFER], 1ull)] = (int32_t)q;
       continue;
     }
     Acc acc{1.0, 0.0, 0.0, 0.0};
     bool done = false;
-    if (n <= 32) done = fold_pixel_reg<1>(recs, S, n, tau, acc);
-    else if (n <= 64) done = fold_pixel_reg<2>(recs, S, n, tau, acc);
-    else if (n <= 128) done = fold_pixel_reg<4>(recs, S, n, tau, acc);
-    else if (n <= 256) done = fold_pixel_reg<8>(recs, S, n, tau, acc);
-    else if (n <= 512) done = fold_pixel_reg<16>(recs, S, n, tau, acc);
+    if (n <= 64) done = fold_pixel_reg<2>(recs, S, base, n, tau, acc);
+    else if (n <= 256) done = fold_pixel_reg<8>(recs, S, base, n, tau, acc);
+    else if (n <= 512) done = fold_pixel_reg<16>(recs, S, base, n, tau, acc);
     if (done) {
       // lane 0 holds the pixel's fold
     } else if (n <= CAP) {
       int m = 1;
       while (m < n) m <<= 1;
       for (int k = lane; k < m; k += 32) {
-        keys[k] = k < n ? sort_key(recs[S[k]]) : ~0ull;
+        keys[k] = k < n ? sort_key(recs[RI(k)]) : ~0ull;
         idxs[k] = (uint16_t)k;
       }
       __syncwarp();
@@ -824,8 +761,8 @@ __global__ void __launch_bounds__(FOLD_WARPS * 32, CAP <= 512 ? 4 : 1) k_fold(
       // overlap detection between consecutive records
       bool ovl = false;
       for (int k = lane; k + 1 < n; k += 32) {
-        const rc_seg& x = recs[S[idxs[k]]];
-        const rc_seg& y = recs[S[idxs[k + 1]]];
+        const rc_seg& x = recs[RI(idxs[k])];
+        const rc_seg& y = recs[RI(idxs[k + 1])];
         float tol = tau * fmaxf(1.0f, fabsf(y.alpha_near));
         ovl |= (x.alpha_far - y.alpha_near) > tol;
       }
@@ -834,7 +771,7 @@ __global__ void __launch_bounds__(FOLD_WARPS * 32, CAP <= 512 ? 4 : 1) k_fold(
           Sweep sw;
           sw.acc = acc;
           sw.tau = tau;
-          for (int k = 0; k < n; ++k) sw.push(piece_of(recs[S[idxs[k]]]));
+          for (int k = 0; k < n; ++k) sw.push(piece_of(recs[RI(idxs[k])]));
           sw.finish();
           acc = sw.acc;
         }
@@ -843,7 +780,7 @@ __global__ void __launch_bounds__(FOLD_WARPS * 32, CAP <= 512 ? 4 : 1) k_fold(
         int per = (n + 31) / 32;
         int lo = min(n, (int)lane * per), hi = min(n, lo + per);
         for (int k = lo; k < hi; ++k) {
-          const rc_seg& s = recs[S[idxs[k]]];
+          const rc_seg& s = recs[RI(idxs[k])];
           acc_push(acc, s.a, s.b[0], s.b[1], s.b[2]);
         }
 #pragma unroll
@@ -867,13 +804,13 @@ __global__ void __launch_bounds__(FOLD_WARPS * 32, CAP <= 512 ? 4 : 1) k_fold(
         uint64_t best = ~0ull;
         int bi = -1;
         for (int k = 0; k < n; ++k) {
-          uint64_t kk = sort_key(recs[S[k]]);
+          uint64_t kk = sort_key(recs[RI(k)]);
           if ((first || kk > last) && kk < best) { best = kk; bi = k; }
         }
         if (bi < 0) break;
         first = false;
         last = best;
-        sw.push(piece_of(recs[S[bi]]));
+        sw.push(piece_of(recs[RI(bi)]));
       }
       sw.finish();
       acc = sw.acc;
@@ -884,6 +821,7 @@ __global__ void __launch_bounds__(FOLD_WARPS * 32, CAP <= 512 ? 4 : 1) k_fold(
       reinterpret_cast<float4*>(rgba)[q] = o;
     }
   }
+#undef RI
 }
 
 
@@ -930,9 +868,7 @@ __global__ void __launch_bounds__(FOLD_WARPS * 32) k_coarsen(const rc_seg* __res
     if (n <= 512) {
       RunCache C{reinterpret_cast<uint32_t*>(keys), reinterpret_cast<float*>(keys) + 512,
                  reinterpret_cast<float*>(keys) + 1024, reinterpret_cast<int32_t*>(keys) + 1536};
-      if (n <= 32) sort_pixel_cache<1>(recs, S, n, leaf_node, key_base, C);
-      else if (n <= 64) sort_pixel_cache<2>(recs, S, n, leaf_node, key_base, C);
-      else if (n <= 128) sort_pixel_cache<4>(recs, S, n, leaf_node, key_base, C);
+      if (n <= 64) sort_pixel_cache<2>(recs, S, n, leaf_node, key_base, C);
       else if (n <= 256) sort_pixel_cache<8>(recs, S, n, leaf_node, key_base, C);
       else sort_pixel_cache<16>(recs, S, n, leaf_node, key_base, C);
       auto head = [&](int k) -> bool {
@@ -1134,6 +1070,13 @@ cudaError_t launch_hist(const rc_seg* segs, int64_t n, int32_t* cnt, int grid, c
 cudaError_t launch_scatter(const rc_seg* segs, int64_t n, const int64_t* off, int32_t* cursor, uint32_t* out,
                            int grid, cudaStream_t s) {
   k_scatter<<<grid, 256, 0, s>>>(segs, n, off, cursor, out);
+  ++g_launches;
+  return cudaGetLastError();
+}
+
+cudaError_t launch_scatter_rec(const rc_seg* segs, int64_t n, const int64_t* off, int32_t* cursor, rc_seg* out,
+                               int grid, cudaStream_t s) {
+  k_scatter_rec<<<grid, 256, 0, s>>>(segs, n, off, cursor, out);
   ++g_launches;
   return cudaGetLastError();
 }

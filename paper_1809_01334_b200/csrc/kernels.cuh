@@ -37,6 +37,8 @@ cudaError_t launch_pack(const rc_seg* segs, const int64_t* nseg_p, int W, int tw
 cudaError_t launch_hist(const rc_seg* segs, int64_t n, int32_t* cnt, int grid, cudaStream_t s);
 cudaError_t launch_scatter(const rc_seg* segs, int64_t n, const int64_t* off, int32_t* cursor, uint32_t* out,
                            int grid, cudaStream_t s);
+cudaError_t launch_scatter_rec(const rc_seg* segs, int64_t n, const int64_t* off, int32_t* cursor, rc_seg* out,
+                               int grid, cudaStream_t s);
 cudaError_t launch_fold(const rc_seg* recs, const uint32_t* perm, const int64_t* off, int W, int H, int tw, int th,
                         const int32_t* my_tiles, int tiles_x, int64_t npix_out, const float bg[3], float tau,
                         float* rgba, int32_t* defer, int64_t* counters, int max_grid, cudaStream_t s);

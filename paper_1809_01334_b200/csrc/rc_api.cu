@@ -164,7 +164,7 @@ extern "C" rc_status rc_forest_destroy(rc_forest* f) {
                   f->d_vis, f->d_vis_rect, f->d_chunk_off, f->d_counters, f->d_trees, f->d_cam,
                   f->d_scan_tmp, f->d_chunk_elem, f->d_segs, f->d_hits_pp, f->d_pix_cnt, f->d_pix_off,
                   f->d_perm, f->d_send, f->d_items, f->d_leaf_nodes[0], f->d_leaf_nodes[1], f->d_ucnt, f->d_uend, f->d_units,
-                  f->d_scratch, f->d_segs2, f->d_uoff, f->d_defer};
+                  f->d_scratch, f->d_segs2, f->d_uoff, f->d_defer, f->d_sorted};
   for (void* p : ptrs)
     if (p) cudaFree(p);
   for (int c = 0; c <= RC_NODE_LEVELS; ++c)
@@ -705,7 +705,17 @@ extern "C" rc_status rc_composite_tiles(rc_forest* f, const rc_tiling* t, const 
   int64_t need_tmp = (int64_t)scan_tmp_size(npix + 1) + 128;
   if (need_tmp > f->scan_tmp_cap) CU(grow(&f->d_scan_tmp, &f->scan_tmp_cap, need_tmp));
   if (nsrc >= (int64_t)UINT32_MAX) return fail(RC_ERR_CAPACITY, "more than 2^32 records in one composite");
-  CU(grow(&f->d_perm, &f->perm_cap, std::max<int64_t>(nsrc, 1)));
+  // pixel-sorted copy of the records when memory allows (contiguous reads in
+  // the fold), else a permutation of record indices
+  bool copy = false;
+  {
+    size_t free_b = 0, total_b = 0;
+    const size_t have = f->sorted_cap >= nsrc ? (size_t)-1 : 0;
+    if (have || (cudaMemGetInfo(&free_b, &total_b) == cudaSuccess &&
+                 free_b > (size_t)nsrc * sizeof(rc_seg) + ((size_t)8 << 30)))
+      copy = grow(&f->d_sorted, &f->sorted_cap, std::max<int64_t>(nsrc, 1)) == cudaSuccess;
+  }
+  if (!copy) CU(grow(&f->d_perm, &f->perm_cap, std::max<int64_t>(nsrc, 1)));
   int32_t* d_my_tiles = nullptr;
   CU(cudaMallocAsync((void**)&d_my_tiles, sizeof(int32_t) * std::max<size_t>(mine.size(), 1), s));
   if (!mine.empty())
@@ -718,14 +728,15 @@ extern "C" rc_status rc_composite_tiles(rc_forest* f, const rc_tiling* t, const 
   CU(scan_exclusive<int32_t>(f->d_pix_cnt, f->d_pix_off, npix, f->d_scan_tmp, s));
   CU(cudaMemsetAsync(f->d_pix_cnt, 0, sizeof(int32_t) * npix, s));
   if (nsrc > 0) {
-    CU(launch_scatter(src, nsrc, f->d_pix_off, f->d_pix_cnt, f->d_perm, grid, s));
+    if (copy) CU(launch_scatter_rec(src, nsrc, f->d_pix_off, f->d_pix_cnt, f->d_sorted, grid, s));
+    else CU(launch_scatter(src, nsrc, f->d_pix_off, f->d_pix_cnt, f->d_perm, grid, s));
   }
   if (npix_out > 0) {
     float bg[3] = {0, 0, 0};
     if (background) memcpy(bg, background, sizeof bg);
     CU(grow(&f->d_defer, &f->defer_cap, npix_out));
-    CU(launch_fold(src, f->d_perm, f->d_pix_off, W, H, tw, th, d_my_tiles, t->tiles_x, npix_out, bg, 1e-6f, d_rgba,
-                   f->d_defer, f->d_counters, sm_count() * 16, s));
+    CU(launch_fold(copy ? f->d_sorted : src, copy ? nullptr : f->d_perm, f->d_pix_off, W, H, tw, th, d_my_tiles,
+                   t->tiles_x, npix_out, bg, 1e-6f, d_rgba, f->d_defer, f->d_counters, sm_count() * 16, s));
   }
   CU(cudaFreeAsync(d_my_tiles, s));
   return RC_OK;

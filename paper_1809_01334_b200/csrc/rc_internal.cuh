@@ -145,6 +145,8 @@ struct rc_forest {
   size_t scratch_bytes = 0;
   // aggregation output (ping-pong with d_segs)
   int32_t* d_defer = nullptr;      // composite: deferred pixels [w*h]
+  rc_seg* d_sorted = nullptr;      // composite: pixel-bucketed copy of the records
+  int64_t sorted_cap = 0;
   int64_t defer_cap = 0;
   rc_seg* d_segs2 = nullptr;
   int64_t seg2_cap = 0;
