@@ -599,7 +599,7 @@ __device__ __noinline__ void prep_element_t(float* __restrict__ sl, double* __re
 #endif
 constexpr int CWARPS = CAST_WARPS;
 #ifndef FAST_Q
-#define FAST_Q 0.5f         // contraction bound below which a face root takes the certified fast path
+#define FAST_Q 0.7f         // contraction bound below which a face root takes the certified fast path
 #endif
 #ifndef CAST_CTAS_PER_SM
 #define CAST_CTAS_PER_SM 3   // resident CTAs per SM (launch bounds: 168 registers, ~60 KB shared memory)

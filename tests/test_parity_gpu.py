@@ -223,6 +223,43 @@ def test_virtual_ranks_tile_exchange(which, nranks):
     assert np.abs(merged - full).max() < 1e-6
 
 
+@pytest.mark.parametrize("nranks", [2, 4])
+def test_virtual_ranks_fold_aggregate_aligned(nranks):
+    """The bench's multi-GPU configuration on one GPU: family-aligned SFC
+    ranges (dist.node_starts / aligned_ranges at fold + cycles levels), the
+    on-chip fold at level 2 and one aggregation cycle per rank, records packed
+    by tile owner and composited by the owner; equals the single-forest image
+    up to the fp32 records (lossless folds)."""
+    import torch
+    from paper_1809_01334_b200 import dist as rdist
+    from paper_1809_01334_b200 import rc
+    sc = sg.shell_uniform(3, 96, 16, gl_points=6)
+    tiles = (4, 4)
+    full = gpu_run(sc)["rgba"].reshape(96, 96, 4)
+    A, T, L = (torch.as_tensor(x) for x in (sc.leaf_anchor, sc.leaf_tree, sc.leaf_level))
+    allowed = rdist.node_starts(A, T, L, 3)
+    ranges = rdist.aligned_ranges(torch.ones(sc.num_leaves, dtype=torch.float64), nranks, allowed)
+    assert all(lo == 0 or bool(allowed[lo]) for lo, hi in ranges if lo < sc.num_leaves)
+    forests, packed = [], []
+    for lo, hi in ranges:
+        f = rc.Forest.from_scene(sc, first=lo, count=hi - lo)
+        f.camera_set(sc.camera)
+        f.cull()
+        f.cast_segments(2)
+        f.aggregate(1)
+        raw, counts = f.pack_tiles(*tiles, nranks, 0)
+        offs = np.r_[0, np.cumsum(counts)]
+        packed.append([raw[offs[d]:offs[d + 1]].clone() for d in range(nranks)])
+        forests.append(f)
+    out = {}
+    for d in range(nranks):
+        recv = torch.cat([packed[s][d] for s in range(nranks)])
+        img, mine = forests[d].composite_tiles(*tiles, nranks, d, recv=recv)
+        out[d] = (img, mine)
+    merged = rdist.assemble_image(out, *tiles, 96, 96).numpy()
+    assert np.abs(merged - full).max() < 1e-5
+
+
 def test_c4_full_size_sampled():
     """BASELINE C4 at full size on one GPU (100,663,296 curved hexes, 2048^2,
     N = 6) in the bench's launch configuration; 256 stratified pixels compared
