@@ -979,6 +979,11 @@ __device__ __forceinline__ void isect_chunk(WarpIsect& W, CastSmem& S, const Cam
   // ---- 1c: per pixel: sort roots, pair entry/exit, emit items ---------------
   int nr = min(W.nroots[lane], MAXR);
   uint8_t* ord = &W.rord[0][lane];   // this lane's sorted root list (stride 32)
+  if (nr == 2) {                      // common case: entry and exit
+    const bool sw = W.roots[1][0][lane] < W.roots[0][0][lane];
+    ord[0] = sw ? 1 : 0;
+    ord[32] = sw ? 0 : 1;
+  } else
   for (int t = 0; t < nr; ++t) {      // insertion sort by beta
     const float bt = W.roots[t][0][lane];
     int z = t;
