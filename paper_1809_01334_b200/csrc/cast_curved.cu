@@ -635,6 +635,7 @@ struct UnitMeta {
   Rect16 rect[RC_UNIT_LEAVES];          // pixel rectangles of the unit's elements
   int32_t pa[RC_UNIT_LEAVES];           // first pair of each element in this unit (rect raster index)
   int32_t pstart[RC_UNIT_LEAVES + 1];   // prefix of the elements' pair counts in the unit
+  uint8_t vmap[RC_UNIT_CHUNKS + 16];    // element of the first pair of each 32-pair chunk
 };
 struct Phase012 {
   float slot[RC_UNIT_LEAVES][SLOT_STRIDE];
@@ -790,14 +791,9 @@ __device__ __forceinline__ void isect_chunk(WarpIsect& W, CastSmem& S, const Cam
   const int g = g0 + (int)lane;
   const bool active = g < S.meta.pstart[nvis];
   int w = 0;
-  if (active) {
-    int lo = 0, hi = nvis;   // pstart[lo] <= g < pstart[hi]
-    while (hi - lo > 1) {
-      const int mid = (lo + hi) >> 1;
-      if (S.meta.pstart[mid] <= g) lo = mid;
-      else hi = mid;
-    }
-    w = lo;
+  if (active) {   // the chunk's first element, then forward (1-2 steps at C4)
+    w = S.meta.vmap[g0 / RC_CHUNK];
+    while (S.meta.pstart[w + 1] <= g) ++w;
   }
   const float* sB = S.u.p.slot[w];
   const double* org = S.meta.org[w];
@@ -1386,6 +1382,12 @@ __global__ void __launch_bounds__(CWARPS * 32, CAST_CTAS_PER_SM) k_cast_curved(C
     }
     for (int w = tid; w < U.nvis; w += CWARPS * 32)
       prep_element_t(S.u.p.slot[w], S.meta.org[w], trees, L, vis[U.vfirst + w], NF, true);
+    __syncthreads();
+    for (int w = tid; w < U.nvis; w += CWARPS * 32) {   // chunk -> first element map
+      const int a = S.meta.pstart[w], b = S.meta.pstart[w + 1];
+      if (b > a)
+        for (int c = (a + RC_CHUNK - 1) / RC_CHUNK; c * RC_CHUNK < b; ++c) S.meta.vmap[c] = (uint8_t)w;
+    }
     __syncthreads();
     // ---- phase 1: intersection -----------------------------------------------
     {
