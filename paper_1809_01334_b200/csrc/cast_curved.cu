@@ -598,6 +598,9 @@ __device__ __noinline__ void prep_element_t(float* __restrict__ sl, double* __re
 #define CAST_WARPS 4        // warps per CTA
 #endif
 constexpr int CWARPS = CAST_WARPS;
+#ifndef CAST_PREFETCH
+#define CAST_PREFETCH 0     // 1: software-pipelined item loads in phase 2 (A/B knob)
+#endif
 #ifndef FAST_Q
 #define FAST_Q 0.7f         // contraction bound below which a face root takes the certified fast path
 #endif
@@ -1414,6 +1417,14 @@ __global__ void __launch_bounds__(CWARPS * 32, CAST_CTAS_PER_SM) k_cast_curved(C
     // ---- phase 2: integration ---------------------------------------------------
     {
       const int ngroups = (nitems + 31) / 32;
+#if CAST_PREFETCH
+      // software pipeline: the next group's item is loaded before this one is integrated
+      float4 n0 = make_float4(0, 0, 0, 0), n1 = n0, n2 = n0, n3 = n0;
+      if (warp < ngroups && warp * 32 + (int)lane < nitems) {
+        const float4* it = items + 4 * (warp * 32 + (int)lane);
+        n0 = it[0]; n1 = it[1]; n2 = it[2]; n3 = it[3];
+      }
+#endif
       for (int g = warp; g < ngroups; g += CWARPS) {
         const int idx = g * 32 + (int)lane;
         const bool act = idx < nitems;
@@ -1421,9 +1432,23 @@ __global__ void __launch_bounds__(CWARPS * 32, CAST_CTAS_PER_SM) k_cast_curved(C
         uint32_t pix = 0;
         float an = 0.f, afar = 0.f;
         int v = 0;
+#if CAST_PREFETCH
+        const float4 c0 = n0, c1 = n1, c2 = n2, c3 = n3;
+        {
+          const int nidx = (g + CWARPS) * 32 + (int)lane;
+          if (nidx < nitems) {
+            const float4* it = items + 4 * nidx;
+            n0 = it[0]; n1 = it[1]; n2 = it[2]; n3 = it[3];
+          }
+        }
+#endif
         if (act) {
+#if CAST_PREFETCH
+          const float4 i0 = c0, i1 = c1, i2 = c2, i3 = c3;
+#else
           const float4* it = items + 4 * idx;
           const float4 i0 = it[0], i1 = it[1], i2 = it[2], i3 = it[3];
+#endif
           v = __float_as_int(i3.w);
           pix = __float_as_uint(i3.z);
           an = i3.x;
