@@ -1,24 +1,18 @@
-// cast_curved.cu -- segment kernel for curved (R=2) trees: rows a4 + a5 of
-// SURVEY.md §8(a) for C3-C5.
-//
-// Per warp work item = 32 candidate pixels of one element (pair generation,
-// kernels.cu).  Steps:
-//  1. element prep (27 lanes, fp64): Bernstein control points of X_E from the
-//     tree's by three sum-factorised blossom passes through shared memory
-//     (restriction of the tensor-product map to the element's subcube,
-//     PAPER.md:104-107); stored fp32 relative to the local origin
-//     C_E = B_(1,1,1) (exactly representable reference point).
-//  2. per lane: ray of pixel (i,j) re-based in fp64 near C_E.
-//  3. per face (App. A.1): project the face's Bernstein
-//     points on d1,d2 perpendicular to r (Eq. intersectiontwod); reject when
-//     the projected hull excludes the ray; else prove at most one root with
-//     ||A J(s) - I|| < 1 (A = J(centre)^-1, J's Bernstein derivative
-//     coefficients bound J(s) on the patch) and run Newton; patches that
-//     fail the test are subdivided (rare: grazing rays).
-//  4. sort roots by alpha, pair entry/exit, and per segment
-//     integrate with the N-point GL rule; the field at each node needs
-//     xi(x): simplified Newton on X_E(xi) = x warm-started on the straight
-//     line between entry and exit xi (tol = camera newton_tol).
+// cast_curved.cu -- the segment kernel for curved (R = 2) trees: rows a4
+// (intersection), a5 (GL segment integration) and a6 (on-chip fold) of
+// SURVEY.md §8(a), for C3-C5, fused into one persistent kernel
+// (k_cast_curved<P,N>, described at its definition below and in DESIGN.md
+// §6.1).  Building blocks, in file order:
+//  - Bernstein evaluation of the element map X_E (relative to the element
+//    origin) and of a face patch; the padded shared-memory slot layout;
+//  - the projected-patch root finding of App. A.1:
+//    Bezier hull rejection, injectivity bound ||A J(s) - I|| < 1, chord /
+//    Newton iteration, Bezier subdivision (rare: grazing rays);
+//  - element preparation (fp64 restriction of the tree's Bernstein points to
+//    the element's subcube; the affine model and its
+//    nonlinearity bounds);
+//  - phase 1 (per 32 packed candidate pairs), phase 2 (per 32 items),
+//    phase 3 (bucket fold per unit) and the kernel.
 #include <cuda_runtime.h>
 #include <math.h>
 
