@@ -222,6 +222,12 @@ rc_status rc_render_frame(rc_forest* f, const rc_camera* cam, int32_t fold_level
                           const float background[3], float* d_rgba, int64_t capacity_floats, int64_t* hit_pairs,
                           void* stream);
 
+/* Device memory: librc keeps the blocks of destroyed forests and regrown
+ * buffers in a caching pool (reused by later allocations of similar size;
+ * released automatically when an allocation would otherwise fail).
+ * rc_pool_trim returns every cached block to the driver. */
+rc_status rc_pool_trim(void);
+
 /* Instrumentation: kernel launches issued by the library since the last
  * reset, and the device time of the segment kernel(s) of the last
  * rc_cast_segments measured with CUDA events on the caller's stream. */

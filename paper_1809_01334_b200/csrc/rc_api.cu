@@ -47,10 +47,10 @@ extern "C" int64_t rc_launch_count(int32_t reset) {
 template <typename T>
 static cudaError_t grow(T** p, int64_t* cap, int64_t need) {
   if (need <= *cap && *p) return cudaSuccess;
-  if (*p) cudaFree(*p);
+  if (*p) dfree(*p);
   *p = nullptr;
   int64_t c = std::max<int64_t>(need + std::min<int64_t>(need / 8, (int64_t)1 << 24), 64);   // bounded slack
-  cudaError_t e = cudaMalloc((void**)p, sizeof(T) * (size_t)c);
+  cudaError_t e = dmalloc((void**)p, sizeof(T) * (size_t)c);
   if (e == cudaSuccess) *cap = c;
   else *cap = 0;
   return e;
@@ -123,7 +123,7 @@ extern "C" rc_status rc_forest_create(const rc_forest_desc* d, void* stream, rc_
     return r;
   };
 #define ALLOC(ptr, bytes)                                        \
-  if ((e = cudaMalloc((void**)&(ptr), (bytes))) != cudaSuccess) \
+  if ((e = dmalloc((void**)&(ptr), (bytes))) != cudaSuccess) \
     return cleanup(RC_ERR_OUT_OF_MEMORY, "cudaMalloc " #ptr);
   ALLOC(f->d_anchor, sizeof(int32_t) * 3 * n);
   ALLOC(f->d_tree, sizeof(int32_t) * n);
@@ -160,15 +160,16 @@ extern "C" rc_status rc_forest_create(const rc_forest_desc* d, void* stream, rc_
 
 extern "C" rc_status rc_forest_destroy(rc_forest* f) {
   if (!f) return RC_OK;
+  cudaDeviceSynchronize();   // blocks go back to the caching pool: no kernel may still use them
   void* ptrs[] = {f->d_anchor, f->d_tree, f->d_level, f->d_field, f->d_flag, f->d_rect_all, f->d_scan,
                   f->d_vis, f->d_vis_rect, f->d_chunk_off, f->d_counters, f->d_trees, f->d_cam,
                   f->d_scan_tmp, f->d_chunk_elem, f->d_segs, f->d_hits_pp, f->d_pix_cnt, f->d_pix_off,
                   f->d_perm, f->d_send, f->d_items, f->d_leaf_nodes[0], f->d_leaf_nodes[1], f->d_ucnt, f->d_uend, f->d_units,
                   f->d_scratch, f->d_segs2, f->d_uoff, f->d_defer, f->d_sorted};
   for (void* p : ptrs)
-    if (p) cudaFree(p);
+    if (p) dfree(p);
   for (int c = 0; c <= RC_NODE_LEVELS; ++c)
-    if (f->d_node_first[c]) cudaFree(f->d_node_first[c]);
+    if (f->d_node_first[c]) dfree(f->d_node_first[c]);
   if (f->ev0) cudaEventDestroy(f->ev0);
   if (f->ev1) cudaEventDestroy(f->ev1);
   for (int k = 0; k < 4; ++k)
@@ -491,9 +492,9 @@ extern "C" rc_status rc_cast_segments(rc_forest* f, int32_t fold_levels, void* s
     if (fold_levels > 0) CU(build_leaf_node(f, fold_levels, s, &leaf_node));
     const int32_t* node_first = fold_levels > 0 ? f->d_node_first[fold_levels] : nullptr;
     if (!f->d_ucnt) {
-      CU(cudaMalloc((void**)&f->d_ucnt, sizeof(int32_t) * (n + 1)));
-      CU(cudaMalloc((void**)&f->d_uoff, sizeof(int64_t) * (n + 1)));
-      CU(cudaMalloc((void**)&f->d_uend, sizeof(int32_t) * (n + 1)));
+      CU(dmalloc((void**)&f->d_ucnt, sizeof(int32_t) * (n + 1)));
+      CU(dmalloc((void**)&f->d_uoff, sizeof(int64_t) * (n + 1)));
+      CU(dmalloc((void**)&f->d_uend, sizeof(int32_t) * (n + 1)));
     }
     CU(launch_units(f->d_vis, f->d_scan + n, nvis, leaf_node, node_first, f->d_chunk_off, f->d_ucnt, f->d_uoff,
                     f->d_uend, f->d_scan_tmp, key_base, nullptr, false, s));
@@ -507,7 +508,7 @@ extern "C" rc_status rc_cast_segments(rc_forest* f, int32_t fold_levels, void* s
   const int grid_curved = sm_count() * cast_curved_ctas_per_sm();
   if (curved && !f->d_scratch) {
     f->scratch_bytes = cast_curved_scratch_per_cta() * (size_t)grid_curved;
-    CU(cudaMalloc(&f->d_scratch, f->scratch_bytes));
+    CU(dmalloc((void**)&f->d_scratch, f->scratch_bytes));
   }
   // record capacity: the previous frame's count, else an estimate; a too
   // small buffer is grown to the exact count and the cast repeated
@@ -694,12 +695,12 @@ extern "C" rc_status rc_composite_tiles(rc_forest* f, const rc_tiling* t, const 
   const int64_t npix = (int64_t)W * H;
   // (re)allocate per-pixel arrays sized to the image
   if (!f->d_pix_cnt || f->pix_cnt_cap < npix) {
-    if (f->d_pix_cnt) cudaFree(f->d_pix_cnt);
-    if (f->d_pix_off) cudaFree(f->d_pix_off);
+    if (f->d_pix_cnt) dfree(f->d_pix_cnt);
+    if (f->d_pix_off) dfree(f->d_pix_off);
     f->d_pix_cnt = nullptr;
     f->d_pix_off = nullptr;
-    CU(cudaMalloc((void**)&f->d_pix_cnt, sizeof(int32_t) * npix));
-    CU(cudaMalloc((void**)&f->d_pix_off, sizeof(int64_t) * (npix + 1)));
+    CU(dmalloc((void**)&f->d_pix_cnt, sizeof(int32_t) * npix));
+    CU(dmalloc((void**)&f->d_pix_off, sizeof(int64_t) * (npix + 1)));
     f->pix_cnt_cap = npix;
   }
   int64_t need_tmp = (int64_t)scan_tmp_size(npix + 1) + 128;
@@ -760,12 +761,12 @@ static rc_status aggregate_to(rc_forest* f, int level, cudaStream_t s) {
   const int64_t npix = (int64_t)f->cc.W * f->cc.H;
   if (nrec >= (int64_t)UINT32_MAX) return fail(RC_ERR_CAPACITY, "more than 2^32 records in one aggregation");
   if (!f->d_pix_cnt || f->pix_cnt_cap < npix) {
-    if (f->d_pix_cnt) cudaFree(f->d_pix_cnt);
-    if (f->d_pix_off) cudaFree(f->d_pix_off);
+    if (f->d_pix_cnt) dfree(f->d_pix_cnt);
+    if (f->d_pix_off) dfree(f->d_pix_off);
     f->d_pix_cnt = nullptr;
     f->d_pix_off = nullptr;
-    CU(cudaMalloc((void**)&f->d_pix_cnt, sizeof(int32_t) * npix));
-    CU(cudaMalloc((void**)&f->d_pix_off, sizeof(int64_t) * (npix + 1)));
+    CU(dmalloc((void**)&f->d_pix_cnt, sizeof(int32_t) * npix));
+    CU(dmalloc((void**)&f->d_pix_off, sizeof(int64_t) * (npix + 1)));
     f->pix_cnt_cap = npix;
   }
   int64_t need_tmp = (int64_t)scan_tmp_size(npix + 1) + 128;

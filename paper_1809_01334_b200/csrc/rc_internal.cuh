@@ -187,6 +187,9 @@ size_t scan_tmp_size(int64_t n);
 
 namespace rc {
 cudaError_t build_node_levels(rc_forest* f, cudaStream_t s);
+cudaError_t dmalloc(void** p, size_t bytes);   // caching pool (pool.cu)
+void dfree(void* p);
+void dtrim();
 cudaError_t build_leaf_node(rc_forest* f, int c, cudaStream_t s, const int32_t** out);
 template <typename Tin>
 cudaError_t scan_exclusive(const Tin* in, int64_t* out, int64_t n, int64_t* tmp, cudaStream_t s);

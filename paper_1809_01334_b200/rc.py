@@ -61,7 +61,7 @@ SEG_BYTES = 32
 EXPORTS = ["rc_last_error", "rc_version", "rc_forest_create", "rc_forest_destroy", "rc_camera_set", "rc_cull",
            "rc_cull_result", "rc_cast_segments", "rc_segments_get", "rc_aggregate", "rc_pack_tiles",
            "rc_composite_tiles", "rc_composite", "rc_render_frame", "rc_launch_count", "rc_last_cast_ms",
-           "rc_last_phase_ms", "rc_node_table"]
+           "rc_last_phase_ms", "rc_node_table", "rc_pool_trim"]
 
 _lib = None
 
@@ -312,6 +312,11 @@ class Forest:
 
     def last_phase_ms(self, phase):
         return float(lib().rc_last_phase_ms(self.h, int(phase)))
+
+
+def pool_trim() -> None:
+    """Return librc's cached device blocks to the driver."""
+    _check(lib().rc_pool_trim())
 
 
 def launch_count(reset=False) -> int:

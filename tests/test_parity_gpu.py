@@ -264,6 +264,8 @@ def test_c4_full_size_sampled():
     """BASELINE C4 at full size on one GPU (100,663,296 curved hexes, 2048^2,
     N = 6) in the bench's launch configuration; 256 stratified pixels compared
     one by one with the oracle (which culls all 1e8 leaves in fp64)."""
+    from paper_1809_01334_b200 import rc
+    rc.pool_trim()
     sc = sg.config4(device="cuda")
     g = gpu_run(sc, device_copy=True, fold=2, keep_raw=False)     # bench.py's launch configuration
     assert g["newton_failures"] == 0
@@ -285,6 +287,8 @@ def test_c5_full_size_sampled():
     (which culls every leaf in fp64)."""
     import torch
     import bench
+    from paper_1809_01334_b200 import rc
+    rc.pool_trim()   # earlier tests' cached blocks back to the driver (the generator needs them)
     sc = bench.scene_to_host(sg.config5(device="cuda"))   # generated on the GPU, kept on the host
     torch.cuda.empty_cache()
     g = gpu_run(sc, fold=2, cycles=3, keep_raw=False)
