@@ -592,6 +592,9 @@ __device__ __noinline__ void prep_element_t(float* __restrict__ sl, double* __re
 #define CAST_WARPS 4        // warps per CTA
 #endif
 constexpr int CWARPS = CAST_WARPS;
+#ifndef CAST_COMPACT
+#define CAST_COMPACT 1      // 1: fp32 prefilter first, the exact path only for candidates it keeps
+#endif
 #ifndef CAST_PREFETCH
 #define CAST_PREFETCH 0     // 1: software-pipelined item loads in phase 2 (A/B knob)
 #endif
@@ -614,6 +617,7 @@ struct WarpIsect {
   uint8_t rord[MAXR][32];   // per-lane sorted root order (1c)
   int nroots[32];
   int pw[32];               // element (unit slot) of each lane's pixel
+  int queue[64];            // packed pairs kept by the prefilter (CAST_COMPACT)
   int stats[2];             // face tasks, 2D-path tasks (flushed per unit)
   uint8_t task[MAXT];       // lane << 3 | face
 };
@@ -633,6 +637,8 @@ struct UnitMeta {
   int32_t pa[RC_UNIT_LEAVES];           // first pair of each element in this unit (rect raster index)
   int32_t pstart[RC_UNIT_LEAVES + 1];   // prefix of the elements' pair counts in the unit
   uint8_t vmap[RC_UNIT_CHUNKS + 16];    // element of the first pair of each 32-pair chunk
+  float Dc[RC_UNIT_LEAVES][3];          // (float)(origin - O0): prefilter ray re-basing
+  float pm[RC_UNIT_LEAVES];             // prefilter margin in xi~ units
 };
 struct Phase012 {
   float slot[RC_UNIT_LEAVES][SLOT_STRIDE];
@@ -779,19 +785,59 @@ __device__ __noinline__ void face_2d(WarpIsect& W, const float* __restrict__ sB,
 // pa[w] + g - pstart[w] of its rectangle (row-major).  A warp takes 32
 // consecutive pairs, so small elements (a few pixels each at C4/C5) do not
 // leave most lanes idle.
+__device__ __forceinline__ int pair_element(const CastSmem& S, int g) {
+  int w = S.meta.vmap[g / RC_CHUNK];   // the chunk's first element, then forward (1-2 steps at C4)
+  while (S.meta.pstart[w + 1] <= g) ++w;
+  return w;
+}
+
+// Conservative fp32 version of 1a's prefilter (CAST_COMPACT): the line of
+// pair g in xi~ coordinates must meet the element's box inflated by dp and by
+// a margin pm that covers the fp32 re-basing error; keeps every pair the
+// exact prefilter keeps.
+__device__ __forceinline__ bool prefilter_f32(const CastSmem& S, const CamConst& cc, int g) {
+  const int w = pair_element(S, g);
+  const float* af = S.u.p.slot[w] + SLOT_AFF;
+  const Rect16 r = S.meta.rect[w];
+  const int rw = r.i1 - r.i0 + 1;
+  const int p = S.meta.pa[w] + g - S.meta.pstart[w];
+  const float di = (float)(r.i0 + p % rw) - 0.5f * (cc.W - 1), dj = (float)(r.j0 + p / rw) - 0.5f * (cc.H - 1);
+  float rf[3], D[3];
+#pragma unroll
+  for (int k = 0; k < 3; ++k) {
+    rf[k] = fmaf(dj, cc.f_Ru[k], fmaf(di, cc.f_Rt[k], cc.f_R0[k]));
+    D[k] = S.meta.Dc[w][k] - fmaf(dj, cc.f_Ou[k], di * cc.f_Ot[k]);
+  }
+  const float rr = rf[0] * rf[0] + rf[1] * rf[1] + rf[2] * rf[2];
+  const float a0 = (D[0] * rf[0] + D[1] * rf[1] + D[2] * rf[2]) / rr;
+  const float q0 = fmaf(a0, rf[0], -D[0]) - af[0], q1 = fmaf(a0, rf[1], -D[1]) - af[1],
+              q2 = fmaf(a0, rf[2], -D[2]) - af[2];
+  const float m = S.meta.pm[w];
+  float ben = -3.4e38f, bex = 3.4e38f;
+#pragma unroll
+  for (int k = 0; k < 3; ++k) {
+    const float x0 = 0.5f + af[3 + 3 * k] * q0 + af[4 + 3 * k] * q1 + af[5 + 3 * k] * q2;
+    const float dl = af[3 + 3 * k] * rf[0] + af[4 + 3 * k] * rf[1] + af[5 + 3 * k] * rf[2];
+    const float lo = -af[12 + k] - m - x0, hi = 1.0f + af[12 + k] + m - x0;
+    if (dl == 0.0f) {
+      if (lo > 0.0f || hi < 0.0f) return false;
+      continue;
+    }
+    const float inv = 1.0f / dl, ta = lo * inv, tb = hi * inv;
+    ben = fmaxf(ben, fminf(ta, tb));
+    bex = fminf(bex, fmaxf(ta, tb));
+  }
+  return bex >= ben;
+}
+
 __device__ __forceinline__ void isect_chunk(WarpIsect& W, CastSmem& S, const CamConst& cc, int nvis, int vfirst,
-                                            int g0, float4* __restrict__ items, int* s_nitems,
+                                            int g, float4* __restrict__ items, int* s_nitems,
                                             int32_t* __restrict__ hits_pp, int& local_hits, int& face_fail) {
   const unsigned lane = threadIdx.x & 31;
   const float tol = cc.newton_tol;
   const int max_it = cc.newton_max;
-  const int g = g0 + (int)lane;
-  const bool active = g < S.meta.pstart[nvis];
-  int w = 0;
-  if (active) {   // the chunk's first element, then forward (1-2 steps at C4)
-    w = S.meta.vmap[g0 / RC_CHUNK];
-    while (S.meta.pstart[w + 1] <= g) ++w;
-  }
+  const bool active = g >= 0 && g < S.meta.pstart[nvis];
+  const int w = active ? pair_element(S, g) : 0;
   const float* sB = S.u.p.slot[w];
   const double* org = S.meta.org[w];
   const Rect16 r = S.meta.rect[w];
@@ -800,7 +846,7 @@ __device__ __forceinline__ void isect_chunk(WarpIsect& W, CastSmem& S, const Cam
   const float dpv[3] = {af[12], af[13], af[14]};
   const float dpm = fmaxf(dpv[0], fmaxf(dpv[1], dpv[2]));
   const int rw = r.i1 - r.i0 + 1;
-  const int p = S.meta.pa[w] + g - S.meta.pstart[w];
+  const int p = S.meta.pa[w] + (active ? g : 0) - S.meta.pstart[w];
   const int i = r.i0 + p % rw, j = r.j0 + p / rw;
 
   // ---- 1a: ray of pixel (i,j), re-based near the element (fp64) -----------
@@ -1384,6 +1430,18 @@ __global__ void __launch_bounds__(CWARPS * 32, CAST_CTAS_PER_SM) k_cast_curved(C
       const int a = S.meta.pstart[w], b = S.meta.pstart[w + 1];
       if (b > a)
         for (int c = (a + RC_CHUNK - 1) / RC_CHUNK; c * RC_CHUNK < b; ++c) S.meta.vmap[c] = (uint8_t)w;
+      // prefilter constants: re-basing vector and a margin covering its fp32 error
+      float dn = 0.0f, jn = 0.0f;
+#pragma unroll
+      for (int k = 0; k < 3; ++k) {
+        const double d = S.meta.org[w][k] - cc.O0[k];
+        S.meta.Dc[w][k] = (float)d;
+        dn = fmaxf(dn, fabsf((float)d));
+        const float* ji = S.u.p.slot[w] + SLOT_AFF + 3 + 3 * k;
+        jn = fmaxf(jn, fabsf(ji[0]) + fabsf(ji[1]) + fabsf(ji[2]));
+      }
+      const float ext = fmaxf(dn, (float)(cc.ell * (cc.W + cc.H)) + dn);   // |D| incl. ortho pixel offsets
+      S.meta.pm[w] = 4e-6f * (ext + 1.0f) * jn + 1e-4f;
     }
     __syncthreads();
     // ---- phase 1: intersection -----------------------------------------------
@@ -1392,13 +1450,47 @@ __global__ void __launch_bounds__(CWARPS * 32, CAST_CTAS_PER_SM) k_cast_curved(C
       if (lane == 0) W.stats[0] = W.stats[1] = 0;
       __syncwarp();
       const int nvchunks = (S.meta.pstart[U.nvis] + RC_CHUNK - 1) / RC_CHUNK;
+#if CAST_COMPACT
+      // candidates that pass the conservative fp32 prefilter are queued and
+      // intersected 32 at a time (misses no longer occupy the exact path)
+      const int npairs = S.meta.pstart[U.nvis];
+      int qn = 0;
       for (;;) {
         int k = 0;
         if (lane == 0) k = atomicAdd(&ctl.next_chunk, 1);
         k = __shfl_sync(0xffffffffu, k, 0);
         if (k >= nvchunks) break;
-        isect_chunk(W, S, cc, U.nvis, U.vfirst, k * RC_CHUNK, items, &ctl.nitems, hits_pp, local_hits, face_fail);
+        const int g = k * RC_CHUNK + (int)lane;
+        const bool keep = g < npairs && prefilter_f32(S, cc, g);
+        const unsigned bal = __ballot_sync(0xffffffffu, keep);
+        if (keep) W.queue[qn + __popc(bal & ((1u << lane) - 1u))] = g;
+        qn += __popc(bal);
+        __syncwarp();
+        if (qn >= 32) {
+          const int gq = W.queue[lane];
+          const int rest = qn > 32 + (int)lane ? W.queue[32 + lane] : 0;
+          __syncwarp();
+          if (32 + (int)lane < qn) W.queue[lane] = rest;
+          qn -= 32;
+          __syncwarp();
+          isect_chunk(W, S, cc, U.nvis, U.vfirst, gq, items, &ctl.nitems, hits_pp, local_hits, face_fail);
+        }
       }
+      if (qn > 0) {
+        const int gq = (int)lane < qn ? W.queue[lane] : -1;
+        __syncwarp();
+        isect_chunk(W, S, cc, U.nvis, U.vfirst, gq, items, &ctl.nitems, hits_pp, local_hits, face_fail);
+      }
+#else
+      for (;;) {
+        int k = 0;
+        if (lane == 0) k = atomicAdd(&ctl.next_chunk, 1);
+        k = __shfl_sync(0xffffffffu, k, 0);
+        if (k >= nvchunks) break;
+        isect_chunk(W, S, cc, U.nvis, U.vfirst, k * RC_CHUNK + (int)lane, items, &ctl.nitems, hits_pp,
+                    local_hits, face_fail);
+      }
+#endif
       if (lane == 0) {
         n_tasks += W.stats[0];
         n_fallback += W.stats[1];

@@ -309,6 +309,13 @@ extern "C" rc_status rc_camera_set(rc_forest* f, const rc_camera* cam, void* str
     c.amax = cam->far_dist;
   }
   gl_tables(c.N, c.u, c.w, c.S);
+  for (int k = 0; k < 3; ++k) {
+    c.f_R0[k] = (float)c.R0[k];
+    c.f_Rt[k] = (float)c.Rt[k];
+    c.f_Ru[k] = (float)c.Ru[k];
+    c.f_Ot[k] = (float)c.Ot[k];
+    c.f_Ou[k] = (float)c.Ou[k];
+  }
   c.kappa0 = f->transfer.kappa0;
   c.inv_F = f->transfer.inv_F;
   c.q0 = f->transfer.q0;

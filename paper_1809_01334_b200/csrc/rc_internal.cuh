@@ -49,6 +49,7 @@ struct CamConst {
   double n, ell, far_dist;
   float u[RC_MAX_N], w[RC_MAX_N], S[RC_MAX_N * RC_MAX_N];
   float kappa0, inv_F, q0;
+  float f_R0[3], f_Rt[3], f_Ru[3], f_Ot[3], f_Ou[3];   // fp32 copies for the conservative prefilter
 };
 
 // Per-tree constants (device buffer, warp-uniform reads).
