@@ -328,6 +328,7 @@ def main():
 
     # --- end to end through the public API with HOST buffers --------------
     seg_info = forest.segments()
+    composite_copy = int(forest.last_phase_ms(3))
     newton_failures = seg_info["newton_failures"]
     fold_info = {"face_failures": seg_info["face_failures"], "fold_levels": fold, "records": seg_info["count"], "raw_segments": seg_info["raw_segments"],
                  "record_level": seg_info["level"], "units": seg_info["units"],
@@ -392,7 +393,8 @@ def main():
                            "parallelism": f"sfc{world}"},
                 "roofline": roof, "gpu_launches": launches, "clocks": clk.summary(), "e2e": e2e,
                 "newton_failures": newton_failures, "segments": fold_info,
-                "phase_ms": {k: round(v, 3) for k, v in phase_acc.items()}}
+                "phase_ms": {k: round(v, 3) for k, v in phase_acc.items()},
+                "composite_copy": composite_copy}
         if world == 1 and not args.no_cpu_baseline:
             stride = {1: 1, 2: 8, 3: 32, 4: 64, 5: 128, 45: 32}[args.config]
             sc_cpu = scene_to_host(scene)

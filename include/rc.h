@@ -235,7 +235,9 @@ int64_t rc_launch_count(int32_t reset);
 float rc_last_cast_ms(rc_forest* f);
 /* [sync] device time of the last rc_cast_segments' segment kernel (CUDA
  * events on the caller's stream): phase 0 or 1 = the kernel (intersection,
- * integration and fold are fused), 2 = 0 (kept for ABI stability). */
+ * integration and fold are fused), 2 = 0 (kept for ABI stability);
+ * phase 3 = diagnostic of the last composite: 1 if it sorted a pixel-bucketed
+ * copy of the records, 0 if it gathered them through a permutation. */
 float rc_last_phase_ms(rc_forest* f, int32_t phase);
 
 #ifdef __cplusplus

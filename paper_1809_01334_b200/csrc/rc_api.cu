@@ -591,7 +591,9 @@ extern "C" float rc_last_cast_ms(rc_forest* f) {
 }
 
 extern "C" float rc_last_phase_ms(rc_forest* f, int32_t phase) {
-  if (!f || !f->timed) return -1.0f;
+  if (!f) return -1.0f;
+  if (phase == 3) return (float)f->last_composite_copy;
+  if (!f->timed) return -1.0f;
   if (phase == 0 || phase == 1) return rc_last_cast_ms(f);
   if (phase == 2) return 0.0f;
   return -1.0f;
@@ -720,9 +722,10 @@ extern "C" rc_status rc_composite_tiles(rc_forest* f, const rc_tiling* t, const 
     size_t free_b = 0, total_b = 0;
     const size_t have = f->sorted_cap >= nsrc ? (size_t)-1 : 0;
     if (have || (cudaMemGetInfo(&free_b, &total_b) == cudaSuccess &&
-                 free_b > (size_t)nsrc * sizeof(rc_seg) + ((size_t)8 << 30)))
+                 free_b > (size_t)nsrc * sizeof(rc_seg) + ((size_t)2 << 30)))
       copy = grow(&f->d_sorted, &f->sorted_cap, std::max<int64_t>(nsrc, 1)) == cudaSuccess;
   }
+  f->last_composite_copy = copy ? 1 : 0;
   if (!copy) CU(grow(&f->d_perm, &f->perm_cap, std::max<int64_t>(nsrc, 1)));
   int32_t* d_my_tiles = nullptr;
   CU(cudaMallocAsync((void**)&d_my_tiles, sizeof(int32_t) * std::max<size_t>(mine.size(), 1), s));

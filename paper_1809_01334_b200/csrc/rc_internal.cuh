@@ -147,6 +147,7 @@ struct rc_forest {
   // aggregation output (ping-pong with d_segs)
   int32_t* d_defer = nullptr;      // composite: deferred pixels [w*h]
   rc_seg* d_sorted = nullptr;      // composite: pixel-bucketed copy of the records
+  int last_composite_copy = -1;    // diagnostic: 1 copy path, 0 permutation path
   int64_t sorted_cap = 0;
   int64_t defer_cap = 0;
   rc_seg* d_segs2 = nullptr;
