@@ -639,6 +639,7 @@ struct UnitMeta {
   uint8_t vmap[RC_UNIT_CHUNKS + 16];    // element of the first pair of each 32-pair chunk
   float Dc[RC_UNIT_LEAVES][3];          // (float)(origin - O0): prefilter ray re-basing
   float pm[RC_UNIT_LEAVES];             // prefilter margin in xi~ units
+  float rwinv[RC_UNIT_LEAVES];          // 1 / rectangle width
 };
 struct Phase012 {
   float slot[RC_UNIT_LEAVES][SLOT_STRIDE];
@@ -785,6 +786,14 @@ __device__ __noinline__ void face_2d(WarpIsect& W, const float* __restrict__ sB,
 // pa[w] + g - pstart[w] of its rectangle (row-major).  A warp takes 32
 // consecutive pairs, so small elements (a few pixels each at C4/C5) do not
 // leave most lanes idle.
+// p = q rw + r for 0 <= p < 2^24 with a float reciprocal (exact after one correction)
+__device__ __forceinline__ void divmod_rw(int p, int rw, float rinv, int& q, int& r) {
+  q = (int)(((float)p + 0.5f) * rinv);
+  r = p - q * rw;
+  if (r < 0) { --q; r += rw; }
+  else if (r >= rw) { ++q; r -= rw; }
+}
+
 __device__ __forceinline__ int pair_element(const CastSmem& S, int g) {
   int w = S.meta.vmap[g / RC_CHUNK];   // the chunk's first element, then forward (1-2 steps at C4)
   while (S.meta.pstart[w + 1] <= g) ++w;
@@ -801,7 +810,9 @@ __device__ __forceinline__ bool prefilter_f32(const CastSmem& S, const CamConst&
   const Rect16 r = S.meta.rect[w];
   const int rw = r.i1 - r.i0 + 1;
   const int p = S.meta.pa[w] + g - S.meta.pstart[w];
-  const float di = (float)(r.i0 + p % rw) - 0.5f * (cc.W - 1), dj = (float)(r.j0 + p / rw) - 0.5f * (cc.H - 1);
+  int pq, pr;
+  divmod_rw(p, rw, S.meta.rwinv[w], pq, pr);
+  const float di = (float)(r.i0 + pr) - 0.5f * (cc.W - 1), dj = (float)(r.j0 + pq) - 0.5f * (cc.H - 1);
   float rf[3], D[3];
 #pragma unroll
   for (int k = 0; k < 3; ++k) {
@@ -847,7 +858,9 @@ __device__ __forceinline__ void isect_chunk(WarpIsect& W, CastSmem& S, const Cam
   const float dpm = fmaxf(dpv[0], fmaxf(dpv[1], dpv[2]));
   const int rw = r.i1 - r.i0 + 1;
   const int p = S.meta.pa[w] + (active ? g : 0) - S.meta.pstart[w];
-  const int i = r.i0 + p % rw, j = r.j0 + p / rw;
+  int pq, pr;
+  divmod_rw(p, rw, S.meta.rwinv[w], pq, pr);
+  const int i = r.i0 + pr, j = r.j0 + pq;
 
   // ---- 1a: ray of pixel (i,j), re-based near the element (fp64) -----------
   const double di = (double)i - 0.5 * (cc.W - 1), dj = (double)j - 0.5 * (cc.H - 1);
@@ -1069,7 +1082,8 @@ __device__ __forceinline__ void isect_chunk(WarpIsect& W, CastSmem& S, const Cam
       it[1] = make_float4(fmaf(b1, rf[1], P0[1]), fmaf(b1, rf[2], P0[2]), W.roots[ia][1][lane],
                           W.roots[ia][2][lane]);
       it[2] = make_float4(W.roots[ia][3][lane], W.roots[ib][1][lane], W.roots[ib][2][lane], W.roots[ib][3][lane]);
-      it[3] = make_float4(alpha0 + b0, alpha0 + b1, __uint_as_float(pix), __int_as_float(v));
+      it[3] = make_float4(alpha0 + b0, alpha0 + b1, __uint_as_float((uint32_t)i | ((uint32_t)j << 16)),
+                          __int_as_float(v));
     }
     ++slot;
   }
@@ -1237,9 +1251,11 @@ __device__ __forceinline__ bool touching(float an, float af_prev) {
 // One window of rows [bj0, bj0 + rows) of the unit's pixel rectangle (the
 // caller covers the rectangle with windows of <= PIXCAP pixels); segments of
 // other rows are left to their window.
+// Scratch segments carry the pixel packed relative to the unit's rectangle
+// ((row << 16) | col); the window covers rectangle rows [r0, r0 + rows).
 __device__ void fold_bucket(CastSmem& S, CastCtl& ctl, const rc_seg* __restrict__ segs, int nitems, int bi0, int bj0,
-                            int bw, int rows, int W, uint32_t ukey, rc_seg* __restrict__ out, int64_t out_cap,
-                            int64_t* __restrict__ counters) {
+                            int r0, int bw, int rows, int W, uint32_t ukey, rc_seg* __restrict__ out,
+                            int64_t out_cap, int64_t* __restrict__ counters) {
   const int tid = threadIdx.x;
   constexpr int NT = CWARPS * 32;
   FoldSmem& F = S.u.fold;
@@ -1251,11 +1267,11 @@ __device__ void fold_bucket(CastSmem& S, CastCtl& ctl, const rc_seg* __restrict_
   // shared memory, bucket counts per pixel of the window
   for (int k = tid; k < nitems; k += NT) {
     const float4 h = reinterpret_cast<const float4*>(segs + k)[0];   // pixel, alpha_near, alpha_far, a
-    const uint32_t pix = __float_as_uint(h.x);
-    const int row = (int)(pix / (uint32_t)W) - bj0;
+    const uint32_t lp = __float_as_uint(h.x);
+    const int row = (int)(lp >> 16) - r0;
     F.alpha[k] = make_float2(h.y, h.z);
     if (row < 0 || row >= rows) continue;
-    const int pl = row * bw + ((int)(pix % (uint32_t)W) - bi0);
+    const int pl = row * bw + (int)(lp & 0xffffu);
     F.rank[k] = (uint16_t)atomicAdd(&F.off[pl], 1);
   }
   __syncthreads();
@@ -1274,10 +1290,10 @@ __device__ void fold_bucket(CastSmem& S, CastCtl& ctl, const rc_seg* __restrict_
   if (tid == 0) F.off[area] = total;
   __syncthreads();
   for (int k = tid; k < nitems; k += NT) {   // pixel-bucketed order
-    const uint32_t pix = segs[k].pixel;
-    const int row = (int)(pix / (uint32_t)W) - bj0;
+    const uint32_t lp = segs[k].pixel;
+    const int row = (int)(lp >> 16) - r0;
     if (row < 0 || row >= rows) continue;
-    const int pl = row * bw + ((int)(pix % (uint32_t)W) - bi0);
+    const int pl = row * bw + (int)(lp & 0xffffu);
     F.order[F.off[pl] + F.rank[k]] = (uint16_t)k;
   }
   __syncthreads();
@@ -1334,7 +1350,7 @@ __device__ void fold_bucket(CastSmem& S, CastCtl& ctl, const rc_seg* __restrict_
             B2 = fma(A, (double)hb.z, B2);
             A *= (double)a;
           }
-          const uint32_t pix = (uint32_t)((bj0 + pl / bw) * W + bi0 + pl % bw);
+          const uint32_t pix = (uint32_t)((bj0 + r0 + pl / bw) * W + bi0 + pl % bw);
           if (pos < out_cap) {
             const float bf[3] = {(float)B0, (float)B1, (float)B2};
             store_seg_cs(out + pos, pix, F.alpha[ord[t]].x, afr, (float)A, bf, ukey);
@@ -1442,6 +1458,7 @@ __global__ void __launch_bounds__(CWARPS * 32, CAST_CTAS_PER_SM) k_cast_curved(C
       }
       const float ext = fmaxf(dn, (float)(cc.ell * (cc.W + cc.H)) + dn);   // |D| incl. ortho pixel offsets
       S.meta.pm[w] = 4e-6f * (ext + 1.0f) * jn + 1e-4f;
+      S.meta.rwinv[w] = 1.0f / (float)(S.meta.rect[w].i1 - S.meta.rect[w].i0 + 1);
     }
     __syncthreads();
     // ---- phase 1: intersection -----------------------------------------------
@@ -1501,6 +1518,7 @@ __global__ void __launch_bounds__(CWARPS * 32, CAST_CTAS_PER_SM) k_cast_curved(C
     raw_local += (tid == 0) ? nitems : 0;
     prev_items = nitems;
     // ---- phase 2: integration ---------------------------------------------------
+    const int ubi0 = -ctl.bb[0], ubj0 = -ctl.bb[2];
     {
       const int ngroups = (nitems + 31) / 32;
 #if CAST_PREFETCH
@@ -1536,7 +1554,10 @@ __global__ void __launch_bounds__(CWARPS * 32, CAST_CTAS_PER_SM) k_cast_curved(C
           const float4 i0 = it[0], i1 = it[1], i2 = it[2], i3 = it[3];
 #endif
           v = __float_as_int(i3.w);
-          pix = __float_as_uint(i3.z);
+          const uint32_t ij = __float_as_uint(i3.z);
+          // fold: pixel packed relative to the unit's rectangle; else global j W + i
+          pix = fold > 0 ? ((((ij >> 16) - (uint32_t)ubj0) << 16) | ((ij & 0xffffu) - (uint32_t)ubi0))
+                         : (ij >> 16) * (uint32_t)cc.W + (ij & 0xffffu);
           an = i3.x;
           afar = i3.y;
           integ_item<P, N>(S.u.p.slot[v - U.vfirst], cc, i0, i1, i2, S.u.p.ph.scr + tid, fails, a, bb);
@@ -1563,7 +1584,7 @@ __global__ void __launch_bounds__(CWARPS * 32, CAST_CTAS_PER_SM) k_cast_curved(C
       if (bw <= PIXCAP && nitems <= FCAP) {
         const int rows = PIXCAP / bw;
         for (int r0 = 0; r0 < bh; r0 += rows)
-          fold_bucket(S, ctl, segs, nitems, bi0, bj0 + r0, bw, min(rows, bh - r0), cc.W, U.key, out, out_cap,
+          fold_bucket(S, ctl, segs, nitems, bi0, bj0, r0, bw, min(rows, bh - r0), cc.W, U.key, out, out_cap,
                       counters);
         continue;
       }
@@ -1644,7 +1665,9 @@ __global__ void __launch_bounds__(CWARPS * 32, CAST_CTAS_PER_SM) k_cast_curved(C
         } while (q < n && !is_head(q));
         if (pos < out_cap) {
           const float bf[3] = {(float)B0, (float)B1, (float)B2};
-          store_seg(out + pos, s0.pixel, s0.alpha_near, afr, (float)A, bf, U.key);
+          const uint32_t gpix = (uint32_t)((-ctl.bb[2] + (int)(s0.pixel >> 16)) * cc.W - ctl.bb[0] +
+                                           (int)(s0.pixel & 0xffffu));
+          store_seg(out + pos, gpix, s0.alpha_near, afr, (float)A, bf, U.key);
         } else {
           atomicAdd((unsigned long long*)&counters[CNT_OVERFLOW], 1ull);
         }
