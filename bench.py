@@ -161,7 +161,8 @@ def run_reference(args):
     import torch
     dev = "cuda" if (args.config >= 3 and torch.cuda.is_available()) else None
     scene = scene_to_host(make_scene(args.config, dev))
-    stride = {1: 1, 2: 8, 3: 32, 4: 64, 5: 128, 45: 32}[args.config]
+    # each step a bounded sample (~5-15 s of host work) so that --steps K ends within minutes
+    stride = {1: 1, 2: 16, 3: 64, 4: 128, 5: 256, 45: 64}[args.config]
     for _ in range(args.warmup):
         pass
     vals = []
