@@ -592,6 +592,14 @@ __device__ __noinline__ void prep_element_t(float* __restrict__ sl, double* __re
 #define CAST_WARPS 4        // warps per CTA
 #endif
 constexpr int CWARPS = CAST_WARPS;
+#ifndef CAST_OUTLINE
+#define CAST_OUTLINE 0      // 1: phase bodies as out-of-line functions (instruction-cache A/B knob)
+#endif
+#if CAST_OUTLINE
+#define PHASE_INLINE __noinline__
+#else
+#define PHASE_INLINE __forceinline__
+#endif
 #ifndef CAST_COMPACT
 #define CAST_COMPACT 1      // 1: fp32 prefilter first, the exact path only for candidates it keeps
 #endif
@@ -841,7 +849,7 @@ __device__ __forceinline__ bool prefilter_f32(const CastSmem& S, const CamConst&
   return bex >= ben;
 }
 
-__device__ __forceinline__ void isect_chunk(WarpIsect& W, CastSmem& S, const CamConst& cc, int nvis, int vfirst,
+__device__ PHASE_INLINE void isect_chunk(WarpIsect& W, CastSmem& S, const CamConst& cc, int nvis, int vfirst,
                                             int g, float4* __restrict__ items, int* s_nitems,
                                             int32_t* __restrict__ hits_pp, int& local_hits, int& face_fail) {
   const unsigned lane = threadIdx.x & 31;
@@ -1099,7 +1107,7 @@ __device__ __forceinline__ void isect_chunk(WarpIsect& W, CastSmem& S, const Cam
 // iteration stops when that bound is below tol (plain s < tol when q >= 1/2).
 // scr: this thread's scratch (stride CWARPS*32 floats) for the node values
 template <int P, int N>
-__device__ __forceinline__ void integ_item(const float* __restrict__ gs, const CamConst& cc, float4 i0, float4 i1,
+__device__ PHASE_INLINE void integ_item(const float* __restrict__ gs, const CamConst& cc, float4 i0, float4 i1,
                                            float4 i2, float* __restrict__ scr, int& fails, float& a_out,
                                            float b_out[3]) {
   constexpr int ST = CWARPS * 32;
