@@ -174,7 +174,7 @@ def run_reference(args):
     line = {"impl": "reference", "metric": "element-ray segment evaluations/s (hit pairs/s)", "value": v,
             "unit": "hit pairs/s", "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
             "ms_per_step": 1000.0 * statistics.median([x["seconds"] for x in vals]),
-            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+            "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f64",
             "data": "synthetic", "config": {"workload": WORKLOAD[args.config], "sample_stride": stride},
             "cpu_baseline": {k: cb[k] for k in ("value", "unit", "cores", "kind", "sample")},
             "e2e": {"value": v, "unit": "hit pairs/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
@@ -385,7 +385,7 @@ def main():
     if rank == 0:
         line = {"metric": "element-ray segment evaluations/s (hit pairs/s)", "value": value, "unit": "hit pairs/s",
                 "n_gpus": world, "steps": args.steps, "warmup": max(3, args.warmup), "ms_per_step": ms_step,
-                "higher_is_better": True, "scaling": "weak" if world == 1 else "strong", "vs_baseline": None,
+                "higher_is_better": True, "scaling": "strong", "vs_baseline": None,
                 "dtype": "f32", "data": "synthetic (seeded, scenegen)",
                 "config": {"workload": WORKLOAD[args.config], "leaves": n, "image": [W, H], "gl_points": N,
                            "hit_pairs": hits_total, "candidate_pairs": cand_total,
