@@ -296,6 +296,9 @@ def main():
             torch.cuda.synchronize()
             times.append(e0.elapsed_time(e1))
             cast_ms.append(forest.last_phase_ms(1))
+            if world == 1:
+                for k, nm in ((4, "composite_bucket"), (5, "composite_fold")):
+                    phase_acc[nm] = phase_acc.get(nm, 0.0) + forest.last_phase_ms(k) / args.steps
             names = ["start", "cull", "cast", "aggregate", "composite"]
             for a, b in zip(names, names[1:]):
                 phase_acc[b] = phase_acc.get(b, 0.0) + phase_ev[a].elapsed_time(phase_ev[b]) / args.steps

@@ -237,7 +237,9 @@ float rc_last_cast_ms(rc_forest* f);
  * events on the caller's stream): phase 0 or 1 = the kernel (intersection,
  * integration and fold are fused), 2 = 0 (kept for ABI stability);
  * phase 3 = diagnostic of the last composite: 1 if it sorted a pixel-bucketed
- * copy of the records, 0 if it gathered them through a permutation. */
+ * copy of the records, 0 if it gathered them through a permutation;
+ * phase 4 / 5 = device time of the last composite's pixel bucketing (k_hist,
+ * scan, scatter) / per-pixel fold kernels (k_fold), -1 before any composite. */
 float rc_last_phase_ms(rc_forest* f, int32_t phase);
 
 #ifdef __cplusplus

@@ -558,6 +558,182 @@ __device__ __noinline__ void prep_element_t(float* __restrict__ sl, double* __re
   af[15] = eta * 1.001f + 1e-5f;
 }
 
+// Element preparation by a PAIR of adjacent lanes (h = lane & 1): the same
+// slot as prep_element_t with the work split -- rows (r3, r2) 0..4 / 5..8 of
+// the restriction, half of the Bernstein sums of the affine model and of the
+// bounds each, combined with pair shuffles.  Every lane of the warp calls it
+// (inactive pairs with act = false) because of the shuffles and __syncwarp.
+__device__ __noinline__ void prep_element_pair(float* __restrict__ sl, double* __restrict__ org,
+                                               const TreeConst* __restrict__ trees, const DevLeafView& L, int e,
+                                               int NF, bool act) {
+  const int h = threadIdx.x & 1;
+  double M[3][3][3];
+  const double* __restrict__ Bw = nullptr;
+  double o[3] = {0.0, 0.0, 0.0};
+  if (act) {
+    const double hh = ldexp(1.0, -(int)L.level[e]);
+    Bw = trees[L.tree[e]].Bw;   // [q3][q2][q1][xyz]
+#pragma unroll
+    for (int k = 0; k < 3; ++k) {
+      const double u = ldexp((double)L.anchor[3 * (int64_t)e + k], -RC_MAXLEVEL), w = u + hh;
+#pragma unroll
+      for (int r = 0; r < 3; ++r) {
+        const double x = r == 2 ? w : u, y = r == 0 ? u : w;
+        M[k][r][0] = (1 - x) * (1 - y);
+        M[k][r][1] = (1 - x) * y + x * (1 - y);
+        M[k][r][2] = x * y;
+      }
+    }
+    // origin = point (1,1,1) (both lanes: it re-bases every point)
+#pragma unroll
+    for (int q3 = 0; q3 < 3; ++q3)
+#pragma unroll
+      for (int q2 = 0; q2 < 3; ++q2) {
+        const double w23 = M[2][1][q3] * M[1][1][q2];
+#pragma unroll
+        for (int q1 = 0; q1 < 3; ++q1) {
+          const double wq = w23 * M[0][1][q1];
+          const double* b = Bw + ((q3 * 3 + q2) * 3 + q1) * 3;
+#pragma unroll
+          for (int c = 0; c < 3; ++c) o[c] = fma(wq, b[c], o[c]);
+        }
+      }
+    if (h == 0) {
+      org[0] = o[0];
+      org[1] = o[1];
+      org[2] = o[2];
+    }
+    // rows (r3, r2) = 0..4 on lane h = 0, 5..8 on h = 1
+    const int row0 = h == 0 ? 0 : 5, row1 = h == 0 ? 5 : 9;
+    int cur3 = -1;
+    double T2[9][3];
+#pragma unroll 1
+    for (int row = row0; row < row1; ++row) {
+      const int r3 = row / 3, r2 = row % 3;
+      double m2[3];   // M[1][r2][.] by selects (no local-memory indexing)
+#pragma unroll
+      for (int q = 0; q < 3; ++q) m2[q] = r2 == 0 ? M[1][0][q] : (r2 == 1 ? M[1][1][q] : M[1][2][q]);
+      if (r3 != cur3) {
+        double m3[3];
+#pragma unroll
+        for (int q = 0; q < 3; ++q) m3[q] = r3 == 0 ? M[2][0][q] : (r3 == 1 ? M[2][1][q] : M[2][2][q]);
+#pragma unroll
+        for (int q21 = 0; q21 < 9; ++q21)
+#pragma unroll
+          for (int c = 0; c < 3; ++c) {
+            double acc = 0.0;
+#pragma unroll
+            for (int q3 = 0; q3 < 3; ++q3) acc = fma(m3[q3], Bw[(q3 * 9 + q21) * 3 + c], acc);
+            T2[q21][c] = acc;
+          }
+        cur3 = r3;
+      }
+      double T1[3][3];
+#pragma unroll
+      for (int q1 = 0; q1 < 3; ++q1)
+#pragma unroll
+        for (int c = 0; c < 3; ++c) {
+          double acc = 0.0;
+#pragma unroll
+          for (int q2 = 0; q2 < 3; ++q2) acc = fma(m2[q2], T2[q2 * 3 + q1][c], acc);
+          T1[q1][c] = acc;
+        }
+#pragma unroll
+      for (int r1 = 0; r1 < 3; ++r1) {
+        float* dst = sl + GI(row * 3 + r1);
+#pragma unroll
+        for (int c = 0; c < 3; ++c) {
+          double acc = 0.0;
+#pragma unroll
+          for (int q1 = 0; q1 < 3; ++q1) acc = fma(M[0][r1][q1], T1[q1][c], acc);
+          dst[c] = (float)(acc - o[c]);
+        }
+      }
+    }
+    for (int q = h; q < NF; q += 2) sl[SLOT_FIELD + FI(q, NF)] = __ldg(&L.field[(int64_t)e * NF + q]);
+  }
+  __syncwarp();
+  // affine model at the centre: each lane sums its rows' Bernstein coefficients
+  const float wq[3] = {0.25f, 0.5f, 0.25f}, dq[3] = {-1.0f, 0.0f, 1.0f};
+  float acc[12];
+#pragma unroll
+  for (int t = 0; t < 12; ++t) acc[t] = 0.0f;
+  const int m0 = h == 0 ? 0 : 15, m1e = h == 0 ? 15 : 27;
+  if (act) {
+#pragma unroll 1
+    for (int m = m0; m < m1e; ++m) {
+      const int a1 = m % 3, a2 = (m / 3) % 3, a3 = m / 9;
+      const float* b = sl + GI(m);
+      const float w3 = wq[a1] * wq[a2] * wq[a3];
+      const float g[3] = {dq[a1] * wq[a2] * wq[a3], wq[a1] * dq[a2] * wq[a3], wq[a1] * wq[a2] * dq[a3]};
+#pragma unroll
+      for (int c = 0; c < 3; ++c) {
+        acc[c] = fmaf(w3, b[c], acc[c]);
+#pragma unroll
+        for (int a = 0; a < 3; ++a) acc[3 + 3 * c + a] = fmaf(g[a], b[c], acc[3 + 3 * c + a]);
+      }
+    }
+  }
+#pragma unroll
+  for (int t = 0; t < 12; ++t) acc[t] += __shfl_xor_sync(0xffffffffu, acc[t], 1);
+  const float Xc[3] = {acc[0], acc[1], acc[2]};
+  float J[3][3], Ji[3][3];
+#pragma unroll
+  for (int c = 0; c < 3; ++c)
+#pragma unroll
+    for (int a = 0; a < 3; ++a) J[c][a] = acc[3 + 3 * c + a];
+  if (!inv3(J, Ji)) {
+#pragma unroll
+    for (int a = 0; a < 3; ++a)
+#pragma unroll
+      for (int b = 0; b < 3; ++b) Ji[a][b] = 0.0f;
+  }
+  float dp0 = 0.f, dp1 = 0.f, dp2 = 0.f, eta = 0.0f;
+  if (act) {
+#pragma unroll 1
+    for (int m = m0; m < m1e; ++m) {
+      const int mmv[3] = {m % 3, (m / 3) % 3, m / 9};
+      const float* b = sl + GI(m);
+      const float x0 = 0.5f * mmv[0] - 0.5f, x1 = 0.5f * mmv[1] - 0.5f, x2 = 0.5f * mmv[2] - 0.5f;
+      const float r0 = b[0] - (Xc[0] + J[0][0] * x0 + J[0][1] * x1 + J[0][2] * x2);
+      const float r1 = b[1] - (Xc[1] + J[1][0] * x0 + J[1][1] * x1 + J[1][2] * x2);
+      const float r2 = b[2] - (Xc[2] + J[2][0] * x0 + J[2][1] * x1 + J[2][2] * x2);
+      dp0 = fmaxf(dp0, fabsf(Ji[0][0] * r0 + Ji[0][1] * r1 + Ji[0][2] * r2));
+      dp1 = fmaxf(dp1, fabsf(Ji[1][0] * r0 + Ji[1][1] * r1 + Ji[1][2] * r2));
+      dp2 = fmaxf(dp2, fabsf(Ji[2][0] * r0 + Ji[2][1] * r1 + Ji[2][2] * r2));
+      const int str[3] = {1, 3, 9};
+#pragma unroll
+      for (int ax = 0; ax < 3; ++ax) {
+        if (mmv[ax] < 2) {
+          const float* b2 = sl + GI(m + str[ax]);
+          const float e0 = 2.0f * (b2[0] - b[0]), e1 = 2.0f * (b2[1] - b[1]), e2 = 2.0f * (b2[2] - b[2]);
+          const float t0 = Ji[0][0] * e0 + Ji[0][1] * e1 + Ji[0][2] * e2 - (ax == 0 ? 1.0f : 0.0f);
+          const float t1 = Ji[1][0] * e0 + Ji[1][1] * e1 + Ji[1][2] * e2 - (ax == 1 ? 1.0f : 0.0f);
+          const float t2 = Ji[2][0] * e0 + Ji[2][1] * e1 + Ji[2][2] * e2 - (ax == 2 ? 1.0f : 0.0f);
+          eta = fmaxf(eta, fmaxf(fabsf(t0), fmaxf(fabsf(t1), fabsf(t2))));
+        }
+      }
+    }
+  }
+  dp0 = fmaxf(dp0, __shfl_xor_sync(0xffffffffu, dp0, 1));
+  dp1 = fmaxf(dp1, __shfl_xor_sync(0xffffffffu, dp1, 1));
+  dp2 = fmaxf(dp2, __shfl_xor_sync(0xffffffffu, dp2, 1));
+  eta = fmaxf(eta, __shfl_xor_sync(0xffffffffu, eta, 1));
+  if (act && h == 0) {
+    float* af = sl + SLOT_AFF;
+    af[0] = Xc[0]; af[1] = Xc[1]; af[2] = Xc[2];
+#pragma unroll
+    for (int a = 0; a < 3; ++a)
+#pragma unroll
+      for (int b = 0; b < 3; ++b) af[3 + 3 * a + b] = Ji[a][b];
+    // inflate by a rounding margin relative to the element (fp32)
+    af[12] = dp0 * 1.001f + 1e-5f;
+    af[13] = dp1 * 1.001f + 1e-5f;
+    af[14] = dp2 * 1.001f + 1e-5f;
+    af[15] = eta * 1.001f + 1e-5f;
+  }
+}
+
 // ---------------------------------------------------------------------------
 // The fused segment kernel (rows a4 + a5 + a6 of SURVEY §8(a)).  Persistent
 // CTAs of CWARPS warps take fold units from a global counter; a unit is a
@@ -592,6 +768,9 @@ __device__ __noinline__ void prep_element_t(float* __restrict__ sl, double* __re
 #define CAST_WARPS 4        // warps per CTA
 #endif
 constexpr int CWARPS = CAST_WARPS;
+#ifndef CAST_PAIR_PREP
+#define CAST_PAIR_PREP 0    // 1: two lanes per element in phase 0 (same-box A/B: 643 -> 672 ms, rejected)
+#endif
 #ifndef CAST_OUTLINE
 #define CAST_OUTLINE 0      // 1: phase bodies as out-of-line functions (instruction-cache A/B knob)
 #endif
@@ -1447,8 +1626,17 @@ __global__ void __launch_bounds__(CWARPS * 32, CAST_CTAS_PER_SM) k_cast_curved(C
       if (a1 <= U.nvis) S.meta.pstart[a1] = incl;
       if (lane == 0) S.meta.pstart[0] = 0;
     }
+#if CAST_PAIR_PREP
+    {   // two lanes per element (RC_UNIT_LEAVES <= 64 = half the CTA)
+      const int w = tid >> 1;
+      const bool act = w < U.nvis;
+      prep_element_pair(S.u.p.slot[act ? w : 0], S.meta.org[act ? w : 0], trees, L, act ? vis[U.vfirst + w] : 0, NF,
+                        act);
+    }
+#else
     for (int w = tid; w < U.nvis; w += CWARPS * 32)
       prep_element_t(S.u.p.slot[w], S.meta.org[w], trees, L, vis[U.vfirst + w], NF, true);
+#endif
     __syncthreads();
     for (int w = tid; w < U.nvis; w += CWARPS * 32) {   // chunk -> first element map
       const int a = S.meta.pstart[w], b = S.meta.pstart[w + 1];

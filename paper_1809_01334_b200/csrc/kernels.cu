@@ -697,6 +697,9 @@ __device__ __forceinline__ bool fold_pixel_reg(const rc_seg* __restrict__ recs, 
 // Two passes: CAP = 512 over every pixel (registers, 16 warps per SM); the
 // few pixels with more records are deferred to a list that the CAP = 2048
 // pass (shared-memory bitonic, else selection order) works through.
+#ifndef FOLD_E4
+#define FOLD_E4 1   // 1: a 128-record register bucket (C4's pixels hold ~115 records)
+#endif
 template <int CAP, bool FROM_LIST>
 __global__ void __launch_bounds__(FOLD_WARPS * 32, CAP <= 512 ? 4 : 1) k_fold(
     const rc_seg* __restrict__ recs, const uint32_t* __restrict__ perm, const int64_t* __restrict__ off, int W,
@@ -729,6 +732,9 @@ __global__ void __launch_bounds__(FOLD_WARPS * 32, CAP <= 512 ? 4 : 1) k_fold(
     Acc acc{1.0, 0.0, 0.0, 0.0};
     bool done = false;
     if (n <= 64) done = fold_pixel_reg<2>(recs, S, base, n, tau, acc);
+#if FOLD_E4
+    else if (n <= 128) done = fold_pixel_reg<4>(recs, S, base, n, tau, acc);
+#endif
     else if (n <= 256) done = fold_pixel_reg<8>(recs, S, base, n, tau, acc);
     else if (n <= 512) done = fold_pixel_reg<16>(recs, S, base, n, tau, acc);
     if (done) {

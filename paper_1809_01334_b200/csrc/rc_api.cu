@@ -152,6 +152,8 @@ extern "C" rc_status rc_forest_create(const rc_forest_desc* d, void* stream, rc_
   for (int k = 0; k < f->K; ++k)
     memcpy(f->h_trees[k].lagr, d->tree_ctrl + (size_t)k * n1 * n1 * n1 * 3, sizeof(double) * n1 * n1 * n1 * 3);
   if ((e = cudaEventCreate(&f->ev0)) || (e = cudaEventCreate(&f->ev1))) return cleanup(RC_ERR_CUDA, "event");
+  for (int k = 0; k < 3; ++k)
+    if ((e = cudaEventCreate(&f->evc[k]))) return cleanup(RC_ERR_CUDA, "event");
   if ((e = cudaStreamSynchronize(s))) return cleanup(RC_ERR_CUDA, "sync");
   if ((e = build_node_levels(f, s))) return cleanup(RC_ERR_CUDA, "node levels");
   *out = f;
@@ -172,6 +174,8 @@ extern "C" rc_status rc_forest_destroy(rc_forest* f) {
     if (f->d_node_first[c]) dfree(f->d_node_first[c]);
   if (f->ev0) cudaEventDestroy(f->ev0);
   if (f->ev1) cudaEventDestroy(f->ev1);
+  for (int k = 0; k < 3; ++k)
+    if (f->evc[k]) cudaEventDestroy(f->evc[k]);
   for (int k = 0; k < 4; ++k)
     if (f->evb[k]) cudaEventDestroy(f->evb[k]);
   delete[] f->h_trees;
@@ -593,6 +597,12 @@ extern "C" float rc_last_cast_ms(rc_forest* f) {
 extern "C" float rc_last_phase_ms(rc_forest* f, int32_t phase) {
   if (!f) return -1.0f;
   if (phase == 3) return (float)f->last_composite_copy;
+  if (phase == 4 || phase == 5) {   // composite: bucketing (hist, scan, scatter) / fold kernels
+    if (!f->composite_timed || cudaEventSynchronize(f->evc[2]) != cudaSuccess) return -1.0f;
+    float ms = -1.0f;
+    if (cudaEventElapsedTime(&ms, f->evc[phase - 4], f->evc[phase - 3]) != cudaSuccess) return -1.0f;
+    return ms;
+  }
   if (!f->timed) return -1.0f;
   if (phase == 0 || phase == 1) return rc_last_cast_ms(f);
   if (phase == 2) return 0.0f;
@@ -731,6 +741,7 @@ extern "C" rc_status rc_composite_tiles(rc_forest* f, const rc_tiling* t, const 
   CU(cudaMallocAsync((void**)&d_my_tiles, sizeof(int32_t) * std::max<size_t>(mine.size(), 1), s));
   if (!mine.empty())
     CU(cudaMemcpyAsync(d_my_tiles, mine.data(), sizeof(int32_t) * mine.size(), cudaMemcpyHostToDevice, s));
+  CU(cudaEventRecord(f->evc[0], s));
   CU(cudaMemsetAsync(f->d_pix_cnt, 0, sizeof(int32_t) * npix, s));
   int grid = sm_count() * 8;
   if (nsrc > 0) {
@@ -742,6 +753,7 @@ extern "C" rc_status rc_composite_tiles(rc_forest* f, const rc_tiling* t, const 
     if (copy) CU(launch_scatter_rec(src, nsrc, f->d_pix_off, f->d_pix_cnt, f->d_sorted, grid, s));
     else CU(launch_scatter(src, nsrc, f->d_pix_off, f->d_pix_cnt, f->d_perm, grid, s));
   }
+  CU(cudaEventRecord(f->evc[1], s));
   if (npix_out > 0) {
     float bg[3] = {0, 0, 0};
     if (background) memcpy(bg, background, sizeof bg);
@@ -749,6 +761,8 @@ extern "C" rc_status rc_composite_tiles(rc_forest* f, const rc_tiling* t, const 
     CU(launch_fold(copy ? f->d_sorted : src, copy ? nullptr : f->d_perm, f->d_pix_off, W, H, tw, th, d_my_tiles,
                    t->tiles_x, npix_out, bg, 1e-6f, d_rgba, f->d_defer, f->d_counters, sm_count() * 16, s));
   }
+  CU(cudaEventRecord(f->evc[2], s));
+  f->composite_timed = true;
   CU(cudaFreeAsync(d_my_tiles, s));
   return RC_OK;
 }

@@ -154,6 +154,8 @@ struct rc_forest {
   int64_t seg2_cap = 0;
   // timing
   cudaEvent_t ev0 = nullptr, ev1 = nullptr;
+  cudaEvent_t evc[3] = {nullptr, nullptr, nullptr};   // composite: start, after scatter, after fold
+  bool composite_timed = false;
   cudaEvent_t evb[4] = {nullptr, nullptr, nullptr, nullptr};
   float phase_ms[3] = {0, 0, 0};
   bool timed = false;
