@@ -566,6 +566,9 @@ constexpr int FOLD_CAP = 2048;   // records per pixel sorted in shared memory
 // layout i = lane E + e, ascending.  Stage loops are not unrolled (code size:
 // the per-pixel kernels were instruction-cache bound); only the element loops
 // and the in-register distances (j < E) are static.
+#ifndef FOLD_E4
+#define FOLD_E4 1   // 1: a 128-record register bucket in k_fold / k_coarsen (C4's pixels hold ~115 records)
+#endif
 template <int E>
 __device__ __forceinline__ void warp_sort_blocked(uint64_t (&key)[E], uint32_t (&id)[E]) {
   const unsigned lane = threadIdx.x & 31;
@@ -697,9 +700,6 @@ __device__ __forceinline__ bool fold_pixel_reg(const rc_seg* __restrict__ recs, 
 // Two passes: CAP = 512 over every pixel (registers, 16 warps per SM); the
 // few pixels with more records are deferred to a list that the CAP = 2048
 // pass (shared-memory bitonic, else selection order) works through.
-#ifndef FOLD_E4
-#define FOLD_E4 1   // 1: a 128-record register bucket (C4's pixels hold ~115 records)
-#endif
 template <int CAP, bool FROM_LIST>
 __global__ void __launch_bounds__(FOLD_WARPS * 32, CAP <= 512 ? 4 : 1) k_fold(
     const rc_seg* __restrict__ recs, const uint32_t* __restrict__ perm, const int64_t* __restrict__ off, int W,
@@ -875,6 +875,9 @@ __global__ void __launch_bounds__(FOLD_WARPS * 32) k_coarsen(const rc_seg* __res
       RunCache C{reinterpret_cast<uint32_t*>(keys), reinterpret_cast<float*>(keys) + 512,
                  reinterpret_cast<float*>(keys) + 1024, reinterpret_cast<int32_t*>(keys) + 1536};
       if (n <= 64) sort_pixel_cache<2>(recs, S, n, leaf_node, key_base, C);
+#if FOLD_E4
+      else if (n <= 128) sort_pixel_cache<4>(recs, S, n, leaf_node, key_base, C);
+#endif
       else if (n <= 256) sort_pixel_cache<8>(recs, S, n, leaf_node, key_base, C);
       else sort_pixel_cache<16>(recs, S, n, leaf_node, key_base, C);
       auto head = [&](int k) -> bool {
