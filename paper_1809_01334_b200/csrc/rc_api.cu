@@ -167,7 +167,7 @@ extern "C" rc_status rc_forest_destroy(rc_forest* f) {
                   f->d_vis, f->d_vis_rect, f->d_chunk_off, f->d_counters, f->d_trees, f->d_cam,
                   f->d_scan_tmp, f->d_chunk_elem, f->d_segs, f->d_hits_pp, f->d_pix_cnt, f->d_pix_off,
                   f->d_perm, f->d_send, f->d_items, f->d_leaf_nodes[0], f->d_leaf_nodes[1], f->d_ucnt, f->d_uend, f->d_units,
-                  f->d_scratch, f->d_segs2, f->d_uoff, f->d_defer, f->d_sorted};
+                  f->d_scratch, f->d_segs2, f->d_uoff, f->d_defer, f->d_sorted, f->d_tiles};
   for (void* p : ptrs)
     if (p) dfree(p);
   for (int c = 0; c <= RC_NODE_LEVELS; ++c)
@@ -178,6 +178,7 @@ extern "C" rc_status rc_forest_destroy(rc_forest* f) {
     if (f->evc[k]) cudaEventDestroy(f->evc[k]);
   for (int k = 0; k < 4; ++k)
     if (f->evb[k]) cudaEventDestroy(f->evb[k]);
+  if (f->h_tiles) cudaFreeHost(f->h_tiles);
   delete[] f->h_trees;
   delete f;
   return RC_OK;
@@ -532,14 +533,15 @@ extern "C" rc_status rc_cast_segments(rc_forest* f, int32_t fold_levels, void* s
   // raw segments ~1/2), capped by the free device memory so that a forest
   // near the memory limit falls back to the exact regrowth instead of failing
   int64_t est = curved ? (fold_levels > 0 ? cand / 4 : cand / 2 + cand / 8) : cand;
-  {
+  if (f->h_cast_total > 0) est = 0;   // later frames: the previous count (+1/8), exact regrowth if short
+  else {
     size_t free_b = 0, total_b = 0;
     if (cudaMemGetInfo(&free_b, &total_b) == cudaSuccess) {
       const int64_t cap = (int64_t)(free_b / 2 / sizeof(rc_seg)) + f->seg_cap;
       est = std::min(est, cap);
     }
   }
-  int64_t need = std::max<int64_t>(f->h_seg_total + f->h_seg_total / 8, est) + 4096;
+  int64_t need = std::max<int64_t>(f->h_cast_total + f->h_cast_total / 8, est) + 4096;
   CU(grow(&f->d_segs, &f->seg_cap, need));
   for (int attempt = 0; attempt < 2; ++attempt) {
     CU(cudaMemsetAsync(f->d_hits_pp, 0, sizeof(int32_t) * npix, s));
@@ -564,6 +566,7 @@ extern "C" rc_status rc_cast_segments(rc_forest* f, int32_t fold_levels, void* s
     CU(cudaMemcpyAsync(c + 1, f->d_counters + CNT_OVERFLOW, sizeof(int64_t), cudaMemcpyDeviceToHost, s));
     CU(cudaStreamSynchronize(s));
     f->h_seg_total = c[0];
+    f->h_cast_total = c[0];
     if (c[0] <= f->seg_cap && c[1] == 0) break;
     if (attempt == 1) return fail(RC_ERR_CAPACITY, "segment records overflow after regrowth");
     CU(grow(&f->d_segs, &f->seg_cap, c[0] + c[0] / 16 + 4096));
@@ -737,10 +740,27 @@ extern "C" rc_status rc_composite_tiles(rc_forest* f, const rc_tiling* t, const 
   }
   f->last_composite_copy = copy ? 1 : 0;
   if (!copy) CU(grow(&f->d_perm, &f->perm_cap, std::max<int64_t>(nsrc, 1)));
-  int32_t* d_my_tiles = nullptr;
-  CU(cudaMallocAsync((void**)&d_my_tiles, sizeof(int32_t) * std::max<size_t>(mine.size(), 1), s));
-  if (!mine.empty())
-    CU(cudaMemcpyAsync(d_my_tiles, mine.data(), sizeof(int32_t) * mine.size(), cudaMemcpyHostToDevice, s));
+  // the tile list lives on the device across frames: no per-frame allocation
+  // or pageable copy (both stalled the host for tens of ms at times)
+  const int32_t tkey[4] = {t->tiles_x, t->tiles_y, t->nranks, t->rank};
+  if (memcmp(tkey, f->tiling_key, sizeof tkey) != 0) {
+    const int64_t nt = std::max<int64_t>((int64_t)mine.size(), 1);
+    CU(grow(&f->d_tiles, &f->tiles_cap, nt));
+    if (f->h_tiles_cap < nt) {
+      if (f->h_tiles) cudaFreeHost(f->h_tiles);
+      f->h_tiles = nullptr;
+      f->h_tiles_cap = 0;
+      CU(cudaMallocHost((void**)&f->h_tiles, sizeof(int32_t) * nt));
+      f->h_tiles_cap = nt;
+    }
+    if (!mine.empty()) {
+      memcpy(f->h_tiles, mine.data(), sizeof(int32_t) * mine.size());
+      CU(cudaMemcpyAsync(f->d_tiles, f->h_tiles, sizeof(int32_t) * mine.size(), cudaMemcpyHostToDevice, s));
+      CU(cudaStreamSynchronize(s));   // h_tiles may be rewritten by the next call
+    }
+    memcpy(f->tiling_key, tkey, sizeof tkey);
+  }
+  const int32_t* d_my_tiles = f->d_tiles;
   CU(cudaEventRecord(f->evc[0], s));
   CU(cudaMemsetAsync(f->d_pix_cnt, 0, sizeof(int32_t) * npix, s));
   int grid = sm_count() * 8;
@@ -763,7 +783,6 @@ extern "C" rc_status rc_composite_tiles(rc_forest* f, const rc_tiling* t, const 
   }
   CU(cudaEventRecord(f->evc[2], s));
   f->composite_timed = true;
-  CU(cudaFreeAsync(d_my_tiles, s));
   return RC_OK;
 }
 

@@ -127,6 +127,7 @@ struct rc_forest {
   void* d_items = nullptr;
   int64_t items_cap = 0;
   int64_t h_seg_total = 0;
+  int64_t h_cast_total = 0;   // records written by the last rc_cast_segments (before aggregation)
   int64_t h_raw_affine = 0;        // affine path: segments before folding
   // coarsening hierarchy (nodes.cu): node tables of levels 1..RC_NODE_LEVELS
   int32_t* d_node_first[RC_NODE_LEVELS + 1] = {};
@@ -146,6 +147,10 @@ struct rc_forest {
   size_t scratch_bytes = 0;
   // aggregation output (ping-pong with d_segs)
   int32_t* d_defer = nullptr;      // composite: deferred pixels [w*h]
+  int32_t* d_tiles = nullptr;      // composite: this rank's tile ids (uploaded when the tiling changes)
+  int32_t* h_tiles = nullptr;      // pinned staging of d_tiles
+  int64_t tiles_cap = 0, h_tiles_cap = 0;
+  int32_t tiling_key[4] = {-1, -1, -1, -1};   // tiles_x, tiles_y, nranks, rank of d_tiles
   rc_seg* d_sorted = nullptr;      // composite: pixel-bucketed copy of the records
   int last_composite_copy = -1;    // diagnostic: 1 copy path, 0 permutation path
   int64_t sorted_cap = 0;
