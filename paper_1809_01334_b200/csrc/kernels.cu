@@ -700,8 +700,11 @@ __device__ __forceinline__ bool fold_pixel_reg(const rc_seg* __restrict__ recs, 
 // Two passes: CAP = 512 over every pixel (registers, 16 warps per SM); the
 // few pixels with more records are deferred to a list that the CAP = 2048
 // pass (shared-memory bitonic, else selection order) works through.
+#ifndef FOLD_MINB
+#define FOLD_MINB 4   // resident k_fold<512> CTAs per SM the register budget is sized for
+#endif
 template <int CAP, bool FROM_LIST>
-__global__ void __launch_bounds__(FOLD_WARPS * 32, CAP <= 512 ? 4 : 1) k_fold(
+__global__ void __launch_bounds__(FOLD_WARPS * 32, CAP <= 512 ? FOLD_MINB : 1) k_fold(
     const rc_seg* __restrict__ recs, const uint32_t* __restrict__ perm, const int64_t* __restrict__ off, int W,
     int H, int tw, int th, const int32_t* __restrict__ my_tiles, int tiles_x, int64_t npix_out, float bg0, float bg1,
     float bg2, float tau, float* __restrict__ rgba, int32_t* __restrict__ defer, int64_t* __restrict__ counters) {
