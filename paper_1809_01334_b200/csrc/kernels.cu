@@ -701,7 +701,7 @@ __device__ __forceinline__ bool fold_pixel_reg(const rc_seg* __restrict__ recs, 
 // few pixels with more records are deferred to a list that the CAP = 2048
 // pass (shared-memory bitonic, else selection order) works through.
 #ifndef FOLD_MINB
-#define FOLD_MINB 4   // resident k_fold<512> CTAs per SM the register budget is sized for
+#define FOLD_MINB 8   // resident k_fold<512> CTAs per SM the register budget is sized for (A/B: 4 -> 8 = 31.1 -> 25.4 ms at C4)
 #endif
 template <int CAP, bool FROM_LIST>
 __global__ void __launch_bounds__(FOLD_WARPS * 32, CAP <= 512 ? FOLD_MINB : 1) k_fold(
@@ -843,25 +843,37 @@ __global__ void __launch_bounds__(FOLD_WARPS * 32, CAP <= 512 ? FOLD_MINB : 1) k
 // result is keyed by the node's first leaf.  Records of one node that do not
 // touch stay separate (safe for non-convex curved nodes).
 // ---------------------------------------------------------------------------
-__global__ void __launch_bounds__(FOLD_WARPS * 32) k_coarsen(const rc_seg* __restrict__ recs,
-                                                             const uint32_t* __restrict__ perm,
-                                                             const int64_t* __restrict__ off, int64_t npix,
-                                                             const int32_t* __restrict__ node_first,
-                                                             const int32_t* __restrict__ leaf_node,
-                                                             uint32_t key_base, float tau, rc_seg* __restrict__ out,
-                                                             int64_t out_cap, int64_t* __restrict__ counters) {
+// Two passes (as k_fold): FROM_LIST = false takes every pixel with <= 512
+// records (8 KB of shared memory per warp: 6 resident CTAs per SM instead of
+// 2) and defers the others to a list that FROM_LIST = true works through.
+constexpr int COARSEN_CACHE = 512;
+#ifndef COARSEN_MINB
+#define COARSEN_MINB 6
+#endif
+template <bool FROM_LIST>
+__global__ void __launch_bounds__(FOLD_WARPS * 32, FROM_LIST ? 1 : COARSEN_MINB) k_coarsen(
+    const rc_seg* __restrict__ recs, const uint32_t* __restrict__ perm, const int64_t* __restrict__ off, int64_t npix,
+    const int32_t* __restrict__ node_first, const int32_t* __restrict__ leaf_node, uint32_t key_base, float tau,
+    rc_seg* __restrict__ out, int64_t out_cap, int32_t* __restrict__ defer, int64_t* __restrict__ counters) {
   extern __shared__ unsigned char smem_raw[];
   const int warp = threadIdx.x >> 5;
   const unsigned lane = threadIdx.x & 31;
-  uint64_t* keys = reinterpret_cast<uint64_t*>(smem_raw) + (size_t)warp * FOLD_CAP;
-  uint16_t* idxs = reinterpret_cast<uint16_t*>(reinterpret_cast<uint64_t*>(smem_raw) + (size_t)FOLD_WARPS * FOLD_CAP) +
+  constexpr int WCAP = FROM_LIST ? FOLD_CAP : COARSEN_CACHE * 2;   // uint64 words of keys per warp
+  uint64_t* keys = reinterpret_cast<uint64_t*>(smem_raw) + (size_t)warp * WCAP;
+  uint16_t* idxs = reinterpret_cast<uint16_t*>(reinterpret_cast<uint64_t*>(smem_raw) + (size_t)FOLD_WARPS * WCAP) +
                    (size_t)warp * FOLD_CAP;
-  for (int64_t pix = (int64_t)blockIdx.x * FOLD_WARPS + warp; pix < npix; pix += (int64_t)gridDim.x * FOLD_WARPS) {
+  const int64_t nq = FROM_LIST ? counters[CNT_DEFER] : npix;
+  for (int64_t qi = (int64_t)blockIdx.x * FOLD_WARPS + warp; qi < nq; qi += (int64_t)gridDim.x * FOLD_WARPS) {
+    const int64_t pix = FROM_LIST ? (int64_t)defer[qi] : qi;
     const int64_t base = off[pix];
     const int n = (int)(off[pix + 1] - base);
     if (n == 0) continue;
     const uint32_t* S = perm + base;
-    if (n > FOLD_CAP) {   // rare: pass through, re-keyed by the target node
+    if (!FROM_LIST && n > COARSEN_CACHE) {
+      if (lane == 0) defer[atomicAdd((unsigned long long*)&counters[CNT_DEFER], 1ull)] = (int32_t)pix;
+      continue;
+    }
+    if (FROM_LIST && n > FOLD_CAP) {   // rare: pass through, re-keyed by the target node
       for (int k0 = 0; k0 < n; k0 += 32) {
         const int k = k0 + (int)lane;
         const int64_t slot = warp_append(&counters[CNT_AGG_OUT], k < n ? 1 : 0);
@@ -874,7 +886,7 @@ __global__ void __launch_bounds__(FOLD_WARPS * 32) k_coarsen(const rc_seg* __res
       }
       continue;
     }
-    if (n <= 512) {
+    if (!FROM_LIST) {
       RunCache C{reinterpret_cast<uint32_t*>(keys), reinterpret_cast<float*>(keys) + 512,
                  reinterpret_cast<float*>(keys) + 1024, reinterpret_cast<int32_t*>(keys) + 1536};
       if (n <= 64) sort_pixel_cache<2>(recs, S, n, leaf_node, key_base, C);
@@ -1095,18 +1107,23 @@ cudaError_t launch_scatter_rec(const rc_seg* segs, int64_t n, const int64_t* off
 
 cudaError_t launch_coarsen(const rc_seg* recs, const uint32_t* perm, const int64_t* off, int64_t npix,
                            const int32_t* node_first, const int32_t* leaf_node, uint32_t key_base, float tau, rc_seg* out,
-                           int64_t out_cap, int64_t* counters, int max_grid, cudaStream_t s) {
+                           int64_t out_cap, int32_t* defer, int64_t* counters, int max_grid, cudaStream_t s) {
   static bool attr = false;
-  size_t smem = (size_t)FOLD_WARPS * FOLD_CAP * (sizeof(uint64_t) + sizeof(uint16_t));
+  const size_t smem1 = (size_t)FOLD_WARPS * COARSEN_CACHE * 2 * sizeof(uint64_t);
+  const size_t smem2 = (size_t)FOLD_WARPS * FOLD_CAP * (sizeof(uint64_t) + sizeof(uint16_t));
   if (!attr) {
-    cudaError_t e = cudaFuncSetAttribute(k_coarsen, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    cudaError_t e = cudaFuncSetAttribute(k_coarsen<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem2);
     if (e != cudaSuccess) return e;
     attr = true;
   }
+  cudaError_t e = cudaMemsetAsync(counters + CNT_DEFER, 0, sizeof(int64_t), s);
+  if (e != cudaSuccess) return e;
   int grid = (int)std::min<int64_t>((npix + FOLD_WARPS - 1) / FOLD_WARPS, (int64_t)max_grid);
-  k_coarsen<<<grid, FOLD_WARPS * 32, smem, s>>>(recs, perm, off, npix, node_first, leaf_node, key_base, tau, out,
-                                                out_cap, counters);
-  ++g_launches;
+  k_coarsen<false><<<grid, FOLD_WARPS * 32, smem1, s>>>(recs, perm, off, npix, node_first, leaf_node, key_base, tau,
+                                                        out, out_cap, defer, counters);
+  k_coarsen<true><<<std::min(grid, 296), FOLD_WARPS * 32, smem2, s>>>(recs, perm, off, npix, node_first, leaf_node,
+                                                                      key_base, tau, out, out_cap, defer, counters);
+  g_launches += 2;
   return cudaGetLastError();
 }
 

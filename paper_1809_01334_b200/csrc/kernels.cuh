@@ -30,7 +30,7 @@ size_t cast_curved_scratch_per_cta();
 int cast_curved_ctas_per_sm();
 cudaError_t launch_coarsen(const rc_seg* recs, const uint32_t* perm, const int64_t* off, int64_t npix,
                            const int32_t* node_first, const int32_t* leaf_node, uint32_t key_base, float tau, rc_seg* out,
-                           int64_t out_cap, int64_t* counters, int max_grid, cudaStream_t s);
+                           int64_t out_cap, int32_t* defer, int64_t* counters, int max_grid, cudaStream_t s);
 cudaError_t launch_pack(const rc_seg* segs, const int64_t* nseg_p, int W, int tw, int th, int tiles_x, int nranks,
                         int64_t* counts, const int64_t* dest_off, int64_t* cursor, rc_seg* out, int grid, bool count,
                         cudaStream_t s);

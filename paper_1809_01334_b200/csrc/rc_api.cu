@@ -821,6 +821,7 @@ static rc_status aggregate_to(rc_forest* f, int level, cudaStream_t s) {
   CU(scan_exclusive<int32_t>(f->d_pix_cnt, f->d_pix_off, npix, f->d_scan_tmp, s));
   CU(cudaMemsetAsync(f->d_pix_cnt, 0, sizeof(int32_t) * npix, s));
   if (nrec > 0) CU(launch_scatter(f->d_segs, nrec, f->d_pix_off, f->d_pix_cnt, f->d_perm, grid, s));
+  CU(grow(&f->d_defer, &f->defer_cap, std::max<int64_t>(npix, 1)));   // pixels with > 512 records
   const int32_t* leaf_node = nullptr;   // node of every leaf at the target level
   CU(build_leaf_node(f, level, s, &leaf_node));
   // output buffer: half the input first for one cycle, a quarter for several
@@ -833,7 +834,8 @@ static rc_status aggregate_to(rc_forest* f, int level, cudaStream_t s) {
     CU(cudaMemsetAsync(f->d_counters + CNT_AGG_OUT, 0, sizeof(int64_t), s));
     CU(cudaMemsetAsync(f->d_counters + CNT_OVERFLOW, 0, sizeof(int64_t), s));
     CU(launch_coarsen(f->d_segs, f->d_perm, f->d_pix_off, npix, f->d_node_first[level], leaf_node,
-                      (uint32_t)f->first_global, 1e-6f, f->d_segs2, f->seg2_cap, f->d_counters, sm_count() * 16, s));
+                      (uint32_t)f->first_global, 1e-6f, f->d_segs2, f->seg2_cap, f->d_defer, f->d_counters,
+                      sm_count() * 16, s));
     CU(cudaMemcpyAsync(&nout, f->d_counters + CNT_AGG_OUT, sizeof(int64_t), cudaMemcpyDeviceToHost, s));
     CU(cudaStreamSynchronize(s));
     if (nout <= f->seg2_cap) break;
