@@ -697,6 +697,104 @@ __device__ __forceinline__ bool fold_pixel_reg(const rc_seg* __restrict__ recs, 
   return true;
 }
 
+#ifndef FOLD_PACKED
+#define FOLD_PACKED 1   // 1: sort one 64-bit word per record (alpha, low key bits, bucket position)
+#endif
+// Keys only: the warp bitonic network of warp_sort_blocked without a payload.
+template <int E>
+__device__ __forceinline__ void warp_sort_keys(uint64_t (&key)[E]) {
+  const unsigned lane = threadIdx.x & 31;
+  constexpr int NN = 32 * E;
+#pragma unroll 1
+  for (int k = 2; k <= NN; k <<= 1) {
+#pragma unroll 1
+    for (int j = k >> 1; j >= E; j >>= 1) {
+      const int lj = j / E;
+      const bool lower = (lane & lj) == 0;
+#pragma unroll
+      for (int e = 0; e < E; ++e) {
+        const uint64_t ok = __shfl_xor_sync(0xffffffffu, key[e], lj);
+        const bool up = ((((int)lane * E + e) & k) == 0);
+        const bool take = (lower == up) ? (ok < key[e]) : (ok > key[e]);
+        key[e] = take ? ok : key[e];
+      }
+    }
+#pragma unroll
+    for (int j = E >> 1; j > 0; j >>= 1) {
+      if (j < k) {
+#pragma unroll
+        for (int e = 0; e < E; ++e) {
+          const int p = e ^ j;
+          if (p > e) {
+            const bool up = ((((int)lane * E + e) & k) == 0);
+            const uint64_t lo = key[e] < key[p] ? key[e] : key[p], hi = key[e] < key[p] ? key[p] : key[e];
+            key[e] = up ? lo : hi;
+            key[p] = up ? hi : lo;
+          }
+        }
+      }
+    }
+  }
+}
+
+// fold_pixel_reg with the record's bucket position packed into the sort key
+// (9 bits) below the low 23 bits of its node key: one word per exchange
+// instead of key + index.  The order is (alpha_near, key) as in sort_key
+// except between records of one pixel whose alpha_near are equal AND whose
+// node keys agree in the low 23 bits (then bucket position).
+template <int E>
+__device__ __forceinline__ bool fold_pixel_packed(const rc_seg* __restrict__ recs, const uint32_t* __restrict__ S,
+                                                  int64_t base, int n, float tau, Acc& acc) {
+  const unsigned lane = threadIdx.x & 31;
+  uint64_t key[E];
+#pragma unroll
+  for (int e = 0; e < E; ++e) {
+    const int i = (int)lane * E + e;
+    if (i < n) {
+      const rc_seg& r = recs[S ? S[i] : (uint32_t)(base + i)];
+      uint32_t u = __float_as_uint(r.alpha_near);
+      u = (u & 0x80000000u) ? ~u : (u | 0x80000000u);
+      key[e] = ((uint64_t)u << 32) | ((uint64_t)(r.key & 0x7FFFFFu) << 9) | (uint64_t)i;
+    } else {
+      key[e] = ~0ull;
+    }
+  }
+  warp_sort_keys<E>(key);
+  auto rid = [&](int e) -> uint32_t {
+    const int pos = (int)(key[e] & 511u);
+    return S ? S[pos] : (uint32_t)(base + pos);
+  };
+  const int last = (int)lane * E + E - 1;
+  float prev_af = __shfl_up_sync(0xffffffffu, last < n ? recs[rid(E - 1)].alpha_far : -3.4e38f, 1);
+  if (lane == 0) prev_af = -3.4e38f;
+  bool ovl = false;
+  Acc a{1.0, 0.0, 0.0, 0.0};
+#pragma unroll
+  for (int e = 0; e < E; ++e) {
+    if ((int)lane * E + e >= n) continue;
+    const rc_seg& r = recs[rid(e)];
+    ovl |= (prev_af - r.alpha_near) > tau * fmaxf(1.0f, fabsf(r.alpha_near));
+    prev_af = r.alpha_far;
+    acc_push(a, r.a, r.b[0], r.b[1], r.b[2]);
+  }
+  if (__any_sync(0xffffffffu, ovl)) return false;
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    const double A = __shfl_down_sync(0xffffffffu, a.A, o);
+    const double B0 = __shfl_down_sync(0xffffffffu, a.B0, o);
+    const double B1 = __shfl_down_sync(0xffffffffu, a.B1, o);
+    const double B2 = __shfl_down_sync(0xffffffffu, a.B2, o);
+    if ((lane & (2 * o - 1)) == 0) acc_push(a, A, B0, B1, B2);
+  }
+  acc = a;
+  return true;
+}
+#if FOLD_PACKED
+#define FOLD_PIXEL fold_pixel_packed
+#else
+#define FOLD_PIXEL fold_pixel_reg
+#endif
+
 // Two passes: CAP = 512 over every pixel (registers, 16 warps per SM); the
 // few pixels with more records are deferred to a list that the CAP = 2048
 // pass (shared-memory bitonic, else selection order) works through.
@@ -734,12 +832,12 @@ __global__ void __launch_bounds__(FOLD_WARPS * 32, CAP <= 512 ? FOLD_MINB : 1) k
     }
     Acc acc{1.0, 0.0, 0.0, 0.0};
     bool done = false;
-    if (n <= 64) done = fold_pixel_reg<2>(recs, S, base, n, tau, acc);
+    if (n <= 64) done = FOLD_PIXEL<2>(recs, S, base, n, tau, acc);
 #if FOLD_E4
-    else if (n <= 128) done = fold_pixel_reg<4>(recs, S, base, n, tau, acc);
+    else if (n <= 128) done = FOLD_PIXEL<4>(recs, S, base, n, tau, acc);
 #endif
-    else if (n <= 256) done = fold_pixel_reg<8>(recs, S, base, n, tau, acc);
-    else if (n <= 512) done = fold_pixel_reg<16>(recs, S, base, n, tau, acc);
+    else if (n <= 256) done = FOLD_PIXEL<8>(recs, S, base, n, tau, acc);
+    else if (n <= 512) done = FOLD_PIXEL<16>(recs, S, base, n, tau, acc);
     if (done) {
       // lane 0 holds the pixel's fold
     } else if (n <= CAP) {
