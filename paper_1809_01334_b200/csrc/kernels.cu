@@ -138,7 +138,7 @@ __device__ void element_bezier(const double* __restrict__ Btree, const double t0
 }
 
 #ifndef CULL_ROWWISE
-#define CULL_ROWWISE 1   // 1: R = 2 cull restricts row by row with min / max on the fly
+#define CULL_ROWWISE 0   // 1: R = 2 cull restricts row by row with min / max on the fly (A/B: 17.0 -> 19.1 ms, spills; rejected)
 #endif
 template <int R>
 __global__ void __launch_bounds__(128, CULL_ROWWISE ? 4 : 1) k_cull_curved(CamConst cc, const TreeConst* __restrict__ trees, DevLeafView L, int64_t n,
