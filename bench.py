@@ -400,7 +400,7 @@ def main():
                 "phase_ms": {k: round(v, 3) for k, v in phase_acc.items()},
                 "composite_copy": composite_copy}
         if world == 1 and not args.no_cpu_baseline:
-            stride = {1: 1, 2: 2, 3: 16, 4: 96, 5: 256, 45: 32}[args.config]   # ~10-30 s of oracle work
+            stride = {1: 1, 2: 2, 3: 16, 4: 64, 5: 128, 45: 32}[args.config]   # oracle cull of all leaves is a fixed ~40 s (C4)
             sc_cpu = scene_to_host(scene)
             cb = cpu_baseline(sc_cpu, stride)
             line["cpu_baseline"] = {k: cb[k] for k in ("value", "unit", "cores", "kind", "sample")}
