@@ -768,6 +768,9 @@ __device__ __noinline__ void prep_element_pair(float* __restrict__ sl, double* _
 #define CAST_WARPS 4        // warps per CTA
 #endif
 constexpr int CWARPS = CAST_WARPS;
+#ifndef CAST_ONESITE
+#define CAST_ONESITE 1      // 1: a single isect_chunk call site in phase 1
+#endif
 #ifndef CAST_PAIR_PREP
 #define CAST_PAIR_PREP 0    // 1: two lanes per element in phase 0 (same-box A/B: 643 -> 672 ms, rejected)
 #endif
@@ -1668,6 +1671,39 @@ __global__ void __launch_bounds__(CWARPS * 32, CAST_CTAS_PER_SM) k_cast_curved(C
       // intersected 32 at a time (misses no longer occupy the exact path)
       const int npairs = S.meta.pstart[U.nvis];
       int qn = 0;
+#if CAST_ONESITE
+      // one call site of the (large, inlined) isect_chunk: full batches and
+      // the tail share it (halves the phase's code, instruction-cache bound)
+      bool drained = false;
+      for (;;) {
+        if (!drained) {
+          int k = 0;
+          if (lane == 0) k = atomicAdd(&ctl.next_chunk, 1);
+          k = __shfl_sync(0xffffffffu, k, 0);
+          if (k >= nvchunks) {
+            drained = true;
+          } else {
+            const int g = k * RC_CHUNK + (int)lane;
+            const bool keep = g < npairs && prefilter_f32(S, cc, g);
+            const unsigned bal = __ballot_sync(0xffffffffu, keep);
+            if (keep) W.queue[qn + __popc(bal & ((1u << lane) - 1u))] = g;
+            qn += __popc(bal);
+            __syncwarp();
+          }
+        }
+        if (qn >= 32 || (drained && qn > 0)) {
+          const int gq = (int)lane < qn ? W.queue[lane] : -1;
+          const int rest = qn > 32 + (int)lane ? W.queue[32 + lane] : 0;
+          __syncwarp();
+          if (32 + (int)lane < qn) W.queue[lane] = rest;
+          qn = qn > 32 ? qn - 32 : 0;
+          __syncwarp();
+          isect_chunk(W, S, cc, U.nvis, U.vfirst, gq, items, &ctl.nitems, hits_pp, local_hits, face_fail);
+        } else if (drained) {
+          break;
+        }
+      }
+#else
       for (;;) {
         int k = 0;
         if (lane == 0) k = atomicAdd(&ctl.next_chunk, 1);
@@ -1694,6 +1730,7 @@ __global__ void __launch_bounds__(CWARPS * 32, CAST_CTAS_PER_SM) k_cast_curved(C
         __syncwarp();
         isect_chunk(W, S, cc, U.nvis, U.vfirst, gq, items, &ctl.nitems, hits_pp, local_hits, face_fail);
       }
+#endif
 #else
       for (;;) {
         int k = 0;
