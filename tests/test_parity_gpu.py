@@ -303,3 +303,26 @@ def test_c5_full_size_sampled():
     print(rep, "leaves", sc.num_leaves, "hit_pairs", g["hit_pairs"], "records", g["count"],
           "raw segments", g["raw_segments"])
     _check(rep)
+
+
+@pytest.mark.gpu
+def test_composite_tilings_on_one_forest():
+    """rc_composite_tiles keeps the owner's tile list on the device across calls
+    (re-uploaded when the tiling changes): composites of one forest's own records
+    under several tilings / ranks, in sequence, each equal the full composite."""
+    import torch
+    from paper_1809_01334_b200 import dist as rdist
+    from paper_1809_01334_b200 import rc
+    sc = sg.shell_uniform(3, 96, 16, gl_points=6)
+    f = rc.Forest.from_scene(sc)
+    f.camera_set(sc.camera)
+    f.cull()
+    f.cast_segments(2)
+    full = f.composite().cpu().numpy()
+    for tiles, nranks in (((4, 4), 2), ((2, 3), 3), ((4, 4), 2), ((1, 1), 1)):
+        out = {}
+        for d in range(nranks):
+            img, mine = f.composite_tiles(*tiles, nranks, d)
+            out[d] = (img.clone(), mine)
+        merged = rdist.assemble_image(out, *tiles, 96, 96).numpy()
+        assert np.abs(merged - full).max() < 1e-6, (tiles, nranks)
