@@ -529,9 +529,37 @@ __global__ void k_scatter(const rc_seg* __restrict__ segs, int64_t n, const int6
 
 // pixel-bucketed copy of the records (the composite then reads each pixel's
 // records contiguously instead of gathering them through a permutation)
+#ifndef SCATTER_ILP
+#define SCATTER_ILP 4   // records in flight per thread in k_scatter_rec (independent load/atomic/store chains)
+#endif
 __global__ void k_scatter_rec(const rc_seg* __restrict__ segs, int64_t n, const int64_t* __restrict__ off,
                               int32_t* __restrict__ cursor, rc_seg* __restrict__ out) {
-  for (int64_t s = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; s < n; s += (int64_t)gridDim.x * blockDim.x) {
+  const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+  int64_t s = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+#if SCATTER_ILP > 1
+  for (; s + (SCATTER_ILP - 1) * stride < n; s += SCATTER_ILP * stride) {
+    float4 lo[SCATTER_ILP], hi[SCATTER_ILP];
+#pragma unroll
+    for (int u = 0; u < SCATTER_ILP; ++u) {
+      const float4* src = reinterpret_cast<const float4*>(segs + s + u * stride);
+      lo[u] = __ldcs(src);
+      hi[u] = __ldcs(src + 1);
+    }
+    int64_t dst[SCATTER_ILP];
+#pragma unroll
+    for (int u = 0; u < SCATTER_ILP; ++u) {
+      const uint32_t pix = __float_as_uint(lo[u].x);
+      dst[u] = off[pix] + atomicAdd(&cursor[pix], 1);
+    }
+#pragma unroll
+    for (int u = 0; u < SCATTER_ILP; ++u) {
+      float4* d = reinterpret_cast<float4*>(out + dst[u]);
+      d[0] = lo[u];
+      d[1] = hi[u];
+    }
+  }
+#endif
+  for (; s < n; s += stride) {
     const float4* src = reinterpret_cast<const float4*>(segs + s);
     const float4 lo = __ldcs(src), hi = __ldcs(src + 1);
     const uint32_t pix = __float_as_uint(lo.x);
