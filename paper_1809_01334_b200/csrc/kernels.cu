@@ -530,7 +530,7 @@ __global__ void k_scatter(const rc_seg* __restrict__ segs, int64_t n, const int6
 // pixel-bucketed copy of the records (the composite then reads each pixel's
 // records contiguously instead of gathering them through a permutation)
 #ifndef SCATTER_ILP
-#define SCATTER_ILP 4   // records in flight per thread in k_scatter_rec (independent load/atomic/store chains)
+#define SCATTER_ILP 1   // records in flight per thread in k_scatter_rec (A/B: 4 -> 17.9 ms vs 1 -> 16.0 ms bucketing, rejected)
 #endif
 __global__ void k_scatter_rec(const rc_seg* __restrict__ segs, int64_t n, const int64_t* __restrict__ off,
                               int32_t* __restrict__ cursor, rc_seg* __restrict__ out) {
