@@ -934,69 +934,120 @@ static int cmp_hit(const void* x, const void* y) {
   return (a->elem > b->elem) - (a->elem < b->elem);
 }
 
-static void split_hit(const orc_hit* s, double at, orc_hit* lo, orc_hit* hi) {
-  double d1 = at - s->alpha_near, d2 = s->alpha_far - at, out[4];
-  *lo = *s; *hi = *s;
-  lo->alpha_far = at; hi->alpha_near = at;
-  orc_split(s->a, 0.0, d1, d2, out);
-  lo->a = out[0]; hi->a = out[2];
-  for (int c = 0; c < 3; ++c) {
-    orc_split(s->a, s->b[c], d1, d2, out);
-    lo->b[c] = out[1]; hi->b[c] = out[3];
+/* The piece of segment s on [x, y] (an <= x < y <= af): Eq. segsplit
+ * applied twice -- cut at x and keep the far part, cut
+ * that at y and keep the near part. */
+static orc_hit sub_hit(const orc_hit* s, double x, double y) {
+  orc_hit p = *s;
+  double out[4];
+  if (x > s->alpha_near) {          /* far part of the cut at x */
+    orc_split(p.a, 0.0, x - p.alpha_near, p.alpha_far - x, out);
+    double a_far = out[2];
+    for (int c = 0; c < 3; ++c) {
+      orc_split(p.a, p.b[c], x - p.alpha_near, p.alpha_far - x, out);
+      p.b[c] = out[3];
+    }
+    p.a = a_far;
+    p.alpha_near = x;
   }
+  if (y < p.alpha_far) {            /* near part of the cut at y */
+    orc_split(p.a, 0.0, y - p.alpha_near, p.alpha_far - y, out);
+    double a_near = out[0];
+    for (int c = 0; c < 3; ++c) {
+      orc_split(p.a, p.b[c], y - p.alpha_near, p.alpha_far - y, out);
+      p.b[c] = out[1];
+    }
+    p.a = a_near;
+    p.alpha_far = y;
+  }
+  return p;
 }
 
-static void avg_hit(const orc_hit* x, const orc_hit* y, orc_hit* out) {
-  *out = *x;
-  double bb;
-  orc_average(x->a, 0.0, y->a, 0.0, &out->a, &bb);
-  for (int c = 0; c < 3; ++c) out->b[c] = 0.5 * (x->b[c] + y->b[c]);
+static int cmp_double(const void* x, const void* y) {
+  double a = *(const double*)x, b = *(const double*)y;
+  return (a > b) - (a < b);
 }
 
+/* Per-pixel fold (PAPER.md:295-301 back to front, Eq. aggregate
+ * PAPER.md:386-394) with the overlap resolution of PAPER.md:495-558 ("cutting
+ * the segments into pieces to isolate the overlapping section and then
+ * averaging the segment values in the overlapping interval"), read for any
+ * number of mutually overlapping segments as DESIGN.md D14:
+ *  - sort by (alpha_near, elem);
+ *  - a cluster is a maximal run of the sorted list in which every segment
+ *    starts more than tol = tau max(1,|alpha|) before the largest alpha_far of
+ *    the segments before it in the run (overlap beyond the tolerance, R15);
+ *  - every member of a cluster is cut (Eq. segsplit) at all end points of the
+ *    cluster; on each elementary interval between consecutive end points the
+ *    pieces covering it are averaged, geometric mean of A and arithmetic mean
+ *    of B (Eq. segaverage; for m pieces: (prod A)^(1/m), sum B / m);
+ *  - an elementary interval covered by no piece is an empty gap (identity,
+ *    PAPER.md:427). */
 void orc_fold_pixel(int n, orc_hit* segs, double tau, const double background[3], double rgba[4],
                     double ab[4]) {
   qsort(segs, n, sizeof(orc_hit), cmp_hit);
-  orc_hit* out = (orc_hit*)malloc(sizeof(orc_hit) * (3 * n + 4));
+  orc_hit* out = (orc_hit*)malloc(sizeof(orc_hit) * (4 * n + 4));
+  double* pts = (double*)malloc(sizeof(double) * (2 * n + 2));
   int m = 0;
-  if (n > 0) {
-    orc_hit cur = segs[0];
-    for (int k = 1; k < n; ++k) {
-      orc_hit nx = segs[k];
-      double tol = tau * fmax(1.0, fabs(nx.alpha_near));
-      if (nx.alpha_near >= cur.alpha_far - tol) { out[m++] = cur; cur = nx; continue; }
-      /* overlap: cut cur at nx.alpha_near */
-      orc_hit A, Bp;
-      if (nx.alpha_near - cur.alpha_near > 0) { split_hit(&cur, nx.alpha_near, &A, &Bp); out[m++] = A; }
-      else Bp = cur;
-      if (nx.alpha_far < Bp.alpha_far) {
-        orc_hit B1, B2, av;
-        split_hit(&Bp, nx.alpha_far, &B1, &B2);
-        avg_hit(&B1, &nx, &av);
-        out[m++] = av;
-        cur = B2;
-      } else {
-        orc_hit C1, C2, av;
-        if (nx.alpha_far - Bp.alpha_far > 0) split_hit(&nx, Bp.alpha_far, &C1, &C2);
-        else { C1 = nx; C2 = nx; C2.alpha_near = C2.alpha_far; C2.a = 1; C2.b[0] = C2.b[1] = C2.b[2] = 0; }
-        avg_hit(&Bp, &C1, &av);
-        out[m++] = av;
-        cur = C2;
-      }
+  int k = 0;
+  while (k < n) {
+    int j = k + 1;
+    double far = segs[k].alpha_far;
+    while (j < n && segs[j].alpha_near < far - tau * fmax(1.0, fabs(segs[j].alpha_near))) {
+      if (segs[j].alpha_far > far) far = segs[j].alpha_far;
+      ++j;
     }
-    out[m++] = cur;
+    if (j == k + 1) {                 /* no overlap: the segment as it is */
+      out[m++] = segs[k];
+      k = j;
+      continue;
+    }
+    int np = 0;
+    for (int t = k; t < j; ++t) {
+      pts[np++] = segs[t].alpha_near;
+      pts[np++] = segs[t].alpha_far;
+    }
+    qsort(pts, np, sizeof(double), cmp_double);
+    for (int q = 0; q + 1 < np; ++q) {
+      double x = pts[q], y = pts[q + 1];
+      if (!(y > x)) continue;
+      int cnt = 0;
+      double prodA = 1.0, sumB[3] = {0.0, 0.0, 0.0};
+      orc_hit first;
+      for (int t = k; t < j; ++t) {
+        if (segs[t].alpha_near <= x && y <= segs[t].alpha_far) {
+          orc_hit p = sub_hit(&segs[t], x, y);
+          if (cnt == 0) first = p;
+          prodA *= p.a;
+          for (int c = 0; c < 3; ++c) sumB[c] += p.b[c];
+          ++cnt;
+        }
+      }
+      if (cnt == 0) continue;         /* empty gap inside the cluster */
+      orc_hit av = first;
+      av.alpha_near = x;
+      av.alpha_far = y;
+      if (cnt > 1) {
+        av.a = (cnt == 2) ? sqrt(prodA) : pow(prodA, 1.0 / cnt);
+        for (int c = 0; c < 3; ++c) av.b[c] = sumB[c] / cnt;
+      }
+      out[m++] = av;
+    }
+    k = j;
   }
   /* back to front */
   double I[3] = {background[0], background[1], background[2]}, B[3] = {0, 0, 0}, T = 1.0;
-  for (int k = m - 1; k >= 0; --k) {
+  for (int q = m - 1; q >= 0; --q) {
     for (int c = 0; c < 3; ++c) {
-      I[c] = out[k].a * I[c] + out[k].b[c];
-      B[c] = out[k].a * B[c] + out[k].b[c];
+      I[c] = out[q].a * I[c] + out[q].b[c];
+      B[c] = out[q].a * B[c] + out[q].b[c];
     }
-    T = out[k].a * T;
+    T = out[q].a * T;
   }
   rgba[0] = I[0]; rgba[1] = I[1]; rgba[2] = I[2]; rgba[3] = 1.0 - T;
   if (ab) { ab[0] = T; ab[1] = B[0]; ab[2] = B[1]; ab[3] = B[2]; }
   free(out);
+  free(pts);
 }
 
 /* ======================================================================

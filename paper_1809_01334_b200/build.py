@@ -23,6 +23,8 @@ def _stale(out, deps):
 def build(force: bool = False, verbose: bool = False, defines=(), tag: str = "") -> str:
     """Compile csrc/*.cu into librc.so; `defines` + `tag` build an experiment
     variant into build_<tag>/ and librc_<tag>.so (same sources)."""
+    if defines and not tag:
+        raise ValueError("build variants with -D defines need a tag (they must not overwrite librc.so)")
     BUILD = os.path.join(HERE, "build" + (f"_{tag}" if tag else ""))
     OUT = os.path.join(HERE, f"librc_{tag}.so" if tag else "librc.so")
     os.makedirs(BUILD, exist_ok=True)

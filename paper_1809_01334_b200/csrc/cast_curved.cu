@@ -558,182 +558,6 @@ __device__ __noinline__ void prep_element_t(float* __restrict__ sl, double* __re
   af[15] = eta * 1.001f + 1e-5f;
 }
 
-// Element preparation by a PAIR of adjacent lanes (h = lane & 1): the same
-// slot as prep_element_t with the work split -- rows (r3, r2) 0..4 / 5..8 of
-// the restriction, half of the Bernstein sums of the affine model and of the
-// bounds each, combined with pair shuffles.  Every lane of the warp calls it
-// (inactive pairs with act = false) because of the shuffles and __syncwarp.
-__device__ __noinline__ void prep_element_pair(float* __restrict__ sl, double* __restrict__ org,
-                                               const TreeConst* __restrict__ trees, const DevLeafView& L, int e,
-                                               int NF, bool act) {
-  const int h = threadIdx.x & 1;
-  double M[3][3][3];
-  const double* __restrict__ Bw = nullptr;
-  double o[3] = {0.0, 0.0, 0.0};
-  if (act) {
-    const double hh = ldexp(1.0, -(int)L.level[e]);
-    Bw = trees[L.tree[e]].Bw;   // [q3][q2][q1][xyz]
-#pragma unroll
-    for (int k = 0; k < 3; ++k) {
-      const double u = ldexp((double)L.anchor[3 * (int64_t)e + k], -RC_MAXLEVEL), w = u + hh;
-#pragma unroll
-      for (int r = 0; r < 3; ++r) {
-        const double x = r == 2 ? w : u, y = r == 0 ? u : w;
-        M[k][r][0] = (1 - x) * (1 - y);
-        M[k][r][1] = (1 - x) * y + x * (1 - y);
-        M[k][r][2] = x * y;
-      }
-    }
-    // origin = point (1,1,1) (both lanes: it re-bases every point)
-#pragma unroll
-    for (int q3 = 0; q3 < 3; ++q3)
-#pragma unroll
-      for (int q2 = 0; q2 < 3; ++q2) {
-        const double w23 = M[2][1][q3] * M[1][1][q2];
-#pragma unroll
-        for (int q1 = 0; q1 < 3; ++q1) {
-          const double wq = w23 * M[0][1][q1];
-          const double* b = Bw + ((q3 * 3 + q2) * 3 + q1) * 3;
-#pragma unroll
-          for (int c = 0; c < 3; ++c) o[c] = fma(wq, b[c], o[c]);
-        }
-      }
-    if (h == 0) {
-      org[0] = o[0];
-      org[1] = o[1];
-      org[2] = o[2];
-    }
-    // rows (r3, r2) = 0..4 on lane h = 0, 5..8 on h = 1
-    const int row0 = h == 0 ? 0 : 5, row1 = h == 0 ? 5 : 9;
-    int cur3 = -1;
-    double T2[9][3];
-#pragma unroll 1
-    for (int row = row0; row < row1; ++row) {
-      const int r3 = row / 3, r2 = row % 3;
-      double m2[3];   // M[1][r2][.] by selects (no local-memory indexing)
-#pragma unroll
-      for (int q = 0; q < 3; ++q) m2[q] = r2 == 0 ? M[1][0][q] : (r2 == 1 ? M[1][1][q] : M[1][2][q]);
-      if (r3 != cur3) {
-        double m3[3];
-#pragma unroll
-        for (int q = 0; q < 3; ++q) m3[q] = r3 == 0 ? M[2][0][q] : (r3 == 1 ? M[2][1][q] : M[2][2][q]);
-#pragma unroll
-        for (int q21 = 0; q21 < 9; ++q21)
-#pragma unroll
-          for (int c = 0; c < 3; ++c) {
-            double acc = 0.0;
-#pragma unroll
-            for (int q3 = 0; q3 < 3; ++q3) acc = fma(m3[q3], Bw[(q3 * 9 + q21) * 3 + c], acc);
-            T2[q21][c] = acc;
-          }
-        cur3 = r3;
-      }
-      double T1[3][3];
-#pragma unroll
-      for (int q1 = 0; q1 < 3; ++q1)
-#pragma unroll
-        for (int c = 0; c < 3; ++c) {
-          double acc = 0.0;
-#pragma unroll
-          for (int q2 = 0; q2 < 3; ++q2) acc = fma(m2[q2], T2[q2 * 3 + q1][c], acc);
-          T1[q1][c] = acc;
-        }
-#pragma unroll
-      for (int r1 = 0; r1 < 3; ++r1) {
-        float* dst = sl + GI(row * 3 + r1);
-#pragma unroll
-        for (int c = 0; c < 3; ++c) {
-          double acc = 0.0;
-#pragma unroll
-          for (int q1 = 0; q1 < 3; ++q1) acc = fma(M[0][r1][q1], T1[q1][c], acc);
-          dst[c] = (float)(acc - o[c]);
-        }
-      }
-    }
-    for (int q = h; q < NF; q += 2) sl[SLOT_FIELD + FI(q, NF)] = __ldg(&L.field[(int64_t)e * NF + q]);
-  }
-  __syncwarp();
-  // affine model at the centre: each lane sums its rows' Bernstein coefficients
-  const float wq[3] = {0.25f, 0.5f, 0.25f}, dq[3] = {-1.0f, 0.0f, 1.0f};
-  float acc[12];
-#pragma unroll
-  for (int t = 0; t < 12; ++t) acc[t] = 0.0f;
-  const int m0 = h == 0 ? 0 : 15, m1e = h == 0 ? 15 : 27;
-  if (act) {
-#pragma unroll 1
-    for (int m = m0; m < m1e; ++m) {
-      const int a1 = m % 3, a2 = (m / 3) % 3, a3 = m / 9;
-      const float* b = sl + GI(m);
-      const float w3 = wq[a1] * wq[a2] * wq[a3];
-      const float g[3] = {dq[a1] * wq[a2] * wq[a3], wq[a1] * dq[a2] * wq[a3], wq[a1] * wq[a2] * dq[a3]};
-#pragma unroll
-      for (int c = 0; c < 3; ++c) {
-        acc[c] = fmaf(w3, b[c], acc[c]);
-#pragma unroll
-        for (int a = 0; a < 3; ++a) acc[3 + 3 * c + a] = fmaf(g[a], b[c], acc[3 + 3 * c + a]);
-      }
-    }
-  }
-#pragma unroll
-  for (int t = 0; t < 12; ++t) acc[t] += __shfl_xor_sync(0xffffffffu, acc[t], 1);
-  const float Xc[3] = {acc[0], acc[1], acc[2]};
-  float J[3][3], Ji[3][3];
-#pragma unroll
-  for (int c = 0; c < 3; ++c)
-#pragma unroll
-    for (int a = 0; a < 3; ++a) J[c][a] = acc[3 + 3 * c + a];
-  if (!inv3(J, Ji)) {
-#pragma unroll
-    for (int a = 0; a < 3; ++a)
-#pragma unroll
-      for (int b = 0; b < 3; ++b) Ji[a][b] = 0.0f;
-  }
-  float dp0 = 0.f, dp1 = 0.f, dp2 = 0.f, eta = 0.0f;
-  if (act) {
-#pragma unroll 1
-    for (int m = m0; m < m1e; ++m) {
-      const int mmv[3] = {m % 3, (m / 3) % 3, m / 9};
-      const float* b = sl + GI(m);
-      const float x0 = 0.5f * mmv[0] - 0.5f, x1 = 0.5f * mmv[1] - 0.5f, x2 = 0.5f * mmv[2] - 0.5f;
-      const float r0 = b[0] - (Xc[0] + J[0][0] * x0 + J[0][1] * x1 + J[0][2] * x2);
-      const float r1 = b[1] - (Xc[1] + J[1][0] * x0 + J[1][1] * x1 + J[1][2] * x2);
-      const float r2 = b[2] - (Xc[2] + J[2][0] * x0 + J[2][1] * x1 + J[2][2] * x2);
-      dp0 = fmaxf(dp0, fabsf(Ji[0][0] * r0 + Ji[0][1] * r1 + Ji[0][2] * r2));
-      dp1 = fmaxf(dp1, fabsf(Ji[1][0] * r0 + Ji[1][1] * r1 + Ji[1][2] * r2));
-      dp2 = fmaxf(dp2, fabsf(Ji[2][0] * r0 + Ji[2][1] * r1 + Ji[2][2] * r2));
-      const int str[3] = {1, 3, 9};
-#pragma unroll
-      for (int ax = 0; ax < 3; ++ax) {
-        if (mmv[ax] < 2) {
-          const float* b2 = sl + GI(m + str[ax]);
-          const float e0 = 2.0f * (b2[0] - b[0]), e1 = 2.0f * (b2[1] - b[1]), e2 = 2.0f * (b2[2] - b[2]);
-          const float t0 = Ji[0][0] * e0 + Ji[0][1] * e1 + Ji[0][2] * e2 - (ax == 0 ? 1.0f : 0.0f);
-          const float t1 = Ji[1][0] * e0 + Ji[1][1] * e1 + Ji[1][2] * e2 - (ax == 1 ? 1.0f : 0.0f);
-          const float t2 = Ji[2][0] * e0 + Ji[2][1] * e1 + Ji[2][2] * e2 - (ax == 2 ? 1.0f : 0.0f);
-          eta = fmaxf(eta, fmaxf(fabsf(t0), fmaxf(fabsf(t1), fabsf(t2))));
-        }
-      }
-    }
-  }
-  dp0 = fmaxf(dp0, __shfl_xor_sync(0xffffffffu, dp0, 1));
-  dp1 = fmaxf(dp1, __shfl_xor_sync(0xffffffffu, dp1, 1));
-  dp2 = fmaxf(dp2, __shfl_xor_sync(0xffffffffu, dp2, 1));
-  eta = fmaxf(eta, __shfl_xor_sync(0xffffffffu, eta, 1));
-  if (act && h == 0) {
-    float* af = sl + SLOT_AFF;
-    af[0] = Xc[0]; af[1] = Xc[1]; af[2] = Xc[2];
-#pragma unroll
-    for (int a = 0; a < 3; ++a)
-#pragma unroll
-      for (int b = 0; b < 3; ++b) af[3 + 3 * a + b] = Ji[a][b];
-    // inflate by a rounding margin relative to the element (fp32)
-    af[12] = dp0 * 1.001f + 1e-5f;
-    af[13] = dp1 * 1.001f + 1e-5f;
-    af[14] = dp2 * 1.001f + 1e-5f;
-    af[15] = eta * 1.001f + 1e-5f;
-  }
-}
-
 // ---------------------------------------------------------------------------
 // The fused segment kernel (rows a4 + a5 + a6 of SURVEY §8(a)).  Persistent
 // CTAs of CWARPS warps take fold units from a global counter; a unit is a
@@ -756,47 +580,19 @@ __device__ __noinline__ void prep_element_pair(float* __restrict__ sl, double* _
 //         float alpha_near, alpha_far; uint32 pixel; int32 visible index
 //  phase 2 (integration): warps take 32 items at a time (full warps, no idle
 //    lanes on misses) and integrate them with the N-point GL rule;
-//  phase 3 (fold, fold level >= 1): the unit's segments are sorted by
-//    (pixel, alpha_near) in shared memory (batches of SORT_CAP) and every
+//  phase 3 (fold, fold level >= 1): the unit's segments are bucketed by
+//    pixel in shared memory, ordered per pixel under a total order, and every
 //    maximal run of touching segments of one pixel (|gap| <= 1e-6 max(1,
 //    alpha)) is combined nearest-first with Eq. aggregate
 //     into one record keyed by the node: the first levels of
 //    the paper's coarsening done on chip.
 //    Without folding every segment is a record keyed by its leaf.
 // ---------------------------------------------------------------------------
-#ifndef CAST_WARPS
-#define CAST_WARPS 4        // warps per CTA
-#endif
-constexpr int CWARPS = CAST_WARPS;
-#ifndef CAST_ONESITE
-#define CAST_ONESITE 1      // 1: a single isect_chunk call site in phase 1 (A/B: kernel 643.5 -> 636.1 ms)
-#endif
-#ifndef CAST_PAIR_PREP
-#define CAST_PAIR_PREP 0    // 1: two lanes per element in phase 0 (same-box A/B: 643 -> 672 ms, rejected)
-#endif
-#ifndef CAST_OUTLINE
-#define CAST_OUTLINE 0      // 1: phase bodies as out-of-line functions (instruction-cache A/B knob)
-#endif
-#if CAST_OUTLINE
-#define PHASE_INLINE __noinline__
-#else
-#define PHASE_INLINE __forceinline__
-#endif
-#ifndef CAST_COMPACT
-#define CAST_COMPACT 1      // 1: fp32 prefilter first, the exact path only for candidates it keeps
-#endif
-#ifndef CAST_PREFETCH
-#define CAST_PREFETCH 0     // 1: software-pipelined item loads in phase 2 (A/B knob)
-#endif
-#ifndef FAST_Q
-#define FAST_Q 0.7f         // contraction bound below which a face root takes the certified fast path
-#endif
-#ifndef CAST_CTAS_PER_SM
-#define CAST_CTAS_PER_SM 3   // resident CTAs per SM (launch bounds: 168 registers, ~60 KB shared memory)
-#endif
+constexpr int CWARPS = 4;   // warps per CTA
+constexpr float FAST_Q = 0.7f;       // contraction bound below which a face root takes the certified fast path
+constexpr int CAST_CTAS_PER_SM = 3;  // resident CTAs per SM (launch bounds: 168 registers, ~72 KB shared memory)
 constexpr int MAXR = 8;                                   // face roots per (element, pixel) pair
 constexpr int ITEM_CAP = (MAXR / 2) * RC_CHUNK * RC_UNIT_CHUNKS;   // <= MAXR/2 segments per pair
-constexpr int SORT_CAP = 2048;
 constexpr int MAXT = 6 * RC_CHUNK;                        // face tasks of one chunk
 constexpr float FOLD_TAU = 1e-6f;
 constexpr int PS_N = 14;                                  // per-pixel ray state (floats)
@@ -807,13 +603,9 @@ struct WarpIsect {
   uint8_t rord[MAXR][32];   // per-lane sorted root order (1c)
   int nroots[32];
   int pw[32];               // element (unit slot) of each lane's pixel
-  int queue[64];            // packed pairs kept by the prefilter (CAST_COMPACT)
+  int queue[64];            // packed pairs kept by the fp32 prefilter
   int stats[2];             // face tasks, 2D-path tasks (flushed per unit)
   uint8_t task[MAXT];       // lane << 3 | face
-};
-struct SortSmem {
-  unsigned long long key[SORT_CAP];
-  uint16_t idx[SORT_CAP];
 };
 constexpr int PIXCAP = 4096;   // pixels of a unit's bounding rectangle for the bucket fold
 constexpr int FCAP = 4096;     // segments of a unit for the bucket fold
@@ -846,7 +638,6 @@ struct CastSmem {
   union __align__(16) {   // the slots are read with 16-byte loads
     Phase012 p;
     FoldSmem fold;
-    SortSmem sort;
   } u;
 };
 struct CastCtl {
@@ -893,13 +684,6 @@ __device__ __forceinline__ int warp_append_smem(int* counter, int want) {
   if (lane == 31 && total > 0) base = atomicAdd(counter, total);
   base = __shfl_sync(0xffffffffu, base, 31);
   return base + incl - want;
-}
-
-// monotone map of (pixel, alpha_near) to a 64-bit sort key
-__device__ __forceinline__ unsigned long long fold_key(uint32_t pix, float an) {
-  uint32_t u = __float_as_uint(an);
-  u = (u & 0x80000000u) ? ~u : (u | 0x80000000u);
-  return ((unsigned long long)pix << 32) | u;
 }
 
 __device__ __forceinline__ void push_root(WarpIsect& W, int pl, float beta, const float xi[3], int& face_fail) {
@@ -990,7 +774,7 @@ __device__ __forceinline__ int pair_element(const CastSmem& S, int g) {
   return w;
 }
 
-// Conservative fp32 version of 1a's prefilter (CAST_COMPACT): the line of
+// Conservative fp32 version of 1a's prefilter: the line of
 // pair g in xi~ coordinates must meet the element's box inflated by dp and by
 // a margin pm that covers the fp32 re-basing error; keeps every pair the
 // exact prefilter keeps.
@@ -1031,7 +815,7 @@ __device__ __forceinline__ bool prefilter_f32(const CastSmem& S, const CamConst&
   return bex >= ben;
 }
 
-__device__ PHASE_INLINE void isect_chunk(WarpIsect& W, CastSmem& S, const CamConst& cc, int nvis, int vfirst,
+__device__ __forceinline__ void isect_chunk(WarpIsect& W, CastSmem& S, const CamConst& cc, int nvis, int vfirst,
                                             int g, float4* __restrict__ items, int* s_nitems,
                                             int32_t* __restrict__ hits_pp, int& local_hits, int& face_fail) {
   const unsigned lane = threadIdx.x & 31;
@@ -1289,7 +1073,7 @@ __device__ PHASE_INLINE void isect_chunk(WarpIsect& W, CastSmem& S, const CamCon
 // iteration stops when that bound is below tol (plain s < tol when q >= 1/2).
 // scr: this thread's scratch (stride CWARPS*32 floats) for the node values
 template <int P, int N>
-__device__ PHASE_INLINE void integ_item(const float* __restrict__ gs, const CamConst& cc, float4 i0, float4 i1,
+__device__ __forceinline__ void integ_item(const float* __restrict__ gs, const CamConst& cc, float4 i0, float4 i1,
                                            float4 i2, float* __restrict__ scr, int& fails, float& a_out,
                                            float b_out[3]) {
   constexpr int ST = CWARPS * 32;
@@ -1503,15 +1287,25 @@ __device__ void fold_bucket(CastSmem& S, CastCtl& ctl, const rc_seg* __restrict_
       if (n == 0) continue;
       uint16_t* ord = F.order + o;
       if (pass == 0) {
-        // insertion sort of the pixel's slice by (alpha_near, index), in place
+        // insertion sort of the pixel's slice, in place, under the total order
+        // (alpha_near, alpha_far, visible leaf, slot): the runs, and so the
+        // records, do not depend on the order the items were produced in
         for (int t = 1; t < n; ++t) {
           const int k = ord[t];
-          const float an = F.alpha[k].x;
+          const float2 ak = F.alpha[k];
           int z = t;
           while (z > 0) {
             const int kp = ord[z - 1];
-            const float ap = F.alpha[kp].x;
-            if (!(ap > an || (ap == an && kp > k))) break;
+            const float2 ap = F.alpha[kp];
+            bool after = ap.x > ak.x;
+            if (ap.x == ak.x) {
+              if (ap.y != ak.y) after = ap.y > ak.y;
+              else {
+                const uint32_t vp = segs[kp].key, vk = segs[k].key;   // visible leaf index (tie: rare)
+                after = vp != vk ? vp > vk : kp > k;
+              }
+            }
+            if (!after) break;
             ord[z] = (uint16_t)kp;
             --z;
           }
@@ -1629,17 +1423,8 @@ __global__ void __launch_bounds__(CWARPS * 32, CAST_CTAS_PER_SM) k_cast_curved(C
       if (a1 <= U.nvis) S.meta.pstart[a1] = incl;
       if (lane == 0) S.meta.pstart[0] = 0;
     }
-#if CAST_PAIR_PREP
-    {   // two lanes per element (RC_UNIT_LEAVES <= 64 = half the CTA)
-      const int w = tid >> 1;
-      const bool act = w < U.nvis;
-      prep_element_pair(S.u.p.slot[act ? w : 0], S.meta.org[act ? w : 0], trees, L, act ? vis[U.vfirst + w] : 0, NF,
-                        act);
-    }
-#else
     for (int w = tid; w < U.nvis; w += CWARPS * 32)
       prep_element_t(S.u.p.slot[w], S.meta.org[w], trees, L, vis[U.vfirst + w], NF, true);
-#endif
     __syncthreads();
     for (int w = tid; w < U.nvis; w += CWARPS * 32) {   // chunk -> first element map
       const int a = S.meta.pstart[w], b = S.meta.pstart[w + 1];
@@ -1666,12 +1451,10 @@ __global__ void __launch_bounds__(CWARPS * 32, CAST_CTAS_PER_SM) k_cast_curved(C
       if (lane == 0) W.stats[0] = W.stats[1] = 0;
       __syncwarp();
       const int nvchunks = (S.meta.pstart[U.nvis] + RC_CHUNK - 1) / RC_CHUNK;
-#if CAST_COMPACT
       // candidates that pass the conservative fp32 prefilter are queued and
       // intersected 32 at a time (misses no longer occupy the exact path)
       const int npairs = S.meta.pstart[U.nvis];
       int qn = 0;
-#if CAST_ONESITE
       // one call site of the (large, inlined) isect_chunk: full batches and
       // the tail share it (halves the phase's code, instruction-cache bound)
       bool drained = false;
@@ -1703,44 +1486,6 @@ __global__ void __launch_bounds__(CWARPS * 32, CAST_CTAS_PER_SM) k_cast_curved(C
           break;
         }
       }
-#else
-      for (;;) {
-        int k = 0;
-        if (lane == 0) k = atomicAdd(&ctl.next_chunk, 1);
-        k = __shfl_sync(0xffffffffu, k, 0);
-        if (k >= nvchunks) break;
-        const int g = k * RC_CHUNK + (int)lane;
-        const bool keep = g < npairs && prefilter_f32(S, cc, g);
-        const unsigned bal = __ballot_sync(0xffffffffu, keep);
-        if (keep) W.queue[qn + __popc(bal & ((1u << lane) - 1u))] = g;
-        qn += __popc(bal);
-        __syncwarp();
-        if (qn >= 32) {
-          const int gq = W.queue[lane];
-          const int rest = qn > 32 + (int)lane ? W.queue[32 + lane] : 0;
-          __syncwarp();
-          if (32 + (int)lane < qn) W.queue[lane] = rest;
-          qn -= 32;
-          __syncwarp();
-          isect_chunk(W, S, cc, U.nvis, U.vfirst, gq, items, &ctl.nitems, hits_pp, local_hits, face_fail);
-        }
-      }
-      if (qn > 0) {
-        const int gq = (int)lane < qn ? W.queue[lane] : -1;
-        __syncwarp();
-        isect_chunk(W, S, cc, U.nvis, U.vfirst, gq, items, &ctl.nitems, hits_pp, local_hits, face_fail);
-      }
-#endif
-#else
-      for (;;) {
-        int k = 0;
-        if (lane == 0) k = atomicAdd(&ctl.next_chunk, 1);
-        k = __shfl_sync(0xffffffffu, k, 0);
-        if (k >= nvchunks) break;
-        isect_chunk(W, S, cc, U.nvis, U.vfirst, k * RC_CHUNK + (int)lane, items, &ctl.nitems, hits_pp,
-                    local_hits, face_fail);
-      }
-#endif
       if (lane == 0) {
         n_tasks += W.stats[0];
         n_fallback += W.stats[1];
@@ -1754,14 +1499,6 @@ __global__ void __launch_bounds__(CWARPS * 32, CAST_CTAS_PER_SM) k_cast_curved(C
     const int ubi0 = -ctl.bb[0], ubj0 = -ctl.bb[2];
     {
       const int ngroups = (nitems + 31) / 32;
-#if CAST_PREFETCH
-      // software pipeline: the next group's item is loaded before this one is integrated
-      float4 n0 = make_float4(0, 0, 0, 0), n1 = n0, n2 = n0, n3 = n0;
-      if (warp < ngroups && warp * 32 + (int)lane < nitems) {
-        const float4* it = items + 4 * (warp * 32 + (int)lane);
-        n0 = it[0]; n1 = it[1]; n2 = it[2]; n3 = it[3];
-      }
-#endif
       for (int g = warp; g < ngroups; g += CWARPS) {
         const int idx = g * 32 + (int)lane;
         const bool act = idx < nitems;
@@ -1769,23 +1506,9 @@ __global__ void __launch_bounds__(CWARPS * 32, CAST_CTAS_PER_SM) k_cast_curved(C
         uint32_t pix = 0;
         float an = 0.f, afar = 0.f;
         int v = 0;
-#if CAST_PREFETCH
-        const float4 c0 = n0, c1 = n1, c2 = n2, c3 = n3;
-        {
-          const int nidx = (g + CWARPS) * 32 + (int)lane;
-          if (nidx < nitems) {
-            const float4* it = items + 4 * nidx;
-            n0 = it[0]; n1 = it[1]; n2 = it[2]; n3 = it[3];
-          }
-        }
-#endif
         if (act) {
-#if CAST_PREFETCH
-          const float4 i0 = c0, i1 = c1, i2 = c2, i3 = c3;
-#else
           const float4* it = items + 4 * idx;
           const float4 i0 = it[0], i1 = it[1], i2 = it[2], i3 = it[3];
-#endif
           v = __float_as_int(i3.w);
           const uint32_t ij = __float_as_uint(i3.z);
           // fold: pixel packed relative to the unit's rectangle; else global j W + i
@@ -1797,7 +1520,7 @@ __global__ void __launch_bounds__(CWARPS * 32, CAST_CTAS_PER_SM) k_cast_curved(C
         }
         if (fold > 0) {
           if (act) {
-            store_seg(segs + idx, pix, an, afar, a, bb, U.key);
+            store_seg(segs + idx, pix, an, afar, a, bb, (uint32_t)v);   // key field: visible leaf (fold tie-break)
           }
         } else {
           const int64_t slot = warp_append(&counters[CNT_SEGS], act ? 1 : 0);
@@ -1822,89 +1545,25 @@ __global__ void __launch_bounds__(CWARPS * 32, CAST_CTAS_PER_SM) k_cast_curved(C
         continue;
       }
     }
-    // large units: bitonic sort by (pixel, alpha) in batches of SORT_CAP
-    for (int b0 = 0; b0 < nitems; b0 += SORT_CAP) {
-      const int n = min(SORT_CAP, nitems - b0);
-      int m = 1;
-      while (m < n) m <<= 1;
+    // large units (more segments or a wider rectangle than the bucket fold
+    // holds; none at C3-C5): every segment is its own record, keyed by the
+    // node (folding is optional: rc_aggregate / the composite combine them)
+    {
+      int tot;
+      const int per = (nitems + CWARPS * 32 - 1) / (CWARPS * 32);
+      const int k0 = min(nitems, tid * per), k1 = min(nitems, k0 + per);
+      const int ex = block_excl_scan(ctl, k1 - k0, tot);
+      if (tid == 0) ctl.base = atomicAdd((unsigned long long*)&counters[CNT_SEGS], (unsigned long long)tot);
       __syncthreads();
-      for (int k = tid; k < m; k += CWARPS * 32) {
-        S.u.sort.key[k] = k < n ? fold_key(segs[b0 + k].pixel, segs[b0 + k].alpha_near) : ~0ull;
-        S.u.sort.idx[k] = (uint16_t)k;
-      }
-      __syncthreads();
-      for (int size = 2; size <= m; size <<= 1) {
-        for (int stride = size >> 1; stride > 0; stride >>= 1) {
-          for (int k = tid; k < m; k += CWARPS * 32) {
-            const int p = k ^ stride;
-            if (p > k) {
-              const bool up = (k & size) == 0;
-              const unsigned long long ka = S.u.sort.key[k], kb = S.u.sort.key[p];
-              if ((ka > kb) == up) {
-                S.u.sort.key[k] = kb;
-                S.u.sort.key[p] = ka;
-                const uint16_t t2 = S.u.sort.idx[k];
-                S.u.sort.idx[k] = S.u.sort.idx[p];
-                S.u.sort.idx[p] = t2;
-              }
-            }
-          }
-          __syncthreads();
-        }
-      }
-      const rc_seg* bs = segs + b0;
-      // run heads: new pixel, or a gap / overlap beyond the tolerance
-      auto is_head = [&](int k) -> bool {
-        if (k == 0) return true;
-        if ((S.u.sort.key[k] >> 32) != (S.u.sort.key[k - 1] >> 32)) return true;
-        const float an2 = bs[S.u.sort.idx[k]].alpha_near, afp = bs[S.u.sort.idx[k - 1]].alpha_far;
-        return fabsf(an2 - afp) > FOLD_TAU * fmaxf(1.0f, fabsf(an2));
-      };
-      const int per = (n + CWARPS * 32 - 1) / (CWARPS * 32);
-      const int k0 = min(n, tid * per), k1 = min(n, k0 + per);
-      int nh = 0;
-      for (int k = k0; k < k1; ++k) nh += is_head(k) ? 1 : 0;
-      int incl = nh;
-#pragma unroll
-      for (int off = 1; off < 32; off <<= 1) {
-        const int y = __shfl_up_sync(0xffffffffu, incl, off);
-        if ((int)lane >= off) incl += y;
-      }
-      if (lane == 31) ctl.warp_sum[warp] = incl;
-      __syncthreads();
-      int wbase = 0, total = 0;
-#pragma unroll
-      for (int w = 0; w < CWARPS; ++w) {
-        wbase += w < warp ? ctl.warp_sum[w] : 0;
-        total += ctl.warp_sum[w];
-      }
-      if (tid == 0) ctl.base = atomicAdd((unsigned long long*)&counters[CNT_SEGS], (unsigned long long)total);
-      __syncthreads();
-      int64_t pos = (int64_t)ctl.base + wbase + incl - nh;
-      for (int k = k0; k < k1; ++k) {
-        if (!is_head(k)) continue;
-        const rc_seg& s0 = bs[S.u.sort.idx[k]];
-        double A = 1.0, B0 = 0.0, B1 = 0.0, B2 = 0.0;
-        float afr = s0.alpha_far;
-        int q = k;
-        do {
-          const rc_seg& sq = bs[S.u.sort.idx[q]];
-          B0 = fma(A, (double)sq.b[0], B0);
-          B1 = fma(A, (double)sq.b[1], B1);
-          B2 = fma(A, (double)sq.b[2], B2);
-          A *= (double)sq.a;
-          afr = sq.alpha_far;
-          ++q;
-        } while (q < n && !is_head(q));
+      int64_t pos = (int64_t)ctl.base + ex;
+      for (int k = k0; k < k1; ++k, ++pos) {
+        const rc_seg& sq = segs[k];
         if (pos < out_cap) {
-          const float bf[3] = {(float)B0, (float)B1, (float)B2};
-          const uint32_t gpix = (uint32_t)((-ctl.bb[2] + (int)(s0.pixel >> 16)) * cc.W - ctl.bb[0] +
-                                           (int)(s0.pixel & 0xffffu));
-          store_seg(out + pos, gpix, s0.alpha_near, afr, (float)A, bf, U.key);
+          const uint32_t gpix = (uint32_t)((ubj0 + (int)(sq.pixel >> 16)) * cc.W + ubi0 + (int)(sq.pixel & 0xffffu));
+          store_seg_cs(out + pos, gpix, sq.alpha_near, sq.alpha_far, sq.a, sq.b, U.key);
         } else {
           atomicAdd((unsigned long long*)&counters[CNT_OVERFLOW], 1ull);
         }
-        ++pos;
       }
     }
     if (tid == 0) atomicAdd((unsigned long long*)&counters[CNT_UNFOLDED], 1ull);

@@ -137,11 +137,8 @@ __device__ void element_bezier(const double* __restrict__ Btree, const double t0
   for (int q = 0; q < n1 * n1 * n1 * 3; ++q) B[q] = tmp[q];
 }
 
-#ifndef CULL_ROWWISE
-#define CULL_ROWWISE 0   // 1: R = 2 cull restricts row by row with min / max on the fly (A/B: 17.0 -> 19.1 ms, spills; rejected)
-#endif
 template <int R>
-__global__ void __launch_bounds__(128, CULL_ROWWISE ? 4 : 1) k_cull_curved(CamConst cc, const TreeConst* __restrict__ trees, DevLeafView L, int64_t n,
+__global__ void __launch_bounds__(128) k_cull_curved(CamConst cc, const TreeConst* __restrict__ trees, DevLeafView L, int64_t n,
                               int32_t* __restrict__ flag, Rect16* __restrict__ rect) {
   int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (e >= n) return;
@@ -151,62 +148,6 @@ __global__ void __launch_bounds__(128, CULL_ROWWISE ? 4 : 1) k_cull_curved(CamCo
   double t0[3];
   for (int k = 0; k < 3; ++k) t0[k] = ldexp((double)L.anchor[3 * e + k], -RC_MAXLEVEL);
   double lo[3] = {1e300, 1e300, 1e300}, hi[3] = {-1e300, -1e300, -1e300};
-#if CULL_ROWWISE
-  if constexpr (R == 2) {
-    // the same restriction row by row (axis 3, then 2, then 1), min / max on
-    // the fly: ~100 registers instead of two 81-double arrays
-    double M0[3][3];   // axis 1; the rows of axes 2 and 3 are formed when used
-    bz_restrict_row<2>(t0[0], t0[0] + h, M0);
-    const double* __restrict__ Bt = T.Bc;
-    auto row = [&](int k, int r, double m[3]) {   // blossom row r of axis k (bz_restrict_row<2>)
-      const double u = t0[k], v = t0[k] + h;
-      const double x = r == 2 ? v : u, y = r == 0 ? u : v;
-      m[0] = (1 - x) * (1 - y);
-      m[1] = (1 - x) * y + x * (1 - y);
-      m[2] = x * y;
-    };
-#pragma unroll 1
-    for (int r3 = 0; r3 < 3; ++r3) {
-      double m3[3];
-      row(2, r3, m3);
-      double T2[9][3];
-#pragma unroll
-      for (int q21 = 0; q21 < 9; ++q21)
-#pragma unroll
-        for (int c = 0; c < 3; ++c) {
-          double acc = 0.0;
-#pragma unroll
-          for (int q3 = 0; q3 < 3; ++q3) acc = fma(m3[q3], Bt[(q3 * 9 + q21) * 3 + c], acc);
-          T2[q21][c] = acc;
-        }
-#pragma unroll 1
-      for (int r2 = 0; r2 < 3; ++r2) {
-        double m2[3];
-        row(1, r2, m2);
-        double T1[3][3];
-#pragma unroll
-        for (int q1 = 0; q1 < 3; ++q1)
-#pragma unroll
-          for (int c = 0; c < 3; ++c) {
-            double acc = 0.0;
-#pragma unroll
-            for (int q2 = 0; q2 < 3; ++q2) acc = fma(m2[q2], T2[q2 * 3 + q1][c], acc);
-            T1[q1][c] = acc;
-          }
-#pragma unroll
-        for (int r1 = 0; r1 < 3; ++r1)
-#pragma unroll
-          for (int c = 0; c < 3; ++c) {
-            double acc = 0.0;
-#pragma unroll
-            for (int q1 = 0; q1 < 3; ++q1) acc = fma(M0[r1][q1], T1[q1][c], acc);
-            lo[c] = fmin(lo[c], acc);
-            hi[c] = fmax(hi[c], acc);
-          }
-      }
-    }
-  } else
-#endif
   {
     double B[NP * 3];
     element_bezier<R>(T.Bc, t0, h, B);
@@ -529,36 +470,10 @@ __global__ void k_scatter(const rc_seg* __restrict__ segs, int64_t n, const int6
 
 // pixel-bucketed copy of the records (the composite then reads each pixel's
 // records contiguously instead of gathering them through a permutation)
-#ifndef SCATTER_ILP
-#define SCATTER_ILP 1   // records in flight per thread in k_scatter_rec (A/B: 4 -> 17.9 ms vs 1 -> 16.0 ms bucketing, rejected)
-#endif
 __global__ void k_scatter_rec(const rc_seg* __restrict__ segs, int64_t n, const int64_t* __restrict__ off,
                               int32_t* __restrict__ cursor, rc_seg* __restrict__ out) {
   const int64_t stride = (int64_t)gridDim.x * blockDim.x;
   int64_t s = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-#if SCATTER_ILP > 1
-  for (; s + (SCATTER_ILP - 1) * stride < n; s += SCATTER_ILP * stride) {
-    float4 lo[SCATTER_ILP], hi[SCATTER_ILP];
-#pragma unroll
-    for (int u = 0; u < SCATTER_ILP; ++u) {
-      const float4* src = reinterpret_cast<const float4*>(segs + s + u * stride);
-      lo[u] = __ldcs(src);
-      hi[u] = __ldcs(src + 1);
-    }
-    int64_t dst[SCATTER_ILP];
-#pragma unroll
-    for (int u = 0; u < SCATTER_ILP; ++u) {
-      const uint32_t pix = __float_as_uint(lo[u].x);
-      dst[u] = off[pix] + atomicAdd(&cursor[pix], 1);
-    }
-#pragma unroll
-    for (int u = 0; u < SCATTER_ILP; ++u) {
-      float4* d = reinterpret_cast<float4*>(out + dst[u]);
-      d[0] = lo[u];
-      d[1] = hi[u];
-    }
-  }
-#endif
   for (; s < n; s += stride) {
     const float4* src = reinterpret_cast<const float4*>(segs + s);
     const float4 lo = __ldcs(src), hi = __ldcs(src + 1);
@@ -587,66 +502,175 @@ __device__ __forceinline__ uint64_t sort_key(const rc_seg& s) {
   return ((uint64_t)u << 32) | s.key;
 }
 
-struct Piece {
-  double an, af, a, b0, b1, b2;
-};
-__device__ __forceinline__ Piece piece_of(const rc_seg& s) {
-  return Piece{s.alpha_near, s.alpha_far, s.a, s.b[0], s.b[1], s.b[2]};
+// Total order of the records of one pixel, so that every fold is
+// deterministic: the sort key (alpha_near, key), then alpha_far,
+// a, b (float bits in order-preserving integer form), then the caller's
+// index (records equal in every field are interchangeable).
+__device__ __forceinline__ uint32_t ord_bits(float x) {
+  const uint32_t u = __float_as_uint(x);
+  return (u & 0x80000000u) ? ~u : (u | 0x80000000u);
 }
-// Eq. segsplit at alpha = at: returns near piece, far piece in *farp
-__device__ Piece split_piece(const Piece& s, double at, Piece* farp) {
-  double d = s.af - s.an, d1 = at - s.an, d2 = s.af - at;
-  Piece n1 = s, f1 = s;
-  n1.af = at;
-  f1.an = at;
-  if (s.a == 1.0 || d <= 0.0) {
-    double r1 = d > 0 ? d1 / d : 0.5, r2 = d > 0 ? d2 / d : 0.5;
-    n1.b0 = s.b0 * r1; n1.b1 = s.b1 * r1; n1.b2 = s.b2 * r1;
-    f1.b0 = s.b0 * r2; f1.b1 = s.b1 * r2; f1.b2 = s.b2 * r2;
-  } else {
-    double la = log(s.a);
-    double a1 = exp(la * d1 / d), a2 = exp(la * d2 / d);
-    double q1 = (1.0 - a1) / (1.0 - s.a), q2 = (1.0 - a2) / (1.0 - s.a);
-    n1.a = a1; f1.a = a2;
-    n1.b0 = s.b0 * q1; n1.b1 = s.b1 * q1; n1.b2 = s.b2 * q1;
-    f1.b0 = s.b0 * q2; f1.b1 = s.b1 * q2; f1.b2 = s.b2 * q2;
+__device__ __forceinline__ bool rec_tail_less(const rc_seg& x, const rc_seg& y, uint32_t ix, uint32_t iy) {
+  const float fx[5] = {x.alpha_far, x.a, x.b[0], x.b[1], x.b[2]};
+  const float fy[5] = {y.alpha_far, y.a, y.b[0], y.b[1], y.b[2]};
+#pragma unroll
+  for (int t = 0; t < 5; ++t) {
+    const uint32_t ox = ord_bits(fx[t]), oy = ord_bits(fy[t]);
+    if (ox != oy) return ox < oy;
   }
-  *farp = f1;
-  return n1;
-}
-__device__ __forceinline__ Piece avg_piece(const Piece& x, const Piece& y) {   // Eq. segaverage
-  return Piece{x.an, x.af, sqrt(x.a * y.a), 0.5 * (x.b0 + y.b0), 0.5 * (x.b1 + y.b1), 0.5 * (x.b2 + y.b2)};
+  return ix < iy;
 }
 
-// Sequential sweep with overlap resolution (single lane).
-struct Sweep {
-  Acc acc;
-  Piece cur;
-  bool have = false;
-  double tau;
-  __device__ void emit(const Piece& p) { acc_push(acc, p.a, p.b0, p.b1, p.b2); }
-  __device__ void push(Piece nx) {
-    if (!have) { cur = nx; have = true; return; }
-    double tol = tau * fmax(1.0, fabs(nx.an));
-    if (nx.an >= cur.af - tol) { emit(cur); cur = nx; return; }
-    Piece B;
-    if (nx.an > cur.an) { Piece A = split_piece(cur, nx.an, &B); emit(A); }
-    else B = cur;
-    if (nx.af < B.af) {
-      Piece B2;
-      Piece B1 = split_piece(B, nx.af, &B2);
-      emit(avg_piece(B1, nx));
-      cur = B2;
-    } else {
-      Piece C2;
-      Piece C1 = (nx.af > B.af) ? split_piece(nx, B.af, &C2) : nx;
-      if (!(nx.af > B.af)) { C2 = nx; C2.an = C2.af; C2.a = 1.0; C2.b0 = C2.b1 = C2.b2 = 0.0; }
-      emit(avg_piece(B, C1));
-      cur = C2;
+// Overlap clusters, one lane ("cutting the segments into
+// pieces to isolate the overlapping section and then averaging"; DESIGN.md
+// D14).  at(k) is the k-th record in order.  A cluster is a run of records
+// each starting more than tol = tau max(1,|alpha|) before the largest far end
+// of the run so far.  Inside a cluster the elementary intervals [x, y] are
+// visited left to right (y = the smallest member end point above x); every
+// member covering [x, y] contributes its piece in closed form -- Eq. segsplit
+// with the length fraction phi = (y - x)/(af - an): A^phi and
+// B (1 - A^phi)/(1 - A), or B phi when A = 1 -- and the m pieces are averaged
+// as in Eq. segaverage: exp(mean ln A), mean B.  Uncovered intervals are
+// empty gaps (identity).
+template <class At>
+__device__ void fold_clusters(At at, int n, float tau, Acc& acc) {
+  int k = 0;
+  while (k < n) {
+    const rc_seg& s0 = at(k);
+    double far = s0.alpha_far;
+    int j = k + 1;
+    while (j < n) {
+      const rc_seg& r = at(j);
+      if (!((double)r.alpha_near < far - (double)tau * fmax(1.0, fabs((double)r.alpha_near)))) break;
+      far = fmax(far, (double)r.alpha_far);
+      ++j;
+    }
+    if (j == k + 1) {
+      acc_push(acc, s0.a, s0.b[0], s0.b[1], s0.b[2]);
+      k = j;
+      continue;
+    }
+    double x = s0.alpha_near;   // the cluster's first start (records are in alpha_near order)
+    for (;;) {
+      double y = INFINITY;
+      for (int t = k; t < j; ++t) {
+        const rc_seg& r = at(t);
+        if (r.alpha_near > x) y = fmin(y, (double)r.alpha_near);
+        if (r.alpha_far > x) y = fmin(y, (double)r.alpha_far);
+      }
+      if (!(y < INFINITY)) break;
+      int m = 0;
+      bool opaque = false;
+      double lnA = 0.0, B0 = 0.0, B1 = 0.0, B2 = 0.0;
+      for (int t = k; t < j; ++t) {
+        const rc_seg& r = at(t);
+        if (!(r.alpha_near <= x && y <= r.alpha_far)) continue;
+        const double phi = (y - x) / ((double)r.alpha_far - (double)r.alpha_near);
+        const double a = r.a;
+        double ap, qb;
+        if (a == 1.0) {
+          ap = 1.0;
+          qb = phi;
+        } else if (a <= 0.0) {
+          ap = 0.0;
+          qb = 1.0;
+        } else {
+          ap = exp(phi * log(a));
+          qb = (1.0 - ap) / (1.0 - a);
+        }
+        if (ap > 0.0) lnA += log(ap);
+        else opaque = true;
+        B0 = fma(qb, (double)r.b[0], B0);
+        B1 = fma(qb, (double)r.b[1], B1);
+        B2 = fma(qb, (double)r.b[2], B2);
+        ++m;
+      }
+      if (m > 0) {
+        const double im = 1.0 / m;
+        acc_push(acc, opaque ? 0.0 : exp(lnA * im), B0 * im, B1 * im, B2 * im);
+      }
+      x = y;
+    }
+    k = j;
+  }
+}
+
+// Warp fold of one pixel's records in order: lane l takes the l-th
+// contiguous range; a running far end (exclusive prefix max across lanes)
+// detects overlaps beyond the tolerance.  Without overlaps the lanes fold
+// their ranges and an ordered tree reduction combines them (Eq. aggregate is
+// associative); with overlaps lane 0 resolves the clusters.
+// The result is in lane 0's acc.
+template <class At>
+__device__ void fold_sorted(At at, int n, float tau, Acc& acc) {
+  const unsigned lane = threadIdx.x & 31;
+  const int per = (n + 31) / 32;
+  const int lo = min(n, (int)lane * per), hi = min(n, lo + per);
+  float lmax = -3.4e38f;
+  for (int k = lo; k < hi; ++k) lmax = fmaxf(lmax, at(k).alpha_far);
+  float run = -3.4e38f;   // exclusive prefix max of the lanes' far ends
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    const float y = __shfl_up_sync(0xffffffffu, lmax, o);
+    if ((int)lane >= o) lmax = fmaxf(lmax, y);
+  }
+  run = __shfl_up_sync(0xffffffffu, lmax, 1);
+  if (lane == 0) run = -3.4e38f;
+  bool ovl = false;
+  Acc a{1.0, 0.0, 0.0, 0.0};
+  for (int k = lo; k < hi; ++k) {
+    const rc_seg& r = at(k);
+    ovl |= (run - r.alpha_near) > tau * fmaxf(1.0f, fabsf(r.alpha_near));
+    run = fmaxf(run, r.alpha_far);
+    acc_push(a, r.a, r.b[0], r.b[1], r.b[2]);
+  }
+  if (__any_sync(0xffffffffu, ovl)) {
+    if (lane == 0) fold_clusters(at, n, tau, acc);
+    __syncwarp();
+    return;
+  }
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    const double A = __shfl_down_sync(0xffffffffu, a.A, o);
+    const double B0 = __shfl_down_sync(0xffffffffu, a.B0, o);
+    const double B1 = __shfl_down_sync(0xffffffffu, a.B1, o);
+    const double B2 = __shfl_down_sync(0xffffffffu, a.B2, o);
+    if ((lane & (2 * o - 1)) == 0) acc_push(a, A, B0, B1, B2);
+  }
+  acc = a;
+}
+
+// Warp bitonic sort of m (power of two) (key, idx) pairs in shared memory
+// under the total order above; entries with idx >= n are padding (+inf).
+template <class Rec>
+__device__ void warp_sort_smem(uint64_t* keys, uint16_t* idxs, int n, int m, Rec rec) {
+  const unsigned lane = threadIdx.x & 31;
+  auto less = [&](uint64_t ka, uint16_t ia, uint64_t kb, uint16_t ib) -> bool {
+    if (ia >= n) return false;
+    if (ib >= n) return true;
+    if (ka != kb) return ka < kb;
+    return rec_tail_less(rec(ia), rec(ib), ia, ib);
+  };
+  for (int size = 2; size <= m; size <<= 1) {
+    for (int stride = size >> 1; stride > 0; stride >>= 1) {
+      for (int k = lane; k < m; k += 32) {
+        const int p = k ^ stride;
+        if (p > k) {
+          const bool up = (k & size) == 0;
+          const uint64_t ka = keys[k], kb = keys[p];
+          const uint16_t ia = idxs[k], ib = idxs[p];
+          if (less(kb, ib, ka, ia) == up) {
+            keys[k] = kb;
+            keys[p] = ka;
+            idxs[k] = ib;
+            idxs[p] = ia;
+          }
+        }
+      }
+      __syncwarp();
     }
   }
-  __device__ void finish() { if (have) emit(cur); have = false; }
-};
+}
 
 constexpr int FOLD_WARPS = 4;
 constexpr int FOLD_CAP = 2048;   // records per pixel sorted in shared memory
@@ -655,9 +679,6 @@ constexpr int FOLD_CAP = 2048;   // records per pixel sorted in shared memory
 // layout i = lane E + e, ascending.  Stage loops are not unrolled (code size:
 // the per-pixel kernels were instruction-cache bound); only the element loops
 // and the in-register distances (j < E) are static.
-#ifndef FOLD_E4
-#define FOLD_E4 1   // 1: a 128-record register bucket in k_fold / k_coarsen (C4's pixels hold ~115 records)
-#endif
 template <int E>
 __device__ __forceinline__ void warp_sort_blocked(uint64_t (&key)[E], uint32_t (&id)[E]) {
   const unsigned lane = threadIdx.x & 31;
@@ -711,11 +732,10 @@ struct RunCache {
 };
 
 template <int E>
-__device__ __forceinline__ void sort_pixel_cache(const rc_seg* __restrict__ recs, const uint32_t* __restrict__ S,
+__device__ __forceinline__ bool sort_pixel_cache(const rc_seg* __restrict__ recs, const uint32_t* __restrict__ S,
                                                  int n, const int32_t* __restrict__ leaf_node, uint32_t key_base,
                                                  RunCache C) {
   const unsigned lane = threadIdx.x & 31;
-  constexpr int NN = 32 * E;
   uint64_t key[E];
   uint32_t id[E];
 #pragma unroll
@@ -725,6 +745,17 @@ __device__ __forceinline__ void sort_pixel_cache(const rc_seg* __restrict__ recs
     key[e] = i < n ? sort_key(recs[id[e]]) : ~0ull;
   }
   warp_sort_blocked<E>(key, id);
+  // equal sort keys: the register order is not total -> the caller defers the pixel
+  uint64_t prev_key = __shfl_up_sync(0xffffffffu, key[E - 1], 1);
+  if (lane == 0) prev_key = ~0ull;
+  bool tie = false;
+#pragma unroll
+  for (int e = 0; e < E; ++e) {
+    const int i = (int)lane * E + e;
+    tie |= i < n && key[e] == prev_key;
+    prev_key = key[e];
+  }
+  if (__any_sync(0xffffffffu, tie)) return false;
 #pragma unroll
   for (int e = 0; e < E; ++e) {
     const int i = (int)lane * E + e;
@@ -737,6 +768,7 @@ __device__ __forceinline__ void sort_pixel_cache(const rc_seg* __restrict__ recs
     }
   }
   __syncwarp();
+  return true;
 }
 
 // Common case of the per-pixel fold: up to 32 E records sorted by
@@ -744,8 +776,9 @@ __device__ __forceinline__ void sort_pixel_cache(const rc_seg* __restrict__ recs
 // layout i = lane E + e: in-register exchanges for distances < E, shuffles
 // beyond), then each lane folds its E consecutive records and the lanes are
 // combined by an ordered tree reduction (Eq. aggregate is associative,
-// PAPER.md:395-427).  Returns false when consecutive records overlap beyond
-// tau (the caller then cuts and averages in the sequential sweep).
+// PAPER.md:395-427).  Returns false when records overlap beyond tau or two
+// records share the sort key (the caller then sorts under the total order
+// and resolves the overlap clusters).
 template <int E>
 __device__ __forceinline__ bool fold_pixel_reg(const rc_seg* __restrict__ recs, const uint32_t* __restrict__ S,
                                                int64_t base, int n, float tau, Acc& acc) {
@@ -760,17 +793,32 @@ __device__ __forceinline__ bool fold_pixel_reg(const rc_seg* __restrict__ recs, 
     key[e] = i < n ? sort_key(recs[id[e]]) : ~0ull;
   }
   warp_sort_blocked<E>(key, id);
-  // overlap check between consecutive records, then the lane's ordered fold
-  float prev_af = __shfl_up_sync(0xffffffffu, id[E - 1] != 0xffffffffu ? recs[id[E - 1]].alpha_far : -3.4e38f, 1);
-  if (lane == 0) prev_af = -3.4e38f;
+  // overlaps beyond tau against the running far end (lane prefix max) and
+  // equal sort keys (order not total): both go to the caller's slow path
+  float lmax = -3.4e38f;
+#pragma unroll
+  for (int e = 0; e < E; ++e)
+    if (id[e] != 0xffffffffu) lmax = fmaxf(lmax, recs[id[e]].alpha_far);
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    const float y = __shfl_up_sync(0xffffffffu, lmax, o);
+    if ((int)lane >= o) lmax = fmaxf(lmax, y);
+  }
+  float run = __shfl_up_sync(0xffffffffu, lmax, 1);
+  uint64_t prev_key = __shfl_up_sync(0xffffffffu, key[E - 1], 1);
+  if (lane == 0) {
+    run = -3.4e38f;
+    prev_key = ~0ull;
+  }
   bool ovl = false;
   Acc a{1.0, 0.0, 0.0, 0.0};
 #pragma unroll
   for (int e = 0; e < E; ++e) {
     if (id[e] == 0xffffffffu) continue;
     const rc_seg& r = recs[id[e]];
-    ovl |= (prev_af - r.alpha_near) > tau * fmaxf(1.0f, fabsf(r.alpha_near));
-    prev_af = r.alpha_far;
+    ovl |= (run - r.alpha_near) > tau * fmaxf(1.0f, fabsf(r.alpha_near)) || key[e] == prev_key;
+    run = fmaxf(run, r.alpha_far);
+    prev_key = key[e];
     acc_push(a, r.a, r.b[0], r.b[1], r.b[2]);
   }
   if (__any_sync(0xffffffffu, ovl)) return false;
@@ -786,112 +834,15 @@ __device__ __forceinline__ bool fold_pixel_reg(const rc_seg* __restrict__ recs, 
   return true;
 }
 
-#ifndef FOLD_PACKED
-#define FOLD_PACKED 0   // 1: sort one 64-bit word per record (alpha, low key bits, bucket position); A/B 25.4 -> 29.8 ms, rejected
-#endif
-// Keys only: the warp bitonic network of warp_sort_blocked without a payload.
-template <int E>
-__device__ __forceinline__ void warp_sort_keys(uint64_t (&key)[E]) {
-  const unsigned lane = threadIdx.x & 31;
-  constexpr int NN = 32 * E;
-#pragma unroll 1
-  for (int k = 2; k <= NN; k <<= 1) {
-#pragma unroll 1
-    for (int j = k >> 1; j >= E; j >>= 1) {
-      const int lj = j / E;
-      const bool lower = (lane & lj) == 0;
-#pragma unroll
-      for (int e = 0; e < E; ++e) {
-        const uint64_t ok = __shfl_xor_sync(0xffffffffu, key[e], lj);
-        const bool up = ((((int)lane * E + e) & k) == 0);
-        const bool take = (lower == up) ? (ok < key[e]) : (ok > key[e]);
-        key[e] = take ? ok : key[e];
-      }
-    }
-#pragma unroll
-    for (int j = E >> 1; j > 0; j >>= 1) {
-      if (j < k) {
-#pragma unroll
-        for (int e = 0; e < E; ++e) {
-          const int p = e ^ j;
-          if (p > e) {
-            const bool up = ((((int)lane * E + e) & k) == 0);
-            const uint64_t lo = key[e] < key[p] ? key[e] : key[p], hi = key[e] < key[p] ? key[p] : key[e];
-            key[e] = up ? lo : hi;
-            key[p] = up ? hi : lo;
-          }
-        }
-      }
-    }
-  }
-}
-
-// fold_pixel_reg with the record's bucket position packed into the sort key
-// (9 bits) below the low 23 bits of its node key: one word per exchange
-// instead of key + index.  The order is (alpha_near, key) as in sort_key
-// except between records of one pixel whose alpha_near are equal AND whose
-// node keys agree in the low 23 bits (then bucket position).
-template <int E>
-__device__ __forceinline__ bool fold_pixel_packed(const rc_seg* __restrict__ recs, const uint32_t* __restrict__ S,
-                                                  int64_t base, int n, float tau, Acc& acc) {
-  const unsigned lane = threadIdx.x & 31;
-  uint64_t key[E];
-#pragma unroll
-  for (int e = 0; e < E; ++e) {
-    const int i = (int)lane * E + e;
-    if (i < n) {
-      const rc_seg& r = recs[S ? S[i] : (uint32_t)(base + i)];
-      uint32_t u = __float_as_uint(r.alpha_near);
-      u = (u & 0x80000000u) ? ~u : (u | 0x80000000u);
-      key[e] = ((uint64_t)u << 32) | ((uint64_t)(r.key & 0x7FFFFFu) << 9) | (uint64_t)i;
-    } else {
-      key[e] = ~0ull;
-    }
-  }
-  warp_sort_keys<E>(key);
-  auto rid = [&](int e) -> uint32_t {
-    const int pos = (int)(key[e] & 511u);
-    return S ? S[pos] : (uint32_t)(base + pos);
-  };
-  const int last = (int)lane * E + E - 1;
-  float prev_af = __shfl_up_sync(0xffffffffu, last < n ? recs[rid(E - 1)].alpha_far : -3.4e38f, 1);
-  if (lane == 0) prev_af = -3.4e38f;
-  bool ovl = false;
-  Acc a{1.0, 0.0, 0.0, 0.0};
-#pragma unroll
-  for (int e = 0; e < E; ++e) {
-    if ((int)lane * E + e >= n) continue;
-    const rc_seg& r = recs[rid(e)];
-    ovl |= (prev_af - r.alpha_near) > tau * fmaxf(1.0f, fabsf(r.alpha_near));
-    prev_af = r.alpha_far;
-    acc_push(a, r.a, r.b[0], r.b[1], r.b[2]);
-  }
-  if (__any_sync(0xffffffffu, ovl)) return false;
-#pragma unroll
-  for (int o = 1; o < 32; o <<= 1) {
-    const double A = __shfl_down_sync(0xffffffffu, a.A, o);
-    const double B0 = __shfl_down_sync(0xffffffffu, a.B0, o);
-    const double B1 = __shfl_down_sync(0xffffffffu, a.B1, o);
-    const double B2 = __shfl_down_sync(0xffffffffu, a.B2, o);
-    if ((lane & (2 * o - 1)) == 0) acc_push(a, A, B0, B1, B2);
-  }
-  acc = a;
-  return true;
-}
-#if FOLD_PACKED
-#define FOLD_PIXEL fold_pixel_packed
-#else
-#define FOLD_PIXEL fold_pixel_reg
-#endif
-
-// Two passes: CAP = 512 over every pixel (registers, 16 warps per SM); the
-// few pixels with more records are deferred to a list that the CAP = 2048
-// pass (shared-memory bitonic, else selection order) works through.
-#ifndef FOLD_MINB
-#define FOLD_MINB 8   // resident k_fold<512> CTAs per SM the register budget is sized for (A/B: 4 -> 8 = 31.1 -> 25.4 ms at C4)
-#endif
-template <int CAP, bool FROM_LIST>
-__global__ void __launch_bounds__(FOLD_WARPS * 32, CAP <= 512 ? FOLD_MINB : 1) k_fold(
+// Two passes: CAP = 512 over every pixel with FOLD_WARPS warps per CTA
+// (register sort; a shared-memory sort under the total order when records
+// overlap or tie); the few pixels with more records are deferred to a list
+// that the second pass (one warp per CTA, CAP = FOLD_CAP_LIST records in
+// shared memory) works through.
+constexpr int FOLD_MINB = 8;   // resident k_fold<512> CTAs per SM the register budget is sized for (A/B: 4 -> 8 = 31.1 -> 25.4 ms at C4)
+constexpr int FOLD_CAP_LIST = 16384;   // records per pixel the composite can order (more: NaN pixel, counted)
+template <int CAP, bool FROM_LIST, int NW>
+__global__ void __launch_bounds__(NW * 32, CAP <= 512 ? FOLD_MINB : 1) k_fold(
     const rc_seg* __restrict__ recs, const uint32_t* __restrict__ perm, const int64_t* __restrict__ off, int W,
     int H, int tw, int th, const int32_t* __restrict__ my_tiles, int tiles_x, int64_t npix_out, float bg0, float bg1,
     float bg2, float tau, float* __restrict__ rgba, int32_t* __restrict__ defer, int64_t* __restrict__ counters) {
@@ -899,125 +850,58 @@ __global__ void __launch_bounds__(FOLD_WARPS * 32, CAP <= 512 ? FOLD_MINB : 1) k
   const int warp = threadIdx.x >> 5;
   const unsigned lane = threadIdx.x & 31;
   uint64_t* keys = reinterpret_cast<uint64_t*>(smem_raw) + (size_t)warp * CAP;
-  uint16_t* idxs = reinterpret_cast<uint16_t*>(reinterpret_cast<uint64_t*>(smem_raw) + (size_t)FOLD_WARPS * CAP) +
+  uint16_t* idxs = reinterpret_cast<uint16_t*>(reinterpret_cast<uint64_t*>(smem_raw) + (size_t)NW * CAP) +
                    (size_t)warp * CAP;
   const int64_t tile_px = (int64_t)tw * th;
   const int64_t nq = FROM_LIST ? counters[CNT_DEFER] : npix_out;
-  for (int64_t qi = (int64_t)blockIdx.x * FOLD_WARPS + warp; qi < nq; qi += (int64_t)gridDim.x * FOLD_WARPS) {
+  for (int64_t qi = (int64_t)blockIdx.x * NW + warp; qi < nq; qi += (int64_t)gridDim.x * NW) {
     const int64_t q = FROM_LIST ? (int64_t)defer[qi] : qi;
-    int t = (int)(q / tile_px);
-    int rem = (int)(q - (int64_t)t * tile_px);
-    int tile = my_tiles[t];
-    int tx = tile % tiles_x, ty = tile / tiles_x;
-    int i = tx * tw + rem % tw, j = ty * th + rem / tw;
-    int64_t pix = (int64_t)j * W + i;
-    int64_t base = off[pix];
-    int n = (int)(off[pix + 1] - base);
-    const uint32_t* S = perm ? perm + base : nullptr;   // S[k] = index of the pixel's k-th record
-#define RI(k) (S ? S[(k)] : (uint32_t)(base + (k)))
-    if (!FROM_LIST && n > CAP && defer) {
+    const int t = (int)(q / tile_px);
+    const int rem = (int)(q - (int64_t)t * tile_px);
+    const int tile = my_tiles[t];
+    const int tx = tile % tiles_x, ty = tile / tiles_x;
+    const int i = tx * tw + rem % tw, j = ty * th + rem / tw;
+    const int64_t pix = (int64_t)j * W + i;
+    const int64_t base = off[pix];
+    const int n = (int)(off[pix + 1] - base);
+    const uint32_t* S = perm ? perm + base : nullptr;   // S[k] = index of the pixel's k-th record (else contiguous copy)
+    auto rec = [&](int k) -> const rc_seg& { return recs[S ? S[k] : (uint32_t)(base + k)]; };
+    if (!FROM_LIST && n > CAP) {
       if (lane == 0) defer[atomicAdd((unsigned long long*)&counters[CNT_DEFER], 1ull)] = (int32_t)q;
       continue;
     }
     Acc acc{1.0, 0.0, 0.0, 0.0};
-    bool done = false;
-    if (n <= 64) done = FOLD_PIXEL<2>(recs, S, base, n, tau, acc);
-#if FOLD_E4
-    else if (n <= 128) done = FOLD_PIXEL<4>(recs, S, base, n, tau, acc);
-#endif
-    else if (n <= 256) done = FOLD_PIXEL<8>(recs, S, base, n, tau, acc);
-    else if (n <= 512) done = FOLD_PIXEL<16>(recs, S, base, n, tau, acc);
-    if (done) {
-      // lane 0 holds the pixel's fold
-    } else if (n <= CAP) {
-      int m = 1;
-      while (m < n) m <<= 1;
-      for (int k = lane; k < m; k += 32) {
-        keys[k] = k < n ? sort_key(recs[RI(k)]) : ~0ull;
-        idxs[k] = (uint16_t)k;
-      }
-      __syncwarp();
-      // bitonic sort of (key, idx), ascending
-      for (int size = 2; size <= m; size <<= 1) {
-        for (int stride = size >> 1; stride > 0; stride >>= 1) {
-          for (int k = lane; k < m; k += 32) {
-            int p = k ^ stride;
-            if (p > k) {
-              bool up = (k & size) == 0;
-              uint64_t ka = keys[k], kb = keys[p];
-              if ((ka > kb) == up) {
-                keys[k] = kb; keys[p] = ka;
-                uint16_t t2 = idxs[k]; idxs[k] = idxs[p]; idxs[p] = t2;
-              }
-            }
-          }
-          __syncwarp();
+    bool done = false, bad = false;
+    if (!FROM_LIST) {
+      if (n <= 64) done = fold_pixel_reg<2>(recs, S, base, n, tau, acc);
+      else if (n <= 128) done = fold_pixel_reg<4>(recs, S, base, n, tau, acc);
+      else if (n <= 256) done = fold_pixel_reg<8>(recs, S, base, n, tau, acc);
+      else done = fold_pixel_reg<16>(recs, S, base, n, tau, acc);
+    }
+    if (!done) {
+      if (n <= CAP) {
+        int m = 1;
+        while (m < n) m <<= 1;
+        for (int k = lane; k < m; k += 32) {
+          keys[k] = k < n ? sort_key(rec(k)) : ~0ull;
+          idxs[k] = (uint16_t)k;
         }
-      }
-      // overlap detection between consecutive records
-      bool ovl = false;
-      for (int k = lane; k + 1 < n; k += 32) {
-        const rc_seg& x = recs[RI(idxs[k])];
-        const rc_seg& y = recs[RI(idxs[k + 1])];
-        float tol = tau * fmaxf(1.0f, fabsf(y.alpha_near));
-        ovl |= (x.alpha_far - y.alpha_near) > tol;
-      }
-      if (__any_sync(0xffffffffu, ovl)) {
-        if (lane == 0) {
-          Sweep sw;
-          sw.acc = acc;
-          sw.tau = tau;
-          for (int k = 0; k < n; ++k) sw.push(piece_of(recs[RI(idxs[k])]));
-          sw.finish();
-          acc = sw.acc;
-        }
+        __syncwarp();
+        warp_sort_smem(keys, idxs, n, m, rec);
+        fold_sorted([&](int k) -> const rc_seg& { return rec(idxs[k]); }, n, tau, acc);
+        __syncwarp();
       } else {
-        // warp-parallel ordered fold: lane l folds the l-th contiguous run
-        int per = (n + 31) / 32;
-        int lo = min(n, (int)lane * per), hi = min(n, lo + per);
-        for (int k = lo; k < hi; ++k) {
-          const rc_seg& s = recs[RI(idxs[k])];
-          acc_push(acc, s.a, s.b[0], s.b[1], s.b[2]);
-        }
-#pragma unroll
-        for (int o = 1; o < 32; o <<= 1) {
-          double A = __shfl_down_sync(0xffffffffu, acc.A, o);
-          double B0 = __shfl_down_sync(0xffffffffu, acc.B0, o);
-          double B1 = __shfl_down_sync(0xffffffffu, acc.B1, o);
-          double B2 = __shfl_down_sync(0xffffffffu, acc.B2, o);
-          if ((lane & (2 * o - 1)) == 0) acc_push(acc, A, B0, B1, B2);
-        }
+        bad = true;   // more records than one warp can order (FOLD_CAP_LIST): loud NaN pixel
+        if (lane == 0) atomicAdd((unsigned long long*)&counters[CNT_BIGPIX], 1ull);
       }
-      __syncwarp();
-    } else if (lane == 0) {
-      // rare: more records than the shared-memory sort holds -> selection order
-      Sweep sw;
-      sw.acc = acc;
-      sw.tau = tau;
-      uint64_t last = 0;
-      bool first = true;
-      for (int cnt = 0; cnt < n; ++cnt) {
-        uint64_t best = ~0ull;
-        int bi = -1;
-        for (int k = 0; k < n; ++k) {
-          uint64_t kk = sort_key(recs[RI(k)]);
-          if ((first || kk > last) && kk < best) { best = kk; bi = k; }
-        }
-        if (bi < 0) break;
-        first = false;
-        last = best;
-        sw.push(piece_of(recs[RI(bi)]));
-      }
-      sw.finish();
-      acc = sw.acc;
     }
     if (lane == 0) {
-      float4 o = make_float4((float)(acc.B0 + acc.A * bg0), (float)(acc.B1 + acc.A * bg1),
-                             (float)(acc.B2 + acc.A * bg2), (float)(1.0 - acc.A));
+      const float4 o = bad ? make_float4(NAN, NAN, NAN, NAN)
+                           : make_float4((float)(acc.B0 + acc.A * bg0), (float)(acc.B1 + acc.A * bg1),
+                                         (float)(acc.B2 + acc.A * bg2), (float)(1.0 - acc.A));
       reinterpret_cast<float4*>(rgba)[q] = o;
     }
   }
-#undef RI
 }
 
 
@@ -1034,9 +918,7 @@ __global__ void __launch_bounds__(FOLD_WARPS * 32, CAP <= 512 ? FOLD_MINB : 1) k
 // records (8 KB of shared memory per warp: 6 resident CTAs per SM instead of
 // 2) and defers the others to a list that FROM_LIST = true works through.
 constexpr int COARSEN_CACHE = 512;
-#ifndef COARSEN_MINB
-#define COARSEN_MINB 6
-#endif
+constexpr int COARSEN_MINB = 6;
 template <bool FROM_LIST>
 __global__ void __launch_bounds__(FOLD_WARPS * 32, FROM_LIST ? 1 : COARSEN_MINB) k_coarsen(
     const rc_seg* __restrict__ recs, const uint32_t* __restrict__ perm, const int64_t* __restrict__ off, int64_t npix,
@@ -1076,12 +958,15 @@ __global__ void __launch_bounds__(FOLD_WARPS * 32, FROM_LIST ? 1 : COARSEN_MINB)
     if (!FROM_LIST) {
       RunCache C{reinterpret_cast<uint32_t*>(keys), reinterpret_cast<float*>(keys) + 512,
                  reinterpret_cast<float*>(keys) + 1024, reinterpret_cast<int32_t*>(keys) + 1536};
-      if (n <= 64) sort_pixel_cache<2>(recs, S, n, leaf_node, key_base, C);
-#if FOLD_E4
-      else if (n <= 128) sort_pixel_cache<4>(recs, S, n, leaf_node, key_base, C);
-#endif
-      else if (n <= 256) sort_pixel_cache<8>(recs, S, n, leaf_node, key_base, C);
-      else sort_pixel_cache<16>(recs, S, n, leaf_node, key_base, C);
+      bool sorted;
+      if (n <= 64) sorted = sort_pixel_cache<2>(recs, S, n, leaf_node, key_base, C);
+      else if (n <= 128) sorted = sort_pixel_cache<4>(recs, S, n, leaf_node, key_base, C);
+      else if (n <= 256) sorted = sort_pixel_cache<8>(recs, S, n, leaf_node, key_base, C);
+      else sorted = sort_pixel_cache<16>(recs, S, n, leaf_node, key_base, C);
+      if (!sorted) {   // tied sort keys: the list pass orders the pixel under the total order
+        if (lane == 0) defer[atomicAdd((unsigned long long*)&counters[CNT_DEFER], 1ull)] = (int32_t)pix;
+        continue;
+      }
       auto head = [&](int k) -> bool {
         return k == 0 || fabsf(C.an[k] - C.af[k - 1]) > tau * fmaxf(1.0f, fabsf(C.an[k])) || C.anc[k] != C.anc[k - 1];
       };
@@ -1121,25 +1006,7 @@ __global__ void __launch_bounds__(FOLD_WARPS * 32, FROM_LIST ? 1 : COARSEN_MINB)
         idxs[k] = (uint16_t)k;
       }
       __syncwarp();
-      for (int size = 2; size <= m; size <<= 1) {
-        for (int stride = size >> 1; stride > 0; stride >>= 1) {
-          for (int k = lane; k < m; k += 32) {
-            const int p = k ^ stride;
-            if (p > k) {
-              const bool up = (k & size) == 0;
-              const uint64_t ka = keys[k], kb = keys[p];
-              if ((ka > kb) == up) {
-                keys[k] = kb;
-                keys[p] = ka;
-                const uint16_t t2 = idxs[k];
-                idxs[k] = idxs[p];
-                idxs[p] = t2;
-              }
-            }
-          }
-          __syncwarp();
-        }
-      }
+      warp_sort_smem(keys, idxs, n, m, [&](int k) -> const rc_seg& { return recs[S[k]]; });
     }
     auto anc = [&](int k) -> int64_t {
       return (int64_t)leaf_node[recs[S[idxs[k]]].key - key_base];
@@ -1314,20 +1181,20 @@ cudaError_t launch_coarsen(const rc_seg* recs, const uint32_t* perm, const int64
   return cudaGetLastError();
 }
 
-template <int CAP, bool FROM_LIST>
+template <int CAP, bool FROM_LIST, int NW>
 static cudaError_t fold_pass(const rc_seg* recs, const uint32_t* perm, const int64_t* off, int W, int H, int tw,
                              int th, const int32_t* my_tiles, int tiles_x, int64_t npix_out, const float bg[3],
                              float tau, float* rgba, int32_t* defer, int64_t* counters, int grid, cudaStream_t s) {
   static bool attr = false;
-  const size_t smem = (size_t)FOLD_WARPS * CAP * (sizeof(uint64_t) + sizeof(uint16_t));
+  const size_t smem = (size_t)NW * CAP * (sizeof(uint64_t) + sizeof(uint16_t));
   if (!attr) {
-    cudaError_t e = cudaFuncSetAttribute(k_fold<CAP, FROM_LIST>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    cudaError_t e = cudaFuncSetAttribute(k_fold<CAP, FROM_LIST, NW>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                         (int)smem);
     if (e != cudaSuccess) return e;
     attr = true;
   }
-  k_fold<CAP, FROM_LIST><<<grid, FOLD_WARPS * 32, smem, s>>>(recs, perm, off, W, H, tw, th, my_tiles, tiles_x,
-                                                             npix_out, bg[0], bg[1], bg[2], tau, rgba, defer,
-                                                             counters);
+  k_fold<CAP, FROM_LIST, NW><<<grid, NW * 32, smem, s>>>(recs, perm, off, W, H, tw, th, my_tiles, tiles_x, npix_out,
+                                                         bg[0], bg[1], bg[2], tau, rgba, defer, counters);
   ++g_launches;
   return cudaGetLastError();
 }
@@ -1338,12 +1205,12 @@ cudaError_t launch_fold(const rc_seg* recs, const uint32_t* perm, const int64_t*
   const int grid = (int)std::min<int64_t>((npix_out + FOLD_WARPS - 1) / FOLD_WARPS, (int64_t)max_grid);
   cudaError_t e = cudaMemsetAsync(counters + CNT_DEFER, 0, sizeof(int64_t), s);
   if (e != cudaSuccess) return e;
-  e = fold_pass<512, false>(recs, perm, off, W, H, tw, th, my_tiles, tiles_x, npix_out, bg, tau, rgba, defer,
-                            counters, grid, s);
+  e = fold_pass<512, false, FOLD_WARPS>(recs, perm, off, W, H, tw, th, my_tiles, tiles_x, npix_out, bg, tau, rgba,
+                                        defer, counters, grid, s);
   if (e != cudaSuccess) return e;
   // the deferred pixels (n > 512): a fixed grid reading the list length on the device
-  return fold_pass<FOLD_CAP, true>(recs, perm, off, W, H, tw, th, my_tiles, tiles_x, npix_out, bg, tau, rgba, defer,
-                                   counters, std::min(grid, 296), s);
+  return fold_pass<FOLD_CAP_LIST, true, 1>(recs, perm, off, W, H, tw, th, my_tiles, tiles_x, npix_out, bg, tau, rgba,
+                                           defer, counters, std::min(grid, 296), s);
 }
 
 }  // namespace rc

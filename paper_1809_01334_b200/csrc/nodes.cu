@@ -110,14 +110,14 @@ cudaError_t build_node_levels(rc_forest* f, cudaStream_t s) {
   if ((e = (x)) != cudaSuccess) { \
     goto done;                      \
   }
-  TRY(dmalloc((void**)&start, sizeof(int32_t) * (n + 1)));
-  TRY(dmalloc((void**)&keep, sizeof(int32_t) * (n + 1)));
-  TRY(dmalloc((void**)&pos, sizeof(int64_t) * (n + 1)));
+  TRY(dmalloc((void**)&start, sizeof(int32_t) * (n + 1), s));
+  TRY(dmalloc((void**)&keep, sizeof(int32_t) * (n + 1), s));
+  TRY(dmalloc((void**)&pos, sizeof(int64_t) * (n + 1), s));
   for (int b = 0; b < 2; ++b) {
-    TRY(dmalloc((void**)&tree[b], sizeof(int32_t) * (n + 8)));
-    TRY(dmalloc((void**)&anchor[b], sizeof(int32_t) * 3 * (n + 8)));
-    TRY(dmalloc((void**)&level[b], sizeof(int8_t) * (n + 8)));
-    TRY(dmalloc((void**)&first[b], sizeof(int32_t) * (n + 8)));
+    TRY(dmalloc((void**)&tree[b], sizeof(int32_t) * (n + 8), s));
+    TRY(dmalloc((void**)&anchor[b], sizeof(int32_t) * 3 * (n + 8), s));
+    TRY(dmalloc((void**)&level[b], sizeof(int8_t) * (n + 8), s));
+    TRY(dmalloc((void**)&first[b], sizeof(int32_t) * (n + 8), s));
   }
   {
     f->n_nodes[0] = n;
@@ -133,7 +133,7 @@ cudaError_t build_node_levels(rc_forest* f, cudaStream_t s) {
       TRY(cudaMemcpyAsync(&next, pos + cur, sizeof(int64_t), cudaMemcpyDeviceToHost, s));
       TRY(cudaStreamSynchronize(s));
       int32_t* fo = nullptr;
-      TRY(dmalloc((void**)&fo, sizeof(int32_t) * (next + 1)));
+      TRY(dmalloc((void**)&fo, sizeof(int32_t) * (next + 1), s));
       f->d_node_first[c] = fo;
       f->n_nodes[c] = next;
       k_family_emit<<<nb(cur, 256), 256, 0, s>>>(V, cur, start, keep, pos, tree[out], anchor[out], level[out],
@@ -150,14 +150,14 @@ cudaError_t build_node_levels(rc_forest* f, cudaStream_t s) {
   }
 done:
 #undef TRY
-  dfree(start);
-  dfree(keep);
-  dfree(pos);
+  dfree(start, s);
+  dfree(keep, s);
+  dfree(pos, s);
   for (int b = 0; b < 2; ++b) {
-    dfree(tree[b]);
-    dfree(anchor[b]);
-    dfree(level[b]);
-    dfree(first[b]);
+    dfree(tree[b], s);
+    dfree(anchor[b], s);
+    dfree(level[b], s);
+    dfree(first[b], s);
   }
   return e;
 }
@@ -173,7 +173,7 @@ cudaError_t build_leaf_node(rc_forest* f, int c, cudaStream_t s, const int32_t**
   const int k = f->leaf_node_next;
   f->leaf_node_next ^= 1;
   if (!f->d_leaf_nodes[k]) {
-    cudaError_t e = dmalloc((void**)&f->d_leaf_nodes[k], sizeof(int32_t) * f->n);
+    cudaError_t e = dmalloc((void**)&f->d_leaf_nodes[k], sizeof(int32_t) * f->n, s);
     if (e != cudaSuccess) return e;
   }
   k_leaf_node<<<nb(f->n, 256), 256, 0, s>>>(f->d_node_first[c], f->n_nodes[c], f->n, f->d_leaf_nodes[k]);

@@ -45,12 +45,12 @@ extern "C" int64_t rc_launch_count(int32_t reset) {
 }
 
 template <typename T>
-static cudaError_t grow(T** p, int64_t* cap, int64_t need) {
+static cudaError_t grow(T** p, int64_t* cap, int64_t need, cudaStream_t s) {
   if (need <= *cap && *p) return cudaSuccess;
-  if (*p) dfree(*p);
+  if (*p) dfree(*p, s);
   *p = nullptr;
   int64_t c = std::max<int64_t>(need + std::min<int64_t>(need / 8, (int64_t)1 << 24), 64);   // bounded slack
-  cudaError_t e = dmalloc((void**)p, sizeof(T) * (size_t)c);
+  cudaError_t e = dmalloc((void**)p, sizeof(T) * (size_t)c, s);
   if (e == cudaSuccess) *cap = c;
   else *cap = 0;
   return e;
@@ -123,7 +123,7 @@ extern "C" rc_status rc_forest_create(const rc_forest_desc* d, void* stream, rc_
     return r;
   };
 #define ALLOC(ptr, bytes)                                        \
-  if ((e = dmalloc((void**)&(ptr), (bytes))) != cudaSuccess) \
+  if ((e = dmalloc((void**)&(ptr), (bytes), s)) != cudaSuccess) \
     return cleanup(RC_ERR_OUT_OF_MEMORY, "cudaMalloc " #ptr);
   ALLOC(f->d_anchor, sizeof(int32_t) * 3 * n);
   ALLOC(f->d_tree, sizeof(int32_t) * n);
@@ -169,9 +169,9 @@ extern "C" rc_status rc_forest_destroy(rc_forest* f) {
                   f->d_perm, f->d_send, f->d_items, f->d_leaf_nodes[0], f->d_leaf_nodes[1], f->d_ucnt, f->d_uend, f->d_units,
                   f->d_scratch, f->d_segs2, f->d_uoff, f->d_defer, f->d_sorted, f->d_tiles};
   for (void* p : ptrs)
-    if (p) dfree(p);
+    if (p) dfree(p, 0, true);
   for (int c = 0; c <= RC_NODE_LEVELS; ++c)
-    if (f->d_node_first[c]) dfree(f->d_node_first[c]);
+    if (f->d_node_first[c]) dfree(f->d_node_first[c], 0, true);
   if (f->ev0) cudaEventDestroy(f->ev0);
   if (f->ev1) cudaEventDestroy(f->ev1);
   for (int k = 0; k < 3; ++k)
@@ -490,8 +490,8 @@ extern "C" rc_status rc_cast_segments(rc_forest* f, int32_t fold_levels, void* s
   f->h_candidates = hv[2];
   const int64_t cand = hv[2], nvis = hv[0];
   const int64_t npix = (int64_t)f->cc.W * f->cc.H;
-  CU(grow(&f->d_chunk_elem, &f->chunk_cap, std::max<int64_t>(f->h_chunks, 1)));
-  CU(grow(&f->d_hits_pp, &f->pix_cap, npix));
+  CU(grow(&f->d_chunk_elem, &f->chunk_cap, std::max<int64_t>(f->h_chunks, 1), s));
+  CU(grow(&f->d_hits_pp, &f->pix_cap, npix, s));
   if (nvis > 0) CU(launch_expand(f->d_chunk_off, f->d_scan + n, nvis, f->d_chunk_elem, s));
   const bool curved = !f->all_affine;
   const uint32_t key_base = (uint32_t)f->first_global;
@@ -504,15 +504,15 @@ extern "C" rc_status rc_cast_segments(rc_forest* f, int32_t fold_levels, void* s
     if (fold_levels > 0) CU(build_leaf_node(f, fold_levels, s, &leaf_node));
     const int32_t* node_first = fold_levels > 0 ? f->d_node_first[fold_levels] : nullptr;
     if (!f->d_ucnt) {
-      CU(dmalloc((void**)&f->d_ucnt, sizeof(int32_t) * (n + 1)));
-      CU(dmalloc((void**)&f->d_uoff, sizeof(int64_t) * (n + 1)));
-      CU(dmalloc((void**)&f->d_uend, sizeof(int32_t) * (n + 1)));
+      CU(dmalloc((void**)&f->d_ucnt, sizeof(int32_t) * (n + 1), s));
+      CU(dmalloc((void**)&f->d_uoff, sizeof(int64_t) * (n + 1), s));
+      CU(dmalloc((void**)&f->d_uend, sizeof(int32_t) * (n + 1), s));
     }
     CU(launch_units(f->d_vis, f->d_scan + n, nvis, leaf_node, node_first, f->d_chunk_off, f->d_ucnt, f->d_uoff,
                     f->d_uend, f->d_scan_tmp, key_base, nullptr, false, s));
     CU(cudaMemcpyAsync(&nunits, f->d_uoff + nvis, sizeof(int64_t), cudaMemcpyDeviceToHost, s));
     CU(cudaStreamSynchronize(s));
-    CU(grow(&f->d_units, &f->units_cap, std::max<int64_t>(nunits, 1)));
+    CU(grow(&f->d_units, &f->units_cap, std::max<int64_t>(nunits, 1), s));
     CU(launch_units(f->d_vis, f->d_scan + n, nvis, leaf_node, node_first, f->d_chunk_off, f->d_ucnt, f->d_uoff,
                     f->d_uend, f->d_scan_tmp, key_base, f->d_units, true, s));
   }
@@ -520,7 +520,7 @@ extern "C" rc_status rc_cast_segments(rc_forest* f, int32_t fold_levels, void* s
   const int grid_curved = sm_count() * cast_curved_ctas_per_sm();
   if (curved && !f->d_scratch) {
     f->scratch_bytes = cast_curved_scratch_per_cta() * (size_t)grid_curved;
-    CU(dmalloc((void**)&f->d_scratch, f->scratch_bytes));
+    CU(dmalloc((void**)&f->d_scratch, f->scratch_bytes, s));
   }
   // record capacity: the previous frame's count, else an estimate; a too
   // small buffer is grown to the exact count and the cast repeated
@@ -542,7 +542,7 @@ extern "C" rc_status rc_cast_segments(rc_forest* f, int32_t fold_levels, void* s
     }
   }
   int64_t need = std::max<int64_t>(f->h_cast_total + f->h_cast_total / 8, est) + 4096;
-  CU(grow(&f->d_segs, &f->seg_cap, need));
+  CU(grow(&f->d_segs, &f->seg_cap, need, s));
   for (int attempt = 0; attempt < 2; ++attempt) {
     CU(cudaMemsetAsync(f->d_hits_pp, 0, sizeof(int32_t) * npix, s));
     CU(cudaMemsetAsync(f->d_counters + CNT_SEGS, 0, sizeof(int64_t) * 3, s));
@@ -569,7 +569,7 @@ extern "C" rc_status rc_cast_segments(rc_forest* f, int32_t fold_levels, void* s
     f->h_cast_total = c[0];
     if (c[0] <= f->seg_cap && c[1] == 0) break;
     if (attempt == 1) return fail(RC_ERR_CAPACITY, "segment records overflow after regrowth");
-    CU(grow(&f->d_segs, &f->seg_cap, c[0] + c[0] / 16 + 4096));
+    CU(grow(&f->d_segs, &f->seg_cap, c[0] + c[0] / 16 + 4096, s));
   }
   float ms = 0.0f;
   CU(cudaEventElapsedTime(&ms, f->ev0, f->ev1));
@@ -662,7 +662,7 @@ extern "C" rc_status rc_pack_tiles(rc_forest* f, const rc_tiling* t, int64_t* h_
   CU(cudaMemcpyAsync(&nseg, f->d_counters + CNT_SEGS, sizeof(int64_t), cudaMemcpyDeviceToHost, s));
   CU(cudaStreamSynchronize(s));
   nseg = std::min(nseg, f->seg_cap);
-  CU(grow(&f->d_send, &f->send_cap, std::max<int64_t>(nseg, 1)));
+  CU(grow(&f->d_send, &f->send_cap, std::max<int64_t>(nseg, 1), s));
   // counts in the counter block; [offsets(nranks+1) | cursors(nranks)] in the scan scratch
   int64_t* d_cnt = f->d_counters + CNT_SEND;
   static_assert(CNT_TOTAL >= CNT_SEND + 64, "counter space");
@@ -717,16 +717,16 @@ extern "C" rc_status rc_composite_tiles(rc_forest* f, const rc_tiling* t, const 
   const int64_t npix = (int64_t)W * H;
   // (re)allocate per-pixel arrays sized to the image
   if (!f->d_pix_cnt || f->pix_cnt_cap < npix) {
-    if (f->d_pix_cnt) dfree(f->d_pix_cnt);
-    if (f->d_pix_off) dfree(f->d_pix_off);
+    if (f->d_pix_cnt) dfree(f->d_pix_cnt, s);
+    if (f->d_pix_off) dfree(f->d_pix_off, s);
     f->d_pix_cnt = nullptr;
     f->d_pix_off = nullptr;
-    CU(dmalloc((void**)&f->d_pix_cnt, sizeof(int32_t) * npix));
-    CU(dmalloc((void**)&f->d_pix_off, sizeof(int64_t) * (npix + 1)));
+    CU(dmalloc((void**)&f->d_pix_cnt, sizeof(int32_t) * npix, s));
+    CU(dmalloc((void**)&f->d_pix_off, sizeof(int64_t) * (npix + 1), s));
     f->pix_cnt_cap = npix;
   }
   int64_t need_tmp = (int64_t)scan_tmp_size(npix + 1) + 128;
-  if (need_tmp > f->scan_tmp_cap) CU(grow(&f->d_scan_tmp, &f->scan_tmp_cap, need_tmp));
+  if (need_tmp > f->scan_tmp_cap) CU(grow(&f->d_scan_tmp, &f->scan_tmp_cap, need_tmp, s));
   if (nsrc >= (int64_t)UINT32_MAX) return fail(RC_ERR_CAPACITY, "more than 2^32 records in one composite");
   // pixel-sorted copy of the records when memory allows (contiguous reads in
   // the fold), else a permutation of record indices
@@ -736,16 +736,16 @@ extern "C" rc_status rc_composite_tiles(rc_forest* f, const rc_tiling* t, const 
     const size_t have = f->sorted_cap >= nsrc ? (size_t)-1 : 0;
     if (have || (cudaMemGetInfo(&free_b, &total_b) == cudaSuccess &&
                  free_b > (size_t)nsrc * sizeof(rc_seg) + ((size_t)2 << 30)))
-      copy = grow(&f->d_sorted, &f->sorted_cap, std::max<int64_t>(nsrc, 1)) == cudaSuccess;
+      copy = grow(&f->d_sorted, &f->sorted_cap, std::max<int64_t>(nsrc, 1), s) == cudaSuccess;
   }
   f->last_composite_copy = copy ? 1 : 0;
-  if (!copy) CU(grow(&f->d_perm, &f->perm_cap, std::max<int64_t>(nsrc, 1)));
+  if (!copy) CU(grow(&f->d_perm, &f->perm_cap, std::max<int64_t>(nsrc, 1), s));
   // the tile list lives on the device across frames: no per-frame allocation
   // or pageable copy (both stalled the host for tens of ms at times)
   const int32_t tkey[4] = {t->tiles_x, t->tiles_y, t->nranks, t->rank};
   if (memcmp(tkey, f->tiling_key, sizeof tkey) != 0) {
     const int64_t nt = std::max<int64_t>((int64_t)mine.size(), 1);
-    CU(grow(&f->d_tiles, &f->tiles_cap, nt));
+    CU(grow(&f->d_tiles, &f->tiles_cap, nt, s));
     if (f->h_tiles_cap < nt) {
       if (f->h_tiles) cudaFreeHost(f->h_tiles);
       f->h_tiles = nullptr;
@@ -777,7 +777,7 @@ extern "C" rc_status rc_composite_tiles(rc_forest* f, const rc_tiling* t, const 
   if (npix_out > 0) {
     float bg[3] = {0, 0, 0};
     if (background) memcpy(bg, background, sizeof bg);
-    CU(grow(&f->d_defer, &f->defer_cap, npix_out));
+    CU(grow(&f->d_defer, &f->defer_cap, npix_out, s));
     CU(launch_fold(copy ? f->d_sorted : src, copy ? nullptr : f->d_perm, f->d_pix_off, W, H, tw, th, d_my_tiles,
                    t->tiles_x, npix_out, bg, 1e-6f, d_rgba, f->d_defer, f->d_counters, sm_count() * 16, s));
   }
@@ -804,24 +804,24 @@ static rc_status aggregate_to(rc_forest* f, int level, cudaStream_t s) {
   const int64_t npix = (int64_t)f->cc.W * f->cc.H;
   if (nrec >= (int64_t)UINT32_MAX) return fail(RC_ERR_CAPACITY, "more than 2^32 records in one aggregation");
   if (!f->d_pix_cnt || f->pix_cnt_cap < npix) {
-    if (f->d_pix_cnt) dfree(f->d_pix_cnt);
-    if (f->d_pix_off) dfree(f->d_pix_off);
+    if (f->d_pix_cnt) dfree(f->d_pix_cnt, s);
+    if (f->d_pix_off) dfree(f->d_pix_off, s);
     f->d_pix_cnt = nullptr;
     f->d_pix_off = nullptr;
-    CU(dmalloc((void**)&f->d_pix_cnt, sizeof(int32_t) * npix));
-    CU(dmalloc((void**)&f->d_pix_off, sizeof(int64_t) * (npix + 1)));
+    CU(dmalloc((void**)&f->d_pix_cnt, sizeof(int32_t) * npix, s));
+    CU(dmalloc((void**)&f->d_pix_off, sizeof(int64_t) * (npix + 1), s));
     f->pix_cnt_cap = npix;
   }
   int64_t need_tmp = (int64_t)scan_tmp_size(npix + 1) + 128;
-  if (need_tmp > f->scan_tmp_cap) CU(grow(&f->d_scan_tmp, &f->scan_tmp_cap, need_tmp));
-  CU(grow(&f->d_perm, &f->perm_cap, std::max<int64_t>(nrec, 1)));
+  if (need_tmp > f->scan_tmp_cap) CU(grow(&f->d_scan_tmp, &f->scan_tmp_cap, need_tmp, s));
+  CU(grow(&f->d_perm, &f->perm_cap, std::max<int64_t>(nrec, 1), s));
   const int grid = sm_count() * 8;
   CU(cudaMemsetAsync(f->d_pix_cnt, 0, sizeof(int32_t) * npix, s));
   if (nrec > 0) CU(launch_hist(f->d_segs, nrec, f->d_pix_cnt, grid, s));
   CU(scan_exclusive<int32_t>(f->d_pix_cnt, f->d_pix_off, npix, f->d_scan_tmp, s));
   CU(cudaMemsetAsync(f->d_pix_cnt, 0, sizeof(int32_t) * npix, s));
   if (nrec > 0) CU(launch_scatter(f->d_segs, nrec, f->d_pix_off, f->d_pix_cnt, f->d_perm, grid, s));
-  CU(grow(&f->d_defer, &f->defer_cap, std::max<int64_t>(npix, 1)));   // pixels with > 512 records
+  CU(grow(&f->d_defer, &f->defer_cap, std::max<int64_t>(npix, 1), s));   // pixels with > 512 records
   const int32_t* leaf_node = nullptr;   // node of every leaf at the target level
   CU(build_leaf_node(f, level, s, &leaf_node));
   // output buffer: half the input first for one cycle, a quarter for several
@@ -830,7 +830,7 @@ static rc_status aggregate_to(rc_forest* f, int level, cudaStream_t s) {
   int64_t want = std::max<int64_t>(nrec / (level - f->rec_level >= 2 ? 4 : 2) + 4096, 1);
   int64_t nout = 0;
   for (int attempt = 0; attempt < 2; ++attempt) {
-    CU(grow(&f->d_segs2, &f->seg2_cap, want));
+    CU(grow(&f->d_segs2, &f->seg2_cap, want, s));
     CU(cudaMemsetAsync(f->d_counters + CNT_AGG_OUT, 0, sizeof(int64_t), s));
     CU(cudaMemsetAsync(f->d_counters + CNT_OVERFLOW, 0, sizeof(int64_t), s));
     CU(launch_coarsen(f->d_segs, f->d_perm, f->d_pix_off, npix, f->d_node_first[level], leaf_node,

@@ -184,6 +184,7 @@ enum {
   CNT_TASKS = 76,      // curved path: (pixel, face) root-finding tasks
   CNT_FALLBACK = 77,   // ... of which needed the projected-patch (2D) method
   CNT_DEFER = 78,      // composite: pixels deferred to the large-pixel pass
+  CNT_BIGPIX = 79,     // composite: pixels with more records than FOLD_CAP_LIST (written as NaN)
   CNT_TOTAL = 80
 };
 
@@ -196,8 +197,9 @@ size_t scan_tmp_size(int64_t n);
 
 namespace rc {
 cudaError_t build_node_levels(rc_forest* f, cudaStream_t s);
-cudaError_t dmalloc(void** p, size_t bytes);   // caching pool (pool.cu)
-void dfree(void* p);
+// caching pool (pool.cu): stream-ordered reuse; idle = no pending work reads p
+cudaError_t dmalloc(void** p, size_t bytes, cudaStream_t s);
+void dfree(void* p, cudaStream_t s, bool idle = false);
 void dtrim();
 cudaError_t build_leaf_node(rc_forest* f, int c, cudaStream_t s, const int32_t** out);
 template <typename Tin>

@@ -12,9 +12,11 @@ constexpr int SCAN_THREADS = 1024;
 constexpr int SCAN_ITEMS = 4;
 constexpr int SCAN_TILE = SCAN_THREADS * SCAN_ITEMS;
 
+// `in` and `out` may alias (in-place scan of int64 counts): no __restrict__ on
+// them; every thread reads its own items before it writes them.
 template <typename Tin>
-__global__ void __launch_bounds__(SCAN_THREADS) k_scan_tile(const Tin* __restrict__ in, int64_t* __restrict__ out,
-                                                             int64_t n, int64_t* __restrict__ tile_sums) {
+__global__ void __launch_bounds__(SCAN_THREADS) k_scan_tile(const Tin* in, int64_t* out, int64_t n,
+                                                             int64_t* __restrict__ tile_sums) {
   __shared__ int64_t warp_sums[SCAN_THREADS / 32];
   int64_t base = (int64_t)blockIdx.x * SCAN_TILE + (int64_t)threadIdx.x * SCAN_ITEMS;
   int64_t v[SCAN_ITEMS];

@@ -233,6 +233,9 @@ def _frame(view_dir):
     vh = vh / np.linalg.norm(vh)
     zhat = np.array([0.0, 0.0, 1.0])
     u = zhat - zhat.dot(vh) * vh
+    if np.linalg.norm(u) < 1e-9:   # view along +-z: SURVEY R3's up vector is undefined, use +y instead
+        yhat = np.array([0.0, 1.0, 0.0])
+        u = yhat - yhat.dot(vh) * vh
     u /= np.linalg.norm(u)
     t = np.cross(vh, u)
     return vh, t, u

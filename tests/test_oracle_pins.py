@@ -340,6 +340,9 @@ def test_pixel_rect_similar_triangles():
     """Centered box at depth z, axis-aligned camera: rect width from
     similar triangles p = (n/l) X/Z + (w-1)/2."""
     cam = sg.perspective_camera([0, 0, 0], [0, 0, 1.0], 40.0, 101, 101)
+    # view along +z: the frame falls back to +y as the up reference (no NaN)
+    assert np.all(np.isfinite(np.r_[cam.view, cam.right, cam.up]))
+    assert abs(np.dot(cam.right, cam.up)) < 1e-15 and abs(np.linalg.norm(cam.up) - 1) < 1e-15
     o = oracle.OracleScene(sg.Scene("x", 1, 1, sg.identity_cube_ctrl(), np.zeros((1, 3), np.int32),
                                     np.zeros(1, np.int32), np.zeros(1, np.int8), np.zeros((1, 8), np.float32),
                                     5, 1, 1, cam))
@@ -587,6 +590,43 @@ def test_overlap_cut_and_average():
     rgba, ab = oracle.fold_pixel(h)
     avg = oracle.average(s1, s2)
     assert abs(ab[0] - avg[0]) < 1e-14 and abs(ab[1] - avg[1]) < 1e-14
+
+
+def load_overlap_cases():
+    """tests/golden/overlap_cases.txt -> [(name, HIT_DTYPE segments, (A, B))]."""
+    import os
+    cases, cur = [], None
+    for line in open(os.path.join(os.path.dirname(__file__), "golden", "overlap_cases.txt")):
+        t = line.split()
+        if not t or t[0].startswith("#"):
+            continue
+        if t[0] == "case":
+            cur = [t[1], [], None]
+        elif t[0] == "seg":
+            cur[1].append(tuple(float(x) for x in t[1:5]))
+        elif t[0] == "expect":
+            cur[2] = (float(t[1]), float(t[2]))
+        elif t[0] == "end":
+            h = np.zeros(len(cur[1]), dtype=oracle.HIT_DTYPE)
+            for k, (an, af, a, b) in enumerate(cur[1]):
+                h[k]["elem"] = k
+                h[k]["alpha_near"], h[k]["alpha_far"], h[k]["a"] = an, af, a
+                h[k]["b"] = b
+                h[k]["flags"] = oracle.HIT
+            cases.append((cur[0], h, cur[2]))
+    return cases
+
+
+@pytest.mark.parametrize("case", load_overlap_cases(), ids=lambda c: c[0])
+def test_overlap_clusters_hand_evaluated(case):
+    """Nested, triple, third-before-cut, A = 1, identical and touching segments
+    (D14) against the hand-evaluated values of
+    tests/golden/overlap_cases.txt, in every input order."""
+    import itertools
+    name, h, (A, B) = case
+    for perm in itertools.permutations(range(len(h))):
+        rgba, ab = oracle.fold_pixel(h[list(perm)])
+        assert abs(ab[0] - A) < 1e-15 and np.all(np.abs(ab[1:] - B) < 1e-15), (name, ab, A, B)
 
 
 def test_c1_rule_vs_exact_discretisation():
