@@ -45,6 +45,11 @@ HIT_DTYPE = np.dtype([("elem", np.int64), ("pixel", np.int32), ("flags", np.int3
                       ("alpha_near", np.float64), ("alpha_far", np.float64), ("a", np.float64),
                       ("b", np.float64, (3,))])
 
+class Pairs_(C.Structure):
+    _fields_ = [("npix", C.c_int64), ("off", C.POINTER(C.c_int64)), ("elem", C.POINTER(C.c_int64)),
+                ("flags", C.POINTER(C.c_int32))]
+
+
 MEDIUM_FN = C.CFUNCTYPE(None, C.c_void_p, C.c_double, C.POINTER(C.c_double), C.POINTER(C.c_double))
 
 _lib = None
@@ -85,6 +90,11 @@ def lib():
                                     C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p, C.c_int32, C.c_void_p,
                                     C.c_int]
         _lib.orc_render.restype = C.c_int64
+        _lib.orc_render_ex.argtypes = [P(Scene_), P(Camera_), C.c_int, C.c_int, C.c_void_p, C.c_int64,
+                                       C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p, C.c_int, C.c_void_p,
+                                       C.c_void_p, P(Pairs_)]
+        _lib.orc_render_ex.restype = C.c_int64
+        _lib.orc_pairs_free.argtypes = [P(Pairs_)]
         _lib.orc_set_force_general.argtypes = [C.c_int]
         _lib.orc_fold_pixel.argtypes = [C.c_int, C.c_void_p, d, C.c_void_p, C.c_void_p, C.c_void_p]
     return _lib
@@ -189,6 +199,41 @@ class OracleScene:
                                  _ptr(pixels), _ptr(rgba), _ptr(nh), _ptr(na), cap,
                                  _ptr(hits) if with_hits else None, nthreads)
         return dict(pixels=pixels, rgba=rgba, nhits=nh, namb=na, hits=hits, total_hits=int(total))
+
+
+    def render_pairs(self, pixels=None, mode="exact", N=None, background=(0.0, 0.0, 0.0), nthreads=0,
+                     with_cull=True):
+        """orc_render_ex: pixel values plus, per pixel, the (elem, flags) of every
+        hit or eps-ambiguous candidate pair (CSR: pair_off[npix+1], pair_elem,
+        pair_flags) and the culled list of the same run.  mode "hits" skips the
+        integration (rgba = 0)."""
+        if pixels is None:
+            pixels = np.arange(self.W * self.H, dtype=np.int32)
+        pixels = np.ascontiguousarray(pixels, dtype=np.int32)
+        npix = pixels.shape[0]
+        N = N or self.scene.camera.gl_points
+        bg = np.ascontiguousarray(background, dtype=np.float64)
+        rgba = np.zeros((npix, 4)); nh = np.zeros(npix, dtype=np.int32); na = np.zeros(npix, dtype=np.int32)
+        n = self.anchor.shape[0]
+        vis = np.zeros(n, dtype=np.int8) if with_cull else None
+        amb = np.zeros(n, dtype=np.int8) if with_cull else None
+        pr = Pairs_()
+        m = {"exact": 0, "rule": 1, "hits": 2}[mode]
+        total = lib().orc_render_ex(C.byref(self.s), C.byref(self.c), m, N, _ptr(bg), npix, _ptr(pixels),
+                                    _ptr(rgba), _ptr(nh), _ptr(na), nthreads,
+                                    _ptr(vis) if with_cull else None, _ptr(amb) if with_cull else None,
+                                    C.byref(pr))
+        off = np.ctypeslib.as_array(pr.off, shape=(npix + 1,)).copy()
+        tot = int(off[-1])
+        elem = np.ctypeslib.as_array(pr.elem, shape=(max(tot, 1),))[:tot].copy()
+        flags = np.ctypeslib.as_array(pr.flags, shape=(max(tot, 1),))[:tot].copy()
+        lib().orc_pairs_free(C.byref(pr))
+        out = dict(pixels=pixels, rgba=rgba, nhits=nh, namb=na, total_hits=int(total), pair_off=off,
+                   pair_elem=elem, pair_flags=flags)
+        if with_cull:
+            out["visible"] = vis.astype(bool)
+            out["ambiguous"] = amb.astype(bool)
+        return out
 
 
 # ---- algebra / quadrature wrappers --------------------------------------

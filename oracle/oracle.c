@@ -1054,9 +1054,10 @@ void orc_fold_pixel(int n, orc_hit* segs, double tau, const double background[3]
  * Render a subset of pixels: brute force over every leaf whose EPS-inflated
  * rect contains the pixel (SURVEY §8(c) oracle steps 1-7).
  * ==================================================================== */
-int64_t orc_render(const orc_scene* sc, const orc_camera* cam, int mode, int N, const double background[3],
-                   int64_t npix, const int32_t* pixels, double* rgba, int32_t* nhits, int32_t* namb,
-                   int32_t cap, orc_hit* hits, int nthreads) {
+static int64_t render_core(const orc_scene* sc, const orc_camera* cam, int mode, int N, const double background[3],
+                           int64_t npix, const int32_t* pixels, double* rgba, int32_t* nhits, int32_t* namb,
+                           int32_t cap, orc_hit* hits, int nthreads, int8_t* vis_out, int8_t* amb_out,
+                           orc_pairs* pairs) {
 #ifdef _OPENMP
   if (nthreads > 0) omp_set_num_threads(nthreads);
 #endif
@@ -1066,6 +1067,17 @@ int64_t orc_render(const orc_scene* sc, const orc_camera* cam, int mode, int N, 
   int8_t* amb = (int8_t*)malloc(sc->n);
   int32_t* rects = (int32_t*)malloc(sizeof(int32_t) * 4 * sc->n);
   orc_cull(sc, cam, vis, amb, rects);
+  if (vis_out) memcpy(vis_out, vis, sc->n);
+  if (amb_out) memcpy(amb_out, amb, sc->n);
+  /* per-pixel (elem, flags) lists of every candidate with HIT or AMBIGUOUS */
+  int64_t** pe = NULL;
+  int32_t** pf = NULL;
+  int32_t* pn = NULL;
+  if (pairs) {
+    pe = (int64_t**)calloc(npix, sizeof(int64_t*));
+    pf = (int32_t**)calloc(npix, sizeof(int32_t*));
+    pn = (int32_t*)calloc(npix, sizeof(int32_t));
+  }
   int64_t* slot = (int64_t*)malloc(sizeof(int64_t) * npx);
   for (int64_t p = 0; p < npx; ++p) slot[p] = -1;
   for (int64_t q = 0; q < npix; ++q) slot[pixels[q]] = q;
@@ -1108,6 +1120,16 @@ int64_t orc_render(const orc_scene* sc, const orc_camera* cam, int mode, int N, 
       int ns = orc_intersect(sc, cam, e, i, j, 8, seg, &flags);
       if (flags & ORC_AMBIGUOUS) na++;
       if (ns > 0) nh++;
+      if (pairs && (ns > 0 || (flags & ORC_AMBIGUOUS))) {
+        if (!pe[q]) {
+          pe[q] = (int64_t*)malloc(sizeof(int64_t) * (nc + 1));
+          pf[q] = (int32_t*)malloc(sizeof(int32_t) * (nc + 1));
+        }
+        pe[q][pn[q]] = e;
+        pf[q][pn[q]] = flags | (ns > 0 ? ORC_HIT : 0);
+        pn[q]++;
+      }
+      if (mode == 2) continue;   /* hit lists only: no integration */
       if (ns == 0 && (flags & ORC_AMBIGUOUS)) {
         orc_hit hh;
         memset(&hh, 0, sizeof hh);
@@ -1132,7 +1154,8 @@ int64_t orc_render(const orc_scene* sc, const orc_camera* cam, int mode, int N, 
         fold[nf++] = hh;
       }
     }
-    orc_fold_pixel(nf, fold, TAU_OV, background, rgba + 4 * q, NULL);
+    if (mode == 2) { for (int c = 0; c < 4; ++c) rgba[4 * q + c] = 0.0; }
+    else orc_fold_pixel(nf, fold, TAU_OV, background, rgba + 4 * q, NULL);
     nhits[q] = nh;
     namb[q] = na;
     if (hits) {
@@ -1147,5 +1170,43 @@ int64_t orc_render(const orc_scene* sc, const orc_camera* cam, int mode, int N, 
     free(fold);
   }
   free(vis); free(amb); free(rects); free(slot); free(cnt); free(cand); free(fillp);
+  if (pairs) {
+    pairs->npix = npix;
+    pairs->off = (int64_t*)malloc(sizeof(int64_t) * (npix + 1));
+    pairs->off[0] = 0;
+    for (int64_t q = 0; q < npix; ++q) pairs->off[q + 1] = pairs->off[q] + pn[q];
+    int64_t tot = pairs->off[npix];
+    pairs->elem = (int64_t*)malloc(sizeof(int64_t) * (tot + 1));
+    pairs->flags = (int32_t*)malloc(sizeof(int32_t) * (tot + 1));
+    for (int64_t q = 0; q < npix; ++q) {
+      if (pn[q]) {
+        memcpy(pairs->elem + pairs->off[q], pe[q], sizeof(int64_t) * pn[q]);
+        memcpy(pairs->flags + pairs->off[q], pf[q], sizeof(int32_t) * pn[q]);
+      }
+      free(pe[q]);
+      free(pf[q]);
+    }
+    free(pe); free(pf); free(pn);
+  }
   return total_hits;
+}
+
+int64_t orc_render(const orc_scene* sc, const orc_camera* cam, int mode, int N, const double background[3],
+                   int64_t npix, const int32_t* pixels, double* rgba, int32_t* nhits, int32_t* namb,
+                   int32_t cap, orc_hit* hits, int nthreads) {
+  return render_core(sc, cam, mode, N, background, npix, pixels, rgba, nhits, namb, cap, hits, nthreads, NULL,
+                     NULL, NULL);
+}
+
+int64_t orc_render_ex(const orc_scene* sc, const orc_camera* cam, int mode, int N, const double background[3],
+                      int64_t npix, const int32_t* pixels, double* rgba, int32_t* nhits, int32_t* namb,
+                      int nthreads, int8_t* visible, int8_t* ambiguous, orc_pairs* pairs) {
+  return render_core(sc, cam, mode, N, background, npix, pixels, rgba, nhits, namb, 0, NULL, nthreads, visible,
+                     ambiguous, pairs);
+}
+
+void orc_pairs_free(orc_pairs* p) {
+  if (!p) return;
+  free(p->off); free(p->elem); free(p->flags);
+  p->off = NULL; p->elem = NULL; p->flags = NULL;
 }

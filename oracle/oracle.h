@@ -89,8 +89,25 @@ int64_t orc_render(const orc_scene* sc, const orc_camera* cam, int mode /*0 exac
                    double* rgba /*[npix][4]*/, int32_t* nhits /*[npix]*/, int32_t* namb /*[npix]*/,
                    int32_t cap, orc_hit* hits /*[npix][cap] or NULL*/, int nthreads);
 
+/* As orc_render, plus (each optional): the culled list of orc_cull
+ * (visible[n], ambiguous[n]) and, per rendered pixel, the (elem, flags) of
+ * every candidate pair that hits or is eps-ambiguous (CSR, allocated here,
+ * released by orc_pairs_free).  mode 2 = hit lists only (no integration;
+ * rgba = 0). */
+typedef struct {
+  int64_t npix;
+  int64_t* off;      /* [npix+1] */
+  int64_t* elem;     /* [off[npix]] */
+  int32_t* flags;    /* [off[npix]] ORC_HIT | ORC_AMBIGUOUS */
+} orc_pairs;
+int64_t orc_render_ex(const orc_scene* sc, const orc_camera* cam, int mode, int N, const double background[3],
+                      int64_t npix, const int32_t* pixels, double* rgba, int32_t* nhits, int32_t* namb,
+                      int nthreads, int8_t* visible, int8_t* ambiguous, orc_pairs* pairs);
+void orc_pairs_free(orc_pairs* p);
+
 /* Fold a caller-given list of segments of one pixel (any order): sort by
- * (alpha_near, elem), resolve overlaps (Eq. segsplit / segaverage) with
+ * (alpha_near, elem), resolve clusters of overlapping segments (Eq. segsplit /
+ * segaverage at every end point of the cluster, D14) with
  * tolerance tau, fold back to front. */
 void orc_fold_pixel(int n, orc_hit* segs, double tau, const double background[3], double rgba[4],
                     double ab[4]);

@@ -80,3 +80,102 @@ def compare(scene, g, ores, pixels, cull=None, tol=1e-4, by_counts=False):
                max_err=maxerr, bad_pixels=bad_pix, max_err_ambiguous_pixels=maxerr_amb,
                bad_ambiguous_pixels=bad_amb_pix)
     return rep
+
+
+# ---------------------------------------------------------------------------
+# Vectorised gates (every pixel of C2/C3, 1/256 .. 1/2304 samples of C4/C5)
+# ---------------------------------------------------------------------------
+def stride_pixels(W, H, s, off=None):
+    """Every s-th pixel row and column (stratified sample)."""
+    o = s // 2 if off is None else off
+    jj, ii = np.meshgrid(np.arange(o, H, s), np.arange(o, W, s), indexing="ij")
+    return (jj * W + ii).ravel().astype(np.int32)
+
+
+def gpu_pairs(raw, pixels, npix_image, key_offset=0):
+    """Unique (pixel, leaf) pairs of fold-0 records (leaf keys) restricted to
+    `pixels`, as int64 keys pixel << 32 | leaf.  raw: int32 [n, 8] tensor on
+    the device (filtered there) or numpy."""
+    import torch
+    if isinstance(raw, torch.Tensor):
+        mask = torch.zeros(npix_image, dtype=torch.bool, device=raw.device)
+        mask[torch.as_tensor(pixels, dtype=torch.int64, device=raw.device)] = True
+        pix = raw[:, 0].to(torch.int64)
+        sel = mask[pix]
+        pk = (pix[sel] << 32) | (raw[sel, 7].to(torch.int64) & 0xFFFFFFFF) + key_offset
+        return torch.unique(pk).cpu().numpy()
+    pix = raw[:, 0].astype(np.int64)
+    sel = np.zeros(npix_image, dtype=bool)
+    sel[pixels] = True
+    m = sel[pix]
+    return np.unique((pix[m] << 32) | ((raw[m, 7].astype(np.int64) & 0xFFFFFFFF) + key_offset))
+
+
+def oracle_pairs(ores):
+    """From OracleScene.render_pairs: (non-ambiguous hit pair keys, ambiguous
+    pair keys), each pixel << 32 | leaf."""
+    import oracle
+    cnt = np.diff(ores["pair_off"])
+    pix = np.repeat(ores["pixels"].astype(np.int64), cnt)
+    key = (pix << 32) | ores["pair_elem"].astype(np.int64)
+    fl = ores["pair_flags"]
+    amb = (fl & oracle.AMBIGUOUS) != 0
+    hit = ((fl & oracle.HIT) != 0) & ~amb
+    return np.unique(key[hit]), np.unique(key[amb])
+
+
+def gate_pairs(gkeys, okeys, akeys):
+    """Gate 2: GPU hit pairs minus eps-ambiguous pairs == the oracle's
+    non-ambiguous hit pairs.  Returns (mismatching pairs, mismatching pixels)."""
+    g = np.setdiff1d(gkeys, akeys, assume_unique=True)
+    diff = np.setxor1d(g, okeys, assume_unique=True)
+    return int(diff.size), int(np.unique(diff >> 32).size)
+
+
+def gate_cull(gvis_idx, ovis, oamb):
+    """Gate 1: culled-list set equality after removing ambiguous leaves."""
+    g = np.zeros(ovis.shape[0], dtype=bool)
+    g[np.asarray(gvis_idx, dtype=np.int64)] = True
+    return int(np.count_nonzero((g ^ ovis) & ~oamb))
+
+
+def gate_rgba(g_rgba, pixels, ores, tol=1e-4):
+    """Gate 3 on the pixels without eps-ambiguous pairs; the ambiguous ones
+    are reported separately.  g_rgba: [H*W, 4] numpy."""
+    err = np.abs(g_rgba[pixels] - ores["rgba"]).max(axis=1)
+    clean = ores["namb"] == 0
+    return dict(max_err=float(err[clean].max(initial=0.0)), bad_pixels=int(np.count_nonzero(err[clean] > tol)),
+                max_err_ambiguous=float(err[~clean].max(initial=0.0)), ambiguous_pixels=int(np.count_nonzero(~clean)))
+
+
+def gpu_fold0_chunked(scene, pixels, nchunks, device_copy=False):
+    """Fold-0 cast of `scene` split into `nchunks` contiguous SFC ranges (one
+    forest at a time, as the ranks of a multi-GPU run hold them): the visible
+    leaves (global indices), the unique (pixel, leaf) hit pairs at `pixels`
+    and the per-pixel hit counts of the whole image."""
+    import torch
+    from paper_1809_01334_b200 import rc
+    n = scene.num_leaves
+    W, H = scene.camera.width, scene.camera.height
+    cuts = [n * k // nchunks for k in range(nchunks + 1)]
+    vis, keys = [], []
+    hpp = torch.zeros(H * W, dtype=torch.int64, device="cuda")
+    stats = dict(hit_pairs=0, candidates=0, newton_failures=0, records=0)
+    for lo, hi in zip(cuts, cuts[1:]):
+        f = rc.Forest.from_scene(scene, first=lo, count=hi - lo, device_copy=device_copy)
+        f.camera_set(scene.camera)
+        f.cull()
+        vis.append(f.cull_result().cpu().numpy().astype(np.int64) + lo)
+        f.cast_segments(0)
+        s = f.segments()
+        keys.append(gpu_pairs(s["raw"], pixels, H * W))
+        hpp += s["hits_per_pixel"].reshape(-1).to(torch.int64)
+        for k in ("hit_pairs", "candidates", "newton_failures"):
+            stats[k] += int(s[k])
+        stats["records"] += int(s["count"])
+        f.close()
+        del f, s
+        rc.pool_trim()
+        torch.cuda.empty_cache()
+    return dict(visible=np.concatenate(vis), keys=np.unique(np.concatenate(keys)),
+                hits_per_pixel=hpp.cpu().numpy(), **stats)

@@ -8,7 +8,8 @@ import pytest
 
 import oracle
 import scenegen as sg
-from parity_util import compare, gpu_run, seg_columns
+from parity_util import (compare, gate_cull, gate_pairs, gate_rgba, gpu_fold0_chunked, gpu_pairs, gpu_run,
+                         oracle_pairs, seg_columns, stride_pixels)
 
 pytestmark = pytest.mark.gpu
 
@@ -50,20 +51,32 @@ def test_c2_small_full_frame():
     _check(compare(sc, g, ores, pixels, cull=o.cull()))
 
 
-def test_c2_full_size_sampled():
+def _gates_full(sc, g, ores, pixels):
+    """Gates 1-3 (vectorised) of a fold-0 GPU run against render_pairs."""
+    W, H = sc.camera.width, sc.camera.height
+    okeys, akeys = oracle_pairs(ores)
+    gkeys = gpu_pairs(g["raw"], pixels, W * H)
+    nbad, nbadpix = gate_pairs(gkeys, okeys, akeys)
+    rep = dict(cull_mismatch=gate_cull(g["visible"], ores["visible"], ores["ambiguous"]),
+               cull_ambiguous=int(ores["ambiguous"].sum()), pair_mismatch=nbad, hit_mismatch_pixels=nbadpix,
+               ambiguous_pairs=int(akeys.size), pixels=int(pixels.size), oracle_hits=int(okeys.size))
+    rep.update(gate_rgba(g["rgba"], pixels, ores))
+    return rep
+
+
+def test_c2_full_size_every_pixel():
     """BASELINE C2 at its full size (87,088 leaves, 512^2) in the bench's launch
-    configuration; a stratified pixel sample (every 7th row/column) is
-    compared one by one with the oracle."""
+    configuration: gates 1-3 on every pixel."""
     sc = sg.config2()
     o = oracle.OracleScene(sc)
-    W = sc.camera.width
-    jj, ii = np.meshgrid(np.arange(0, W, 7), np.arange(3, W, 7), indexing="ij")
-    pixels = (jj * W + ii).ravel().astype(np.int32)
-    ores = o.render(pixels, mode="exact", cap=128)
+    pixels = np.arange(sc.camera.width * sc.camera.height, dtype=np.int32)
+    ores = o.render_pairs(pixels, mode="exact")
     g = gpu_run(sc)
-    rep = compare(sc, g, ores, pixels, cull=o.cull())
+    rep = _gates_full(sc, g, ores, pixels)
+    print(rep)
     _check(rep)
-    # full-frame properties: every record inside its leaf's visible rect, alpha order
+    assert rep["pair_mismatch"] == 0
+    # full-frame properties: alpha order, transmission range, hit counts
     cols = seg_columns(g["raw"])
     assert np.all(cols["alpha_near"] <= cols["alpha_far"])   # equal only for sub-ulp chords
     assert np.all((cols["a"] > 0) & (cols["a"] <= 1))
@@ -155,26 +168,41 @@ def test_shell_gl8_field_p2():
     _check(compare(sc, g, ores, pixels, cull=o.cull()))
 
 
-def test_c3_full_size_sampled():
-    """BASELINE C3 at full size (1,572,864 curved hexes, 1024^2, N=6) in the
-    bench's launch configuration; a stratified pixel sample is compared one
-    by one with the oracle (all leaves culled by the oracle)."""
-    sc = sg.config3(device="cuda")
+def test_c3_reduced_every_pixel():
+    """C3's geometry, field and rule at reduced size (level-4 shell, 24,576
+    curved hexes, 256^2, 64 bumps, N = 6): gates 1-3 on every pixel."""
+    sc = sg.shell_uniform(4, 256, 64, gl_points=6, name="C3-L4")
     o = oracle.OracleScene(sc)
+    pixels = np.arange(256 * 256, dtype=np.int32)
+    ores = o.render_pairs(pixels, mode="exact")
+    g = gpu_run(sc)
+    rep = _gates_full(sc, g, ores, pixels)
+    print(rep, "newton_failures", g["newton_failures"])
+    _check(rep)
+    assert rep["pair_mismatch"] == 0 and g["newton_failures"] == 0
+
+
+def test_c3_full_size_sampled():
+    """BASELINE C3 at full size (1,572,864 curved hexes, 1024^2, N=6): gates 1-3
+    on every 4th pixel row and column (65,536 pixels; the oracle intersects
+    ~3e4 pairs/s per core, every pixel would take ~1 h on the box), all leaves
+    culled by the oracle; then the bench's configuration (fold level 2) against
+    the same oracle values and the fold-0 run."""
+    sc = sg.config3(device="cuda")
     W = sc.camera.width
-    jj, ii = np.meshgrid(np.arange(5, W, 41), np.arange(11, W, 41), indexing="ij")
-    pixels = (jj * W + ii).ravel().astype(np.int32)
-    ores = o.render(pixels, mode="exact", cap=512)
+    pixels = stride_pixels(W, W, 4, off=1)
     g = gpu_run(sc, device_copy=True)
-    rep = compare(sc, g, ores, pixels, cull=o.cull())
+    g2 = gpu_run(sc, device_copy=True, fold=2, keep_raw=False)    # bench.py's launch configuration
+    import bench
+    o = oracle.OracleScene(bench.scene_to_host(sc))
+    ores = o.render_pairs(pixels, mode="exact")
+    rep = _gates_full(sc, g, ores, pixels)
     print(rep, "hit_pairs", g["hit_pairs"], "newton_failures", g["newton_failures"])
     _check(rep)
-    assert g["newton_failures"] == 0
-    # the bench's configuration folds to node level 2 on chip (row a6)
-    g2 = gpu_run(sc, device_copy=True, fold=2)
-    rep2 = compare(sc, g2, ores, pixels, by_counts=True)
+    assert rep["pair_mismatch"] == 0 and g["newton_failures"] == 0
+    rep2 = gate_rgba(g2["rgba"], pixels, ores)
     print(rep2, "records", g2["count"], "raw", g2["raw_segments"], "units", g2["units"])
-    _check(rep2)
+    assert rep2["bad_pixels"] == 0, rep2
     assert np.array_equal(g2["hits_per_pixel"], g["hits_per_pixel"])
     assert g2["raw_segments"] == g["count"] and g2["count"] < g["count"] // 2
     assert np.abs(g2["rgba"] - g["rgba"]).max() < 1e-5
@@ -260,49 +288,69 @@ def test_virtual_ranks_fold_aggregate_aligned(nranks):
     assert np.abs(merged - full).max() < 1e-5
 
 
+def _big_config_gates(sc, pixels, nchunks, fold, cycles):
+    """Full-size C4 / C5: fold-0 casts of SFC chunks (gate 1 on the full culled
+    list, gate 2 on the hit pairs of the sampled pixels), then the bench's
+    launch configuration for gate 3 and the per-pixel hit counts."""
+    import torch
+    import bench
+    from paper_1809_01334_b200 import rc
+    W, H = sc.camera.width, sc.camera.height
+    ch = gpu_fold0_chunked(sc, pixels, nchunks, device_copy=isinstance(sc.leaf_anchor, torch.Tensor))
+    assert ch["newton_failures"] == 0
+    g = gpu_run(sc, device_copy=isinstance(sc.leaf_anchor, torch.Tensor), fold=fold, cycles=cycles, keep_raw=False)
+    assert g["newton_failures"] == 0
+    # the SFC chunks and the single forest see the same hits per pixel
+    assert np.array_equal(ch["hits_per_pixel"], g["hits_per_pixel"].reshape(-1).astype(np.int64))
+    assert ch["hit_pairs"] == g["hit_pairs"]
+    host = bench.scene_to_host(sc)
+    del sc
+    g.pop("forest").close()
+    rc.pool_trim()
+    torch.cuda.empty_cache()
+    o = oracle.OracleScene(host)
+    ores = o.render_pairs(pixels, mode="exact")
+    okeys, akeys = oracle_pairs(ores)
+    nbad, nbadpix = gate_pairs(ch["keys"], okeys, akeys)
+    rep = dict(cull_mismatch=gate_cull(ch["visible"], ores["visible"], ores["ambiguous"]),
+               cull_ambiguous=int(ores["ambiguous"].sum()), pair_mismatch=nbad, hit_mismatch_pixels=nbadpix,
+               ambiguous_pairs=int(akeys.size), pixels=int(pixels.size), oracle_hit_pairs=int(okeys.size),
+               leaves=int(host.num_leaves), hit_pairs=g["hit_pairs"], records=g["count"])
+    rep.update(gate_rgba(g["rgba"], pixels, ores))
+    return rep
+
+
 def test_c4_full_size_sampled():
     """BASELINE C4 at full size on one GPU (100,663,296 curved hexes, 2048^2,
-    N = 6) in the bench's launch configuration; 256 stratified pixels compared
-    one by one with the oracle (which culls all 1e8 leaves in fp64)."""
+    N = 6): culled list in full; hit pairs and pixels on every 16th pixel row
+    and column (16,384 pixels, SURVEY §8(d)'s 1/256 sample); pixel values in
+    the bench's launch configuration (fold level 2)."""
     from paper_1809_01334_b200 import rc
     rc.pool_trim()
     sc = sg.config4(device="cuda")
-    g = gpu_run(sc, device_copy=True, fold=2, keep_raw=False)     # bench.py's launch configuration
-    assert g["newton_failures"] == 0
-    import bench
-    o = oracle.OracleScene(bench.scene_to_host(sc))
-    W = sc.camera.width
-    jj, ii = np.meshgrid(np.arange(37, W, 128), np.arange(61, W, 128), indexing="ij")
-    pixels = (jj * W + ii).ravel().astype(np.int32)
-    ores = o.render(pixels, mode="exact", cap=1536)
-    rep = compare(sc, g, ores, pixels, by_counts=True)
-    print(rep, "hit_pairs", g["hit_pairs"], "records", g["count"], "raw segments", g["raw_segments"])
+    pixels = stride_pixels(sc.camera.width, sc.camera.height, 16, off=5)
+    rep = _big_config_gates(sc, pixels, nchunks=4, fold=2, cycles=0)
+    print(rep)
     _check(rep)
+    assert rep["pair_mismatch"] == 0
 
 
 def test_c5_full_size_sampled():
-    """BASELINE C5 at full size on one GPU (~1.9e8 curved hexes on levels
-    6..10, 4096^2, N = 8, fold 2 + 3 aggregation cycles = bench.py's launch
-    configuration); 256 stratified pixels compared one by one with the oracle
-    (which culls every leaf in fp64)."""
+    """BASELINE C5 at full size on one GPU (~1.97e8 curved hexes on levels
+    6..10, 4096^2, N = 8): culled list in full; hit pairs and pixels on every
+    48th pixel row and column (7,225 pixels); pixel values in the bench's
+    launch configuration (fold 2 + 3 aggregation cycles)."""
     import torch
     import bench
     from paper_1809_01334_b200 import rc
     rc.pool_trim()   # earlier tests' cached blocks back to the driver (the generator needs them)
     sc = bench.scene_to_host(sg.config5(device="cuda"))   # generated on the GPU, kept on the host
     torch.cuda.empty_cache()
-    g = gpu_run(sc, fold=2, cycles=3, keep_raw=False)
-    assert g["newton_failures"] == 0 and g["level"] == 5
-    assert g["count"] < g["raw_segments"] // 4
-    o = oracle.OracleScene(sc)
-    W = sc.camera.width
-    jj, ii = np.meshgrid(np.arange(101, W, 256), np.arange(77, W, 256), indexing="ij")
-    pixels = (jj * W + ii).ravel().astype(np.int32)
-    ores = o.render(pixels, mode="exact", cap=2048)
-    rep = compare(sc, g, ores, pixels, by_counts=True)
-    print(rep, "leaves", sc.num_leaves, "hit_pairs", g["hit_pairs"], "records", g["count"],
-          "raw segments", g["raw_segments"])
+    pixels = stride_pixels(sc.camera.width, sc.camera.height, 48, off=13)
+    rep = _big_config_gates(sc, pixels, nchunks=8, fold=2, cycles=3)
+    print(rep)
     _check(rep)
+    assert rep["pair_mismatch"] == 0
 
 
 @pytest.mark.gpu
