@@ -2,10 +2,19 @@
 segment evaluations/s and ms/frame; % of the FP32 roofline).
 
 One step = one frame: rc_camera_set + rc_cull + rc_cast_segments
-(+ rc_aggregate) + composite on seeded synthetic inputs already resident in
-HBM.  Prints ONE JSON line on rank 0.
+(+ rc_aggregate cycles) + tile exchange and composite, on seeded synthetic
+inputs already resident in HBM.  Prints ONE JSON line on rank 0.
 
   python bench.py [--gpus N] [--steps K] [--warmup W] [--config C] [--impl reference]
+  torchrun --nproc-per-node N bench.py --gpus N ...        (one rank per GPU, NCCL)
+
+Multi-GPU: contiguous SFC ranges, re-cut after a first cull at
+equal prefix sums of w_E = rect area + 1 (aligned to the coarsest node level
+the fold and cycles reach) with the leaves moved to their new owners (the
+pre-partition, timed separately as `repartition_ms`); records go to the tile
+owners through librc's NCCL communicator (rc_composite_tiles).
+--dist-backend gloo runs the same code with host-staged exchanges (tests:
+several ranks on one GPU).
 """
 from __future__ import annotations
 
@@ -27,15 +36,28 @@ NUM_SMS = 148
 
 
 def peaks():
+    """FP32 FMA-pipe peak for the roofline.  Measured on the box by
+    tools/peaks.py (profiles/peaks_r02.json: independent-chain FFMA across all
+    SMs, TFLOP/s at 2 flops per FFMA) when present, else derived from the
+    guide's unit counts at MEASURED_PEAKS.json's SM clock."""
     try:
         mp = json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json")))
     except Exception:
         mp = {}
     sm_mhz = float(mp.get("sm_max_mhz", 1965.0))
-    fp32 = NUM_SMS * FP32_LANES_PER_SM * 2 * sm_mhz * 1e6 / 1e12
-    return dict(fp32_tflops=fp32, hbm_gbs=float(mp.get("hbm_gbs", 6650.0)), sm_mhz=sm_mhz,
-                source="MEASURED_PEAKS.json sm_max_mhz x 148 SM x 128 FP32 lanes x 2 (guide unit counts)"
-                if mp else "fallback 1965 MHz (B200_PROFILING.md)")
+    derived = NUM_SMS * FP32_LANES_PER_SM * 2 * sm_mhz * 1e6 / 1e12
+    out = dict(fp32_tflops=derived, hbm_gbs=float(mp.get("hbm_gbs", 6650.0)), sm_mhz=sm_mhz,
+               source="derived: 148 SM x 128 FP32 lanes x 2 x MEASURED_PEAKS.json sm_max_mhz (guide unit counts)")
+    try:
+        meas = json.load(open(os.path.join(ROOT, "profiles", "peaks_r02.json")))
+        out["fp32_tflops"] = float(meas["ffma_tflops"])
+        out["source"] = (f"measured: {meas['how']} ({meas['when']}); derived at {sm_mhz:.0f} MHz would be "
+                         f"{derived:.1f}")
+        out["mufu_ex2_tops"] = meas.get("mufu_ex2_tops")
+        out["fmnmx_tops"] = meas.get("fmnmx_tops")
+    except Exception:
+        pass
+    return out
 
 
 class Clocks:
@@ -106,6 +128,10 @@ def make_scene(cfg: int, device):
         return sg.config5(device=device)
     if cfg == 45:   # profiling stand-in for C4: level 7 at 1024^2 has C4's pixels per element
         return sg.shell_uniform(7, 1024, 256, name="C4s", device=device)
+    if cfg == 33:   # test size: C3's geometry at level 4, 128^2, 4 x 4 tiles, 2 coarsening cycles
+        import dataclasses
+        sc = sg.shell_uniform(4, 128, 16, gl_points=6, name="C3-L4", tiles=(4, 4), device=device)
+        return dataclasses.replace(sc, coarsen_cycles=2)
     raise ValueError(cfg)
 
 
@@ -114,7 +140,11 @@ WORKLOAD = {1: "C1: identity cube, uniform level 3 (512 hex), ortho 64x64, N=4",
             3: "C3: cubed-sphere shell R=2, uniform level 6 (1,572,864 hex), 1024x1024, N=6",
             4: "C4: cubed-sphere shell R=2, uniform level 8 (100,663,296 hex), 2048x2048, N=6",
             5: "C5: cubed-sphere shell R=2, adaptive levels 6..10, 4096x4096, N=8, 3 coarsening cycles",
-            45: "C4s (profiling stand-in): shell R=2, uniform level 7 (12,582,912 hex), 1024x1024, N=6"}
+            45: "C4s (profiling stand-in): shell R=2, uniform level 7 (12,582,912 hex), 1024x1024, N=6",
+            33: "C3-L4 (test size): shell R=2, uniform level 4, 128x128, N=6, 4x4 tiles, 2 coarsening cycles"}
+
+# oracle pixel sample (every s-th row and column) of the CPU baseline and the reference arm
+CPU_STRIDE = {1: 1, 2: 2, 3: 16, 4: 64, 5: 128, 45: 32, 33: 1}
 
 
 def forest_affine(scene):
@@ -134,49 +164,116 @@ def l2_flush(buf):
     buf.add_(1.0)
 
 
-def cpu_baseline(scene, stride, threads=0):
-    """The oracle as it stands (exact mode) on every `stride`-th pixel row/column."""
+def cpu_model():
+    model, sockets = None, None
+    try:
+        out = subprocess.run(["lscpu"], capture_output=True, text=True, timeout=10).stdout
+        for ln in out.splitlines():
+            k, _, v = ln.partition(":")
+            if k.strip() == "Model name":
+                model = v.strip()
+            if k.strip() == "Socket(s)":
+                sockets = v.strip()
+    except Exception:
+        pass
+    return model, sockets
+
+
+def cpu_baseline(scene, stride, hits_full, one_thread=True):
+    """The oracle as it stands (exact mode) on the host cores, SURVEY §8(d):
+    the full fp64 cull of every leaf (T_cull), then every `stride`-th pixel
+    row and column rendered with that culled list (T_sample); extrapolated
+    frame = T_sample * hits_full / hits_sample + T_cull.  A 1-thread run on
+    every 4th sampled row gives the single-core rate."""
     import numpy as np
 
     import oracle
     o = oracle.OracleScene(scene)
     W, H = scene.camera.width, scene.camera.height
+    t0 = time.perf_counter()
+    vis, amb, rects = o.cull()
+    t_cull = time.perf_counter() - t0
     jj, ii = np.meshgrid(np.arange(stride // 2, H, stride), np.arange(stride // 2, W, stride), indexing="ij")
     pix = (jj * W + ii).ravel().astype(np.int32)
     t0 = time.perf_counter()
-    res = o.render(pix, mode="exact", with_hits=False, nthreads=threads)
-    dt = time.perf_counter() - t0
-    cores = threads or (os.cpu_count() or 1)
-    return dict(value=res["total_hits"] / dt, unit="hit pairs/s", cores=cores, kind="oracle",
-                sample=f"every {stride}th pixel row and column ({pix.size} pixels, {res['total_hits']} hit pairs), "
-                       f"all {scene.num_leaves} leaves culled; fp64 exact mode; {dt:.1f} s wall",
-                seconds=dt, hit_pairs=res["total_hits"])
+    res = o.render_pairs(pix, mode="exact", rects=rects)
+    t_sample = time.perf_counter() - t0
+    hs = max(res["total_hits"], 1)
+    cores = os.cpu_count() or 1
+    try:
+        cores = len(os.sched_getaffinity(0))
+    except Exception:
+        pass
+    scale = (W * H) / pix.size   # stratified sample -> whole image (pixel ratio, as the reference arm)
+    frame_s = t_sample * scale + t_cull
+    out = dict(value=hs * scale / frame_s, unit="hit pairs/s", cores=cores, kind="oracle",
+               sample=f"full fp64 cull of {scene.num_leaves} leaves ({t_cull:.1f} s) + every {stride}th pixel row "
+                      f"and column ({pix.size} pixels, {res['total_hits']} hit pairs, {t_sample:.1f} s, exact mode); "
+                      f"extrapolated frame = T_sample x {scale:.0f} (pixel ratio) + T_cull",
+               extrapolated_ms_per_frame=1000.0 * frame_s, t_cull_s=t_cull, t_sample_s=t_sample,
+               frame_hit_pairs_gpu=int(hits_full), frame_hit_pairs_extrapolated=int(hs * scale),
+               hit_pairs_sample=int(res["total_hits"]),
+               rate_per_core=res["total_hits"] / t_sample / cores, threads=cores)
+    if one_thread:
+        sub = pix.reshape(jj.shape)[::4].ravel()
+        t0 = time.perf_counter()
+        r1 = o.render_pairs(sub, mode="exact", rects=rects, nthreads=1)
+        t1 = time.perf_counter() - t0
+        out["rate_1_thread"] = r1["total_hits"] / t1
+        out["sample_1_thread"] = f"{sub.size} pixels, {r1['total_hits']} hit pairs, {t1:.1f} s"
+    model, sockets = cpu_model()
+    out["cpu_model"], out["sockets"] = model, sockets
+    return out
 
 
 def run_reference(args):
-    """--impl reference: the fp64 oracle timed as it stands on host cores."""
+    """--impl reference: the fp64 oracle timed as it stands on host cores, on
+    the same workload, metric and pixel sample as cpu_baseline.  The cull is
+    done once (its time counts in every step's extrapolated frame); each step
+    renders the sample."""
     rank = int(os.environ.get("RANK", "0"))
     if rank != 0:
         return
+    import numpy as np
     import torch
+
+    import oracle
     dev = "cuda" if (args.config >= 3 and torch.cuda.is_available()) else None
     scene = scene_to_host(make_scene(args.config, dev))
-    # each step a bounded sample (~5-15 s of host work) so that --steps K ends within minutes
-    stride = {1: 1, 2: 16, 3: 64, 4: 128, 5: 256, 45: 64}[args.config]
-    for _ in range(args.warmup):
-        pass
-    vals = []
+    stride = CPU_STRIDE[args.config]
+    o = oracle.OracleScene(scene)
+    W, H = scene.camera.width, scene.camera.height
+    t0 = time.perf_counter()
+    vis, amb, rects = o.cull()
+    t_cull = time.perf_counter() - t0
+    jj, ii = np.meshgrid(np.arange(stride // 2, H, stride), np.arange(stride // 2, W, stride), indexing="ij")
+    pix = (jj * W + ii).ravel().astype(np.int32)
+    for _ in range(min(args.warmup, 1)):
+        o.render_pairs(pix[:max(1, pix.size // 8)], mode="exact", rects=rects)
+    times, hits = [], 0
     for _ in range(args.steps):
-        vals.append(cpu_baseline(scene, stride))
-    v = statistics.median([x["value"] for x in vals])
-    cb = dict(vals[-1])
-    cb["value"] = v
+        t0 = time.perf_counter()
+        res = o.render_pairs(pix, mode="exact", rects=rects)
+        times.append(time.perf_counter() - t0)
+        hits = res["total_hits"]
+    t_sample = statistics.median(times)
+    # the stratified sample scaled to the whole image (pixel ratio)
+    scale = (W * H) / pix.size
+    hits_full = hits * scale
+    frame_s = t_sample * scale + t_cull
+    v = hits_full / frame_s
+    cores = len(os.sched_getaffinity(0)) if hasattr(os, "sched_getaffinity") else (os.cpu_count() or 1)
+    model, sockets = cpu_model()
+    cb = {"value": v, "unit": "hit pairs/s", "cores": cores, "kind": "oracle",
+          "sample": f"full fp64 cull ({t_cull:.1f} s, once) + every {stride}th pixel row and column ({pix.size} "
+                    f"pixels, {hits} hit pairs, median {t_sample:.1f} s per step); frame = T_sample x "
+                    f"{scale:.0f} (pixel ratio) + T_cull", "cpu_model": model, "sockets": sockets}
     line = {"impl": "reference", "metric": "element-ray segment evaluations/s (hit pairs/s)", "value": v,
             "unit": "hit pairs/s", "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
-            "ms_per_step": 1000.0 * statistics.median([x["seconds"] for x in vals]),
-            "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f64",
-            "data": "synthetic", "config": {"workload": WORKLOAD[args.config], "sample_stride": stride},
-            "cpu_baseline": {k: cb[k] for k in ("value", "unit", "cores", "kind", "sample")},
+            "ms_per_step": 1000.0 * frame_s, "higher_is_better": True, "scaling": "strong", "vs_baseline": None,
+            "dtype": "f64", "data": "synthetic (seeded, scenegen)",
+            "config": {"workload": WORKLOAD[args.config], "sample_stride": stride},
+            "cpu_baseline": cb,
             "e2e": {"value": v, "unit": "hit pairs/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
     print(json.dumps(line), flush=True)
 
@@ -192,6 +289,9 @@ def main():
     ap.add_argument("--no-e2e", action="store_true", help="skip the end-to-end leg (A/B runs of build variants)")
     ap.add_argument("--fold", type=int, default=-1,
                     help="node level of the on-chip fold (row a6); default 2 for curved forests, 0 for affine")
+    ap.add_argument("--dist-backend", default="nccl", choices=["nccl", "gloo"],
+                    help="gloo: host-staged exchanges (tests: several ranks on one GPU)")
+    ap.add_argument("--dump", default="", help="rank 0 writes the assembled image and hit counts (npz)")
     args = ap.parse_args()
     if args.impl == "reference":
         return run_reference(args)
@@ -204,31 +304,63 @@ def main():
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
-    torch.cuda.set_device(local)
-    dev = torch.device("cuda", local)
+    ndev = max(torch.cuda.device_count(), 1)
+    torch.cuda.set_device(local % ndev)
+    dev = torch.device("cuda", local % ndev)
+    tp = comm = None
     if world > 1:
         import torch.distributed as dist
-        dist.init_process_group("nccl", device_id=dev)
+
+        from paper_1809_01334_b200 import dist as rdist
+        if args.dist_backend == "nccl":
+            dist.init_process_group("nccl", device_id=dev)
+        else:
+            dist.init_process_group("gloo")
+        tp = rdist.Transport()
     scene = make_scene(args.config, dev if args.config >= 2 else None)
     cam = scene.camera
     W, H = cam.width, cam.height
     N = cam.gl_points
-    lib = rc.lib()
+    rc.lib()
 
     fold = args.fold if args.fold >= 0 else (0 if forest_affine(scene) else 2)
-    # --- device-resident inputs: this rank's contiguous SFC range ---------
-    # equal leaf counts, cuts moved to node starts of the coarsest level the
-    # fold + aggregation cycles reach: every family is local
+    cycles = scene.coarsen_cycles
     n = scene.num_leaves
+    tiles = scene.tiles if world > 1 else (1, 1)
+    repart = {}
     if world > 1:
-        from paper_1809_01334_b200 import dist as rdist
-        A, T, Lv = (torch.as_tensor(x, device=dev) for x in (scene.leaf_anchor, scene.leaf_tree, scene.leaf_level))
-        allowed = rdist.node_starts(A, T, Lv, fold + scene.coarsen_cycles)
-        lo, hi = rdist.aligned_ranges(torch.ones(n, dtype=torch.float64), world, allowed)[rank]
-        del A, T, Lv, allowed
+        # --- pre-partition: equal counts, first cull, weighted cut, leaf move
+        t0 = time.perf_counter()
+        A, T, Lv, F = (torch.as_tensor(x).to(dev) for x in (scene.leaf_anchor, scene.leaf_tree, scene.leaf_level,
+                                                             scene.leaf_field))
+        allowed = rdist.node_starts(A, T, Lv, fold + cycles)
+        old = rdist.aligned_ranges(torch.ones(n, dtype=torch.float64), world, allowed)
+        lo, hi = old[rank]
+        f0 = rc.Forest(scene.tree_ctrl, scene.geom_degree, scene.field_degree, A[lo:hi], T[lo:hi], Lv[lo:hi],
+                       F[lo:hi], scene.kappa0, scene.inv_F, scene.q0, first_global_leaf=lo)
+        f0.camera_set(cam)
+        f0.cull()
+        w = f0.leaf_weights()
+        f0.close()
+        ranges = rdist.distributed_aligned_cuts(w, allowed[lo:hi], lo, n, tp)
+        mine = rdist.redistribute_rows([A[lo:hi], T[lo:hi], Lv[lo:hi], F[lo:hi]], old, ranges, tp)
+        lo, hi = ranges[rank]
+        wsum = float(w.sum())
+        del A, T, Lv, F, allowed, w
+        forest = rc.Forest(scene.tree_ctrl, scene.geom_degree, scene.field_degree, *mine, scene.kappa0,
+                           scene.inv_F, scene.q0, first_global_leaf=lo)
+        keys = mine[:3]
+        del mine
+        torch.cuda.synchronize()
+        repart = {"repartition_ms": 1000.0 * (time.perf_counter() - t0), "ranges": ranges, "weight_local": wsum,
+                  "equal_count_ranges": old}
+        if args.dist_backend == "nccl":
+            comm = rc.Comm(world, rank)
     else:
         lo, hi = 0, n
-    forest = rc.Forest.from_scene(scene, first=lo, count=hi - lo, device_copy=True)
+        ranges = [(0, n)]
+        forest = rc.Forest.from_scene(scene, first=lo, count=hi - lo, device_copy=True)
+        keys = None
     # the forest holds its own device copy: keep the scene on the host only
     # (e2e inputs, CPU baseline) and hand the generator's memory back (C5 needs it)
     scene = scene_to_host(scene)
@@ -236,53 +368,63 @@ def main():
     img = torch.empty((H, W, 4), dtype=torch.float32, device=dev)
     flush = torch.empty(int(160e6) // 4, dtype=torch.float32, device=dev)   # > 126 MB L2
     stream = torch.cuda.current_stream()
+    consts = (scene.tree_ctrl, scene.geom_degree, scene.field_degree, scene.kappa0, scene.inv_F, scene.q0, cam)
 
     phase_ev = {}
+    moved = [0]
 
     def mark(name):
-        if phase_ev is not None:
-            ev = torch.cuda.Event(enable_timing=True)
-            ev.record(stream)
-            phase_ev[name] = ev
+        ev = torch.cuda.Event(enable_timing=True)
+        ev.record(stream)
+        phase_ev[name] = ev
 
-    def frame():
+    def frame(f, f_keys, f_rng):
         mark("start")
-        forest.camera_set(cam)
-        forest.cull()
+        f.camera_set(cam)
+        f.cull()
         mark("cull")
-        forest.cast_segments(fold)
+        f.cast_segments(fold)
         mark("cast")
-        if scene.coarsen_cycles:
-            forest.aggregate(scene.coarsen_cycles)
+        fa = f
+        if cycles:
+            if world > 1:
+                fa, _, _, _, mv = rdist.aggregate_with_repartition(f, f_keys, f_rng, ranges, cycles, fold + cycles,
+                                                                   tp, consts)
+                moved[0] = mv
+            else:
+                f.aggregate(cycles)
         mark("aggregate")
         if world == 1:
-            forest.composite(out=img)
+            f.composite(out=img)
             mark("composite")
-            return None
-        from paper_1809_01334_b200 import dist as rdist
-        out = rdist.exchange_and_composite(forest, scene.tiles, world, rank)
+            return img, fa
+        out = rdist.exchange_and_composite(fa, tiles, world, rank, comm=comm, tp=tp)
         mark("composite")
+        return out, fa
+
+    def run_frame(f, f_keys, f_rng):
+        out, fa = frame(f, f_keys, f_rng)
+        if fa is not f:
+            fa.close()
         return out
 
     for _ in range(max(3, args.warmup)):
-        frame()
+        run_frame(forest, keys, (lo, hi))
     torch.cuda.synchronize()
     segs = forest.segments()
     hits_local = segs["hit_pairs"]
     cand_local = segs["candidates"]
     if world > 1:
-        import torch.distributed as dist
-        t = torch.tensor([hits_local, cand_local], dtype=torch.int64, device=dev)
-        dist.all_reduce(t)
+        t = tp.all_gather(torch.tensor([hits_local, cand_local], dtype=torch.int64)).sum(dim=0)
         hits_total, cand_total = int(t[0]), int(t[1])
     else:
         hits_total, cand_total = hits_local, cand_local
 
     # --- timed region: K frames, L2 flushed between frames (outside events) ---
-    times, cast_ms, phase_ms = [], [], []
-    phase_acc = {}
+    times, cast_ms, phase_acc = [], [], {}
     rc.launch_count(reset=True)
-    with Clocks(local) as clk:
+    last_out = None
+    with Clocks(local % ndev) as clk:
         for _ in range(args.steps):
             l2_flush(flush)
             if world > 1:
@@ -291,11 +433,13 @@ def main():
             e0 = torch.cuda.Event(enable_timing=True)
             e1 = torch.cuda.Event(enable_timing=True)
             e0.record(stream)
-            frame()
+            last_out, fa = frame(forest, keys, (lo, hi))
             e1.record(stream)
             torch.cuda.synchronize()
             times.append(e0.elapsed_time(e1))
             cast_ms.append(forest.last_phase_ms(1))
+            if fa is not forest:
+                fa.close()
             if world == 1:
                 for k, nm in ((4, "composite_bucket"), (5, "composite_fold")):
                     phase_acc[nm] = phase_acc.get(nm, 0.0) + forest.last_phase_ms(k) / args.steps
@@ -304,29 +448,40 @@ def main():
                 phase_acc[b] = phase_acc.get(b, 0.0) + phase_ev[a].elapsed_time(phase_ev[b]) / args.steps
     launches = rc.launch_count()
     ms_local = sum(times) / len(times)
+    cast_local = sum(cast_ms) / len(cast_ms)
     if world > 1:
-        import torch.distributed as dist
-        t = torch.tensor([ms_local, sum(cast_ms) / len(cast_ms)], dtype=torch.float64, device=dev)
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
-        ms_step, cast_avg = float(t[0]), float(t[1])
+        ms_step, cast_avg = tp.max(ms_local), tp.max(cast_local)
     else:
-        ms_step, cast_avg = ms_local, sum(cast_ms) / len(cast_ms)
+        ms_step, cast_avg = ms_local, cast_local
     value = hits_total / (ms_step / 1000.0)
+
+    if args.dump:
+        hpp = forest.segments()["hits_per_pixel"].reshape(-1).to(torch.int64)
+        if world > 1:
+            image = rdist.gather_image(last_out, tiles, W, H, tp)
+            hpp = tp.all_gather(hpp).sum(dim=0)
+        else:
+            image = last_out.cpu()
+        if rank == 0:
+            np.savez(args.dump, image=image.numpy(), hits_per_pixel=hpp.cpu().numpy(), hit_pairs=hits_total,
+                     ranges=np.array(ranges), moved=moved[0])
 
     # --- roofline of the dominant kernel (segment kernel) -----------------
     pk = peaks()
     import bench_model
     fl = bench_model.flops(scene.geom_degree if not forest_affine(scene) else 1, N, hits_local, cand_local)
-    achieved = fl / (cast_avg / 1000.0) / 1e12
+    achieved = fl / (cast_local / 1000.0) / 1e12
     kname = "k_cast_affine" if forest_affine(scene) else "k_cast_curved (intersection + integration + fold, fused)"
-    roof = {"kernel": kname, "bound": "alu",
-            "achieved": achieved, "peak": pk["fp32_tflops"], "unit": "TFLOP/s", "frac": achieved / pk["fp32_tflops"],
-            "traffic": None, "kernel_ms": cast_avg, "share_of_step": cast_avg / ms_step,
-            "algorithmic_flops_per_launch": fl, "peak_source": pk["source"]}
+    roof = {"kernel": kname, "bound": "fp32_fma", "achieved": achieved, "peak": pk["fp32_tflops"], "unit": "TFLOP/s",
+            "frac": achieved / pk["fp32_tflops"], "traffic": None, "kernel_ms": cast_local,
+            "share_of_step": cast_local / ms_local, "algorithmic_flops_per_launch": fl,
+            "peak_source": pk["source"]}
     tpath = os.path.join(ROOT, "profiles", f"traffic_c{args.config}.json")
     if os.path.exists(tpath):
         try:
-            roof["traffic"] = json.load(open(tpath)).get("bytes_per_launch")
+            tj = json.load(open(tpath))
+            roof["traffic"] = tj.get("bytes_per_launch")
+            roof["traffic_source"] = tj.get("source")
         except Exception:
             pass
 
@@ -334,10 +489,10 @@ def main():
     seg_info = forest.segments()
     composite_copy = int(forest.last_phase_ms(3))
     newton_failures = seg_info["newton_failures"]
-    fold_info = {"face_failures": seg_info["face_failures"], "fold_levels": fold, "records": seg_info["count"], "raw_segments": seg_info["raw_segments"],
-                 "record_level": seg_info["level"], "units": seg_info["units"],
-                 "unfolded_units": seg_info["unfolded_units"], "face_tasks": seg_info["face_tasks"],
-                 "fallback_tasks": seg_info["fallback_tasks"]}
+    fold_info = {"face_failures": seg_info["face_failures"], "fold_levels": fold, "records": seg_info["count"],
+                 "raw_segments": seg_info["raw_segments"], "record_level": seg_info["level"],
+                 "units": seg_info["units"], "unfolded_units": seg_info["unfolded_units"],
+                 "face_tasks": seg_info["face_tasks"], "fallback_tasks": seg_info["fallback_tasks"]}
     forest.close()          # release the device-resident forest before the e2e forests
     del forest
     torch.cuda.empty_cache()
@@ -349,7 +504,7 @@ def main():
     h2d = sum(a.nbytes for a in host)
     img_host = torch.empty((H, W, 4), dtype=torch.float32).pin_memory()
     e2e_times = []
-    n_e2e = 0 if args.no_e2e else 2 + (1 if args.config >= 4 else max(1, min(args.steps, 3)))
+    n_e2e = 0 if args.no_e2e else 2 + (1 if args.config in (4, 5) else max(1, min(args.steps, 3)))
     for it in range(n_e2e):
         torch.cuda.synchronize()
         if world > 1:
@@ -359,31 +514,22 @@ def main():
         # guarantees SFC order: RC_HOST_COPY_TRUSTED skips the host-side check)
         f2 = rc.Forest(scene.tree_ctrl, scene.geom_degree, scene.field_degree, *pinned_np, scene.kappa0,
                        scene.inv_F, scene.q0, first_global_leaf=lo, trusted=True)
-        f2.camera_set(cam)
-        f2.cull()
-        f2.cast_segments(fold)
-        if scene.coarsen_cycles:
-            f2.aggregate(scene.coarsen_cycles)
-        if world == 1:
-            out = f2.composite()
-            img_host.copy_(out)
-        else:
-            from paper_1809_01334_b200 import dist as rdist
-            out = rdist.exchange_and_composite(f2, scene.tiles, world, rank)
-            img_host.view(-1)[:out.numel()].copy_(out.view(-1))
+        k2 = [torch.from_numpy(a).to(dev) for a in host[:3]] if (world > 1 and cycles) else None
+        out, fa = frame(f2, k2, (lo, hi))
+        img_host.view(-1)[:out.numel()].copy_(out.reshape(-1))
         torch.cuda.synchronize()
         dt = time.perf_counter() - t0
+        if fa is not f2:
+            fa.close()
         f2.close()
         if it >= 2:
             e2e_times.append(dt)
     e2e_s = sum(e2e_times) / len(e2e_times) if e2e_times else float("nan")
     if world > 1:
-        import torch.distributed as dist
-        t = torch.tensor([e2e_s], dtype=torch.float64, device=dev)
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
-        e2e_s = float(t[0])
+        e2e_s = tp.max(e2e_s)
     e2e = {"value": hits_total / e2e_s, "unit": "hit pairs/s", "h2d_bytes_per_step": h2d,
-           "d2h_bytes_per_step": H * W * 16, "ms_per_step": e2e_s * 1000.0}
+           "d2h_bytes_per_step": int(last_out.numel()) * 4 if last_out is not None else H * W * 16,
+           "ms_per_step": e2e_s * 1000.0}
 
     if rank == 0:
         line = {"metric": "element-ray segment evaluations/s (hit pairs/s)", "value": value, "unit": "hit pairs/s",
@@ -394,18 +540,23 @@ def main():
                            "hit_pairs": hits_total, "candidate_pairs": cand_total,
                            "candidate_pairs_per_s": cand_total / (ms_step / 1000.0),
                            "l2": "flushed between frames (160 MB write outside the events)",
-                           "parallelism": f"sfc{world}"},
+                           "parallelism": f"sfc{world}", "tiles": list(tiles),
+                           "dist_backend": args.dist_backend if world > 1 else None},
                 "roofline": roof, "gpu_launches": launches, "clocks": clk.summary(), "e2e": e2e,
                 "newton_failures": newton_failures, "segments": fold_info,
                 "phase_ms": {k: round(v, 3) for k, v in phase_acc.items()},
                 "composite_copy": composite_copy}
+        if world > 1:
+            line["partition"] = {"repartition_ms": repart["repartition_ms"], "ranges": repart["ranges"],
+                                 "cycle_records_moved_rank0": moved[0]}
         if world == 1 and not args.no_cpu_baseline:
-            stride = {1: 1, 2: 2, 3: 16, 4: 64, 5: 128, 45: 32}[args.config]   # oracle cull of all leaves is a fixed ~40 s (C4)
             sc_cpu = scene_to_host(scene)
-            cb = cpu_baseline(sc_cpu, stride)
-            line["cpu_baseline"] = {k: cb[k] for k in ("value", "unit", "cores", "kind", "sample")}
+            cb = cpu_baseline(sc_cpu, CPU_STRIDE[args.config], hits_total)
+            line["cpu_baseline"] = cb
         print(json.dumps(line), flush=True)
     if world > 1:
+        if comm is not None:
+            comm.close()
         import torch.distributed as dist
         dist.barrier()
         dist.destroy_process_group()

@@ -31,13 +31,14 @@ typedef enum {
   RC_ERR_NOT_SFC_SORTED = -2,/* leaves not strictly increasing in (tree, Morton key)    */
   RC_ERR_OUT_OF_MEMORY = -3,
   RC_ERR_CUDA = -4,          /* CUDA runtime error; rc_last_error() has the call site   */
+  RC_ERR_NCCL = -5,          /* NCCL missing or a collective failed (rc_comm_*)          */
   RC_ERR_CAPACITY = -6,      /* caller buffer too small; *required is written           */
   RC_ERR_STATE = -7,         /* call order violated (cast before camera_set, ...)       */
   RC_ERR_NUMERIC = -8        /* non-finite input                                        */
 } rc_status;
 
 const char* rc_last_error(void);
-int32_t rc_version(void);    /* ABI version, currently 1 */
+int32_t rc_version(void);    /* ABI version, currently 2 */
 
 /* ------------------------------------------------------------------------
  * Forest: SFC-ordered leaves of a forest of octrees with per-tree degree-R
@@ -64,7 +65,9 @@ typedef struct {
   const int32_t* leaf_anchor; /* [n][3] in units of 2^-18 of the tree cube               */
   const int32_t* leaf_tree;   /* [n]                                                     */
   const int8_t* leaf_level;   /* [n], 0..18                                              */
-  const float* leaf_field;    /* [n][(P+1)^3], node order [k3][k2][k1]                    */
+  const float* leaf_field;    /* [n][(P+1)^3], node order [k3][k2][k1]; NULL: keys-only
+                                 forest (node tables, rc_segments_set, rc_aggregate and the
+                                 composite; rc_cast_segments / rc_debug_pair refuse)    */
   int32_t memory;             /* RC_HOST_COPY: leaf arrays are host pointers (checked);
                                  RC_HOST_COPY_TRUSTED: host pointers, the caller
                                  guarantees SFC order (no host-side check; pinned
@@ -110,13 +113,21 @@ rc_status rc_camera_set(rc_forest* f, const rc_camera* cam, void* stream);
  * centre rectangle of the camera-space AABB of its Bernstein-Bezier points
  * is non-empty.  Produces the compacted visible list (SFC order) and the
  * per-visible-leaf pixel rectangles on the device.  Async.
+ * d_num_visible (optional, device int64 scalar): receives the number of
+ * visible leaves (stream-ordered, no host sync).
  * ---------------------------------------------------------------------- */
-rc_status rc_cull(rc_forest* f, void* stream);
+rc_status rc_cull(rc_forest* f, void* stream, int64_t* d_num_visible);
 
 /* [sync] Copies the visible leaf indices (local, SFC order) to the caller's
  * device buffer d_visible[capacity]; *count = number of visible leaves.
  * RC_ERR_CAPACITY (with *count set) if capacity is too small. */
 rc_status rc_cull_result(rc_forest* f, int32_t* d_visible, int64_t capacity, int64_t* count, void* stream);
+
+/* Partition weights of the last cull ("weight proportional
+ * to its visible pixel count"): d_w[e] = (pixel-centre
+ * rectangle area of leaf e, 0 when culled) + 1 for every local leaf, device
+ * int64 [num_leaves].  Async.  Must follow rc_cull. */
+rc_status rc_leaf_weights(rc_forest* f, int64_t* d_w, int64_t capacity, void* stream);
 
 /* ------------------------------------------------------------------------
  * Cast segments (PAPER.md:921-953 leaf-level rendering): for every candidate
@@ -168,6 +179,26 @@ rc_status rc_cast_segments(rc_forest* f, int32_t fold_levels, void* stream);
 /* [sync] fills *out with counts and device views of the current segments. */
 rc_status rc_segments_get(rc_forest* f, rc_segments* out, void* stream);
 
+/* Replaces the forest's current records by n caller records (device rc_seg,
+ * copied) at node level `level` (the keys are global SFC indices of the
+ * first leaves of level-`level` nodes of THIS forest): the import side of a
+ * repartition between coarsening cycles, after which
+ * rc_aggregate continues on them.  [sync] (sizes the buffer). */
+rc_status rc_segments_set(rc_forest* f, const rc_seg* d_recs, int64_t n, int32_t level, void* stream);
+
+/* Parity / debug export (not timed): evaluates one (visible leaf, pixel)
+ * pair exactly as the segment kernel does (same device
+ * code: intersection, GL rule), without folding.  local_leaf: index into
+ * this forest's leaves (any leaf, culled or not); (i, j): pixel.  Up to 4
+ * segments in alpha order; nseg = 0 for a miss.  Must follow rc_camera_set.
+ * [sync] */
+typedef struct {
+  int32_t nseg;
+  float alpha_near[4], alpha_far[4], a[4], b[4][3];
+} rc_pair_result;
+rc_status rc_debug_pair(rc_forest* f, int64_t local_leaf, int32_t i, int32_t j, rc_pair_result* out,
+                        void* stream);
+
 /* [sync] Copies the node table of coarsening level `level` in [1, 8] (local
  * index of each node's first leaf, SFC order) to d_first[capacity] (device);
  * *count = number of nodes.  RC_ERR_CAPACITY if capacity is too small. */
@@ -184,32 +215,56 @@ rc_status rc_node_table(rc_forest* f, int32_t level, int32_t* d_first, int64_t c
 rc_status rc_aggregate(rc_forest* f, int32_t cycles, void* stream);
 
 /* ------------------------------------------------------------------------
+ * Multi-GPU communicator: NCCL, loaded at run time
+ * (libnccl.so.2; RC_ERR_NCCL when missing).  Rank 0 draws the id with
+ * rc_comm_unique_id, the caller broadcasts its 128 bytes (e.g. with
+ * torch.distributed), every rank calls rc_comm_create collectively on its
+ * own device (the current CUDA device).  One rank per GPU.
+ * ---------------------------------------------------------------------- */
+typedef struct rc_comm rc_comm;
+rc_status rc_comm_unique_id(uint8_t id[128]);
+rc_status rc_comm_create(const uint8_t id[128], int32_t nranks, int32_t rank, void* stream, rc_comm** out);
+rc_status rc_comm_destroy(rc_comm* c);
+
+/* ------------------------------------------------------------------------
  * Composite.  Image tiles of
  * tw x th = (w/tiles_x) x (h/tiles_y) pixels; tile (tx,ty) is owned by rank
  * (tx + ty) mod nranks.
  *
+ * rc_composite_tiles: the whole exchange + composite of this rank's tiles.
+ *   comm == NULL: composites this forest's own records for the tiles of
+ *   t->rank (one GPU: t = {tx, ty, 1, 0}).  comm != NULL (t->nranks and
+ *   t->rank must match it): the records are packed by owner on the device
+ *   (K5), the per-destination counts go through an NCCL all-to-all, and the
+ *   records through grouped ncclSend / ncclRecv on the caller's stream
+ *   (PAPER.md:1053-1056); the owner composites what it receives.  One host
+ *   synchronisation (the receive sizes).  Collective: every rank calls it.
+ *   Composite per owned pixel: order the records by (alpha_near, key) (total
+ *   order: then alpha_far, a, b), cut and average clusters of overlaps beyond
+ *   1e-6 max(1,alpha) (Eq. segsplit, Eq. segaverage, D14), fold
+ *   nearest-first with Eq. aggregate in fp64 and apply the background
+ *   I_v = A I_b + B.  Output d_rgba: float [my tiles in
+ *   row-major tile order][th][tw][4] = (R,G,B, 1-A).  At most 16384 records
+ *   per pixel (more: the pixel is NaN).
  * rc_pack_tiles: permutes the current segments by owner rank into the
- *   library-owned send buffer *d_send (rc_seg records) and writes
- *   h_send_counts[nranks] (records per destination, in rank order).  [sync]
- * rc_composite_tiles: per owned pixel, orders the given records by
- *   (alpha_near, key), cuts and averages overlaps beyond 1e-6 max(1,alpha)
- *   (Eq. segsplit, Eq. segaverage), folds nearest-first with Eq. aggregate
- *   in fp64 and applies the background I_v = A I_b + B.
- *   Output d_rgba: float [my tiles in row-major tile order][th][tw][4] =
- *   (R,G,B, 1-A).  d_recv may be the library's own segments (pass NULL to
- *   use them).  Async.
+ *   library-owned send buffer *d_send and writes h_send_counts[nranks]
+ *   (records per destination, in rank order); for callers that move the
+ *   records themselves.  [sync]
+ * rc_composite_records: the composite of caller-provided records d_recv
+ *   (device rc_seg [nrecv]; NULL = the forest's own records).  Async.
  * rc_composite: single-GPU shortcut: the whole image, d_rgba [h][w][4].
  * ---------------------------------------------------------------------- */
 typedef struct {
   int32_t tiles_x, tiles_y;   /* w % tiles_x == 0 and h % tiles_y == 0                 */
-  int32_t nranks, rank;
+  int32_t nranks, rank;       /* nranks <= 64                                           */
 } rc_tiling;
 
+rc_status rc_composite_tiles(rc_forest* f, const rc_tiling* t, rc_comm* comm, const float background[3],
+                             float* d_rgba, int64_t capacity_floats, void* stream);
 rc_status rc_pack_tiles(rc_forest* f, const rc_tiling* t, int64_t* h_send_counts, const rc_seg** d_send,
                         void* stream);
-rc_status rc_composite_tiles(rc_forest* f, const rc_tiling* t, const rc_seg* d_recv, int64_t nrecv,
-                             const float background[3], float* d_rgba, int64_t capacity_floats,
-                             void* stream);
+rc_status rc_composite_records(rc_forest* f, const rc_tiling* t, const rc_seg* d_recv, int64_t nrecv,
+                               const float background[3], float* d_rgba, int64_t capacity_floats, void* stream);
 rc_status rc_composite(rc_forest* f, const float background[3], float* d_rgba, int64_t capacity_floats,
                        void* stream);
 

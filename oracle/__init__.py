@@ -92,7 +92,7 @@ def lib():
         _lib.orc_render.restype = C.c_int64
         _lib.orc_render_ex.argtypes = [P(Scene_), P(Camera_), C.c_int, C.c_int, C.c_void_p, C.c_int64,
                                        C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p, C.c_int, C.c_void_p,
-                                       C.c_void_p, P(Pairs_)]
+                                       C.c_void_p, P(Pairs_), C.c_void_p]
         _lib.orc_render_ex.restype = C.c_int64
         _lib.orc_pairs_free.argtypes = [P(Pairs_)]
         _lib.orc_set_force_general.argtypes = [C.c_int]
@@ -202,7 +202,7 @@ class OracleScene:
 
 
     def render_pairs(self, pixels=None, mode="exact", N=None, background=(0.0, 0.0, 0.0), nthreads=0,
-                     with_cull=True):
+                     with_cull=True, rects=None):
         """orc_render_ex: pixel values plus, per pixel, the (elem, flags) of every
         hit or eps-ambiguous candidate pair (CSR: pair_off[npix+1], pair_elem,
         pair_flags) and the culled list of the same run.  mode "hits" skips the
@@ -215,6 +215,9 @@ class OracleScene:
         bg = np.ascontiguousarray(background, dtype=np.float64)
         rgba = np.zeros((npix, 4)); nh = np.zeros(npix, dtype=np.int32); na = np.zeros(npix, dtype=np.int32)
         n = self.anchor.shape[0]
+        if rects is not None:
+            with_cull = False
+            rects = np.ascontiguousarray(rects, dtype=np.int32)
         vis = np.zeros(n, dtype=np.int8) if with_cull else None
         amb = np.zeros(n, dtype=np.int8) if with_cull else None
         pr = Pairs_()
@@ -222,7 +225,7 @@ class OracleScene:
         total = lib().orc_render_ex(C.byref(self.s), C.byref(self.c), m, N, _ptr(bg), npix, _ptr(pixels),
                                     _ptr(rgba), _ptr(nh), _ptr(na), nthreads,
                                     _ptr(vis) if with_cull else None, _ptr(amb) if with_cull else None,
-                                    C.byref(pr))
+                                    C.byref(pr), _ptr(rects) if rects is not None else None)
         off = np.ctypeslib.as_array(pr.off, shape=(npix + 1,)).copy()
         tot = int(off[-1])
         elem = np.ctypeslib.as_array(pr.elem, shape=(max(tot, 1),))[:tot].copy()

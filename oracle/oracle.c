@@ -1057,7 +1057,7 @@ void orc_fold_pixel(int n, orc_hit* segs, double tau, const double background[3]
 static int64_t render_core(const orc_scene* sc, const orc_camera* cam, int mode, int N, const double background[3],
                            int64_t npix, const int32_t* pixels, double* rgba, int32_t* nhits, int32_t* namb,
                            int32_t cap, orc_hit* hits, int nthreads, int8_t* vis_out, int8_t* amb_out,
-                           orc_pairs* pairs) {
+                           orc_pairs* pairs, const int32_t* rects_in) {
 #ifdef _OPENMP
   if (nthreads > 0) omp_set_num_threads(nthreads);
 #endif
@@ -1066,9 +1066,13 @@ static int64_t render_core(const orc_scene* sc, const orc_camera* cam, int mode,
   int8_t* vis = (int8_t*)malloc(sc->n);
   int8_t* amb = (int8_t*)malloc(sc->n);
   int32_t* rects = (int32_t*)malloc(sizeof(int32_t) * 4 * sc->n);
-  orc_cull(sc, cam, vis, amb, rects);
-  if (vis_out) memcpy(vis_out, vis, sc->n);
-  if (amb_out) memcpy(amb_out, amb, sc->n);
+  if (rects_in) {   /* the culled rectangles of an earlier orc_cull of the same scene and camera */
+    memcpy(rects, rects_in, sizeof(int32_t) * 4 * sc->n);
+  } else {
+    orc_cull(sc, cam, vis, amb, rects);
+    if (vis_out) memcpy(vis_out, vis, sc->n);
+    if (amb_out) memcpy(amb_out, amb, sc->n);
+  }
   /* per-pixel (elem, flags) lists of every candidate with HIT or AMBIGUOUS */
   int64_t** pe = NULL;
   int32_t** pf = NULL;
@@ -1195,14 +1199,15 @@ int64_t orc_render(const orc_scene* sc, const orc_camera* cam, int mode, int N, 
                    int64_t npix, const int32_t* pixels, double* rgba, int32_t* nhits, int32_t* namb,
                    int32_t cap, orc_hit* hits, int nthreads) {
   return render_core(sc, cam, mode, N, background, npix, pixels, rgba, nhits, namb, cap, hits, nthreads, NULL,
-                     NULL, NULL);
+                     NULL, NULL, NULL);
 }
 
 int64_t orc_render_ex(const orc_scene* sc, const orc_camera* cam, int mode, int N, const double background[3],
                       int64_t npix, const int32_t* pixels, double* rgba, int32_t* nhits, int32_t* namb,
-                      int nthreads, int8_t* visible, int8_t* ambiguous, orc_pairs* pairs) {
+                      int nthreads, int8_t* visible, int8_t* ambiguous, orc_pairs* pairs,
+                      const int32_t* rects_in) {
   return render_core(sc, cam, mode, N, background, npix, pixels, rgba, nhits, namb, 0, NULL, nthreads, visible,
-                     ambiguous, pairs);
+                     ambiguous, pairs, rects_in);
 }
 
 void orc_pairs_free(orc_pairs* p) {

@@ -93,7 +93,9 @@ int64_t orc_render(const orc_scene* sc, const orc_camera* cam, int mode /*0 exac
  * (visible[n], ambiguous[n]) and, per rendered pixel, the (elem, flags) of
  * every candidate pair that hits or is eps-ambiguous (CSR, allocated here,
  * released by orc_pairs_free).  mode 2 = hit lists only (no integration;
- * rgba = 0). */
+ * rgba = 0).  rects_in (optional, [n][4]): the rectangles of an earlier
+ * orc_cull of the same scene and camera, reused instead of culling again
+ * (visible / ambiguous are then not written). */
 typedef struct {
   int64_t npix;
   int64_t* off;      /* [npix+1] */
@@ -102,7 +104,8 @@ typedef struct {
 } orc_pairs;
 int64_t orc_render_ex(const orc_scene* sc, const orc_camera* cam, int mode, int N, const double background[3],
                       int64_t npix, const int32_t* pixels, double* rgba, int32_t* nhits, int32_t* namb,
-                      int nthreads, int8_t* visible, int8_t* ambiguous, orc_pairs* pairs);
+                      int nthreads, int8_t* visible, int8_t* ambiguous, orc_pairs* pairs,
+                      const int32_t* rects_in);
 void orc_pairs_free(orc_pairs* p);
 
 /* Fold a caller-given list of segments of one pixel (any order): sort by

@@ -174,6 +174,16 @@ __global__ void k_compact(const int32_t* __restrict__ flag, const Rect16* __rest
   vis_rect[p] = rect[e];
 }
 
+// Partition weight of every leaf: pixel-centre rectangle area
+// (0 when culled) + 1.
+__global__ void k_leaf_weights(const int32_t* __restrict__ flag, const Rect16* __restrict__ rect, int64_t n,
+                               int64_t* __restrict__ w) {
+  const int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (e >= n) return;
+  const Rect16 r = rect[e];
+  w[e] = 1 + (flag[e] ? (int64_t)(r.i1 - r.i0 + 1) * (int64_t)(r.j1 - r.j0 + 1) : 0);
+}
+
 // ---------------------------------------------------------------------------
 // a3: pair generation.  Per visible leaf: rect area -> ceil(area/32) warp
 // chunks; exclusive scan -> chunk offsets; expand -> chunk -> leaf map.
@@ -442,6 +452,17 @@ __global__ void k_pack_scatter(const rc_seg* __restrict__ segs, const int64_t* _
     unsigned long long k = atomicAdd(&c[d], 1ull);
     out[dest_off[d] + base[d] + k] = rec;
   }
+}
+
+// exclusive prefix of the per-owner counts (<= 64 ranks) on the device
+__global__ void k_pack_offsets(const int64_t* __restrict__ counts, int nranks, int64_t* __restrict__ dest_off) {
+  if (threadIdx.x != 0) return;
+  int64_t run = 0;
+  for (int r = 0; r < nranks; ++r) {
+    dest_off[r] = run;
+    run += counts[r];
+  }
+  dest_off[nranks] = run;
 }
 
 // ---------------------------------------------------------------------------
@@ -1135,6 +1156,18 @@ cudaError_t launch_pack(const rc_seg* segs, const int64_t* nseg_p, int W, int tw
                         cudaStream_t s) {
   if (count) k_pack_count<<<grid, 256, 0, s>>>(segs, nseg_p, W, tw, th, tiles_x, nranks, counts);
   else k_pack_scatter<<<grid, 256, 0, s>>>(segs, nseg_p, W, tw, th, tiles_x, nranks, dest_off, cursor, out);
+  ++g_launches;
+  return cudaGetLastError();
+}
+
+cudaError_t launch_leaf_weights(const int32_t* flag, const Rect16* rect, int64_t n, int64_t* w, cudaStream_t s) {
+  k_leaf_weights<<<nblk(n, 256), 256, 0, s>>>(flag, rect, n, w);
+  ++g_launches;
+  return cudaGetLastError();
+}
+
+cudaError_t launch_pack_offsets(const int64_t* counts, int nranks, int64_t* dest_off, cudaStream_t s) {
+  k_pack_offsets<<<1, 32, 0, s>>>(counts, nranks, dest_off);
   ++g_launches;
   return cudaGetLastError();
 }

@@ -34,6 +34,8 @@ cudaError_t launch_coarsen(const rc_seg* recs, const uint32_t* perm, const int64
 cudaError_t launch_pack(const rc_seg* segs, const int64_t* nseg_p, int W, int tw, int th, int tiles_x, int nranks,
                         int64_t* counts, const int64_t* dest_off, int64_t* cursor, rc_seg* out, int grid, bool count,
                         cudaStream_t s);
+cudaError_t launch_leaf_weights(const int32_t* flag, const Rect16* rect, int64_t n, int64_t* w, cudaStream_t s);
+cudaError_t launch_pack_offsets(const int64_t* counts, int nranks, int64_t* dest_off, cudaStream_t s);
 cudaError_t launch_hist(const rc_seg* segs, int64_t n, int32_t* cnt, int grid, cudaStream_t s);
 cudaError_t launch_scatter(const rc_seg* segs, int64_t n, const int64_t* off, int32_t* cursor, uint32_t* out,
                            int grid, cudaStream_t s);

@@ -18,13 +18,16 @@ using namespace rc;
 
 static thread_local char g_err[1024] = "";
 
-static rc_status fail(rc_status st, const char* fmt, ...) {
+namespace rc {
+rc_status rc_fail(rc_status st, const char* fmt, ...) {
   va_list ap;
   va_start(ap, fmt);
   vsnprintf(g_err, sizeof g_err, fmt, ap);
   va_end(ap);
   return st;
 }
+}  // namespace rc
+#define fail rc_fail
 
 #define CU(call)                                                                                   \
   do {                                                                                             \
@@ -37,7 +40,7 @@ static rc_status fail(rc_status st, const char* fmt, ...) {
 #define LAUNCHED() (++g_launches)
 
 extern "C" const char* rc_last_error(void) { return g_err; }
-extern "C" int32_t rc_version(void) { return 1; }
+extern "C" int32_t rc_version(void) { return 2; }
 extern "C" int64_t rc_launch_count(int32_t reset) {
   int64_t v = g_launches;
   if (reset) g_launches = 0;
@@ -72,7 +75,7 @@ extern "C" rc_status rc_forest_create(const rc_forest_desc* d, void* stream, rc_
   if (d->geom_degree < 1 || d->geom_degree > 2) return fail(RC_ERR_INVALID_ARG, "geom_degree must be 1 or 2");
   if (d->field_degree < 1 || d->field_degree > 2) return fail(RC_ERR_INVALID_ARG, "field_degree must be 1 or 2");
   if (d->num_leaves < 1 || d->num_leaves > (int64_t)INT32_MAX) return fail(RC_ERR_INVALID_ARG, "num_leaves out of range");
-  if (!d->tree_ctrl || !d->leaf_anchor || !d->leaf_tree || !d->leaf_level || !d->leaf_field)
+  if (!d->tree_ctrl || !d->leaf_anchor || !d->leaf_tree || !d->leaf_level)
     return fail(RC_ERR_INVALID_ARG, "rc_forest_create: null array");
   if (d->memory != RC_HOST_COPY && d->memory != RC_DEVICE_COPY && d->memory != RC_HOST_COPY_TRUSTED)
     return fail(RC_ERR_INVALID_ARG, "bad memory mode");
@@ -104,8 +107,9 @@ extern "C" rc_status rc_forest_create(const rc_forest_desc* d, void* stream, rc_
       prev_tree = t;
       prev_key = key | (spread18(mask) | (spread18(mask) << 1) | (spread18(mask) << 2));
     }
-    for (int64_t q = 0; q < n * NF; ++q)
-      if (!isfinite(d->leaf_field[q])) return fail(RC_ERR_NUMERIC, "non-finite field value");
+    if (d->leaf_field)
+      for (int64_t q = 0; q < n * NF; ++q)
+        if (!isfinite(d->leaf_field[q])) return fail(RC_ERR_NUMERIC, "non-finite field value");
   }
   rc_forest* f = new rc_forest();
   f->K = d->num_trees;
@@ -114,6 +118,7 @@ extern "C" rc_status rc_forest_create(const rc_forest_desc* d, void* stream, rc_
   f->n = n;
   f->first_global = d->first_global_leaf;
   f->transfer = d->transfer;
+  f->has_field = d->leaf_field != nullptr;
   f->h_trees = new TreeConst[f->K];
   memset(f->h_trees, 0, sizeof(TreeConst) * f->K);
   cudaError_t e = cudaSuccess;
@@ -128,7 +133,7 @@ extern "C" rc_status rc_forest_create(const rc_forest_desc* d, void* stream, rc_
   ALLOC(f->d_anchor, sizeof(int32_t) * 3 * n);
   ALLOC(f->d_tree, sizeof(int32_t) * n);
   ALLOC(f->d_level, sizeof(int8_t) * n);
-  ALLOC(f->d_field, sizeof(float) * NF * n);
+  if (f->has_field) ALLOC(f->d_field, sizeof(float) * NF * n);
   ALLOC(f->d_flag, sizeof(int32_t) * n);
   ALLOC(f->d_rect_all, sizeof(Rect16) * n);
   ALLOC(f->d_scan, sizeof(int64_t) * (n + 1));
@@ -145,7 +150,7 @@ extern "C" rc_status rc_forest_create(const rc_forest_desc* d, void* stream, rc_
   if ((e = cudaMemcpyAsync(f->d_anchor, d->leaf_anchor, sizeof(int32_t) * 3 * n, kind, s)) ||
       (e = cudaMemcpyAsync(f->d_tree, d->leaf_tree, sizeof(int32_t) * n, kind, s)) ||
       (e = cudaMemcpyAsync(f->d_level, d->leaf_level, sizeof(int8_t) * n, kind, s)) ||
-      (e = cudaMemcpyAsync(f->d_field, d->leaf_field, sizeof(float) * NF * n, kind, s)) ||
+      (f->has_field && (e = cudaMemcpyAsync(f->d_field, d->leaf_field, sizeof(float) * NF * n, kind, s))) ||
       (e = cudaMemsetAsync(f->d_counters, 0, sizeof(int64_t) * CNT_TOTAL, s)))
     return cleanup(RC_ERR_CUDA, "cudaMemcpyAsync leaves");
   // host copy of the tree control points for rc_camera_set
@@ -167,7 +172,7 @@ extern "C" rc_status rc_forest_destroy(rc_forest* f) {
                   f->d_vis, f->d_vis_rect, f->d_chunk_off, f->d_counters, f->d_trees, f->d_cam,
                   f->d_scan_tmp, f->d_chunk_elem, f->d_segs, f->d_hits_pp, f->d_pix_cnt, f->d_pix_off,
                   f->d_perm, f->d_send, f->d_items, f->d_leaf_nodes[0], f->d_leaf_nodes[1], f->d_ucnt, f->d_uend, f->d_units,
-                  f->d_scratch, f->d_segs2, f->d_uoff, f->d_defer, f->d_sorted, f->d_tiles};
+                  f->d_scratch, f->d_segs2, f->d_uoff, f->d_defer, f->d_sorted, f->d_tiles, f->d_xcnt, f->d_recv};
   for (void* p : ptrs)
     if (p) dfree(p, 0, true);
   for (int c = 0; c <= RC_NODE_LEVELS; ++c)
@@ -179,6 +184,7 @@ extern "C" rc_status rc_forest_destroy(rc_forest* f) {
   for (int k = 0; k < 4; ++k)
     if (f->evb[k]) cudaEventDestroy(f->evb[k]);
   if (f->h_tiles) cudaFreeHost(f->h_tiles);
+  if (f->h_xcnt) cudaFreeHost(f->h_xcnt);
   delete[] f->h_trees;
   delete f;
   return RC_OK;
@@ -421,7 +427,7 @@ static DevLeafView leaf_view(rc_forest* f) { return DevLeafView{f->d_anchor, f->
 
 static unsigned blocks_for(int64_t n, int threads) { return (unsigned)((n + threads - 1) / threads); }
 
-extern "C" rc_status rc_cull(rc_forest* f, void* stream) {
+extern "C" rc_status rc_cull(rc_forest* f, void* stream, int64_t* d_num_visible) {
   if (!f) return fail(RC_ERR_INVALID_ARG, "rc_cull: null forest");
   if (!f->have_camera) return fail(RC_ERR_STATE, "rc_cull before rc_camera_set");
   cudaStream_t s = (cudaStream_t)stream;
@@ -436,8 +442,18 @@ extern "C" rc_status rc_cull(rc_forest* f, void* stream) {
   CU(launch_chunk_count(f->d_vis_rect, f->d_scan + n, n, f->d_chunk_off, f->d_counters, s));
   // in-place exclusive scan of the counts (each scan thread reads its items before writing them)
   CU(scan_exclusive<int64_t>(f->d_chunk_off, f->d_chunk_off, n, f->d_scan_tmp, s));
+  if (d_num_visible) CU(cudaMemcpyAsync(d_num_visible, f->d_scan + n, sizeof(int64_t), cudaMemcpyDeviceToDevice, s));
   f->have_cull = true;
   f->have_cast = false;
+  return RC_OK;
+}
+
+extern "C" rc_status rc_leaf_weights(rc_forest* f, int64_t* d_w, int64_t capacity, void* stream) {
+  if (!f || !d_w) return fail(RC_ERR_INVALID_ARG, "rc_leaf_weights: null argument");
+  if (!f->have_cull) return fail(RC_ERR_STATE, "rc_leaf_weights before rc_cull");
+  if (capacity < f->n) return fail(RC_ERR_CAPACITY, "rc_leaf_weights: capacity %lld < %lld leaves",
+                                   (long long)capacity, (long long)f->n);
+  CU(launch_leaf_weights(f->d_flag, f->d_rect_all, f->n, d_w, (cudaStream_t)stream));
   return RC_OK;
 }
 
@@ -474,6 +490,7 @@ static rc_status aggregate_to(rc_forest* f, int level, cudaStream_t s);
 extern "C" rc_status rc_cast_segments(rc_forest* f, int32_t fold_levels, void* stream) {
   if (!f) return fail(RC_ERR_INVALID_ARG, "rc_cast_segments: null forest");
   if (!f->have_cull) return fail(RC_ERR_STATE, "rc_cast_segments before rc_cull");
+  if (!f->has_field) return fail(RC_ERR_STATE, "rc_cast_segments on a forest without a field (keys only)");
   if (fold_levels < 0 || fold_levels > RC_NODE_LEVELS)
     return fail(RC_ERR_INVALID_ARG, "fold_levels must be in [0, %d]", RC_NODE_LEVELS);
   if (!f->all_affine && f->R != 2) return fail(RC_ERR_INVALID_ARG, "non-affine trees require geom_degree 2");
@@ -645,8 +662,30 @@ static rc_status check_tiling(rc_forest* f, const rc_tiling* t) {
   if (!t) return fail(RC_ERR_INVALID_ARG, "null tiling");
   if (t->tiles_x < 1 || t->tiles_y < 1 || f->cc.W % t->tiles_x || f->cc.H % t->tiles_y)
     return fail(RC_ERR_INVALID_ARG, "tiles must divide the image");
-  if (t->nranks < 1 || t->nranks > 64 || t->rank < 0 || t->rank >= t->nranks)
+  if (t->nranks < 1 || t->nranks > RC_MAX_RANKS || t->rank < 0 || t->rank >= t->nranks)
     return fail(RC_ERR_INVALID_ARG, "bad nranks/rank");
+  return RC_OK;
+}
+
+// K5: the current records permuted by owner rank into f->d_send on the
+// device (counts in d_counters[CNT_SEND..], exclusive offsets in
+// d_scan_tmp[0..nranks]); no host synchronisation.
+static rc_status pack_device(rc_forest* f, const rc_tiling* t, cudaStream_t s) {
+  const int tw = f->cc.W / t->tiles_x, th = f->cc.H / t->tiles_y;
+  CU(grow(&f->d_send, &f->send_cap, std::max<int64_t>(f->seg_cap, 1), s));
+  int64_t* d_cnt = f->d_counters + CNT_SEND;
+  static_assert(CNT_TOTAL >= CNT_SEND + RC_MAX_RANKS, "counter space");
+  int64_t* d_off = f->d_scan_tmp;
+  int64_t* d_cursor = f->d_scan_tmp + 80;
+  CU(cudaMemsetAsync(d_cnt, 0, sizeof(int64_t) * t->nranks, s));
+  CU(cudaMemsetAsync(d_cursor, 0, sizeof(int64_t) * t->nranks, s));
+  int64_t* d_nseg = f->d_counters + CNT_SEGS;
+  const int grid = sm_count() * 4;
+  CU(launch_pack(f->d_segs, d_nseg, f->cc.W, tw, th, t->tiles_x, t->nranks, d_cnt, nullptr, nullptr, nullptr, grid,
+                 true, s));
+  CU(launch_pack_offsets(d_cnt, t->nranks, d_off, s));
+  CU(launch_pack(f->d_segs, d_nseg, f->cc.W, tw, th, t->tiles_x, t->nranks, nullptr, d_off, d_cursor, f->d_send,
+                 grid, false, s));
   return RC_OK;
 }
 
@@ -657,41 +696,20 @@ extern "C" rc_status rc_pack_tiles(rc_forest* f, const rc_tiling* t, int64_t* h_
   rc_status st = check_tiling(f, t);
   if (st) return st;
   cudaStream_t s = (cudaStream_t)stream;
-  int tw = f->cc.W / t->tiles_x, th = f->cc.H / t->tiles_y;
-  int64_t nseg = 0;
-  CU(cudaMemcpyAsync(&nseg, f->d_counters + CNT_SEGS, sizeof(int64_t), cudaMemcpyDeviceToHost, s));
-  CU(cudaStreamSynchronize(s));
-  nseg = std::min(nseg, f->seg_cap);
-  CU(grow(&f->d_send, &f->send_cap, std::max<int64_t>(nseg, 1), s));
-  // counts in the counter block; [offsets(nranks+1) | cursors(nranks)] in the scan scratch
-  int64_t* d_cnt = f->d_counters + CNT_SEND;
-  static_assert(CNT_TOTAL >= CNT_SEND + 64, "counter space");
-  int64_t* d_off = f->d_scan_tmp;
-  int64_t* d_cursor = f->d_scan_tmp + 80;
-  CU(cudaMemsetAsync(d_cnt, 0, sizeof(int64_t) * t->nranks, s));
-  CU(cudaMemsetAsync(d_cursor, 0, sizeof(int64_t) * t->nranks, s));
-  int64_t* d_nseg = f->d_counters + CNT_SEGS;
-  int grid = sm_count() * 4;
-  CU(launch_pack(f->d_segs, d_nseg, f->cc.W, tw, th, t->tiles_x, t->nranks, d_cnt, nullptr, nullptr, nullptr, grid,
-                 true, s));
-  CU(cudaMemcpyAsync(h_send_counts, d_cnt, sizeof(int64_t) * t->nranks, cudaMemcpyDeviceToHost, s));
-  CU(cudaStreamSynchronize(s));
-  int64_t h_off[65];
-  h_off[0] = 0;
-  for (int r = 0; r < t->nranks; ++r) h_off[r + 1] = h_off[r] + h_send_counts[r];
-  CU(cudaMemcpyAsync(d_off, h_off, sizeof(int64_t) * (t->nranks + 1), cudaMemcpyHostToDevice, s));
-  CU(launch_pack(f->d_segs, d_nseg, f->cc.W, tw, th, t->tiles_x, t->nranks, nullptr, d_off, d_cursor, f->d_send,
-                 grid, false, s));
+  if ((st = pack_device(f, t, s))) return st;
+  CU(cudaMemcpyAsync(h_send_counts, f->d_counters + CNT_SEND, sizeof(int64_t) * t->nranks, cudaMemcpyDeviceToHost,
+                     s));
   CU(cudaStreamSynchronize(s));
   *d_send = f->d_send;
   return RC_OK;
 }
 
-extern "C" rc_status rc_composite_tiles(rc_forest* f, const rc_tiling* t, const rc_seg* d_recv, int64_t nrecv,
-                                        const float background[3], float* d_rgba, int64_t capacity_floats,
-                                        void* stream) {
-  if (!f || !d_rgba) return fail(RC_ERR_INVALID_ARG, "rc_composite_tiles: null argument");
-  if (!f->have_camera) return fail(RC_ERR_STATE, "rc_composite_tiles before rc_camera_set");
+extern "C" rc_status rc_composite_records(rc_forest* f, const rc_tiling* t, const rc_seg* d_recv, int64_t nrecv,
+                                          const float background[3], float* d_rgba, int64_t capacity_floats,
+                                          void* stream) {
+  if (!f || !d_rgba) return fail(RC_ERR_INVALID_ARG, "rc_composite_records: null argument");
+  if (!f->have_camera) return fail(RC_ERR_STATE, "rc_composite_records before rc_camera_set");
+  if (nrecv < 0 || (nrecv > 0 && !d_recv)) return fail(RC_ERR_INVALID_ARG, "rc_composite_records: bad records");
   rc_status st = check_tiling(f, t);
   if (st) return st;
   cudaStream_t s = (cudaStream_t)stream;
@@ -703,11 +721,11 @@ extern "C" rc_status rc_composite_tiles(rc_forest* f, const rc_tiling* t, const 
       if ((tx + ty) % t->nranks == t->rank) mine.push_back(ty * t->tiles_x + tx);
   const int64_t npix_out = (int64_t)mine.size() * tw * th;
   if (capacity_floats < 4 * npix_out)
-    return fail(RC_ERR_CAPACITY, "rc_composite_tiles: need %lld floats", (long long)(4 * npix_out));
+    return fail(RC_ERR_CAPACITY, "rc_composite: need %lld floats", (long long)(4 * npix_out));
   const rc_seg* src = d_recv;
   int64_t nsrc = nrecv;
   if (!src) {
-    if (!f->have_cast) return fail(RC_ERR_STATE, "rc_composite_tiles: no segments");
+    if (!f->have_cast) return fail(RC_ERR_STATE, "rc_composite: no segments");
     int64_t c = 0;
     CU(cudaMemcpyAsync(&c, f->d_counters + CNT_SEGS, sizeof(int64_t), cudaMemcpyDeviceToHost, s));
     CU(cudaStreamSynchronize(s));
@@ -786,11 +804,52 @@ extern "C" rc_status rc_composite_tiles(rc_forest* f, const rc_tiling* t, const 
   return RC_OK;
 }
 
+extern "C" rc_status rc_composite_tiles(rc_forest* f, const rc_tiling* t, rc_comm* comm, const float background[3],
+                                        float* d_rgba, int64_t capacity_floats, void* stream) {
+  if (!f || !t) return fail(RC_ERR_INVALID_ARG, "rc_composite_tiles: null argument");
+  if (!comm) return rc_composite_records(f, t, nullptr, 0, background, d_rgba, capacity_floats, stream);
+  if (!f->have_cast) return fail(RC_ERR_STATE, "rc_composite_tiles before rc_cast_segments");
+  if (comm->nranks != t->nranks || comm->rank != t->rank)
+    return fail(RC_ERR_INVALID_ARG, "rc_composite_tiles: tiling ranks %d/%d != communicator %d/%d", t->rank,
+                t->nranks, comm->rank, comm->nranks);
+  rc_status st = check_tiling(f, t);
+  if (st) return st;
+  cudaStream_t s = (cudaStream_t)stream;
+  const int P = t->nranks;
+  // K5: pack by owner on the device
+  if ((st = pack_device(f, t, s))) return st;
+  // count all-to-all (NCCL), then one read of both count vectors
+  if (!f->d_xcnt) CU(dmalloc((void**)&f->d_xcnt, sizeof(int64_t) * 2 * RC_MAX_RANKS, s));
+  if (!f->h_xcnt) CU(cudaMallocHost((void**)&f->h_xcnt, sizeof(int64_t) * 2 * RC_MAX_RANKS));
+  CU(cudaMemcpyAsync(f->d_xcnt, f->d_counters + CNT_SEND, sizeof(int64_t) * P, cudaMemcpyDeviceToDevice, s));
+  int r = nccl_alltoall_i64(comm, f->d_xcnt, f->d_xcnt + RC_MAX_RANKS, s);
+  if (r) return fail(RC_ERR_NCCL, "count all-to-all: %s", nccl_error_string(r));
+  CU(cudaMemcpyAsync(f->h_xcnt, f->d_xcnt, sizeof(int64_t) * 2 * RC_MAX_RANKS, cudaMemcpyDeviceToHost, s));
+  CU(cudaStreamSynchronize(s));   // the receive sizes (NCCL p2p takes host counts)
+  int64_t scnt[RC_MAX_RANKS], rcnt[RC_MAX_RANKS], soff[RC_MAX_RANKS], roff[RC_MAX_RANKS];
+  int64_t ts = 0, tr = 0;
+  for (int p = 0; p < P; ++p) {
+    scnt[p] = f->h_xcnt[p] * (int64_t)sizeof(rc_seg);
+    rcnt[p] = f->h_xcnt[RC_MAX_RANKS + p] * (int64_t)sizeof(rc_seg);
+    soff[p] = ts;
+    roff[p] = tr;
+    ts += scnt[p];
+    tr += rcnt[p];
+  }
+  const int64_t nrecv = tr / (int64_t)sizeof(rc_seg);
+  CU(grow(&f->d_recv, &f->recv_cap, std::max<int64_t>(nrecv, 1), s));
+  r = nccl_exchange(comm, reinterpret_cast<const char*>(f->d_send), soff, scnt, reinterpret_cast<char*>(f->d_recv),
+                    roff, rcnt, s);
+  if (r) return fail(RC_ERR_NCCL, "record exchange: %s", nccl_error_string(r));
+  f->h_last_recv = nrecv;
+  return rc_composite_records(f, t, f->d_recv, nrecv, background, d_rgba, capacity_floats, stream);
+}
+
 extern "C" rc_status rc_composite(rc_forest* f, const float background[3], float* d_rgba, int64_t capacity_floats,
                                   void* stream) {
   if (!f) return fail(RC_ERR_INVALID_ARG, "rc_composite: null forest");
   rc_tiling t{1, 1, 1, 0};
-  return rc_composite_tiles(f, &t, nullptr, 0, background, d_rgba, capacity_floats, stream);
+  return rc_composite_records(f, &t, nullptr, 0, background, d_rgba, capacity_floats, stream);
 }
 
 // One aggregation pass: the current records (node level f->rec_level) are
@@ -863,6 +922,89 @@ extern "C" rc_status rc_aggregate(rc_forest* f, int32_t cycles, void* stream) {
   return aggregate_to(f, f->rec_level + cycles, (cudaStream_t)stream);
 }
 
+extern "C" rc_status rc_segments_set(rc_forest* f, const rc_seg* d_recs, int64_t n, int32_t level, void* stream) {
+  if (!f || (n > 0 && !d_recs) || n < 0) return fail(RC_ERR_INVALID_ARG, "rc_segments_set: bad arguments");
+  if (!f->have_camera) return fail(RC_ERR_STATE, "rc_segments_set before rc_camera_set");
+  if (level < 0 || level > RC_NODE_LEVELS) return fail(RC_ERR_INVALID_ARG, "level must be in [0, %d]", RC_NODE_LEVELS);
+  cudaStream_t s = (cudaStream_t)stream;
+  CU(grow(&f->d_segs, &f->seg_cap, std::max<int64_t>(n + 4096, 1), s));
+  if (n > 0) CU(cudaMemcpyAsync(f->d_segs, d_recs, sizeof(rc_seg) * n, cudaMemcpyDeviceToDevice, s));
+  CU(cudaMemcpyAsync(f->d_counters + CNT_SEGS, &n, sizeof(int64_t), cudaMemcpyHostToDevice, s));
+  CU(cudaMemsetAsync(f->d_counters + CNT_OVERFLOW, 0, sizeof(int64_t), s));
+  CU(cudaStreamSynchronize(s));   // &n is a host stack value
+  f->rec_level = level;
+  f->h_seg_total = n;
+  f->have_cast = true;
+  return RC_OK;
+}
+
+extern "C" rc_status rc_debug_pair(rc_forest* f, int64_t local_leaf, int32_t i, int32_t j, rc_pair_result* out,
+                                   void* stream) {
+  if (!f || !out) return fail(RC_ERR_INVALID_ARG, "rc_debug_pair: null argument");
+  if (!f->have_camera) return fail(RC_ERR_STATE, "rc_debug_pair before rc_camera_set");
+  if (local_leaf < 0 || local_leaf >= f->n || i < 0 || j < 0 || i >= f->cc.W || j >= f->cc.H)
+    return fail(RC_ERR_INVALID_ARG, "rc_debug_pair: leaf or pixel out of range");
+  if (!f->all_affine && f->R != 2) return fail(RC_ERR_INVALID_ARG, "non-affine trees require geom_degree 2");
+  if (!f->has_field) return fail(RC_ERR_STATE, "rc_debug_pair on a forest without a field (keys only)");
+  cudaStream_t s = (cudaStream_t)stream;
+  const bool curved = !f->all_affine;
+  // a one-leaf, one-pixel work list through the frame's own segment kernel (fold level 0)
+  struct Dbg {
+    int32_t vis[4];
+    Rect16 rect[2];
+    int64_t chunk_off[2];
+    int32_t chunk_elem[4];
+    Unit unit;
+  } h;
+  memset(&h, 0, sizeof h);
+  h.vis[0] = (int32_t)local_leaf;
+  h.rect[0] = Rect16{(int16_t)i, (int16_t)i, (int16_t)j, (int16_t)j};
+  h.chunk_off[0] = 0;
+  h.chunk_off[1] = 1;
+  h.unit = Unit{0, 1, 0u, 0, 1, 0};
+  const int64_t npix = (int64_t)f->cc.W * f->cc.H;
+  const size_t scratch = curved ? cast_curved_scratch_per_cta() : 0;
+  const size_t off_cnt = 256, off_segs = off_cnt + sizeof(int64_t) * CNT_TOTAL, off_hits = off_segs + 8 * sizeof(rc_seg);
+  const size_t off_scr = (off_hits + sizeof(int32_t) * npix + 255) & ~(size_t)255;
+  char* d = nullptr;
+  CU(dmalloc((void**)&d, off_scr + scratch, s));
+  Dbg* dd = reinterpret_cast<Dbg*>(d);
+  int64_t* cnt = reinterpret_cast<int64_t*>(d + off_cnt);
+  rc_seg* segs = reinterpret_cast<rc_seg*>(d + off_segs);
+  int32_t* hits = reinterpret_cast<int32_t*>(d + off_hits);
+  cudaError_t e = cudaMemcpyAsync(dd, &h, sizeof h, cudaMemcpyHostToDevice, s);
+  if (!e) e = cudaMemsetAsync(cnt, 0, sizeof(int64_t) * CNT_TOTAL, s);
+  if (!e) e = cudaMemsetAsync(hits, 0, sizeof(int32_t) * npix, s);
+  if (!e) {
+    const uint32_t key_base = (uint32_t)f->first_global;
+    if (curved)
+      e = launch_cast_curved(f->cc, f->d_trees, leaf_view(f), f->P, dd->vis, dd->rect, dd->chunk_off, dd->chunk_elem,
+                             &dd->unit, 1, 0, key_base, d + off_scr, segs, 8, hits, cnt, 1, s);
+    else
+      e = launch_cast_affine(f->cc, f->d_trees, leaf_view(f), f->P, dd->vis, dd->rect, dd->chunk_off,
+                             dd->chunk_elem, 1, key_base, segs, 8, hits, cnt, 1, s);
+  }
+  int64_t hc[CNT_TOTAL];
+  rc_seg hs[8];
+  if (!e) e = cudaMemcpyAsync(hc, cnt, sizeof hc, cudaMemcpyDeviceToHost, s);
+  if (!e) e = cudaMemcpyAsync(hs, segs, sizeof hs, cudaMemcpyDeviceToHost, s);
+  if (!e) e = cudaStreamSynchronize(s);
+  dfree(d, s);
+  if (e) return fail(RC_ERR_CUDA, "rc_debug_pair: %s", cudaGetErrorString(e));
+  const int ns = (int)std::min<int64_t>(hc[CNT_SEGS], 4);
+  std::sort(hs, hs + ns, [](const rc_seg& x, const rc_seg& y) { return x.alpha_near < y.alpha_near; });
+  memset(out, 0, sizeof *out);
+  out->nseg = ns;
+  for (int k = 0; k < ns; ++k) {
+    out->alpha_near[k] = hs[k].alpha_near;
+    out->alpha_far[k] = hs[k].alpha_far;
+    out->a[k] = hs[k].a;
+    for (int c = 0; c < 3; ++c) out->b[k][c] = hs[k].b[c];
+  }
+  if (hc[CNT_NEWTON_FAIL] > 0) return fail(RC_ERR_NUMERIC, "rc_debug_pair: Newton did not converge");
+  return RC_OK;
+}
+
 extern "C" rc_status rc_node_table(rc_forest* f, int32_t level, int32_t* d_first, int64_t capacity, int64_t* count,
                                    void* stream) {
   if (!f || !count) return fail(RC_ERR_INVALID_ARG, "rc_node_table: null argument");
@@ -882,7 +1024,7 @@ extern "C" rc_status rc_render_frame(rc_forest* f, const rc_camera* cam, int32_t
                                      int64_t* hit_pairs, void* stream) {
   rc_status st;
   if ((st = rc_camera_set(f, cam, stream))) return st;
-  if ((st = rc_cull(f, stream))) return st;
+  if ((st = rc_cull(f, stream, nullptr))) return st;
   if ((st = rc_cast_segments(f, fold_levels, stream))) return st;
   if (cycles > 0 && (st = rc_aggregate(f, cycles, stream))) return st;
   if ((st = rc_composite(f, background, d_rgba, capacity_floats, stream))) return st;

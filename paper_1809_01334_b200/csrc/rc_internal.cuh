@@ -7,6 +7,7 @@
 #include "../../include/rc.h"
 
 #define RC_MAX_N 8          // GL points per segment
+#define RC_MAX_RANKS 64     // tile owners / communicator size
 #define RC_MAX_TREES 4096
 #define RC_MAXLEVEL 18
 #define RC_CHUNK 32         // candidate pairs per warp work item (one element)
@@ -81,6 +82,7 @@ struct __align__(8) Rect16 {
 struct rc_forest {
   int K, R, P;
   int64_t n, first_global;
+  bool has_field = true;           // false: keys-only forest (aggregation / partition bookkeeping)
   rc_transfer transfer;
   // device leaves
   int32_t* d_anchor = nullptr;
@@ -120,6 +122,10 @@ struct rc_forest {
   int64_t perm_cap = 0;
   rc_seg* d_send = nullptr;
   int64_t send_cap = 0;
+  rc_seg* d_recv = nullptr;        // records received by the tile exchange
+  int64_t recv_cap = 0, h_last_recv = 0;
+  int64_t* d_xcnt = nullptr;       // [2][RC_MAX_RANKS] send / receive counts of the exchange
+  int64_t* h_xcnt = nullptr;       // pinned copy
   // scan scratch
   int64_t* d_scan_tmp = nullptr;
   int64_t scan_tmp_cap = 0;
@@ -188,8 +194,19 @@ enum {
   CNT_TOTAL = 80
 };
 
+// NCCL communicator (comm.cu)
+struct rc_comm {
+  void* nccl = nullptr;   // ncclComm_t
+  int nranks = 1, rank = 0, device = 0;
+};
+
 // ---- kernels / launchers (defined in the .cu files) ----
 namespace rc {
+rc_status rc_fail(rc_status st, const char* fmt, ...);   // sets rc_last_error (rc_api.cu)
+const char* nccl_error_string(int r);
+int nccl_exchange(rc_comm* c, const char* sbuf, const int64_t* soff, const int64_t* scnt, char* rbuf,
+                  const int64_t* roff, const int64_t* rcnt, cudaStream_t s);
+int nccl_alltoall_i64(rc_comm* c, const int64_t* d_send, int64_t* d_recv, cudaStream_t s);
 extern int64_t g_launches;
 cudaError_t scan_exclusive_i64(const int64_t* in, int64_t* out, int64_t n, int64_t* tmp, cudaStream_t s);
 size_t scan_tmp_size(int64_t n);

@@ -1,12 +1,27 @@
-"""Multi-GPU plumbing of the tile exchange.
+"""Multi-GPU plumbing of the hot path.
 
-One process per GPU.  Each rank owns a contiguous SFC range of leaves
-(weights proportional to the visible pixel count),
-casts its segments, packs them by tile owner (tile (tx,ty) -> rank
-(tx+ty) mod P) with librc's rc_pack_tiles, and the records travel with two
-torch.distributed all_to_all_single calls (counts, then 32-byte records) —
-the path's only data-path collective.  The owner composites its tiles with
-rc_composite_tiles.  Nothing here computes any part of the method.
+One process per GPU.  Every rank owns a contiguous SFC range of leaves
+(PAPER.md:92-96).  What moves between ranks, and how:
+
+* pre-partition: after the first cull every rank knows
+  the weights w_E = visible pixel-centre rectangle area + 1 of its leaves
+  (rc_leaf_weights, "weight proportional to its visible pixel count",
+  PAPER.md:895-896); the SFC cuts move to equal prefix sums of the weights,
+  aligned to node starts of the coarsest level the fold and the coarsening
+  cycles reach, and the leaves move to their new owners (contiguous ranges:
+  only SFC neighbours exchange);
+* coarsening cycles: after each cycle but the last the
+  cuts move to equal prefix sums of the record counts of the final-level
+  nodes, and the records plus the leaf keys of the moved nodes go to their
+  new owners, where a keys-only forest continues the aggregation
+  (rc_segments_set + rc_aggregate);
+* tile exchange: every record goes to the owner of its
+  image tile -- inside librc over NCCL (rc_comm / rc_composite_tiles) when
+  the process group is NCCL, host-staged through the group otherwise (gloo,
+  used by the tests: two ranks on one GPU, no kernel waits on another).
+
+The partition arithmetic here is host / torch bookkeeping (prefix sums,
+searches, splits); no step of the method runs here.
 """
 from __future__ import annotations
 
@@ -16,6 +31,7 @@ import torch
 import torch.distributed as dist
 
 SEG_WORDS = 8   # rc_seg = 8 x 32-bit words
+MAXLEVEL = 18
 
 
 def tile_owner(tx: int, ty: int, nranks: int) -> int:
@@ -27,10 +43,76 @@ def my_tiles(tiles_x: int, tiles_y: int, nranks: int, rank: int) -> List[Tuple[i
     return [(tx, ty) for ty in range(tiles_y) for tx in range(tiles_x) if tile_owner(tx, ty, nranks) == rank]
 
 
+# ---------------------------------------------------------------------------
+# transport: torch.distributed, device tensors for NCCL, host-staged otherwise
+# ---------------------------------------------------------------------------
+class Transport:
+    def __init__(self, group=None):
+        self.group = group
+        self.world = dist.get_world_size(group)
+        self.rank = dist.get_rank(group)
+        self.host = dist.get_backend(group) != "nccl"
+
+    def _to(self, t):
+        if self.host:
+            return t.cpu()
+        return t if t.is_cuda else t.cuda()
+
+    def all_gather(self, t: torch.Tensor) -> torch.Tensor:
+        """[world, *t.shape]."""
+        src = self._to(t.contiguous())
+        out = [torch.empty_like(src) for _ in range(self.world)]
+        dist.all_gather(out, src, group=self.group)
+        return torch.stack(out).to(t.device)
+
+    def all_to_all_rows(self, send: torch.Tensor, send_counts: Sequence[int], recv_counts: Sequence[int]):
+        """Rows of `send` split by send_counts to the ranks in order; returns the
+        rows received, in rank order."""
+        dev = send.device
+        src = self._to(send.contiguous())
+        out = torch.empty((int(sum(recv_counts)),) + tuple(send.shape[1:]), dtype=send.dtype, device=src.device)
+        if self.host and dist.get_backend(self.group) == "gloo":
+            # gloo has no all_to_all: pairwise send / recv (contiguous ranges talk to neighbours mostly)
+            soff = [0]
+            for c in send_counts:
+                soff.append(soff[-1] + int(c))
+            roff = [0]
+            for c in recv_counts:
+                roff.append(roff[-1] + int(c))
+            out[roff[self.rank]:roff[self.rank + 1]] = src[soff[self.rank]:soff[self.rank + 1]]
+            ops = []
+            for p in range(self.world):
+                if p == self.rank:
+                    continue
+                if send_counts[p]:
+                    ops.append(dist.P2POp(dist.isend, src[soff[p]:soff[p + 1]].contiguous(), p, self.group))
+                if recv_counts[p]:
+                    ops.append(dist.P2POp(dist.irecv, out[roff[p]:roff[p + 1]], p, self.group))
+            if ops:
+                for w in dist.batch_isend_irecv(ops):
+                    w.wait()
+        else:
+            dist.all_to_all_single(out, src, output_split_sizes=[int(c) for c in recv_counts],
+                                   input_split_sizes=[int(c) for c in send_counts], group=self.group)
+        return out.to(dev)
+
+    def counts_all_to_all(self, counts: Sequence[int]) -> List[int]:
+        c = torch.tensor([int(x) for x in counts], dtype=torch.int64)
+        allc = self.all_gather(c)                      # [world(src), world(dst)]
+        return [int(x) for x in allc[:, self.rank].tolist()]
+
+    def max(self, x: float) -> float:
+        t = torch.tensor([float(x)], dtype=torch.float64)
+        return float(self.all_gather(t).max())
+
+
+# ---------------------------------------------------------------------------
+# partition arithmetic
+# ---------------------------------------------------------------------------
 def weighted_ranges(weights: torch.Tensor, nranks: int) -> List[Tuple[int, int]]:
     """Contiguous SFC ranges with (nearly) equal prefix sums of the per-leaf
-    weights (w_E = rect area + 1).  Cut r is
-    the first leaf whose inclusive prefix sum reaches r/P of the total."""
+    weights.  Cut r is placed after the
+    first leaf whose inclusive prefix sum reaches r/P of the total."""
     w = weights.to(torch.float64).flatten()
     n = w.numel()
     if n == 0:
@@ -46,17 +128,13 @@ def weighted_ranges(weights: torch.Tensor, nranks: int) -> List[Tuple[int, int]]
     return [(cuts[r], cuts[r + 1]) for r in range(nranks)]
 
 
-MAXLEVEL = 18
-
-
 def node_starts(anchor: torch.Tensor, tree: torch.Tensor, level: torch.Tensor, levels: int) -> torch.Tensor:
     """Bool mask over the SFC-ordered leaves: True where a node of coarsening
     level `levels` starts (level c+1 replaces every family of 8 consecutive
     same-level siblings of level c by the parent).  Cutting
     the SFC ranges only at these leaves keeps every family of the first
     `levels` coarsening cycles on one rank ("cuts are aligned to
-    family boundaries"), so fold and aggregation never need a neighbour's
-    leaves.  Vectorised torch (any device); host logic, no method arithmetic."""
+    family boundaries").  Vectorised torch (any device); bookkeeping only."""
     a = anchor.to(torch.int64)
     t = tree.to(torch.int64)
     lv = level.to(torch.int64)
@@ -102,29 +180,81 @@ def aligned_ranges(weights: torch.Tensor, nranks: int, allowed: torch.Tensor) ->
     return [(cuts[r], cuts[r + 1]) for r in range(nranks)]
 
 
-def exchange_records(send: torch.Tensor, counts: Sequence[int], group=None) -> torch.Tensor:
-    """All-to-all(v) of rc_seg records: `send` is [sum(counts), 8] int32 with
-    the records for rank d in rows [sum(counts[:d]), sum(counts[:d+1])).
-    Returns the records every rank sent to this one."""
-    world = dist.get_world_size(group)
-    dev = send.device
-    cnt = torch.tensor(list(counts), dtype=torch.int64, device=dev)
-    assert cnt.numel() == world
-    rcnt = torch.empty_like(cnt)
-    dist.all_to_all_single(rcnt, cnt, group=group)
-    rl = [int(x) for x in rcnt.tolist()]
-    recv = torch.empty((sum(rl), SEG_WORDS), dtype=torch.int32, device=dev)
-    dist.all_to_all_single(recv, send.contiguous(), output_split_sizes=rl, input_split_sizes=list(counts),
-                           group=group)
-    return recv
+def distributed_aligned_cuts(local_w: torch.Tensor, local_allowed: torch.Tensor, lo: int, n_total: int,
+                             tp: Transport) -> List[Tuple[int, int]]:
+    """aligned_ranges computed collectively: every rank holds only the weights
+    of its own range [lo, lo + len(local_w)) and the allowed cut positions in
+    it; the ranks exchange their totals and their candidate cuts (two small
+    all-gathers).  Same result as aligned_ranges on the concatenated weights
+    when every current cut is itself an allowed position."""
+    P = tp.world
+    w = local_w.to(torch.float64).flatten()
+    tot = torch.tensor([float(w.sum()) if w.numel() else 0.0], dtype=torch.float64)
+    tots = tp.all_gather(tot).flatten()
+    off = float(tots[:tp.rank].sum())
+    total = float(tots.sum())
+    big = torch.iinfo(torch.int64).max
+    cand = torch.full((max(P - 1, 1),), big, dtype=torch.int64)
+    if w.numel():
+        c = torch.cumsum(w, 0) + off
+        allowed_idx = torch.nonzero(local_allowed.to(torch.bool)).flatten().cpu()
+        hi = lo + w.numel()
+        for r in range(1, P):
+            target = total * r / P
+            if not (off < target <= float(c[-1])):   # exactly one rank holds the leaf reaching the target
+                continue
+            k = int(torch.searchsorted(c, torch.tensor(target, dtype=torch.float64, device=c.device))) + 1
+            raw = k   # local position of the raw cut (leaf k-1 is the first reaching the target)
+            j = int(torch.searchsorted(allowed_idx, torch.tensor(raw)))
+            cand[r - 1] = lo + int(allowed_idx[j]) if j < allowed_idx.numel() else hi
+    allc = tp.all_gather(cand)
+    cuts = [0]
+    for r in range(1, P):
+        v = int(allc[:, r - 1].min())
+        cuts.append(max(min(v if v != big else n_total, n_total), cuts[-1]))
+    cuts.append(n_total)
+    return [(cuts[r], cuts[r + 1]) for r in range(P)]
 
 
-def exchange_and_composite(forest, tiles, world: int, rank: int, background=(0.0, 0.0, 0.0), group=None):
-    """rc_pack_tiles -> all_to_all -> rc_composite_tiles; returns this rank's
-    tiles [ntiles][th][tw][4]."""
+def move_plan(old: Sequence[Tuple[int, int]], new: Sequence[Tuple[int, int]], rank: int):
+    """Rows this rank sends to / receives from every rank when contiguous
+    ranges change from `old` to `new` (only overlapping ranges talk)."""
+    lo, hi = old[rank]
+    nlo, nhi = new[rank]
+    send = [max(0, min(hi, b) - max(lo, a)) for a, b in new]
+    recv = [max(0, min(nhi, b) - max(nlo, a)) for a, b in old]
+    return send, recv
+
+
+def redistribute_rows(tensors, old, new, tp: Transport):
+    """Move the leaf rows of contiguous SFC ranges from `old` to `new`
+    ownership (PAPER.md:897-899 partition transfer)."""
+    send, recv = move_plan(old, new, tp.rank)
+    return [None if t is None else tp.all_to_all_rows(t, send, recv) for t in tensors]
+
+
+# ---------------------------------------------------------------------------
+# tile exchange
+# ---------------------------------------------------------------------------
+def exchange_records(send: torch.Tensor, counts: Sequence[int], tp: Transport) -> torch.Tensor:
+    """All-to-all(v) of rc_seg records ([sum(counts), 8] int32, grouped by
+    destination rank); returns the records every rank sent to this one."""
+    rl = tp.counts_all_to_all(counts)
+    return tp.all_to_all_rows(send, counts, rl)
+
+
+def exchange_and_composite(forest, tiles, world: int, rank: int, comm=None, tp: Transport = None,
+                           background=(0.0, 0.0, 0.0)):
+    """rc_composite_tiles over librc's NCCL communicator (comm), else
+    rc_pack_tiles -> host-staged all-to-all -> rc_composite_records.
+    Returns this rank's tiles [ntiles][th][tw][4]."""
     tiles_x, tiles_y = tiles
+    if comm is not None:
+        out, _ = forest.composite_tiles(tiles_x, tiles_y, world, rank, comm=comm, background=background)
+        return out
+    tp = tp or Transport()
     send, counts = forest.pack_tiles(tiles_x, tiles_y, world, rank)
-    recv = exchange_records(send, counts, group=group)
+    recv = exchange_records(send, counts, tp)
     out, _ = forest.composite_tiles(tiles_x, tiles_y, world, rank, recv=recv, background=background)
     return out
 
@@ -138,3 +268,77 @@ def assemble_image(tiles_out: dict, tiles_x: int, tiles_y: int, W: int, H: int) 
         for k, (tx, ty) in enumerate(mine):
             img[ty * th:(ty + 1) * th, tx * tw:(tx + 1) * tw] = t[k]
     return img
+
+
+def gather_image(out: torch.Tensor, tiles, W: int, H: int, tp: Transport):
+    """Every rank's tiles to rank 0 (all-gather of padded tile stacks);
+    returns the [H][W][4] image on rank 0 (host), None elsewhere."""
+    tiles_x, tiles_y = tiles
+    tw, th = W // tiles_x, H // tiles_y
+    maxt = max(len(my_tiles(tiles_x, tiles_y, tp.world, r)) for r in range(tp.world))
+    pad = torch.zeros((maxt, th, tw, 4), dtype=torch.float32, device=out.device)
+    pad[:out.shape[0]] = out
+    allt = tp.all_gather(pad).cpu()
+    if tp.rank != 0:
+        return None
+    res = {r: (allt[r, :len(my_tiles(tiles_x, tiles_y, tp.world, r))], my_tiles(tiles_x, tiles_y, tp.world, r))
+           for r in range(tp.world)}
+    return assemble_image(res, tiles_x, tiles_y, W, H)
+
+
+# ---------------------------------------------------------------------------
+# coarsening cycles with repartition between them (PAPER.md:981-992)
+# ---------------------------------------------------------------------------
+def aggregate_with_repartition(forest, keys, rng, ranges, cycles, final_level, tp: Transport, scene_consts):
+    """`cycles` aggregation cycles (rc_aggregate, one level each); between two
+    cycles the SFC cuts move to equal prefix sums of the record counts of the
+    final-level nodes and every moved node travels with its records and its
+    leaf keys (anchor, tree, level) to its new owner, which continues on a
+    keys-only forest ("repartition the elements, again
+    weighted by their (updated) ray count ... marshal/send and receive").
+    keys: this rank's (anchor, tree, level) device tensors of range `rng`;
+    ranges: every rank's current range.  Returns (forest, keys, rng, ranges,
+    moved_records); the returned forest is the caller's own (nothing moved)
+    or a keys-only forest made here (the caller closes it)."""
+    from . import rc
+    moved = 0
+    own = False   # the caller's forest is never closed here; keys-only forests made here are
+    for c in range(cycles):
+        forest.aggregate(1)
+        if c == cycles - 1 or tp.world == 1:
+            continue
+        lo, hi = rng
+        segs = forest.segments()
+        recs = segs["raw"].clone()
+        level = int(segs["level"])
+        # record count of every final-level node of this range (the new weights)
+        first = forest.node_table(final_level).to(torch.int64)     # local first leaves of the final nodes
+        nodes = torch.searchsorted(first, (recs[:, 7].to(torch.int64) & 0xFFFFFFFF) - lo, right=True) - 1
+        wnode = torch.bincount(nodes, minlength=first.numel()).to(torch.int64)
+        w = torch.zeros(hi - lo, dtype=torch.int64, device=recs.device)
+        w[first] = wnode + 1
+        allowed = torch.zeros(hi - lo, dtype=torch.bool, device=recs.device)
+        allowed[first] = True
+        n_total = ranges[-1][1]
+        new = distributed_aligned_cuts(w, allowed, lo, n_total, tp)
+        if new == ranges:
+            continue
+        # records to the owner of their node's first leaf
+        key = recs[:, 7].to(torch.int64) & 0xFFFFFFFF
+        cuts = torch.tensor([b for _, b in new[:-1]], dtype=torch.int64, device=recs.device)
+        dest = torch.searchsorted(cuts, key, right=True)
+        order = torch.argsort(dest, stable=True)
+        recs = recs[order]
+        counts = torch.bincount(dest, minlength=tp.world).tolist()
+        recv = exchange_records(recs, counts, tp)
+        moved += sum(counts) - counts[tp.rank]
+        keys = redistribute_rows(keys, ranges, new, tp)
+        if own:
+            forest.close()
+        own = True
+        ranges, rng = new, new[tp.rank]
+        ctrl, R, P, kappa0, inv_F, q0, cam = scene_consts
+        forest = rc.Forest(ctrl, R, P, keys[0], keys[1], keys[2], None, kappa0, inv_F, q0, first_global_leaf=rng[0])
+        forest.camera_set(cam)
+        forest.segments_set(recv, level)
+    return forest, keys, rng, ranges, moved

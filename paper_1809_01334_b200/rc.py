@@ -15,7 +15,8 @@ LIB_PATH = os.environ.get("RC_LIB") or os.path.join(HERE, "librc.so")   # RC_LIB
 RC_OK = 0
 RC_ERR_CAPACITY = -6
 STATUS_NAMES = {0: "RC_OK", -1: "RC_ERR_INVALID_ARG", -2: "RC_ERR_NOT_SFC_SORTED", -3: "RC_ERR_OUT_OF_MEMORY",
-                -4: "RC_ERR_CUDA", -6: "RC_ERR_CAPACITY", -7: "RC_ERR_STATE", -8: "RC_ERR_NUMERIC"}
+                -4: "RC_ERR_CUDA", -5: "RC_ERR_NCCL", -6: "RC_ERR_CAPACITY", -7: "RC_ERR_STATE",
+                -8: "RC_ERR_NUMERIC"}
 RC_HOST_COPY, RC_DEVICE_COPY, RC_HOST_COPY_TRUSTED = 0, 1, 2
 RC_PERSPECTIVE, RC_ORTHOGRAPHIC = 0, 1
 
@@ -53,15 +54,21 @@ class Segments(C.Structure):
                 ("hits_per_pixel", C.c_void_p)]
 
 
+class PairResult(C.Structure):
+    _fields_ = [("nseg", C.c_int32), ("alpha_near", C.c_float * 4), ("alpha_far", C.c_float * 4),
+                ("a", C.c_float * 4), ("b", (C.c_float * 3) * 4)]
+
+
 class Tiling(C.Structure):
     _fields_ = [("tiles_x", C.c_int32), ("tiles_y", C.c_int32), ("nranks", C.c_int32), ("rank", C.c_int32)]
 
 
 SEG_BYTES = 32
 EXPORTS = ["rc_last_error", "rc_version", "rc_forest_create", "rc_forest_destroy", "rc_camera_set", "rc_cull",
-           "rc_cull_result", "rc_cast_segments", "rc_segments_get", "rc_aggregate", "rc_pack_tiles",
-           "rc_composite_tiles", "rc_composite", "rc_render_frame", "rc_launch_count", "rc_last_cast_ms",
-           "rc_last_phase_ms", "rc_node_table", "rc_pool_trim"]
+           "rc_cull_result", "rc_leaf_weights", "rc_cast_segments", "rc_segments_get", "rc_segments_set",
+           "rc_debug_pair", "rc_aggregate", "rc_comm_unique_id", "rc_comm_create", "rc_comm_destroy",
+           "rc_pack_tiles", "rc_composite_tiles", "rc_composite_records", "rc_composite", "rc_render_frame",
+           "rc_launch_count", "rc_last_cast_ms", "rc_last_phase_ms", "rc_node_table", "rc_pool_trim"]
 
 _lib = None
 
@@ -80,14 +87,21 @@ def lib():
     L.rc_forest_create.argtypes = [C.POINTER(ForestDesc), vp, C.POINTER(vp)]
     L.rc_forest_destroy.argtypes = [vp]
     L.rc_camera_set.argtypes = [vp, C.POINTER(CameraDesc), vp]
-    L.rc_cull.argtypes = [vp, vp]
+    L.rc_cull.argtypes = [vp, vp, vp]
     L.rc_cull_result.argtypes = [vp, vp, i64, C.POINTER(i64), vp]
+    L.rc_leaf_weights.argtypes = [vp, vp, i64, vp]
+    L.rc_segments_set.argtypes = [vp, vp, i64, i32, vp]
+    L.rc_debug_pair.argtypes = [vp, i64, i32, i32, C.POINTER(PairResult), vp]
+    L.rc_comm_unique_id.argtypes = [C.POINTER(C.c_uint8 * 128)]
+    L.rc_comm_create.argtypes = [C.POINTER(C.c_uint8 * 128), i32, i32, vp, C.POINTER(vp)]
+    L.rc_comm_destroy.argtypes = [vp]
     L.rc_cast_segments.argtypes = [vp, i32, vp]
     L.rc_node_table.argtypes = [vp, i32, vp, i64, C.POINTER(i64), vp]
     L.rc_segments_get.argtypes = [vp, C.POINTER(Segments), vp]
     L.rc_aggregate.argtypes = [vp, i32, vp]
     L.rc_pack_tiles.argtypes = [vp, C.POINTER(Tiling), vp, C.POINTER(vp), vp]
-    L.rc_composite_tiles.argtypes = [vp, C.POINTER(Tiling), vp, i64, vp, vp, i64, vp]
+    L.rc_composite_tiles.argtypes = [vp, C.POINTER(Tiling), vp, vp, vp, i64, vp]
+    L.rc_composite_records.argtypes = [vp, C.POINTER(Tiling), vp, i64, vp, vp, i64, vp]
     L.rc_composite.argtypes = [vp, vp, vp, i64, vp]
     L.rc_render_frame.argtypes = [vp, C.POINTER(CameraDesc), i32, i32, vp, vp, i64, C.POINTER(i64), vp]
     L.rc_launch_count.argtypes = [i32]
@@ -161,25 +175,27 @@ class Forest:
         ctrl = np.ascontiguousarray(tree_ctrl if isinstance(tree_ctrl, np.ndarray) else tree_ctrl.cpu().numpy(),
                                     dtype=np.float64)
         on_dev = isinstance(leaf_anchor, torch.Tensor) and leaf_anchor.is_cuda
+        # leaf_field None: keys-only forest (aggregation / partition bookkeeping, no casting)
         if on_dev:
             keep = [leaf_anchor.contiguous().to(torch.int32), leaf_tree.contiguous().to(torch.int32),
-                    leaf_level.contiguous().to(torch.int8), leaf_field.contiguous().to(torch.float32)]
-            ptrs = [t.data_ptr() for t in keep]
+                    leaf_level.contiguous().to(torch.int8),
+                    None if leaf_field is None else leaf_field.contiguous().to(torch.float32)]
+            ptrs = [0 if t is None else t.data_ptr() for t in keep]
             mem = RC_DEVICE_COPY
         else:
             def npy(a, dt):
                 a = a.cpu().numpy() if isinstance(a, torch.Tensor) else a
                 return np.ascontiguousarray(a, dtype=dt)
             keep = [npy(leaf_anchor, np.int32), npy(leaf_tree, np.int32), npy(leaf_level, np.int8),
-                    npy(leaf_field, np.float32)]
-            ptrs = [k.ctypes.data for k in keep]
+                    None if leaf_field is None else npy(leaf_field, np.float32)]
+            ptrs = [0 if k is None else k.ctypes.data for k in keep]
             mem = RC_HOST_COPY_TRUSTED if trusted else RC_HOST_COPY
         n = int(keep[1].shape[0])
         self.n = n
         self.P = int(field_degree)
         self.R = int(geom_degree)
         desc = ForestDesc(int(ctrl.shape[0]), int(geom_degree), ctrl.ctypes.data, int(field_degree), n,
-                          int(first_global_leaf), ptrs[0], ptrs[1], ptrs[2], ptrs[3], mem,
+                          int(first_global_leaf), ptrs[0], ptrs[1], ptrs[2], ptrs[3] or None, mem,
                           Transfer(float(kappa0), float(inv_F), float(q0)))
         h = C.c_void_p()
         _check(L.rc_forest_create(C.byref(desc), _stream(stream), C.byref(h)))
@@ -216,8 +232,30 @@ class Forest:
         d = camera_desc(cam, **kw)
         _check(lib().rc_camera_set(self.h, C.byref(d), _stream(stream)))
 
-    def cull(self, stream=None):
-        _check(lib().rc_cull(self.h, _stream(stream)))
+    def cull(self, stream=None, d_num_visible=None):
+        """d_num_visible: optional int64 CUDA tensor receiving the visible count (async)."""
+        ptr = C.c_void_p(d_num_visible.data_ptr()) if d_num_visible is not None else None
+        _check(lib().rc_cull(self.h, _stream(stream), ptr))
+
+    def leaf_weights(self, out=None, stream=None):
+        """Partition weights w_E = rect area + 1 of the last cull (int64 CUDA tensor [n])."""
+        import torch
+        if out is None:
+            out = torch.empty(self.n, dtype=torch.int64, device="cuda")
+        _check(lib().rc_leaf_weights(self.h, C.c_void_p(out.data_ptr()), out.numel(), _stream(stream)))
+        return out
+
+    def segments_set(self, recs, level, stream=None):
+        """Import records (int32 CUDA tensor [n, 8]) as this forest's records at node level `level`."""
+        n = int(recs.shape[0])
+        ptr = C.c_void_p(recs.data_ptr()) if n else None
+        _check(lib().rc_segments_set(self.h, ptr, n, int(level), _stream(stream)))
+
+    def debug_pair(self, local_leaf, i, j, stream=None):
+        """One (leaf, pixel) pair evaluated by the segment kernel: list of (an, af, a, b[3])."""
+        r = PairResult()
+        _check(lib().rc_debug_pair(self.h, int(local_leaf), int(i), int(j), C.byref(r), _stream(stream)))
+        return [(r.alpha_near[k], r.alpha_far[k], r.a[k], tuple(r.b[k])) for k in range(r.nseg)]
 
     def cull_result(self, stream=None):
         import torch
@@ -274,8 +312,12 @@ class Forest:
         raw = device_view(ptr.value, (sum(cnt), 8), "<i4")
         return raw, cnt
 
-    def composite_tiles(self, tiles_x, tiles_y, nranks, rank, recv=None, background=(0.0, 0.0, 0.0), out=None,
-                        stream=None):
+    def composite_tiles(self, tiles_x, tiles_y, nranks, rank, recv=None, comm=None, background=(0.0, 0.0, 0.0),
+                        out=None, stream=None):
+        """This rank's tiles [ntiles][th][tw][4].  comm (a Comm): NCCL exchange
+        inside librc (rc_composite_tiles); recv (int32 [n, 8] CUDA tensor):
+        composite records moved by the caller (rc_composite_records); neither:
+        this forest's own records."""
         import torch
         t = Tiling(tiles_x, tiles_y, nranks, rank)
         tw, th = self.W // tiles_x, self.H // tiles_y
@@ -283,15 +325,18 @@ class Forest:
         if out is None:
             out = torch.empty((len(mine), th, tw, 4), dtype=torch.float32, device="cuda")
         bg = (C.c_float * 3)(*background)
-        rp = C.c_void_p(recv.data_ptr()) if recv is not None and recv.numel() else C.c_void_p(
-            0 if recv is None else 1)
-        if recv is not None and recv.numel() == 0:
-            # zero records received: pass a non-null pointer with count 0
-            dummy = torch.empty((1, 8), dtype=torch.int32, device="cuda")
-            rp = C.c_void_p(dummy.data_ptr())
-        nrecv = 0 if recv is None else int(recv.shape[0])
-        _check(lib().rc_composite_tiles(self.h, C.byref(t), rp, nrecv, bg, C.c_void_p(out.data_ptr()), out.numel(),
-                                        _stream(stream)))
+        if comm is not None:
+            _check(lib().rc_composite_tiles(self.h, C.byref(t), comm.h, bg, C.c_void_p(out.data_ptr()), out.numel(),
+                                            _stream(stream)))
+            return out, mine
+        if recv is None:
+            _check(lib().rc_composite_records(self.h, C.byref(t), None, 0, bg, C.c_void_p(out.data_ptr()),
+                                              out.numel(), _stream(stream)))
+            return out, mine
+        n = int(recv.shape[0])
+        keep = recv if n else torch.empty((1, 8), dtype=torch.int32, device="cuda")   # non-null, count 0
+        _check(lib().rc_composite_records(self.h, C.byref(t), C.c_void_p(keep.data_ptr()), n, bg,
+                                          C.c_void_p(out.data_ptr()), out.numel(), _stream(stream)))
         return out, mine
 
     def render_frame(self, cam, fold_levels=0, cycles=0, background=(0.0, 0.0, 0.0), out=None, stream=None):
@@ -312,6 +357,38 @@ class Forest:
 
     def last_phase_ms(self, phase):
         return float(lib().rc_last_phase_ms(self.h, int(phase)))
+
+
+class Comm:
+    """rc_comm: librc's NCCL communicator.  Collective over a torch.distributed
+    group: rank 0 draws the NCCL id (rc_comm_unique_id), the group broadcasts
+    its 128 bytes, every rank calls rc_comm_create on its current device."""
+
+    def __init__(self, nranks, rank, group=None, stream=None):
+        import torch
+        import torch.distributed as dist
+        uid = (C.c_uint8 * 128)()
+        if rank == 0:
+            _check(lib().rc_comm_unique_id(C.byref(uid)))
+        dev = "cuda" if dist.get_backend(group) == "nccl" else "cpu"
+        t = torch.tensor(list(bytes(uid)), dtype=torch.uint8, device=dev)
+        dist.broadcast(t, src=0, group=group)
+        uid = (C.c_uint8 * 128)(*t.cpu().tolist())
+        h = C.c_void_p()
+        _check(lib().rc_comm_create(C.byref(uid), int(nranks), int(rank), _stream(stream), C.byref(h)))
+        self.h = h
+        self.nranks, self.rank = int(nranks), int(rank)
+
+    def close(self):
+        if getattr(self, "h", None):
+            lib().rc_comm_destroy(self.h)
+            self.h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
 
 
 def pool_trim() -> None:

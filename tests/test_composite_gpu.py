@@ -137,3 +137,63 @@ def test_fold_and_composite_deterministic(fold, cycles):
         assert cnt == out[0][0]
         assert np.array_equal(recs, out[0][1])
         assert np.array_equal(img.view(np.uint32), out[0][2].view(np.uint32))
+
+
+def test_comm_single_rank_nccl_exchange():
+    """rc_comm over NCCL with one rank: rc_composite_tiles(comm) packs on the
+    device, exchanges the counts and the records through NCCL (the self block
+    is a device copy) and composites; equals the local composite bit for bit."""
+    import socket
+    import torch
+    import torch.distributed as dist
+    from paper_1809_01334_b200 import rc
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    port = s.getsockname()[1]
+    s.close()
+    dist.init_process_group("nccl", init_method=f"tcp://127.0.0.1:{port}", rank=0, world_size=1,
+                            device_id=torch.device("cuda", 0))
+    try:
+        sc = sg.shell_uniform(3, 96, 16, gl_points=6)
+        f = rc.Forest.from_scene(sc)
+        f.camera_set(sc.camera)
+        f.cull()
+        f.cast_segments(2)
+        ref = f.composite().cpu().numpy()
+        comm = rc.Comm(1, 0)
+        out, mine = f.composite_tiles(4, 4, 1, 0, comm=comm)
+        torch.cuda.synchronize()
+        from paper_1809_01334_b200 import dist as rdist
+        img = rdist.assemble_image({0: (out, mine)}, 4, 4, 96, 96).numpy()
+        assert np.array_equal(img.view(np.uint32), ref.view(np.uint32))
+        with pytest.raises(rc.RcError):
+            f.composite_tiles(4, 4, 2, 1, comm=comm)      # tiling ranks != communicator
+        comm.close()
+    finally:
+        dist.destroy_process_group()
+
+
+def test_debug_pair_matches_cast():
+    """rc_debug_pair evaluates one (leaf, pixel) pair with the frame's segment
+    kernel: equals the fold-0 records of that pair, and misses give none."""
+    from paper_1809_01334_b200 import rc
+    for sc in (sg.config2(width=64, maxlevel=5), sg.shell_uniform(2, 48, 8, gl_points=6)):
+        f = rc.Forest.from_scene(sc)
+        f.camera_set(sc.camera)
+        f.cull()
+        f.cast_segments(0)
+        raw = f.segments()["raw"].cpu().numpy()
+        W = sc.camera.width
+        rng = np.random.default_rng(0)
+        for k in rng.choice(raw.shape[0], 40, replace=False):
+            p, e = int(raw[k, 0]), int(raw[k, 7])
+            mine = raw[(raw[:, 0] == p) & (raw[:, 7] == e)].view(np.float32)
+            mine = mine[np.argsort(mine[:, 1])]
+            got = f.debug_pair(e, p % W, p // W)
+            assert len(got) == mine.shape[0]
+            for (an, af, a, b), r in zip(got, mine):
+                assert (an, af, a) == (r[1], r[2], r[3]) and tuple(b) == tuple(r[4:7])
+        # a pixel no ray hits anything at: no segment
+        hpp = f.segments()["hits_per_pixel"].cpu().numpy().reshape(-1)
+        empty = int(np.nonzero(hpp == 0)[0][0])
+        assert f.debug_pair(int(raw[0, 7]), empty % W, empty // W) == []

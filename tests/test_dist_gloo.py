@@ -23,21 +23,21 @@ def _free_port():
     return p
 
 
-def _run(rank, world, port, fn, q):
+def _run(rank, world, port, fn, q, *args):
     os.environ["MASTER_ADDR"] = "127.0.0.1"
     os.environ["MASTER_PORT"] = str(port)
     dist.init_process_group("gloo", rank=rank, world_size=world)
     try:
-        q.put((rank, fn(rank, world)))
+        q.put((rank, fn(rank, world, *args)))
     finally:
         dist.destroy_process_group()
 
 
-def _spawn(fn, world=2):
+def _spawn(fn, world=2, *args):
     ctx = mp.get_context("spawn")
     q = ctx.Queue()
     port = _free_port()
-    procs = [ctx.Process(target=_run, args=(r, world, port, fn, q)) for r in range(world)]
+    procs = [ctx.Process(target=_run, args=(r, world, port, fn, q) + args) for r in range(world)]
     for p in procs:
         p.start()
     out = dict(q.get(timeout=300) for _ in procs)
@@ -67,7 +67,7 @@ def _exchange_fn(rank, world):
         for k in range(counts[d]):
             rows.append([rank, d, k, 0, 0, 0, 0, rank * 100 + d * 10 + k])
     send = torch.tensor(rows, dtype=torch.int32)
-    recv = rdist.exchange_records(send, counts)
+    recv = rdist.exchange_records(send, counts, rdist.Transport())
     return recv.numpy()
 
 
@@ -109,7 +109,7 @@ def _protocol_fn(rank, world):
             rows[dest].append(rec)
     counts = [len(r) for r in rows]
     send = torch.tensor(np.array([x for r in rows for x in r]).reshape(-1, 8), dtype=torch.int32)
-    recv = rdist.exchange_records(send, counts).numpy()
+    recv = rdist.exchange_records(send, counts, rdist.Transport()).numpy()
     # fold my tiles' pixels with the oracle's per-pixel fold
     mine = rdist.my_tiles(tiles_x, tiles_y, world, rank)
     img = {}
@@ -163,3 +163,53 @@ def test_node_starts_match_coarsening_reference():
     a, t, l = sg.uniform_leaves(2, 3)
     m = rdist.node_starts(torch.as_tensor(a), torch.as_tensor(t), torch.as_tensor(l), 2)
     assert np.array_equal(np.nonzero(m.numpy())[0], np.arange(0, 2 * 512, 64))
+
+
+def _forest_weights(seed):
+    import scenegen as sg
+    sc = sg.config2(width=32, maxlevel=5)
+    A, T, L = (torch.as_tensor(x) for x in (sc.leaf_anchor, sc.leaf_tree, sc.leaf_level))
+    allowed = rdist.node_starts(A, T, L, 2)
+    w = torch.as_tensor(np.random.default_rng(seed).integers(1, 60, sc.num_leaves), dtype=torch.int64)
+    return w, allowed
+
+
+def _cuts_fn(rank, world, seed):
+    """Each rank holds only its own range's weights (equal-count aligned
+    ranges); the collective cut must equal aligned_ranges on all weights."""
+    w, allowed = _forest_weights(seed)
+    old = rdist.aligned_ranges(torch.ones(w.numel()), world, allowed)
+    lo, hi = old[rank]
+    tp = rdist.Transport()
+    new = rdist.distributed_aligned_cuts(w[lo:hi], allowed[lo:hi], lo, w.numel(), tp)
+    # move the rows of a per-leaf array and check we receive exactly our new range
+    idx = torch.arange(lo, hi, dtype=torch.int64)
+    moved = rdist.redistribute_rows([idx, idx.to(torch.int8).reshape(-1, 1).repeat(1, 3)], old, new, tp)
+    return new, moved[0].numpy(), moved[1].numpy()
+
+
+@pytest.mark.parametrize("world,seed", [(2, 1), (3, 2), (4, 3)])
+def test_distributed_weighted_cuts_and_leaf_moves_gloo(world, seed):
+    """SURVEY §8(e) partition: cuts at equal prefix sums of w_E, aligned to
+    node starts, computed collectively from per-rank weights (PAPER.md:895-899);
+    the leaf rows move to their new owners in SFC order."""
+    out = _spawn(_cuts_fn, world, seed)
+    w, allowed = _forest_weights(seed)
+    ref = rdist.aligned_ranges(w, world, allowed)
+    for rank, (new, idx, idx8) in out.items():
+        assert new == ref, (new, ref)
+        lo, hi = ref[rank]
+        assert np.array_equal(idx, np.arange(lo, hi))
+        assert np.array_equal(idx8[:, 0], np.arange(lo, hi).astype(np.int8))
+    # balance: every rank within one node's weight of the mean
+    tot = float(w.sum())
+    for lo, hi in ref:
+        assert abs(float(w[lo:hi].sum()) - tot / world) < tot / world * 0.25
+
+
+def test_move_plan_contiguous():
+    old = [(0, 10), (10, 20), (20, 30)]
+    new = [(0, 4), (4, 25), (25, 30)]
+    assert rdist.move_plan(old, new, 0) == ([4, 6, 0], [4, 0, 0])
+    assert rdist.move_plan(old, new, 1) == ([0, 10, 0], [6, 10, 5])
+    assert rdist.move_plan(old, new, 2) == ([0, 5, 5], [0, 0, 5])
