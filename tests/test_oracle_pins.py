@@ -336,6 +336,58 @@ def test_shell_aabb_contains_samples():
             assert np.all(X >= lo - 1e-13) and np.all(X <= hi + 1e-13)
 
 
+def test_shell_aabb_is_the_bernstein_box():
+    """AABB tightness: the culling box is exactly the camera-space
+    min/max of the element's 27 Bernstein-Bezier points, which this test forms
+    itself from the Lagrange points X_E({0,1/2,1}^3) by the per-axis
+    conversion b_mid = 2 x_mid - (x_0 + x_2)/2 (degree-2 Bernstein basis,
+    textbook identity).  A looser (or tighter) box fails."""
+    sh = sg.shell_uniform(1, 64, 4)
+    o = oracle.OracleScene(sh)
+    eta = (0.0, 0.5, 1.0)
+    for e in range(0, sh.num_leaves, 3):
+        L = np.array([[[o.element_map(e, [eta[m1], eta[m2], eta[m3]])[0] for m1 in range(3)] for m2 in range(3)]
+                      for m3 in range(3)])            # [m3][m2][m1][xyz]
+        B = L.copy()
+        for ax in (2, 1, 0):                          # numpy axis of m1, m2, m3
+            Bm = np.moveaxis(B, ax, 0)
+            Bm[1] = 2.0 * Bm[1] - 0.5 * (Bm[0] + Bm[2])
+        X = np.array([o.camera_transform(p) for p in B.reshape(-1, 3)])
+        lo, hi = o.aabb(e)
+        assert np.allclose(lo, X.min(axis=0), rtol=0, atol=1e-12) and np.allclose(hi, X.max(axis=0), rtol=0,
+                                                                                  atol=1e-12), e
+
+
+def test_constant_shell_exact_sphere_chord_P14():
+    """P14: f == const on the
+    cubed-sphere shell: every pixel is Eq. ABconstant over the ray's chord
+    through the exact spherical shell 0.55 <= |x| <= 1, up to the R=2
+    geometry's deviation from the sphere (~0.8 % of the radius).
+    Rays within 0.1 of tangency to either sphere are left out (the chord is
+    ill-conditioned there)."""
+    sc = sg.constant_field(sg.shell_uniform(2, 48, 4, gl_points=6), 0.6)
+    o = oracle.OracleScene(sc)
+    res = o.render(mode="exact", with_hits=False)
+    ft = float(np.float32(0.6))
+    kap = 5.0 * ft * ft
+    q = np.array([(1 + ft) / 2, (1 - ft) / 2, 0.5])
+    W = sc.camera.width
+    errs = []
+    for k, p in enumerate(res["pixels"]):
+        ro, rd = o.ray(int(p) % W, int(p) // W)
+        d = rd / np.linalg.norm(rd)
+        dist = np.linalg.norm(np.cross(ro, d))        # distance of the line from the centre
+        if dist > 0.9 or abs(dist - 0.55) < 0.1:
+            continue
+        L = 2.0 * math.sqrt(1.0 - dist * dist) - (2.0 * math.sqrt(0.55 ** 2 - dist * dist) if dist < 0.55 else 0.0)
+        A = math.exp(-kap * L)
+        ref = np.r_[q * (1 - A) / kap, 1 - A]
+        errs.append(float(np.abs(res["rgba"][k] - ref).max()))
+    errs = np.array(errs)
+    assert errs.size > 500
+    assert errs.max() < 0.03 and errs.mean() < 0.01, (errs.max(), errs.mean())
+
+
 def test_pixel_rect_similar_triangles():
     """Centered box at depth z, axis-aligned camera: rect width from
     similar triangles p = (n/l) X/Z + (w-1)/2."""
