@@ -52,6 +52,7 @@ __host__ __device__ constexpr int FI(int q, int NF) { return NF == 27 ? (q / 9) 
 constexpr int SLOT_FIELD = 108;
 constexpr int SLOT_AFF = 144;      // Xc[3], J0inv[9], dp[3], eta
 constexpr int SLOT_STRIDE = 164;   // 160 used; 164 mod 32 = 4 spreads slot banks, 656 B keeps 16-B alignment
+constexpr int SLOT_USED = 160;     // floats of a slot in the global slot buffer (640 B, one bulk copy)
 
 // one row (m3, m2) of 3 points by three 16-byte loads
 __device__ __forceinline__ void load_row(const float* __restrict__ sB, int row, float p0[3], float p1[3], float p2[3]) {
@@ -413,7 +414,7 @@ __device__ __noinline__ int face_roots_subdiv(const Patch& root, float tol, int 
 
 
 // ---------------------------------------------------------------------------
-// Element preparation by ONE thread (phase 0 runs one element per thread):
+// Element preparation by ONE thread (k_prep_slots, one element per thread):
 // the element slot (Bernstein points of X_E by restriction of the
 // tree's, fp64, stored fp32 relative to the origin B_(1,1,1); nodal field;
 // affine model A(xi) = Xc + J0 (xi - 1/2) and the bounds dp (nonlinear
@@ -421,7 +422,7 @@ __device__ __noinline__ int face_roots_subdiv(const Patch& root, float tol, int 
 // shuffles.  Restriction to [u, u+h] per axis: blossoms (u,u), (u,u+h),
 // (u+h,u+h) of the degree-2 Bernstein polynomial (de Casteljau).
 // ---------------------------------------------------------------------------
-__device__ __noinline__ void prep_element_t(float* __restrict__ sl, double* __restrict__ org,
+__device__ __forceinline__ void prep_element_t(float* __restrict__ sl, double* __restrict__ org,
                                             const TreeConst* __restrict__ trees, const DevLeafView& L, int e, int NF,
                                             bool with_field) {
   const double h = ldexp(1.0, -(int)L.level[e]);
@@ -614,7 +615,7 @@ union PhaseSmem {              // per-phase scratch of phases 0-2
   float scr[RC_MAX_N * CWARPS * 32];   // phase 2: per-thread node values
 };
 struct UnitMeta {
-  double org[RC_UNIT_LEAVES][3];        // element origins (fp64)
+  double org[RC_UNIT_LEAVES][4];        // element origins (fp64; 32-B rows, bulk-copied)
   Rect16 rect[RC_UNIT_LEAVES];          // pixel rectangles of the unit's elements
   int32_t pa[RC_UNIT_LEAVES];           // first pair of each element in this unit (rect raster index)
   int32_t pstart[RC_UNIT_LEAVES + 1];   // prefix of the elements' pair counts in the unit
@@ -641,13 +642,77 @@ struct CastSmem {
   } u;
 };
 struct CastCtl {
+  unsigned long long mbar;     // mbarrier of the unit's slot bulk copies
   int64_t unit;
+  int64_t ubeg, uend;          // this launch's unit range (the batch's units)
   int next_chunk;
   int nitems;
   unsigned long long base;
   int warp_sum[CWARPS];
   int bb[4];                   // unit pixel bounding rectangle: -i0, i1, -j0, j1 (atomicMax)
 };
+
+// ---- bulk copies global -> shared, tracked by an mbarrier (sm_90+ async proxy) ----
+__device__ __forceinline__ uint32_t smem_addr(const void* p) {
+  return (uint32_t)__cvta_generic_to_shared(p);
+}
+__device__ __forceinline__ void mbar_init(unsigned long long* bar, int count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_addr(bar)), "r"(count) : "memory");
+  asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+}
+__device__ __forceinline__ void mbar_arrive_expect_tx(unsigned long long* bar, uint32_t bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_addr(bar)), "r"(bytes) : "memory");
+}
+__device__ __forceinline__ void mbar_wait(unsigned long long* bar, uint32_t parity) {
+  asm volatile(
+      "{\n"
+      ".reg .pred p;\n"
+      "WAIT_%=:\n"
+      "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n"
+      "@!p bra WAIT_%=;\n"
+      "}\n" ::"r"(smem_addr(bar)),
+      "r"(parity)
+      : "memory");
+}
+__device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t bytes, unsigned long long* bar) {
+  asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+                   smem_addr(dst)),
+               "l"(src), "r"(bytes), "r"(smem_addr(bar))
+               : "memory");
+}
+// generic-proxy accesses of shared memory before async-proxy writes into it
+__device__ __forceinline__ void fence_proxy_async_smem() { asm volatile("fence.proxy.async.shared::cta;" ::: "memory"); }
+
+// ---- element preparation kernel -------------------------------------------
+// Slots of the visible leaves [v0, v1) (v1 clipped to the visible count) into
+// the global slot buffer (record v - v0: SLOT_USED floats + the fp64 origin as
+// 4 doubles), 64 elements per CTA staged in shared memory and written out
+// coalesced.  The segment kernel stages a unit's records with bulk copies.
+constexpr int PREP_THREADS = 64;
+template <int P>
+__global__ void __launch_bounds__(PREP_THREADS) k_prep_slots(const TreeConst* __restrict__ trees, DevLeafView L,
+                                                             const int32_t* __restrict__ vis,
+                                                             const int64_t* __restrict__ nvis_p, int64_t v0, int64_t v1,
+                                                             float4* __restrict__ gslot, double* __restrict__ gorg) {
+  constexpr int NF = (P + 1) * (P + 1) * (P + 1);
+  __shared__ __align__(16) float sl[PREP_THREADS][SLOT_STRIDE];
+  __shared__ double so[PREP_THREADS][4];
+  const int64_t vend = min(v1, *nvis_p);
+  const int64_t vb = v0 + (int64_t)blockIdx.x * PREP_THREADS;
+  if (vb >= vend) return;
+  const int nloc = (int)min((int64_t)PREP_THREADS, vend - vb);
+  const int tid = threadIdx.x;
+  if (tid < nloc) {
+    prep_element_t(sl[tid], so[tid], trees, L, vis[vb + tid], NF, true);
+    so[tid][3] = 0.0;
+  }
+  __syncthreads();
+  constexpr int Q = SLOT_USED / 4;   // float4 per slot
+  float4* dst = gslot + (vb - v0) * Q;
+  for (int k = tid; k < nloc * Q; k += PREP_THREADS) dst[k] = reinterpret_cast<const float4*>(sl[k / Q])[k % Q];
+  double* od = gorg + (vb - v0) * 4;
+  for (int k = tid; k < nloc * 4; k += PREP_THREADS) od[k] = so[k / 4][k % 4];
+}
 
 // per-CTA global scratch (bytes)
 constexpr size_t SCR_ITEMS = (size_t)ITEM_CAP * 64;
@@ -1361,8 +1426,10 @@ __global__ void __launch_bounds__(CWARPS * 32, CAST_CTAS_PER_SM) k_cast_curved(C
                                                                 unsigned char* __restrict__ scratch,
                                                                 rc_seg* __restrict__ out, int64_t out_cap,
                                                                 int32_t* __restrict__ hits_pp,
-                                                                int64_t* __restrict__ counters) {
-  constexpr int NF = (P + 1) * (P + 1) * (P + 1);
+                                                                int64_t* __restrict__ counters,
+                                                                const float4* __restrict__ gslot,
+                                                                const double* __restrict__ gorg, int64_t v0,
+                                                                int64_t v1) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
   CastSmem& S = *reinterpret_cast<CastSmem*>(smem_raw);
   __shared__ CastCtl ctl;
@@ -1375,6 +1442,25 @@ __global__ void __launch_bounds__(CWARPS * 32, CAST_CTAS_PER_SM) k_cast_curved(C
   int local_hits = 0, face_fail = 0, fails = 0;
   long long raw_local = 0, n_tasks = 0, n_fallback = 0;
   int prev_items = 0;
+  uint32_t mbar_parity = 0;
+  if (tid == 0) {
+    mbar_init(&ctl.mbar, 1);
+    // this launch's units: those whose visible window starts in [v0, v1) (units are in vfirst order)
+    int64_t lo = 0, hi = nunits;
+    while (lo < hi) {
+      const int64_t mid = (lo + hi) >> 1;
+      if (units[mid].vfirst < v0) lo = mid + 1;
+      else hi = mid;
+    }
+    ctl.ubeg = lo;
+    hi = nunits;
+    while (lo < hi) {
+      const int64_t mid = (lo + hi) >> 1;
+      if (units[mid].vfirst < v1) lo = mid + 1;
+      else hi = mid;
+    }
+    ctl.uend = lo;
+  }
   for (;;) {
     __syncthreads();   // the previous unit's shared state (ctl, S) and scratch are no longer read
     if (prev_items > 0) {
@@ -1382,15 +1468,26 @@ __global__ void __launch_bounds__(CWARPS * 32, CAST_CTAS_PER_SM) k_cast_curved(C
       if (fold > 0) discard_l2(segs, ((size_t)prev_items * sizeof(rc_seg) + 127) & ~(size_t)127);
     }
     if (tid == 0) {
-      ctl.unit = (int64_t)atomicAdd((unsigned long long*)&counters[CNT_UNITS], 1ull);
+      ctl.unit = ctl.ubeg + (int64_t)atomicAdd((unsigned long long*)&counters[CNT_UNITS], 1ull);
       ctl.next_chunk = 0;
       ctl.nitems = 0;
     }
     __syncthreads();
     const int64_t u = ctl.unit;
-    if (u >= nunits) break;
+    if (u >= ctl.uend) break;
     const Unit U = units[u];
-    // ---- phase 0: the unit's elements into shared memory ---------------------
+    // ---- phase 0: the unit's prepared element slots arrive by bulk copies ----
+    // (k_prep_slots made them; one 640-byte record per element plus the fp64
+    // origins), tracked by the CTA's mbarrier while the threads set up the
+    // unit's pair bookkeeping
+    if (tid == 0) {
+      fence_proxy_async_smem();   // the previous unit's generic reads of the slots are done (barrier above)
+      const int64_t g0 = U.vfirst - v0;
+      mbar_arrive_expect_tx(&ctl.mbar, (uint32_t)U.nvis * (SLOT_USED * 4 + 32));
+      for (int w = 0; w < U.nvis; ++w)
+        bulk_g2s(S.u.p.slot[w], gslot + (g0 + w) * (SLOT_USED / 4), SLOT_USED * 4, &ctl.mbar);
+      bulk_g2s(S.meta.org, gorg + g0 * 4, (uint32_t)U.nvis * 32, &ctl.mbar);
+    }
     if (tid < 4) ctl.bb[tid] = -0x7fffffff;
     __syncthreads();
     for (int w = tid; w < U.nvis; w += CWARPS * 32) {
@@ -1423,8 +1520,8 @@ __global__ void __launch_bounds__(CWARPS * 32, CAST_CTAS_PER_SM) k_cast_curved(C
       if (a1 <= U.nvis) S.meta.pstart[a1] = incl;
       if (lane == 0) S.meta.pstart[0] = 0;
     }
-    for (int w = tid; w < U.nvis; w += CWARPS * 32)
-      prep_element_t(S.u.p.slot[w], S.meta.org[w], trees, L, vis[U.vfirst + w], NF, true);
+    mbar_wait(&ctl.mbar, mbar_parity);
+    mbar_parity ^= 1u;
     __syncthreads();
     for (int w = tid; w < U.nvis; w += CWARPS * 32) {   // chunk -> first element map
       const int a = S.meta.pstart[w], b = S.meta.pstart[w + 1];
@@ -1596,7 +1693,8 @@ template <int P, int N>
 static cudaError_t cast_PN(const CamConst& cc, const TreeConst* trees, DevLeafView L, const int32_t* vis,
                            const Rect16* vrect, const int64_t* chunk_off, const int32_t* chunk_elem, const Unit* units,
                            int64_t nunits, int fold, uint32_t key_base, void* scratch, rc_seg* out, int64_t out_cap,
-                           int32_t* hits_pp, int64_t* counters, int grid, cudaStream_t s) {
+                           int32_t* hits_pp, int64_t* counters, int grid, const float4* gslot, const double* gorg,
+                           int64_t v0, int64_t v1, cudaStream_t s) {
   const size_t smem = sizeof(CastSmem);
   static bool attr = false;
   if (!attr) {
@@ -1606,7 +1704,22 @@ static cudaError_t cast_PN(const CamConst& cc, const TreeConst* trees, DevLeafVi
   }
   k_cast_curved<P, N><<<grid, CWARPS * 32, smem, s>>>(cc, trees, L, vis, vrect, chunk_off, chunk_elem, units, nunits,
                                                       fold, key_base, (unsigned char*)scratch, out, out_cap, hits_pp,
-                                                      counters);
+                                                      counters, gslot, gorg, v0, v1);
+  return cudaGetLastError();
+}
+
+size_t slot_record_bytes() { return SLOT_USED * sizeof(float) + 4 * sizeof(double); }
+
+cudaError_t launch_prep_slots(const TreeConst* trees, DevLeafView L, int P, const int32_t* vis,
+                              const int64_t* nvis_p, int64_t v0, int64_t v1, void* gslot, void* gorg,
+                              cudaStream_t s) {
+  if (v1 <= v0) return cudaSuccess;
+  const unsigned grid = (unsigned)((v1 - v0 + PREP_THREADS - 1) / PREP_THREADS);
+  if (P == 1)
+    k_prep_slots<1><<<grid, PREP_THREADS, 0, s>>>(trees, L, vis, nvis_p, v0, v1, (float4*)gslot, (double*)gorg);
+  else
+    k_prep_slots<2><<<grid, PREP_THREADS, 0, s>>>(trees, L, vis, nvis_p, v0, v1, (float4*)gslot, (double*)gorg);
+  ++g_launches;
   return cudaGetLastError();
 }
 
@@ -1614,12 +1727,13 @@ cudaError_t launch_cast_curved(const CamConst& cc, const TreeConst* trees, DevLe
                                const Rect16* vrect, const int64_t* chunk_off, const int32_t* chunk_elem,
                                const Unit* units, int64_t nunits, int fold, uint32_t key_base, void* scratch,
                                rc_seg* out, int64_t out_cap, int32_t* hits_pp, int64_t* counters, int grid,
-                               cudaStream_t s) {
+                               const void* gslot, const void* gorg, int64_t v0, int64_t v1, cudaStream_t s) {
   ++g_launches;
 #define CASE(PP, NN)                                                                                             \
   if (P == PP && cc.N == NN)                                                                                     \
     return cast_PN<PP, NN>(cc, trees, L, vis, vrect, chunk_off, chunk_elem, units, nunits, fold, key_base, scratch, \
-                           out, out_cap, hits_pp, counters, grid, s);
+                           out, out_cap, hits_pp, counters, grid, (const float4*)gslot, (const double*)gorg, v0, v1, \
+                           s);
   CASE(1, 1) CASE(1, 2) CASE(1, 3) CASE(1, 4) CASE(1, 5) CASE(1, 6) CASE(1, 7) CASE(1, 8)
   CASE(2, 1) CASE(2, 2) CASE(2, 3) CASE(2, 4) CASE(2, 5) CASE(2, 6) CASE(2, 7) CASE(2, 8)
 #undef CASE

@@ -25,7 +25,12 @@ cudaError_t launch_cast_curved(const CamConst& cc, const TreeConst* trees, DevLe
                                const Rect16* vrect, const int64_t* chunk_off, const int32_t* chunk_elem,
                                const Unit* units, int64_t nunits, int fold, uint32_t key_base, void* scratch,
                                rc_seg* out, int64_t out_cap, int32_t* hits_pp, int64_t* counters, int grid,
-                               cudaStream_t s);
+                               const void* gslot, const void* gorg, int64_t v0, int64_t v1, cudaStream_t s);
+// element slots of the visible leaves [v0, v1) for the curved segment kernel (slot_record_bytes() each)
+cudaError_t launch_prep_slots(const TreeConst* trees, DevLeafView L, int P, const int32_t* vis,
+                              const int64_t* nvis_p, int64_t v0, int64_t v1, void* gslot, void* gorg,
+                              cudaStream_t s);
+size_t slot_record_bytes();
 size_t cast_curved_scratch_per_cta();
 int cast_curved_ctas_per_sm();
 cudaError_t launch_coarsen(const rc_seg* recs, const uint32_t* perm, const int64_t* off, int64_t npix,

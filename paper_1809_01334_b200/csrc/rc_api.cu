@@ -172,7 +172,7 @@ extern "C" rc_status rc_forest_destroy(rc_forest* f) {
                   f->d_vis, f->d_vis_rect, f->d_chunk_off, f->d_counters, f->d_trees, f->d_cam,
                   f->d_scan_tmp, f->d_chunk_elem, f->d_segs, f->d_hits_pp, f->d_pix_cnt, f->d_pix_off,
                   f->d_perm, f->d_send, f->d_items, f->d_leaf_nodes[0], f->d_leaf_nodes[1], f->d_ucnt, f->d_uend, f->d_units,
-                  f->d_scratch, f->d_segs2, f->d_uoff, f->d_defer, f->d_sorted, f->d_tiles, f->d_xcnt, f->d_recv};
+                  f->d_scratch, f->d_segs2, f->d_uoff, f->d_defer, f->d_sorted, f->d_tiles, f->d_xcnt, f->d_recv, f->d_gslot};
   for (void* p : ptrs)
     if (p) dfree(p, 0, true);
   for (int c = 0; c <= RC_NODE_LEVELS; ++c)
@@ -539,6 +539,17 @@ extern "C" rc_status rc_cast_segments(rc_forest* f, int32_t fold_levels, void* s
     f->scratch_bytes = cast_curved_scratch_per_cta() * (size_t)grid_curved;
     CU(dmalloc((void**)&f->d_scratch, f->scratch_bytes, s));
   }
+  // element slots (k_prep_slots): the visible list in batches of at most
+  // RC_SLOT_BATCH leaves (+ one unit window of margin), bounded memory
+  const int64_t slot_need = curved ? std::min<int64_t>(nvis + RC_UNIT_LEAVES, RC_SLOT_BATCH + RC_UNIT_LEAVES) : 0;
+  if (curved && f->slot_cap < slot_need) {
+    if (f->d_gslot) dfree(f->d_gslot, s);
+    f->d_gslot = nullptr;
+    f->slot_cap = 0;
+    CU(dmalloc((void**)&f->d_gslot, slot_record_bytes() * (size_t)slot_need, s));
+    f->slot_cap = slot_need;
+  }
+  const int64_t batch = std::max<int64_t>(f->slot_cap - RC_UNIT_LEAVES, 1);
   // record capacity: the previous frame's count, else an estimate; a too
   // small buffer is grown to the exact count and the cast repeated
   // reuse the larger of the two record buffers (aggregation swaps them)
@@ -572,9 +583,18 @@ extern "C" rc_status rc_cast_segments(rc_forest* f, int32_t fold_levels, void* s
                               f->d_chunk_elem, f->h_chunks, key_base, f->d_segs, f->seg_cap, f->d_hits_pp,
                               f->d_counters, sm_count() * 8, s));
       } else {
-        CU(launch_cast_curved(f->cc, f->d_trees, leaf_view(f), f->P, f->d_vis, f->d_vis_rect, f->d_chunk_off,
-                              f->d_chunk_elem, f->d_units, nunits, fold_levels, key_base, f->d_scratch,
-                              f->d_segs, f->seg_cap, f->d_hits_pp, f->d_counters, grid_curved, s));
+        char* gslot = reinterpret_cast<char*>(f->d_gslot);
+        char* gorg = gslot + (size_t)f->slot_cap * (slot_record_bytes() - 32);
+        for (int64_t v0 = 0; v0 < nvis; v0 += batch) {
+          const int64_t v1 = std::min(nvis, v0 + batch);
+          CU(cudaMemsetAsync(f->d_counters + CNT_UNITS, 0, sizeof(int64_t), s));
+          CU(launch_prep_slots(f->d_trees, leaf_view(f), f->P, f->d_vis, f->d_scan + n, v0,
+                               std::min(nvis, v1 + RC_UNIT_LEAVES), gslot, gorg, s));
+          CU(launch_cast_curved(f->cc, f->d_trees, leaf_view(f), f->P, f->d_vis, f->d_vis_rect, f->d_chunk_off,
+                                f->d_chunk_elem, f->d_units, nunits, fold_levels, key_base, f->d_scratch,
+                                f->d_segs, f->seg_cap, f->d_hits_pp, f->d_counters, grid_curved, gslot, gorg, v0,
+                                v1, s));
+        }
       }
     }
     CU(cudaEventRecord(f->ev1, s));
@@ -962,12 +982,15 @@ extern "C" rc_status rc_debug_pair(rc_forest* f, int64_t local_leaf, int32_t i, 
   h.chunk_off[0] = 0;
   h.chunk_off[1] = 1;
   h.unit = Unit{0, 1, 0u, 0, 1, 0};
+  static const int64_t one = 1;
   const int64_t npix = (int64_t)f->cc.W * f->cc.H;
   const size_t scratch = curved ? cast_curved_scratch_per_cta() : 0;
   const size_t off_cnt = 256, off_segs = off_cnt + sizeof(int64_t) * CNT_TOTAL, off_hits = off_segs + 8 * sizeof(rc_seg);
   const size_t off_scr = (off_hits + sizeof(int32_t) * npix + 255) & ~(size_t)255;
+  const size_t off_slot = (off_scr + scratch + 255) & ~(size_t)255;
+  const size_t off_org = off_slot + slot_record_bytes();
   char* d = nullptr;
-  CU(dmalloc((void**)&d, off_scr + scratch, s));
+  CU(dmalloc((void**)&d, off_org + 64, s));
   Dbg* dd = reinterpret_cast<Dbg*>(d);
   int64_t* cnt = reinterpret_cast<int64_t*>(d + off_cnt);
   rc_seg* segs = reinterpret_cast<rc_seg*>(d + off_segs);
@@ -977,15 +1000,23 @@ extern "C" rc_status rc_debug_pair(rc_forest* f, int64_t local_leaf, int32_t i, 
   if (!e) e = cudaMemsetAsync(hits, 0, sizeof(int32_t) * npix, s);
   if (!e) {
     const uint32_t key_base = (uint32_t)f->first_global;
-    if (curved)
-      e = launch_cast_curved(f->cc, f->d_trees, leaf_view(f), f->P, dd->vis, dd->rect, dd->chunk_off, dd->chunk_elem,
-                             &dd->unit, 1, 0, key_base, d + off_scr, segs, 8, hits, cnt, 1, s);
-    else
+    if (curved) {
+      e = cudaMemcpyAsync(cnt + CNT_SEGS, &one, sizeof(int64_t), cudaMemcpyHostToDevice, s);   // visible count 1
+      if (!e) e = launch_prep_slots(f->d_trees, leaf_view(f), f->P, dd->vis, cnt + CNT_SEGS, 0, 1, d + off_slot,
+                                    d + off_org, s);
+      if (!e) e = cudaMemsetAsync(cnt, 0, sizeof(int64_t) * CNT_TOTAL, s);
+      if (!e)
+        e = launch_cast_curved(f->cc, f->d_trees, leaf_view(f), f->P, dd->vis, dd->rect, dd->chunk_off,
+                               dd->chunk_elem, &dd->unit, 1, 0, key_base, d + off_scr, segs, 8, hits, cnt, 1,
+                               d + off_slot, d + off_org, 0, 1, s);
+    } else {
       e = launch_cast_affine(f->cc, f->d_trees, leaf_view(f), f->P, dd->vis, dd->rect, dd->chunk_off,
                              dd->chunk_elem, 1, key_base, segs, 8, hits, cnt, 1, s);
+    }
   }
   int64_t hc[CNT_TOTAL];
   rc_seg hs[8];
+  (void)one;
   if (!e) e = cudaMemcpyAsync(hc, cnt, sizeof hc, cudaMemcpyDeviceToHost, s);
   if (!e) e = cudaMemcpyAsync(hs, segs, sizeof hs, cudaMemcpyDeviceToHost, s);
   if (!e) e = cudaStreamSynchronize(s);

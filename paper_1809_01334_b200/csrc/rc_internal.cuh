@@ -14,6 +14,7 @@
 #define RC_NODE_LEVELS 8    // coarsening levels of the node tables (fold + aggregation cycles)
 #define RC_UNIT_CHUNKS 128  // chunks per fold unit of the curved segment kernel (<= 4096 pairs)
 #define RC_UNIT_LEAVES 64   // visible leaves per fold unit (their geometry is staged in shared memory)
+#define RC_SLOT_BATCH (1 << 24)   // visible leaves per element-slot batch of the curved path (672 B each)
 
 // Fold unit of the curved segment kernel (row a6): a contiguous chunk range
 // of at most RC_UNIT_LEAVES visible leaves [vfirst, vfirst+nvis) inside one
@@ -150,6 +151,8 @@ struct rc_forest {
   int64_t units_cap = 0;
   int64_t h_units = 0;
   void* d_scratch = nullptr;       // per-CTA item / segment / key scratch of the fused kernel
+  void* d_gslot = nullptr;         // element slots of one batch of visible leaves (k_prep_slots)
+  int64_t slot_cap = 0;
   size_t scratch_bytes = 0;
   // aggregation output (ping-pong with d_segs)
   int32_t* d_defer = nullptr;      // composite: deferred pixels [w*h]
