@@ -101,7 +101,17 @@ typedef struct {
   int32_t gl_points;      /* N in [1,8] Gauss-Legendre points per segment  */
   double newton_tol;      /* R=2: stop when ||dxi||_inf < tol                */
   int32_t newton_max_iter;/* R=2: iteration cap; failures are counted, never silent     */
+  /* segment integrator (§2.7).  RC_SCHEME_GL with c_rk = 0 is the
+   * N-point rule of SURVEY R13 (the default); every scheme with c_rk > 0 runs
+   * Alg. 1: a step evaluating dx*kappa > c_rk at one of its nodes is replaced by
+   * its two halves (downstream half (+) upstream half), at most max_depth levels
+   * (steps at the cap are taken and counted in rc_segments.depth_capped). */
+  int32_t scheme;         /* RC_SCHEME_*                                                */
+  double c_rk;            /* Alg. 1 threshold (0: no recursion)                         */
+  int32_t max_depth;      /* Alg. 1 recursion cap in [0, 24] (0 = 24)                   */
 } rc_camera;
+enum { RC_SCHEME_GL = 0, RC_SCHEME_EULER = 1, RC_SCHEME_HEUN2 = 2, RC_SCHEME_HEUN3 = 3, RC_SCHEME_RK4 = 4,
+       RC_SCHEME_GAUSS2 = 5, RC_SCHEME_SIMPSON = 6 };
 
 /* Host fp64 preprocessing: per-tree camera constants and GL tables
  * (Eq. camerapoints).  Validates the camera (orthonormal
@@ -173,6 +183,7 @@ typedef struct {
   int64_t fallback_tasks;      /* ... of which needed the projected-patch method (diagnostic) */
   const rc_seg* segs;          /* device view, library-owned                           */
   const int32_t* hits_per_pixel; /* device [w*h]: pairs with >= 1 segment per pixel     */
+  int64_t depth_capped;        /* Alg. 1 steps taken at max_depth (must be 0)          */
 } rc_segments;
 
 rc_status rc_cast_segments(rc_forest* f, int32_t fold_levels, void* stream);

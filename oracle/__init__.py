@@ -16,7 +16,8 @@ _HERE = os.path.dirname(os.path.abspath(__file__))
 _SO = os.path.join(_HERE, "liboracle.so")
 _SRC = os.path.join(_HERE, "oracle.c")
 
-HIT, AMBIGUOUS, NEWTON_FAIL, OVERFLOW = 1, 2, 4, 8
+HIT, AMBIGUOUS, NEWTON_FAIL, OVERFLOW, SPLIT_NEAR = 1, 2, 4, 8, 16
+SCHEMES = {"gl": 0, "euler": 1, "heun2": 2, "heun3": 3, "rk4": 4, "gauss2": 5, "simpson": 6}
 
 
 def build(force: bool = False) -> str:
@@ -95,6 +96,9 @@ def lib():
                                        C.c_void_p, P(Pairs_), C.c_void_p]
         _lib.orc_render_ex.restype = C.c_int64
         _lib.orc_pairs_free.argtypes = [P(Pairs_)]
+        _lib.orc_segment_scheme.argtypes = [C.c_int, C.c_int, d, C.c_int, MEDIUM_FN, C.c_void_p, d, P(d),
+                                            C.c_void_p, P(C.c_int)]
+        _lib.orc_set_scheme.argtypes = [C.c_int, d, C.c_int]
         _lib.orc_set_force_general.argtypes = [C.c_int]
         _lib.orc_fold_pixel.argtypes = [C.c_int, C.c_void_p, d, C.c_void_p, C.c_void_p, C.c_void_p]
     return _lib
@@ -221,7 +225,7 @@ class OracleScene:
         vis = np.zeros(n, dtype=np.int8) if with_cull else None
         amb = np.zeros(n, dtype=np.int8) if with_cull else None
         pr = Pairs_()
-        m = {"exact": 0, "rule": 1, "hits": 2}[mode]
+        m = {"exact": 0, "rule": 1, "hits": 2, "scheme": 3}[mode]
         total = lib().orc_render_ex(C.byref(self.s), C.byref(self.c), m, N, _ptr(bg), npix, _ptr(pixels),
                                     _ptr(rgba), _ptr(nh), _ptr(na), nthreads,
                                     _ptr(vis) if with_cull else None, _ptr(amb) if with_cull else None,
@@ -314,6 +318,21 @@ def segment_rule(N, fn, L):
     cb = _medium(fn)
     lib().orc_segment_rule(N, cb, None, L, C.byref(a), _ptr(b))
     return a.value, b
+
+
+def segment_scheme(scheme, fn, L, N=4, c_rk=0.0, max_depth=24):
+    """Alg. 1 adaptive integration with scheme in SCHEMES.
+    Returns (a, b[3], depth, flags)."""
+    a = C.c_double(); b = np.zeros(3); fl = C.c_int(0)
+    cb = _medium(fn)
+    depth = lib().orc_segment_scheme(SCHEMES[scheme], N, c_rk, max_depth, cb, None, L, C.byref(a), _ptr(b),
+                                     C.byref(fl))
+    return a.value, b, depth, fl.value
+
+
+def set_scheme(scheme, c_rk=0.0, max_depth=24):
+    """Scheme of OracleScene.render_pairs(mode="scheme")."""
+    lib().orc_set_scheme(SCHEMES[scheme], c_rk, max_depth)
 
 
 def gll(R):

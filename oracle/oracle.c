@@ -199,6 +199,159 @@ void orc_segment_rule(int N, orc_medium_fn fn, void* ctx, double L, double* a, d
 }
 
 /* ======================================================================
+ * The paper's per-segment integrators with the adaptive recursion of Alg. 1
+ * (§2.7): explicit RK
+ * (Eq. RKresultAB: Euler, Heun 2, Heun 3, classical RK4), the implicit
+ * Gauss method of order 4 (Eq. gaussAB / gaussABab), Simpson's rule on the
+ * closed form (Eq. simpson) and the N-point GL rule of SURVEY R13.  x runs
+ * from the upstream (far) end x1 to the downstream (near) end x2;
+ * the medium callback takes s = distance from the near end: s = L - x.
+ * Alg. 1: a step of length dx whose computation evaluates dx beta > c_RK is
+ * abandoned and replaced by segeval(x_1/2, x2) (+) segeval(x1, x_1/2).  The
+ * same test at the scheme's own nodes applies to Gauss-2, Simpson and GL
+ * (D17).  c_RK <= 0: no recursion.
+ * ==================================================================== */
+typedef struct {
+  int M;
+  double c[4], a[4][4], b[4];
+} rk_tableau;
+static const rk_tableau RK_TAB[5] = {
+    {0, {0}, {{0}}, {0}},
+    {1, {0}, {{0}}, {1}},                                                            /* explicit Euler  */
+    {2, {0, 1}, {{0}, {1}}, {0.5, 0.5}},                                             /* Heun, order 2   */
+    {3, {0, 1.0 / 3, 2.0 / 3}, {{0}, {1.0 / 3}, {0, 2.0 / 3}}, {0.25, 0, 0.75}},     /* Heun, order 3   */
+    {4, {0, 0.5, 0.5, 1}, {{0}, {0.5}, {0, 0.5}, {0, 0, 1}}, {1.0 / 6, 1.0 / 3, 1.0 / 3, 1.0 / 6}}, /* RK4 */
+};
+
+typedef struct {
+  int scheme, N, max_depth;
+  double c_rk, L;
+  orc_medium_fn fn;
+  void* ctx;
+  int depth, capped, near_threshold;
+} seg_scheme;
+
+static void bg_at(seg_scheme* q, double x, double* beta, double gamma[3]) { q->fn(q->ctx, q->L - x, beta, gamma); }
+
+/* the split test of Alg. 1; flags decisions within 1e-4 of the threshold */
+static int split_test(seg_scheme* q, double dx, double beta) {
+  if (!(q->c_rk > 0.0)) return 0;
+  if (fabs(dx * beta - q->c_rk) <= 1e-4 * q->c_rk) q->near_threshold = 1;
+  return dx * beta > q->c_rk;
+}
+
+static void segeval(seg_scheme* q, double x1, double x2, int d, double* A, double B[3]) {
+  const double dx = x2 - x1;
+  if (d > q->depth) q->depth = d;
+  int split = 0;
+  double beta[64], gamma[64][3];
+  if (q->scheme >= ORC_EULER && q->scheme <= ORC_RK4) {
+    const rk_tableau* T = &RK_TAB[q->scheme];
+    double Ab[5], Bb[5][3];
+    for (int i = 0; i <= T->M && !split; ++i) {
+      /* stage i, Eq. RKresultAB (a_Mj = b_j for the final values) */
+      Ab[i] = 1.0;
+      Bb[i][0] = Bb[i][1] = Bb[i][2] = 0.0;
+      for (int j = 0; j < i; ++j) {
+        const double aij = (i == T->M) ? T->b[j] : T->a[i][j];
+        Ab[i] += dx * aij * (-beta[j] * Ab[j]);
+        for (int c = 0; c < 3; ++c) Bb[i][c] += dx * aij * (gamma[j][c] - beta[j] * Bb[j][c]);
+      }
+      if (i > 0 && split_test(q, dx, beta[i - 1])) split = 1;   /* Alg. 1 */
+      if (!split && i < T->M) bg_at(q, x1 + T->c[i] * dx, &beta[i], gamma[i]);
+    }
+    if (!split) {
+      *A = Ab[T->M];
+      for (int c = 0; c < 3; ++c) B[c] = Bb[T->M][c];
+    }
+  } else if (q->scheme == ORC_GAUSS2) {
+    const double xi[2] = {0.5 - sqrt(3.0) / 6.0, 0.5 + sqrt(3.0) / 6.0};   /* DESIGN.md D6 */
+    for (int j = 0; j < 2; ++j) {
+      bg_at(q, x1 + xi[j] * dx, &beta[j], gamma[j]);
+      split |= split_test(q, dx, beta[j]);
+    }
+    if (!split) {   /* Eq. gaussAB, Eq. gaussABab */
+      const double a1 = dx * (beta[0] + beta[1]) / 4.0, a2 = dx * dx * beta[0] * beta[1] / 12.0;
+      *A = (1.0 - a1 + a2) / (1.0 + a1 + a2);
+      for (int c = 0; c < 3; ++c) {
+        const double b1 = dx * (gamma[0][c] + gamma[1][c]) / 2.0;
+        const double b2 = dx * dx * (beta[0] * gamma[1][c] - beta[1] * gamma[0][c]) * sqrt(3.0) / 12.0;
+        B[c] = (b1 + b2) / (1.0 + a1 + a2);
+      }
+    }
+  } else if (q->scheme == ORC_SIMPSON) {
+    const double cj[3] = {0.0, 0.5, 1.0}, bj[3] = {1.0 / 6, 4.0 / 6, 1.0 / 6};
+    for (int j = 0; j < 3; ++j) {
+      bg_at(q, x1 + cj[j] * dx, &beta[j], gamma[j]);
+      split |= split_test(q, dx, beta[j]);
+    }
+    if (!split) {   /* Eq. simpson */
+      double sb = 0.0;
+      for (int j = 0; j < 3; ++j) sb += bj[j] * beta[j];
+      *A = exp(-dx * sb);
+      for (int c = 0; c < 3; ++c)
+        B[c] = dx * (bj[0] * *A * gamma[0][c] + bj[1] * sqrt(*A) * gamma[1][c] + bj[2] * gamma[2][c]);
+    }
+  } else {   /* ORC_GL: the R13 rule on [x1, x2], nodes u_j from the downstream (near) end */
+    double u[64], w[64], S[64 * 64];
+    orc_gauss_legendre(q->N, u, w);
+    orc_lagrange_integrals(q->N, u, S);
+    for (int j = 0; j < q->N; ++j) {
+      bg_at(q, x2 - u[j] * dx, &beta[j], gamma[j]);
+      split |= split_test(q, dx, beta[j]);
+    }
+    if (!split) {
+      double sum = 0.0;
+      for (int j = 0; j < q->N; ++j) sum += w[j] * beta[j];
+      *A = exp(-dx * sum);
+      B[0] = B[1] = B[2] = 0.0;
+      for (int j = 0; j < q->N; ++j) {
+        double tau = 0.0;
+        for (int k = 0; k < q->N; ++k) tau += S[j * q->N + k] * beta[k];
+        for (int c = 0; c < 3; ++c) B[c] += dx * w[j] * gamma[j][c] * exp(-dx * tau);
+      }
+    }
+  }
+  if (split) {
+    if (d >= q->max_depth) {   /* depth cap: report, and take the step without the test */
+      q->capped = 1;
+      const double keep = q->c_rk;
+      q->c_rk = 0.0;
+      segeval(q, x1, x2, d, A, B);
+      q->c_rk = keep;
+      return;
+    }
+    const double xm = 0.5 * (x1 + x2);
+    double An, Bn[3], Af, Bf[3];
+    segeval(q, xm, x2, d + 1, &An, Bn);   /* downstream (near) half */
+    segeval(q, x1, xm, d + 1, &Af, Bf);   /* upstream (far) half */
+    for (int c = 0; c < 3; ++c) orc_combine(An, Bn[c], Af, Bf[c], A, &B[c]);   /* near (+) far */
+  }
+}
+
+int orc_segment_scheme(int scheme, int N, double c_rk, int max_depth, orc_medium_fn fn, void* ctx, double L,
+                       double* a, double b[3], int* flags) {
+  seg_scheme q = {scheme, N, max_depth, c_rk, L, fn, ctx, 0, 0, 0};
+  if (!(L > 0.0)) {
+    *a = 1.0;
+    b[0] = b[1] = b[2] = 0.0;
+    if (flags) *flags = 0;
+    return 0;
+  }
+  segeval(&q, 0.0, L, 0, a, b);
+  if (flags) *flags = (q.capped ? 1 : 0) | (q.near_threshold ? 2 : 0);
+  return q.depth;
+}
+
+static int g_scheme = ORC_GL, g_scheme_depth = 24;
+static double g_scheme_crk = 0.0;
+void orc_set_scheme(int scheme, double c_rk, int max_depth) {
+  g_scheme = scheme;
+  g_scheme_crk = c_rk;
+  g_scheme_depth = max_depth;
+}
+
+/* ======================================================================
  * Geometry.  Gauss-Lobatto nodes, Lagrange
  * basis (Eq. nodal), tensor-product map (Eq. tensorgeom),
  * element = subcube of the tree.
@@ -1151,11 +1304,18 @@ static int64_t render_core(const orc_scene* sc, const orc_camera* cam, int mode,
         double L = (hh.alpha_far - hh.alpha_near) * rn;   /* s = alpha |r| */
         if (mode == 0) {
           if (orc_segment_exact(medium_eval, &mc, L, &hh.a, hh.b) < 0) hh.flags |= ORC_NEWTON_FAIL;
+        } else if (mode == 3) {   /* the paper's integrators, Alg. 1 (orc_set_scheme) */
+          int sf = 0;
+          orc_segment_scheme(g_scheme, N, g_scheme_crk, g_scheme_depth, medium_eval, &mc, L, &hh.a, hh.b, &sf);
+          if (sf & 1) hh.flags |= ORC_NEWTON_FAIL;
+          if (sf & 2) hh.flags |= ORC_SPLIT_NEAR;
         } else {
           orc_segment_rule(N, medium_eval, &mc, L, &hh.a, hh.b);
         }
         list[nl++] = hh;
         fold[nf++] = hh;
+        /* integration flags (Alg. 1 decisions near c_RK, depth cap) onto the pair's entry */
+        if (pairs && (hh.flags & (ORC_SPLIT_NEAR | ORC_NEWTON_FAIL))) pf[q][pn[q] - 1] |= hh.flags & (ORC_SPLIT_NEAR | ORC_NEWTON_FAIL);
       }
     }
     if (mode == 2) { for (int c = 0; c < 4; ++c) rgba[4 * q + c] = 0.0; }

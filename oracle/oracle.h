@@ -46,7 +46,8 @@ typedef struct {
   double alpha_near, alpha_far, a, b[3];
 } orc_hit;
 
-enum { ORC_HIT = 1, ORC_AMBIGUOUS = 2, ORC_NEWTON_FAIL = 4, ORC_OVERFLOW = 8 };
+enum { ORC_HIT = 1, ORC_AMBIGUOUS = 2, ORC_NEWTON_FAIL = 4, ORC_OVERFLOW = 8, ORC_SPLIT_NEAR = 16 };
+enum { ORC_GL = 0, ORC_EULER = 1, ORC_HEUN2 = 2, ORC_HEUN3 = 3, ORC_RK4 = 4, ORC_GAUSS2 = 5, ORC_SIMPSON = 6 };
 
 /* ---- segment algebra, PAPER.md:386-558 ---- */
 void orc_combine(double an, double bn, double af, double bf, double* a, double* b);
@@ -62,6 +63,12 @@ void orc_lagrange_integrals(int N, const double* u, double* S);
 typedef void (*orc_medium_fn)(void* ctx, double s, double* kappa, double* q3);
 int  orc_segment_exact(orc_medium_fn fn, void* ctx, double L, double* a, double b[3]);
 void orc_segment_rule(int N, orc_medium_fn fn, void* ctx, double L, double* a, double b[3]);
+/* Alg. 1 adaptive integration with a scheme (ORC_*); returns the recursion
+ * depth reached; *flags: 1 = depth cap hit, 2 = a split decision within 1e-4
+ * of c_RK.  orc_set_scheme selects the scheme of orc_render mode 3. */
+int  orc_segment_scheme(int scheme, int N, double c_rk, int max_depth, orc_medium_fn fn, void* ctx, double L,
+                        double* a, double b[3], int* flags);
+void orc_set_scheme(int scheme, double c_rk, int max_depth);
 
 /* ---- geometry / camera ---- */
 void orc_gll(int R, double* eta);

@@ -414,152 +414,6 @@ __device__ __noinline__ int face_roots_subdiv(const Patch& root, float tol, int 
 
 
 // ---------------------------------------------------------------------------
-// Element preparation by ONE thread (k_prep_slots, one element per thread):
-// the element slot (Bernstein points of X_E by restriction of the
-// tree's, fp64, stored fp32 relative to the origin B_(1,1,1); nodal field;
-// affine model A(xi) = Xc + J0 (xi - 1/2) and the bounds dp (nonlinear
-// remainder in J0^-1 coordinates) and eta (its derivative)), without warp
-// shuffles.  Restriction to [u, u+h] per axis: blossoms (u,u), (u,u+h),
-// (u+h,u+h) of the degree-2 Bernstein polynomial (de Casteljau).
-// ---------------------------------------------------------------------------
-__device__ __forceinline__ void prep_element_t(float* __restrict__ sl, double* __restrict__ org,
-                                            const TreeConst* __restrict__ trees, const DevLeafView& L, int e, int NF,
-                                            bool with_field) {
-  const double h = ldexp(1.0, -(int)L.level[e]);
-  const double* __restrict__ Bw = trees[L.tree[e]].Bw;   // [q3][q2][q1][xyz]
-  double M[3][3][3];                                     // [axis][r][q]
-#pragma unroll
-  for (int k = 0; k < 3; ++k) {
-    const double u = ldexp((double)L.anchor[3 * (int64_t)e + k], -RC_MAXLEVEL), w = u + h;
-#pragma unroll
-    for (int r = 0; r < 3; ++r) {
-      const double x = r == 2 ? w : u, y = r == 0 ? u : w;
-      M[k][r][0] = (1 - x) * (1 - y);
-      M[k][r][1] = (1 - x) * y + x * (1 - y);
-      M[k][r][2] = x * y;
-    }
-  }
-  // origin = point (1,1,1)
-  double o[3] = {0.0, 0.0, 0.0};
-#pragma unroll
-  for (int q3 = 0; q3 < 3; ++q3)
-#pragma unroll
-    for (int q2 = 0; q2 < 3; ++q2) {
-      const double w23 = M[2][1][q3] * M[1][1][q2];
-#pragma unroll
-      for (int q1 = 0; q1 < 3; ++q1) {
-        const double wq = w23 * M[0][1][q1];
-        const double* b = Bw + ((q3 * 3 + q2) * 3 + q1) * 3;
-#pragma unroll
-        for (int c = 0; c < 3; ++c) o[c] = fma(wq, b[c], o[c]);
-      }
-    }
-  org[0] = o[0];
-  org[1] = o[1];
-  org[2] = o[2];
-  // all 27 points, sum-factorised: axis 3, then 2, then 1
-#pragma unroll 1
-  for (int r3 = 0; r3 < 3; ++r3) {
-    double T2[9][3];
-#pragma unroll
-    for (int q21 = 0; q21 < 9; ++q21)
-#pragma unroll
-      for (int c = 0; c < 3; ++c) {
-        double acc = 0.0;
-#pragma unroll
-        for (int q3 = 0; q3 < 3; ++q3) acc = fma(M[2][r3][q3], Bw[(q3 * 9 + q21) * 3 + c], acc);
-        T2[q21][c] = acc;
-      }
-#pragma unroll 1
-    for (int r2 = 0; r2 < 3; ++r2) {
-      double T1[3][3];
-#pragma unroll
-      for (int q1 = 0; q1 < 3; ++q1)
-#pragma unroll
-        for (int c = 0; c < 3; ++c) {
-          double acc = 0.0;
-#pragma unroll
-          for (int q2 = 0; q2 < 3; ++q2) acc = fma(M[1][r2][q2], T2[q2 * 3 + q1][c], acc);
-          T1[q1][c] = acc;
-        }
-#pragma unroll
-      for (int r1 = 0; r1 < 3; ++r1) {
-        float* dst = sl + GI((r3 * 3 + r2) * 3 + r1);
-#pragma unroll
-        for (int c = 0; c < 3; ++c) {
-          double acc = 0.0;
-#pragma unroll
-          for (int q1 = 0; q1 < 3; ++q1) acc = fma(M[0][r1][q1], T1[q1][c], acc);
-          dst[c] = (float)(acc - o[c]);
-        }
-      }
-    }
-  }
-  if (with_field)
-    for (int q = 0; q < NF; ++q) sl[SLOT_FIELD + FI(q, NF)] = __ldg(&L.field[(int64_t)e * NF + q]);
-  // affine model at the centre from the Bernstein coefficients (fp32)
-  const float wq[3] = {0.25f, 0.5f, 0.25f}, dq[3] = {-1.0f, 0.0f, 1.0f};
-  float Xc[3] = {0.f, 0.f, 0.f}, J[3][3] = {{0.f, 0.f, 0.f}, {0.f, 0.f, 0.f}, {0.f, 0.f, 0.f}};
-#pragma unroll 1
-  for (int m = 0; m < 27; ++m) {
-    const int m1 = m % 3, m2 = (m / 3) % 3, m3 = m / 9;
-    const float* b = sl + GI(m);
-    const float w3 = wq[m1] * wq[m2] * wq[m3];
-    const float g[3] = {dq[m1] * wq[m2] * wq[m3], wq[m1] * dq[m2] * wq[m3], wq[m1] * wq[m2] * dq[m3]};
-#pragma unroll
-    for (int c = 0; c < 3; ++c) {
-      Xc[c] = fmaf(w3, b[c], Xc[c]);
-#pragma unroll
-      for (int a = 0; a < 3; ++a) J[c][a] = fmaf(g[a], b[c], J[c][a]);
-    }
-  }
-  float Ji[3][3];
-  if (!inv3(J, Ji)) {
-#pragma unroll
-    for (int a = 0; a < 3; ++a)
-#pragma unroll
-      for (int b = 0; b < 3; ++b) Ji[a][b] = 0.0f;
-  }
-  float dp0 = 0.f, dp1 = 0.f, dp2 = 0.f, eta = 0.0f;
-#pragma unroll 1
-  for (int m = 0; m < 27; ++m) {
-    const int mmv[3] = {m % 3, (m / 3) % 3, m / 9};
-    const float* b = sl + GI(m);
-    const float x0 = 0.5f * mmv[0] - 0.5f, x1 = 0.5f * mmv[1] - 0.5f, x2 = 0.5f * mmv[2] - 0.5f;
-    const float r0 = b[0] - (Xc[0] + J[0][0] * x0 + J[0][1] * x1 + J[0][2] * x2);
-    const float r1 = b[1] - (Xc[1] + J[1][0] * x0 + J[1][1] * x1 + J[1][2] * x2);
-    const float r2 = b[2] - (Xc[2] + J[2][0] * x0 + J[2][1] * x1 + J[2][2] * x2);
-    dp0 = fmaxf(dp0, fabsf(Ji[0][0] * r0 + Ji[0][1] * r1 + Ji[0][2] * r2));
-    dp1 = fmaxf(dp1, fabsf(Ji[1][0] * r0 + Ji[1][1] * r1 + Ji[1][2] * r2));
-    dp2 = fmaxf(dp2, fabsf(Ji[2][0] * r0 + Ji[2][1] * r1 + Ji[2][2] * r2));
-    // eta: Bernstein coefficients of dE/dxi_a = 2 J0^-1 (B_{m+e_a} - B_m) - e_a (inf-norm)
-    const int str[3] = {1, 3, 9};
-#pragma unroll
-    for (int ax = 0; ax < 3; ++ax) {
-      if (mmv[ax] < 2) {
-        const float* b2 = sl + GI(m + str[ax]);
-        const float e0 = 2.0f * (b2[0] - b[0]), e1 = 2.0f * (b2[1] - b[1]), e2 = 2.0f * (b2[2] - b[2]);
-        const float t0 = Ji[0][0] * e0 + Ji[0][1] * e1 + Ji[0][2] * e2 - (ax == 0 ? 1.0f : 0.0f);
-        const float t1 = Ji[1][0] * e0 + Ji[1][1] * e1 + Ji[1][2] * e2 - (ax == 1 ? 1.0f : 0.0f);
-        const float t2 = Ji[2][0] * e0 + Ji[2][1] * e1 + Ji[2][2] * e2 - (ax == 2 ? 1.0f : 0.0f);
-        eta = fmaxf(eta, fmaxf(fabsf(t0), fmaxf(fabsf(t1), fabsf(t2))));
-      }
-    }
-  }
-  float* af = sl + SLOT_AFF;
-  af[0] = Xc[0]; af[1] = Xc[1]; af[2] = Xc[2];
-#pragma unroll
-  for (int a = 0; a < 3; ++a)
-#pragma unroll
-    for (int b = 0; b < 3; ++b) af[3 + 3 * a + b] = Ji[a][b];
-  // inflate by a rounding margin relative to the element (fp32)
-  af[12] = dp0 * 1.001f + 1e-5f;
-  af[13] = dp1 * 1.001f + 1e-5f;
-  af[14] = dp2 * 1.001f + 1e-5f;
-  af[15] = eta * 1.001f + 1e-5f;
-}
-
-// ---------------------------------------------------------------------------
 // The fused segment kernel (rows a4 + a5 + a6 of SURVEY §8(a)).  Persistent
 // CTAs of CWARPS warps take fold units from a global counter; a unit is a
 // range of <= RC_UNIT_CHUNKS chunks of <= RC_UNIT_LEAVES visible leaves
@@ -686,32 +540,215 @@ __device__ __forceinline__ void fence_proxy_async_smem() { asm volatile("fence.p
 // ---- element preparation kernel -------------------------------------------
 // Slots of the visible leaves [v0, v1) (v1 clipped to the visible count) into
 // the global slot buffer (record v - v0: SLOT_USED floats + the fp64 origin as
-// 4 doubles), 64 elements per CTA staged in shared memory and written out
-// coalesced.  The segment kernel stages a unit's records with bulk copies.
-constexpr int PREP_THREADS = 64;
+// 4 doubles); the segment kernel stages a unit's records with bulk copies.
+// PREP_E elements per CTA, three threads per element (warp c = coordinate c):
+//  1. fp64: coordinate c of the 27 Bernstein points of X_E by restriction of
+//     the tree's Bernstein points to the element's subcube (blossoms
+//     (u,u), (u,u+h), (u+h,u+h) per axis, sum-factorised: axis 3, 2, 1),
+//     stored fp32 relative to the origin B_(1,1,1);
+//  2. fp32: row c of the affine model A(xi) = Xc + J0 (xi - 1/2) (Bernstein
+//     coefficients at the centre);
+//  3. fp32: J0^-1 (each thread), the bound dp_c of the nonlinear remainder in
+//     J0^-1 coordinates and the part of eta (sup |dE/dxi|) along axis c;
+//  then the slots are written out coalesced.
+// Stages 2-3 of k_prep_slots for coordinate C (one warp per coordinate).
+template <int C>
+__device__ __forceinline__ void prep_affine(const float* __restrict__ slw, float* sJw, bool act) {
+  constexpr float wq[3] = {0.25f, 0.5f, 0.25f}, dq[3] = {-1.0f, 0.0f, 1.0f};
+  if (act) {
+    float xc = 0.f, j0 = 0.f, j1 = 0.f, j2 = 0.f;
+#pragma unroll
+    for (int m = 0; m < 27; ++m) {
+      const int a1 = m % 3, a2 = (m / 3) % 3, a3 = m / 9;
+      const float b = slw[GI(m) + C];
+      xc = fmaf(wq[a1] * wq[a2] * wq[a3], b, xc);
+      j0 = fmaf(dq[a1] * wq[a2] * wq[a3], b, j0);
+      j1 = fmaf(wq[a1] * dq[a2] * wq[a3], b, j1);
+      j2 = fmaf(wq[a1] * wq[a2] * dq[a3], b, j2);
+    }
+    sJw[C] = xc;
+    sJw[3 + 3 * C] = j0;
+    sJw[4 + 3 * C] = j1;
+    sJw[5 + 3 * C] = j2;
+  }
+}
+template <int C>
+__device__ __forceinline__ void prep_bounds(const float* __restrict__ slw, const float* sJw, float (*sbw)[3],
+                                            float (&Ji)[3][3], bool act) {
+  if (!act) return;
+  float J[3][3];
+#pragma unroll
+  for (int i = 0; i < 3; ++i)
+#pragma unroll
+    for (int a = 0; a < 3; ++a) J[i][a] = sJw[3 + 3 * i + a];
+  const float Xc[3] = {sJw[0], sJw[1], sJw[2]};
+  if (!inv3(J, Ji)) {
+#pragma unroll
+    for (int i = 0; i < 3; ++i)
+#pragma unroll
+      for (int a = 0; a < 3; ++a) Ji[i][a] = 0.0f;
+  }
+  float dpc = 0.0f, eta = 0.0f;
+  constexpr int str[3] = {1, 3, 9};
+#pragma unroll
+  for (int m = 0; m < 27; ++m) {
+    const int mmv[3] = {m % 3, (m / 3) % 3, m / 9};
+    const float* b = slw + GI(m);
+    const float x0 = 0.5f * mmv[0] - 0.5f, x1 = 0.5f * mmv[1] - 0.5f, x2 = 0.5f * mmv[2] - 0.5f;
+    const float r0 = b[0] - (Xc[0] + J[0][0] * x0 + J[0][1] * x1 + J[0][2] * x2);
+    const float r1 = b[1] - (Xc[1] + J[1][0] * x0 + J[1][1] * x1 + J[1][2] * x2);
+    const float r2 = b[2] - (Xc[2] + J[2][0] * x0 + J[2][1] * x1 + J[2][2] * x2);
+    dpc = fmaxf(dpc, fabsf(Ji[C][0] * r0 + Ji[C][1] * r1 + Ji[C][2] * r2));
+    // eta: Bernstein coefficients of dE/dxi_C = 2 J0^-1 (B_{m+e_C} - B_m) - e_C (inf-norm)
+    if (mmv[C] < 2) {
+      const float* b2 = slw + GI(m + str[C]);
+      const float e0 = 2.0f * (b2[0] - b[0]), e1 = 2.0f * (b2[1] - b[1]), e2 = 2.0f * (b2[2] - b[2]);
+      const float t0 = Ji[0][0] * e0 + Ji[0][1] * e1 + Ji[0][2] * e2 - (C == 0 ? 1.0f : 0.0f);
+      const float t1 = Ji[1][0] * e0 + Ji[1][1] * e1 + Ji[1][2] * e2 - (C == 1 ? 1.0f : 0.0f);
+      const float t2 = Ji[2][0] * e0 + Ji[2][1] * e1 + Ji[2][2] * e2 - (C == 2 ? 1.0f : 0.0f);
+      eta = fmaxf(eta, fmaxf(fabsf(t0), fmaxf(fabsf(t1), fabsf(t2))));
+    }
+  }
+  sbw[0][C] = dpc;
+  sbw[1][C] = eta;
+}
+
+constexpr int PREP_E = 32;
 template <int P>
-__global__ void __launch_bounds__(PREP_THREADS) k_prep_slots(const TreeConst* __restrict__ trees, DevLeafView L,
-                                                             const int32_t* __restrict__ vis,
-                                                             const int64_t* __restrict__ nvis_p, int64_t v0, int64_t v1,
-                                                             float4* __restrict__ gslot, double* __restrict__ gorg) {
+__global__ void __launch_bounds__(3 * PREP_E) k_prep_slots(const TreeConst* __restrict__ trees, DevLeafView L,
+                                                           const int32_t* __restrict__ vis,
+                                                           const int64_t* __restrict__ nvis_p, int64_t v0, int64_t v1,
+                                                           float4* __restrict__ gslot, double* __restrict__ gorg) {
   constexpr int NF = (P + 1) * (P + 1) * (P + 1);
-  __shared__ __align__(16) float sl[PREP_THREADS][SLOT_STRIDE];
-  __shared__ double so[PREP_THREADS][4];
+  __shared__ __align__(16) float sl[PREP_E][SLOT_STRIDE];
+  __shared__ double so[PREP_E][4];
+  __shared__ float sJ[PREP_E][12];     // Xc[3], J[3][3]
+  __shared__ float sb[PREP_E][2][3];   // per coordinate thread: dp_c, eta part
   const int64_t vend = min(v1, *nvis_p);
-  const int64_t vb = v0 + (int64_t)blockIdx.x * PREP_THREADS;
+  const int64_t vb = v0 + (int64_t)blockIdx.x * PREP_E;
   if (vb >= vend) return;
-  const int nloc = (int)min((int64_t)PREP_THREADS, vend - vb);
-  const int tid = threadIdx.x;
-  if (tid < nloc) {
-    prep_element_t(sl[tid], so[tid], trees, L, vis[vb + tid], NF, true);
-    so[tid][3] = 0.0;
+  const int nloc = (int)min((int64_t)PREP_E, vend - vb);
+  __shared__ int32_t se[PREP_E], skey[PREP_E][5];   // leaf index; tree, level, anchor[3]
+  const int c = threadIdx.x >> 5, w = threadIdx.x & 31;
+  const bool act = w < nloc;
+  float* slw = sl[w];
+  // the CTA's leaf keys and fields, all loads in flight at once (no dependent chains per thread)
+  if (threadIdx.x < nloc) se[threadIdx.x] = vis[vb + threadIdx.x];
+  __syncthreads();
+  for (int k = threadIdx.x; k < nloc * 5; k += 3 * PREP_E) {
+    const int ew = k / 5, q = k - ew * 5;
+    const int64_t e = se[ew];
+    skey[ew][q] = q == 0 ? L.tree[e] : (q == 1 ? (int32_t)L.level[e] : L.anchor[3 * e + q - 2]);
+  }
+  for (int k = threadIdx.x; k < nloc * NF; k += 3 * PREP_E) {
+    const int ew = k / NF, q = k - ew * NF;
+    sl[ew][SLOT_FIELD + FI(q, NF)] = __ldg(&L.field[(int64_t)se[ew] * NF + q]);
+  }
+  __syncthreads();
+  // 1. restriction (fp64), coordinate c
+  if (act) {
+    const double h = ldexp(1.0, -skey[w][1]);
+    const double* __restrict__ Bw = trees[skey[w][0]].Bw;   // [q3][q2][q1][xyz]
+    double uu[3];
+#pragma unroll
+    for (int k = 0; k < 3; ++k) uu[k] = ldexp((double)skey[w][2 + k], -RC_MAXLEVEL);
+    auto Mrow = [&](int k, int r, double m[3]) {   // blossom row r of axis k
+      const double u = uu[k], v = u + h;
+      const double x = r == 2 ? v : u, y = r == 0 ? u : v;
+      m[0] = (1 - x) * (1 - y);
+      m[1] = (1 - x) * y + x * (1 - y);
+      m[2] = x * y;
+    };
+    double m0[3], m1[3], m2[3];
+    Mrow(0, 1, m0);
+    Mrow(1, 1, m1);
+    Mrow(2, 1, m2);
+    double o = 0.0;   // origin = point (1,1,1)
+#pragma unroll
+    for (int q3 = 0; q3 < 3; ++q3)
+#pragma unroll
+      for (int q2 = 0; q2 < 3; ++q2) {
+        const double w23 = m2[q3] * m1[q2];
+#pragma unroll
+        for (int q1 = 0; q1 < 3; ++q1) o = fma(w23 * m0[q1], Bw[((q3 * 3 + q2) * 3 + q1) * 3 + c], o);
+      }
+    so[w][c] = o;
+    if (c == 0) so[w][3] = 0.0;
+    double M0[3][3];
+#pragma unroll
+    for (int r = 0; r < 3; ++r) Mrow(0, r, M0[r]);
+#pragma unroll
+    for (int r3 = 0; r3 < 3; ++r3) {
+      double m3[3];
+      Mrow(2, r3, m3);
+      double T2[9];
+#pragma unroll
+      for (int q21 = 0; q21 < 9; ++q21) {
+        double acc = 0.0;
+#pragma unroll
+        for (int q3 = 0; q3 < 3; ++q3) acc = fma(m3[q3], Bw[(q3 * 9 + q21) * 3 + c], acc);
+        T2[q21] = acc;
+      }
+#pragma unroll
+      for (int r2 = 0; r2 < 3; ++r2) {
+        double mm2[3];
+        Mrow(1, r2, mm2);
+        double T1[3];
+#pragma unroll
+        for (int q1 = 0; q1 < 3; ++q1) {
+          double acc = 0.0;
+#pragma unroll
+          for (int q2 = 0; q2 < 3; ++q2) acc = fma(mm2[q2], T2[q2 * 3 + q1], acc);
+          T1[q1] = acc;
+        }
+#pragma unroll
+        for (int r1 = 0; r1 < 3; ++r1) {
+          double acc = 0.0;
+#pragma unroll
+          for (int q1 = 0; q1 < 3; ++q1) acc = fma(M0[r1][q1], T1[q1], acc);
+          slw[GI((r3 * 3 + r2) * 3 + r1) + c] = (float)(acc - o);
+        }
+      }
+    }
+  }
+  __syncthreads();
+  // 2. affine model at the centre, row c (fp32); 3. J0^-1, dp_c and the eta
+  // part along axis c.  Per coordinate a fully unrolled instance (constant
+  // indices: no integer division or selects in the loops over the 27 points).
+  switch (c) {   // warp-uniform
+    case 0: prep_affine<0>(slw, sJ[w], act); break;
+    case 1: prep_affine<1>(slw, sJ[w], act); break;
+    default: prep_affine<2>(slw, sJ[w], act); break;
+  }
+  __syncthreads();
+  float Ji[3][3];
+  switch (c) {
+    case 0: prep_bounds<0>(slw, sJ[w], sb[w], Ji, act); break;
+    case 1: prep_bounds<1>(slw, sJ[w], sb[w], Ji, act); break;
+    default: prep_bounds<2>(slw, sJ[w], sb[w], Ji, act); break;
+  }
+  __syncthreads();
+  if (act && c == 0) {
+    float* af = slw + SLOT_AFF;
+    af[0] = sJ[w][0];
+    af[1] = sJ[w][1];
+    af[2] = sJ[w][2];
+#pragma unroll
+    for (int i = 0; i < 3; ++i)
+#pragma unroll
+      for (int a = 0; a < 3; ++a) af[3 + 3 * i + a] = Ji[i][a];
+    // inflate by a rounding margin relative to the element (fp32)
+    af[12] = sb[w][0][0] * 1.001f + 1e-5f;
+    af[13] = sb[w][0][1] * 1.001f + 1e-5f;
+    af[14] = sb[w][0][2] * 1.001f + 1e-5f;
+    af[15] = fmaxf(sb[w][1][0], fmaxf(sb[w][1][1], sb[w][1][2])) * 1.001f + 1e-5f;
   }
   __syncthreads();
   constexpr int Q = SLOT_USED / 4;   // float4 per slot
   float4* dst = gslot + (vb - v0) * Q;
-  for (int k = tid; k < nloc * Q; k += PREP_THREADS) dst[k] = reinterpret_cast<const float4*>(sl[k / Q])[k % Q];
+  for (int k = threadIdx.x; k < nloc * Q; k += 3 * PREP_E) dst[k] = reinterpret_cast<const float4*>(sl[k / Q])[k % Q];
   double* od = gorg + (vb - v0) * 4;
-  for (int k = tid; k < nloc * 4; k += PREP_THREADS) od[k] = so[k / 4][k % 4];
+  for (int k = threadIdx.x; k < nloc * 4; k += 3 * PREP_E) od[k] = so[k / 4][k % 4];
 }
 
 // per-CTA global scratch (bytes)
@@ -1129,6 +1166,73 @@ __device__ __forceinline__ void isect_chunk(WarpIsect& W, CastSmem& S, const Cam
   __syncwarp();   // W is reused by the warp's next chunk
 }
 
+// ---- phase 2 with the paper's integrators (rc_camera.scheme, Alg. 1) ---------
+// The medium at near-end parameter u: xi(u) by the chord iteration of phase 2
+// from the quadratic prediction through (entry, midpoint, exit) xi, then the
+// nodal field.  Out of line: an opt-in path that must not grow the default
+// phase's code.
+template <int P>
+struct CurvedMedium {
+  const float* gs;
+  const CamConst* cc;
+  float xin[3], dX[3], xia[3], xm[3], xib[3], Ji[3][3], qfac;
+  int* fails;
+  __device__ MediumSample operator()(float u) const {
+    const float l0 = (1.0f - u) * (1.0f - 2.0f * u), l1 = 4.0f * u * (1.0f - u), l2 = u * (2.0f * u - 1.0f);
+    float x[3], t[3];
+#pragma unroll
+    for (int d = 0; d < 3; ++d) {
+      x[d] = l0 * xia[d] + l1 * xm[d] + l2 * xib[d];
+      t[d] = fmaf(u, dX[d], xin[d]);
+    }
+    bool conv = false;
+    for (int it = 0; it < 2 * cc->newton_max; ++it) {
+      float X[3];
+      eval_X(gs, x, X);
+      float step = 0.0f;
+      const float r0 = t[0] - X[0], r1 = t[1] - X[1], r2 = t[2] - X[2];
+#pragma unroll
+      for (int d = 0; d < 3; ++d) {
+        const float sd = Ji[d][0] * r0 + Ji[d][1] * r1 + Ji[d][2] * r2;
+        x[d] += sd;
+        step = fmaxf(step, fabsf(sd));
+      }
+      if (step * qfac < cc->newton_tol) {
+        conv = true;
+        break;
+      }
+    }
+    if (!conv) ++*fails;
+#pragma unroll
+    for (int d = 0; d < 3; ++d) x[d] = fminf(fmaxf(x[d], 0.0f), 1.0f);   // nodes lie inside the element
+    return medium_from_f(*cc, field_pad<P>(gs + SLOT_FIELD, x[0], x[1], x[2]) * cc->inv_F);
+  }
+};
+
+template <int P>
+__device__ __noinline__ void integ_scheme(const float* __restrict__ gs, const CamConst& cc, const float xin[3],
+                                          const float dX[3], const float xia[3], const float xm[3],
+                                          const float xib[3], float Lseg, float qfac, int& fails, int& capped,
+                                          float& a_out, float b_out[3]) {
+  CurvedMedium<P> med;
+  med.gs = gs;
+  med.cc = &cc;
+  med.qfac = qfac;
+  med.fails = &fails;
+  const float* afm = gs + SLOT_AFF;
+#pragma unroll
+  for (int d = 0; d < 3; ++d) {
+    med.xin[d] = xin[d];
+    med.dX[d] = dX[d];
+    med.xia[d] = xia[d];
+    med.xm[d] = xm[d];
+    med.xib[d] = xib[d];
+#pragma unroll
+    for (int e = 0; e < 3; ++e) med.Ji[d][e] = afm[3 + 3 * d + e];
+  }
+  segment_scheme(cc, Lseg, med, a_out, b_out, capped);
+}
+
 // ---- phase 2: integrate one item per lane ----------------------------------
 // The field at each GL node needs xi(x): chord iteration with
 // the element's J0^-1, started from a quadratic prediction through (entry,
@@ -1137,9 +1241,9 @@ __device__ __forceinline__ void isect_chunk(WarpIsect& W, CastSmem& S, const Cam
 // element, so after a step s the error is <= q/(1-q) s (q = 3 eta); the
 // iteration stops when that bound is below tol (plain s < tol when q >= 1/2).
 // scr: this thread's scratch (stride CWARPS*32 floats) for the node values
-template <int P, int N>
+template <int P, int N, bool ADAPT>
 __device__ __forceinline__ void integ_item(const float* __restrict__ gs, const CamConst& cc, float4 i0, float4 i1,
-                                           float4 i2, float* __restrict__ scr, int& fails, float& a_out,
+                                           float4 i2, float* __restrict__ scr, int& fails, int& capped, float& a_out,
                                            float b_out[3]) {
   constexpr int ST = CWARPS * 32;
   const float tol = cc.newton_tol;
@@ -1177,6 +1281,10 @@ __device__ __forceinline__ void integ_item(const float* __restrict__ gs, const C
     }
   }
   if (!ok) ++fails;
+  if constexpr (ADAPT) {   // the paper's integrators with Alg. 1 (rc_camera.scheme)
+    integ_scheme<P>(gs, cc, xin, dX, xia, xm, xib, Lseg, qfac, fails, capped, a_out, b_out);
+    return;
+  }
   float sumk = 0.0f;
   // the GL nodes two at a time: independent chord iterations in lockstep
 #pragma unroll 1
@@ -1415,7 +1523,7 @@ __device__ void fold_bucket(CastSmem& S, CastCtl& ctl, const rc_seg* __restrict_
 }
 
 // ---- the kernel --------------------------------------------------------------
-template <int P, int N>
+template <int P, int N, bool ADAPT>
 __global__ void __launch_bounds__(CWARPS * 32, CAST_CTAS_PER_SM) k_cast_curved(CamConst cc, const TreeConst* __restrict__ trees,
                                                                 DevLeafView L, const int32_t* __restrict__ vis,
                                                                 const Rect16* __restrict__ vrect,
@@ -1439,7 +1547,7 @@ __global__ void __launch_bounds__(CWARPS * 32, CAST_CTAS_PER_SM) k_cast_curved(C
   unsigned char* my = scratch + (size_t)blockIdx.x * SCR_PER_CTA;
   float4* items = reinterpret_cast<float4*>(my);
   rc_seg* segs = reinterpret_cast<rc_seg*>(my + SCR_ITEMS);
-  int local_hits = 0, face_fail = 0, fails = 0;
+  int local_hits = 0, face_fail = 0, fails = 0, capped = 0;
   long long raw_local = 0, n_tasks = 0, n_fallback = 0;
   int prev_items = 0;
   uint32_t mbar_parity = 0;
@@ -1613,7 +1721,7 @@ __global__ void __launch_bounds__(CWARPS * 32, CAST_CTAS_PER_SM) k_cast_curved(C
                          : (ij >> 16) * (uint32_t)cc.W + (ij & 0xffffu);
           an = i3.x;
           afar = i3.y;
-          integ_item<P, N>(S.u.p.slot[v - U.vfirst], cc, i0, i1, i2, S.u.p.ph.scr + tid, fails, a, bb);
+          integ_item<P, N, ADAPT>(S.u.p.slot[v - U.vfirst], cc, i0, i1, i2, S.u.p.ph.scr + tid, fails, capped, a, bb);
         }
         if (fold > 0) {
           if (act) {
@@ -1678,6 +1786,7 @@ __global__ void __launch_bounds__(CWARPS * 32, CAST_CTAS_PER_SM) k_cast_curved(C
       atomicAdd((unsigned long long*)&counters[CNT_NEWTON_FAIL], (unsigned long long)(face_fail + fails));
   }
   if (tid == 0 && raw_local) atomicAdd((unsigned long long*)&counters[CNT_RAW], (unsigned long long)raw_local);
+  if (capped) atomicAdd((unsigned long long*)&counters[CNT_DEPTH_CAP], (unsigned long long)capped);
   if (lane == 0 && n_tasks) {
     atomicAdd((unsigned long long*)&counters[CNT_TASKS], (unsigned long long)n_tasks);
     atomicAdd((unsigned long long*)&counters[CNT_FALLBACK], (unsigned long long)n_fallback);
@@ -1689,23 +1798,39 @@ __global__ void __launch_bounds__(CWARPS * 32, CAST_CTAS_PER_SM) k_cast_curved(C
 size_t cast_curved_scratch_per_cta() { return SCR_PER_CTA; }
 int cast_curved_ctas_per_sm() { return CAST_CTAS_PER_SM; }
 
+template <int P, int N, bool ADAPT>
+static cudaError_t cast_PNA(const CamConst& cc, const TreeConst* trees, DevLeafView L, const int32_t* vis,
+                            const Rect16* vrect, const int64_t* chunk_off, const int32_t* chunk_elem,
+                            const Unit* units, int64_t nunits, int fold, uint32_t key_base, void* scratch, rc_seg* out,
+                            int64_t out_cap, int32_t* hits_pp, int64_t* counters, int grid, const float4* gslot,
+                            const double* gorg, int64_t v0, int64_t v1, cudaStream_t s) {
+  const size_t smem = sizeof(CastSmem);
+  static bool attr = false;
+  if (!attr) {
+    cudaError_t e =
+        cudaFuncSetAttribute(k_cast_curved<P, N, ADAPT>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    if (e != cudaSuccess) return e;
+    attr = true;
+  }
+  k_cast_curved<P, N, ADAPT><<<grid, CWARPS * 32, smem, s>>>(cc, trees, L, vis, vrect, chunk_off, chunk_elem, units,
+                                                             nunits, fold, key_base, (unsigned char*)scratch, out,
+                                                             out_cap, hits_pp, counters, gslot, gorg, v0, v1);
+  return cudaGetLastError();
+}
+
+// the default GL rule (R13) and the opt-in integrators (Alg. 1) are separate instantiations,
+// so the default path carries no code or registers of the other
 template <int P, int N>
 static cudaError_t cast_PN(const CamConst& cc, const TreeConst* trees, DevLeafView L, const int32_t* vis,
                            const Rect16* vrect, const int64_t* chunk_off, const int32_t* chunk_elem, const Unit* units,
                            int64_t nunits, int fold, uint32_t key_base, void* scratch, rc_seg* out, int64_t out_cap,
                            int32_t* hits_pp, int64_t* counters, int grid, const float4* gslot, const double* gorg,
                            int64_t v0, int64_t v1, cudaStream_t s) {
-  const size_t smem = sizeof(CastSmem);
-  static bool attr = false;
-  if (!attr) {
-    cudaError_t e = cudaFuncSetAttribute(k_cast_curved<P, N>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    if (e != cudaSuccess) return e;
-    attr = true;
-  }
-  k_cast_curved<P, N><<<grid, CWARPS * 32, smem, s>>>(cc, trees, L, vis, vrect, chunk_off, chunk_elem, units, nunits,
-                                                      fold, key_base, (unsigned char*)scratch, out, out_cap, hits_pp,
-                                                      counters, gslot, gorg, v0, v1);
-  return cudaGetLastError();
+  if (cc.scheme != RC_SCHEME_GL || cc.c_rk > 0.0f)
+    return cast_PNA<P, N, true>(cc, trees, L, vis, vrect, chunk_off, chunk_elem, units, nunits, fold, key_base, scratch,
+                                out, out_cap, hits_pp, counters, grid, gslot, gorg, v0, v1, s);
+  return cast_PNA<P, N, false>(cc, trees, L, vis, vrect, chunk_off, chunk_elem, units, nunits, fold, key_base, scratch,
+                               out, out_cap, hits_pp, counters, grid, gslot, gorg, v0, v1, s);
 }
 
 size_t slot_record_bytes() { return SLOT_USED * sizeof(float) + 4 * sizeof(double); }
@@ -1714,11 +1839,11 @@ cudaError_t launch_prep_slots(const TreeConst* trees, DevLeafView L, int P, cons
                               const int64_t* nvis_p, int64_t v0, int64_t v1, void* gslot, void* gorg,
                               cudaStream_t s) {
   if (v1 <= v0) return cudaSuccess;
-  const unsigned grid = (unsigned)((v1 - v0 + PREP_THREADS - 1) / PREP_THREADS);
+  const unsigned grid = (unsigned)((v1 - v0 + PREP_E - 1) / PREP_E);
   if (P == 1)
-    k_prep_slots<1><<<grid, PREP_THREADS, 0, s>>>(trees, L, vis, nvis_p, v0, v1, (float4*)gslot, (double*)gorg);
+    k_prep_slots<1><<<grid, 3 * PREP_E, 0, s>>>(trees, L, vis, nvis_p, v0, v1, (float4*)gslot, (double*)gorg);
   else
-    k_prep_slots<2><<<grid, PREP_THREADS, 0, s>>>(trees, L, vis, nvis_p, v0, v1, (float4*)gslot, (double*)gorg);
+    k_prep_slots<2><<<grid, 3 * PREP_E, 0, s>>>(trees, L, vis, nvis_p, v0, v1, (float4*)gslot, (double*)gorg);
   ++g_launches;
   return cudaGetLastError();
 }

@@ -302,7 +302,7 @@ __global__ void k_unit_emit(const int32_t* __restrict__ vis, const int64_t* __re
 // centre with a few fp64 operations, P0 = T(alpha0) - C_E; everything after
 // that is fp32 on quantities of the element's size.
 // ---------------------------------------------------------------------------
-template <int P, int N>
+template <int P, int N, bool ADAPT>
 __global__ void __launch_bounds__(256) k_cast_affine(CamConst cc, const TreeConst* __restrict__ trees, DevLeafView L,
                                                      const int32_t* __restrict__ vis, const Rect16* __restrict__ vrect,
                                                      const int64_t* __restrict__ chunk_off,
@@ -312,7 +312,7 @@ __global__ void __launch_bounds__(256) k_cast_affine(CamConst cc, const TreeCons
   constexpr int NF = (P + 1) * (P + 1) * (P + 1);
   const unsigned lane = threadIdx.x & 31;
   const float half_w = 0.5f * (cc.W - 1), half_h = 0.5f * (cc.H - 1);
-  int local_hits = 0;
+  int local_hits = 0, capped = 0;
   for (;;) {
     int64_t c = 0;
     if (lane == 0) c = (int64_t)atomicAdd((unsigned long long*)&counters[CNT_WORK], 1ull);
@@ -381,15 +381,37 @@ __global__ void __launch_bounds__(256) k_cast_affine(CamConst cc, const TreeCons
         xin[k] = 0.5f + (P0[k] + b_in * trf[k]) * inv_h;
         dx[k] = db * trf[k] * inv_h;
       }
-      float ft[N];
+      if constexpr (!ADAPT) {
+        float ft[N];
 #pragma unroll
-      for (int q = 0; q < N; ++q) {
-        float x1 = fmaf(cc.u[q], dx[0], xin[0]);
-        float x2 = fmaf(cc.u[q], dx[1], xin[1]);
-        float x3 = fmaf(cc.u[q], dx[2], xin[2]);
-        ft[q] = field_at<P>(f, x1, x2, x3) * cc.inv_F;
+        for (int q = 0; q < N; ++q) {
+          float x1 = fmaf(cc.u[q], dx[0], xin[0]);
+          float x2 = fmaf(cc.u[q], dx[1], xin[1]);
+          float x3 = fmaf(cc.u[q], dx[2], xin[2]);
+          ft[q] = field_at<P>(f, x1, x2, x3) * cc.inv_F;
+        }
+        gl_rule<N>(cc, ft, Lseg, a, b);
+      } else {
+        // the paper's integrators with Alg. 1 (the medium is affine in the element: xi(u) = xin + u dx)
+        struct Med {
+          float f[NF], xin[3], dx[3], inv_F;
+          const CamConst* cc;
+          __device__ MediumSample operator()(float u) const {
+            return medium_from_f(*cc, field_at<P>(f, fmaf(u, dx[0], xin[0]), fmaf(u, dx[1], xin[1]),
+                                                  fmaf(u, dx[2], xin[2])) * inv_F);
+          }
+        } med;
+#pragma unroll
+        for (int q = 0; q < NF; ++q) med.f[q] = f[q];
+#pragma unroll
+        for (int k = 0; k < 3; ++k) {
+          med.xin[k] = xin[k];
+          med.dx[k] = dx[k];
+        }
+        med.inv_F = cc.inv_F;
+        med.cc = &cc;
+        segment_scheme(cc, Lseg, med, a, b, capped);
       }
-      gl_rule<N>(cc, ft, Lseg, a, b);
     }
     int64_t slot = warp_append(&counters[CNT_SEGS], hit ? 1 : 0);
     if (hit) {
@@ -407,6 +429,7 @@ __global__ void __launch_bounds__(256) k_cast_affine(CamConst cc, const TreeCons
 #pragma unroll
   for (int off = 16; off > 0; off >>= 1) local_hits += __shfl_down_sync(0xffffffffu, local_hits, off);
   if (lane == 0 && local_hits) atomicAdd((unsigned long long*)&counters[CNT_HITPAIRS], (unsigned long long)local_hits);
+  if (capped) atomicAdd((unsigned long long*)&counters[CNT_DEPTH_CAP], (unsigned long long)capped);
 }
 
 // ---------------------------------------------------------------------------
@@ -742,56 +765,6 @@ __device__ __forceinline__ void warp_sort_blocked(uint64_t (&key)[E], uint32_t (
 }
 
 
-// Aggregation fast path (n <= 32 E): register sort, then per sorted record
-// its index, alpha_near, alpha_far and target-level node cached in shared
-// memory, so that run detection needs no dependent global loads.
-struct RunCache {
-  uint32_t* rid;
-  float* an;
-  float* af;
-  int32_t* anc;
-};
-
-template <int E>
-__device__ __forceinline__ bool sort_pixel_cache(const rc_seg* __restrict__ recs, const uint32_t* __restrict__ S,
-                                                 int n, const int32_t* __restrict__ leaf_node, uint32_t key_base,
-                                                 RunCache C) {
-  const unsigned lane = threadIdx.x & 31;
-  uint64_t key[E];
-  uint32_t id[E];
-#pragma unroll
-  for (int e = 0; e < E; ++e) {
-    const int i = (int)lane * E + e;
-    id[e] = i < n ? S[i] : 0u;
-    key[e] = i < n ? sort_key(recs[id[e]]) : ~0ull;
-  }
-  warp_sort_blocked<E>(key, id);
-  // equal sort keys: the register order is not total -> the caller defers the pixel
-  uint64_t prev_key = __shfl_up_sync(0xffffffffu, key[E - 1], 1);
-  if (lane == 0) prev_key = ~0ull;
-  bool tie = false;
-#pragma unroll
-  for (int e = 0; e < E; ++e) {
-    const int i = (int)lane * E + e;
-    tie |= i < n && key[e] == prev_key;
-    prev_key = key[e];
-  }
-  if (__any_sync(0xffffffffu, tie)) return false;
-#pragma unroll
-  for (int e = 0; e < E; ++e) {
-    const int i = (int)lane * E + e;
-    if (i < n) {
-      const rc_seg& r = recs[id[e]];
-      C.rid[i] = id[e];
-      C.an[i] = r.alpha_near;
-      C.af[i] = r.alpha_far;
-      C.anc[i] = leaf_node[r.key - key_base];
-    }
-  }
-  __syncwarp();
-  return true;
-}
-
 // Common case of the per-pixel fold: up to 32 E records sorted by
 // (alpha_near, key) in registers (warp bitonic network over the blocked
 // layout i = lane E + e: in-register exchanges for distances < E, shuffles
@@ -935,35 +908,28 @@ __global__ void __launch_bounds__(NW * 32, CAP <= 512 ? FOLD_MINB : 1) k_fold(
 // result is keyed by the node's first leaf.  Records of one node that do not
 // touch stay separate (safe for non-convex curved nodes).
 // ---------------------------------------------------------------------------
-// Two passes (as k_fold): FROM_LIST = false takes every pixel with <= 512
-// records (8 KB of shared memory per warp: 6 resident CTAs per SM instead of
-// 2) and defers the others to a list that FROM_LIST = true works through.
-constexpr int COARSEN_CACHE = 512;
-constexpr int COARSEN_MINB = 6;
-template <bool FROM_LIST>
-__global__ void __launch_bounds__(FOLD_WARPS * 32, FROM_LIST ? 1 : COARSEN_MINB) k_coarsen(
-    const rc_seg* __restrict__ recs, const uint32_t* __restrict__ perm, const int64_t* __restrict__ off, int64_t npix,
+// Two passes (as k_fold): k_coarsen_fast takes every pixel with <= 512
+// records; the others (and pixels with tied sort keys) are deferred to a list
+// that k_coarsen_list works through with a shared-memory sort under the total
+// order (FOLD_CAP records; more are passed through re-keyed, unmerged).
+__global__ void __launch_bounds__(FOLD_WARPS * 32, 1) k_coarsen_list(
+    const rc_seg* __restrict__ recs, const uint32_t* __restrict__ perm, const int64_t* __restrict__ off,
     const int32_t* __restrict__ node_first, const int32_t* __restrict__ leaf_node, uint32_t key_base, float tau,
-    rc_seg* __restrict__ out, int64_t out_cap, int32_t* __restrict__ defer, int64_t* __restrict__ counters) {
+    rc_seg* __restrict__ out, int64_t out_cap, const int32_t* __restrict__ defer, int64_t* __restrict__ counters) {
   extern __shared__ unsigned char smem_raw[];
   const int warp = threadIdx.x >> 5;
   const unsigned lane = threadIdx.x & 31;
-  constexpr int WCAP = FROM_LIST ? FOLD_CAP : COARSEN_CACHE * 2;   // uint64 words of keys per warp
-  uint64_t* keys = reinterpret_cast<uint64_t*>(smem_raw) + (size_t)warp * WCAP;
-  uint16_t* idxs = reinterpret_cast<uint16_t*>(reinterpret_cast<uint64_t*>(smem_raw) + (size_t)FOLD_WARPS * WCAP) +
+  uint64_t* keys = reinterpret_cast<uint64_t*>(smem_raw) + (size_t)warp * FOLD_CAP;
+  uint16_t* idxs = reinterpret_cast<uint16_t*>(reinterpret_cast<uint64_t*>(smem_raw) + (size_t)FOLD_WARPS * FOLD_CAP) +
                    (size_t)warp * FOLD_CAP;
-  const int64_t nq = FROM_LIST ? counters[CNT_DEFER] : npix;
+  const int64_t nq = counters[CNT_DEFER];
   for (int64_t qi = (int64_t)blockIdx.x * FOLD_WARPS + warp; qi < nq; qi += (int64_t)gridDim.x * FOLD_WARPS) {
-    const int64_t pix = FROM_LIST ? (int64_t)defer[qi] : qi;
+    const int64_t pix = (int64_t)defer[qi];
     const int64_t base = off[pix];
     const int n = (int)(off[pix + 1] - base);
     if (n == 0) continue;
     const uint32_t* S = perm + base;
-    if (!FROM_LIST && n > COARSEN_CACHE) {
-      if (lane == 0) defer[atomicAdd((unsigned long long*)&counters[CNT_DEFER], 1ull)] = (int32_t)pix;
-      continue;
-    }
-    if (FROM_LIST && n > FOLD_CAP) {   // rare: pass through, re-keyed by the target node
+    if (n > FOLD_CAP) {   // rare: pass through, re-keyed by the target node
       for (int k0 = 0; k0 < n; k0 += 32) {
         const int k = k0 + (int)lane;
         const int64_t slot = warp_append(&counters[CNT_AGG_OUT], k < n ? 1 : 0);
@@ -974,49 +940,6 @@ __global__ void __launch_bounds__(FOLD_WARPS * 32, FROM_LIST ? 1 : COARSEN_MINB)
           else atomicAdd((unsigned long long*)&counters[CNT_OVERFLOW], 1ull);
         }
       }
-      continue;
-    }
-    if (!FROM_LIST) {
-      RunCache C{reinterpret_cast<uint32_t*>(keys), reinterpret_cast<float*>(keys) + 512,
-                 reinterpret_cast<float*>(keys) + 1024, reinterpret_cast<int32_t*>(keys) + 1536};
-      bool sorted;
-      if (n <= 64) sorted = sort_pixel_cache<2>(recs, S, n, leaf_node, key_base, C);
-      else if (n <= 128) sorted = sort_pixel_cache<4>(recs, S, n, leaf_node, key_base, C);
-      else if (n <= 256) sorted = sort_pixel_cache<8>(recs, S, n, leaf_node, key_base, C);
-      else sorted = sort_pixel_cache<16>(recs, S, n, leaf_node, key_base, C);
-      if (!sorted) {   // tied sort keys: the list pass orders the pixel under the total order
-        if (lane == 0) defer[atomicAdd((unsigned long long*)&counters[CNT_DEFER], 1ull)] = (int32_t)pix;
-        continue;
-      }
-      auto head = [&](int k) -> bool {
-        return k == 0 || fabsf(C.an[k] - C.af[k - 1]) > tau * fmaxf(1.0f, fabsf(C.an[k])) || C.anc[k] != C.anc[k - 1];
-      };
-      for (int k0 = 0; k0 < n; k0 += 32) {
-        const int k = k0 + (int)lane;
-        const bool h = k < n && head(k);
-        const int64_t slot = warp_append(&counters[CNT_AGG_OUT], h ? 1 : 0);
-        if (!h) continue;
-        double A = 1.0, B0 = 0.0, B1 = 0.0, B2 = 0.0;
-        int q = k;
-        do {
-          const rc_seg* sq = recs + C.rid[q];
-          const float a = sq->a;
-          const float4 hb = reinterpret_cast<const float4*>(sq)[1];   // b0, b1, b2, key
-          B0 = fma(A, (double)hb.x, B0);
-          B1 = fma(A, (double)hb.y, B1);
-          B2 = fma(A, (double)hb.z, B2);
-          A *= (double)a;
-          ++q;
-        } while (q < n && !head(q));
-        if (slot < out_cap) {
-          const float bb[3] = {(float)B0, (float)B1, (float)B2};
-          store_seg(out + slot, (uint32_t)pix, C.an[k], C.af[q - 1], (float)A, bb,
-                    key_base + (uint32_t)node_first[C.anc[k]]);
-        } else {
-          atomicAdd((unsigned long long*)&counters[CNT_OVERFLOW], 1ull);
-        }
-      }
-      __syncwarp();
       continue;
     }
     {
@@ -1061,6 +984,122 @@ __global__ void __launch_bounds__(FOLD_WARPS * 32, FROM_LIST ? 1 : COARSEN_MINB)
         const float bb[3] = {(float)B0, (float)B1, (float)B2};
         store_seg(out + slot, s0.pixel, s0.alpha_near, af, (float)A, bb,
                   key_base + (uint32_t)node_first[anc(k)]);
+      } else {
+        atomicAdd((unsigned long long*)&counters[CNT_OVERFLOW], 1ull);
+      }
+    }
+    __syncwarp();
+  }
+}
+
+// Fast path of the aggregation pass: pixels with <= COARSEN_FAST_CAP records
+// (C5: ~240 records per covered pixel after the on-chip fold).
+// Each record is gathered ONCE (32 bytes, through the pixel-bucketed
+// permutation) into the warp's shared memory together with its target-level
+// node; the sort (register bitonic over (sort key, local index)), the run
+// detection and the folds then read shared memory only (round 1 re-gathered
+// every record three times from HBM: latency bound).  Pixels with tied sort
+// keys or more records go to the list pass.
+constexpr int COARSEN_FAST_CAP = 512;
+constexpr int COARSEN_FAST_WARPS = 2;   // 19.5 KB of shared memory per warp: 5 CTAs (10 warps) per SM
+constexpr size_t COARSEN_FAST_SMEM_WARP = (size_t)COARSEN_FAST_CAP * (sizeof(rc_seg) + sizeof(int32_t) + sizeof(uint16_t));
+
+template <int E>
+__device__ __forceinline__ bool sort_local(const rc_seg* R, int n, uint16_t* ord) {
+  const unsigned lane = threadIdx.x & 31;
+  uint64_t key[E];
+  uint32_t id[E];
+#pragma unroll
+  for (int e = 0; e < E; ++e) {
+    const int i = (int)lane * E + e;
+    id[e] = (uint32_t)i;
+    key[e] = i < n ? sort_key(R[i]) : ~0ull;
+  }
+  warp_sort_blocked<E>(key, id);
+  uint64_t prev_key = __shfl_up_sync(0xffffffffu, key[E - 1], 1);
+  if (lane == 0) prev_key = ~0ull;
+  bool tie = false;
+#pragma unroll
+  for (int e = 0; e < E; ++e) {
+    const int i = (int)lane * E + e;
+    tie |= i < n && key[e] == prev_key;
+    prev_key = key[e];
+    if (i < n) ord[i] = (uint16_t)id[e];
+  }
+  __syncwarp();
+  return !__any_sync(0xffffffffu, tie);
+}
+
+__global__ void __launch_bounds__(COARSEN_FAST_WARPS * 32, 5) k_coarsen_fast(
+    const rc_seg* __restrict__ recs, const uint32_t* __restrict__ perm, const int64_t* __restrict__ off, int64_t npix,
+    const int32_t* __restrict__ node_first, const int32_t* __restrict__ leaf_node, uint32_t key_base, float tau,
+    rc_seg* __restrict__ out, int64_t out_cap, int32_t* __restrict__ defer, int64_t* __restrict__ counters) {
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  const int warp = threadIdx.x >> 5;
+  const unsigned lane = threadIdx.x & 31;
+  unsigned char* wb = smem_raw + (size_t)warp * COARSEN_FAST_SMEM_WARP;
+  rc_seg* R = reinterpret_cast<rc_seg*>(wb);
+  int32_t* anc = reinterpret_cast<int32_t*>(wb + COARSEN_FAST_CAP * sizeof(rc_seg));
+  uint16_t* ord = reinterpret_cast<uint16_t*>(wb + COARSEN_FAST_CAP * (sizeof(rc_seg) + sizeof(int32_t)));
+  const float4* recs4 = reinterpret_cast<const float4*>(recs);
+  for (int64_t pix = (int64_t)blockIdx.x * COARSEN_FAST_WARPS + warp; pix < npix;
+       pix += (int64_t)gridDim.x * COARSEN_FAST_WARPS) {
+    const int64_t base = off[pix];
+    const int n = (int)(off[pix + 1] - base);
+    if (n == 0) continue;
+    if (n > COARSEN_FAST_CAP) {
+      if (lane == 0) defer[atomicAdd((unsigned long long*)&counters[CNT_DEFER], 1ull)] = (int32_t)pix;
+      continue;
+    }
+    const uint32_t* S = perm + base;
+    // 1. one gather per record (and its node at the target level)
+#pragma unroll 2
+    for (int k = lane; k < n; k += 32) {
+      const uint32_t id = S[k];
+      const float4 lo = recs4[2 * (size_t)id], hi = recs4[2 * (size_t)id + 1];
+      float4* d = reinterpret_cast<float4*>(R + k);
+      d[0] = lo;
+      d[1] = hi;
+      anc[k] = leaf_node[__float_as_uint(hi.w) - key_base];
+    }
+    __syncwarp();
+    // 2. order by (alpha_near, key) in registers
+    bool sorted;
+    if (n <= 64) sorted = sort_local<2>(R, n, ord);
+    else if (n <= 128) sorted = sort_local<4>(R, n, ord);
+    else if (n <= 256) sorted = sort_local<8>(R, n, ord);
+    else sorted = sort_local<16>(R, n, ord);
+    if (!sorted) {   // tied sort keys: the list pass orders the pixel under the total order
+      if (lane == 0) defer[atomicAdd((unsigned long long*)&counters[CNT_DEFER], 1ull)] = (int32_t)pix;
+      __syncwarp();
+      continue;
+    }
+    // 3. maximal runs of touching records of one target node, folded nearest first (Eq. aggregate)
+    auto head = [&](int k) -> bool {
+      if (k == 0) return true;
+      const rc_seg& x = R[ord[k - 1]];
+      const rc_seg& y = R[ord[k]];
+      return fabsf(y.alpha_near - x.alpha_far) > tau * fmaxf(1.0f, fabsf(y.alpha_near)) || anc[ord[k]] != anc[ord[k - 1]];
+    };
+    for (int k0 = 0; k0 < n; k0 += 32) {
+      const int k = k0 + (int)lane;
+      const bool h = k < n && head(k);
+      const int64_t slot = warp_append(&counters[CNT_AGG_OUT], h ? 1 : 0);
+      if (!h) continue;
+      double A = 1.0, B0 = 0.0, B1 = 0.0, B2 = 0.0;
+      int q = k;
+      do {
+        const rc_seg& sq = R[ord[q]];
+        B0 = fma(A, (double)sq.b[0], B0);
+        B1 = fma(A, (double)sq.b[1], B1);
+        B2 = fma(A, (double)sq.b[2], B2);
+        A *= (double)sq.a;
+        ++q;
+      } while (q < n && !head(q));
+      if (slot < out_cap) {
+        const float bb[3] = {(float)B0, (float)B1, (float)B2};
+        store_seg(out + slot, (uint32_t)pix, R[ord[k]].alpha_near, R[ord[q - 1]].alpha_far, (float)A, bb,
+                  key_base + (uint32_t)node_first[anc[ord[k]]]);
       } else {
         atomicAdd((unsigned long long*)&counters[CNT_OVERFLOW], 1ull);
       }
@@ -1130,10 +1169,15 @@ static void cast_affine_P(const CamConst& cc, const TreeConst* trees, DevLeafVie
                           const Rect16* vrect, const int64_t* chunk_off, const int32_t* chunk_elem, int64_t nchunks,
                           uint32_t key_base, rc_seg* segs, int64_t seg_cap, int32_t* hits_pp, int64_t* counters,
                           int grid, cudaStream_t s) {
+  const bool adapt = cc.scheme != RC_SCHEME_GL || cc.c_rk > 0.0f;   // separate instantiation (see cast_curved.cu)
 #define CASE(N)                                                                                                    \
   case N:                                                                                                          \
-    k_cast_affine<P, N><<<grid, 256, 0, s>>>(cc, trees, L, vis, vrect, chunk_off, chunk_elem, nchunks, key_base,   \
-                                             segs, seg_cap, hits_pp, counters);                                    \
+    if (adapt)                                                                                                     \
+      k_cast_affine<P, N, true><<<grid, 256, 0, s>>>(cc, trees, L, vis, vrect, chunk_off, chunk_elem, nchunks,     \
+                                                     key_base, segs, seg_cap, hits_pp, counters);                  \
+    else                                                                                                           \
+      k_cast_affine<P, N, false><<<grid, 256, 0, s>>>(cc, trees, L, vis, vrect, chunk_off, chunk_elem, nchunks,    \
+                                                      key_base, segs, seg_cap, hits_pp, counters);                 \
     break;
   switch (cc.N) { CASE(1) CASE(2) CASE(3) CASE(4) CASE(5) CASE(6) CASE(7) CASE(8) }
 #undef CASE
@@ -1196,20 +1240,22 @@ cudaError_t launch_coarsen(const rc_seg* recs, const uint32_t* perm, const int64
                            const int32_t* node_first, const int32_t* leaf_node, uint32_t key_base, float tau, rc_seg* out,
                            int64_t out_cap, int32_t* defer, int64_t* counters, int max_grid, cudaStream_t s) {
   static bool attr = false;
-  const size_t smem1 = (size_t)FOLD_WARPS * COARSEN_CACHE * 2 * sizeof(uint64_t);
-  const size_t smem2 = (size_t)FOLD_WARPS * FOLD_CAP * (sizeof(uint64_t) + sizeof(uint16_t));
+  const size_t smemf = COARSEN_FAST_SMEM_WARP * COARSEN_FAST_WARPS;
+  const size_t smeml = (size_t)FOLD_WARPS * FOLD_CAP * (sizeof(uint64_t) + sizeof(uint16_t));
   if (!attr) {
-    cudaError_t e = cudaFuncSetAttribute(k_coarsen<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem2);
+    cudaError_t e = cudaFuncSetAttribute(k_coarsen_fast, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smemf);
+    if (e == cudaSuccess)
+      e = cudaFuncSetAttribute(k_coarsen_list, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smeml);
     if (e != cudaSuccess) return e;
     attr = true;
   }
   cudaError_t e = cudaMemsetAsync(counters + CNT_DEFER, 0, sizeof(int64_t), s);
   if (e != cudaSuccess) return e;
-  int grid = (int)std::min<int64_t>((npix + FOLD_WARPS - 1) / FOLD_WARPS, (int64_t)max_grid);
-  k_coarsen<false><<<grid, FOLD_WARPS * 32, smem1, s>>>(recs, perm, off, npix, node_first, leaf_node, key_base, tau,
-                                                        out, out_cap, defer, counters);
-  k_coarsen<true><<<std::min(grid, 296), FOLD_WARPS * 32, smem2, s>>>(recs, perm, off, npix, node_first, leaf_node,
-                                                                      key_base, tau, out, out_cap, defer, counters);
+  const int grid = (int)std::min<int64_t>((npix + COARSEN_FAST_WARPS - 1) / COARSEN_FAST_WARPS, (int64_t)max_grid);
+  k_coarsen_fast<<<grid, COARSEN_FAST_WARPS * 32, smemf, s>>>(recs, perm, off, npix, node_first, leaf_node, key_base,
+                                                              tau, out, out_cap, defer, counters);
+  k_coarsen_list<<<std::min(grid, 296), FOLD_WARPS * 32, smeml, s>>>(recs, perm, off, node_first, leaf_node, key_base,
+                                                                     tau, out, out_cap, defer, counters);
   g_launches += 2;
   return cudaGetLastError();
 }

@@ -290,6 +290,13 @@ extern "C" rc_status rc_camera_set(rc_forest* f, const rc_camera* cam, void* str
   c.N = cam->gl_points;
   c.newton_max = cam->newton_max_iter > 0 ? cam->newton_max_iter : 20;
   c.newton_tol = (float)(cam->newton_tol > 0 ? cam->newton_tol : 1e-6);
+  if (cam->scheme < RC_SCHEME_GL || cam->scheme > RC_SCHEME_SIMPSON)
+    return fail(RC_ERR_INVALID_ARG, "scheme must be one of RC_SCHEME_*");
+  if (!(cam->c_rk >= 0.0) || cam->max_depth < 0 || cam->max_depth > 24)
+    return fail(RC_ERR_INVALID_ARG, "c_rk must be >= 0 and max_depth in [0, 24]");
+  c.scheme = cam->scheme;
+  c.c_rk = (float)cam->c_rk;
+  c.max_depth = cam->max_depth > 0 ? cam->max_depth : 24;
   c.n = n;
   c.ell = cam->pixel_size;
   c.far_dist = cam->far_dist;
@@ -539,17 +546,6 @@ extern "C" rc_status rc_cast_segments(rc_forest* f, int32_t fold_levels, void* s
     f->scratch_bytes = cast_curved_scratch_per_cta() * (size_t)grid_curved;
     CU(dmalloc((void**)&f->d_scratch, f->scratch_bytes, s));
   }
-  // element slots (k_prep_slots): the visible list in batches of at most
-  // RC_SLOT_BATCH leaves (+ one unit window of margin), bounded memory
-  const int64_t slot_need = curved ? std::min<int64_t>(nvis + RC_UNIT_LEAVES, RC_SLOT_BATCH + RC_UNIT_LEAVES) : 0;
-  if (curved && f->slot_cap < slot_need) {
-    if (f->d_gslot) dfree(f->d_gslot, s);
-    f->d_gslot = nullptr;
-    f->slot_cap = 0;
-    CU(dmalloc((void**)&f->d_gslot, slot_record_bytes() * (size_t)slot_need, s));
-    f->slot_cap = slot_need;
-  }
-  const int64_t batch = std::max<int64_t>(f->slot_cap - RC_UNIT_LEAVES, 1);
   // record capacity: the previous frame's count, else an estimate; a too
   // small buffer is grown to the exact count and the cast repeated
   // reuse the larger of the two record buffers (aggregation swaps them)
@@ -569,13 +565,35 @@ extern "C" rc_status rc_cast_segments(rc_forest* f, int32_t fold_levels, void* s
       est = std::min(est, cap);
     }
   }
-  int64_t need = std::max<int64_t>(f->h_cast_total + f->h_cast_total / 8, est) + 4096;
+  int64_t need = std::max<int64_t>(f->h_cast_total + f->h_cast_total / 32, est) + 4096;
   CU(grow(&f->d_segs, &f->seg_cap, need, s));
+  // element slots (k_prep_slots): the visible list in batches of at most
+  // RC_SLOT_BATCH leaves (+ one unit window of margin), sized after the
+  // records from the memory left (at least 1M leaves per batch)
+  if (curved) {
+    int64_t want = std::min<int64_t>(nvis + RC_UNIT_LEAVES, RC_SLOT_BATCH + RC_UNIT_LEAVES);
+    if (f->slot_cap < want) {
+      size_t free_b = 0, total_b = 0;
+      if (cudaMemGetInfo(&free_b, &total_b) == cudaSuccess) {
+        const int64_t fit = (int64_t)(free_b / 3 / slot_record_bytes());
+        want = std::max<int64_t>(std::min(want, fit), std::min<int64_t>(want, ((int64_t)1 << 20) + RC_UNIT_LEAVES));
+      }
+    }
+    if (f->slot_cap < want) {
+      if (f->d_gslot) dfree(f->d_gslot, s);
+      f->d_gslot = nullptr;
+      f->slot_cap = 0;
+      CU(dmalloc((void**)&f->d_gslot, slot_record_bytes() * (size_t)want, s));
+      f->slot_cap = want;
+    }
+  }
+  const int64_t batch = std::max<int64_t>(f->slot_cap - RC_UNIT_LEAVES, 1);
   for (int attempt = 0; attempt < 2; ++attempt) {
     CU(cudaMemsetAsync(f->d_hits_pp, 0, sizeof(int32_t) * npix, s));
     CU(cudaMemsetAsync(f->d_counters + CNT_SEGS, 0, sizeof(int64_t) * 3, s));
     CU(cudaMemsetAsync(f->d_counters + CNT_OVERFLOW, 0, sizeof(int64_t) * 3, s));
     CU(cudaMemsetAsync(f->d_counters + CNT_UNITS, 0, sizeof(int64_t) * 6, s));
+    CU(cudaMemsetAsync(f->d_counters + CNT_DEPTH_CAP, 0, sizeof(int64_t), s));
     CU(cudaEventRecord(f->ev0, s));
     if (f->h_chunks > 0) {
       if (!curved) {
@@ -670,6 +688,7 @@ extern "C" rc_status rc_segments_get(rc_forest* f, rc_segments* out, void* strea
   out->fallback_tasks = c[CNT_FALLBACK];
   out->segs = f->d_segs;
   out->hits_per_pixel = f->d_hits_pp;
+  out->depth_capped = c[CNT_DEPTH_CAP];
   if (c[CNT_OVERFLOW] > 0)
     return fail(RC_ERR_CAPACITY, "segment buffer overflow: %lld records dropped", (long long)c[CNT_OVERFLOW]);
   return RC_OK;

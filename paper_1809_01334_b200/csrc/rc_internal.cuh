@@ -14,7 +14,7 @@
 #define RC_NODE_LEVELS 8    // coarsening levels of the node tables (fold + aggregation cycles)
 #define RC_UNIT_CHUNKS 128  // chunks per fold unit of the curved segment kernel (<= 4096 pairs)
 #define RC_UNIT_LEAVES 64   // visible leaves per fold unit (their geometry is staged in shared memory)
-#define RC_SLOT_BATCH (1 << 24)   // visible leaves per element-slot batch of the curved path (672 B each)
+#define RC_SLOT_BATCH (1 << 23)   // visible leaves per element-slot batch of the curved path (672 B each)
 
 // Fold unit of the curved segment kernel (row a6): a contiguous chunk range
 // of at most RC_UNIT_LEAVES visible leaves [vfirst, vfirst+nvis) inside one
@@ -52,6 +52,9 @@ struct CamConst {
   float u[RC_MAX_N], w[RC_MAX_N], S[RC_MAX_N * RC_MAX_N];
   float kappa0, inv_F, q0;
   float f_R0[3], f_Rt[3], f_Ru[3], f_Ot[3], f_Ou[3];   // fp32 copies for the conservative prefilter
+  int scheme;                   // RC_SCHEME_* (segment integrator)
+  int max_depth;                // Alg. 1 recursion cap
+  float c_rk;                   // Alg. 1 threshold (0: no recursion)
 };
 
 // Per-tree constants (device buffer, warp-uniform reads).
@@ -194,7 +197,8 @@ enum {
   CNT_FALLBACK = 77,   // ... of which needed the projected-patch (2D) method
   CNT_DEFER = 78,      // composite: pixels deferred to the large-pixel pass
   CNT_BIGPIX = 79,     // composite: pixels with more records than FOLD_CAP_LIST (written as NaN)
-  CNT_TOTAL = 80
+  CNT_DEPTH_CAP = 80,  // Alg. 1 steps taken at the recursion cap (must be 0)
+  CNT_TOTAL = 96
 };
 
 // NCCL communicator (comm.cu)

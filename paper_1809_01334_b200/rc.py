@@ -19,6 +19,7 @@ STATUS_NAMES = {0: "RC_OK", -1: "RC_ERR_INVALID_ARG", -2: "RC_ERR_NOT_SFC_SORTED
                 -8: "RC_ERR_NUMERIC"}
 RC_HOST_COPY, RC_DEVICE_COPY, RC_HOST_COPY_TRUSTED = 0, 1, 2
 RC_PERSPECTIVE, RC_ORTHOGRAPHIC = 0, 1
+SCHEMES = {"gl": 0, "euler": 1, "heun2": 2, "heun3": 3, "rk4": 4, "gauss2": 5, "simpson": 6}   # RC_SCHEME_*
 
 
 class RcError(RuntimeError):
@@ -42,7 +43,8 @@ class CameraDesc(C.Structure):
     _fields_ = [("projection", C.c_int32), ("origin", C.c_double * 3), ("view", C.c_double * 3),
                 ("right", C.c_double * 3), ("up", C.c_double * 3), ("pixel_size", C.c_double),
                 ("far_dist", C.c_double), ("width", C.c_int32), ("height", C.c_int32), ("gl_points", C.c_int32),
-                ("newton_tol", C.c_double), ("newton_max_iter", C.c_int32)]
+                ("newton_tol", C.c_double), ("newton_max_iter", C.c_int32), ("scheme", C.c_int32),
+                ("c_rk", C.c_double), ("max_depth", C.c_int32)]
 
 
 class Segments(C.Structure):
@@ -51,7 +53,7 @@ class Segments(C.Structure):
                 ("raw_segments", C.c_int64), ("level", C.c_int64), ("units", C.c_int64),
                 ("unfolded_units", C.c_int64), ("face_tasks", C.c_int64), ("fallback_tasks", C.c_int64),
                 ("segs", C.c_void_p),
-                ("hits_per_pixel", C.c_void_p)]
+                ("hits_per_pixel", C.c_void_p), ("depth_capped", C.c_int64)]
 
 
 class PairResult(C.Structure):
@@ -147,13 +149,19 @@ def device_view(ptr, shape, typestr):
     return torch.as_tensor(_DevArray(ptr, shape, typestr), device="cuda")
 
 
-def camera_desc(cam, gl_points=None, newton_tol=None, newton_max_iter=None) -> CameraDesc:
+def camera_desc(cam, gl_points=None, newton_tol=None, newton_max_iter=None, scheme=None, c_rk=None,
+                max_depth=None) -> CameraDesc:
+    """scheme / c_rk / max_depth: the segment integrator; defaults from the camera
+    object's attributes when present, else the R13 GL rule without recursion."""
     d3 = C.c_double * 3
+    sch = scheme if scheme is not None else getattr(cam, "scheme", "gl")
     return CameraDesc(int(cam.projection), d3(*map(float, cam.origin)), d3(*map(float, cam.view)),
                       d3(*map(float, cam.right)), d3(*map(float, cam.up)), float(cam.pixel_size),
                       float(cam.far_dist), int(cam.width), int(cam.height),
                       int(gl_points or cam.gl_points), float(newton_tol or cam.newton_tol),
-                      int(newton_max_iter or cam.newton_max_iter))
+                      int(newton_max_iter or cam.newton_max_iter), SCHEMES[sch] if isinstance(sch, str) else int(sch),
+                      float(c_rk if c_rk is not None else getattr(cam, "c_rk", 0.0)),
+                      int(max_depth if max_depth is not None else getattr(cam, "max_depth", 0)))
 
 
 def unpack_segments(raw):
@@ -289,7 +297,7 @@ class Forest:
                 "newton_failures": s.newton_failures, "face_failures": s.face_failures,
                 "num_visible": s.num_visible, "raw": raw, "raw_segments": s.raw_segments, "level": s.level,
                 "units": s.units, "unfolded_units": s.unfolded_units, "face_tasks": s.face_tasks,
-                "fallback_tasks": s.fallback_tasks,
+                "fallback_tasks": s.fallback_tasks, "depth_capped": s.depth_capped,
                 "hits_per_pixel": hpp}
 
     def aggregate(self, cycles, stream=None):

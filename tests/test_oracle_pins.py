@@ -744,3 +744,57 @@ def test_skimming_rays_two_roots_one_face_P11():
                     if abs(x0[2] - 1) < 1e-9 and abs(x1[2] - 1) < 1e-9:
                         skims += 1       # entry and exit on the outer face
     assert checked > 50 and skims > 3
+
+
+# ---------------------------------------------------------------------------
+# The paper's integrators with Alg. 1
+# ---------------------------------------------------------------------------
+def _amp(scheme, z):
+    """Stability function R(z) of the explicit schemes for y' = lambda y (z = lambda dx)."""
+    return {"euler": 1 + z, "heun2": 1 + z + z * z / 2, "heun3": 1 + z + z * z / 2 + z ** 3 / 6,
+            "rk4": 1 + z + z * z / 2 + z ** 3 / 6 + z ** 4 / 24}[scheme]
+
+
+@pytest.mark.parametrize("scheme", ["euler", "heun2", "heun3", "rk4"])
+def test_alg1_constant_medium_closed_form(scheme):
+    """Constant beta = 10, gamma = 2, dx = 1, c_RK = 0.5: Alg. 1 halves the step
+    until dx beta <= c_RK, i.e. to 1/32 (depth ceil(log2(10/0.5)) = 5, SPEC.md:195);
+    the explicit scheme then applies its stability function R(z), z = -10/32,
+    32 times: A = R^32, and B = (gamma/beta)(1 - A) because every RK method
+    keeps the equilibrium gamma/beta of B' = gamma - beta B exactly."""
+    a, b, depth, fl = oracle.segment_scheme(scheme, lambda s: (10.0, 2.0), 1.0, c_rk=0.5)
+    A = _amp(scheme, -10.0 / 32) ** 32
+    assert depth == 5 and fl == 0
+    assert abs(a - A) <= 1e-13 * abs(A)
+    assert np.all(np.abs(b - 0.2 * (1 - A)) <= 1e-13)
+
+
+def test_alg1_empirical_orders():
+    """Halving c_RK on a smooth medium: error ratios 2^M for the explicit
+    M-stage schemes ("error rate of c_RK^M"), 2^4 for Gauss-2 ("rate
+    c_RK^2M"), 2^2 for Simpson's B; exact mode is the
+    reference (P12-pinned)."""
+    fn = lambda s: (1.0 + 0.5 * math.sin(3 * s), [0.3 + 0.2 * math.cos(2 * s), 0.5, 0.1 * s])
+    ae, be, _ = oracle.segment_exact(fn, 1.7)
+    for scheme, order in (("euler", 1), ("heun2", 2), ("heun3", 3), ("rk4", 4), ("gauss2", 4), ("simpson", 2)):
+        errs = []
+        for c in (0.2, 0.1, 0.05):
+            a, b, _, _ = oracle.segment_scheme(scheme, fn, 1.7, c_rk=c)
+            errs.append(max(abs(a - ae), float(np.abs(b - be).max())))
+        rates = [math.log2(errs[k] / errs[k + 1]) for k in range(2)]
+        assert all(abs(r - order) <= 0.5 for r in rates), (scheme, rates)
+
+
+def test_gauss2_and_simpson_special_cases():
+    """Gauss-2 without recursion: A -> 1 for dx beta -> infinity (the unphysical
+    limit the paper notes); Simpson: A exact for constant
+    beta (Eq. simpson), B = gamma dx (b0 A + b1 sqrt(A) + b2) written out."""
+    a, b, _, _ = oracle.segment_scheme("gauss2", lambda s: (1e7, 1.0), 1.0, c_rk=0.0)
+    assert abs(a - 1.0) < 1e-5
+    a, b, d, _ = oracle.segment_scheme("simpson", lambda s: (0.8, 0.3), 2.0, c_rk=0.0)
+    A = math.exp(-1.6)
+    assert d == 0 and abs(a - A) < 1e-15
+    assert np.all(np.abs(b - 2.0 * 0.3 * (A / 6 + 4 / 6 * math.sqrt(A) + 1 / 6)) < 1e-15)
+    # gauss2 with recursion: depth ceil(log2(beta L / c)) and the exact constant-medium value within c^4
+    a, b, d, _ = oracle.segment_scheme("gauss2", lambda s: (4.0, 1.0), 1.0, c_rk=0.25)
+    assert d == 4 and abs(a - math.exp(-4.0)) < 1e-5
