@@ -288,6 +288,17 @@ rc_status rc_render_frame(rc_forest* f, const rc_camera* cam, int32_t fold_level
                           const float background[3], float* d_rgba, int64_t capacity_floats, int64_t* hit_pairs,
                           void* stream);
 
+/* CUDA-graph frames for launch-bound affine forests (C1, C2).
+ * rc_frame_capture runs one rc_render_frame (fold level 0, no cycles) that
+ * sizes every buffer for the camera, then captures the same frame without host
+ * synchronisation (counts read on the device) into a graph owned by the
+ * forest; rc_frame_replay launches it on the caller's stream (async).  The
+ * graph renders this camera into this d_rgba; capture again after a camera
+ * change.  RC_ERR_STATE for curved forests. */
+rc_status rc_frame_capture(rc_forest* f, const rc_camera* cam, const float background[3], float* d_rgba,
+                           int64_t capacity_floats, void* stream);
+rc_status rc_frame_replay(rc_forest* f, void* stream);
+
 /* Device memory: librc keeps the blocks of destroyed forests and regrown
  * buffers in a caching pool (reused by later allocations of similar size;
  * released automatically when an allocation would otherwise fail).

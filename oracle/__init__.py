@@ -99,6 +99,8 @@ def lib():
         _lib.orc_segment_scheme.argtypes = [C.c_int, C.c_int, d, C.c_int, MEDIUM_FN, C.c_void_p, d, P(d),
                                             C.c_void_p, P(C.c_int)]
         _lib.orc_set_scheme.argtypes = [C.c_int, d, C.c_int]
+        _lib.orc_medium_evals.argtypes = [C.c_int]
+        _lib.orc_medium_evals.restype = C.c_longlong
         _lib.orc_set_force_general.argtypes = [C.c_int]
         _lib.orc_fold_pixel.argtypes = [C.c_int, C.c_void_p, d, C.c_void_p, C.c_void_p, C.c_void_p]
     return _lib
@@ -328,6 +330,11 @@ def segment_scheme(scheme, fn, L, N=4, c_rk=0.0, max_depth=24):
     depth = lib().orc_segment_scheme(SCHEMES[scheme], N, c_rk, max_depth, cb, None, L, C.byref(a), _ptr(b),
                                      C.byref(fl))
     return a.value, b, depth, fl.value
+
+
+def medium_evals(reset=False):
+    """Field evaluations made by orc_render since the last reset (diagnostic)."""
+    return int(lib().orc_medium_evals(1 if reset else 0))
 
 
 def set_scheme(scheme, c_rk=0.0, max_depth=24):

@@ -1062,8 +1062,17 @@ typedef struct {
   const orc_scene* sc; int64_t e; double o[3], r[3], alpha_near, rn;
 } medium_ctx;
 
+static long long g_medium_evals = 0;   /* field evaluations of orc_render (diagnostic) */
+long long orc_medium_evals(int reset) {
+  long long v = g_medium_evals;
+  if (reset) g_medium_evals = 0;
+  return v;
+}
+
 static void medium_eval(void* vctx, double s, double* kappa, double* q3) {
   medium_ctx* m = (medium_ctx*)vctx;
+#pragma omp atomic
+  g_medium_evals++;
   double al = m->alpha_near + s / m->rn;
   double p[3] = {m->o[0] + al * m->r[0], m->o[1] + al * m->r[1], m->o[2] + al * m->r[2]};
   double xi[3];

@@ -69,6 +69,7 @@ void orc_segment_rule(int N, orc_medium_fn fn, void* ctx, double L, double* a, d
 int  orc_segment_scheme(int scheme, int N, double c_rk, int max_depth, orc_medium_fn fn, void* ctx, double L,
                         double* a, double b[3], int* flags);
 void orc_set_scheme(int scheme, double c_rk, int max_depth);
+long long orc_medium_evals(int reset);   /* field evaluations of orc_render so far (diagnostic) */
 
 /* ---- geometry / camera ---- */
 void orc_gll(int R, double* eta);

@@ -307,11 +307,13 @@ __global__ void __launch_bounds__(256) k_cast_affine(CamConst cc, const TreeCons
                                                      const int32_t* __restrict__ vis, const Rect16* __restrict__ vrect,
                                                      const int64_t* __restrict__ chunk_off,
                                                      const int32_t* __restrict__ chunk_elem, int64_t nchunks,
+                                                     const int64_t* __restrict__ d_nchunks,
                                                      uint32_t key_base, rc_seg* __restrict__ segs, int64_t seg_cap,
                                                      int32_t* __restrict__ hits_pp, int64_t* __restrict__ counters) {
   constexpr int NF = (P + 1) * (P + 1) * (P + 1);
   const unsigned lane = threadIdx.x & 31;
   const float half_w = 0.5f * (cc.W - 1), half_h = 0.5f * (cc.H - 1);
+  if (d_nchunks) nchunks = min(nchunks, *d_nchunks);   // device-side count (CUDA-graph frames), nchunks = capacity
   int local_hits = 0, capped = 0;
   for (;;) {
     int64_t c = 0;
@@ -496,15 +498,18 @@ __global__ void k_pack_offsets(const int64_t* __restrict__ counts, int nranks, i
 // PAPER.md:395-427), overlaps resolved sequentially by Eq. segsplit /
 // Eq. segaverage.
 // ---------------------------------------------------------------------------
-__global__ void k_hist(const rc_seg* __restrict__ segs, int64_t n, int32_t* __restrict__ cnt) {
+__global__ void k_hist(const rc_seg* __restrict__ segs, int64_t n, const int64_t* __restrict__ d_n,
+                       int32_t* __restrict__ cnt) {
+  if (d_n) n = min(n, *d_n);   // device-side count (CUDA-graph frames), n = capacity
   for (int64_t s = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; s < n; s += (int64_t)gridDim.x * blockDim.x)
     atomicAdd(&cnt[segs[s].pixel], 1);
 }
 
 // bucket by pixel as a permutation (record indices, 4 bytes each) instead of
 // a sorted copy of the 32-byte records
-__global__ void k_scatter(const rc_seg* __restrict__ segs, int64_t n, const int64_t* __restrict__ off,
-                          int32_t* __restrict__ cursor, uint32_t* __restrict__ out) {
+__global__ void k_scatter(const rc_seg* __restrict__ segs, int64_t n, const int64_t* __restrict__ d_n,
+                          const int64_t* __restrict__ off, int32_t* __restrict__ cursor, uint32_t* __restrict__ out) {
+  if (d_n) n = min(n, *d_n);
   for (int64_t s = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; s < n; s += (int64_t)gridDim.x * blockDim.x) {
     const uint32_t pix = segs[s].pixel;
     int k = atomicAdd(&cursor[pix], 1);
@@ -514,8 +519,9 @@ __global__ void k_scatter(const rc_seg* __restrict__ segs, int64_t n, const int6
 
 // pixel-bucketed copy of the records (the composite then reads each pixel's
 // records contiguously instead of gathering them through a permutation)
-__global__ void k_scatter_rec(const rc_seg* __restrict__ segs, int64_t n, const int64_t* __restrict__ off,
-                              int32_t* __restrict__ cursor, rc_seg* __restrict__ out) {
+__global__ void k_scatter_rec(const rc_seg* __restrict__ segs, int64_t n, const int64_t* __restrict__ d_n,
+                              const int64_t* __restrict__ off, int32_t* __restrict__ cursor, rc_seg* __restrict__ out) {
+  if (d_n) n = min(n, *d_n);
   const int64_t stride = (int64_t)gridDim.x * blockDim.x;
   int64_t s = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   for (; s < n; s += stride) {
@@ -1074,36 +1080,80 @@ __global__ void __launch_bounds__(COARSEN_FAST_WARPS * 32, 5) k_coarsen_fast(
       __syncwarp();
       continue;
     }
-    // 3. maximal runs of touching records of one target node, folded nearest first (Eq. aggregate)
+    // 3. maximal runs of touching records of one target node, folded nearest
+    // first (Eq. aggregate) by the whole warp: lane l takes the l-th
+    // contiguous range of the sorted records; a segmented warp scan (head
+    // flags) carries the open run across lanes, so long runs (deep
+    // coarsening: one run per ray and node) do not serialise on one lane
     auto head = [&](int k) -> bool {
       if (k == 0) return true;
       const rc_seg& x = R[ord[k - 1]];
       const rc_seg& y = R[ord[k]];
       return fabsf(y.alpha_near - x.alpha_far) > tau * fmaxf(1.0f, fabsf(y.alpha_near)) || anc[ord[k]] != anc[ord[k - 1]];
     };
-    for (int k0 = 0; k0 < n; k0 += 32) {
-      const int k = k0 + (int)lane;
-      const bool h = k < n && head(k);
-      const int64_t slot = warp_append(&counters[CNT_AGG_OUT], h ? 1 : 0);
-      if (!h) continue;
-      double A = 1.0, B0 = 0.0, B1 = 0.0, B2 = 0.0;
-      int q = k;
-      do {
-        const rc_seg& sq = R[ord[q]];
-        B0 = fma(A, (double)sq.b[0], B0);
-        B1 = fma(A, (double)sq.b[1], B1);
-        B2 = fma(A, (double)sq.b[2], B2);
-        A *= (double)sq.a;
-        ++q;
-      } while (q < n && !head(q));
+    auto emit = [&](int64_t slot, int k0, int k1, const Acc& v) {
       if (slot < out_cap) {
-        const float bb[3] = {(float)B0, (float)B1, (float)B2};
-        store_seg(out + slot, (uint32_t)pix, R[ord[k]].alpha_near, R[ord[q - 1]].alpha_far, (float)A, bb,
-                  key_base + (uint32_t)node_first[anc[ord[k]]]);
+        const float bb[3] = {(float)v.B0, (float)v.B1, (float)v.B2};
+        store_seg(out + slot, (uint32_t)pix, R[ord[k0]].alpha_near, R[ord[k1]].alpha_far, (float)v.A, bb,
+                  key_base + (uint32_t)node_first[anc[ord[k0]]]);
       } else {
         atomicAdd((unsigned long long*)&counters[CNT_OVERFLOW], 1ull);
       }
+    };
+    const int per = (n + 31) / 32;
+    const int lo = min(n, (int)lane * per), hi = min(n, lo + per);
+    // pass 1: the lane's open tail (from its last head, or its start) and last head
+    bool F = false;
+    int HS = -1, nemit = 0;
+    Acc X{1.0, 0.0, 0.0, 0.0};
+    for (int k = lo; k < hi; ++k) {
+      if (head(k)) {
+        F = true;
+        HS = k;
+        X = Acc{1.0, 0.0, 0.0, 0.0};
+        nemit += k > 0 ? 1 : 0;   // the run ending at k - 1
+      }
+      const rc_seg& r = R[ord[k]];
+      acc_push(X, r.a, r.b[0], r.b[1], r.b[2]);
     }
+    nemit += (lo < hi && hi == n) ? 1 : 0;   // the pixel's last run
+    // exclusive segmented scan across lanes: the run entering this lane
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const bool Fo = __shfl_up_sync(0xffffffffu, F, o);
+      const int HSo = __shfl_up_sync(0xffffffffu, HS, o);
+      const double Ao = __shfl_up_sync(0xffffffffu, X.A, o), B0o = __shfl_up_sync(0xffffffffu, X.B0, o);
+      const double B1o = __shfl_up_sync(0xffffffffu, X.B1, o), B2o = __shfl_up_sync(0xffffffffu, X.B2, o);
+      if ((int)lane >= o && !F) {   // (nearer lanes) (+) (this one)
+        Acc y{Ao, B0o, B1o, B2o};
+        acc_push(y, X.A, X.B0, X.B1, X.B2);
+        X = y;
+        F = Fo;
+        HS = HSo;
+      }
+    }
+    Acc C{__shfl_up_sync(0xffffffffu, X.A, 1), __shfl_up_sync(0xffffffffu, X.B0, 1),
+          __shfl_up_sync(0xffffffffu, X.B1, 1), __shfl_up_sync(0xffffffffu, X.B2, 1)};
+    int start = __shfl_up_sync(0xffffffffu, HS, 1);
+    if (lane == 0) {
+      C = Acc{1.0, 0.0, 0.0, 0.0};
+      start = 0;
+    }
+    // pass 2: emit every run that ends in this lane's range
+    int64_t slot = warp_append(&counters[CNT_AGG_OUT], nemit);
+    Acc acc = C;
+    for (int k = lo; k < hi; ++k) {
+      if (k > 0 && head(k)) {
+        emit(slot++, start, k - 1, acc);
+        acc = Acc{1.0, 0.0, 0.0, 0.0};
+        start = k;
+      } else if (k == 0) {
+        start = 0;
+      }
+      const rc_seg& r = R[ord[k]];
+      acc_push(acc, r.a, r.b[0], r.b[1], r.b[2]);
+    }
+    if (lo < hi && hi == n) emit(slot++, start, n - 1, acc);
     __syncwarp();
   }
 }
@@ -1167,17 +1217,17 @@ cudaError_t launch_units(const int32_t* vis, const int64_t* nvis_p, int64_t nvis
 template <int P>
 static void cast_affine_P(const CamConst& cc, const TreeConst* trees, DevLeafView L, const int32_t* vis,
                           const Rect16* vrect, const int64_t* chunk_off, const int32_t* chunk_elem, int64_t nchunks,
-                          uint32_t key_base, rc_seg* segs, int64_t seg_cap, int32_t* hits_pp, int64_t* counters,
-                          int grid, cudaStream_t s) {
+                          const int64_t* d_nchunks, uint32_t key_base, rc_seg* segs, int64_t seg_cap,
+                          int32_t* hits_pp, int64_t* counters, int grid, cudaStream_t s) {
   const bool adapt = cc.scheme != RC_SCHEME_GL || cc.c_rk > 0.0f;   // separate instantiation (see cast_curved.cu)
 #define CASE(N)                                                                                                    \
   case N:                                                                                                          \
     if (adapt)                                                                                                     \
       k_cast_affine<P, N, true><<<grid, 256, 0, s>>>(cc, trees, L, vis, vrect, chunk_off, chunk_elem, nchunks,     \
-                                                     key_base, segs, seg_cap, hits_pp, counters);                  \
+                                                     d_nchunks, key_base, segs, seg_cap, hits_pp, counters);       \
     else                                                                                                           \
       k_cast_affine<P, N, false><<<grid, 256, 0, s>>>(cc, trees, L, vis, vrect, chunk_off, chunk_elem, nchunks,    \
-                                                      key_base, segs, seg_cap, hits_pp, counters);                 \
+                                                      d_nchunks, key_base, segs, seg_cap, hits_pp, counters);      \
     break;
   switch (cc.N) { CASE(1) CASE(2) CASE(3) CASE(4) CASE(5) CASE(6) CASE(7) CASE(8) }
 #undef CASE
@@ -1186,11 +1236,11 @@ static void cast_affine_P(const CamConst& cc, const TreeConst* trees, DevLeafVie
 cudaError_t launch_cast_affine(const CamConst& cc, const TreeConst* trees, DevLeafView L, int P, const int32_t* vis,
                                const Rect16* vrect, const int64_t* chunk_off, const int32_t* chunk_elem,
                                int64_t nchunks, uint32_t key_base, rc_seg* segs, int64_t seg_cap, int32_t* hits_pp,
-                               int64_t* counters, int grid, cudaStream_t s) {
-  if (P == 1) cast_affine_P<1>(cc, trees, L, vis, vrect, chunk_off, chunk_elem, nchunks, key_base, segs, seg_cap,
-                               hits_pp, counters, grid, s);
-  else cast_affine_P<2>(cc, trees, L, vis, vrect, chunk_off, chunk_elem, nchunks, key_base, segs, seg_cap, hits_pp,
-                        counters, grid, s);
+                               int64_t* counters, int grid, cudaStream_t s, const int64_t* d_nchunks) {
+  if (P == 1) cast_affine_P<1>(cc, trees, L, vis, vrect, chunk_off, chunk_elem, nchunks, d_nchunks, key_base, segs,
+                               seg_cap, hits_pp, counters, grid, s);
+  else cast_affine_P<2>(cc, trees, L, vis, vrect, chunk_off, chunk_elem, nchunks, d_nchunks, key_base, segs, seg_cap,
+                        hits_pp, counters, grid, s);
   ++g_launches;
   return cudaGetLastError();
 }
@@ -1216,22 +1266,22 @@ cudaError_t launch_pack_offsets(const int64_t* counts, int nranks, int64_t* dest
   return cudaGetLastError();
 }
 
-cudaError_t launch_hist(const rc_seg* segs, int64_t n, int32_t* cnt, int grid, cudaStream_t s) {
-  k_hist<<<grid, 256, 0, s>>>(segs, n, cnt);
+cudaError_t launch_hist(const rc_seg* segs, int64_t n, int32_t* cnt, int grid, cudaStream_t s, const int64_t* d_n) {
+  k_hist<<<grid, 256, 0, s>>>(segs, n, d_n, cnt);
   ++g_launches;
   return cudaGetLastError();
 }
 
 cudaError_t launch_scatter(const rc_seg* segs, int64_t n, const int64_t* off, int32_t* cursor, uint32_t* out,
-                           int grid, cudaStream_t s) {
-  k_scatter<<<grid, 256, 0, s>>>(segs, n, off, cursor, out);
+                           int grid, cudaStream_t s, const int64_t* d_n) {
+  k_scatter<<<grid, 256, 0, s>>>(segs, n, d_n, off, cursor, out);
   ++g_launches;
   return cudaGetLastError();
 }
 
 cudaError_t launch_scatter_rec(const rc_seg* segs, int64_t n, const int64_t* off, int32_t* cursor, rc_seg* out,
-                               int grid, cudaStream_t s) {
-  k_scatter_rec<<<grid, 256, 0, s>>>(segs, n, off, cursor, out);
+                               int grid, cudaStream_t s, const int64_t* d_n) {
+  k_scatter_rec<<<grid, 256, 0, s>>>(segs, n, d_n, off, cursor, out);
   ++g_launches;
   return cudaGetLastError();
 }

@@ -16,7 +16,7 @@ cudaError_t launch_expand(const int64_t* off, const int64_t* nvis_p, int64_t nvi
 cudaError_t launch_cast_affine(const CamConst& cc, const TreeConst* trees, DevLeafView L, int P, const int32_t* vis,
                                const Rect16* vrect, const int64_t* chunk_off, const int32_t* chunk_elem,
                                int64_t nchunks, uint32_t key_base, rc_seg* segs, int64_t seg_cap, int32_t* hits_pp,
-                               int64_t* counters, int grid, cudaStream_t s);
+                               int64_t* counters, int grid, cudaStream_t s, const int64_t* d_nchunks = nullptr);
 cudaError_t launch_units(const int32_t* vis, const int64_t* nvis_p, int64_t nvis, const int32_t* leaf_node,
                          const int32_t* node_first, const int64_t* chunk_off, int32_t* ucnt, int64_t* uoff,
                          int32_t* uend, int64_t* scan_tmp, uint32_t key_base, Unit* units, bool emit,
@@ -41,11 +41,13 @@ cudaError_t launch_pack(const rc_seg* segs, const int64_t* nseg_p, int W, int tw
                         cudaStream_t s);
 cudaError_t launch_leaf_weights(const int32_t* flag, const Rect16* rect, int64_t n, int64_t* w, cudaStream_t s);
 cudaError_t launch_pack_offsets(const int64_t* counts, int nranks, int64_t* dest_off, cudaStream_t s);
-cudaError_t launch_hist(const rc_seg* segs, int64_t n, int32_t* cnt, int grid, cudaStream_t s);
+// d_n (optional): the record count read on the device (CUDA-graph frames), n ignored
+cudaError_t launch_hist(const rc_seg* segs, int64_t n, int32_t* cnt, int grid, cudaStream_t s,
+                        const int64_t* d_n = nullptr);
 cudaError_t launch_scatter(const rc_seg* segs, int64_t n, const int64_t* off, int32_t* cursor, uint32_t* out,
-                           int grid, cudaStream_t s);
+                           int grid, cudaStream_t s, const int64_t* d_n = nullptr);
 cudaError_t launch_scatter_rec(const rc_seg* segs, int64_t n, const int64_t* off, int32_t* cursor, rc_seg* out,
-                               int grid, cudaStream_t s);
+                               int grid, cudaStream_t s, const int64_t* d_n = nullptr);
 cudaError_t launch_fold(const rc_seg* recs, const uint32_t* perm, const int64_t* off, int W, int H, int tw, int th,
                         const int32_t* my_tiles, int tiles_x, int64_t npix_out, const float bg[3], float tau,
                         float* rgba, int32_t* defer, int64_t* counters, int max_grid, cudaStream_t s);

@@ -185,6 +185,8 @@ extern "C" rc_status rc_forest_destroy(rc_forest* f) {
     if (f->evb[k]) cudaEventDestroy(f->evb[k]);
   if (f->h_tiles) cudaFreeHost(f->h_tiles);
   if (f->h_xcnt) cudaFreeHost(f->h_xcnt);
+  if (f->h_trees_pin) cudaFreeHost(f->h_trees_pin);
+  if (f->graph_exec) cudaGraphExecDestroy(f->graph_exec);
   delete[] f->h_trees;
   delete f;
   return RC_OK;
@@ -1066,6 +1068,86 @@ extern "C" rc_status rc_node_table(rc_forest* f, int32_t level, int32_t* d_first
     CU(cudaMemcpyAsync(d_first, f->d_node_first[level], sizeof(int32_t) * f->n_nodes[level],
                        cudaMemcpyDeviceToDevice, s));
   CU(cudaStreamSynchronize(s));
+  return RC_OK;
+}
+
+// ---------------------------------------------------------------------------
+// CUDA-graph frames (C1 / C2 frames are launch bound).  Affine
+// forests, fold level 0, one image: after an ordinary frame has sized every
+// buffer for the camera, the frame is enqueued without host synchronisation
+// -- counts are read on the device (chunk total, record total), the grids
+// cover the forest's capacity -- captured once and replayed.
+// ---------------------------------------------------------------------------
+static rc_status enqueue_affine_frame(rc_forest* f, const float bg[3], float* d_rgba, cudaStream_t s) {
+  const int64_t n = f->n;
+  const int W = f->cc.W, H = f->cc.H;
+  const int64_t npix = (int64_t)W * H;
+  // camera constants (rc_camera_set's upload, from pinned copies)
+  CU(cudaMemcpyAsync(f->d_trees, f->h_trees_pin, sizeof(TreeConst) * f->K, cudaMemcpyHostToDevice, s));
+  // cull + pair generation (rc_cull)
+  DevLeafView L = leaf_view(f);
+  CU(launch_cull(f->cc, f->d_trees, L, n, f->R, true, f->d_flag, f->d_rect_all, s));
+  CU(scan_exclusive<int32_t>(f->d_flag, f->d_scan, n, f->d_scan_tmp, s));
+  CU(launch_compact(f->d_flag, f->d_rect_all, f->d_scan, n, f->d_vis, f->d_vis_rect, s));
+  CU(cudaMemsetAsync(f->d_counters, 0, sizeof(int64_t) * CNT_TOTAL, s));
+  CU(cudaMemsetAsync(f->d_chunk_off, 0, sizeof(int64_t) * (n + 1), s));
+  CU(launch_chunk_count(f->d_vis_rect, f->d_scan + n, n, f->d_chunk_off, f->d_counters, s));
+  CU(scan_exclusive<int64_t>(f->d_chunk_off, f->d_chunk_off, n, f->d_scan_tmp, s));
+  // segments (rc_cast_segments): counts on the device
+  CU(launch_expand(f->d_chunk_off, f->d_scan + n, n, f->d_chunk_elem, s));
+  CU(cudaMemsetAsync(f->d_hits_pp, 0, sizeof(int32_t) * npix, s));
+  CU(launch_cast_affine(f->cc, f->d_trees, L, f->P, f->d_vis, f->d_vis_rect, f->d_chunk_off, f->d_chunk_elem,
+                        f->chunk_cap, (uint32_t)f->first_global, f->d_segs, f->seg_cap, f->d_hits_pp, f->d_counters,
+                        sm_count() * 8, s, f->d_chunk_off + n));
+  // composite of the whole image (rc_composite), record count on the device
+  const int64_t* d_nrec = f->d_counters + CNT_SEGS;
+  const int grid = sm_count() * 8;
+  CU(cudaMemsetAsync(f->d_pix_cnt, 0, sizeof(int32_t) * npix, s));
+  CU(launch_hist(f->d_segs, f->seg_cap, f->d_pix_cnt, grid, s, d_nrec));
+  CU(scan_exclusive<int32_t>(f->d_pix_cnt, f->d_pix_off, npix, f->d_scan_tmp, s));
+  CU(cudaMemsetAsync(f->d_pix_cnt, 0, sizeof(int32_t) * npix, s));
+  CU(launch_scatter_rec(f->d_segs, f->seg_cap, f->d_pix_off, f->d_pix_cnt, f->d_sorted, grid, s, d_nrec));
+  CU(launch_fold(f->d_sorted, nullptr, f->d_pix_off, W, H, W, H, f->d_tiles, 1, npix, bg, 1e-6f, d_rgba, f->d_defer,
+                 f->d_counters, sm_count() * 16, s));
+  return RC_OK;
+}
+
+extern "C" rc_status rc_frame_capture(rc_forest* f, const rc_camera* cam, const float background[3], float* d_rgba,
+                                      int64_t capacity_floats, void* stream) {
+  if (!f || !cam || !d_rgba) return fail(RC_ERR_INVALID_ARG, "rc_frame_capture: null argument");
+  cudaStream_t s = (cudaStream_t)stream;
+  rc_status st = rc_render_frame(f, cam, 0, 0, background, d_rgba, capacity_floats, nullptr, stream);
+  if (st) return st;
+  if (!f->all_affine) return fail(RC_ERR_STATE, "rc_frame_capture: graph frames are for affine forests");
+  if (f->last_composite_copy != 1) return fail(RC_ERR_STATE, "rc_frame_capture: no memory for the record copy");
+  if (!f->h_trees_pin) CU(cudaMallocHost((void**)&f->h_trees_pin, sizeof(TreeConst) * f->K));
+  memcpy(f->h_trees_pin, f->h_trees, sizeof(TreeConst) * f->K);
+  float bg[3] = {0, 0, 0};
+  if (background) memcpy(bg, background, sizeof bg);
+  if (f->graph_exec) {
+    cudaGraphExecDestroy(f->graph_exec);
+    f->graph_exec = nullptr;
+  }
+  CU(cudaStreamSynchronize(s));
+  CU(cudaStreamBeginCapture(s, cudaStreamCaptureModeThreadLocal));
+  st = enqueue_affine_frame(f, bg, d_rgba, s);
+  cudaGraph_t g = nullptr;
+  cudaError_t e = cudaStreamEndCapture(s, &g);
+  if (st) {
+    if (g) cudaGraphDestroy(g);
+    return st;
+  }
+  if (e != cudaSuccess) return fail(RC_ERR_CUDA, "rc_frame_capture: %s", cudaGetErrorString(e));
+  e = cudaGraphInstantiate(&f->graph_exec, g, 0);
+  cudaGraphDestroy(g);
+  if (e != cudaSuccess) return fail(RC_ERR_CUDA, "rc_frame_capture: instantiate: %s", cudaGetErrorString(e));
+  return RC_OK;
+}
+
+extern "C" rc_status rc_frame_replay(rc_forest* f, void* stream) {
+  if (!f) return fail(RC_ERR_INVALID_ARG, "rc_frame_replay: null forest");
+  if (!f->graph_exec) return fail(RC_ERR_STATE, "rc_frame_replay before rc_frame_capture");
+  CU(cudaGraphLaunch(f->graph_exec, (cudaStream_t)stream));
   return RC_OK;
 }
 

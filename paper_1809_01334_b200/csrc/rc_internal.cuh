@@ -130,6 +130,8 @@ struct rc_forest {
   int64_t recv_cap = 0, h_last_recv = 0;
   int64_t* d_xcnt = nullptr;       // [2][RC_MAX_RANKS] send / receive counts of the exchange
   int64_t* h_xcnt = nullptr;       // pinned copy
+  TreeConst* h_trees_pin = nullptr; // graph frames: pinned camera constants of the captured frame
+  cudaGraphExec_t graph_exec = nullptr;
   // scan scratch
   int64_t* d_scan_tmp = nullptr;
   int64_t scan_tmp_cap = 0;

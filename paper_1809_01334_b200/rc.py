@@ -70,7 +70,8 @@ EXPORTS = ["rc_last_error", "rc_version", "rc_forest_create", "rc_forest_destroy
            "rc_cull_result", "rc_leaf_weights", "rc_cast_segments", "rc_segments_get", "rc_segments_set",
            "rc_debug_pair", "rc_aggregate", "rc_comm_unique_id", "rc_comm_create", "rc_comm_destroy",
            "rc_pack_tiles", "rc_composite_tiles", "rc_composite_records", "rc_composite", "rc_render_frame",
-           "rc_launch_count", "rc_last_cast_ms", "rc_last_phase_ms", "rc_node_table", "rc_pool_trim"]
+           "rc_launch_count", "rc_last_cast_ms", "rc_last_phase_ms", "rc_node_table", "rc_pool_trim",
+           "rc_frame_capture", "rc_frame_replay"]
 
 _lib = None
 
@@ -106,6 +107,8 @@ def lib():
     L.rc_composite_records.argtypes = [vp, C.POINTER(Tiling), vp, i64, vp, vp, i64, vp]
     L.rc_composite.argtypes = [vp, vp, vp, i64, vp]
     L.rc_render_frame.argtypes = [vp, C.POINTER(CameraDesc), i32, i32, vp, vp, i64, C.POINTER(i64), vp]
+    L.rc_frame_capture.argtypes = [vp, C.POINTER(CameraDesc), vp, vp, i64, vp]
+    L.rc_frame_replay.argtypes = [vp, vp]
     L.rc_launch_count.argtypes = [i32]
     L.rc_launch_count.restype = i64
     L.rc_last_cast_ms.argtypes = [vp]
@@ -359,6 +362,24 @@ class Forest:
         _check(lib().rc_render_frame(self.h, C.byref(d), int(fold_levels), int(cycles), bg,
                                      C.c_void_p(out.data_ptr()), out.numel(), C.byref(hp), _stream(stream)))
         return out, hp.value
+
+    def frame_capture(self, cam, background=(0.0, 0.0, 0.0), out=None, stream=None):
+        """CUDA-graph frame (affine forests): one ordinary frame, then the captured copy; returns the image
+        tensor the graph writes."""
+        import torch
+        self.cam = cam
+        self.W, self.H = int(cam.width), int(cam.height)
+        if out is None:
+            out = torch.empty((self.H, self.W, 4), dtype=torch.float32, device="cuda")
+        d = camera_desc(cam)
+        bg = (C.c_float * 3)(*background)
+        _check(lib().rc_frame_capture(self.h, C.byref(d), bg, C.c_void_p(out.data_ptr()), out.numel(), _stream(stream)))
+        self._graph_out = out
+        return out
+
+    def frame_replay(self, stream=None):
+        _check(lib().rc_frame_replay(self.h, _stream(stream)))
+        return self._graph_out
 
     def last_cast_ms(self):
         return float(lib().rc_last_cast_ms(self.h))

@@ -197,3 +197,28 @@ def test_debug_pair_matches_cast():
         hpp = f.segments()["hits_per_pixel"].cpu().numpy().reshape(-1)
         empty = int(np.nonzero(hpp == 0)[0][0])
         assert f.debug_pair(int(raw[0, 7]), empty % W, empty // W) == []
+
+
+@pytest.mark.parametrize("which", ["c1", "c2"])
+def test_graph_frame_replay_equals_frame(which):
+    """rc_frame_capture / rc_frame_replay (CUDA-graph frames of affine forests,
+    SURVEY §8(d)): every replay writes the same image as the ordinary frame,
+    bit for bit, and the oracle's within the gate."""
+    import torch
+    from paper_1809_01334_b200 import rc
+    sc = sg.config1() if which == "c1" else sg.config2(width=96, maxlevel=5)
+    f = rc.Forest.from_scene(sc)
+    ref, hits = f.render_frame(sc.camera)
+    ref = ref.cpu().numpy().copy()
+    img = f.frame_capture(sc.camera)
+    torch.cuda.synchronize()
+    for _ in range(3):
+        img.zero_()
+        f.frame_replay()
+        torch.cuda.synchronize()
+        assert np.array_equal(img.cpu().numpy().view(np.uint32), ref.view(np.uint32))
+    assert f.segments()["hit_pairs"] == hits
+    o = oracle.OracleScene(sc)
+    ores = o.render(mode="exact", with_hits=False)
+    clean = ores["namb"] == 0
+    assert np.abs(img.cpu().numpy().reshape(-1, 4)[clean] - ores["rgba"][clean]).max() < 1e-4
