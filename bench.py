@@ -128,6 +128,8 @@ def make_scene(cfg: int, device):
         return sg.config5(device=device)
     if cfg == 45:   # profiling stand-in for C4: level 7 at 1024^2 has C4's pixels per element
         return sg.shell_uniform(7, 1024, 256, name="C4s", device=device)
+    if cfg == 55:   # profiling stand-in for C5: maxlevel 8 at 1024^2 (about C5's records per pixel)
+        return sg.config5(device=device, maxlevel=8, width=1024)
     if cfg == 33:   # test size: C3's geometry at level 4, 128^2, 4 x 4 tiles, 2 coarsening cycles
         import dataclasses
         sc = sg.shell_uniform(4, 128, 16, gl_points=6, name="C3-L4", tiles=(4, 4), device=device)
@@ -141,10 +143,11 @@ WORKLOAD = {1: "C1: identity cube, uniform level 3 (512 hex), ortho 64x64, N=4",
             4: "C4: cubed-sphere shell R=2, uniform level 8 (100,663,296 hex), 2048x2048, N=6",
             5: "C5: cubed-sphere shell R=2, adaptive levels 6..10, 4096x4096, N=8, 3 coarsening cycles",
             45: "C4s (profiling stand-in): shell R=2, uniform level 7 (12,582,912 hex), 1024x1024, N=6",
+            55: "C5s (profiling stand-in): shell R=2, adaptive levels ..8, 1024x1024, N=8, 3 coarsening cycles",
             33: "C3-L4 (test size): shell R=2, uniform level 4, 128x128, N=6, 4x4 tiles, 2 coarsening cycles"}
 
 # oracle pixel sample (every s-th row and column) of the CPU baseline and the reference arm
-CPU_STRIDE = {1: 1, 2: 2, 3: 16, 4: 64, 5: 128, 45: 32, 33: 1}
+CPU_STRIDE = {1: 1, 2: 2, 3: 16, 4: 64, 5: 128, 45: 32, 55: 32, 33: 1}
 
 
 def forest_affine(scene):

@@ -999,19 +999,31 @@ __global__ void __launch_bounds__(FOLD_WARPS * 32, 1) k_coarsen_list(
 }
 
 // Fast path of the aggregation pass: pixels with <= COARSEN_FAST_CAP records
-// (C5: ~240 records per covered pixel after the on-chip fold).
-// Each record is gathered ONCE (32 bytes, through the pixel-bucketed
-// permutation) into the warp's shared memory together with its target-level
-// node; the sort (register bitonic over (sort key, local index)), the run
-// detection and the folds then read shared memory only (round 1 re-gathered
-// every record three times from HBM: latency bound).  Pixels with tied sort
-// keys or more records go to the list pass.
+// (C5: ~240 records per covered pixel after the on-chip fold).  Each record is
+// gathered ONCE (32 bytes, through the pixel-bucketed permutation) into the
+// warp's shared memory (structure of arrays: no bank-aligned record stride)
+// together with its record key and target-level node; a register bitonic sort
+// of (sort key, local index) leaves sorted positions l E .. l E + E - 1 in
+// lane l; the maximal runs of touching records of one node are folded nearest
+// first (Eq. aggregate) by the whole warp: per-lane partial folds and a
+// segmented scan of the open run across the lanes, so long runs (deep
+// coarsening: a ray crossing one big node) do not serialise on one lane.
+// Pixels with tied sort keys or more records go to the list pass.
 constexpr int COARSEN_FAST_CAP = 512;
-constexpr int COARSEN_FAST_WARPS = 2;   // 19.5 KB of shared memory per warp: 5 CTAs (10 warps) per SM
-constexpr size_t COARSEN_FAST_SMEM_WARP = (size_t)COARSEN_FAST_CAP * (sizeof(rc_seg) + sizeof(int32_t) + sizeof(uint16_t));
+constexpr int COARSEN_FAST_WARPS = 2;
+struct CoarsenSmem {                    // per warp, structure of arrays
+  float an[COARSEN_FAST_CAP], af[COARSEN_FAST_CAP], a[COARSEN_FAST_CAP], b0[COARSEN_FAST_CAP],
+      b1[COARSEN_FAST_CAP], b2[COARSEN_FAST_CAP];
+  uint32_t key[COARSEN_FAST_CAP];
+  int32_t node[COARSEN_FAST_CAP];
+};
 
+// returns false when two records share the sort key (the caller defers the pixel)
 template <int E>
-__device__ __forceinline__ bool sort_local(const rc_seg* R, int n, uint16_t* ord) {
+__device__ __forceinline__ bool coarsen_pixel(const CoarsenSmem& C, int n, int64_t pix,
+                                              const int32_t* __restrict__ node_first, uint32_t key_base, float tau,
+                                              rc_seg* __restrict__ out, int64_t out_cap,
+                                              int64_t* __restrict__ counters) {
   const unsigned lane = threadIdx.x & 31;
   uint64_t key[E];
   uint32_t id[E];
@@ -1019,34 +1031,113 @@ __device__ __forceinline__ bool sort_local(const rc_seg* R, int n, uint16_t* ord
   for (int e = 0; e < E; ++e) {
     const int i = (int)lane * E + e;
     id[e] = (uint32_t)i;
-    key[e] = i < n ? sort_key(R[i]) : ~0ull;
+    key[e] = i < n ? (((uint64_t)ord_bits(C.an[i]) << 32) | C.key[i]) : ~0ull;
   }
   warp_sort_blocked<E>(key, id);
-  uint64_t prev_key = __shfl_up_sync(0xffffffffu, key[E - 1], 1);
-  if (lane == 0) prev_key = ~0ull;
-  bool tie = false;
+  // ties: the register order is not total
+  {
+    uint64_t prev_key = __shfl_up_sync(0xffffffffu, key[E - 1], 1);
+    if (lane == 0) prev_key = ~0ull;
+    bool tie = false;
+#pragma unroll
+    for (int e = 0; e < E; ++e) {
+      tie |= (int)lane * E + e < n && key[e] == prev_key;
+      prev_key = key[e];
+    }
+    if (__any_sync(0xffffffffu, tie)) return false;
+  }
+  // head flags of this lane's positions (a run starts at a gap / overlap or a new node)
+  const int lo = (int)lane * E;
+  uint32_t prev = __shfl_up_sync(0xffffffffu, id[E - 1], 1);
+  uint32_t heads = 0;
 #pragma unroll
   for (int e = 0; e < E; ++e) {
-    const int i = (int)lane * E + e;
-    tie |= i < n && key[e] == prev_key;
-    prev_key = key[e];
-    if (i < n) ord[i] = (uint16_t)id[e];
+    const int k = lo + e;
+    if (k < n) {
+      bool h = k == 0;
+      if (!h) {
+        const float an = C.an[id[e]];
+        h = fabsf(an - C.af[prev]) > tau * fmaxf(1.0f, fabsf(an)) || C.node[id[e]] != C.node[prev];
+      }
+      heads |= (h ? 1u : 0u) << e;
+    }
+    prev = id[e];
   }
-  __syncwarp();
-  return !__any_sync(0xffffffffu, tie);
+  // pass 1: the lane's open tail (from its last head, or its start)
+  bool F = false;
+  uint32_t HID = 0;   // local index of the lane's last head record
+  Acc X{1.0, 0.0, 0.0, 0.0};
+#pragma unroll
+  for (int e = 0; e < E; ++e) {
+    if (lo + e >= n) break;
+    if ((heads >> e) & 1u) {
+      F = true;
+      HID = id[e];
+      X = Acc{1.0, 0.0, 0.0, 0.0};
+    }
+    acc_push(X, C.a[id[e]], C.b0[id[e]], C.b1[id[e]], C.b2[id[e]]);
+  }
+  const int hi = min(n, lo + E);
+  int nemit = __popc(heads & ~(lo == 0 ? 1u : 0u)) + ((lo < hi && hi == n) ? 1 : 0);
+  // exclusive segmented scan across lanes: the run entering this lane
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    const bool Fo = __shfl_up_sync(0xffffffffu, F, o);
+    const uint32_t HIDo = __shfl_up_sync(0xffffffffu, HID, o);
+    const double Ao = __shfl_up_sync(0xffffffffu, X.A, o), B0o = __shfl_up_sync(0xffffffffu, X.B0, o);
+    const double B1o = __shfl_up_sync(0xffffffffu, X.B1, o), B2o = __shfl_up_sync(0xffffffffu, X.B2, o);
+    if ((int)lane >= o && !F) {   // (nearer lanes) (+) (this one)
+      Acc y{Ao, B0o, B1o, B2o};
+      acc_push(y, X.A, X.B0, X.B1, X.B2);
+      X = y;
+      F = Fo;
+      HID = HIDo;
+    }
+  }
+  Acc acc{__shfl_up_sync(0xffffffffu, X.A, 1), __shfl_up_sync(0xffffffffu, X.B0, 1),
+          __shfl_up_sync(0xffffffffu, X.B1, 1), __shfl_up_sync(0xffffffffu, X.B2, 1)};
+  uint32_t start_id = __shfl_up_sync(0xffffffffu, HID, 1);   // head of the run entering this lane
+  if (lane == 0) {
+    acc = Acc{1.0, 0.0, 0.0, 0.0};
+    start_id = id[0];
+  }
+  // pass 2: emit every run that ends in this lane's positions
+  int64_t slot = warp_append(&counters[CNT_AGG_OUT], nemit);
+  auto emit = [&](uint32_t i0, uint32_t i1, const Acc& v) {
+    if (slot < out_cap) {
+      const float bb[3] = {(float)v.B0, (float)v.B1, (float)v.B2};
+      store_seg(out + slot, (uint32_t)pix, C.an[i0], C.af[i1], (float)v.A, bb,
+                key_base + (uint32_t)node_first[C.node[i0]]);
+    } else {
+      atomicAdd((unsigned long long*)&counters[CNT_OVERFLOW], 1ull);
+    }
+    ++slot;
+  };
+  uint32_t last_id = __shfl_up_sync(0xffffffffu, id[E - 1], 1);
+#pragma unroll
+  for (int e = 0; e < E; ++e) {
+    const int k = lo + e;
+    if (k >= n) break;
+    if (k > 0 && ((heads >> e) & 1u)) {
+      emit(start_id, last_id, acc);
+      acc = Acc{1.0, 0.0, 0.0, 0.0};
+      start_id = id[e];
+    }
+    acc_push(acc, C.a[id[e]], C.b0[id[e]], C.b1[id[e]], C.b2[id[e]]);
+    last_id = id[e];
+  }
+  if (lo < hi && hi == n) emit(start_id, last_id, acc);
+  return true;
 }
 
-__global__ void __launch_bounds__(COARSEN_FAST_WARPS * 32, 5) k_coarsen_fast(
+__global__ void __launch_bounds__(COARSEN_FAST_WARPS * 32, 8) k_coarsen_fast(
     const rc_seg* __restrict__ recs, const uint32_t* __restrict__ perm, const int64_t* __restrict__ off, int64_t npix,
     const int32_t* __restrict__ node_first, const int32_t* __restrict__ leaf_node, uint32_t key_base, float tau,
     rc_seg* __restrict__ out, int64_t out_cap, int32_t* __restrict__ defer, int64_t* __restrict__ counters) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
   const int warp = threadIdx.x >> 5;
   const unsigned lane = threadIdx.x & 31;
-  unsigned char* wb = smem_raw + (size_t)warp * COARSEN_FAST_SMEM_WARP;
-  rc_seg* R = reinterpret_cast<rc_seg*>(wb);
-  int32_t* anc = reinterpret_cast<int32_t*>(wb + COARSEN_FAST_CAP * sizeof(rc_seg));
-  uint16_t* ord = reinterpret_cast<uint16_t*>(wb + COARSEN_FAST_CAP * (sizeof(rc_seg) + sizeof(int32_t)));
+  CoarsenSmem& C = reinterpret_cast<CoarsenSmem*>(smem_raw)[warp];
   const float4* recs4 = reinterpret_cast<const float4*>(recs);
   for (int64_t pix = (int64_t)blockIdx.x * COARSEN_FAST_WARPS + warp; pix < npix;
        pix += (int64_t)gridDim.x * COARSEN_FAST_WARPS) {
@@ -1059,101 +1150,27 @@ __global__ void __launch_bounds__(COARSEN_FAST_WARPS * 32, 5) k_coarsen_fast(
     }
     const uint32_t* S = perm + base;
     // 1. one gather per record (and its node at the target level)
-#pragma unroll 2
+#pragma unroll 4
     for (int k = lane; k < n; k += 32) {
       const uint32_t id = S[k];
       const float4 lo = recs4[2 * (size_t)id], hi = recs4[2 * (size_t)id + 1];
-      float4* d = reinterpret_cast<float4*>(R + k);
-      d[0] = lo;
-      d[1] = hi;
-      anc[k] = leaf_node[__float_as_uint(hi.w) - key_base];
+      C.an[k] = lo.y;
+      C.af[k] = lo.z;
+      C.a[k] = lo.w;
+      C.b0[k] = hi.x;
+      C.b1[k] = hi.y;
+      C.b2[k] = hi.z;
+      const uint32_t key = __float_as_uint(hi.w);
+      C.key[k] = key;
+      C.node[k] = leaf_node[key - key_base];
     }
     __syncwarp();
-    // 2. order by (alpha_near, key) in registers
-    bool sorted;
-    if (n <= 64) sorted = sort_local<2>(R, n, ord);
-    else if (n <= 128) sorted = sort_local<4>(R, n, ord);
-    else if (n <= 256) sorted = sort_local<8>(R, n, ord);
-    else sorted = sort_local<16>(R, n, ord);
-    if (!sorted) {   // tied sort keys: the list pass orders the pixel under the total order
-      if (lane == 0) defer[atomicAdd((unsigned long long*)&counters[CNT_DEFER], 1ull)] = (int32_t)pix;
-      __syncwarp();
-      continue;
-    }
-    // 3. maximal runs of touching records of one target node, folded nearest
-    // first (Eq. aggregate) by the whole warp: lane l takes the l-th
-    // contiguous range of the sorted records; a segmented warp scan (head
-    // flags) carries the open run across lanes, so long runs (deep
-    // coarsening: one run per ray and node) do not serialise on one lane
-    auto head = [&](int k) -> bool {
-      if (k == 0) return true;
-      const rc_seg& x = R[ord[k - 1]];
-      const rc_seg& y = R[ord[k]];
-      return fabsf(y.alpha_near - x.alpha_far) > tau * fmaxf(1.0f, fabsf(y.alpha_near)) || anc[ord[k]] != anc[ord[k - 1]];
-    };
-    auto emit = [&](int64_t slot, int k0, int k1, const Acc& v) {
-      if (slot < out_cap) {
-        const float bb[3] = {(float)v.B0, (float)v.B1, (float)v.B2};
-        store_seg(out + slot, (uint32_t)pix, R[ord[k0]].alpha_near, R[ord[k1]].alpha_far, (float)v.A, bb,
-                  key_base + (uint32_t)node_first[anc[ord[k0]]]);
-      } else {
-        atomicAdd((unsigned long long*)&counters[CNT_OVERFLOW], 1ull);
-      }
-    };
-    const int per = (n + 31) / 32;
-    const int lo = min(n, (int)lane * per), hi = min(n, lo + per);
-    // pass 1: the lane's open tail (from its last head, or its start) and last head
-    bool F = false;
-    int HS = -1, nemit = 0;
-    Acc X{1.0, 0.0, 0.0, 0.0};
-    for (int k = lo; k < hi; ++k) {
-      if (head(k)) {
-        F = true;
-        HS = k;
-        X = Acc{1.0, 0.0, 0.0, 0.0};
-        nemit += k > 0 ? 1 : 0;   // the run ending at k - 1
-      }
-      const rc_seg& r = R[ord[k]];
-      acc_push(X, r.a, r.b[0], r.b[1], r.b[2]);
-    }
-    nemit += (lo < hi && hi == n) ? 1 : 0;   // the pixel's last run
-    // exclusive segmented scan across lanes: the run entering this lane
-#pragma unroll
-    for (int o = 1; o < 32; o <<= 1) {
-      const bool Fo = __shfl_up_sync(0xffffffffu, F, o);
-      const int HSo = __shfl_up_sync(0xffffffffu, HS, o);
-      const double Ao = __shfl_up_sync(0xffffffffu, X.A, o), B0o = __shfl_up_sync(0xffffffffu, X.B0, o);
-      const double B1o = __shfl_up_sync(0xffffffffu, X.B1, o), B2o = __shfl_up_sync(0xffffffffu, X.B2, o);
-      if ((int)lane >= o && !F) {   // (nearer lanes) (+) (this one)
-        Acc y{Ao, B0o, B1o, B2o};
-        acc_push(y, X.A, X.B0, X.B1, X.B2);
-        X = y;
-        F = Fo;
-        HS = HSo;
-      }
-    }
-    Acc C{__shfl_up_sync(0xffffffffu, X.A, 1), __shfl_up_sync(0xffffffffu, X.B0, 1),
-          __shfl_up_sync(0xffffffffu, X.B1, 1), __shfl_up_sync(0xffffffffu, X.B2, 1)};
-    int start = __shfl_up_sync(0xffffffffu, HS, 1);
-    if (lane == 0) {
-      C = Acc{1.0, 0.0, 0.0, 0.0};
-      start = 0;
-    }
-    // pass 2: emit every run that ends in this lane's range
-    int64_t slot = warp_append(&counters[CNT_AGG_OUT], nemit);
-    Acc acc = C;
-    for (int k = lo; k < hi; ++k) {
-      if (k > 0 && head(k)) {
-        emit(slot++, start, k - 1, acc);
-        acc = Acc{1.0, 0.0, 0.0, 0.0};
-        start = k;
-      } else if (k == 0) {
-        start = 0;
-      }
-      const rc_seg& r = R[ord[k]];
-      acc_push(acc, r.a, r.b[0], r.b[1], r.b[2]);
-    }
-    if (lo < hi && hi == n) emit(slot++, start, n - 1, acc);
+    bool ok;
+    if (n <= 64) ok = coarsen_pixel<2>(C, n, pix, node_first, key_base, tau, out, out_cap, counters);
+    else if (n <= 128) ok = coarsen_pixel<4>(C, n, pix, node_first, key_base, tau, out, out_cap, counters);
+    else if (n <= 256) ok = coarsen_pixel<8>(C, n, pix, node_first, key_base, tau, out, out_cap, counters);
+    else ok = coarsen_pixel<16>(C, n, pix, node_first, key_base, tau, out, out_cap, counters);
+    if (!ok && lane == 0) defer[atomicAdd((unsigned long long*)&counters[CNT_DEFER], 1ull)] = (int32_t)pix;
     __syncwarp();
   }
 }
@@ -1290,7 +1307,7 @@ cudaError_t launch_coarsen(const rc_seg* recs, const uint32_t* perm, const int64
                            const int32_t* node_first, const int32_t* leaf_node, uint32_t key_base, float tau, rc_seg* out,
                            int64_t out_cap, int32_t* defer, int64_t* counters, int max_grid, cudaStream_t s) {
   static bool attr = false;
-  const size_t smemf = COARSEN_FAST_SMEM_WARP * COARSEN_FAST_WARPS;
+  const size_t smemf = sizeof(CoarsenSmem) * COARSEN_FAST_WARPS;
   const size_t smeml = (size_t)FOLD_WARPS * FOLD_CAP * (sizeof(uint64_t) + sizeof(uint16_t));
   if (!attr) {
     cudaError_t e = cudaFuncSetAttribute(k_coarsen_fast, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smemf);

@@ -187,6 +187,7 @@ extern "C" rc_status rc_forest_destroy(rc_forest* f) {
   if (f->h_xcnt) cudaFreeHost(f->h_xcnt);
   if (f->h_trees_pin) cudaFreeHost(f->h_trees_pin);
   if (f->graph_exec) cudaGraphExecDestroy(f->graph_exec);
+  if (f->cap_stream) cudaStreamDestroy(f->cap_stream);
   delete[] f->h_trees;
   delete f;
   return RC_OK;
@@ -1129,10 +1130,14 @@ extern "C" rc_status rc_frame_capture(rc_forest* f, const rc_camera* cam, const 
     f->graph_exec = nullptr;
   }
   CU(cudaStreamSynchronize(s));
-  CU(cudaStreamBeginCapture(s, cudaStreamCaptureModeThreadLocal));
-  st = enqueue_affine_frame(f, bg, d_rgba, s);
+  // capture on a library stream (the caller's may be the legacy default stream, which cannot
+  // capture); the graph is launched on the caller's stream
+  if (!f->cap_stream) CU(cudaStreamCreateWithFlags(&f->cap_stream, cudaStreamNonBlocking));
+  cudaStream_t cs = f->cap_stream;
+  CU(cudaStreamBeginCapture(cs, cudaStreamCaptureModeThreadLocal));
+  st = enqueue_affine_frame(f, bg, d_rgba, cs);
   cudaGraph_t g = nullptr;
-  cudaError_t e = cudaStreamEndCapture(s, &g);
+  cudaError_t e = cudaStreamEndCapture(cs, &g);
   if (st) {
     if (g) cudaGraphDestroy(g);
     return st;

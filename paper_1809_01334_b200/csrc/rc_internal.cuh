@@ -132,6 +132,7 @@ struct rc_forest {
   int64_t* h_xcnt = nullptr;       // pinned copy
   TreeConst* h_trees_pin = nullptr; // graph frames: pinned camera constants of the captured frame
   cudaGraphExec_t graph_exec = nullptr;
+  cudaStream_t cap_stream = nullptr;
   // scan scratch
   int64_t* d_scan_tmp = nullptr;
   int64_t scan_tmp_cap = 0;

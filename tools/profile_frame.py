@@ -20,6 +20,11 @@ if __name__ == "__main__":
     torch.cuda.empty_cache()
     for _ in range(a.frames):
         img, hits = f.render_frame(sc.camera, fold_levels=(0 if a.config <= 2 else 2), cycles=sc.coarsen_cycles)
+    if a.config == 55:   # the aggregation pass alone, for ncu -k k_coarsen (records of the last cast)
+        f.camera_set(sc.camera)
+        f.cull()
+        f.cast_segments(2)
+        f.aggregate(sc.coarsen_cycles)
     torch.cuda.synchronize()
     s = f.segments()
     print("hit_pairs", hits, "candidates", s["candidates"], "records", s["count"], "raw", s["raw_segments"],
