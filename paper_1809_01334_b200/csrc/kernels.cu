@@ -740,15 +740,13 @@ __device__ __forceinline__ void warp_sort_blocked(uint64_t (&key)[E], uint32_t (
       const int lj = j / E;
       const bool lower = (lane & lj) == 0;
 #pragma unroll
-      for (int e = 0; e < E; ++e) {
+      for (int e = 0; e < E; ++e) {   // branch-free: selects, no divergent swaps
         const uint64_t ok = __shfl_xor_sync(0xffffffffu, key[e], lj);
         const uint32_t oi = __shfl_xor_sync(0xffffffffu, id[e], lj);
         const bool up = ((((int)lane * E + e) & k) == 0);
         const bool take = (lower == up) ? (ok < key[e]) : (ok > key[e]);
-        if (take) {
-          key[e] = ok;
-          id[e] = oi;
-        }
+        key[e] = take ? ok : key[e];
+        id[e] = take ? oi : id[e];
       }
     }
 #pragma unroll
@@ -759,10 +757,13 @@ __device__ __forceinline__ void warp_sort_blocked(uint64_t (&key)[E], uint32_t (
           const int p = e ^ j;
           if (p > e) {
             const bool up = ((((int)lane * E + e) & k) == 0);
-            if ((key[e] > key[p]) == up) {
-              const uint64_t tk = key[e]; key[e] = key[p]; key[p] = tk;
-              const uint32_t ti = id[e]; id[e] = id[p]; id[p] = ti;
-            }
+            const bool sw = (key[e] > key[p]) == up;
+            const uint64_t ke = key[e], kp = key[p];
+            const uint32_t ie = id[e], ip = id[p];
+            key[e] = sw ? kp : ke;
+            key[p] = sw ? ke : kp;
+            id[e] = sw ? ip : ie;
+            id[p] = sw ? ie : ip;
           }
         }
       }
