@@ -33,7 +33,8 @@ def build(force: bool = False) -> str:
 class Scene_(C.Structure):
     _fields_ = [("R", C.c_int32), ("P", C.c_int32), ("K", C.c_int32), ("tree_ctrl", C.c_void_p),
                 ("n", C.c_int64), ("anchor", C.c_void_p), ("tree", C.c_void_p), ("level", C.c_void_p),
-                ("field", C.c_void_p), ("kappa0", C.c_double), ("inv_F", C.c_double), ("q0", C.c_double)]
+                ("field", C.c_void_p), ("kappa0", C.c_double), ("inv_F", C.c_double), ("q0", C.c_double),
+                ("dim", C.c_int32), ("surf_a", C.c_double * 2), ("surf_i", C.c_double * 9), ("surf_k", C.c_double)]
 
 
 class Camera_(C.Structure):
@@ -102,6 +103,7 @@ def lib():
         _lib.orc_medium_evals.argtypes = [C.c_int]
         _lib.orc_medium_evals.restype = C.c_longlong
         _lib.orc_set_force_general.argtypes = [C.c_int]
+        _lib.orc_surface_roots.argtypes = [C.c_void_p, C.c_void_p, C.c_void_p, d, d, C.c_void_p]
         _lib.orc_fold_pixel.argtypes = [C.c_int, C.c_void_p, d, C.c_void_p, C.c_void_p, C.c_void_p]
     return _lib
 
@@ -126,7 +128,13 @@ class OracleScene:
         self.field = npy(scene.leaf_field, np.float32)
         self.s = Scene_(scene.geom_degree, scene.field_degree, self.ctrl.shape[0], _ptr(self.ctrl).value,
                         self.anchor.shape[0], _ptr(self.anchor).value, _ptr(self.tree).value,
-                        _ptr(self.level).value, _ptr(self.field).value, scene.kappa0, scene.inv_F, scene.q0)
+                        _ptr(self.level).value, _ptr(self.field).value, scene.kappa0, scene.inv_F, scene.q0,
+                        int(getattr(scene, "dim", 3)))
+        if self.s.dim == 2:
+            a0, a1, ii, k = scene.surface
+            self.s.surf_a[:] = [float(a0), float(a1)]
+            self.s.surf_i[:] = [float(x) for row in ii for x in row]
+            self.s.surf_k = float(k)
         cam = scene.camera
         self.c = Camera_(cam.projection, (C.c_double * 3)(*cam.origin), (C.c_double * 3)(*cam.view),
                          (C.c_double * 3)(*cam.right), (C.c_double * 3)(*cam.up), cam.pixel_size, cam.far_dist,
@@ -366,3 +374,14 @@ def fold_pixel(segs, tau=1e-12, background=(0.0, 0.0, 0.0)):
     bg = np.ascontiguousarray(background, dtype=np.float64)
     lib().orc_fold_pixel(s.shape[0], _ptr(s), tau, _ptr(bg), _ptr(rgba), _ptr(ab))
     return rgba, ab
+
+
+def surface_roots(P, o, r, lo=0.0, hi=1.0):
+    """Parameters s = (s1, s2) in [lo, hi)^2 where the ray o + alpha r meets the
+    bilinear patch with corners P [2][2][3] ([m2][m1][xyz]) (App. A.1)."""
+    P = np.ascontiguousarray(P, dtype=np.float64)
+    o = np.ascontiguousarray(o, dtype=np.float64)
+    r = np.ascontiguousarray(r, dtype=np.float64)
+    out = np.zeros(4)
+    n = lib().orc_surface_roots(_ptr(P), _ptr(o), _ptr(r), lo, hi, _ptr(out))
+    return out[:2 * n].reshape(n, 2)

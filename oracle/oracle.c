@@ -488,7 +488,20 @@ static void element_bezier(const orc_scene* sc, int64_t e, const double lo[3], c
 }
 
 /* Camera-space AABB of the element's Bezier points. */
+static void surface_corners(const orc_scene* sc, int64_t e, double P[2][2][3]);
+static int is_surface(const orc_scene* sc);
 int orc_element_aabb(const orc_scene* sc, const orc_camera* cam, int64_t e, double lo[3], double hi[3]) {
+  if (is_surface(sc)) {   /* a bilinear patch lies in the convex hull of its four corners */
+    double P[2][2][3];
+    surface_corners(sc, e, P);
+    for (int c = 0; c < 3; ++c) { lo[c] = INFINITY; hi[c] = -INFINITY; }
+    for (int q = 0; q < 4; ++q) {
+      double X[3];
+      orc_camera_transform(cam, P[q / 2][q % 2], X);
+      for (int c = 0; c < 3; ++c) { lo[c] = fmin(lo[c], X[c]); hi[c] = fmax(hi[c], X[c]); }
+    }
+    return 0;
+  }
   double B[27][3], plo[3] = {0, 0, 0}, phi[3] = {1, 1, 1};
   element_bezier(sc, e, plo, phi, B);
   int np = (sc->R + 1) * (sc->R + 1) * (sc->R + 1);
@@ -1001,6 +1014,173 @@ int orc_intersect_domain(const orc_scene* sc, const orc_camera* cam, int64_t e, 
  * ambiguity classification of SURVEY R7: hit(E+) != hit(E-) where E+/- is
  * the element with its boundary pushed out/in by EPS_AMBIG, or a chord
  * < EPS_AMBIG, or a tangent root. */
+/* ======================================================================
+ * Surface forests (§2.8 "Visualization of surfaces", App.
+ * A.1 PAPER.md:1473-1514).  An element is the bilinear
+ * patch X_E(s) = J_k(a 2^-18 + 2^-l s), s in [0,1)^2, of its tree's bilinear
+ * map (tree_ctrl [k][m2][m1][xyz]).  A ray meets it in points: projected on
+ * d1, d2 perpendicular to r (Eq. intersectiontwod) the patch is the 2D
+ * bilinear map g(s) = a + b s1 + c s2 + d s1 s2, and g(s) = 0 is a quadratic
+ * in s2 after eliminating s1 (App. A.1).  Each point is a zero-length segment
+ * with Eq. ABphi: A_phi = A_s^(1/cos phi), B_phi = I_s (1 - A_phi)
+ * (Eq. BIrelation), phi the angle between the ray and the patch normal.
+ * ==================================================================== */
+static int is_surface(const orc_scene* sc) { return sc->dim == 2; }
+
+/* corner points P[m2][m1] of the element's patch */
+static void surface_corners(const orc_scene* sc, int64_t e, double P[2][2][3]) {
+  const double* z = sc->tree_ctrl + (size_t)sc->tree[e] * 12;   /* [m2][m1][xyz] */
+  const double h = elem_h(sc, e);
+  for (int q2 = 0; q2 < 2; ++q2)
+    for (int q1 = 0; q1 < 2; ++q1) {
+      const double t1 = ldexp((double)sc->anchor[3 * e], -MAXL) + h * q1;
+      const double t2 = ldexp((double)sc->anchor[3 * e + 1], -MAXL) + h * q2;
+      for (int c = 0; c < 3; ++c)
+        P[q2][q1][c] = (1 - t2) * ((1 - t1) * z[0 * 3 + c] + t1 * z[1 * 3 + c]) +
+                       t2 * ((1 - t1) * z[2 * 3 + c] + t1 * z[3 * 3 + c]);
+    }
+}
+
+static void surface_point(const double P[2][2][3], double s1, double s2, double X[3], double n[3]) {
+  double d1[3], d2[3];
+  for (int c = 0; c < 3; ++c) {
+    X[c] = (1 - s2) * ((1 - s1) * P[0][0][c] + s1 * P[0][1][c]) + s2 * ((1 - s1) * P[1][0][c] + s1 * P[1][1][c]);
+    d1[c] = (1 - s2) * (P[0][1][c] - P[0][0][c]) + s2 * (P[1][1][c] - P[1][0][c]);
+    d2[c] = (1 - s1) * (P[1][0][c] - P[0][0][c]) + s1 * (P[1][1][c] - P[0][1][c]);
+  }
+  n[0] = d1[1] * d2[2] - d1[2] * d2[1];
+  n[1] = d1[2] * d2[0] - d1[0] * d2[2];
+  n[2] = d1[0] * d2[1] - d1[1] * d2[0];
+}
+
+/* All s in [lo, hi)^2 with X(s) on the ray line; returns the count (<= 2). */
+static int surface_roots(const double P[2][2][3], const double o[3], const double r[3], double lo, double hi,
+                         double s_out[2][2]) {
+  double ax[3] = {0, 0, 0};   /* the coordinate axis least aligned with r */
+  {
+    const double a0 = fabs(r[0]), a1 = fabs(r[1]), a2 = fabs(r[2]);
+    ax[(a0 <= a1 && a0 <= a2) ? 0 : (a1 <= a2 ? 1 : 2)] = 1.0;
+  }
+  double d1[3] = {r[1] * ax[2] - r[2] * ax[1], r[2] * ax[0] - r[0] * ax[2], r[0] * ax[1] - r[1] * ax[0]};
+  double n1 = sqrt(dot3(d1, d1));
+  for (int c = 0; c < 3; ++c) d1[c] /= n1;
+  double d2[3] = {r[1] * d1[2] - r[2] * d1[1], r[2] * d1[0] - r[0] * d1[2], r[0] * d1[1] - r[1] * d1[0]};
+  double n2 = sqrt(dot3(d2, d2));
+  for (int c = 0; c < 3; ++c) d2[c] /= n2;
+  double g[2][2][2];   /* projected corners [m2][m1][k] relative to the ray */
+  for (int q2 = 0; q2 < 2; ++q2)
+    for (int q1 = 0; q1 < 2; ++q1) {
+      double rel[3] = {P[q2][q1][0] - o[0], P[q2][q1][1] - o[1], P[q2][q1][2] - o[2]};
+      g[q2][q1][0] = dot3(d1, rel);
+      g[q2][q1][1] = dot3(d2, rel);
+    }
+  double a[2], b[2], c[2], d[2];
+  for (int k = 0; k < 2; ++k) {
+    a[k] = g[0][0][k];
+    b[k] = g[0][1][k] - g[0][0][k];
+    c[k] = g[1][0][k] - g[0][0][k];
+    d[k] = g[1][1][k] - g[1][0][k] - g[0][1][k] + g[0][0][k];
+  }
+  /* (a + c s2) x (b + d s2) = 0: q2 s2^2 + q1 s2 + q0 = 0 */
+  const double q0 = a[0] * b[1] - a[1] * b[0];
+  const double q1 = a[0] * d[1] - a[1] * d[0] + c[0] * b[1] - c[1] * b[0];
+  const double qq = c[0] * d[1] - c[1] * d[0];
+  double roots[2];
+  int nr = 0;
+  const double scale = fabs(q0) + fabs(q1) + fabs(qq);
+  if (fabs(qq) <= 1e-14 * scale) {
+    if (fabs(q1) > 0) roots[nr++] = -q0 / q1;
+  } else {
+    const double disc = q1 * q1 - 4 * qq * q0;
+    if (disc >= 0) {
+      const double sq = sqrt(disc);
+      const double t = -0.5 * (q1 + (q1 >= 0 ? sq : -sq));   /* stable quadratic formula */
+      roots[nr++] = t / qq;
+      if (t != 0) roots[nr++] = q0 / t;
+    }
+  }
+  int ns = 0;
+  for (int k = 0; k < nr; ++k) {
+    const double s2 = roots[k];
+    if (!(s2 >= lo && s2 < hi)) continue;
+    const double u[2] = {b[0] + d[0] * s2, b[1] + d[1] * s2};
+    const double w[2] = {a[0] + c[0] * s2, a[1] + c[1] * s2};
+    const double uu = u[0] * u[0] + u[1] * u[1];
+    if (!(uu > 0)) continue;
+    const double s1 = -(w[0] * u[0] + w[1] * u[1]) / uu;
+    if (!(s1 >= lo && s1 < hi)) continue;
+    s_out[ns][0] = s1;
+    s_out[ns][1] = s2;
+    ++ns;
+  }
+  return ns;
+}
+
+/* exported for the pins: P [2][2][3] ([m2][m1][xyz]), s_out [2][2] */
+int orc_surface_roots(const double* P, const double o[3], const double r[3], double lo, double hi, double* s_out) {
+  double Q[2][2][3], S[2][2];
+  memcpy(Q, P, sizeof Q);
+  const int ns = surface_roots(Q, o, r, lo, hi, S);
+  memcpy(s_out, S, sizeof(double) * 2 * ns);
+  return ns;
+}
+
+/* Surface hits of pixel (i,j)'s ray on element e: alpha and (a, b[3]) per point
+ * (Eq. ABphi), at most 2; ambiguity as SURVEY R7 (s within eps / edge length of
+ * the boundary, or |cos phi| < 1e-6). */
+static int surface_hits(const orc_scene* sc, const orc_camera* cam, int64_t e, int i, int j, double* alpha,
+                        double (*ab)[4], int* flags) {
+  double o[3], r[3], amin, amax, P[2][2][3];
+  orc_ray(cam, i, j, o, r);
+  alpha_range(cam, &amin, &amax);
+  surface_corners(sc, e, P);
+  double emin = INFINITY;
+  for (int q = 0; q < 2; ++q) {
+    double e1[3], e2[3];
+    for (int c = 0; c < 3; ++c) {
+      e1[c] = P[q][1][c] - P[q][0][c];
+      e2[c] = P[1][q][c] - P[0][q][c];
+    }
+    emin = fmin(emin, fmin(sqrt(dot3(e1, e1)), sqrt(dot3(e2, e2))));
+  }
+  const double delta = EPS_AMBIG / emin;
+  double s[2][2], sp[2][2], sm[2][2];
+  const int ns = surface_roots(P, o, r, 0.0, 1.0, s);
+  const int np = surface_roots(P, o, r, -delta, 1.0 + delta, sp);
+  const int nm = surface_roots(P, o, r, delta, 1.0 - delta, sm);
+  (void)sp;
+  (void)sm;
+  *flags = 0;
+  if (np != nm) *flags |= ORC_AMBIGUOUS;
+  const double rr = dot3(r, r), rn = sqrt(rr);
+  int nh = 0;
+  for (int k = 0; k < ns; ++k) {
+    double X[3], n[3];
+    surface_point(P, s[k][0], s[k][1], X, n);
+    const double al = ((X[0] - o[0]) * r[0] + (X[1] - o[1]) * r[1] + (X[2] - o[2]) * r[2]) / rr;
+    if (!(al >= amin && al <= amax)) continue;
+    const double cphi = fabs(dot3(n, r)) / (sqrt(dot3(n, n)) * rn);
+    if (cphi < 1e-6) *flags |= ORC_AMBIGUOUS;
+    /* the nodal value (bilinear in s, corners [k2][k1]) and the surface transfer */
+    const float* f = sc->field + 4 * e;
+    const double v = (1 - s[k][1]) * ((1 - s[k][0]) * f[0] + s[k][0] * f[1]) +
+                     s[k][1] * ((1 - s[k][0]) * f[2] + s[k][0] * f[3]);
+    double As = sc->surf_a[0] + sc->surf_a[1] * v;
+    As = fmin(1.0, fmax(0.0, As));
+    const double w = exp(-0.5 * ((1 - v) * sc->surf_k) * ((1 - v) * sc->surf_k));
+    const double Aphi = (As == 0.0) ? 0.0 : pow(As, 1.0 / cphi);   /* Eq. ABphi (A_s = 0: opaque) */
+    alpha[nh] = al;
+    ab[nh][0] = Aphi;
+    for (int c = 0; c < 3; ++c) {
+      const double Is = sc->surf_i[c][0] + sc->surf_i[c][1] * v + sc->surf_i[c][2] * w;
+      ab[nh][1 + c] = Is * (1.0 - Aphi);   /* Eq. BIrelation */
+    }
+    ++nh;
+  }
+  if (nh > 0) *flags |= ORC_HIT;
+  return nh;
+}
+
 int orc_intersect(const orc_scene* sc, const orc_camera* cam, int64_t e, int i, int j, int max_seg,
                   double* seg, int* flags) {
   double o[3], r[3], amin, amax;
@@ -1283,7 +1463,9 @@ static int64_t render_core(const orc_scene* sc, const orc_camera* cam, int mode,
       int64_t e = cand[t];
       double seg[16];
       int flags = 0;
-      int ns = orc_intersect(sc, cam, e, i, j, 8, seg, &flags);
+      double sal[2], sab[2][4];
+      int ns = is_surface(sc) ? surface_hits(sc, cam, e, i, j, sal, sab, &flags)
+                              : orc_intersect(sc, cam, e, i, j, 8, seg, &flags);
       if (flags & ORC_AMBIGUOUS) na++;
       if (ns > 0) nh++;
       if (pairs && (ns > 0 || (flags & ORC_AMBIGUOUS))) {
@@ -1306,6 +1488,14 @@ static int64_t render_core(const orc_scene* sc, const orc_camera* cam, int mode,
         orc_hit hh;
         memset(&hh, 0, sizeof hh);
         hh.elem = e; hh.pixel = pix; hh.flags = flags;
+        if (is_surface(sc)) {   /* a zero-length segment (Eq. ABphi) */
+          hh.alpha_near = hh.alpha_far = sal[s];
+          hh.a = sab[s][0];
+          for (int c = 0; c < 3; ++c) hh.b[c] = sab[s][1 + c];
+          list[nl++] = hh;
+          fold[nf++] = hh;
+          continue;
+        }
         hh.alpha_near = seg[2 * s]; hh.alpha_far = seg[2 * s + 1];
         medium_ctx mc;
         mc.sc = sc; mc.e = e; memcpy(mc.o, o, sizeof o); memcpy(mc.r, r, sizeof r);

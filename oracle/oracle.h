@@ -27,8 +27,15 @@ typedef struct {
   const int32_t* anchor;   /* [n][3], units 2^-18 */
   const int32_t* tree;     /* [n] */
   const int8_t* level;     /* [n] */
-  const float* field;      /* [n][(P+1)^3], node order [k3][k2][k1] */
+  const float* field;      /* [n][(P+1)^3], node order [k3][k2][k1]; surfaces: [n][4] corners [k2][k1] */
   double kappa0, inv_F, q0;
+  /* surface forests (§2.8): dim = 2 means
+   * quadtree leaves (anchor[3*e+2] = 0) on bilinear tree patches tree_ctrl
+   * [K][2][2][3] ([k][m2][m1][xyz]); the corner values v of an element give
+   * A_s = clamp(surf_a[0] + surf_a[1] v, 0, 1) and the per-channel intensity
+   * I_s = surf_i[c][0] + surf_i[c][1] v + surf_i[c][2] w(v), w = exp(-((1-v) surf_k)^2 / 2). */
+  int32_t dim;             /* 3 (or 0): volume forest; 2: surface forest */
+  double surf_a[2], surf_i[3][3], surf_k;
 } orc_scene;
 
 typedef struct {
@@ -122,6 +129,11 @@ void orc_pairs_free(orc_pairs* p);
  * tolerance tau, fold back to front. */
 void orc_fold_pixel(int n, orc_hit* segs, double tau, const double background[3], double rgba[4],
                     double ab[4]);
+
+/* Surface forests (App. A.1): all s in [lo, hi)^2 with
+ * X(s) = o + alpha r on the bilinear patch with corners P [2][2][3]
+ * ([m2][m1][xyz]); writes s_out [count][2] and returns the count (<= 2). */
+int orc_surface_roots(const double* P, const double o[3], const double r[3], double lo, double hi, double* s_out);
 
 #ifdef __cplusplus
 }

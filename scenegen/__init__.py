@@ -68,6 +68,13 @@ class Scene:
     tiles: tuple = (1, 1)
     coarsen_cycles: int = 0
     notes: str = ""
+    # surface forests (§2.8; NEXT(3)): dim = 2 means quadtree
+    # leaves (anchor z = 0) on bilinear tree patches tree_ctrl [K][2][2][3]
+    # ([k][m2][m1][xyz]) with 4 corner values per leaf ([k2][k1]); `surface` is
+    # the transfer (a0, a1, ((i0, i1, i2) per RGB channel), k): A_s = clamp(a0 +
+    # a1 v, 0, 1), I_s = i0 + i1 v + i2 exp(-((1 - v) k)^2 / 2)
+    dim: int = 3
+    surface: tuple = (0.0, 0.0, ((0.0, 0.0, 0.0),) * 3, 0.0)
 
     @property
     def num_leaves(self) -> int:
@@ -469,6 +476,116 @@ def constant_field(scene: Scene, value: float = 0.7) -> Scene:
     F is kept at 1 so kappa = kappa0 * value^2."""
     fld = np.full_like(_np(scene.leaf_field), np.float32(value))
     return dataclasses.replace(scene, name=scene.name + "-const", leaf_field=fld, inv_F=1.0)
+
+
+# ---------------------------------------------------------------------------
+# Surface workload (NEXT(3)): the Mandelbrot hexagon of PAPER.md:1296-1367
+# ---------------------------------------------------------------------------
+HEX_TOP = ((-2.3, 0.75), (-0.25, 1.8), (1.3, 1.0))   # PAPER.md:1316-1320; bottom: y negated
+
+
+def _spread2(v: np.ndarray) -> np.ndarray:
+    v = v.astype(np.uint64) & np.uint64(0x3FFFF)
+    out = np.zeros_like(v)
+    for b in range(18):
+        out |= ((v >> np.uint64(b)) & np.uint64(1)) << np.uint64(2 * b)
+    return out
+
+
+def hexagon_ctrl(bend: float = 0.0) -> np.ndarray:
+    """Two bilinear quadtree patches [2][2][2][3] ([k][m2][m1][xyz]) forming the
+    hexagon (tree 0: x <= -1/4, tree 1: x >= -1/4; t1 along x, t2 along y).
+    bend != 0 lifts the corners to +-bend/2 (saddle patches, continuous across
+    the shared edge) so that the ray-patch equation is a true quadratic."""
+    (t1x, t1y), (t2x, t2y), (t3x, t3y) = HEX_TOP
+    T1, T2, T3 = (t1x, t1y), (t2x, t2y), (t3x, t3y)
+    B1, B2, B3 = (t1x, -t1y), (t2x, -t2y), (t3x, -t3y)
+    z = np.zeros((2, 2, 2, 3))
+    h = 0.5 * bend
+    for k, (c00, c01, c10, c11, zs) in enumerate(((B1, B2, T1, T2, (h, -h, -h, h)),
+                                                   (B2, B3, T2, T3, (-h, h, h, -h)))):
+        for q, c in enumerate((c00, c01, c10, c11)):
+            z[k, q // 2, q % 2] = (c[0], c[1], zs[q])
+    return z
+
+
+def mandelbrot_value(x, y, max_iter: int):
+    """Escape count of z <- z^2 + c, z0 = 0, c = x + i y (Eq. mbiter) divided by
+    max_iter: the first m >= 1 with |z_m| > 2, else max_iter."""
+    c = np.asarray(x, dtype=np.float64) + 1j * np.asarray(y, dtype=np.float64)
+    z = np.zeros_like(c)
+    n = np.full(c.shape, max_iter, dtype=np.int64)
+    alive = np.ones(c.shape, dtype=bool)
+    for m in range(1, max_iter + 1):
+        z = np.where(alive, z * z + c, z)
+        esc = alive & (np.abs(z) > 2.0)
+        n[esc] = m
+        alive &= ~esc
+    return n / float(max_iter)
+
+
+def _hex_corner_xy(ctrl, tree, anchor, level):
+    """xy of the 4 corners [k2][k1] of quadtree leaves (bilinear tree map)."""
+    h = np.ldexp(1.0, -level.astype(np.int64))
+    out = np.zeros((tree.shape[0], 4, 3))
+    for q in range(4):
+        t1 = anchor[:, 0] / float(1 << MAXLEVEL) + h * (q % 2)
+        t2 = anchor[:, 1] / float(1 << MAXLEVEL) + h * (q // 2)
+        Z = ctrl[tree]
+        out[:, q] = ((1 - t2)[:, None] * ((1 - t1)[:, None] * Z[:, 0, 0] + t1[:, None] * Z[:, 0, 1]) +
+                     t2[:, None] * ((1 - t1)[:, None] * Z[:, 1, 0] + t1[:, None] * Z[:, 1, 1]))
+    return out
+
+
+SURF_OPAQUE = (0.0, 0.0, ((0.5, 0.5, 0.0),) * 3, 0.0)                      # grey to white, A_s = 0
+SURF_TRANSPARENT = (0.8, -0.5, ((0.1, 0.2, 0.8), (0.1, 0.2, 0.8), (0.2, 0.3, 0.0)), 20.0)   # yellow near the limit
+
+
+def mandelbrot_hexagon(level0=3, maxlevel=7, max_iter=30, width=256, bend=0.0, opaque=False, camera=None,
+                       name="MB") -> Scene:
+    """The Mandelbrot surface: two quadtrees mapped to the
+    hexagon, uniform at level0, refined where an element's four corner values
+    differ (up to maxlevel; D18: no 2:1 balance, corner values taken
+    at every leaf corner), bilinear corner values = escape count / max_iter."""
+    ctrl = hexagon_ctrl(bend)
+    n1 = 4 ** level0
+    idx = np.arange(n1, dtype=np.uint64)
+    # Morton (x fastest) in 2D: bits alternate x, y
+    xs = np.zeros(n1, dtype=np.uint64)
+    ys = np.zeros(n1, dtype=np.uint64)
+    for b in range(level0):
+        xs |= ((idx >> np.uint64(2 * b)) & np.uint64(1)) << np.uint64(b)
+        ys |= ((idx >> np.uint64(2 * b + 1)) & np.uint64(1)) << np.uint64(b)
+    sh = np.uint64(MAXLEVEL - level0)
+    anc = np.tile(np.stack([xs << sh, ys << sh, np.zeros_like(xs)], axis=1).astype(np.int32), (2, 1))
+    tree = np.repeat(np.arange(2, dtype=np.int32), n1)
+    lev = np.full(2 * n1, level0, dtype=np.int8)
+    done = []
+    for L in range(level0, maxlevel + 1):
+        if anc.shape[0] == 0:
+            break
+        xy = _hex_corner_xy(ctrl, tree, anc, lev)
+        v = mandelbrot_value(xy[..., 0], xy[..., 1], max_iter)
+        sel = np.zeros(anc.shape[0], dtype=bool) if L == maxlevel else (v.max(axis=1) != v.min(axis=1))
+        done.append((anc[~sel], tree[~sel], lev[~sel], v[~sel]))
+        pa, pt = anc[sel], tree[sel]
+        hh = np.int32(1 << (MAXLEVEL - L - 1))
+        kids = [pa + np.array([(c & 1) * hh, ((c >> 1) & 1) * hh, 0], dtype=np.int32) for c in range(4)]
+        anc = np.concatenate(kids, axis=0)
+        tree = np.tile(pt, 4)
+        lev = np.full(anc.shape[0], L + 1, dtype=np.int8)
+    A = np.concatenate([d[0] for d in done])
+    T = np.concatenate([d[1] for d in done])
+    Lv = np.concatenate([d[2] for d in done])
+    V = np.concatenate([d[3] for d in done])
+    key = _spread2(A[:, 0]) | (_spread2(A[:, 1]) << np.uint64(1))
+    order = np.lexsort((key, T))
+    if camera is None:
+        camera = perspective_camera([-0.5, -2.6, 3.2], [-0.5, 0.0, 0.0], 62.0, width, width)
+    surf = SURF_OPAQUE if opaque else SURF_TRANSPARENT
+    return Scene(name, 1, 1, ctrl, A[order].copy(), T[order].copy(), Lv[order].copy(),
+                 V[order].astype(np.float32), 0.0, 1.0, 0.0, camera, dim=2, surface=surf,
+                 notes=f"Mandelbrot hexagon, levels {level0}..{maxlevel}, {max_iter} iterations, bend {bend}")
 
 
 def get_config(cid: int, **kw) -> Scene:
