@@ -54,6 +54,9 @@ def peaks():
         out["source"] = (f"measured: {meas['how']} ({meas['when']}); derived at {sm_mhz:.0f} MHz would be "
                          f"{derived:.1f}")
         out["mufu_ex2_tops"] = meas.get("mufu_ex2_tops")
+        if meas.get("dfma_tflops"):
+            out["fp64_tflops"] = float(meas["dfma_tflops"])
+            out["fp64_source"] = f"measured: tools/peaks.cu fma.rn.f64 chains ({meas['when']})"
         out["fmnmx_tops"] = meas.get("fmnmx_tops")
     except Exception:
         pass
@@ -130,6 +133,8 @@ def make_scene(cfg: int, device):
         return sg.shell_uniform(7, 1024, 256, name="C4s", device=device)
     if cfg == 55:   # profiling stand-in for C5: maxlevel 8 at 1024^2 (about C5's records per pixel)
         return sg.config5(device=device, maxlevel=8, width=1024)
+    if cfg == 6:    # NEXT(3) surface workload: the Mandelbrot hexagon, bent patches
+        return sg.mandelbrot_hexagon(3, 11, width=2048, bend=0.35, name="MB")
     if cfg == 33:   # test size: C3's geometry at level 4, 128^2, 4 x 4 tiles, 2 coarsening cycles
         import dataclasses
         sc = sg.shell_uniform(4, 128, 16, gl_points=6, name="C3-L4", tiles=(4, 4), device=device)
@@ -142,12 +147,14 @@ WORKLOAD = {1: "C1: identity cube, uniform level 3 (512 hex), ortho 64x64, N=4",
             3: "C3: cubed-sphere shell R=2, uniform level 6 (1,572,864 hex), 1024x1024, N=6",
             4: "C4: cubed-sphere shell R=2, uniform level 8 (100,663,296 hex), 2048x2048, N=6",
             5: "C5: cubed-sphere shell R=2, adaptive levels 6..10, 4096x4096, N=8, 3 coarsening cycles",
+            6: "MB (surfaces, NEXT(3)): Mandelbrot hexagon, 2 quadtrees, levels 3..11, bent bilinear patches, "
+               "2048x2048, Eq. ABphi points",
             45: "C4s (profiling stand-in): shell R=2, uniform level 7 (12,582,912 hex), 1024x1024, N=6",
             55: "C5s (profiling stand-in): shell R=2, adaptive levels ..8, 1024x1024, N=8, 3 coarsening cycles",
             33: "C3-L4 (test size): shell R=2, uniform level 4, 128x128, N=6, 4x4 tiles, 2 coarsening cycles"}
 
 # oracle pixel sample (every s-th row and column) of the CPU baseline and the reference arm
-CPU_STRIDE = {1: 1, 2: 2, 3: 16, 4: 64, 5: 128, 45: 32, 55: 32, 33: 1}
+CPU_STRIDE = {1: 1, 2: 2, 3: 16, 4: 64, 5: 128, 6: 4, 45: 32, 55: 32, 33: 1}
 
 
 def forest_affine(scene):
@@ -326,7 +333,9 @@ def main():
     N = cam.gl_points
     rc.lib()
 
-    fold = args.fold if args.fold >= 0 else (0 if forest_affine(scene) else 2)
+    surface = getattr(scene, "dim", 3) == 2
+    surf_kw = dict(dim=2, surface=scene.surface) if surface else {}
+    fold = args.fold if args.fold >= 0 else (0 if forest_affine(scene) or surface else 2)
     cycles = scene.coarsen_cycles
     n = scene.num_leaves
     tiles = scene.tiles if world > 1 else (1, 1)
@@ -340,7 +349,7 @@ def main():
         old = rdist.aligned_ranges(torch.ones(n, dtype=torch.float64), world, allowed)
         lo, hi = old[rank]
         f0 = rc.Forest(scene.tree_ctrl, scene.geom_degree, scene.field_degree, A[lo:hi], T[lo:hi], Lv[lo:hi],
-                       F[lo:hi], scene.kappa0, scene.inv_F, scene.q0, first_global_leaf=lo)
+                       F[lo:hi], scene.kappa0, scene.inv_F, scene.q0, first_global_leaf=lo, **surf_kw)
         f0.camera_set(cam)
         f0.cull()
         w = f0.leaf_weights()
@@ -351,7 +360,7 @@ def main():
         wsum = float(w.sum())
         del A, T, Lv, F, allowed, w
         forest = rc.Forest(scene.tree_ctrl, scene.geom_degree, scene.field_degree, *mine, scene.kappa0,
-                           scene.inv_F, scene.q0, first_global_leaf=lo)
+                           scene.inv_F, scene.q0, first_global_leaf=lo, **surf_kw)
         keys = mine[:3]
         del mine
         torch.cuda.synchronize()
@@ -488,13 +497,18 @@ def main():
     # --- roofline of the dominant kernel (segment kernel) -----------------
     pk = peaks()
     import bench_model
-    fl = bench_model.flops(scene.geom_degree if not forest_affine(scene) else 1, N, hits_local, cand_local)
+    if surface:   # NEXT(3): fp64 ray-patch geometry
+        fl = bench_model.surface_flops(hits_local, cand_local)
+        kname, bound, peak = "k_cast_surface (ray-patch quadratic + Eq. ABphi)", "fp64_fma", pk.get("fp64_tflops")
+    else:
+        fl = bench_model.flops(scene.geom_degree if not forest_affine(scene) else 1, N, hits_local, cand_local)
+        kname = "k_cast_affine" if forest_affine(scene) else "k_cast_curved (intersection + integration + fold, fused)"
+        bound, peak = "fp32_fma", pk["fp32_tflops"]
     achieved = fl / (cast_local / 1000.0) / 1e12
-    kname = "k_cast_affine" if forest_affine(scene) else "k_cast_curved (intersection + integration + fold, fused)"
-    roof = {"kernel": kname, "bound": "fp32_fma", "achieved": achieved, "peak": pk["fp32_tflops"], "unit": "TFLOP/s",
-            "frac": achieved / pk["fp32_tflops"], "traffic": None, "kernel_ms": cast_local,
+    roof = {"kernel": kname, "bound": bound, "achieved": achieved, "peak": peak, "unit": "TFLOP/s",
+            "frac": achieved / peak if peak else None, "traffic": None, "kernel_ms": cast_local,
             "share_of_step": cast_local / ms_local, "algorithmic_flops_per_launch": fl,
-            "peak_source": pk["source"]}
+            "peak_source": pk["source"] if not surface else pk.get("fp64_source")}
     tpath = os.path.join(ROOT, "profiles", f"traffic_c{args.config}.json")
     if os.path.exists(tpath):
         try:
@@ -532,7 +546,7 @@ def main():
         # rc_forest_create copies the pinned host arrays (the scene generator
         # guarantees SFC order: RC_HOST_COPY_TRUSTED skips the host-side check)
         f2 = rc.Forest(scene.tree_ctrl, scene.geom_degree, scene.field_degree, *pinned_np, scene.kappa0,
-                       scene.inv_F, scene.q0, first_global_leaf=lo, trusted=True)
+                       scene.inv_F, scene.q0, first_global_leaf=lo, trusted=True, **surf_kw)
         k2 = [torch.from_numpy(a).to(dev) for a in host[:3]] if (world > 1 and cycles) else None
         out, fa = frame(f2, k2, (lo, hi))
         img_host.view(-1)[:out.numel()].copy_(out.reshape(-1))

@@ -30,3 +30,17 @@ def flops(R, N, hit_pairs, candidates):
 
 def flops_curved(hit_pairs, candidates, N, P):
     return flops(2, N, hit_pairs, candidates)
+
+
+# Surface forests (NEXT(3), surface.cu): fp64 FMA-pipe instructions per pair
+# of the ray-patch method (App. A.1), counted from the
+# arithmetic the method needs: per candidate the ray (6), the element's four
+# corner points from the tree patch (36), their projection onto d1, d2 (24),
+# the basis (12), the bilinear coefficients and the quadratic (20); per hit
+# root s1 (6), the point and the two tangents (27), alpha (4), the normal and
+# cos phi (12).  1 FMA-pipe instruction = 2 flops.
+SURFACE_MISS, SURFACE_HIT = 98.0, 49.0
+
+
+def surface_flops(hit_pairs, candidates):
+    return 2.0 * (SURFACE_MISS * candidates + SURFACE_HIT * hit_pairs)

@@ -38,7 +38,7 @@ typedef enum {
 } rc_status;
 
 const char* rc_last_error(void);
-int32_t rc_version(void);    /* ABI version, currently 2 */
+int32_t rc_version(void);    /* ABI version, currently 3 */
 
 /* ------------------------------------------------------------------------
  * Forest: SFC-ordered leaves of a forest of octrees with per-tree degree-R
@@ -52,6 +52,12 @@ typedef struct {
   float inv_F;    /* 1/F, F = max |nodal f|                                       */
   float q0;       /* q = q0 ((1+f~)/2, (1-f~)/2, 1/2)  RGB emission density      */
 } rc_transfer;
+
+typedef struct {      /* surface transfer of the corner-interpolated value v (surface forests) */
+  float a[2];         /* A_s = clamp(a[0] + a[1] v, 0, 1)                                  */
+  float i[3][3];      /* I_s,c = i[c][0] + i[c][1] v + i[c][2] exp(-((1 - v) k)^2 / 2)      */
+  float k;
+} rc_surface;
 
 enum { RC_HOST_COPY = 0, RC_DEVICE_COPY = 1, RC_HOST_COPY_TRUSTED = 2 };
 
@@ -74,6 +80,17 @@ typedef struct {
                                  memory gives asynchronous DMA);
                                  RC_DEVICE_COPY: leaf arrays are device pointers        */
   rc_transfer transfer;
+  /* surface forests (§2.8, App. A.1):
+   * dim = 2 makes the leaves quadtree leaves (leaf_anchor[3e+2] == 0) of
+   * bilinear tree patches: geom_degree = field_degree = 1, tree_ctrl is
+   * [K][2][2][3] ([k][m2][m1][xyz]) and leaf_field [n][4] the corner values
+   * ([k2][k1]).  A ray meets a leaf patch X_E(s), s in [0,1)^2, in at most two
+   * points; each is a zero-length record (alpha_near == alpha_far) with
+   * Eq. ABphi: A = A_s^(1/cos phi), b = I_s (1 - A) (Eq. BIrelation), phi the
+   * angle between the ray and the patch normal; A_s = 0 is opaque.  dim = 0
+   * or 3: volume forest (the rest of this header), surface ignored. */
+  int32_t dim;
+  rc_surface surface;
 } rc_forest_desc;
 
 typedef struct rc_forest rc_forest;

@@ -19,41 +19,6 @@ namespace rc {
 // pixel-centre rectangle.  fp64 so that the decision differs
 // from the fp64 oracle only for eps-ambiguous leaves.
 // ---------------------------------------------------------------------------
-__device__ bool project_rect(const CamConst& cc, const double lo[3], const double hi[3], Rect16& rc) {
-  double pmin[2], pmax[2];
-  int dims[2] = {cc.W, cc.H};
-  if (cc.proj == RC_PERSPECTIVE) {
-    if (hi[2] < cc.n || lo[2] > cc.far_dist) return false;
-    double z0 = fmax(lo[2], cc.n), z1 = fmax(hi[2], cc.n);
-    double s = cc.n / cc.ell;
-    for (int d = 0; d < 2; ++d) {
-      double a = lo[d] / z0, b = lo[d] / z1, c = hi[d] / z0, e = hi[d] / z1;
-      pmin[d] = s * fmin(fmin(a, b), fmin(c, e)) + 0.5 * (dims[d] - 1);
-      pmax[d] = s * fmax(fmax(a, b), fmax(c, e)) + 0.5 * (dims[d] - 1);
-    }
-  } else {
-    if (hi[2] < 0.0 || lo[2] > cc.far_dist) return false;
-    for (int d = 0; d < 2; ++d) {
-      pmin[d] = lo[d] / cc.ell + 0.5 * (dims[d] - 1);
-      pmax[d] = hi[d] / cc.ell + 0.5 * (dims[d] - 1);
-    }
-  }
-  int r[4];
-  for (int d = 0; d < 2; ++d) {
-    double a = ceil(pmin[d]), b = floor(pmax[d]);
-    a = fmax(a, 0.0);
-    b = fmin(b, (double)(dims[d] - 1));
-    if (!(a <= b)) return false;
-    r[2 * d] = (int)a;
-    r[2 * d + 1] = (int)b;
-  }
-  rc.i0 = (int16_t)r[0];
-  rc.i1 = (int16_t)r[1];
-  rc.j0 = (int16_t)r[2];
-  rc.j1 = (int16_t)r[3];
-  return true;
-}
-
 __global__ void k_cull_affine(CamConst cc, const TreeConst* __restrict__ trees, DevLeafView L, int64_t n,
                               int32_t* __restrict__ flag, Rect16* __restrict__ rect) {
   int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
@@ -515,6 +480,106 @@ __global__ void k_scatter(const rc_seg* __restrict__ segs, int64_t n, const int6
     int k = atomicAdd(&cursor[pix], 1);
     out[off[pix] + k] = (uint32_t)s;
   }
+}
+
+// Banded pixel bucketing of the aggregation pass (row a7): a permutation
+// grouping the records by pixel, built without scattered 4-byte writes into
+// the 4-byte-per-record permutation (each would cost a DRAM read-modify-write
+// of its 32-byte sector).  Bands of RC_BAND pixels: (1) band counts with
+// warp-aggregated atomics, (2) record indices appended to their band's range
+// of a scratch array in warp runs (a warp's records are mostly one band: its
+// 32 pixels are one chunk of one leaf's rectangle row), (3) one CTA per band
+// counts its pixels in shared memory, writes their offsets and places the
+// indices within the band's range (an L2-resident window).
+constexpr int BAND_SH = 6;   // 64 pixels per band
+constexpr int BAND_SMEM = 9216;    // entries cached in shared memory per band (index + local pixel; static smem < 48 KB)
+
+__device__ __forceinline__ unsigned lanemask_lt() {
+  unsigned m;
+  asm("mov.u32 %0, %%lanemask_lt;" : "=r"(m));
+  return m;
+}
+
+__global__ void k_band_count(const rc_seg* __restrict__ segs, int64_t n, int32_t* __restrict__ bcnt) {
+  const unsigned lane = threadIdx.x & 31;
+  const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+  for (int64_t base = (int64_t)blockIdx.x * blockDim.x + (threadIdx.x & ~31u); base < n; base += stride) {
+    const int64_t s = base + lane;
+    const int b = s < n ? (int)(__ldcs(&segs[s].pixel) >> BAND_SH) : -1;
+    const unsigned m = __match_any_sync(0xffffffffu, b);
+    if (b >= 0 && lane == (unsigned)(__ffs(m) - 1)) atomicAdd(&bcnt[b], __popc(m));
+  }
+}
+
+__global__ void k_band_scatter(const rc_seg* __restrict__ segs, int64_t n, const int64_t* __restrict__ boff,
+                               int32_t* __restrict__ bcur, uint32_t* __restrict__ tmp) {
+  const unsigned lane = threadIdx.x & 31;
+  const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+  for (int64_t base = (int64_t)blockIdx.x * blockDim.x + (threadIdx.x & ~31u); base < n; base += stride) {
+    const int64_t s = base + lane;
+    const int b = s < n ? (int)(__ldcs(&segs[s].pixel) >> BAND_SH) : -1;
+    const unsigned m = __match_any_sync(0xffffffffu, b);
+    const int leader = __ffs(m) - 1;
+    int first = 0;
+    if (b >= 0 && (int)lane == leader) first = atomicAdd(&bcur[b], __popc(m));
+    first = __shfl_sync(0xffffffffu, first, leader);
+    if (b >= 0) tmp[boff[b] + first + __popc(m & lanemask_lt())] = (uint32_t)s;
+  }
+}
+
+__global__ void __launch_bounds__(512) k_band_sort(const rc_seg* __restrict__ segs, const uint32_t* __restrict__ tmp,
+                                                   const int64_t* __restrict__ boff, int64_t nbands, int64_t npix,
+                                                   uint32_t* __restrict__ perm, int64_t* __restrict__ off) {
+  __shared__ int32_t hist[1 << BAND_SH];
+  __shared__ uint32_t sidx[BAND_SMEM];
+  __shared__ uint8_t spix[BAND_SMEM];
+  constexpr int NB = 1 << BAND_SH;
+  for (int64_t b = blockIdx.x; b < nbands; b += gridDim.x) {
+    const int64_t e0 = boff[b], ne = boff[b + 1] - e0;
+    if (threadIdx.x < NB) hist[threadIdx.x] = 0;
+    __syncthreads();
+    for (int64_t i = threadIdx.x; i < ne; i += blockDim.x) {
+      const uint32_t sidx_i = tmp[e0 + i];
+      const int p = (int)(segs[sidx_i].pixel & (NB - 1));
+      if (i < BAND_SMEM) {
+        sidx[i] = sidx_i;
+        spix[i] = (uint8_t)p;
+      }
+      atomicAdd(&hist[p], 1);
+    }
+    __syncthreads();
+    if (threadIdx.x < 32) {   // exclusive scan of the NB counts (NB = 64: two per lane)
+      const int lane = threadIdx.x;
+      const int c0 = hist[2 * lane], c1 = hist[2 * lane + 1];
+      int incl = c0 + c1;
+#pragma unroll
+      for (int o = 1; o < 32; o <<= 1) {
+        const int y = __shfl_up_sync(0xffffffffu, incl, o);
+        if (lane >= o) incl += y;
+      }
+      const int ex = incl - c0 - c1;
+      hist[2 * lane] = ex;
+      hist[2 * lane + 1] = ex + c0;
+      const int64_t p0 = b * NB + 2 * lane;
+      if (p0 < npix) off[p0] = e0 + ex;
+      if (p0 + 1 < npix) off[p0 + 1] = e0 + ex + c0;
+    }
+    __syncthreads();
+    for (int64_t i = threadIdx.x; i < ne; i += blockDim.x) {
+      uint32_t sidx_i;
+      int p;
+      if (i < BAND_SMEM) {
+        sidx_i = sidx[i];
+        p = spix[i];
+      } else {
+        sidx_i = tmp[e0 + i];
+        p = (int)(segs[sidx_i].pixel & (NB - 1));
+      }
+      perm[e0 + atomicAdd(&hist[p], 1)] = sidx_i;
+    }
+    __syncthreads();
+  }
+  if (blockIdx.x == 0 && threadIdx.x == 0) off[npix] = boff[nbands];
 }
 
 // pixel-bucketed copy of the records (the composite then reads each pixel's
@@ -1011,41 +1076,115 @@ __global__ void __launch_bounds__(FOLD_WARPS * 32, 1) k_coarsen_list(
 // coarsening: a ray crossing one big node) do not serialise on one lane.
 // Pixels with tied sort keys or more records go to the list pass.
 constexpr int COARSEN_FAST_CAP = 512;
+constexpr int COARSEN_MAIN_CAP = 256;   // main pass; 256 < n <= 512 go to a second pass over a list
 constexpr int COARSEN_FAST_WARPS = 2;
-struct CoarsenSmem {                    // per warp, structure of arrays
-  float an[COARSEN_FAST_CAP], af[COARSEN_FAST_CAP], a[COARSEN_FAST_CAP], b0[COARSEN_FAST_CAP],
-      b1[COARSEN_FAST_CAP], b2[COARSEN_FAST_CAP];
-  uint32_t key[COARSEN_FAST_CAP];
-  int32_t node[COARSEN_FAST_CAP];
+template <int CAP>
+struct CoarsenSmemT {                   // per warp, structure of arrays
+  float an[CAP], af[CAP], a[CAP], b0[CAP], b1[CAP], b2[CAP];
+  int32_t node[CAP];
 };
 
-// returns false when two records share the sort key (the caller defers the pixel)
+// Warp bitonic sort of 32 E 32-bit keys in the blocked layout i = lane E + e,
+// ascending (as warp_sort_blocked, one register per element: the aggregation
+// pass embeds the local index in the key's low bits).
 template <int E>
-__device__ __forceinline__ bool coarsen_pixel(const CoarsenSmem& C, int n, int64_t pix,
+__device__ __forceinline__ void warp_sort32(uint32_t (&key)[E]) {
+  const unsigned lane = threadIdx.x & 31;
+  constexpr int NN = 32 * E;
+#pragma unroll 1
+  for (int k = 2; k <= NN; k <<= 1) {
+#pragma unroll 1
+    for (int j = k >> 1; j >= E; j >>= 1) {   // partners in other lanes
+      const int lj = j / E;
+      const bool lower = (lane & lj) == 0;
+#pragma unroll
+      for (int e = 0; e < E; ++e) {
+        const uint32_t ok = __shfl_xor_sync(0xffffffffu, key[e], lj);
+        const bool up = ((((int)lane * E + e) & k) == 0);
+        key[e] = (lower == up) ? min(ok, key[e]) : max(ok, key[e]);
+      }
+    }
+#pragma unroll
+    for (int j = E >> 1; j > 0; j >>= 1) {     // partners in the same lane
+      if (j < k) {
+#pragma unroll
+        for (int e = 0; e < E; ++e) {
+          const int p = e ^ j;
+          if (p > e) {
+            const bool up = ((((int)lane * E + e) & k) == 0);
+            const uint32_t lo = min(key[e], key[p]), hi = max(key[e], key[p]);
+            key[e] = up ? lo : hi;
+            key[p] = up ? hi : lo;
+          }
+        }
+      }
+    }
+  }
+}
+
+// returns false when two records' alpha_near cannot be told apart by the
+// 22-bit sort key (their order-preserving bits agree after the pixel's range
+// shift; the caller defers the pixel to the list pass, which sorts under the
+// total order)
+template <int E, class Smem>
+__device__ __forceinline__ bool coarsen_pixel(const Smem& C, int n, int64_t pix,
                                               const int32_t* __restrict__ node_first, uint32_t key_base, float tau,
                                               rc_seg* __restrict__ out, int64_t out_cap,
-                                              int64_t* __restrict__ counters) {
+                                              int64_t* __restrict__ counters, const uint16_t* list = nullptr,
+                                              int* agree = nullptr) {
+  // list: the local indices of the n records to fold (nullptr: 0 .. n-1);
+  // agree: the CTA's warps fold disjoint groups of one pixel and emit only if
+  // none of them found a tie (two shared-memory flags, CTA barriers)
   const unsigned lane = threadIdx.x & 31;
-  uint64_t key[E];
-  uint32_t id[E];
+  // sort key: alpha_near's order-preserving bits relative to the pixel's
+  // smallest, shifted into 22 bits (exact while the pixel's alpha range spans
+  // < 2^22 ulps), above the 9-bit local index; < 2^31, below the 0xffffffff pad
+  uint32_t key[E];
+  uint32_t omin = 0xffffffffu, omax = 0u;
 #pragma unroll
   for (int e = 0; e < E; ++e) {
-    const int i = (int)lane * E + e;
-    id[e] = (uint32_t)i;
-    key[e] = i < n ? (((uint64_t)ord_bits(C.an[i]) << 32) | C.key[i]) : ~0ull;
+    const int pos = (int)lane * E + e;
+    const int i = pos < n ? (list ? (int)list[pos] : pos) : 0;
+    key[e] = pos < n ? ord_bits(C.an[i]) : 0u;
+    if (pos < n) {
+      omin = min(omin, key[e]);
+      omax = max(omax, key[e]);
+    }
   }
-  warp_sort_blocked<E>(key, id);
-  // ties: the register order is not total
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) {
+    omin = min(omin, __shfl_xor_sync(0xffffffffu, omin, o));
+    omax = max(omax, __shfl_xor_sync(0xffffffffu, omax, o));
+  }
+  const uint32_t range = omax - omin;
+  const int sh = max(0, 32 - __clz((int)range) - 22);
+#pragma unroll
+  for (int e = 0; e < E; ++e) {
+    const int pos = (int)lane * E + e;
+    const uint32_t i = pos < n ? (list ? (uint32_t)list[pos] : (uint32_t)pos) : 0u;
+    key[e] = pos < n ? ((((key[e] - omin) >> sh) << 9) | i) : 0xffffffffu;
+  }
+  warp_sort32<E>(key);
+  uint32_t id[E];
+#pragma unroll
+  for (int e = 0; e < E; ++e) id[e] = key[e] & 0x1FFu;
   {
-    uint64_t prev_key = __shfl_up_sync(0xffffffffu, key[E - 1], 1);
-    if (lane == 0) prev_key = ~0ull;
+    uint32_t prev_key = __shfl_up_sync(0xffffffffu, key[E - 1], 1);
     bool tie = false;
 #pragma unroll
     for (int e = 0; e < E; ++e) {
-      tie |= (int)lane * E + e < n && key[e] == prev_key;
+      const int k = (int)lane * E + e;
+      tie |= k > 0 && k < n && (key[e] >> 9) == (prev_key >> 9);
       prev_key = key[e];
     }
-    if (__any_sync(0xffffffffu, tie)) return false;
+    bool any = __any_sync(0xffffffffu, tie);
+    if (agree) {
+      if (lane == 0) agree[threadIdx.x >> 5] = any ? 1 : 0;
+      __syncthreads();
+      any = agree[0] | agree[1];
+      __syncthreads();
+    }
+    if (any) return false;
   }
   // head flags of this lane's positions (a run starts at a gap / overlap or a new node)
   const int lo = (int)lane * E;
@@ -1070,13 +1209,14 @@ __device__ __forceinline__ bool coarsen_pixel(const CoarsenSmem& C, int n, int64
   Acc X{1.0, 0.0, 0.0, 0.0};
 #pragma unroll
   for (int e = 0; e < E; ++e) {
-    if (lo + e >= n) break;
-    if ((heads >> e) & 1u) {
-      F = true;
-      HID = id[e];
-      X = Acc{1.0, 0.0, 0.0, 0.0};
+    if (lo + e < n) {   // predicated, no early exit (positions >= n are the tail)
+      if ((heads >> e) & 1u) {
+        F = true;
+        HID = id[e];
+        X = Acc{1.0, 0.0, 0.0, 0.0};
+      }
+      acc_push(X, C.a[id[e]], C.b0[id[e]], C.b1[id[e]], C.b2[id[e]]);
     }
-    acc_push(X, C.a[id[e]], C.b0[id[e]], C.b1[id[e]], C.b2[id[e]]);
   }
   const int hi = min(n, lo + E);
   int nemit = __popc(heads & ~(lo == 0 ? 1u : 0u)) + ((lo < hi && hi == n) ? 1 : 0);
@@ -1118,39 +1258,48 @@ __device__ __forceinline__ bool coarsen_pixel(const CoarsenSmem& C, int n, int64
 #pragma unroll
   for (int e = 0; e < E; ++e) {
     const int k = lo + e;
-    if (k >= n) break;
-    if (k > 0 && ((heads >> e) & 1u)) {
-      emit(start_id, last_id, acc);
-      acc = Acc{1.0, 0.0, 0.0, 0.0};
-      start_id = id[e];
+    if (k < n) {
+      if (k > 0 && ((heads >> e) & 1u)) {
+        emit(start_id, last_id, acc);
+        acc = Acc{1.0, 0.0, 0.0, 0.0};
+        start_id = id[e];
+      }
+      acc_push(acc, C.a[id[e]], C.b0[id[e]], C.b1[id[e]], C.b2[id[e]]);
+      last_id = id[e];
     }
-    acc_push(acc, C.a[id[e]], C.b0[id[e]], C.b1[id[e]], C.b2[id[e]]);
-    last_id = id[e];
   }
   if (lo < hi && hi == n) emit(start_id, last_id, acc);
   return true;
 }
 
-__global__ void __launch_bounds__(COARSEN_FAST_WARPS * 32, 8) k_coarsen_fast(
+// Main pass (CAP = 256): one warp per pixel (grid-stride over all pixels);
+// 256 < n <= 512 go to the mid list, larger ones to the defer list.  The
+// record gathers and the target-node lookups are separate loops (independent
+// loads in flight).
+__global__ void __launch_bounds__(COARSEN_FAST_WARPS * 32, 10) k_coarsen_fast(
     const rc_seg* __restrict__ recs, const uint32_t* __restrict__ perm, const int64_t* __restrict__ off, int64_t npix,
     const int32_t* __restrict__ node_first, const int32_t* __restrict__ leaf_node, uint32_t key_base, float tau,
-    rc_seg* __restrict__ out, int64_t out_cap, int32_t* __restrict__ defer, int64_t* __restrict__ counters) {
+    rc_seg* __restrict__ out, int64_t out_cap, int32_t* __restrict__ defer, int32_t* __restrict__ mid,
+    int64_t* __restrict__ counters) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
   const int warp = threadIdx.x >> 5;
   const unsigned lane = threadIdx.x & 31;
-  CoarsenSmem& C = reinterpret_cast<CoarsenSmem*>(smem_raw)[warp];
+  CoarsenSmemT<COARSEN_MAIN_CAP>& C = reinterpret_cast<CoarsenSmemT<COARSEN_MAIN_CAP>*>(smem_raw)[warp];
   const float4* recs4 = reinterpret_cast<const float4*>(recs);
   for (int64_t pix = (int64_t)blockIdx.x * COARSEN_FAST_WARPS + warp; pix < npix;
        pix += (int64_t)gridDim.x * COARSEN_FAST_WARPS) {
     const int64_t base = off[pix];
     const int n = (int)(off[pix + 1] - base);
     if (n == 0) continue;
-    if (n > COARSEN_FAST_CAP) {
-      if (lane == 0) defer[atomicAdd((unsigned long long*)&counters[CNT_DEFER], 1ull)] = (int32_t)pix;
+    if (n > COARSEN_MAIN_CAP) {
+      if (lane == 0) {
+        if (n <= COARSEN_FAST_CAP) mid[atomicAdd((unsigned long long*)&counters[CNT_MID], 1ull)] = (int32_t)pix;
+        else defer[atomicAdd((unsigned long long*)&counters[CNT_DEFER], 1ull)] = (int32_t)pix;
+      }
       continue;
     }
     const uint32_t* S = perm + base;
-    // 1. one gather per record (and its node at the target level)
+    // 1. one gather per record; the record key parks in node[] ...
 #pragma unroll 4
     for (int k = lane; k < n; k += 32) {
       const uint32_t id = S[k];
@@ -1161,18 +1310,85 @@ __global__ void __launch_bounds__(COARSEN_FAST_WARPS * 32, 8) k_coarsen_fast(
       C.b0[k] = hi.x;
       C.b1[k] = hi.y;
       C.b2[k] = hi.z;
-      const uint32_t key = __float_as_uint(hi.w);
-      C.key[k] = key;
-      C.node[k] = leaf_node[key - key_base];
+      C.node[k] = (int32_t)(__float_as_uint(hi.w) - key_base);
     }
+    // ... 2. and becomes its node at the target level (independent lookups)
+#pragma unroll 8
+    for (int k = lane; k < n; k += 32) C.node[k] = leaf_node[C.node[k]];
     __syncwarp();
     bool ok;
     if (n <= 64) ok = coarsen_pixel<2>(C, n, pix, node_first, key_base, tau, out, out_cap, counters);
     else if (n <= 128) ok = coarsen_pixel<4>(C, n, pix, node_first, key_base, tau, out, out_cap, counters);
-    else if (n <= 256) ok = coarsen_pixel<8>(C, n, pix, node_first, key_base, tau, out, out_cap, counters);
-    else ok = coarsen_pixel<16>(C, n, pix, node_first, key_base, tau, out, out_cap, counters);
+    else ok = coarsen_pixel<8>(C, n, pix, node_first, key_base, tau, out, out_cap, counters);
     if (!ok && lane == 0) defer[atomicAdd((unsigned long long*)&counters[CNT_DEFER], 1ull)] = (int32_t)pix;
     __syncwarp();
+  }
+}
+
+// Mid pass: 256 < n <= 512.  Runs never cross target nodes, so the records
+// split into two independent groups by node parity: one CTA per pixel, warp
+// g folds group g (<= 256 records each, else the pixel is deferred) with the
+// main pass's warp code; the warps emit only if neither met a tie.
+struct CoarsenMidSmem {
+  CoarsenSmemT<COARSEN_FAST_CAP> C;
+  uint16_t list[2][COARSEN_MAIN_CAP];
+  int ng[2];
+  int agree[2];
+};
+
+__global__ void __launch_bounds__(64, 8) k_coarsen_mid(
+    const rc_seg* __restrict__ recs, const uint32_t* __restrict__ perm, const int64_t* __restrict__ off,
+    const int32_t* __restrict__ node_first, const int32_t* __restrict__ leaf_node, uint32_t key_base, float tau,
+    rc_seg* __restrict__ out, int64_t out_cap, int32_t* __restrict__ defer, const int32_t* __restrict__ mid,
+    int64_t* __restrict__ counters) {
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  CoarsenMidSmem& M = *reinterpret_cast<CoarsenMidSmem*>(smem_raw);
+  CoarsenSmemT<COARSEN_FAST_CAP>& C = M.C;
+  const int warp = threadIdx.x >> 5;
+  const unsigned lane = threadIdx.x & 31;
+  const float4* recs4 = reinterpret_cast<const float4*>(recs);
+  const int64_t nq = counters[CNT_MID];
+  for (int64_t q = blockIdx.x; q < nq; q += gridDim.x) {
+    const int64_t pix = mid[q];
+    const int64_t base = off[pix];
+    const int n = (int)(off[pix + 1] - base);
+    const uint32_t* S = perm + base;
+#pragma unroll 4
+    for (int k = threadIdx.x; k < n; k += 64) {
+      const uint32_t id = S[k];
+      const float4 lo = recs4[2 * (size_t)id], hi = recs4[2 * (size_t)id + 1];
+      C.an[k] = lo.y;
+      C.af[k] = lo.z;
+      C.a[k] = lo.w;
+      C.b0[k] = hi.x;
+      C.b1[k] = hi.y;
+      C.b2[k] = hi.z;
+      C.node[k] = (int32_t)(__float_as_uint(hi.w) - key_base);
+    }
+#pragma unroll 8
+    for (int k = threadIdx.x; k < n; k += 64) C.node[k] = leaf_node[C.node[k]];
+    __syncthreads();
+    // warp g lists the records of group g (node parity), in index order
+    int ng = 0;
+    for (int k0 = 0; k0 < n; k0 += 32) {
+      const int k = k0 + (int)lane;
+      const bool mine = k < n && (C.node[k] & 1) == warp;
+      const unsigned bal = __ballot_sync(0xffffffffu, mine);
+      const int pos = ng + __popc(bal & lanemask_lt());
+      if (mine && pos < COARSEN_MAIN_CAP) M.list[warp][pos] = (uint16_t)k;
+      ng += __popc(bal);
+    }
+    if (lane == 0) M.ng[warp] = ng;
+    __syncthreads();
+    const int ngmax = max(M.ng[0], M.ng[1]);
+    bool ok = ngmax <= COARSEN_MAIN_CAP;
+    if (ok) {   // uniform over the CTA: the same instantiation in both warps
+      if (ngmax <= 64) ok = coarsen_pixel<2>(C, ng, pix, node_first, key_base, tau, out, out_cap, counters, M.list[warp], M.agree);
+      else if (ngmax <= 128) ok = coarsen_pixel<4>(C, ng, pix, node_first, key_base, tau, out, out_cap, counters, M.list[warp], M.agree);
+      else ok = coarsen_pixel<8>(C, ng, pix, node_first, key_base, tau, out, out_cap, counters, M.list[warp], M.agree);
+    }
+    if (!ok && threadIdx.x == 0) defer[atomicAdd((unsigned long long*)&counters[CNT_DEFER], 1ull)] = (int32_t)pix;
+    __syncthreads();
   }
 }
 
@@ -1297,6 +1513,22 @@ cudaError_t launch_scatter(const rc_seg* segs, int64_t n, const int64_t* off, in
   return cudaGetLastError();
 }
 
+cudaError_t launch_band_bucket(const rc_seg* segs, int64_t n, int64_t npix, int32_t* bcnt, int64_t* boff,
+                               int64_t* scan_tmp, uint32_t* tmp, uint32_t* perm, int64_t* off, int grid,
+                               cudaStream_t s) {
+  const int64_t nb = (npix + (1 << BAND_SH) - 1) >> BAND_SH;
+  cudaError_t e = cudaMemsetAsync(bcnt, 0, sizeof(int32_t) * (nb + 1), s);
+  if (e != cudaSuccess) return e;
+  if (n > 0) k_band_count<<<grid, 256, 0, s>>>(segs, n, bcnt);
+  e = scan_exclusive<int32_t>(bcnt, boff, nb, scan_tmp, s);
+  if (e == cudaSuccess) e = cudaMemsetAsync(bcnt, 0, sizeof(int32_t) * (nb + 1), s);   // reused as cursors
+  if (e != cudaSuccess) return e;
+  if (n > 0) k_band_scatter<<<grid, 256, 0, s>>>(segs, n, boff, bcnt, tmp);
+  k_band_sort<<<(unsigned)std::min<int64_t>(nb, 148 * 4), 512, 0, s>>>(segs, tmp, boff, nb, npix, perm, off);
+  g_launches += 3;
+  return cudaGetLastError();
+}
+
 cudaError_t launch_scatter_rec(const rc_seg* segs, int64_t n, const int64_t* off, int32_t* cursor, rc_seg* out,
                                int grid, cudaStream_t s, const int64_t* d_n) {
   k_scatter_rec<<<grid, 256, 0, s>>>(segs, n, d_n, off, cursor, out);
@@ -1306,25 +1538,32 @@ cudaError_t launch_scatter_rec(const rc_seg* segs, int64_t n, const int64_t* off
 
 cudaError_t launch_coarsen(const rc_seg* recs, const uint32_t* perm, const int64_t* off, int64_t npix,
                            const int32_t* node_first, const int32_t* leaf_node, uint32_t key_base, float tau, rc_seg* out,
-                           int64_t out_cap, int32_t* defer, int64_t* counters, int max_grid, cudaStream_t s) {
+                           int64_t out_cap, int32_t* defer, int32_t* mid, int64_t* counters, int max_grid,
+                           cudaStream_t s) {
   static bool attr = false;
-  const size_t smemf = sizeof(CoarsenSmem) * COARSEN_FAST_WARPS;
+  const size_t smem_main = sizeof(CoarsenSmemT<COARSEN_MAIN_CAP>) * COARSEN_FAST_WARPS;
+  const size_t smem_mid = sizeof(CoarsenMidSmem);
   const size_t smeml = (size_t)FOLD_WARPS * FOLD_CAP * (sizeof(uint64_t) + sizeof(uint16_t));
   if (!attr) {
-    cudaError_t e = cudaFuncSetAttribute(k_coarsen_fast, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smemf);
+    cudaError_t e = cudaFuncSetAttribute(k_coarsen_fast, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem_main);
+    if (e == cudaSuccess)
+      e = cudaFuncSetAttribute(k_coarsen_mid, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem_mid);
     if (e == cudaSuccess)
       e = cudaFuncSetAttribute(k_coarsen_list, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smeml);
     if (e != cudaSuccess) return e;
     attr = true;
   }
   cudaError_t e = cudaMemsetAsync(counters + CNT_DEFER, 0, sizeof(int64_t), s);
+  if (e == cudaSuccess) e = cudaMemsetAsync(counters + CNT_MID, 0, sizeof(int64_t), s);
   if (e != cudaSuccess) return e;
   const int grid = (int)std::min<int64_t>((npix + COARSEN_FAST_WARPS - 1) / COARSEN_FAST_WARPS, (int64_t)max_grid);
-  k_coarsen_fast<<<grid, COARSEN_FAST_WARPS * 32, smemf, s>>>(recs, perm, off, npix, node_first, leaf_node, key_base,
-                                                              tau, out, out_cap, defer, counters);
+  k_coarsen_fast<<<grid, COARSEN_FAST_WARPS * 32, smem_main, s>>>(recs, perm, off, npix, node_first, leaf_node,
+                                                                  key_base, tau, out, out_cap, defer, mid, counters);
+  k_coarsen_mid<<<grid, 64, smem_mid, s>>>(recs, perm, off, node_first, leaf_node, key_base, tau, out, out_cap, defer,
+                                           mid, counters);
   k_coarsen_list<<<std::min(grid, 296), FOLD_WARPS * 32, smeml, s>>>(recs, perm, off, node_first, leaf_node, key_base,
                                                                      tau, out, out_cap, defer, counters);
-  g_launches += 2;
+  g_launches += 3;
   return cudaGetLastError();
 }
 

@@ -3,7 +3,7 @@
 // parent, one level per cycle).
 //
 // Level 0 is the SFC-ordered leaf array itself.  Level c+1 is level c with
-// every complete family of 8 same-level siblings (8 consecutive nodes with
+// every complete family of 8 same-level siblings (4 for the quadtrees of surface forests; 8 consecutive nodes with
 // the same tree, level l >= 1 and parent, child ids 0..7 in Morton order)
 // replaced by its parent.  Families split across ranks are incomplete
 // locally and stay.  A node is stored by the local index
@@ -31,18 +31,19 @@ __device__ __forceinline__ int child_id(const int32_t* a, int lvl) {
   return ((a[0] >> b) & 1) | (((a[1] >> b) & 1) << 1) | (((a[2] >> b) & 1) << 2);
 }
 
-// flag[k] = 1 iff nodes k..k+7 form a complete family (k is child 0)
-__global__ void k_family_start(NodeView V, int64_t n, int32_t* __restrict__ flag) {
+// flag[k] = 1 iff nodes k..k+fam-1 form a complete family (k is child 0);
+// fam = 8 (octrees) or 4 (quadtrees of surface forests: z anchors are 0)
+__global__ void k_family_start(NodeView V, int64_t n, int fam, int32_t* __restrict__ flag) {
   const int64_t k = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (k >= n) return;
   int f = 0;
   const int lvl = V.level[k];
-  if (k + 7 < n && lvl >= 1 && child_id(V.anchor + 3 * k, lvl) == 0) {
+  if (k + fam - 1 < n && lvl >= 1 && child_id(V.anchor + 3 * k, lvl) == 0) {
     const int t = V.tree[k];
     const int32_t pm = ~((1 << (RC_MAXLEVEL - lvl + 1)) - 1);
     const int32_t p0 = V.anchor[3 * k] & pm, p1 = V.anchor[3 * k + 1] & pm, p2 = V.anchor[3 * k + 2] & pm;
     f = 1;
-    for (int j = 1; j < 8 && f; ++j) {
+    for (int j = 1; j < fam && f; ++j) {
       const int64_t q = k + j;
       const int32_t* a = V.anchor + 3 * q;
       if (V.tree[q] != t || V.level[q] != lvl || (a[0] & pm) != p0 || (a[1] & pm) != p1 || (a[2] & pm) != p2 ||
@@ -54,11 +55,11 @@ __global__ void k_family_start(NodeView V, int64_t n, int32_t* __restrict__ flag
 }
 
 // keep[k] = 1 unless k is a non-first member of a family
-__global__ void k_family_keep(const int32_t* __restrict__ start, int64_t n, int32_t* __restrict__ keep) {
+__global__ void k_family_keep(const int32_t* __restrict__ start, int64_t n, int fam, int32_t* __restrict__ keep) {
   const int64_t k = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (k >= n) return;
   int in_family = 0;
-  for (int j = 1; j < 8; ++j)
+  for (int j = 1; j < fam; ++j)
     if (k - j >= 0 && start[k - j]) in_family = 1;
   keep[k] = in_family ? 0 : 1;
 }
@@ -124,9 +125,10 @@ cudaError_t build_node_levels(rc_forest* f, cudaStream_t s) {
     NodeView V{f->d_tree, f->d_anchor, f->d_level, nullptr};
     int64_t cur = n;
     int out = 0;
+    const int fam = f->surface ? 4 : 8;   // complete sibling families
     for (int c = 1; c <= RC_NODE_LEVELS; ++c) {
-      k_family_start<<<nb(cur, 256), 256, 0, s>>>(V, cur, start);
-      k_family_keep<<<nb(cur, 256), 256, 0, s>>>(start, cur, keep);
+      k_family_start<<<nb(cur, 256), 256, 0, s>>>(V, cur, fam, start);
+      k_family_keep<<<nb(cur, 256), 256, 0, s>>>(start, cur, fam, keep);
       g_launches += 2;
       TRY(scan_exclusive<int32_t>(keep, pos, cur, f->d_scan_tmp, s));
       int64_t next = 0;

@@ -40,7 +40,7 @@ rc_status rc_fail(rc_status st, const char* fmt, ...) {
 #define LAUNCHED() (++g_launches)
 
 extern "C" const char* rc_last_error(void) { return g_err; }
-extern "C" int32_t rc_version(void) { return 2; }
+extern "C" int32_t rc_version(void) { return 3; }
 extern "C" int64_t rc_launch_count(int32_t reset) {
   int64_t v = g_launches;
   if (reset) g_launches = 0;
@@ -72,6 +72,10 @@ extern "C" rc_status rc_forest_create(const rc_forest_desc* d, void* stream, rc_
   if (!d || !out) return fail(RC_ERR_INVALID_ARG, "rc_forest_create: null argument");
   *out = nullptr;
   if (d->num_trees < 1 || d->num_trees > RC_MAX_TREES) return fail(RC_ERR_INVALID_ARG, "num_trees out of range");
+  if (d->dim != 0 && d->dim != 2 && d->dim != 3) return fail(RC_ERR_INVALID_ARG, "dim must be 0, 2 or 3");
+  const bool surface = d->dim == 2;
+  if (surface && (d->geom_degree != 1 || d->field_degree != 1))
+    return fail(RC_ERR_INVALID_ARG, "surface forests take geom_degree = field_degree = 1 (bilinear patches)");
   if (d->geom_degree < 1 || d->geom_degree > 2) return fail(RC_ERR_INVALID_ARG, "geom_degree must be 1 or 2");
   if (d->field_degree < 1 || d->field_degree > 2) return fail(RC_ERR_INVALID_ARG, "field_degree must be 1 or 2");
   if (d->num_leaves < 1 || d->num_leaves > (int64_t)INT32_MAX) return fail(RC_ERR_INVALID_ARG, "num_leaves out of range");
@@ -83,9 +87,10 @@ extern "C" rc_status rc_forest_create(const rc_forest_desc* d, void* stream, rc_
     return fail(RC_ERR_INVALID_ARG, "global leaf index must fit 32 bits");
   cudaStream_t s = (cudaStream_t)stream;
   const int64_t n = d->num_leaves;
-  const int NF = (d->field_degree + 1) * (d->field_degree + 1) * (d->field_degree + 1);
+  const int NF = surface ? 4 : (d->field_degree + 1) * (d->field_degree + 1) * (d->field_degree + 1);
   int n1 = d->geom_degree + 1;
-  for (int q = 0; q < d->num_trees * n1 * n1 * n1 * 3; ++q)
+  const int nctrl = surface ? 12 : n1 * n1 * n1 * 3;   // doubles per tree
+  for (int q = 0; q < d->num_trees * nctrl; ++q)
     if (!isfinite(d->tree_ctrl[q])) return fail(RC_ERR_NUMERIC, "non-finite control point");
   if (d->memory == RC_HOST_COPY) {
     // strict SFC order: (tree, Morton key) increasing; anchors aligned to their level
@@ -100,6 +105,7 @@ extern "C" rc_status rc_forest_create(const rc_forest_desc* d, void* stream, rc_
       for (int k = 0; k < 3; ++k)
         if (a[k] < 0 || a[k] >= (1 << RC_MAXLEVEL) || ((uint32_t)a[k] & mask))
           return fail(RC_ERR_INVALID_ARG, "leaf %lld: anchor not aligned to its level", (long long)e);
+      if (surface && a[2] != 0) return fail(RC_ERR_INVALID_ARG, "leaf %lld: quadtree leaf with z anchor != 0", (long long)e);
       uint64_t key = spread18(a[0]) | (spread18(a[1]) << 1) | (spread18(a[2]) << 2);
       if (t < prev_tree || (t == prev_tree && key <= prev_key))
         return fail(RC_ERR_NOT_SFC_SORTED, "leaf %lld breaks SFC order", (long long)e);
@@ -119,6 +125,8 @@ extern "C" rc_status rc_forest_create(const rc_forest_desc* d, void* stream, rc_
   f->first_global = d->first_global_leaf;
   f->transfer = d->transfer;
   f->has_field = d->leaf_field != nullptr;
+  f->surface = surface;
+  if (surface) f->surf = d->surface;
   f->h_trees = new TreeConst[f->K];
   memset(f->h_trees, 0, sizeof(TreeConst) * f->K);
   cudaError_t e = cudaSuccess;
@@ -155,7 +163,7 @@ extern "C" rc_status rc_forest_create(const rc_forest_desc* d, void* stream, rc_
     return cleanup(RC_ERR_CUDA, "cudaMemcpyAsync leaves");
   // host copy of the tree control points for rc_camera_set
   for (int k = 0; k < f->K; ++k)
-    memcpy(f->h_trees[k].lagr, d->tree_ctrl + (size_t)k * n1 * n1 * n1 * 3, sizeof(double) * n1 * n1 * n1 * 3);
+    memcpy(f->h_trees[k].lagr, d->tree_ctrl + (size_t)k * nctrl, sizeof(double) * nctrl);
   if ((e = cudaEventCreate(&f->ev0)) || (e = cudaEventCreate(&f->ev1))) return cleanup(RC_ERR_CUDA, "event");
   for (int k = 0; k < 3; ++k)
     if ((e = cudaEventCreate(&f->evc[k]))) return cleanup(RC_ERR_CUDA, "event");
@@ -172,7 +180,7 @@ extern "C" rc_status rc_forest_destroy(rc_forest* f) {
                   f->d_vis, f->d_vis_rect, f->d_chunk_off, f->d_counters, f->d_trees, f->d_cam,
                   f->d_scan_tmp, f->d_chunk_elem, f->d_segs, f->d_hits_pp, f->d_pix_cnt, f->d_pix_off,
                   f->d_perm, f->d_send, f->d_items, f->d_leaf_nodes[0], f->d_leaf_nodes[1], f->d_ucnt, f->d_uend, f->d_units,
-                  f->d_scratch, f->d_segs2, f->d_uoff, f->d_defer, f->d_sorted, f->d_tiles, f->d_xcnt, f->d_recv, f->d_gslot};
+                  f->d_scratch, f->d_segs2, f->d_uoff, f->d_defer, f->d_sorted, f->d_tiles, f->d_xcnt, f->d_recv, f->d_gslot, f->d_boff};
   for (void* p : ptrs)
     if (p) dfree(p, 0, true);
   for (int c = 0; c <= RC_NODE_LEVELS; ++c)
@@ -341,6 +349,27 @@ extern "C" rc_status rc_camera_set(rc_forest* f, const rc_camera* cam, void* str
   c.inv_F = f->transfer.inv_F;
   c.q0 = f->transfer.q0;
 
+  c.surf = f->surf;
+  if (f->surface) {   // bilinear patches: world and camera-space corners [m2][m1][xyz]
+    f->all_affine = 0;
+    for (int k = 0; k < f->K; ++k) {
+      TreeConst& T = f->h_trees[k];
+      T.affine = 0;
+      memcpy(T.Bw, T.lagr, sizeof(double) * 12);
+      for (int m = 0; m < 4; ++m)
+        for (int r = 0; r < 3; ++r) {
+          double acc = 0.0;
+          for (int q = 0; q < 3; ++q) acc += c.cam_rot[3 * r + q] * (T.lagr[3 * m + q] - c.cam_org[q]);
+          T.Bc[3 * m + r] = acc;
+        }
+    }
+    CU(cudaMemcpyAsync(f->d_trees, f->h_trees, sizeof(TreeConst) * f->K, cudaMemcpyHostToDevice, s));
+    CU(cudaMemcpyAsync(f->d_cam, &f->cc, sizeof(CamConst), cudaMemcpyHostToDevice, s));
+    CU(cudaStreamSynchronize(s));
+    f->have_camera = true;
+    f->have_cull = f->have_cast = false;
+    return RC_OK;
+  }
   // per tree: affine detection, affine ray constants, Bernstein points
   const int R = f->R, n1 = R + 1, NP = n1 * n1 * n1;
   const double eta2[3] = {0.0, 0.5, 1.0};
@@ -443,7 +472,8 @@ extern "C" rc_status rc_cull(rc_forest* f, void* stream, int64_t* d_num_visible)
   cudaStream_t s = (cudaStream_t)stream;
   const int64_t n = f->n;
   DevLeafView L = leaf_view(f);
-  CU(launch_cull(f->cc, f->d_trees, L, n, f->R, f->all_affine != 0, f->d_flag, f->d_rect_all, s));
+  if (f->surface) CU(launch_cull_surface(f->cc, f->d_trees, L, n, f->d_flag, f->d_rect_all, s));
+  else CU(launch_cull(f->cc, f->d_trees, L, n, f->R, f->all_affine != 0, f->d_flag, f->d_rect_all, s));
   CU(scan_exclusive<int32_t>(f->d_flag, f->d_scan, n, f->d_scan_tmp, s));
   CU(launch_compact(f->d_flag, f->d_rect_all, f->d_scan, n, f->d_vis, f->d_vis_rect, s));
   // pair generation: chunk counts over all n slots (entries >= nvis are 0)
@@ -503,7 +533,7 @@ extern "C" rc_status rc_cast_segments(rc_forest* f, int32_t fold_levels, void* s
   if (!f->has_field) return fail(RC_ERR_STATE, "rc_cast_segments on a forest without a field (keys only)");
   if (fold_levels < 0 || fold_levels > RC_NODE_LEVELS)
     return fail(RC_ERR_INVALID_ARG, "fold_levels must be in [0, %d]", RC_NODE_LEVELS);
-  if (!f->all_affine && f->R != 2) return fail(RC_ERR_INVALID_ARG, "non-affine trees require geom_degree 2");
+  if (!f->all_affine && !f->surface && f->R != 2) return fail(RC_ERR_INVALID_ARG, "non-affine trees require geom_degree 2");
   cudaStream_t s = (cudaStream_t)stream;
   const int64_t n = f->n;
   // one small readback to size the chunk map, the units and the record buffer
@@ -520,7 +550,7 @@ extern "C" rc_status rc_cast_segments(rc_forest* f, int32_t fold_levels, void* s
   CU(grow(&f->d_chunk_elem, &f->chunk_cap, std::max<int64_t>(f->h_chunks, 1), s));
   CU(grow(&f->d_hits_pp, &f->pix_cap, npix, s));
   if (nvis > 0) CU(launch_expand(f->d_chunk_off, f->d_scan + n, nvis, f->d_chunk_elem, s));
-  const bool curved = !f->all_affine;
+  const bool curved = !f->all_affine && !f->surface;
   const uint32_t key_base = (uint32_t)f->first_global;
   // fold units (curved path): the visible leaves of every node of the fold
   // level (64-leaf windows without folding) cut into <= 64 leaves and
@@ -599,7 +629,11 @@ extern "C" rc_status rc_cast_segments(rc_forest* f, int32_t fold_levels, void* s
     CU(cudaMemsetAsync(f->d_counters + CNT_DEPTH_CAP, 0, sizeof(int64_t), s));
     CU(cudaEventRecord(f->ev0, s));
     if (f->h_chunks > 0) {
-      if (!curved) {
+      if (f->surface) {
+        CU(launch_cast_surface(f->cc, f->d_trees, leaf_view(f), f->d_vis, f->d_vis_rect, f->d_chunk_off,
+                               f->d_chunk_elem, f->h_chunks, key_base, f->d_segs, f->seg_cap, f->d_hits_pp,
+                               f->d_counters, sm_count() * 8, s));
+      } else if (!curved) {
         CU(launch_cast_affine(f->cc, f->d_trees, leaf_view(f), f->P, f->d_vis, f->d_vis_rect, f->d_chunk_off,
                               f->d_chunk_elem, f->h_chunks, key_base, f->d_segs, f->seg_cap, f->d_hits_pp,
                               f->d_counters, sm_count() * 8, s));
@@ -634,7 +668,7 @@ extern "C" rc_status rc_cast_segments(rc_forest* f, int32_t fold_levels, void* s
   f->phase_ms[1] = ms;
   f->phase_ms[2] = 0.0f;
   f->rec_level = 0;
-  if (!curved) f->h_raw_affine = f->h_seg_total;
+  if (!curved) f->h_raw_affine = f->h_seg_total;   // affine and surface kernels write unfolded records
   f->timed = true;
   f->have_cast = true;
   if (curved) {
@@ -683,7 +717,7 @@ extern "C" rc_status rc_segments_get(rc_forest* f, rc_segments* out, void* strea
   out->newton_failures = c[CNT_NEWTON_FAIL];
   out->face_failures = c[CNT_FACE_FAIL];
   out->num_visible = f->h_num_visible;
-  out->raw_segments = f->all_affine ? f->h_raw_affine : c[CNT_RAW];
+  out->raw_segments = (f->all_affine || f->surface) ? f->h_raw_affine : c[CNT_RAW];
   out->level = f->rec_level;
   out->units = f->h_units;
   out->unfolded_units = c[CNT_UNFOLDED];
@@ -781,7 +815,7 @@ extern "C" rc_status rc_composite_records(rc_forest* f, const rc_tiling* t, cons
     if (f->d_pix_off) dfree(f->d_pix_off, s);
     f->d_pix_cnt = nullptr;
     f->d_pix_off = nullptr;
-    CU(dmalloc((void**)&f->d_pix_cnt, sizeof(int32_t) * npix, s));
+    CU(dmalloc((void**)&f->d_pix_cnt, sizeof(int32_t) * (npix + 2), s));   // also the band counts (<= npix/64 + 1)
     CU(dmalloc((void**)&f->d_pix_off, sizeof(int64_t) * (npix + 1), s));
     f->pix_cnt_cap = npix;
   }
@@ -909,7 +943,7 @@ static rc_status aggregate_to(rc_forest* f, int level, cudaStream_t s) {
     if (f->d_pix_off) dfree(f->d_pix_off, s);
     f->d_pix_cnt = nullptr;
     f->d_pix_off = nullptr;
-    CU(dmalloc((void**)&f->d_pix_cnt, sizeof(int32_t) * npix, s));
+    CU(dmalloc((void**)&f->d_pix_cnt, sizeof(int32_t) * (npix + 2), s));   // also the band counts (<= npix/64 + 1)
     CU(dmalloc((void**)&f->d_pix_off, sizeof(int64_t) * (npix + 1), s));
     f->pix_cnt_cap = npix;
   }
@@ -917,25 +951,28 @@ static rc_status aggregate_to(rc_forest* f, int level, cudaStream_t s) {
   if (need_tmp > f->scan_tmp_cap) CU(grow(&f->d_scan_tmp, &f->scan_tmp_cap, need_tmp, s));
   CU(grow(&f->d_perm, &f->perm_cap, std::max<int64_t>(nrec, 1), s));
   const int grid = sm_count() * 8;
-  CU(cudaMemsetAsync(f->d_pix_cnt, 0, sizeof(int32_t) * npix, s));
-  if (nrec > 0) CU(launch_hist(f->d_segs, nrec, f->d_pix_cnt, grid, s));
-  CU(scan_exclusive<int32_t>(f->d_pix_cnt, f->d_pix_off, npix, f->d_scan_tmp, s));
-  CU(cudaMemsetAsync(f->d_pix_cnt, 0, sizeof(int32_t) * npix, s));
-  if (nrec > 0) CU(launch_scatter(f->d_segs, nrec, f->d_pix_off, f->d_pix_cnt, f->d_perm, grid, s));
-  CU(grow(&f->d_defer, &f->defer_cap, std::max<int64_t>(npix, 1), s));   // pixels with > 512 records
-  const int32_t* leaf_node = nullptr;   // node of every leaf at the target level
-  CU(build_leaf_node(f, level, s, &leaf_node));
   // output buffer: half the input first for one cycle, a quarter for several
   // (a cycle roughly halves the count), grown to the exact
-  // count and the pass repeated if short
+  // count and the pass repeated if short; before the pass it holds the
+  // bucketing's scratch indices (>= 4 bytes per input record)
   int64_t want = std::max<int64_t>(nrec / (level - f->rec_level >= 2 ? 4 : 2) + 4096, 1);
+  CU(grow(&f->d_segs2, &f->seg2_cap, want, s));
+  const int64_t nbands = (npix + 63) / 64;
+  if (f->boff_cap < nbands + 1) CU(grow(&f->d_boff, &f->boff_cap, nbands + 1, s));
+  CU(launch_band_bucket(f->d_segs, nrec, npix, f->d_pix_cnt, f->d_boff, f->d_scan_tmp,
+                        reinterpret_cast<uint32_t*>(f->d_segs2), f->d_perm, f->d_pix_off, grid, s));
+  // pixels deferred to the list pass [0, npix) and pixels of the mid pass (256 < n <= 512) [npix, 2 npix)
+  CU(grow(&f->d_defer, &f->defer_cap, std::max<int64_t>(2 * npix, 1), s));
+  const int32_t* leaf_node = nullptr;   // node of every leaf at the target level
+  CU(build_leaf_node(f, level, s, &leaf_node));
   int64_t nout = 0;
   for (int attempt = 0; attempt < 2; ++attempt) {
     CU(grow(&f->d_segs2, &f->seg2_cap, want, s));
     CU(cudaMemsetAsync(f->d_counters + CNT_AGG_OUT, 0, sizeof(int64_t), s));
     CU(cudaMemsetAsync(f->d_counters + CNT_OVERFLOW, 0, sizeof(int64_t), s));
     CU(launch_coarsen(f->d_segs, f->d_perm, f->d_pix_off, npix, f->d_node_first[level], leaf_node,
-                      (uint32_t)f->first_global, 1e-6f, f->d_segs2, f->seg2_cap, f->d_defer, f->d_counters,
+                      (uint32_t)f->first_global, 1e-6f, f->d_segs2, f->seg2_cap, f->d_defer, f->d_defer + npix,
+                      f->d_counters,
                       sm_count() * 16, s));
     CU(cudaMemcpyAsync(&nout, f->d_counters + CNT_AGG_OUT, sizeof(int64_t), cudaMemcpyDeviceToHost, s));
     CU(cudaStreamSynchronize(s));
@@ -988,6 +1025,7 @@ extern "C" rc_status rc_debug_pair(rc_forest* f, int64_t local_leaf, int32_t i, 
     return fail(RC_ERR_INVALID_ARG, "rc_debug_pair: leaf or pixel out of range");
   if (!f->all_affine && f->R != 2) return fail(RC_ERR_INVALID_ARG, "non-affine trees require geom_degree 2");
   if (!f->has_field) return fail(RC_ERR_STATE, "rc_debug_pair on a forest without a field (keys only)");
+  if (f->surface) return fail(RC_ERR_INVALID_ARG, "rc_debug_pair: surface forests are not supported");
   cudaStream_t s = (cudaStream_t)stream;
   const bool curved = !f->all_affine;
   // a one-leaf, one-pixel work list through the frame's own segment kernel (fold level 0)

@@ -55,6 +55,7 @@ struct CamConst {
   int scheme;                   // RC_SCHEME_* (segment integrator)
   int max_depth;                // Alg. 1 recursion cap
   float c_rk;                   // Alg. 1 threshold (0: no recursion)
+  rc_surface surf;              // surface forests: transfer of the corner-interpolated value
 };
 
 // Per-tree constants (device buffer, warp-uniform reads).
@@ -87,6 +88,8 @@ struct rc_forest {
   int K, R, P;
   int64_t n, first_global;
   bool has_field = true;           // false: keys-only forest (aggregation / partition bookkeeping)
+  bool surface = false;            // dim = 2: quadtree leaves on bilinear patches (surface.cu)
+  rc_surface surf{};
   rc_transfer transfer;
   // device leaves
   int32_t* d_anchor = nullptr;
@@ -162,6 +165,8 @@ struct rc_forest {
   size_t scratch_bytes = 0;
   // aggregation output (ping-pong with d_segs)
   int32_t* d_defer = nullptr;      // composite: deferred pixels [w*h]
+  int64_t* d_boff = nullptr;       // aggregation: band offsets of the banded pixel bucketing
+  int64_t boff_cap = 0;
   int32_t* d_tiles = nullptr;      // composite: this rank's tile ids (uploaded when the tiling changes)
   int32_t* h_tiles = nullptr;      // pinned staging of d_tiles
   int64_t tiles_cap = 0, h_tiles_cap = 0;
@@ -201,6 +206,7 @@ enum {
   CNT_DEFER = 78,      // composite: pixels deferred to the large-pixel pass
   CNT_BIGPIX = 79,     // composite: pixels with more records than FOLD_CAP_LIST (written as NaN)
   CNT_DEPTH_CAP = 80,  // Alg. 1 steps taken at the recursion cap (must be 0)
+  CNT_MID = 81,        // aggregation: pixels with 256 < n <= 512 records (second fast pass)
   CNT_TOTAL = 96
 };
 

@@ -32,11 +32,16 @@ class Transfer(C.Structure):
     _fields_ = [("kappa0", C.c_float), ("inv_F", C.c_float), ("q0", C.c_float)]
 
 
+class SurfaceTransfer(C.Structure):
+    _fields_ = [("a", C.c_float * 2), ("i", C.c_float * 9), ("k", C.c_float)]
+
+
 class ForestDesc(C.Structure):
     _fields_ = [("num_trees", C.c_int32), ("geom_degree", C.c_int32), ("tree_ctrl", C.c_void_p),
                 ("field_degree", C.c_int32), ("num_leaves", C.c_int64), ("first_global_leaf", C.c_int64),
                 ("leaf_anchor", C.c_void_p), ("leaf_tree", C.c_void_p), ("leaf_level", C.c_void_p),
-                ("leaf_field", C.c_void_p), ("memory", C.c_int32), ("transfer", Transfer)]
+                ("leaf_field", C.c_void_p), ("memory", C.c_int32), ("transfer", Transfer), ("dim", C.c_int32),
+                ("surface", SurfaceTransfer)]
 
 
 class CameraDesc(C.Structure):
@@ -180,7 +185,7 @@ class Forest:
     (device copy); they are copied by rc_forest_create."""
 
     def __init__(self, tree_ctrl, geom_degree, field_degree, leaf_anchor, leaf_tree, leaf_level, leaf_field,
-                 kappa0, inv_F, q0, first_global_leaf=0, stream=None, trusted=False):
+                 kappa0, inv_F, q0, first_global_leaf=0, stream=None, trusted=False, dim=3, surface=None):
         import torch
         L = lib()
         ctrl = np.ascontiguousarray(tree_ctrl if isinstance(tree_ctrl, np.ndarray) else tree_ctrl.cpu().numpy(),
@@ -207,7 +212,13 @@ class Forest:
         self.R = int(geom_degree)
         desc = ForestDesc(int(ctrl.shape[0]), int(geom_degree), ctrl.ctypes.data, int(field_degree), n,
                           int(first_global_leaf), ptrs[0], ptrs[1], ptrs[2], ptrs[3] or None, mem,
-                          Transfer(float(kappa0), float(inv_F), float(q0)))
+                          Transfer(float(kappa0), float(inv_F), float(q0)), int(dim))
+        if int(dim) == 2:   # surface forest: (a0, a1, ((i0, i1, i2) x 3), k)
+            a0, a1, ii, k = surface
+            desc.surface.a[:] = [float(a0), float(a1)]
+            desc.surface.i[:] = [float(x) for row in ii for x in row]
+            desc.surface.k = float(k)
+        self.surface = int(dim) == 2
         h = C.c_void_p()
         _check(L.rc_forest_create(C.byref(desc), _stream(stream), C.byref(h)))
         self.h = h
@@ -223,7 +234,8 @@ class Forest:
         if device_copy:
             arrs = [torch.as_tensor(np.ascontiguousarray(a) if isinstance(a, np.ndarray) else a).cuda() for a in arrs]
         return cls(scene.tree_ctrl, scene.geom_degree, scene.field_degree, *arrs, scene.kappa0, scene.inv_F,
-                   scene.q0, first_global_leaf=first, stream=stream)
+                   scene.q0, first_global_leaf=first, stream=stream, dim=getattr(scene, "dim", 3),
+                   surface=getattr(scene, "surface", None))
 
     def close(self):
         if getattr(self, "h", None):

@@ -54,6 +54,20 @@ __global__ void k_fmnmx(float* out, float a, float b) {
   if (s == 1234.5f) out[threadIdx.x] = s;
 }
 
+__global__ void k_dfma(double* out, double a, double b) {   // FP64 pipe (surface kernel's geometry)
+  double x[CH];
+#pragma unroll
+  for (int c = 0; c < CH; ++c) x[c] = threadIdx.x * 1e-3 + c;
+#pragma unroll 32
+  for (int i = 0; i < ITERS / 4; ++i)
+#pragma unroll
+    for (int c = 0; c < CH; ++c) asm volatile("fma.rn.f64 %0, %0, %1, %2;" : "+d"(x[c]) : "d"(a), "d"(b));
+  double s = 0.0;
+#pragma unroll
+  for (int c = 0; c < CH; ++c) s += x[c];
+  if (s == 1234.5) out[threadIdx.x] = s;
+}
+
 template <class F>
 static double run(F launch, double insts_per_thread, int blocks, int threads) {
   cudaEvent_t e0, e1;
@@ -87,8 +101,11 @@ int main() {
   const double ex2 = run([&] { k_ex2<<<blocks, threads>>>(out); }, (double)ITERS * CH, blocks, threads);
   const double mnx = run([&] { k_fmnmx<<<blocks, threads>>>(out, 1e3f, -1e3f); }, (double)ITERS * CH * 2, blocks,
                          threads);
+  const double dfma = run([&] { k_dfma<<<blocks, threads>>>(reinterpret_cast<double*>(out), 0.999, 1e-4); },
+                          (double)(ITERS / 4) * CH, blocks, threads);
   cudaError_t e = cudaGetLastError();
-  printf("{\"sms\": %d, \"clock_attr_mhz\": %.0f, \"ffma_ginst_s\": %.1f, \"ffma_tflops\": %.2f, "
+  printf("{\"dfma_ginst_s\": %.1f, \"dfma_tflops\": %.3f, ", dfma, 2 * dfma / 1000.0);
+  printf("\"sms\": %d, \"clock_attr_mhz\": %.0f, \"ffma_ginst_s\": %.1f, \"ffma_tflops\": %.2f, "
          "\"mufu_ex2_ginst_s\": %.1f, \"mufu_ex2_tops\": %.3f, \"fmnmx_ginst_s\": %.1f, \"fmnmx_tops\": %.3f, "
          "\"per_sm_per_clk_at_attr\": {\"ffma\": %.1f, \"ex2\": %.2f, \"fmnmx\": %.1f}, \"error\": \"%s\"}\n",
          sms, clk / 1000.0, ffma, 2 * ffma / 1000.0, ex2, ex2 / 1000.0, mnx, mnx / 1000.0,

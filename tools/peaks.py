@@ -21,7 +21,7 @@ if __name__ == "__main__":
     line = json.loads(r.stdout.strip().splitlines()[-1])
     line["clocks"] = clk.summary()
     line["how"] = ("tools/peaks.cu: 8 independent chains per thread of fma.rn.f32 / ex2.approx.ftz.f32 / "
-                   "min.f32+max.f32, 512 threads x 4 CTAs per SM on all SMs, ~10 ms launches, best of 20 (CUDA events)")
+                   "min.f32+max.f32 (and fma.rn.f64 at 1/4 the iterations), 512 threads x 4 CTAs per SM on all SMs, ~10 ms launches, best of 20 (CUDA events)")
     line["when"] = datetime.datetime.utcnow().strftime("%Y-%m-%dT%H:%M:%SZ")
     out = sys.argv[1] if len(sys.argv) > 1 else os.path.join(ROOT, "profiles", "peaks_r02.json")
     json.dump(line, open(out, "w"), indent=1)
