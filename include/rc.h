@@ -333,7 +333,11 @@ float rc_last_cast_ms(rc_forest* f);
  * phase 3 = diagnostic of the last composite: 1 if it sorted a pixel-bucketed
  * copy of the records, 0 if it gathered them through a permutation;
  * phase 4 / 5 = device time of the last composite's pixel bucketing (k_hist,
- * scan, scatter) / per-pixel fold kernels (k_fold), -1 before any composite. */
+ * scan, scatter) / per-pixel fold kernels (k_fold), -1 before any composite;
+ * phase 6 / 7 = summed device time of the last rc_cast_segments' segment
+ * kernel launches alone / of its element-preparation launches (curved forests:
+ * k_prep_slots per batch; 0 otherwise), events around each launch, -1 when
+ * not measured. */
 float rc_last_phase_ms(rc_forest* f, int32_t phase);
 
 #ifdef __cplusplus

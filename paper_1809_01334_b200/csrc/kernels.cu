@@ -491,7 +491,7 @@ __global__ void k_scatter(const rc_seg* __restrict__ segs, int64_t n, const int6
 // 32 pixels are one chunk of one leaf's rectangle row), (3) one CTA per band
 // counts its pixels in shared memory, writes their offsets and places the
 // indices within the band's range (an L2-resident window).
-constexpr int BAND_SH = 6;   // 64 pixels per band
+constexpr int BAND_SH = 5;   // 32 pixels per band (the scan in k_band_sort assumes 32)
 constexpr int BAND_SMEM = 9216;    // entries cached in shared memory per band (index + local pixel; static smem < 48 KB)
 
 __device__ __forceinline__ unsigned lanemask_lt() {
@@ -512,22 +512,28 @@ __global__ void k_band_count(const rc_seg* __restrict__ segs, int64_t n, int32_t
 }
 
 __global__ void k_band_scatter(const rc_seg* __restrict__ segs, int64_t n, const int64_t* __restrict__ boff,
-                               int32_t* __restrict__ bcur, uint32_t* __restrict__ tmp) {
+                               int32_t* __restrict__ bcur, uint64_t* __restrict__ tmp) {
   const unsigned lane = threadIdx.x & 31;
   const int64_t stride = (int64_t)gridDim.x * blockDim.x;
   for (int64_t base = (int64_t)blockIdx.x * blockDim.x + (threadIdx.x & ~31u); base < n; base += stride) {
     const int64_t s = base + lane;
-    const int b = s < n ? (int)(__ldcs(&segs[s].pixel) >> BAND_SH) : -1;
+    const uint32_t pix = s < n ? __ldcs(&segs[s].pixel) : 0u;
+    const int b = s < n ? (int)(pix >> BAND_SH) : -1;
     const unsigned m = __match_any_sync(0xffffffffu, b);
     const int leader = __ffs(m) - 1;
     int first = 0;
     if (b >= 0 && (int)lane == leader) first = atomicAdd(&bcur[b], __popc(m));
     first = __shfl_sync(0xffffffffu, first, leader);
-    if (b >= 0) tmp[boff[b] + first + __popc(m & lanemask_lt())] = (uint32_t)s;
+    if (b >= 0) {
+      // index and band-local pixel in one 8-byte entry (full-sector runs; no gather in k_band_sort)
+      const int64_t slot = boff[b] + first + __popc(m & lanemask_lt());
+      RC_DCHECK(slot < boff[b + 1]);
+      tmp[slot] = ((uint64_t)(pix & ((1u << BAND_SH) - 1)) << 32) | (uint64_t)(uint32_t)s;
+    }
   }
 }
 
-__global__ void __launch_bounds__(512) k_band_sort(const rc_seg* __restrict__ segs, const uint32_t* __restrict__ tmp,
+__global__ void __launch_bounds__(512) k_band_sort(const uint64_t* __restrict__ tmp,
                                                    const int64_t* __restrict__ boff, int64_t nbands, int64_t npix,
                                                    uint32_t* __restrict__ perm, int64_t* __restrict__ off) {
   __shared__ int32_t hist[1 << BAND_SH];
@@ -539,8 +545,9 @@ __global__ void __launch_bounds__(512) k_band_sort(const rc_seg* __restrict__ se
     if (threadIdx.x < NB) hist[threadIdx.x] = 0;
     __syncthreads();
     for (int64_t i = threadIdx.x; i < ne; i += blockDim.x) {
-      const uint32_t sidx_i = tmp[e0 + i];
-      const int p = (int)(segs[sidx_i].pixel & (NB - 1));
+      const uint64_t t = tmp[e0 + i];
+      const uint32_t sidx_i = (uint32_t)t;
+      const int p = (int)(t >> 32);
       if (i < BAND_SMEM) {
         sidx[i] = sidx_i;
         spix[i] = (uint8_t)p;
@@ -548,21 +555,18 @@ __global__ void __launch_bounds__(512) k_band_sort(const rc_seg* __restrict__ se
       atomicAdd(&hist[p], 1);
     }
     __syncthreads();
-    if (threadIdx.x < 32) {   // exclusive scan of the NB counts (NB = 64: two per lane)
+    if (threadIdx.x < 32) {   // exclusive scan of the NB = 32 counts, one per lane
       const int lane = threadIdx.x;
-      const int c0 = hist[2 * lane], c1 = hist[2 * lane + 1];
-      int incl = c0 + c1;
+      const int c0 = hist[lane];
+      int incl = c0;
 #pragma unroll
       for (int o = 1; o < 32; o <<= 1) {
         const int y = __shfl_up_sync(0xffffffffu, incl, o);
         if (lane >= o) incl += y;
       }
-      const int ex = incl - c0 - c1;
-      hist[2 * lane] = ex;
-      hist[2 * lane + 1] = ex + c0;
-      const int64_t p0 = b * NB + 2 * lane;
-      if (p0 < npix) off[p0] = e0 + ex;
-      if (p0 + 1 < npix) off[p0 + 1] = e0 + ex + c0;
+      hist[lane] = incl - c0;
+      const int64_t p0 = b * NB + lane;
+      if (p0 < npix) off[p0] = e0 + incl - c0;
     }
     __syncthreads();
     for (int64_t i = threadIdx.x; i < ne; i += blockDim.x) {
@@ -572,10 +576,13 @@ __global__ void __launch_bounds__(512) k_band_sort(const rc_seg* __restrict__ se
         sidx_i = sidx[i];
         p = spix[i];
       } else {
-        sidx_i = tmp[e0 + i];
-        p = (int)(segs[sidx_i].pixel & (NB - 1));
+        const uint64_t t = tmp[e0 + i];
+        sidx_i = (uint32_t)t;
+        p = (int)(t >> 32);
       }
-      perm[e0 + atomicAdd(&hist[p], 1)] = sidx_i;
+      const int pos = atomicAdd(&hist[p], 1);
+      RC_DCHECK(p < NB && pos < ne);
+      perm[e0 + pos] = sidx_i;
     }
     __syncthreads();
   }
@@ -594,6 +601,7 @@ __global__ void k_scatter_rec(const rc_seg* __restrict__ segs, int64_t n, const 
     const float4 lo = __ldcs(src), hi = __ldcs(src + 1);
     const uint32_t pix = __float_as_uint(lo.x);
     const int k = atomicAdd(&cursor[pix], 1);
+    RC_DCHECK(off[pix] + k < off[pix + 1]);
     float4* dst = reinterpret_cast<float4*>(out + off[pix] + k);
     dst[0] = lo;
     dst[1] = hi;
@@ -920,16 +928,57 @@ __global__ void __launch_bounds__(NW * 32, CAP <= 512 ? FOLD_MINB : 1) k_fold(
                    (size_t)warp * CAP;
   const int64_t tile_px = (int64_t)tw * th;
   const int64_t nq = FROM_LIST ? counters[CNT_DEFER] : npix_out;
-  for (int64_t qi = (int64_t)blockIdx.x * NW + warp; qi < nq; qi += (int64_t)gridDim.x * NW) {
-    const int64_t q = FROM_LIST ? (int64_t)defer[qi] : qi;
+  auto locate = [&](int64_t q) -> int64_t {   // output slot q -> image pixel
     const int t = (int)(q / tile_px);
     const int rem = (int)(q - (int64_t)t * tile_px);
     const int tile = my_tiles[t];
     const int tx = tile % tiles_x, ty = tile / tiles_x;
-    const int i = tx * tw + rem % tw, j = ty * th + rem / tw;
-    const int64_t pix = (int64_t)j * W + i;
-    const int64_t base = off[pix];
-    const int n = (int)(off[pix + 1] - base);
+    return (int64_t)(ty * th + rem / tw) * W + (tx * tw + rem % tw);
+  };
+  // 32 output pixels per warp step: a lane finishes its pixel alone when it
+  // has at most one record (no ordering needed); the others are folded one
+  // at a time by the whole warp below
+  const int64_t nsteps = FROM_LIST ? nq : (nq + 31) / 32;
+  for (int64_t st = (int64_t)blockIdx.x * NW + warp; st < nsteps; st += (int64_t)gridDim.x * NW) {
+    unsigned todo = 1u;
+    int64_t my_q = 0, my_pix = 0, my_base = 0;
+    int my_n = 0;
+    if (!FROM_LIST) {
+      my_q = st * 32 + lane;
+      if (my_q < nq) {
+        my_pix = locate(my_q);
+        my_base = off[my_pix];
+        my_n = (int)(off[my_pix + 1] - my_base);
+        if (my_n <= 1) {
+          Acc a1{1.0, 0.0, 0.0, 0.0};
+          if (my_n == 1) {
+            const rc_seg& r = recs[perm ? perm[my_base] : (uint32_t)my_base];
+            acc_push(a1, r.a, r.b[0], r.b[1], r.b[2]);
+          }
+          reinterpret_cast<float4*>(rgba)[my_q] =
+              make_float4((float)(a1.B0 + a1.A * bg0), (float)(a1.B1 + a1.A * bg1), (float)(a1.B2 + a1.A * bg2),
+                          (float)(1.0 - a1.A));
+        }
+      }
+      todo = __ballot_sync(0xffffffffu, my_q < nq && my_n > 1);
+    }
+  while (todo) {
+    const int src = __ffs(todo) - 1;
+    todo &= todo - 1;
+    int64_t q, pix, base;
+    int n;
+    if (FROM_LIST) {
+      q = (int64_t)defer[st];
+      pix = locate(q);
+      base = off[pix];
+      n = (int)(off[pix + 1] - base);
+    } else {
+      q = __shfl_sync(0xffffffffu, my_q, src);
+      pix = __shfl_sync(0xffffffffu, my_pix, src);
+      base = __shfl_sync(0xffffffffu, my_base, src);
+      n = __shfl_sync(0xffffffffu, my_n, src);
+    }
+    (void)pix;
     const uint32_t* S = perm ? perm + base : nullptr;   // S[k] = index of the pixel's k-th record (else contiguous copy)
     auto rec = [&](int k) -> const rc_seg& { return recs[S ? S[k] : (uint32_t)(base + k)]; };
     if (!FROM_LIST && n > CAP) {
@@ -967,6 +1016,7 @@ __global__ void __launch_bounds__(NW * 32, CAP <= 512 ? FOLD_MINB : 1) k_fold(
                                          (float)(acc.B2 + acc.A * bg2), (float)(1.0 - acc.A));
       reinterpret_cast<float4*>(rgba)[q] = o;
     }
+  }
   }
 }
 
@@ -1078,10 +1128,13 @@ __global__ void __launch_bounds__(FOLD_WARPS * 32, 1) k_coarsen_list(
 constexpr int COARSEN_FAST_CAP = 512;
 constexpr int COARSEN_MAIN_CAP = 256;   // main pass; 256 < n <= 512 go to a second pass over a list
 constexpr int COARSEN_FAST_WARPS = 2;
+struct Acc;
+__device__ __forceinline__ void acc_push(Acc& acc, double a, double b0, double b1, double b2);
 template <int CAP>
 struct CoarsenSmemT {                   // per warp, structure of arrays
   float an[CAP], af[CAP], a[CAP], b0[CAP], b1[CAP], b2[CAP];
   int32_t node[CAP];
+  __device__ __forceinline__ void push(Acc& x, uint32_t i) const { acc_push(x, a[i], b0[i], b1[i], b2[i]); }
 };
 
 // Warp bitonic sort of 32 E 32-bit keys in the blocked layout i = lane E + e,
@@ -1167,7 +1220,10 @@ __device__ __forceinline__ bool coarsen_pixel(const Smem& C, int n, int64_t pix,
   warp_sort32<E>(key);
   uint32_t id[E];
 #pragma unroll
-  for (int e = 0; e < E; ++e) id[e] = key[e] & 0x1FFu;
+  for (int e = 0; e < E; ++e) {
+    id[e] = key[e] & 0x1FFu;
+    RC_DCHECK((int)lane * E + e >= n || (int)id[e] < (list ? COARSEN_FAST_CAP : n));
+  }
   {
     uint32_t prev_key = __shfl_up_sync(0xffffffffu, key[E - 1], 1);
     bool tie = false;
@@ -1181,7 +1237,8 @@ __device__ __forceinline__ bool coarsen_pixel(const Smem& C, int n, int64_t pix,
     if (agree) {
       if (lane == 0) agree[threadIdx.x >> 5] = any ? 1 : 0;
       __syncthreads();
-      any = agree[0] | agree[1];
+      any = false;
+      for (int w = 0; w < (int)(blockDim.x >> 5); ++w) any |= agree[w] != 0;
       __syncthreads();
     }
     if (any) return false;
@@ -1215,7 +1272,7 @@ __device__ __forceinline__ bool coarsen_pixel(const Smem& C, int n, int64_t pix,
         HID = id[e];
         X = Acc{1.0, 0.0, 0.0, 0.0};
       }
-      acc_push(X, C.a[id[e]], C.b0[id[e]], C.b1[id[e]], C.b2[id[e]]);
+      C.push(X, id[e]);
     }
   }
   const int hi = min(n, lo + E);
@@ -1264,7 +1321,7 @@ __device__ __forceinline__ bool coarsen_pixel(const Smem& C, int n, int64_t pix,
         acc = Acc{1.0, 0.0, 0.0, 0.0};
         start_id = id[e];
       }
-      acc_push(acc, C.a[id[e]], C.b0[id[e]], C.b1[id[e]], C.b2[id[e]]);
+      C.push(acc, id[e]);
       last_id = id[e];
     }
   }
@@ -1277,7 +1334,8 @@ __device__ __forceinline__ bool coarsen_pixel(const Smem& C, int n, int64_t pix,
 // record gathers and the target-node lookups are separate loops (independent
 // loads in flight).
 __global__ void __launch_bounds__(COARSEN_FAST_WARPS * 32, 10) k_coarsen_fast(
-    const rc_seg* __restrict__ recs, const uint32_t* __restrict__ perm, const int64_t* __restrict__ off, int64_t npix,
+    const rc_seg* __restrict__ recs, int64_t nrec, int64_t nleaf, const uint32_t* __restrict__ perm,
+    const int64_t* __restrict__ off, int64_t npix,
     const int32_t* __restrict__ node_first, const int32_t* __restrict__ leaf_node, uint32_t key_base, float tau,
     rc_seg* __restrict__ out, int64_t out_cap, int32_t* __restrict__ defer, int32_t* __restrict__ mid,
     int64_t* __restrict__ counters) {
@@ -1303,6 +1361,7 @@ __global__ void __launch_bounds__(COARSEN_FAST_WARPS * 32, 10) k_coarsen_fast(
 #pragma unroll 4
     for (int k = lane; k < n; k += 32) {
       const uint32_t id = S[k];
+      RC_DCHECK((int64_t)id < nrec);
       const float4 lo = recs4[2 * (size_t)id], hi = recs4[2 * (size_t)id + 1];
       C.an[k] = lo.y;
       C.af[k] = lo.z;
@@ -1314,7 +1373,10 @@ __global__ void __launch_bounds__(COARSEN_FAST_WARPS * 32, 10) k_coarsen_fast(
     }
     // ... 2. and becomes its node at the target level (independent lookups)
 #pragma unroll 8
-    for (int k = lane; k < n; k += 32) C.node[k] = leaf_node[C.node[k]];
+    for (int k = lane; k < n; k += 32) {
+      RC_DCHECK(C.node[k] >= 0 && C.node[k] < nleaf);
+      C.node[k] = leaf_node[C.node[k]];
+    }
     __syncwarp();
     bool ok;
     if (n <= 64) ok = coarsen_pixel<2>(C, n, pix, node_first, key_base, tau, out, out_cap, counters);
@@ -1326,21 +1388,27 @@ __global__ void __launch_bounds__(COARSEN_FAST_WARPS * 32, 10) k_coarsen_fast(
 }
 
 // Mid pass: 256 < n <= 512.  Runs never cross target nodes, so the records
-// split into two independent groups by node parity: one CTA per pixel, warp
-// g folds group g (<= 256 records each, else the pixel is deferred) with the
-// main pass's warp code; the warps emit only if neither met a tie.
+// split into two independent groups by one bit of the node id (of the lowest
+// four, the one with the most even split): one CTA per pixel, warp g folds
+// group g (<= 256 records, else the pixel is deferred) with the main pass's
+// warp code; the warps emit only if neither met a tie (shared-memory flags
+// between CTA barriers).  (A/B at C5: this kernel 106 ms; four warps and
+// groups by node id mod 4 133 ms; a 16-byte layout re-reading (a, b) from
+// L1/L2 158 ms; one warp per (pixel, parity) with the main pass's layout
+// 132 ms + 20 ms more in the list pass.)
+constexpr int MID_WARPS = 2;
 struct CoarsenMidSmem {
   CoarsenSmemT<COARSEN_FAST_CAP> C;
-  uint16_t list[2][COARSEN_MAIN_CAP];
-  int ng[2];
-  int agree[2];
+  uint16_t list[MID_WARPS][COARSEN_MAIN_CAP];
+  int ng[MID_WARPS];
+  int agree[MID_WARPS];
 };
 
-__global__ void __launch_bounds__(64, 8) k_coarsen_mid(
-    const rc_seg* __restrict__ recs, const uint32_t* __restrict__ perm, const int64_t* __restrict__ off,
-    const int32_t* __restrict__ node_first, const int32_t* __restrict__ leaf_node, uint32_t key_base, float tau,
-    rc_seg* __restrict__ out, int64_t out_cap, int32_t* __restrict__ defer, const int32_t* __restrict__ mid,
-    int64_t* __restrict__ counters) {
+__global__ void __launch_bounds__(MID_WARPS * 32, 8) k_coarsen_mid(
+    const rc_seg* __restrict__ recs, int64_t nrec, int64_t nleaf, const uint32_t* __restrict__ perm,
+    const int64_t* __restrict__ off, const int32_t* __restrict__ node_first, const int32_t* __restrict__ leaf_node,
+    uint32_t key_base, float tau, rc_seg* __restrict__ out, int64_t out_cap, int32_t* __restrict__ defer,
+    const int32_t* __restrict__ mid, int64_t* __restrict__ counters) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
   CoarsenMidSmem& M = *reinterpret_cast<CoarsenMidSmem*>(smem_raw);
   CoarsenSmemT<COARSEN_FAST_CAP>& C = M.C;
@@ -1354,8 +1422,9 @@ __global__ void __launch_bounds__(64, 8) k_coarsen_mid(
     const int n = (int)(off[pix + 1] - base);
     const uint32_t* S = perm + base;
 #pragma unroll 4
-    for (int k = threadIdx.x; k < n; k += 64) {
+    for (int k = threadIdx.x; k < n; k += MID_WARPS * 32) {
       const uint32_t id = S[k];
+      RC_DCHECK((int64_t)id < nrec);
       const float4 lo = recs4[2 * (size_t)id], hi = recs4[2 * (size_t)id + 1];
       C.an[k] = lo.y;
       C.af[k] = lo.z;
@@ -1366,13 +1435,32 @@ __global__ void __launch_bounds__(64, 8) k_coarsen_mid(
       C.node[k] = (int32_t)(__float_as_uint(hi.w) - key_base);
     }
 #pragma unroll 8
-    for (int k = threadIdx.x; k < n; k += 64) C.node[k] = leaf_node[C.node[k]];
+    for (int k = threadIdx.x; k < n; k += MID_WARPS * 32) {
+      RC_DCHECK(C.node[k] >= 0 && C.node[k] < nleaf);
+      C.node[k] = leaf_node[C.node[k]];
+    }
     __syncthreads();
-    // warp g lists the records of group g (node parity), in index order
+    int c1[4] = {0, 0, 0, 0};
+    for (int k0 = 0; k0 < n; k0 += 32) {
+      const int k = k0 + (int)lane;
+      const int nd = k < n ? C.node[k] : 0;
+#pragma unroll
+      for (int bit = 0; bit < 4; ++bit) c1[bit] += __popc(__ballot_sync(0xffffffffu, k < n && ((nd >> bit) & 1)));
+    }
+    int sbit = 0, best = n;
+#pragma unroll
+    for (int bit = 0; bit < 4; ++bit) {
+      const int worst = max(c1[bit], n - c1[bit]);
+      if (worst < best) {
+        best = worst;
+        sbit = bit;
+      }
+    }
+    // warp g lists the records of group g, in index order
     int ng = 0;
     for (int k0 = 0; k0 < n; k0 += 32) {
       const int k = k0 + (int)lane;
-      const bool mine = k < n && (C.node[k] & 1) == warp;
+      const bool mine = k < n && ((C.node[k] >> sbit) & 1) == warp;
       const unsigned bal = __ballot_sync(0xffffffffu, mine);
       const int pos = ng + __popc(bal & lanemask_lt());
       if (mine && pos < COARSEN_MAIN_CAP) M.list[warp][pos] = (uint16_t)k;
@@ -1514,8 +1602,9 @@ cudaError_t launch_scatter(const rc_seg* segs, int64_t n, const int64_t* off, in
 }
 
 cudaError_t launch_band_bucket(const rc_seg* segs, int64_t n, int64_t npix, int32_t* bcnt, int64_t* boff,
-                               int64_t* scan_tmp, uint32_t* tmp, uint32_t* perm, int64_t* off, int grid,
+                               int64_t* scan_tmp, void* scratch, uint32_t* perm, int64_t* off, int grid,
                                cudaStream_t s) {
+  uint64_t* tmp = reinterpret_cast<uint64_t*>(scratch);
   const int64_t nb = (npix + (1 << BAND_SH) - 1) >> BAND_SH;
   cudaError_t e = cudaMemsetAsync(bcnt, 0, sizeof(int32_t) * (nb + 1), s);
   if (e != cudaSuccess) return e;
@@ -1524,7 +1613,7 @@ cudaError_t launch_band_bucket(const rc_seg* segs, int64_t n, int64_t npix, int3
   if (e == cudaSuccess) e = cudaMemsetAsync(bcnt, 0, sizeof(int32_t) * (nb + 1), s);   // reused as cursors
   if (e != cudaSuccess) return e;
   if (n > 0) k_band_scatter<<<grid, 256, 0, s>>>(segs, n, boff, bcnt, tmp);
-  k_band_sort<<<(unsigned)std::min<int64_t>(nb, 148 * 4), 512, 0, s>>>(segs, tmp, boff, nb, npix, perm, off);
+  k_band_sort<<<(unsigned)std::min<int64_t>(nb, 148 * 4), 512, 0, s>>>(tmp, boff, nb, npix, perm, off);
   g_launches += 3;
   return cudaGetLastError();
 }
@@ -1536,7 +1625,8 @@ cudaError_t launch_scatter_rec(const rc_seg* segs, int64_t n, const int64_t* off
   return cudaGetLastError();
 }
 
-cudaError_t launch_coarsen(const rc_seg* recs, const uint32_t* perm, const int64_t* off, int64_t npix,
+cudaError_t launch_coarsen(const rc_seg* recs, int64_t nrec, int64_t nleaf, const uint32_t* perm, const int64_t* off,
+                           int64_t npix,
                            const int32_t* node_first, const int32_t* leaf_node, uint32_t key_base, float tau, rc_seg* out,
                            int64_t out_cap, int32_t* defer, int32_t* mid, int64_t* counters, int max_grid,
                            cudaStream_t s) {
@@ -1557,10 +1647,10 @@ cudaError_t launch_coarsen(const rc_seg* recs, const uint32_t* perm, const int64
   if (e == cudaSuccess) e = cudaMemsetAsync(counters + CNT_MID, 0, sizeof(int64_t), s);
   if (e != cudaSuccess) return e;
   const int grid = (int)std::min<int64_t>((npix + COARSEN_FAST_WARPS - 1) / COARSEN_FAST_WARPS, (int64_t)max_grid);
-  k_coarsen_fast<<<grid, COARSEN_FAST_WARPS * 32, smem_main, s>>>(recs, perm, off, npix, node_first, leaf_node,
+  k_coarsen_fast<<<grid, COARSEN_FAST_WARPS * 32, smem_main, s>>>(recs, nrec, nleaf, perm, off, npix, node_first, leaf_node,
                                                                   key_base, tau, out, out_cap, defer, mid, counters);
-  k_coarsen_mid<<<grid, 64, smem_mid, s>>>(recs, perm, off, node_first, leaf_node, key_base, tau, out, out_cap, defer,
-                                           mid, counters);
+  k_coarsen_mid<<<grid, MID_WARPS * 32, smem_mid, s>>>(recs, nrec, nleaf, perm, off, node_first, leaf_node, key_base,
+                                                       tau, out, out_cap, defer, mid, counters);
   k_coarsen_list<<<std::min(grid, 296), FOLD_WARPS * 32, smeml, s>>>(recs, perm, off, node_first, leaf_node, key_base,
                                                                      tau, out, out_cap, defer, counters);
   g_launches += 3;

@@ -40,7 +40,8 @@ cudaError_t launch_prep_slots(const TreeConst* trees, DevLeafView L, int P, cons
 size_t slot_record_bytes();
 size_t cast_curved_scratch_per_cta();
 int cast_curved_ctas_per_sm();
-cudaError_t launch_coarsen(const rc_seg* recs, const uint32_t* perm, const int64_t* off, int64_t npix,
+cudaError_t launch_coarsen(const rc_seg* recs, int64_t nrec, int64_t nleaf, const uint32_t* perm, const int64_t* off,
+                           int64_t npix,
                            const int32_t* node_first, const int32_t* leaf_node, uint32_t key_base, float tau, rc_seg* out,
                            int64_t out_cap, int32_t* defer, int32_t* mid, int64_t* counters, int max_grid,
                            cudaStream_t s);
@@ -54,9 +55,9 @@ cudaError_t launch_hist(const rc_seg* segs, int64_t n, int32_t* cnt, int grid, c
                         const int64_t* d_n = nullptr);
 cudaError_t launch_scatter(const rc_seg* segs, int64_t n, const int64_t* off, int32_t* cursor, uint32_t* out,
                            int grid, cudaStream_t s, const int64_t* d_n = nullptr);
-// aggregation: pixel-bucketed permutation (perm, off[npix+1]) by 64-pixel bands; tmp: n scratch entries
+// aggregation: pixel-bucketed permutation (perm, off[npix+1]) by 32-pixel bands; scratch: >= 8 n bytes
 cudaError_t launch_band_bucket(const rc_seg* segs, int64_t n, int64_t npix, int32_t* bcnt, int64_t* boff,
-                               int64_t* scan_tmp, uint32_t* tmp, uint32_t* perm, int64_t* off, int grid,
+                               int64_t* scan_tmp, void* scratch, uint32_t* perm, int64_t* off, int grid,
                                cudaStream_t s);
 cudaError_t launch_scatter_rec(const rc_seg* segs, int64_t n, const int64_t* off, int32_t* cursor, rc_seg* out,
                                int grid, cudaStream_t s, const int64_t* d_n = nullptr);

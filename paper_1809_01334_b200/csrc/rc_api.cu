@@ -191,6 +191,8 @@ extern "C" rc_status rc_forest_destroy(rc_forest* f) {
     if (f->evc[k]) cudaEventDestroy(f->evc[k]);
   for (int k = 0; k < 4; ++k)
     if (f->evb[k]) cudaEventDestroy(f->evb[k]);
+  for (cudaEvent_t ev : f->evk)
+    if (ev) cudaEventDestroy(ev);
   if (f->h_tiles) cudaFreeHost(f->h_tiles);
   if (f->h_xcnt) cudaFreeHost(f->h_xcnt);
   if (f->h_trees_pin) cudaFreeHost(f->h_trees_pin);
@@ -628,27 +630,50 @@ extern "C" rc_status rc_cast_segments(rc_forest* f, int32_t fold_levels, void* s
     CU(cudaMemsetAsync(f->d_counters + CNT_UNITS, 0, sizeof(int64_t) * 6, s));
     CU(cudaMemsetAsync(f->d_counters + CNT_DEPTH_CAP, 0, sizeof(int64_t), s));
     CU(cudaEventRecord(f->ev0, s));
+    // per-launch events: the segment kernel alone (bench roofline) and the element preparation
+    f->evk_used = 0;
+    auto mark = [&](int k) -> cudaError_t {
+      if (f->evk_used >= rc_forest::kEvBatches) return cudaSuccess;
+      cudaEvent_t& ev = f->evk[4 * f->evk_used + k];
+      if (!ev) {
+        cudaError_t e = cudaEventCreate(&ev);
+        if (e != cudaSuccess) return e;
+      }
+      return cudaEventRecord(ev, s);
+    };
     if (f->h_chunks > 0) {
       if (f->surface) {
+        CU(mark(0));
         CU(launch_cast_surface(f->cc, f->d_trees, leaf_view(f), f->d_vis, f->d_vis_rect, f->d_chunk_off,
                                f->d_chunk_elem, f->h_chunks, key_base, f->d_segs, f->seg_cap, f->d_hits_pp,
                                f->d_counters, sm_count() * 8, s));
+        CU(mark(1));
+        ++f->evk_used;
       } else if (!curved) {
+        CU(mark(0));
         CU(launch_cast_affine(f->cc, f->d_trees, leaf_view(f), f->P, f->d_vis, f->d_vis_rect, f->d_chunk_off,
                               f->d_chunk_elem, f->h_chunks, key_base, f->d_segs, f->seg_cap, f->d_hits_pp,
                               f->d_counters, sm_count() * 8, s));
+        CU(mark(1));
+        ++f->evk_used;
       } else {
         char* gslot = reinterpret_cast<char*>(f->d_gslot);
         char* gorg = gslot + (size_t)f->slot_cap * (slot_record_bytes() - 32);
         for (int64_t v0 = 0; v0 < nvis; v0 += batch) {
           const int64_t v1 = std::min(nvis, v0 + batch);
           CU(cudaMemsetAsync(f->d_counters + CNT_UNITS, 0, sizeof(int64_t), s));
+          CU(mark(2));
           CU(launch_prep_slots(f->d_trees, leaf_view(f), f->P, f->d_vis, f->d_scan + n, v0,
                                std::min(nvis, v1 + RC_UNIT_LEAVES), gslot, gorg, s));
+          CU(mark(3));
+          CU(mark(0));
           CU(launch_cast_curved(f->cc, f->d_trees, leaf_view(f), f->P, f->d_vis, f->d_vis_rect, f->d_chunk_off,
                                 f->d_chunk_elem, f->d_units, nunits, fold_levels, key_base, f->d_scratch,
                                 f->d_segs, f->seg_cap, f->d_hits_pp, f->d_counters, grid_curved, gslot, gorg, v0,
                                 v1, s));
+          CU(mark(1));
+          if (f->evk_used < rc_forest::kEvBatches) ++f->evk_used;
+          else f->evk_used = rc_forest::kEvBatches + 1;   // too many batches to time: report -1
         }
       }
     }
@@ -691,6 +716,19 @@ extern "C" float rc_last_cast_ms(rc_forest* f) {
 
 extern "C" float rc_last_phase_ms(rc_forest* f, int32_t phase) {
   if (!f) return -1.0f;
+  if (phase == 6 || phase == 7) {   // segment kernel launches alone / element preparation launches
+    if (!f->timed || f->evk_used <= 0 || f->evk_used > rc_forest::kEvBatches) return -1.0f;
+    if (cudaEventSynchronize(f->ev1) != cudaSuccess) return -1.0f;
+    float tot = 0.0f;
+    for (int b = 0; b < f->evk_used; ++b) {
+      const int k = phase == 6 ? 0 : 2;
+      if (!f->evk[4 * b + k] || !f->evk[4 * b + k + 1]) continue;
+      float ms = 0.0f;
+      if (cudaEventElapsedTime(&ms, f->evk[4 * b + k], f->evk[4 * b + k + 1]) != cudaSuccess) return -1.0f;
+      tot += ms;
+    }
+    return tot;
+  }
   if (phase == 3) return (float)f->last_composite_copy;
   if (phase == 4 || phase == 5) {   // composite: bucketing (hist, scan, scatter) / fold kernels
     if (!f->composite_timed || cudaEventSynchronize(f->evc[2]) != cudaSuccess) return -1.0f;
@@ -815,7 +853,7 @@ extern "C" rc_status rc_composite_records(rc_forest* f, const rc_tiling* t, cons
     if (f->d_pix_off) dfree(f->d_pix_off, s);
     f->d_pix_cnt = nullptr;
     f->d_pix_off = nullptr;
-    CU(dmalloc((void**)&f->d_pix_cnt, sizeof(int32_t) * (npix + 2), s));   // also the band counts (<= npix/64 + 1)
+    CU(dmalloc((void**)&f->d_pix_cnt, sizeof(int32_t) * (npix + 2), s));   // also the band counts (<= npix/32 + 1)
     CU(dmalloc((void**)&f->d_pix_off, sizeof(int64_t) * (npix + 1), s));
     f->pix_cnt_cap = npix;
   }
@@ -943,7 +981,7 @@ static rc_status aggregate_to(rc_forest* f, int level, cudaStream_t s) {
     if (f->d_pix_off) dfree(f->d_pix_off, s);
     f->d_pix_cnt = nullptr;
     f->d_pix_off = nullptr;
-    CU(dmalloc((void**)&f->d_pix_cnt, sizeof(int32_t) * (npix + 2), s));   // also the band counts (<= npix/64 + 1)
+    CU(dmalloc((void**)&f->d_pix_cnt, sizeof(int32_t) * (npix + 2), s));   // also the band counts (<= npix/32 + 1)
     CU(dmalloc((void**)&f->d_pix_off, sizeof(int64_t) * (npix + 1), s));
     f->pix_cnt_cap = npix;
   }
@@ -954,13 +992,14 @@ static rc_status aggregate_to(rc_forest* f, int level, cudaStream_t s) {
   // output buffer: half the input first for one cycle, a quarter for several
   // (a cycle roughly halves the count), grown to the exact
   // count and the pass repeated if short; before the pass it holds the
-  // bucketing's scratch indices (>= 4 bytes per input record)
+  // bucketing's scratch (index + band-local pixel: 8 bytes per input record,
+  // the buffer has >= 8)
   int64_t want = std::max<int64_t>(nrec / (level - f->rec_level >= 2 ? 4 : 2) + 4096, 1);
   CU(grow(&f->d_segs2, &f->seg2_cap, want, s));
-  const int64_t nbands = (npix + 63) / 64;
+  const int64_t nbands = (npix + 31) / 32;
   if (f->boff_cap < nbands + 1) CU(grow(&f->d_boff, &f->boff_cap, nbands + 1, s));
-  CU(launch_band_bucket(f->d_segs, nrec, npix, f->d_pix_cnt, f->d_boff, f->d_scan_tmp,
-                        reinterpret_cast<uint32_t*>(f->d_segs2), f->d_perm, f->d_pix_off, grid, s));
+  CU(launch_band_bucket(f->d_segs, nrec, npix, f->d_pix_cnt, f->d_boff, f->d_scan_tmp, f->d_segs2, f->d_perm,
+                        f->d_pix_off, grid, s));
   // pixels deferred to the list pass [0, npix) and pixels of the mid pass (256 < n <= 512) [npix, 2 npix)
   CU(grow(&f->d_defer, &f->defer_cap, std::max<int64_t>(2 * npix, 1), s));
   const int32_t* leaf_node = nullptr;   // node of every leaf at the target level
@@ -970,7 +1009,7 @@ static rc_status aggregate_to(rc_forest* f, int level, cudaStream_t s) {
     CU(grow(&f->d_segs2, &f->seg2_cap, want, s));
     CU(cudaMemsetAsync(f->d_counters + CNT_AGG_OUT, 0, sizeof(int64_t), s));
     CU(cudaMemsetAsync(f->d_counters + CNT_OVERFLOW, 0, sizeof(int64_t), s));
-    CU(launch_coarsen(f->d_segs, f->d_perm, f->d_pix_off, npix, f->d_node_first[level], leaf_node,
+    CU(launch_coarsen(f->d_segs, nrec, f->n, f->d_perm, f->d_pix_off, npix, f->d_node_first[level], leaf_node,
                       (uint32_t)f->first_global, 1e-6f, f->d_segs2, f->seg2_cap, f->d_defer, f->d_defer + npix,
                       f->d_counters,
                       sm_count() * 16, s));

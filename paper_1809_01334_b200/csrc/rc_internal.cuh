@@ -6,6 +6,26 @@
 
 #include "../../include/rc.h"
 
+// Device-side bounds checks of the checked build (tag "checks": -DRC_CHECKS,
+// tools/gpu_checks.sh).  compute-sanitizer is not available on the GPU pool
+// this project runs on, so index bounds of the gathers and scatters are
+// asserted in place instead; a violation prints the condition and traps.
+#ifdef RC_CHECKS
+#include <cstdio>
+#define RC_DCHECK(c)                                                                   \
+  do {                                                                                 \
+    if (!(c)) {                                                                        \
+      printf("RC_CHECKS %s:%d: %s (block %d thread %d)\n", __FILE__, __LINE__, #c,     \
+             (int)blockIdx.x, (int)threadIdx.x);                                      \
+      __trap();                                                                        \
+    }                                                                                  \
+  } while (0)
+#else
+#define RC_DCHECK(c) \
+  do {               \
+  } while (0)
+#endif
+
 #define RC_MAX_N 8          // GL points per segment
 #define RC_MAX_RANKS 64     // tile owners / communicator size
 #define RC_MAX_TREES 4096
@@ -182,6 +202,10 @@ struct rc_forest {
   cudaEvent_t evc[3] = {nullptr, nullptr, nullptr};   // composite: start, after scatter, after fold
   bool composite_timed = false;
   cudaEvent_t evb[4] = {nullptr, nullptr, nullptr, nullptr};
+  // per batch of the last rc_cast_segments: segment kernel start/end, prep start/end
+  static constexpr int kEvBatches = 64;
+  cudaEvent_t evk[4 * kEvBatches] = {};
+  int evk_used = 0;   // batches timed (0: none)
   float phase_ms[3] = {0, 0, 0};
   bool timed = false;
 };
