@@ -174,6 +174,25 @@ def l2_flush(buf):
     buf.add_(1.0)
 
 
+def instance_cameras(scene, count):
+    """Image instances (PAPER.md:835-841): instance 0 is the config's camera;
+    instance k >= 1 turns it by 35 k degrees about the vertical axis through
+    the scene centre and narrows the field of view to 0.6 of it (a camera that
+    culls part of the forest), same image size and rule."""
+    import dataclasses
+    import numpy as np
+    cam = scene.camera
+    cams = [cam]
+    piv = np.zeros(3) if scene.geom_degree == 2 or getattr(scene, "dim", 3) == 2 else np.full(3, 0.5)
+    for k in range(1, count):
+        a = math.radians(35.0 * k)
+        Rz = np.array([[math.cos(a), -math.sin(a), 0.0], [math.sin(a), math.cos(a), 0.0], [0.0, 0.0, 1.0]])
+        rot = lambda v: Rz @ np.asarray(v, dtype=np.float64)
+        cams.append(dataclasses.replace(cam, origin=piv + rot(np.asarray(cam.origin) - piv), view=rot(cam.view),
+                                        right=rot(cam.right), up=rot(cam.up), pixel_size=cam.pixel_size * 0.6))
+    return cams
+
+
 def cpu_model():
     model, sockets = None, None
     try:
@@ -302,6 +321,13 @@ def main():
     ap.add_argument("--dist-backend", default="nccl", choices=["nccl", "gloo"],
                     help="gloo: host-staged exchanges (tests: several ranks on one GPU)")
     ap.add_argument("--dump", default="", help="rank 0 writes the assembled image and hit counts (npz)")
+    ap.add_argument("--instances", type=int, default=1,
+                    help="image instances per frame (PAPER.md:835-841): the config camera + turned, narrower ones")
+    ap.add_argument("--prepartition", default="vforest", choices=["vforest", "leaves"],
+                    help="N > 1: vforest = copy only the leaves some instance sees, weighted by their summed "
+                         "visible pixels (PAPER.md:873-899); leaves = weight and move every leaf")
+    ap.add_argument("--all-to-all", action="store_true",
+                    help="N > 1: count all-to-all instead of the partners discovered from the partition markers")
     args = ap.parse_args()
     if args.impl == "reference":
         return run_reference(args)
@@ -329,6 +355,8 @@ def main():
         tp = rdist.Transport()
     scene = make_scene(args.config, dev if args.config >= 2 else None)
     cam = scene.camera
+    cams = instance_cameras(scene, max(1, args.instances))
+    NI = len(cams)
     W, H = cam.width, cam.height
     N = cam.gl_points
     rc.lib()
@@ -350,22 +378,32 @@ def main():
         lo, hi = old[rank]
         f0 = rc.Forest(scene.tree_ctrl, scene.geom_degree, scene.field_degree, A[lo:hi], T[lo:hi], Lv[lo:hi],
                        F[lo:hi], scene.kappa0, scene.inv_F, scene.q0, first_global_leaf=lo, **surf_kw)
-        f0.camera_set(cam)
-        f0.cull()
-        w = f0.leaf_weights()
-        f0.close()
-        ranges = rdist.distributed_aligned_cuts(w, allowed[lo:hi], lo, n, tp)
-        mine = rdist.redistribute_rows([A[lo:hi], T[lo:hi], Lv[lo:hi], F[lo:hi]], old, ranges, tp)
+        if args.prepartition == "vforest":   # only what some instance sees moves
+            consts6 = (scene.tree_ctrl, scene.geom_degree, scene.field_degree, scene.kappa0, scene.inv_F, scene.q0,
+                       surf_kw)
+            forest, keys, ranges, vst = rdist.vforest_prepartition(f0, cams, tp, fold + cycles, consts6)
+            f0.close()
+            wsum = vst["visible_weight_local"]
+            n_vf = vst["vforest_leaves"]
+            del A, T, Lv, F, allowed
+        else:
+            f0.camera_set(cam)
+            f0.cull()
+            w = f0.leaf_weights()
+            f0.close()
+            ranges = rdist.distributed_aligned_cuts(w, allowed[lo:hi], lo, n, tp)
+            mine = rdist.redistribute_rows([A[lo:hi], T[lo:hi], Lv[lo:hi], F[lo:hi]], old, ranges, tp)
+            wsum = float(w.sum())
+            n_vf = n
+            del A, T, Lv, F, allowed, w
+            forest = rc.Forest(scene.tree_ctrl, scene.geom_degree, scene.field_degree, *mine, scene.kappa0,
+                               scene.inv_F, scene.q0, first_global_leaf=ranges[rank][0], **surf_kw)
+            keys = mine[:3]
+            del mine
         lo, hi = ranges[rank]
-        wsum = float(w.sum())
-        del A, T, Lv, F, allowed, w
-        forest = rc.Forest(scene.tree_ctrl, scene.geom_degree, scene.field_degree, *mine, scene.kappa0,
-                           scene.inv_F, scene.q0, first_global_leaf=lo, **surf_kw)
-        keys = mine[:3]
-        del mine
         torch.cuda.synchronize()
         repart = {"repartition_ms": 1000.0 * (time.perf_counter() - t0), "ranges": ranges, "weight_local": wsum,
-                  "equal_count_ranges": old}
+                  "equal_count_ranges": old, "prepartition": args.prepartition, "vforest_leaves": n_vf}
         if args.dist_backend == "nccl":
             comm = rc.Comm(world, rank)
     else:
@@ -384,60 +422,105 @@ def main():
 
     phase_ev = {}
     moved = [0]
+    imgs = [img] + [torch.empty((H, W, 4), dtype=torch.float32, device=dev) for _ in range(NI - 1)]
+    kt = {1: 0.0, 6: 0.0, 7: 0.0}   # instances > 1: summed cast / kernel / prep ms of the last frame
+    partners = [None] * NI          # per instance (send_to, recv_from), discovered after the warm-up
+    final_keys = [keys] * NI        # this rank's leaf keys at the exchange (after the cycles' repartition)
 
-    def mark(name):
+    def mark(name, k=0):
         ev = torch.cuda.Event(enable_timing=True)
         ev.record(stream)
-        phase_ev[name] = ev
+        phase_ev[(name, k)] = ev
 
-    def frame(f, f_keys, f_rng):
-        mark("start")
-        f.camera_set(cam)
-        f.cull()
-        mark("cull")
-        f.cast_segments(fold)
-        mark("cast")
+    def frame(f, f_keys, f_rng, collect=None):
+        """One frame: every image instance in turn (camera, cull, cast with the
+        on-chip fold, cycles, exchange + composite).  Returns (outputs per
+        instance, the last instance's aggregation forest)."""
+        outs = []
         fa = f
-        if cycles:
-            if world > 1:
-                fa, _, _, _, mv = rdist.aggregate_with_repartition(f, f_keys, f_rng, ranges, cycles, fold + cycles,
-                                                                   tp, consts)
-                moved[0] = mv
-            else:
-                f.aggregate(cycles)
-        mark("aggregate")
-        if world == 1:
-            f.composite(out=img)
-            mark("composite")
-            return img, fa
-        out = rdist.exchange_and_composite(fa, tiles, world, rank, comm=comm, tp=tp)
-        mark("composite")
-        return out, fa
+        for k in range(NI):
+            if fa is not f:
+                fa.close()
+            mark("start", k)
+            f.camera_set(cams[k])
+            f.cull()
+            mark("cull", k)
+            f.cast_segments(fold)
+            mark("cast", k)
+            if NI > 1:   # the segment-kernel timings of every instance ([sync] reads)
+                for ph in (1, 6, 7):
+                    kt[ph] = (kt[ph] if k else 0.0) + f.last_phase_ms(ph)
+            fa = f
+            if cycles:
+                if world > 1:
+                    fa, fk, _, _, mv = rdist.aggregate_with_repartition(f, f_keys, f_rng, ranges, cycles,
+                                                                       fold + cycles, tp, consts[:6] + (cams[k],))
+                    moved[0] = mv
+                    final_keys[k] = fk
+                else:
+                    f.aggregate(cycles)
+            mark("aggregate", k)
+            if collect is not None:
+                sg_ = f.segments()
+                collect.append((sg_["hit_pairs"], sg_["candidates"], sg_["hits_per_pixel"].reshape(-1).to(torch.int64)))
+            if world == 1:
+                f.composite(out=imgs[k])
+                mark("composite", k)
+                outs.append(imgs[k])
+                continue
+            if comm is not None:
+                if partners[k] is None:
+                    comm.set_partners()
+                else:
+                    comm.set_partners(*partners[k])
+            out = rdist.exchange_and_composite(fa, tiles, world, rank, comm=comm, tp=tp,
+                                               partners=partners[k] if comm is None else None)
+            mark("composite", k)
+            outs.append(out)
+        return outs, fa
 
-    use_graph = world == 1 and forest_affine(scene) and fold == 0 and not cycles   # launch-bound C1 / C2
+    use_graph = world == 1 and forest_affine(scene) and fold == 0 and not cycles and NI == 1   # launch-bound C1 / C2
 
     def graph_frame():
         mark("start")
         forest.frame_replay()
         mark("composite")
-        return img, forest
+        return [img], forest
 
-    def run_frame(f, f_keys, f_rng):
-        out, fa = frame(f, f_keys, f_rng)
+    def run_frame(f, f_keys, f_rng, collect=None):
+        out, fa = frame(f, f_keys, f_rng, collect)
         if fa is not f:
             fa.close()
         return out
 
     for _ in range(max(3, args.warmup)):
         run_frame(forest, keys, (lo, hi))
+    partners_ms = None
+    if world > 1 and not args.all_to_all:
+        # exchange partners from the partition markers (PAPER.md:1030-1114): the markers are
+        # all-gathered with the partition; the traversal itself is local
+        t0 = time.perf_counter()
+        for k in range(NI):
+            mk = rdist.partition_markers(final_keys[k], scene.num_trees, tp)
+            forest.camera_set(cams[k])
+            partners[k] = rdist.discover_partners(forest, tiles, mk, tp)
+        partners_ms = 1000.0 * (time.perf_counter() - t0)
+        for _ in range(2):
+            run_frame(forest, keys, (lo, hi))
     if use_graph:
         img = forest.frame_capture(cam)
+        imgs[0] = img
         for _ in range(3):
             forest.frame_replay()
     torch.cuda.synchronize()
-    segs = forest.segments()
-    hits_local = segs["hit_pairs"]
-    cand_local = segs["candidates"]
+    per_inst = []
+    if not use_graph:
+        run_frame(forest, keys, (lo, hi), collect=per_inst)
+    else:
+        sg_ = forest.segments()
+        per_inst.append((sg_["hit_pairs"], sg_["candidates"], sg_["hits_per_pixel"].reshape(-1).to(torch.int64)))
+    hits_local = sum(int(c[0]) for c in per_inst)
+    cand_local = sum(int(c[1]) for c in per_inst)
     if world > 1:
         t = tp.all_gather(torch.tensor([hits_local, cand_local], dtype=torch.int64)).sum(dim=0)
         hits_total, cand_total = int(t[0]), int(t[1])
@@ -461,21 +544,23 @@ def main():
             e1.record(stream)
             torch.cuda.synchronize()
             times.append(e0.elapsed_time(e1))
-            cast_ms.append(forest.last_phase_ms(1))
-            kern_ms.append(forest.last_phase_ms(6))
-            prep_ms.append(forest.last_phase_ms(7))
+            ph_ms = kt if NI > 1 else {ph: forest.last_phase_ms(ph) for ph in (1, 6, 7)}
+            cast_ms.append(ph_ms[1])
+            kern_ms.append(ph_ms[6])
+            prep_ms.append(ph_ms[7])
             if fa is not forest:
                 fa.close()
             if use_graph:   # one graph: no phase events inside (the kernel time is the last ordinary frame's)
                 phase_acc["graph_frame"] = phase_acc.get("graph_frame", 0.0) + \
-                    phase_ev["start"].elapsed_time(phase_ev["composite"]) / args.steps
+                    phase_ev[("start", 0)].elapsed_time(phase_ev[("composite", 0)]) / args.steps
                 continue
             if world == 1:
                 for k, nm in ((4, "composite_bucket"), (5, "composite_fold")):
                     phase_acc[nm] = phase_acc.get(nm, 0.0) + forest.last_phase_ms(k) / args.steps
             names = ["start", "cull", "cast", "aggregate", "composite"]
-            for a, b in zip(names, names[1:]):
-                phase_acc[b] = phase_acc.get(b, 0.0) + phase_ev[a].elapsed_time(phase_ev[b]) / args.steps
+            for k in range(NI):
+                for a, b in zip(names, names[1:]):
+                    phase_acc[b] = phase_acc.get(b, 0.0) + phase_ev[(a, k)].elapsed_time(phase_ev[(b, k)]) / args.steps
     launches = rc.launch_count()
     ms_local = sum(times) / len(times)
     cast_local = sum(cast_ms) / len(cast_ms)
@@ -490,15 +575,20 @@ def main():
     value = hits_total / (ms_step / 1000.0)
 
     if args.dump:
-        hpp = forest.segments()["hits_per_pixel"].reshape(-1).to(torch.int64)
-        if world > 1:
-            image = rdist.gather_image(last_out, tiles, W, H, tp)
-            hpp = tp.all_gather(hpp).sum(dim=0)
-        else:
-            image = last_out.cpu()
+        dumps = {}
+        for k in range(NI):
+            hpp = per_inst[k][2]
+            if world > 1:
+                image = rdist.gather_image(last_out[k], tiles, W, H, tp)
+                hpp = tp.all_gather(hpp).sum(dim=0)
+            else:
+                image = last_out[k].cpu()
+            sfx = "" if k == 0 else f"_{k}"
+            if rank == 0:
+                dumps["image" + sfx] = image.numpy()
+                dumps["hits_per_pixel" + sfx] = hpp.cpu().numpy()
         if rank == 0:
-            np.savez(args.dump, image=image.numpy(), hits_per_pixel=hpp.cpu().numpy(), hit_pairs=hits_total,
-                     ranges=np.array(ranges), moved=moved[0])
+            np.savez(args.dump, hit_pairs=hits_total, ranges=np.array(ranges), moved=moved[0], instances=NI, **dumps)
 
     # --- roofline of the dominant kernel (segment kernel) -----------------
     pk = peaks()
@@ -536,16 +626,19 @@ def main():
                  "raw_segments": seg_info["raw_segments"], "record_level": seg_info["level"],
                  "units": seg_info["units"], "unfolded_units": seg_info["unfolded_units"],
                  "face_tasks": seg_info["face_tasks"], "fallback_tasks": seg_info["fallback_tasks"]}
+    if world > 1:   # this rank's inputs after the pre-partition (vforest rows or moved leaf rows)
+        host = [a.cpu().numpy() for a in forest.leaves()]
+    else:
+        host = [np.ascontiguousarray(a if isinstance(a, np.ndarray) else a.cpu().numpy())
+                for a in (scene.leaf_anchor[lo:hi], scene.leaf_tree[lo:hi], scene.leaf_level[lo:hi],
+                          scene.leaf_field[lo:hi])]
     forest.close()          # release the device-resident forest before the e2e forests
     del forest
     torch.cuda.empty_cache()
-    host = [np.ascontiguousarray(a if isinstance(a, np.ndarray) else a.cpu().numpy())
-            for a in (scene.leaf_anchor[lo:hi], scene.leaf_tree[lo:hi], scene.leaf_level[lo:hi],
-                      scene.leaf_field[lo:hi])]
     pinned = [torch.from_numpy(a).pin_memory() for a in host]
     pinned_np = [p.numpy() for p in pinned]
     h2d = sum(a.nbytes for a in host)
-    img_host = torch.empty((H, W, 4), dtype=torch.float32).pin_memory()
+    img_host = torch.empty((NI, H, W, 4), dtype=torch.float32).pin_memory()
     e2e_times = []
     n_e2e = 0 if args.no_e2e else 2 + (1 if args.config in (4, 5) else max(1, min(args.steps, 3)))
     for it in range(n_e2e):
@@ -558,8 +651,9 @@ def main():
         f2 = rc.Forest(scene.tree_ctrl, scene.geom_degree, scene.field_degree, *pinned_np, scene.kappa0,
                        scene.inv_F, scene.q0, first_global_leaf=lo, trusted=True, **surf_kw)
         k2 = [torch.from_numpy(a).to(dev) for a in host[:3]] if (world > 1 and cycles) else None
-        out, fa = frame(f2, k2, (lo, hi))
-        img_host.view(-1)[:out.numel()].copy_(out.reshape(-1))
+        outs, fa = frame(f2, k2, (lo, hi))
+        for k, out in enumerate(outs):
+            img_host[k].view(-1)[:out.numel()].copy_(out.reshape(-1))
         torch.cuda.synchronize()
         dt = time.perf_counter() - t0
         if fa is not f2:
@@ -571,7 +665,7 @@ def main():
     if world > 1:
         e2e_s = tp.max(e2e_s)
     e2e = {"value": hits_total / e2e_s, "unit": "hit pairs/s", "h2d_bytes_per_step": h2d,
-           "d2h_bytes_per_step": int(last_out.numel()) * 4 if last_out is not None else H * W * 16,
+           "d2h_bytes_per_step": sum(int(o.numel()) * 4 for o in last_out) if last_out else NI * H * W * 16,
            "ms_per_step": e2e_s * 1000.0}
 
     if rank == 0:
@@ -584,14 +678,16 @@ def main():
                            "candidate_pairs_per_s": cand_total / (ms_step / 1000.0),
                            "l2": "flushed between frames (160 MB write outside the events)",
                            "parallelism": f"sfc{world}", "tiles": list(tiles), "cuda_graph_frame": use_graph,
-                           "dist_backend": args.dist_backend if world > 1 else None},
+                           "dist_backend": args.dist_backend if world > 1 else None, "instances": NI},
                 "roofline": roof, "gpu_launches": launches, "clocks": clk.summary(), "e2e": e2e,
                 "newton_failures": newton_failures, "segments": fold_info,
                 "phase_ms": {k: round(v, 3) for k, v in phase_acc.items()},
                 "composite_copy": composite_copy}
         if world > 1:
             line["partition"] = {"repartition_ms": repart["repartition_ms"], "ranges": repart["ranges"],
-                                 "cycle_records_moved_rank0": moved[0]}
+                                 "cycle_records_moved_rank0": moved[0], "prepartition": repart["prepartition"],
+                                 "vforest_leaves": repart["vforest_leaves"], "partners_ms": partners_ms,
+                                 "partners_rank0": partners if not args.all_to_all else None}
         if world == 1 and not args.no_cpu_baseline:
             sc_cpu = scene_to_host(scene)
             cb = cpu_baseline(sc_cpu, CPU_STRIDE[args.config], hits_total)

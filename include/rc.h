@@ -38,7 +38,7 @@ typedef enum {
 } rc_status;
 
 const char* rc_last_error(void);
-int32_t rc_version(void);    /* ABI version, currently 3 */
+int32_t rc_version(void);    /* ABI version, currently 4 */
 
 /* ------------------------------------------------------------------------
  * Forest: SFC-ordered leaves of a forest of octrees with per-tree degree-R
@@ -295,6 +295,65 @@ rc_status rc_composite_records(rc_forest* f, const rc_tiling* t, const rc_seg* d
                                const float background[3], float* d_rgba, int64_t capacity_floats, void* stream);
 rc_status rc_composite(rc_forest* f, const float background[3], float* d_rgba, int64_t capacity_floats,
                        void* stream);
+
+/* ------------------------------------------------------------------------
+ * Exchange partners without communication (
+ * PAPER.md:1030-1114).  Partition markers: the tree and anchor of every rank's
+ * first leaf, known to every rank.  h_markers[nranks+1]:
+ * marker p = first leaf of rank p in SFC order (an empty rank repeats the next
+ * rank's marker), marker 0 = (0, {0,0,0}), marker nranks = (num_trees,
+ * {0,0,0}); rank p owns the SFC positions [marker p, marker p+1).
+ *
+ * rc_exchange_partners: the paper's receiver-side traversal -- top down from
+ * every tree root over virtual nodes, the marker range split by nested binary
+ * searches, stopping where the node's pixel-centre rectangle (SURVEY R6 on the
+ * node's camera-space Bernstein box, padded by 1e-9) misses the writer's
+ * tiles and recording the owner once the range holds one non-empty rank
+ * (PAPER.md:1093-1103).  h_recv_from[p] = 1: rank p sends records to this
+ * rank (t->rank); h_send_to[q] = 1: this rank sends to writer q (the same
+ * relation evaluated for every writer, DESIGN D19), so the lists of all ranks
+ * agree by construction.  Tile owners as in rc_composite_tiles.  Either
+ * output may be NULL.  Host only (O(nranks x depth x 8) node boxes per
+ * writer); must follow rc_camera_set.  Every pair that carries a record is
+ * listed (node boxes contain their leaves' boxes).
+ * rc_comm_set_partners: the lists for the exchanges of rc_composite_tiles on
+ * this communicator: the counts move by grouped ncclSend / ncclRecv between
+ * listed pairs only (instead of the count all-to-all), the records likewise.
+ * Records for an unlisted writer are not sent and the call returns
+ * RC_ERR_STATE after the collective.  NULL, NULL: back to the all-to-all.
+ * ---------------------------------------------------------------------- */
+typedef struct {
+  int32_t tree;
+  int32_t anchor[3];          /* units of 2^-18 of the tree cube */
+} rc_marker;
+rc_status rc_exchange_partners(rc_forest* f, const rc_tiling* t, const rc_marker* h_markers, uint8_t* h_send_to,
+                               uint8_t* h_recv_from);
+rc_status rc_comm_set_partners(rc_comm* c, const uint8_t* h_send_to, const uint8_t* h_recv_from);
+
+/* ------------------------------------------------------------------------
+ * Multiple image instances and the vforest (
+ * PAPER.md:835-841, 861-919).  Per instance: rc_camera_set(instance camera) +
+ * rc_cull, then rc_visible_area_add(f, d_w) adds the pixel-centre rectangle
+ * area of every leaf (0 when culled) to d_w (device int64 [num_leaves],
+ * caller-owned and zeroed by the caller; async): a leaf is visible while one
+ * instance sees it and its weight is its visible pixel count summed over the
+ * instances.
+ * rc_vforest_create: a new forest (the vforest, "copying only the data of
+ * the visible elements") of the leaves with d_w[e] > 0 in
+ * SFC order -- keys and field gathered on the device, same trees, transfer
+ * and kind; first_global_leaf = its SFC index offset (the vforest's own
+ * numbering).  *h_count = its leaves; 0 leaves: *out = NULL.  d_w_out
+ * (optional, device int64 [num_leaves]): the kept leaves' weights, for the
+ * repartition.  The input forest is unchanged.  [sync]
+ * ---------------------------------------------------------------------- */
+rc_status rc_visible_area_add(rc_forest* f, int64_t* d_w, int64_t capacity, void* stream);
+/* Copies the forest's leaves out (device buffers of capacity >= num_leaves
+ * rows, layouts as rc_forest_desc; any pointer may be NULL): the rows a
+ * repartition moves to their new owners.  Async. */
+rc_status rc_forest_leaves(rc_forest* f, int32_t* d_anchor, int32_t* d_tree, int8_t* d_level, float* d_field,
+                           int64_t capacity, void* stream);
+rc_status rc_vforest_create(rc_forest* f, const int64_t* d_w, int64_t first_global_leaf, void* stream,
+                            rc_forest** out, int64_t* h_count, int64_t* d_w_out);
 
 /* ------------------------------------------------------------------------
  * One whole frame on one GPU from device-resident inputs:

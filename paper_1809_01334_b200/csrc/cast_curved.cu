@@ -614,8 +614,11 @@ __device__ __forceinline__ void prep_bounds(const float* __restrict__ slw, const
 }
 
 constexpr int PREP_E = 32;
+#ifndef PREP_MINB
+#define PREP_MINB 1
+#endif
 template <int P>
-__global__ void __launch_bounds__(3 * PREP_E) k_prep_slots(const TreeConst* __restrict__ trees, DevLeafView L,
+__global__ void __launch_bounds__(3 * PREP_E, PREP_MINB) k_prep_slots(const TreeConst* __restrict__ trees, DevLeafView L,
                                                            const int32_t* __restrict__ vis,
                                                            const int64_t* __restrict__ nvis_p, int64_t v0, int64_t v1,
                                                            float4* __restrict__ gslot, double* __restrict__ gorg) {

@@ -114,9 +114,39 @@ int nccl_alltoall_i64(rc_comm* c, const int64_t* d_send, int64_t* d_recv, cudaSt
   return 0;
 }
 
+// One int64 to every discovered receiver, one from every discovered sender
+// (rc_comm_set_partners); entries of other peers are left untouched.
+int nccl_partner_i64(rc_comm* c, const int64_t* d_send, int64_t* d_recv, cudaStream_t s) {
+  int r = g_nccl.GroupStart();
+  if (r) return r;
+  for (int p = 0; p < c->nranks; ++p) {
+    if (p == c->rank) continue;
+    if (c->send_to[p] && (r = g_nccl.Send(d_send + p, 1, ncclInt64, p, (ncclComm_t)c->nccl, s))) break;
+    if (c->recv_from[p] && (r = g_nccl.Recv(d_recv + p, 1, ncclInt64, p, (ncclComm_t)c->nccl, s))) break;
+  }
+  const int r2 = g_nccl.GroupEnd();
+  if (r) return r;
+  if (r2) return r2;
+  if (cudaMemcpyAsync(d_recv + c->rank, d_send + c->rank, sizeof(int64_t), cudaMemcpyDeviceToDevice, s) !=
+      cudaSuccess)
+    return -1;
+  return 0;
+}
+
 }  // namespace rc
 
 using namespace rc;
+
+extern "C" rc_status rc_comm_set_partners(rc_comm* c, const uint8_t* h_send_to, const uint8_t* h_recv_from) {
+  if (!c) return rc_fail(RC_ERR_INVALID_ARG, "rc_comm_set_partners: null communicator");
+  if (!h_send_to != !h_recv_from) return rc_fail(RC_ERR_INVALID_ARG, "rc_comm_set_partners: give both lists or neither");
+  c->partners = h_send_to != nullptr;
+  for (int p = 0; p < c->nranks; ++p) {
+    c->send_to[p] = c->partners ? (h_send_to[p] != 0) : 0;
+    c->recv_from[p] = c->partners ? (h_recv_from[p] != 0) : 0;
+  }
+  return RC_OK;
+}
 
 extern "C" rc_status rc_comm_unique_id(uint8_t id[128]) {
   if (!id) return rc_fail(RC_ERR_INVALID_ARG, "rc_comm_unique_id: null argument");

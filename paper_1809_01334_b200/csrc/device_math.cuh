@@ -2,6 +2,7 @@
 // interpolation, the nested Gauss-Legendre segment rule, record output.
 #pragma once
 #include "rc_internal.cuh"
+#include "geom.cuh"
 
 namespace rc {
 
@@ -235,41 +236,6 @@ __device__ __noinline__ void segment_scheme(const CamConst& cc, float L, const M
   b_out[2] = B2;
 }
 
-// pixel-centre rectangle of a camera-space AABB; false: culled
-__device__ __forceinline__ bool project_rect(const CamConst& cc, const double lo[3], const double hi[3], Rect16& rc) {
-  double pmin[2], pmax[2];
-  int dims[2] = {cc.W, cc.H};
-  if (cc.proj == RC_PERSPECTIVE) {
-    if (hi[2] < cc.n || lo[2] > cc.far_dist) return false;
-    double z0 = fmax(lo[2], cc.n), z1 = fmax(hi[2], cc.n);
-    double s = cc.n / cc.ell;
-    for (int d = 0; d < 2; ++d) {
-      double a = lo[d] / z0, b = lo[d] / z1, c = hi[d] / z0, e = hi[d] / z1;
-      pmin[d] = s * fmin(fmin(a, b), fmin(c, e)) + 0.5 * (dims[d] - 1);
-      pmax[d] = s * fmax(fmax(a, b), fmax(c, e)) + 0.5 * (dims[d] - 1);
-    }
-  } else {
-    if (hi[2] < 0.0 || lo[2] > cc.far_dist) return false;
-    for (int d = 0; d < 2; ++d) {
-      pmin[d] = lo[d] / cc.ell + 0.5 * (dims[d] - 1);
-      pmax[d] = hi[d] / cc.ell + 0.5 * (dims[d] - 1);
-    }
-  }
-  int r[4];
-  for (int d = 0; d < 2; ++d) {
-    double a = ceil(pmin[d]), b = floor(pmax[d]);
-    a = fmax(a, 0.0);
-    b = fmin(b, (double)(dims[d] - 1));
-    if (!(a <= b)) return false;
-    r[2 * d] = (int)a;
-    r[2 * d + 1] = (int)b;
-  }
-  rc.i0 = (int16_t)r[0];
-  rc.i1 = (int16_t)r[1];
-  rc.j0 = (int16_t)r[2];
-  rc.j1 = (int16_t)r[3];
-  return true;
-}
 
 __device__ __forceinline__ void store_seg(rc_seg* dst, uint32_t pixel, float an, float af, float a, const float b[3],
                                           uint32_t key) {

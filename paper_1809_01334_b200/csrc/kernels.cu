@@ -44,63 +44,6 @@ __global__ void k_cull_affine(CamConst cc, const TreeConst* __restrict__ trees, 
   rect[e] = rc;
 }
 
-// Restriction of a degree-R Bernstein polynomial (along one axis) to [u,v]:
-// new control points are blossom values P(u..u, v..v) (de Casteljau).
-template <int R>
-__device__ __forceinline__ void bz_restrict_row(double u, double v, double M[R + 1][R + 1]);
-
-template <>
-__device__ __forceinline__ void bz_restrict_row<1>(double u, double v, double M[2][2]) {
-  M[0][0] = 1 - u; M[0][1] = u;
-  M[1][0] = 1 - v; M[1][1] = v;
-}
-template <>
-__device__ __forceinline__ void bz_restrict_row<2>(double u, double v, double M[3][3]) {
-  // blossom P(x,y) = (1-x)(1-y) p0 + ((1-x)y + x(1-y)) p1 + x y p2
-  double x[3] = {u, u, v}, y[3] = {u, v, v};
-  for (int r = 0; r < 3; ++r) {
-    M[r][0] = (1 - x[r]) * (1 - y[r]);
-    M[r][1] = (1 - x[r]) * y[r] + x[r] * (1 - y[r]);
-    M[r][2] = x[r] * y[r];
-  }
-}
-
-// Element Bernstein points from the tree's (index [m3][m2][m1][xyz]).
-template <int R>
-__device__ void element_bezier(const double* __restrict__ Btree, const double t0[3], double h, double* B) {
-  constexpr int n1 = R + 1;
-  double M[3][n1][n1];
-  for (int k = 0; k < 3; ++k) bz_restrict_row<R>(t0[k], t0[k] + h, M[k]);
-  double tmp[n1 * n1 * n1 * 3];
-  // axis 1
-  for (int m3 = 0; m3 < n1; ++m3)
-    for (int m2 = 0; m2 < n1; ++m2)
-      for (int r = 0; r < n1; ++r)
-        for (int c = 0; c < 3; ++c) {
-          double s = 0;
-          for (int m1 = 0; m1 < n1; ++m1) s = fma(M[0][r][m1], Btree[((m3 * n1 + m2) * n1 + m1) * 3 + c], s);
-          tmp[((m3 * n1 + m2) * n1 + r) * 3 + c] = s;
-        }
-  // axis 2
-  for (int m3 = 0; m3 < n1; ++m3)
-    for (int r = 0; r < n1; ++r)
-      for (int m1 = 0; m1 < n1; ++m1)
-        for (int c = 0; c < 3; ++c) {
-          double s = 0;
-          for (int m2 = 0; m2 < n1; ++m2) s = fma(M[1][r][m2], tmp[((m3 * n1 + m2) * n1 + m1) * 3 + c], s);
-          B[((m3 * n1 + r) * n1 + m1) * 3 + c] = s;
-        }
-  // axis 3
-  for (int r = 0; r < n1; ++r)
-    for (int m2 = 0; m2 < n1; ++m2)
-      for (int m1 = 0; m1 < n1; ++m1)
-        for (int c = 0; c < 3; ++c) {
-          double s = 0;
-          for (int m3 = 0; m3 < n1; ++m3) s = fma(M[2][r][m3], B[((m3 * n1 + m2) * n1 + m1) * 3 + c], s);
-          tmp[((r * n1 + m2) * n1 + m1) * 3 + c] = s;
-        }
-  for (int q = 0; q < n1 * n1 * n1 * 3; ++q) B[q] = tmp[q];
-}
 
 template <int R>
 __global__ void __launch_bounds__(128) k_cull_curved(CamConst cc, const TreeConst* __restrict__ trees, DevLeafView L, int64_t n,
@@ -112,16 +55,8 @@ __global__ void __launch_bounds__(128) k_cull_curved(CamConst cc, const TreeCons
   double h = ldexp(1.0, -(int)L.level[e]);
   double t0[3];
   for (int k = 0; k < 3; ++k) t0[k] = ldexp((double)L.anchor[3 * e + k], -RC_MAXLEVEL);
-  double lo[3] = {1e300, 1e300, 1e300}, hi[3] = {-1e300, -1e300, -1e300};
-  {
-    double B[NP * 3];
-    element_bezier<R>(T.Bc, t0, h, B);
-    for (int m = 0; m < NP; ++m)
-      for (int c = 0; c < 3; ++c) {
-        lo[c] = fmin(lo[c], B[3 * m + c]);
-        hi[c] = fmax(hi[c], B[3 * m + c]);
-      }
-  }
+  double lo[3], hi[3];
+  element_aabb<R>(T.Bc, t0, h, lo, hi);
   Rect16 rc{0, -1, 0, -1};
   bool v = project_rect(cc, lo, hi, rc);
   flag[e] = v ? 1 : 0;

@@ -40,7 +40,7 @@ rc_status rc_fail(rc_status st, const char* fmt, ...) {
 #define LAUNCHED() (++g_launches)
 
 extern "C" const char* rc_last_error(void) { return g_err; }
-extern "C" int32_t rc_version(void) { return 3; }
+extern "C" int32_t rc_version(void) { return 4; }
 extern "C" int64_t rc_launch_count(int32_t reset) {
   int64_t v = g_launches;
   if (reset) g_launches = 0;
@@ -936,12 +936,19 @@ extern "C" rc_status rc_composite_tiles(rc_forest* f, const rc_tiling* t, rc_com
   if (!f->d_xcnt) CU(dmalloc((void**)&f->d_xcnt, sizeof(int64_t) * 2 * RC_MAX_RANKS, s));
   if (!f->h_xcnt) CU(cudaMallocHost((void**)&f->h_xcnt, sizeof(int64_t) * 2 * RC_MAX_RANKS));
   CU(cudaMemcpyAsync(f->d_xcnt, f->d_counters + CNT_SEND, sizeof(int64_t) * P, cudaMemcpyDeviceToDevice, s));
-  int r = nccl_alltoall_i64(comm, f->d_xcnt, f->d_xcnt + RC_MAX_RANKS, s);
-  if (r) return fail(RC_ERR_NCCL, "count all-to-all: %s", nccl_error_string(r));
+  int r = 0;
+  if (comm->partners) {   // counts only between the discovered pairs (rc_exchange_partners)
+    CU(cudaMemsetAsync(f->d_xcnt + RC_MAX_RANKS, 0, sizeof(int64_t) * RC_MAX_RANKS, s));
+    r = nccl_partner_i64(comm, f->d_xcnt, f->d_xcnt + RC_MAX_RANKS, s);
+  } else {
+    r = nccl_alltoall_i64(comm, f->d_xcnt, f->d_xcnt + RC_MAX_RANKS, s);
+  }
+  if (r) return fail(RC_ERR_NCCL, "count exchange: %s", nccl_error_string(r));
   CU(cudaMemcpyAsync(f->h_xcnt, f->d_xcnt, sizeof(int64_t) * 2 * RC_MAX_RANKS, cudaMemcpyDeviceToHost, s));
   CU(cudaStreamSynchronize(s));   // the receive sizes (NCCL p2p takes host counts)
   int64_t scnt[RC_MAX_RANKS], rcnt[RC_MAX_RANKS], soff[RC_MAX_RANKS], roff[RC_MAX_RANKS];
   int64_t ts = 0, tr = 0;
+  int missed = -1;   // a destination with records that the partner discovery did not list
   for (int p = 0; p < P; ++p) {
     scnt[p] = f->h_xcnt[p] * (int64_t)sizeof(rc_seg);
     rcnt[p] = f->h_xcnt[RC_MAX_RANKS + p] * (int64_t)sizeof(rc_seg);
@@ -949,6 +956,10 @@ extern "C" rc_status rc_composite_tiles(rc_forest* f, const rc_tiling* t, rc_com
     roff[p] = tr;
     ts += scnt[p];
     tr += rcnt[p];
+    if (comm->partners && p != t->rank && !comm->send_to[p] && scnt[p] > 0) {
+      missed = p;
+      scnt[p] = 0;   // its receiver posts no receive: drop, report after the collective
+    }
   }
   const int64_t nrecv = tr / (int64_t)sizeof(rc_seg);
   CU(grow(&f->d_recv, &f->recv_cap, std::max<int64_t>(nrecv, 1), s));
@@ -956,7 +967,11 @@ extern "C" rc_status rc_composite_tiles(rc_forest* f, const rc_tiling* t, rc_com
                     roff, rcnt, s);
   if (r) return fail(RC_ERR_NCCL, "record exchange: %s", nccl_error_string(r));
   f->h_last_recv = nrecv;
-  return rc_composite_records(f, t, f->d_recv, nrecv, background, d_rgba, capacity_floats, stream);
+  st = rc_composite_records(f, t, f->d_recv, nrecv, background, d_rgba, capacity_floats, stream);
+  if (st == RC_OK && missed >= 0)
+    return fail(RC_ERR_STATE, "rc_composite_tiles: records for rank %d, which the partner discovery did not list",
+                missed);
+  return st;
 }
 
 extern "C" rc_status rc_composite(rc_forest* f, const float background[3], float* d_rgba, int64_t capacity_floats,

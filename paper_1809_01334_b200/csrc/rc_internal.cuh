@@ -238,6 +238,10 @@ enum {
 struct rc_comm {
   void* nccl = nullptr;   // ncclComm_t
   int nranks = 1, rank = 0, device = 0;
+  // exchange partners (rc_comm_set_partners, NEXT(4)): counts and records move
+  // only between discovered pairs instead of an all-to-all
+  bool partners = false;
+  uint8_t send_to[RC_MAX_RANKS] = {}, recv_from[RC_MAX_RANKS] = {};
 };
 
 // ---- kernels / launchers (defined in the .cu files) ----
@@ -247,6 +251,7 @@ const char* nccl_error_string(int r);
 int nccl_exchange(rc_comm* c, const char* sbuf, const int64_t* soff, const int64_t* scnt, char* rbuf,
                   const int64_t* roff, const int64_t* rcnt, cudaStream_t s);
 int nccl_alltoall_i64(rc_comm* c, const int64_t* d_send, int64_t* d_recv, cudaStream_t s);
+int nccl_partner_i64(rc_comm* c, const int64_t* d_send, int64_t* d_recv, cudaStream_t s);
 extern int64_t g_launches;
 cudaError_t scan_exclusive_i64(const int64_t* in, int64_t* out, int64_t n, int64_t* tmp, cudaStream_t s);
 size_t scan_tmp_size(int64_t n);

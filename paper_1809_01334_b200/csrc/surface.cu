@@ -20,12 +20,6 @@
 
 namespace rc {
 
-// X(s) of the tree patch with corners Z [m2][m1][xyz] (TreeConst Bw / Bc)
-__device__ __forceinline__ void patch_point(const double* __restrict__ Z, double s1, double s2, double X[3]) {
-#pragma unroll
-  for (int c = 0; c < 3; ++c)
-    X[c] = (1.0 - s2) * ((1.0 - s1) * Z[c] + s1 * Z[3 + c]) + s2 * ((1.0 - s1) * Z[6 + c] + s1 * Z[9 + c]);
-}
 
 // a2 (surfaces): camera-space AABB of the leaf patch's four corners (a
 // bilinear patch lies in their convex hull) -> pixel-centre rectangle.

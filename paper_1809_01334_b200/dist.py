@@ -236,27 +236,127 @@ def redistribute_rows(tensors, old, new, tp: Transport):
 # ---------------------------------------------------------------------------
 # tile exchange
 # ---------------------------------------------------------------------------
-def exchange_records(send: torch.Tensor, counts: Sequence[int], tp: Transport) -> torch.Tensor:
+def partner_counts(counts: Sequence[int], partners, tp: Transport) -> List[int]:
+    """Record counts between discovered pairs only: one
+    int64 to every listed receiver, one from every listed sender, instead of
+    the count all-to-all.  partners = (send_to, recv_from) rank lists."""
+    send_to, recv_from = partners
+    me = tp.rank
+    missed = [q for q in range(tp.world) if q != me and counts[q] and q not in send_to]
+    if missed:
+        raise RuntimeError(f"records for ranks {missed}, which the partner discovery did not list")
+    out = [0] * tp.world
+    out[me] = int(counts[me])
+    bufs, ops = {}, []
+    for q in send_to:
+        if q != me:
+            bufs[("s", q)] = torch.tensor([int(counts[q])], dtype=torch.int64)
+            ops.append(dist.P2POp(dist.isend, bufs[("s", q)], q, tp.group))
+    for p in recv_from:
+        if p != me:
+            bufs[("r", p)] = torch.zeros(1, dtype=torch.int64)
+            ops.append(dist.P2POp(dist.irecv, bufs[("r", p)], p, tp.group))
+    if ops:
+        for w in dist.batch_isend_irecv(ops):
+            w.wait()
+    for p in recv_from:
+        if p != me:
+            out[p] = int(bufs[("r", p)][0])
+    return out
+
+
+def exchange_records(send: torch.Tensor, counts: Sequence[int], tp: Transport, partners=None) -> torch.Tensor:
     """All-to-all(v) of rc_seg records ([sum(counts), 8] int32, grouped by
-    destination rank); returns the records every rank sent to this one."""
-    rl = tp.counts_all_to_all(counts)
+    destination rank); returns the records every rank sent to this one.
+    partners (send_to, recv_from): counts move between those pairs only."""
+    rl = tp.counts_all_to_all(counts) if partners is None else partner_counts(counts, partners, tp)
     return tp.all_to_all_rows(send, counts, rl)
 
 
 def exchange_and_composite(forest, tiles, world: int, rank: int, comm=None, tp: Transport = None,
-                           background=(0.0, 0.0, 0.0)):
-    """rc_composite_tiles over librc's NCCL communicator (comm), else
-    rc_pack_tiles -> host-staged all-to-all -> rc_composite_records.
-    Returns this rank's tiles [ntiles][th][tw][4]."""
+                           background=(0.0, 0.0, 0.0), partners=None):
+    """rc_composite_tiles over librc's NCCL communicator (comm; partners set on
+    it with Comm.set_partners), else rc_pack_tiles -> host-staged exchange ->
+    rc_composite_records.  Returns this rank's tiles [ntiles][th][tw][4]."""
     tiles_x, tiles_y = tiles
     if comm is not None:
         out, _ = forest.composite_tiles(tiles_x, tiles_y, world, rank, comm=comm, background=background)
         return out
     tp = tp or Transport()
     send, counts = forest.pack_tiles(tiles_x, tiles_y, world, rank)
-    recv = exchange_records(send, counts, tp)
+    recv = exchange_records(send, counts, tp, partners)
     out, _ = forest.composite_tiles(tiles_x, tiles_y, world, rank, recv=recv, background=background)
     return out
+
+
+# ---------------------------------------------------------------------------
+# NEXT(4): partition markers, partner discovery, vforest of several instances
+# ---------------------------------------------------------------------------
+def partition_markers(keys, num_trees: int, tp: Transport):
+    """Partition markers: the tree and anchor of every
+    rank's first leaf, all-gathered once per partition (the metadata every
+    rank keeps).  keys = this rank's (anchor, tree, level) tensors.  Returns
+    the rc_marker list of rc_exchange_partners: an empty rank repeats the next
+    rank's marker, marker 0 = (0, (0,0,0)), marker P = (K, (0,0,0))."""
+    anchor, tree = keys[0], keys[1]
+    has = int(tree.numel() > 0)
+    row = torch.tensor([has, int(tree[0]) if has else 0] + ([int(x) for x in anchor[0]] if has else [0, 0, 0]),
+                       dtype=torch.int64)
+    allm = tp.all_gather(row).cpu().tolist()
+    P = tp.world
+    out = [None] * (P + 1)
+    out[P] = (num_trees, (0, 0, 0))
+    for p in range(P - 1, -1, -1):
+        out[p] = (allm[p][1], tuple(allm[p][2:5])) if allm[p][0] else out[p + 1]
+    first = next((p for p in range(P) if allm[p][0]), P)
+    for p in range(min(first + 1, P)):
+        out[p] = (0, (0, 0, 0))
+    return out
+
+
+def discover_partners(forest, tiles, markers, tp: Transport):
+    """rc_exchange_partners: (send_to, recv_from) of this rank, no communication."""
+    return forest.exchange_partners(tiles[0], tiles[1], tp.world, tp.rank, markers)
+
+
+def vforest_prepartition(forest, cameras, tp: Transport, align_levels: int, consts):
+    """The paper's culling and pre-partition for one or
+    more image instances: per instance camera_set + cull +
+    rc_visible_area_add, then rc_vforest_create (only the leaves some
+    instance sees, weights = visible pixel counts summed over the instances),
+    the weighted SFC cut aligned to node starts and the move of the vforest's
+    leaf rows to their new owners.  Returns (vforest, keys, ranges, stats);
+    the input forest is left as it was (rendering is non-destructive)."""
+    from . import rc
+    w = torch.zeros(forest.n, dtype=torch.int64, device="cuda")
+    for cam in cameras:
+        forest.camera_set(cam)
+        forest.cull()
+        forest.visible_area_add(w)
+    cnt = tp.all_gather(torch.tensor([int((w > 0).sum())], dtype=torch.int64)).flatten().tolist()
+    first = int(sum(cnt[:tp.rank]))
+    n_total = int(sum(cnt))
+    vf, m, wv = forest.vforest(w, first_global_leaf=first)
+    if vf is not None:
+        rows = vf.leaves()
+        vf.close()
+    else:
+        P = forest.P
+        rows = [torch.zeros((0, 3), dtype=torch.int32, device="cuda"), torch.zeros(0, dtype=torch.int32, device="cuda"),
+                torch.zeros(0, dtype=torch.int8, device="cuda"),
+                torch.zeros((0, 4 if forest.surface else (P + 1) ** 3), dtype=torch.float32, device="cuda")]
+    old = [(int(sum(cnt[:p])), int(sum(cnt[:p + 1]))) for p in range(tp.world)]
+    allowed = node_starts(rows[0], rows[1], rows[2], align_levels) if m else torch.zeros(0, dtype=torch.bool)
+    ranges = distributed_aligned_cuts(wv, allowed, first, n_total, tp)
+    rows = redistribute_rows(rows, old, ranges, tp)
+    ctrl, R, P, kappa0, inv_F, q0 = consts[:6]
+    extra = consts[6] if len(consts) > 6 else {}
+    lo, hi = ranges[tp.rank]
+    if hi <= lo:
+        raise RuntimeError("empty vforest range on a rank (too few visible leaves for the ranks)")
+    vf = rc.Forest(ctrl, R, P, *rows, kappa0, inv_F, q0, first_global_leaf=lo, **extra)
+    stats = {"vforest_leaves": n_total, "visible_weight_local": int(wv.sum()) if m else 0, "vforest_ranges": ranges}
+    return vf, rows[:3], ranges, stats
 
 
 def assemble_image(tiles_out: dict, tiles_x: int, tiles_y: int, W: int, H: int) -> torch.Tensor:

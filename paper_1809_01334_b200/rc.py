@@ -70,13 +70,18 @@ class Tiling(C.Structure):
     _fields_ = [("tiles_x", C.c_int32), ("tiles_y", C.c_int32), ("nranks", C.c_int32), ("rank", C.c_int32)]
 
 
+class Marker(C.Structure):
+    _fields_ = [("tree", C.c_int32), ("anchor", C.c_int32 * 3)]
+
+
 SEG_BYTES = 32
 EXPORTS = ["rc_last_error", "rc_version", "rc_forest_create", "rc_forest_destroy", "rc_camera_set", "rc_cull",
            "rc_cull_result", "rc_leaf_weights", "rc_cast_segments", "rc_segments_get", "rc_segments_set",
            "rc_debug_pair", "rc_aggregate", "rc_comm_unique_id", "rc_comm_create", "rc_comm_destroy",
            "rc_pack_tiles", "rc_composite_tiles", "rc_composite_records", "rc_composite", "rc_render_frame",
            "rc_launch_count", "rc_last_cast_ms", "rc_last_phase_ms", "rc_node_table", "rc_pool_trim",
-           "rc_frame_capture", "rc_frame_replay"]
+           "rc_frame_capture", "rc_frame_replay", "rc_exchange_partners", "rc_comm_set_partners",
+           "rc_visible_area_add", "rc_vforest_create", "rc_forest_leaves"]
 
 _lib = None
 
@@ -114,6 +119,11 @@ def lib():
     L.rc_render_frame.argtypes = [vp, C.POINTER(CameraDesc), i32, i32, vp, vp, i64, C.POINTER(i64), vp]
     L.rc_frame_capture.argtypes = [vp, C.POINTER(CameraDesc), vp, vp, i64, vp]
     L.rc_frame_replay.argtypes = [vp, vp]
+    L.rc_exchange_partners.argtypes = [vp, C.POINTER(Tiling), vp, vp, vp]
+    L.rc_comm_set_partners.argtypes = [vp, vp, vp]
+    L.rc_visible_area_add.argtypes = [vp, vp, i64, vp]
+    L.rc_vforest_create.argtypes = [vp, vp, i64, vp, C.POINTER(vp), C.POINTER(i64), vp]
+    L.rc_forest_leaves.argtypes = [vp, vp, vp, vp, vp, i64, vp]
     L.rc_launch_count.argtypes = [i32]
     L.rc_launch_count.restype = i64
     L.rc_last_cast_ms.argtypes = [vp]
@@ -396,6 +406,51 @@ class Forest:
     def last_cast_ms(self):
         return float(lib().rc_last_cast_ms(self.h))
 
+    # -- NEXT(4): partner discovery, image instances, vforest -------------
+    def exchange_partners(self, tiles_x, tiles_y, nranks, rank, markers, send=True, recv=True):
+        """rc_exchange_partners: markers = [(tree, (ax, ay, az))] * (nranks + 1).
+        Returns (send_to, recv_from): lists of ranks (None when not asked)."""
+        t = Tiling(tiles_x, tiles_y, nranks, rank)
+        mk = (Marker * (nranks + 1))()
+        for p, (tr, a) in enumerate(markers):
+            mk[p].tree = int(tr)
+            mk[p].anchor[:] = [int(x) for x in a]
+        so = (C.c_uint8 * nranks)()
+        ro = (C.c_uint8 * nranks)()
+        _check(lib().rc_exchange_partners(self.h, C.byref(t), mk, so if send else None, ro if recv else None))
+        return ([q for q in range(nranks) if so[q]] if send else None,
+                [p for p in range(nranks) if ro[p]] if recv else None)
+
+    def visible_area_add(self, w, stream=None):
+        """w (int64 CUDA tensor [n]) += pixel-centre rectangle area of every leaf in the last cull."""
+        _check(lib().rc_visible_area_add(self.h, C.c_void_p(w.data_ptr()), w.numel(), _stream(stream)))
+        return w
+
+    def leaves(self, stream=None):
+        """rc_forest_leaves: (anchor [n,3] int32, tree int32, level int8, field [n,nf] f32) CUDA tensors."""
+        import torch
+        nf = 4 if self.surface else (self.P + 1) ** 3
+        out = [torch.empty((self.n, 3), dtype=torch.int32, device="cuda"),
+               torch.empty(self.n, dtype=torch.int32, device="cuda"),
+               torch.empty(self.n, dtype=torch.int8, device="cuda"),
+               torch.empty((self.n, nf), dtype=torch.float32, device="cuda")]
+        _check(lib().rc_forest_leaves(self.h, *[C.c_void_p(t.data_ptr()) for t in out], self.n, _stream(stream)))
+        return out
+
+    def vforest(self, w, first_global_leaf=0, stream=None):
+        """rc_vforest_create: (Forest of the leaves with w > 0 or None, count, their weights)."""
+        import torch
+        h = C.c_void_p()
+        cnt = C.c_int64()
+        wout = torch.zeros(self.n, dtype=torch.int64, device="cuda")
+        _check(lib().rc_vforest_create(self.h, C.c_void_p(w.data_ptr()), int(first_global_leaf), _stream(stream),
+                                       C.byref(h), C.byref(cnt), C.c_void_p(wout.data_ptr())))
+        if cnt.value == 0:
+            return None, 0, wout[:0]
+        vf = Forest.__new__(Forest)
+        vf.h, vf.n, vf.P, vf.R, vf.surface, vf.cam = h, int(cnt.value), self.P, self.R, self.surface, None
+        return vf, int(cnt.value), wout[:cnt.value]
+
     def last_phase_ms(self, phase):
         return float(lib().rc_last_phase_ms(self.h, int(phase)))
 
@@ -419,6 +474,15 @@ class Comm:
         _check(lib().rc_comm_create(C.byref(uid), int(nranks), int(rank), _stream(stream), C.byref(h)))
         self.h = h
         self.nranks, self.rank = int(nranks), int(rank)
+
+    def set_partners(self, send_to=None, recv_from=None):
+        """rc_comm_set_partners: exchanges only between the listed ranks (None: all-to-all)."""
+        if send_to is None:
+            _check(lib().rc_comm_set_partners(self.h, None, None))
+            return
+        so = (C.c_uint8 * self.nranks)(*[1 if q in set(send_to) else 0 for q in range(self.nranks)])
+        ro = (C.c_uint8 * self.nranks)(*[1 if p in set(recv_from) else 0 for p in range(self.nranks)])
+        _check(lib().rc_comm_set_partners(self.h, so, ro))
 
     def close(self):
         if getattr(self, "h", None):

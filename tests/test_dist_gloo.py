@@ -213,3 +213,60 @@ def test_move_plan_contiguous():
     assert rdist.move_plan(old, new, 0) == ([4, 6, 0], [4, 0, 0])
     assert rdist.move_plan(old, new, 1) == ([0, 10, 0], [6, 10, 5])
     assert rdist.move_plan(old, new, 2) == ([0, 5, 5], [0, 0, 5])
+
+
+def _partner_fn(rank, world):
+    """Counts only between listed pairs (NEXT(4)): the
+    partner relation {(p, q): (p + 2 q) % 3 != 0}; the records received equal
+    those of the all-to-all path, and a record for an unlisted writer is an
+    error."""
+    rel = {(p, q) for p in range(world) for q in range(world) if (p + 2 * q) % 3 != 0 or p == q}
+    send_to = [q for q in range(world) if (rank, q) in rel]
+    recv_from = [p for p in range(world) if (p, rank) in rel]
+    counts = [(rank + 2 * d + 1) if (rank, d) in rel else 0 for d in range(world)]
+    rows = [[rank, d, k, 0, 0, 0, 0, rank * 100 + d * 10 + k] for d in range(world) for k in range(counts[d])]
+    send = torch.tensor(rows, dtype=torch.int32).reshape(-1, 8)
+    tp = rdist.Transport()
+    a = rdist.exchange_records(send, counts, tp, partners=(send_to, recv_from)).numpy()
+    b = rdist.exchange_records(send, counts, tp).numpy()
+    bad = list(counts)
+    q_unlisted = next((q for q in range(world) if (rank, q) not in rel), None)
+    raised = None
+    if q_unlisted is not None:
+        bad[q_unlisted] += 1
+        try:
+            rdist.partner_counts(bad, (send_to, recv_from), tp)
+            raised = False
+        except RuntimeError:
+            raised = True
+    return a, b, raised
+
+
+def test_exchange_with_partners_gloo():
+    out = _spawn(_partner_fn, 3)
+    for rank, (a, b, raised) in out.items():
+        assert np.array_equal(a, b)
+        assert len(a) > 0
+        assert raised in (None, True)
+
+
+def _markers_fn(rank, world):
+    import scenegen as sg
+    sc = sg.shell_uniform(2, 16, 4)
+    cuts = [0, 100, 100, sc.num_leaves]   # rank 1 holds no leaves
+    lo, hi = cuts[rank], cuts[rank + 1]
+    keys = (torch.as_tensor(sc.leaf_anchor[lo:hi]), torch.as_tensor(sc.leaf_tree[lo:hi]),
+            torch.as_tensor(sc.leaf_level[lo:hi]))
+    return rdist.partition_markers(keys, sc.num_trees, rdist.Transport())
+
+
+def test_partition_markers_gloo():
+    """dist.partition_markers (all-gathered first leaves) equals the oracle's
+    markers of the same cuts, including an empty rank."""
+    import scenegen as sg
+    from oracle import partition as op
+    sc = sg.shell_uniform(2, 16, 4)
+    want = op.markers(sc, [0, 100, 100, sc.num_leaves])
+    out = _spawn(_markers_fn, 3)
+    for rank, mk in out.items():
+        assert [op.sfc_key(t, a) for t, a in mk] == want

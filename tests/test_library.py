@@ -22,7 +22,7 @@ def test_build_and_exports():
     for n in names:
         assert hasattr(lib, n), f"librc.so does not export {n}"
     lib.rc_version.restype = ctypes.c_int32
-    assert lib.rc_version() == 3
+    assert lib.rc_version() == 4
 
 
 def test_binding_covers_header():
