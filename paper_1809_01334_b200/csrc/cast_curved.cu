@@ -614,144 +614,189 @@ __device__ __forceinline__ void prep_bounds(const float* __restrict__ slw, const
 }
 
 constexpr int PREP_E = 32;
-#ifndef PREP_MINB
-#define PREP_MINB 1
-#endif
+constexpr int PREP_CTAS_PER_SM = 5;   // <= 128 registers x 96 threads; ~31 KB shared memory
+__device__ __forceinline__ void cp_async4(void* dst, const void* src) {
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 4;" ::"r"(smem_addr(dst)), "l"(src) : "memory");
+}
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
+__device__ __forceinline__ void cp_async_wait_all() { asm volatile("cp.async.wait_group 0;" ::: "memory"); }
+
+// Persistent CTAs over groups of PREP_E visible leaves, software-pipelined:
+// while group g is computed, the keys and nodal field of group g + G and the
+// visible-list entries of group g + 2G (G = gridDim.x) are in flight as
+// cp.async copies into the other buffer (the loads are dependent gathers,
+// vis -> leaf -> field, that 15 resident warps per SM cannot hide otherwise).
 template <int P>
-__global__ void __launch_bounds__(3 * PREP_E, PREP_MINB) k_prep_slots(const TreeConst* __restrict__ trees, DevLeafView L,
-                                                           const int32_t* __restrict__ vis,
-                                                           const int64_t* __restrict__ nvis_p, int64_t v0, int64_t v1,
-                                                           float4* __restrict__ gslot, double* __restrict__ gorg) {
+__global__ void __launch_bounds__(3 * PREP_E, PREP_CTAS_PER_SM) k_prep_slots(
+    const TreeConst* __restrict__ trees, DevLeafView L, const int32_t* __restrict__ vis,
+    const int64_t* __restrict__ nvis_p, int64_t v0, int64_t v1, float4* __restrict__ gslot,
+    double* __restrict__ gorg) {
   constexpr int NF = (P + 1) * (P + 1) * (P + 1);
   __shared__ __align__(16) float sl[PREP_E][SLOT_STRIDE];
+  __shared__ float sfb[2][PREP_E][NF];   // nodal fields in flight (copied into the slots per group)
   __shared__ double so[PREP_E][4];
   __shared__ float sJ[PREP_E][12];     // Xc[3], J[3][3]
   __shared__ float sb[PREP_E][2][3];   // per coordinate thread: dp_c, eta part
+  __shared__ int32_t seb[2][PREP_E];   // visible-list entries (leaf indices) of the next two groups
+  __shared__ int32_t skb[2][PREP_E][6];  // tree, level word, anchor[3], level byte offset
   const int64_t vend = min(v1, *nvis_p);
-  const int64_t vb = v0 + (int64_t)blockIdx.x * PREP_E;
-  if (vb >= vend) return;
-  const int nloc = (int)min((int64_t)PREP_E, vend - vb);
-  __shared__ int32_t se[PREP_E], skey[PREP_E][5];   // leaf index; tree, level, anchor[3]
+  const int64_t ngroups = (vend - v0 + PREP_E - 1) / PREP_E;
+  const int64_t G = gridDim.x;
   const int c = threadIdx.x >> 5, w = threadIdx.x & 31;
-  const bool act = w < nloc;
-  float* slw = sl[w];
-  // the CTA's leaf keys and fields, all loads in flight at once (no dependent chains per thread)
-  if (threadIdx.x < nloc) se[threadIdx.x] = vis[vb + threadIdx.x];
+  auto group_n = [&](int64_t g) -> int { return (int)min((int64_t)PREP_E, vend - (v0 + g * PREP_E)); };
+  // stage the visible-list entries of group g into seb[b]
+  auto issue_vis = [&](int64_t g, int b) {
+    if (g < ngroups && threadIdx.x < group_n(g)) cp_async4(&seb[b][threadIdx.x], &vis[v0 + g * PREP_E + threadIdx.x]);
+  };
+  // stage keys and field of group g (leaf indices in seb[b]) into buffer b
+  auto issue_data = [&](int64_t g, int b) {
+    if (g >= ngroups) return;
+    const int nl = group_n(g);
+    for (int k = threadIdx.x; k < nl * 5; k += 3 * PREP_E) {
+      const int ew = k / 5, q = k - ew * 5;
+      const int64_t e = seb[b][ew];
+      const void* src = q == 0 ? (const void*)&L.tree[e]
+                        : (q == 1 ? (const void*)(L.level + (e & ~(int64_t)3)) : (const void*)&L.anchor[3 * e + q - 2]);
+      cp_async4(&skb[b][ew][q], src);
+    }
+    for (int k = threadIdx.x; k < nl * NF; k += 3 * PREP_E) {
+      const int ew = k / NF, q = k - ew * NF;
+      cp_async4(&sfb[b][ew][q], &L.field[(int64_t)seb[b][ew] * NF + q]);
+    }
+  };
+  int64_t g = blockIdx.x;
+  if (g >= ngroups) return;
+  // prologue: entries of g and g + G, data of g
+  issue_vis(g, 0);
+  cp_async_commit();
+  cp_async_wait_all();
   __syncthreads();
-  for (int k = threadIdx.x; k < nloc * 5; k += 3 * PREP_E) {
-    const int ew = k / 5, q = k - ew * 5;
-    const int64_t e = se[ew];
-    skey[ew][q] = q == 0 ? L.tree[e] : (q == 1 ? (int32_t)L.level[e] : L.anchor[3 * e + q - 2]);
-  }
-  for (int k = threadIdx.x; k < nloc * NF; k += 3 * PREP_E) {
-    const int ew = k / NF, q = k - ew * NF;
-    sl[ew][SLOT_FIELD + FI(q, NF)] = __ldg(&L.field[(int64_t)se[ew] * NF + q]);
-  }
-  __syncthreads();
-  // 1. restriction (fp64), coordinate c
-  if (act) {
-    const double h = ldexp(1.0, -skey[w][1]);
-    const double* __restrict__ Bw = trees[skey[w][0]].Bw;   // [q3][q2][q1][xyz]
-    double uu[3];
-#pragma unroll
-    for (int k = 0; k < 3; ++k) uu[k] = ldexp((double)skey[w][2 + k], -RC_MAXLEVEL);
-    auto Mrow = [&](int k, int r, double m[3]) {   // blossom row r of axis k
-      const double u = uu[k], v = u + h;
-      const double x = r == 2 ? v : u, y = r == 0 ? u : v;
-      m[0] = (1 - x) * (1 - y);
-      m[1] = (1 - x) * y + x * (1 - y);
-      m[2] = x * y;
-    };
-    double m0[3], m1[3], m2[3];
-    Mrow(0, 1, m0);
-    Mrow(1, 1, m1);
-    Mrow(2, 1, m2);
-    double o = 0.0;   // origin = point (1,1,1)
-#pragma unroll
-    for (int q3 = 0; q3 < 3; ++q3)
-#pragma unroll
-      for (int q2 = 0; q2 < 3; ++q2) {
-        const double w23 = m2[q3] * m1[q2];
-#pragma unroll
-        for (int q1 = 0; q1 < 3; ++q1) o = fma(w23 * m0[q1], Bw[((q3 * 3 + q2) * 3 + q1) * 3 + c], o);
-      }
-    so[w][c] = o;
-    if (c == 0) so[w][3] = 0.0;
-    double M0[3][3];
-#pragma unroll
-    for (int r = 0; r < 3; ++r) Mrow(0, r, M0[r]);
-#pragma unroll
-    for (int r3 = 0; r3 < 3; ++r3) {
-      double m3[3];
-      Mrow(2, r3, m3);
-      double T2[9];
-#pragma unroll
-      for (int q21 = 0; q21 < 9; ++q21) {
-        double acc = 0.0;
-#pragma unroll
-        for (int q3 = 0; q3 < 3; ++q3) acc = fma(m3[q3], Bw[(q3 * 9 + q21) * 3 + c], acc);
-        T2[q21] = acc;
-      }
-#pragma unroll
-      for (int r2 = 0; r2 < 3; ++r2) {
-        double mm2[3];
-        Mrow(1, r2, mm2);
-        double T1[3];
-#pragma unroll
-        for (int q1 = 0; q1 < 3; ++q1) {
-          double acc = 0.0;
-#pragma unroll
-          for (int q2 = 0; q2 < 3; ++q2) acc = fma(mm2[q2], T2[q2 * 3 + q1], acc);
-          T1[q1] = acc;
+  issue_data(g, 0);
+  issue_vis(g + G, 1);
+  cp_async_commit();
+  for (int cb = 0; g < ngroups; g += G, cb ^= 1) {
+    const int nb = cb ^ 1;
+    cp_async_wait_all();
+    __syncthreads();   // group g's data and group g + G's entries have landed
+    const int nloc = group_n(g);
+    const int64_t vb = v0 + g * PREP_E;
+    if (threadIdx.x < PREP_E) skb[cb][threadIdx.x][5] = (int32_t)(seb[cb][threadIdx.x] & 3);
+    for (int k = threadIdx.x; k < nloc * NF; k += 3 * PREP_E) {
+      const int ew = k / NF, q = k - ew * NF;
+      sl[ew][SLOT_FIELD + FI(q, NF)] = sfb[cb][ew][q];
+    }
+    issue_data(g + G, nb);      // the next group's gathers fly while this one computes
+    __syncthreads();
+    issue_vis(g + 2 * G, cb);   // seb[cb] is free once the level offsets are taken
+    cp_async_commit();
+    const bool act = w < nloc;
+    float* slw = sl[w];
+    // 1. restriction (fp64), coordinate c
+    if (act) {
+      const double h = ldexp(1.0, -(int)(int8_t)(skb[cb][w][1] >> (8 * skb[cb][w][5])));
+      const double* __restrict__ Bw = trees[skb[cb][w][0]].Bw;   // [q3][q2][q1][xyz]
+      double uu[3];
+  #pragma unroll
+      for (int k = 0; k < 3; ++k) uu[k] = ldexp((double)skb[cb][w][2 + k], -RC_MAXLEVEL);
+      auto Mrow = [&](int k, int r, double m[3]) {   // blossom row r of axis k
+        const double u = uu[k], v = u + h;
+        const double x = r == 2 ? v : u, y = r == 0 ? u : v;
+        m[0] = (1 - x) * (1 - y);
+        m[1] = (1 - x) * y + x * (1 - y);
+        m[2] = x * y;
+      };
+      double m0[3], m1[3], m2[3];
+      Mrow(0, 1, m0);
+      Mrow(1, 1, m1);
+      Mrow(2, 1, m2);
+      double o = 0.0;   // origin = point (1,1,1)
+  #pragma unroll
+      for (int q3 = 0; q3 < 3; ++q3)
+  #pragma unroll
+        for (int q2 = 0; q2 < 3; ++q2) {
+          const double w23 = m2[q3] * m1[q2];
+  #pragma unroll
+          for (int q1 = 0; q1 < 3; ++q1) o = fma(w23 * m0[q1], Bw[((q3 * 3 + q2) * 3 + q1) * 3 + c], o);
         }
-#pragma unroll
-        for (int r1 = 0; r1 < 3; ++r1) {
+      so[w][c] = o;
+      if (c == 0) so[w][3] = 0.0;
+      double M0[3][3];
+  #pragma unroll
+      for (int r = 0; r < 3; ++r) Mrow(0, r, M0[r]);
+  #pragma unroll
+      for (int r3 = 0; r3 < 3; ++r3) {
+        double m3[3];
+        Mrow(2, r3, m3);
+        double T2[9];
+  #pragma unroll
+        for (int q21 = 0; q21 < 9; ++q21) {
           double acc = 0.0;
-#pragma unroll
-          for (int q1 = 0; q1 < 3; ++q1) acc = fma(M0[r1][q1], T1[q1], acc);
-          slw[GI((r3 * 3 + r2) * 3 + r1) + c] = (float)(acc - o);
+  #pragma unroll
+          for (int q3 = 0; q3 < 3; ++q3) acc = fma(m3[q3], Bw[(q3 * 9 + q21) * 3 + c], acc);
+          T2[q21] = acc;
+        }
+  #pragma unroll
+        for (int r2 = 0; r2 < 3; ++r2) {
+          double mm2[3];
+          Mrow(1, r2, mm2);
+          double T1[3];
+  #pragma unroll
+          for (int q1 = 0; q1 < 3; ++q1) {
+            double acc = 0.0;
+  #pragma unroll
+            for (int q2 = 0; q2 < 3; ++q2) acc = fma(mm2[q2], T2[q2 * 3 + q1], acc);
+            T1[q1] = acc;
+          }
+  #pragma unroll
+          for (int r1 = 0; r1 < 3; ++r1) {
+            double acc = 0.0;
+  #pragma unroll
+            for (int q1 = 0; q1 < 3; ++q1) acc = fma(M0[r1][q1], T1[q1], acc);
+            slw[GI((r3 * 3 + r2) * 3 + r1) + c] = (float)(acc - o);
+          }
         }
       }
     }
+    __syncthreads();
+    // 2. affine model at the centre, row c (fp32); 3. J0^-1, dp_c and the eta
+    // part along axis c.  Per coordinate a fully unrolled instance (constant
+    // indices: no integer division or selects in the loops over the 27 points).
+    switch (c) {   // warp-uniform
+      case 0: prep_affine<0>(slw, sJ[w], act); break;
+      case 1: prep_affine<1>(slw, sJ[w], act); break;
+      default: prep_affine<2>(slw, sJ[w], act); break;
+    }
+    __syncthreads();
+    float Ji[3][3];
+    switch (c) {
+      case 0: prep_bounds<0>(slw, sJ[w], sb[w], Ji, act); break;
+      case 1: prep_bounds<1>(slw, sJ[w], sb[w], Ji, act); break;
+      default: prep_bounds<2>(slw, sJ[w], sb[w], Ji, act); break;
+    }
+    __syncthreads();
+    if (act && c == 0) {
+      float* af = slw + SLOT_AFF;
+      af[0] = sJ[w][0];
+      af[1] = sJ[w][1];
+      af[2] = sJ[w][2];
+  #pragma unroll
+      for (int i = 0; i < 3; ++i)
+  #pragma unroll
+        for (int a = 0; a < 3; ++a) af[3 + 3 * i + a] = Ji[i][a];
+      // inflate by a rounding margin relative to the element (fp32)
+      af[12] = sb[w][0][0] * 1.001f + 1e-5f;
+      af[13] = sb[w][0][1] * 1.001f + 1e-5f;
+      af[14] = sb[w][0][2] * 1.001f + 1e-5f;
+      af[15] = fmaxf(sb[w][1][0], fmaxf(sb[w][1][1], sb[w][1][2])) * 1.001f + 1e-5f;
+    }
+    __syncthreads();
+    constexpr int Q = SLOT_USED / 4;   // float4 per slot
+    float4* dst = gslot + (vb - v0) * Q;
+    for (int k = threadIdx.x; k < nloc * Q; k += 3 * PREP_E) dst[k] = reinterpret_cast<const float4*>(sl[k / Q])[k % Q];
+    double* od = gorg + (vb - v0) * 4;
+    for (int k = threadIdx.x; k < nloc * 4; k += 3 * PREP_E) od[k] = so[k / 4][k % 4];
   }
-  __syncthreads();
-  // 2. affine model at the centre, row c (fp32); 3. J0^-1, dp_c and the eta
-  // part along axis c.  Per coordinate a fully unrolled instance (constant
-  // indices: no integer division or selects in the loops over the 27 points).
-  switch (c) {   // warp-uniform
-    case 0: prep_affine<0>(slw, sJ[w], act); break;
-    case 1: prep_affine<1>(slw, sJ[w], act); break;
-    default: prep_affine<2>(slw, sJ[w], act); break;
-  }
-  __syncthreads();
-  float Ji[3][3];
-  switch (c) {
-    case 0: prep_bounds<0>(slw, sJ[w], sb[w], Ji, act); break;
-    case 1: prep_bounds<1>(slw, sJ[w], sb[w], Ji, act); break;
-    default: prep_bounds<2>(slw, sJ[w], sb[w], Ji, act); break;
-  }
-  __syncthreads();
-  if (act && c == 0) {
-    float* af = slw + SLOT_AFF;
-    af[0] = sJ[w][0];
-    af[1] = sJ[w][1];
-    af[2] = sJ[w][2];
-#pragma unroll
-    for (int i = 0; i < 3; ++i)
-#pragma unroll
-      for (int a = 0; a < 3; ++a) af[3 + 3 * i + a] = Ji[i][a];
-    // inflate by a rounding margin relative to the element (fp32)
-    af[12] = sb[w][0][0] * 1.001f + 1e-5f;
-    af[13] = sb[w][0][1] * 1.001f + 1e-5f;
-    af[14] = sb[w][0][2] * 1.001f + 1e-5f;
-    af[15] = fmaxf(sb[w][1][0], fmaxf(sb[w][1][1], sb[w][1][2])) * 1.001f + 1e-5f;
-  }
-  __syncthreads();
-  constexpr int Q = SLOT_USED / 4;   // float4 per slot
-  float4* dst = gslot + (vb - v0) * Q;
-  for (int k = threadIdx.x; k < nloc * Q; k += 3 * PREP_E) dst[k] = reinterpret_cast<const float4*>(sl[k / Q])[k % Q];
-  double* od = gorg + (vb - v0) * 4;
-  for (int k = threadIdx.x; k < nloc * 4; k += 3 * PREP_E) od[k] = so[k / 4][k % 4];
+  cp_async_wait_all();
 }
 
 // per-CTA global scratch (bytes)
@@ -1842,7 +1887,9 @@ cudaError_t launch_prep_slots(const TreeConst* trees, DevLeafView L, int P, cons
                               const int64_t* nvis_p, int64_t v0, int64_t v1, void* gslot, void* gorg,
                               cudaStream_t s) {
   if (v1 <= v0) return cudaSuccess;
-  const unsigned grid = (unsigned)((v1 - v0 + PREP_E - 1) / PREP_E);
+  static int sms = 0;
+  if (!sms) cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, 0);
+  const unsigned grid = (unsigned)std::min<int64_t>((v1 - v0 + PREP_E - 1) / PREP_E, (int64_t)sms * PREP_CTAS_PER_SM);
   if (P == 1)
     k_prep_slots<1><<<grid, 3 * PREP_E, 0, s>>>(trees, L, vis, nvis_p, v0, v1, (float4*)gslot, (double*)gorg);
   else

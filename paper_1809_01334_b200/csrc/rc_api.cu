@@ -140,7 +140,7 @@ extern "C" rc_status rc_forest_create(const rc_forest_desc* d, void* stream, rc_
     return cleanup(RC_ERR_OUT_OF_MEMORY, "cudaMalloc " #ptr);
   ALLOC(f->d_anchor, sizeof(int32_t) * 3 * n);
   ALLOC(f->d_tree, sizeof(int32_t) * n);
-  ALLOC(f->d_level, sizeof(int8_t) * n);
+  ALLOC(f->d_level, sizeof(int8_t) * ((n + 3) & ~(int64_t)3));   // whole words: k_prep_slots stages the level bytes with 4-byte copies
   if (f->has_field) ALLOC(f->d_field, sizeof(float) * NF * n);
   ALLOC(f->d_flag, sizeof(int32_t) * n);
   ALLOC(f->d_rect_all, sizeof(Rect16) * n);
