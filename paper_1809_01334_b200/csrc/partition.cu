@@ -152,6 +152,7 @@ struct Traversal {
 
 extern "C" rc_status rc_exchange_partners(rc_forest* f, const rc_tiling* t, const rc_marker* h_markers,
                                           uint8_t* h_send_to, uint8_t* h_recv_from) {
+  RC_NVTX("rc_exchange_partners");
   if (!f || !t || !h_markers) return rc_fail(RC_ERR_INVALID_ARG, "rc_exchange_partners: null argument");
   if (!f->have_camera) return rc_fail(RC_ERR_STATE, "rc_exchange_partners before rc_camera_set");
   const int P = t->nranks;

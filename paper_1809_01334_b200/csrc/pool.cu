@@ -112,6 +112,19 @@ void dfree(void* p, cudaStream_t s, bool idle) {
   g_free.insert({Key{current_device(), it->second}, c});
 }
 
+size_t device_free_bytes() {
+  size_t free_b = 0, total_b = 0;
+  if (cudaMemGetInfo(&free_b, &total_b) != cudaSuccess) {
+    cudaGetLastError();
+    return 0;
+  }
+  const int dev = current_device();
+  std::lock_guard<std::mutex> lk(g_mu);
+  for (auto& kv : g_free)
+    if (kv.first.dev == dev) free_b += kv.first.size;   // cached blocks are released on demand
+  return free_b;
+}
+
 void dtrim() {
   std::lock_guard<std::mutex> lk(g_mu);
   release_cached_locked();

@@ -69,6 +69,7 @@ static uint64_t spread18(uint32_t v) {
 }
 
 extern "C" rc_status rc_forest_create(const rc_forest_desc* d, void* stream, rc_forest** out) {
+  RC_NVTX("rc_forest_create");
   if (!d || !out) return fail(RC_ERR_INVALID_ARG, "rc_forest_create: null argument");
   *out = nullptr;
   if (d->num_trees < 1 || d->num_trees > RC_MAX_TREES) return fail(RC_ERR_INVALID_ARG, "num_trees out of range");
@@ -276,6 +277,7 @@ static void mat3_inv(const double A[9], double inv[9], double* det_out) {
 }
 
 extern "C" rc_status rc_camera_set(rc_forest* f, const rc_camera* cam, void* stream) {
+  RC_NVTX("rc_camera_set");
   if (!f || !cam) return fail(RC_ERR_INVALID_ARG, "rc_camera_set: null argument");
   auto dot = [](const double* a, const double* b) { return a[0] * b[0] + a[1] * b[1] + a[2] * b[2]; };
   double n = sqrt(dot(cam->view, cam->view));
@@ -469,6 +471,7 @@ static DevLeafView leaf_view(rc_forest* f) { return DevLeafView{f->d_anchor, f->
 static unsigned blocks_for(int64_t n, int threads) { return (unsigned)((n + threads - 1) / threads); }
 
 extern "C" rc_status rc_cull(rc_forest* f, void* stream, int64_t* d_num_visible) {
+  RC_NVTX("rc_cull");
   if (!f) return fail(RC_ERR_INVALID_ARG, "rc_cull: null forest");
   if (!f->have_camera) return fail(RC_ERR_STATE, "rc_cull before rc_camera_set");
   cudaStream_t s = (cudaStream_t)stream;
@@ -530,6 +533,7 @@ static int sm_count() {
 static rc_status aggregate_to(rc_forest* f, int level, cudaStream_t s);
 
 extern "C" rc_status rc_cast_segments(rc_forest* f, int32_t fold_levels, void* stream) {
+  RC_NVTX("rc_cast_segments");
   if (!f) return fail(RC_ERR_INVALID_ARG, "rc_cast_segments: null forest");
   if (!f->have_cull) return fail(RC_ERR_STATE, "rc_cast_segments before rc_cull");
   if (!f->has_field) return fail(RC_ERR_STATE, "rc_cast_segments on a forest without a field (keys only)");
@@ -589,15 +593,23 @@ extern "C" rc_status rc_cast_segments(rc_forest* f, int32_t fold_levels, void* s
     std::swap(f->seg_cap, f->seg2_cap);
   }
   // first-frame estimate (C3-C5: fold-2 records are 1/7..1/4 of the candidates,
-  // raw segments ~1/2), capped by the free device memory so that a forest
-  // near the memory limit falls back to the exact regrowth instead of failing
+  // raw segments ~1/2), capped by the free device memory less what the
+  // element slots and the aggregation / composite buffers need (the slots'
+  // batch, 1/8 of the estimate and 2 GB), so that a forest near the memory
+  // limit falls back to the exact regrowth instead of failing.  A short
+  // buffer costs a second cast (C5's first frame: 5.1 s instead of 2.7 s with
+  // a cap of half the free memory).
   int64_t est = curved ? (fold_levels > 0 ? cand / 4 : cand / 2 + cand / 8) : cand;
   if (f->h_cast_total > 0) est = 0;   // later frames: the previous count (+1/8), exact regrowth if short
   else {
-    size_t free_b = 0, total_b = 0;
-    if (cudaMemGetInfo(&free_b, &total_b) == cudaSuccess) {
-      const int64_t cap = (int64_t)(free_b / 2 / sizeof(rc_seg)) + f->seg_cap;
-      est = std::min(est, cap);
+    const size_t free_b = device_free_bytes();
+    if (free_b > 0) {
+      const int64_t slot_b = curved ? (int64_t)slot_record_bytes() *
+                                          std::min<int64_t>(nvis + RC_UNIT_LEAVES, RC_SLOT_BATCH + RC_UNIT_LEAVES)
+                                    : 0;
+      const int64_t avail = (int64_t)free_b - slot_b - ((int64_t)2 << 30);
+      const int64_t cap = std::max<int64_t>(avail / (int64_t)(sizeof(rc_seg) + sizeof(rc_seg) / 8), 0) + f->seg_cap;
+      est = std::min(est, std::max<int64_t>(cap, (int64_t)(free_b / 2 / sizeof(rc_seg)) + f->seg_cap));
     }
   }
   int64_t need = std::max<int64_t>(f->h_cast_total + f->h_cast_total / 32, est) + 4096;
@@ -608,8 +620,8 @@ extern "C" rc_status rc_cast_segments(rc_forest* f, int32_t fold_levels, void* s
   if (curved) {
     int64_t want = std::min<int64_t>(nvis + RC_UNIT_LEAVES, RC_SLOT_BATCH + RC_UNIT_LEAVES);
     if (f->slot_cap < want) {
-      size_t free_b = 0, total_b = 0;
-      if (cudaMemGetInfo(&free_b, &total_b) == cudaSuccess) {
+      const size_t free_b = device_free_bytes();
+      if (free_b > 0) {
         const int64_t fit = (int64_t)(free_b / 3 / slot_record_bytes());
         want = std::max<int64_t>(std::min(want, fit), std::min<int64_t>(want, ((int64_t)1 << 20) + RC_UNIT_LEAVES));
       }
@@ -821,6 +833,7 @@ extern "C" rc_status rc_pack_tiles(rc_forest* f, const rc_tiling* t, int64_t* h_
 extern "C" rc_status rc_composite_records(rc_forest* f, const rc_tiling* t, const rc_seg* d_recv, int64_t nrecv,
                                           const float background[3], float* d_rgba, int64_t capacity_floats,
                                           void* stream) {
+  RC_NVTX("rc_composite_records");
   if (!f || !d_rgba) return fail(RC_ERR_INVALID_ARG, "rc_composite_records: null argument");
   if (!f->have_camera) return fail(RC_ERR_STATE, "rc_composite_records before rc_camera_set");
   if (nrecv < 0 || (nrecv > 0 && !d_recv)) return fail(RC_ERR_INVALID_ARG, "rc_composite_records: bad records");
@@ -864,10 +877,8 @@ extern "C" rc_status rc_composite_records(rc_forest* f, const rc_tiling* t, cons
   // the fold), else a permutation of record indices
   bool copy = false;
   {
-    size_t free_b = 0, total_b = 0;
     const size_t have = f->sorted_cap >= nsrc ? (size_t)-1 : 0;
-    if (have || (cudaMemGetInfo(&free_b, &total_b) == cudaSuccess &&
-                 free_b > (size_t)nsrc * sizeof(rc_seg) + ((size_t)2 << 30)))
+    if (have || device_free_bytes() > (size_t)nsrc * sizeof(rc_seg) + ((size_t)2 << 30))
       copy = grow(&f->d_sorted, &f->sorted_cap, std::max<int64_t>(nsrc, 1), s) == cudaSuccess;
   }
   f->last_composite_copy = copy ? 1 : 0;
@@ -920,6 +931,7 @@ extern "C" rc_status rc_composite_records(rc_forest* f, const rc_tiling* t, cons
 
 extern "C" rc_status rc_composite_tiles(rc_forest* f, const rc_tiling* t, rc_comm* comm, const float background[3],
                                         float* d_rgba, int64_t capacity_floats, void* stream) {
+  RC_NVTX("rc_composite_tiles");
   if (!f || !t) return fail(RC_ERR_INVALID_ARG, "rc_composite_tiles: null argument");
   if (!comm) return rc_composite_records(f, t, nullptr, 0, background, d_rgba, capacity_floats, stream);
   if (!f->have_cast) return fail(RC_ERR_STATE, "rc_composite_tiles before rc_cast_segments");
@@ -1045,6 +1057,7 @@ static rc_status aggregate_to(rc_forest* f, int level, cudaStream_t s) {
 }
 
 extern "C" rc_status rc_aggregate(rc_forest* f, int32_t cycles, void* stream) {
+  RC_NVTX("rc_aggregate");
   if (!f) return fail(RC_ERR_INVALID_ARG, "rc_aggregate: null forest");
   if (cycles < 0) return fail(RC_ERR_INVALID_ARG, "cycles must be >= 0");
   if (cycles == 0) return RC_OK;
@@ -1056,6 +1069,7 @@ extern "C" rc_status rc_aggregate(rc_forest* f, int32_t cycles, void* stream) {
 }
 
 extern "C" rc_status rc_segments_set(rc_forest* f, const rc_seg* d_recs, int64_t n, int32_t level, void* stream) {
+  RC_NVTX("rc_segments_set");
   if (!f || (n > 0 && !d_recs) || n < 0) return fail(RC_ERR_INVALID_ARG, "rc_segments_set: bad arguments");
   if (!f->have_camera) return fail(RC_ERR_STATE, "rc_segments_set before rc_camera_set");
   if (level < 0 || level > RC_NODE_LEVELS) return fail(RC_ERR_INVALID_ARG, "level must be in [0, %d]", RC_NODE_LEVELS);
@@ -1242,6 +1256,7 @@ extern "C" rc_status rc_frame_capture(rc_forest* f, const rc_camera* cam, const 
 }
 
 extern "C" rc_status rc_frame_replay(rc_forest* f, void* stream) {
+  RC_NVTX("rc_frame_replay");
   if (!f) return fail(RC_ERR_INVALID_ARG, "rc_frame_replay: null forest");
   if (!f->graph_exec) return fail(RC_ERR_STATE, "rc_frame_replay before rc_frame_capture");
   CU(cudaGraphLaunch(f->graph_exec, (cudaStream_t)stream));
@@ -1251,6 +1266,7 @@ extern "C" rc_status rc_frame_replay(rc_forest* f, void* stream) {
 extern "C" rc_status rc_render_frame(rc_forest* f, const rc_camera* cam, int32_t fold_levels, int32_t cycles,
                                      const float background[3], float* d_rgba, int64_t capacity_floats,
                                      int64_t* hit_pairs, void* stream) {
+  RC_NVTX("rc_render_frame");
   rc_status st;
   if ((st = rc_camera_set(f, cam, stream))) return st;
   if ((st = rc_cull(f, stream, nullptr))) return st;

@@ -26,6 +26,17 @@
   } while (0)
 #endif
 
+// NVTX ranges around the C ABI's phases (SURVEY §5 tracing): header-only
+// NVTX3, a no-op unless a tool (nsys / ncu --nvtx) injects itself.
+#include <nvtx3/nvToolsExt.h>
+namespace rc {
+struct NvtxScope {
+  explicit NvtxScope(const char* name) { nvtxRangePushA(name); }
+  ~NvtxScope() { nvtxRangePop(); }
+};
+}  // namespace rc
+#define RC_NVTX(name) ::rc::NvtxScope rc_nvtx_scope_(name)
+
 #define RC_MAX_N 8          // GL points per segment
 #define RC_MAX_RANKS 64     // tile owners / communicator size
 #define RC_MAX_TREES 4096
@@ -263,6 +274,7 @@ cudaError_t build_node_levels(rc_forest* f, cudaStream_t s);
 cudaError_t dmalloc(void** p, size_t bytes, cudaStream_t s);
 void dfree(void* p, cudaStream_t s, bool idle = false);
 void dtrim();
+size_t device_free_bytes();   // cudaMemGetInfo's free bytes + the pool's cached blocks on this device
 cudaError_t build_leaf_node(rc_forest* f, int c, cudaStream_t s, const int32_t** out);
 template <typename Tin>
 cudaError_t scan_exclusive(const Tin* in, int64_t* out, int64_t n, int64_t* tmp, cudaStream_t s);

@@ -79,6 +79,7 @@ extern "C" rc_status rc_visible_area_add(rc_forest* f, int64_t* d_w, int64_t cap
 
 extern "C" rc_status rc_vforest_create(rc_forest* f, const int64_t* d_w, int64_t first_global_leaf, void* stream,
                                        rc_forest** out, int64_t* h_count, int64_t* d_w_out) {
+  RC_NVTX("rc_vforest_create");
   if (!f || !d_w || !out || !h_count) return rc_fail(RC_ERR_INVALID_ARG, "rc_vforest_create: null argument");
   *out = nullptr;
   *h_count = 0;
