@@ -614,7 +614,10 @@ __device__ __forceinline__ void prep_bounds(const float* __restrict__ slw, const
 }
 
 constexpr int PREP_E = 32;
-constexpr int PREP_CTAS_PER_SM = 5;   // <= 128 registers x 96 threads; ~31 KB shared memory
+#ifndef RC_PREP_CTAS
+#define RC_PREP_CTAS 5
+#endif
+constexpr int PREP_CTAS_PER_SM = RC_PREP_CTAS;   // <= 128 registers x 96 threads; ~31 KB shared memory
 __device__ __forceinline__ void cp_async4(void* dst, const void* src) {
   asm volatile("cp.async.ca.shared.global [%0], [%1], 4;" ::"r"(smem_addr(dst)), "l"(src) : "memory");
 }

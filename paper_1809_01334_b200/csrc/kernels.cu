@@ -848,7 +848,10 @@ __device__ __forceinline__ bool fold_pixel_reg(const rc_seg* __restrict__ recs, 
 // overlap or tie); the few pixels with more records are deferred to a list
 // that the second pass (one warp per CTA, CAP = FOLD_CAP_LIST records in
 // shared memory) works through.
-constexpr int FOLD_MINB = 8;   // resident k_fold<512> CTAs per SM the register budget is sized for (A/B: 4 -> 8 = 31.1 -> 25.4 ms at C4)
+#ifndef RC_FOLD_MINB
+#define RC_FOLD_MINB 8
+#endif
+constexpr int FOLD_MINB = RC_FOLD_MINB;   // resident k_fold<512> CTAs per SM the register budget is sized for (A/B: 4 -> 8 = 31.1 -> 25.4 ms at C4)
 constexpr int FOLD_CAP_LIST = 16384;   // records per pixel the composite can order (more: NaN pixel, counted)
 template <int CAP, bool FROM_LIST, int NW>
 __global__ void __launch_bounds__(NW * 32, CAP <= 512 ? FOLD_MINB : 1) k_fold(
