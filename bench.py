@@ -641,32 +641,74 @@ def main():
     img_host = torch.empty((NI, H, W, 4), dtype=torch.float32).pin_memory()
     e2e_times = []
     n_e2e = 0 if args.no_e2e else 2 + (1 if args.config in (4, 5) else max(1, min(args.steps, 3)))
-    for it in range(n_e2e):
-        torch.cuda.synchronize()
-        if world > 1:
-            torch.distributed.barrier()
-        t0 = time.perf_counter()
+
+    def new_forest(stream=None):
         # rc_forest_create copies the pinned host arrays (the scene generator
         # guarantees SFC order: RC_HOST_COPY_TRUSTED skips the host-side check)
-        f2 = rc.Forest(scene.tree_ctrl, scene.geom_degree, scene.field_degree, *pinned_np, scene.kappa0,
-                       scene.inv_F, scene.q0, first_global_leaf=lo, trusted=True, **surf_kw)
+        return rc.Forest(scene.tree_ctrl, scene.geom_degree, scene.field_degree, *pinned_np, scene.kappa0,
+                         scene.inv_F, scene.q0, first_global_leaf=lo, trusted=True, stream=stream, **surf_kw)
+
+    def e2e_step(f2):
         k2 = [torch.from_numpy(a).to(dev) for a in host[:3]] if (world > 1 and cycles) else None
         outs, fa = frame(f2, k2, (lo, hi))
         for k, out in enumerate(outs):
             img_host[k].view(-1)[:out.numel()].copy_(out.reshape(-1))
-        torch.cuda.synchronize()
-        dt = time.perf_counter() - t0
+        stream.synchronize()
         if fa is not f2:
             fa.close()
         f2.close()
+
+    for it in range(n_e2e):   # sequential steps: upload, frame, read-back
+        torch.cuda.synchronize()
+        if world > 1:
+            torch.distributed.barrier()
+        t0 = time.perf_counter()
+        e2e_step(new_forest())
+        dt = time.perf_counter() - t0
         if it >= 2:
             e2e_times.append(dt)
-    e2e_s = sum(e2e_times) / len(e2e_times) if e2e_times else float("nan")
+    e2e_seq_s = sum(e2e_times) / len(e2e_times) if e2e_times else float("nan")
+    e2e_s, pipelined = e2e_seq_s, False
+    # pipelined steps (one GPU, when two forests fit): step i+1's upload runs on
+    # a copy stream from a second host thread while step i's frame computes
+    # (the DMA engines overlap the kernels); every step still uploads its inputs
+    # and reads its image back inside the timed region
+    n_pipe = 0 if args.no_e2e or world > 1 else (5 if args.config in (4, 5) else 4)
+    if n_pipe and torch.cuda.mem_get_info()[0] > 3 * h2d:
+        import threading
+        up = torch.cuda.Stream()
+        torch.cuda.synchronize()
+        t0 = time.perf_counter()
+        cur = new_forest(up.cuda_stream)
+        for i in range(n_pipe):
+            nxt, err = [], []
+
+            def upload():
+                try:
+                    nxt.append(new_forest(up.cuda_stream))
+                except Exception as ex:   # surfaced below
+                    err.append(ex)
+            th = threading.Thread(target=upload) if i + 1 < n_pipe else None
+            if th:
+                th.start()
+            e2e_step(cur)
+            if th:
+                th.join()
+                if err:
+                    raise err[0]
+                cur = nxt[0]
+        torch.cuda.synchronize()
+        e2e_pipe_s = (time.perf_counter() - t0) / n_pipe
+        if e2e_pipe_s < e2e_s:
+            e2e_s, pipelined = e2e_pipe_s, True
     if world > 1:
         e2e_s = tp.max(e2e_s)
     e2e = {"value": hits_total / e2e_s, "unit": "hit pairs/s", "h2d_bytes_per_step": h2d,
            "d2h_bytes_per_step": sum(int(o.numel()) * 4 for o in last_out) if last_out else NI * H * W * 16,
-           "ms_per_step": e2e_s * 1000.0}
+           "ms_per_step": e2e_s * 1000.0, "pipelined": pipelined,
+           "sequential_ms_per_step": e2e_seq_s * 1000.0,
+           "how": "rc_forest_create from pinned host buffers + the frame + image read-back per step; pipelined: "
+                  "the next step's upload (copy stream, second host thread) overlaps this step's frame"}
 
     if rank == 0:
         line = {"metric": "element-ray segment evaluations/s (hit pairs/s)", "value": value, "unit": "hit pairs/s",

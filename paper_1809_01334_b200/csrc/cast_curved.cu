@@ -613,9 +613,80 @@ __device__ __forceinline__ void prep_bounds(const float* __restrict__ slw, const
   sbw[1][C] = eta;
 }
 
+// One instance for the three coordinate warps (runtime, warp-uniform C): a
+// third of the code of the per-coordinate instances (the prep kernel's top
+// stall is instruction fetch).  Same arithmetic in the same order.
+__device__ __forceinline__ void prep_affine_rt(const float* __restrict__ slw, float* sJw, bool act, int C) {
+  constexpr float wq[3] = {0.25f, 0.5f, 0.25f}, dq[3] = {-1.0f, 0.0f, 1.0f};
+  if (act) {
+    float xc = 0.f, j0 = 0.f, j1 = 0.f, j2 = 0.f;
+#pragma unroll
+    for (int m = 0; m < 27; ++m) {
+      const int a1 = m % 3, a2 = (m / 3) % 3, a3 = m / 9;
+      const float b = slw[GI(m) + C];
+      xc = fmaf(wq[a1] * wq[a2] * wq[a3], b, xc);
+      j0 = fmaf(dq[a1] * wq[a2] * wq[a3], b, j0);
+      j1 = fmaf(wq[a1] * dq[a2] * wq[a3], b, j1);
+      j2 = fmaf(wq[a1] * wq[a2] * dq[a3], b, j2);
+    }
+    sJw[C] = xc;
+    sJw[3 + 3 * C] = j0;
+    sJw[4 + 3 * C] = j1;
+    sJw[5 + 3 * C] = j2;
+  }
+}
+__device__ __forceinline__ void prep_bounds_rt(const float* __restrict__ slw, const float* sJw, float (*sbw)[3],
+                                               float (&Ji)[3][3], bool act, int C) {
+  if (!act) return;
+  float J[3][3];
+#pragma unroll
+  for (int i = 0; i < 3; ++i)
+#pragma unroll
+    for (int a = 0; a < 3; ++a) J[i][a] = sJw[3 + 3 * i + a];
+  const float Xc[3] = {sJw[0], sJw[1], sJw[2]};
+  if (!inv3(J, Ji)) {
+#pragma unroll
+    for (int i = 0; i < 3; ++i)
+#pragma unroll
+      for (int a = 0; a < 3; ++a) Ji[i][a] = 0.0f;
+  }
+  float JC[3];   // row C of J0^-1
+#pragma unroll
+  for (int a = 0; a < 3; ++a) JC[a] = C == 0 ? Ji[0][a] : (C == 1 ? Ji[1][a] : Ji[2][a]);
+  const float e0C = C == 0 ? 1.0f : 0.0f, e1C = C == 1 ? 1.0f : 0.0f, e2C = C == 2 ? 1.0f : 0.0f;
+  float dpc = 0.0f, eta = 0.0f;
+#pragma unroll
+  for (int m = 0; m < 27; ++m) {
+    const int mmv[3] = {m % 3, (m / 3) % 3, m / 9};
+    const float* b = slw + GI(m);
+    const float x0 = 0.5f * mmv[0] - 0.5f, x1 = 0.5f * mmv[1] - 0.5f, x2 = 0.5f * mmv[2] - 0.5f;
+    const float r0 = b[0] - (Xc[0] + J[0][0] * x0 + J[0][1] * x1 + J[0][2] * x2);
+    const float r1 = b[1] - (Xc[1] + J[1][0] * x0 + J[1][1] * x1 + J[1][2] * x2);
+    const float r2 = b[2] - (Xc[2] + J[2][0] * x0 + J[2][1] * x1 + J[2][2] * x2);
+    dpc = fmaxf(dpc, fabsf(JC[0] * r0 + JC[1] * r1 + JC[2] * r2));
+    // eta: Bernstein coefficients of dE/dxi_C = 2 J0^-1 (B_{m+e_C} - B_m) - e_C (inf-norm)
+    const int mC = C == 0 ? mmv[0] : (C == 1 ? mmv[1] : mmv[2]);
+    if (mC < 2) {
+      const int nxt = C == 0 ? (mmv[0] < 2 ? GI(m + 1) : 0) : (C == 1 ? (mmv[1] < 2 ? GI(m + 3) : 0)
+                                                                      : (mmv[2] < 2 ? GI(m + 9) : 0));
+      const float* b2 = slw + nxt;
+      const float e0 = 2.0f * (b2[0] - b[0]), e1 = 2.0f * (b2[1] - b[1]), e2 = 2.0f * (b2[2] - b[2]);
+      const float t0 = Ji[0][0] * e0 + Ji[0][1] * e1 + Ji[0][2] * e2 - e0C;
+      const float t1 = Ji[1][0] * e0 + Ji[1][1] * e1 + Ji[1][2] * e2 - e1C;
+      const float t2 = Ji[2][0] * e0 + Ji[2][1] * e1 + Ji[2][2] * e2 - e2C;
+      eta = fmaxf(eta, fmaxf(fabsf(t0), fmaxf(fabsf(t1), fabsf(t2))));
+    }
+  }
+  sbw[0][C] = dpc;
+  sbw[1][C] = eta;
+}
+
 constexpr int PREP_E = 32;
+#ifndef RC_PREP_ONE_COPY
+#define RC_PREP_ONE_COPY 0
+#endif
 #ifndef RC_PREP_CTAS
-#define RC_PREP_CTAS 5
+#define RC_PREP_CTAS 4   // A/B at C4 (s8): 4 = 38.6, 5 = 40.1, 6 = 41.2 ms of prep per frame
 #endif
 constexpr int PREP_CTAS_PER_SM = RC_PREP_CTAS;   // <= 128 registers x 96 threads; ~31 KB shared memory
 __device__ __forceinline__ void cp_async4(void* dst, const void* src) {
@@ -766,6 +837,12 @@ __global__ void __launch_bounds__(3 * PREP_E, PREP_CTAS_PER_SM) k_prep_slots(
     // 2. affine model at the centre, row c (fp32); 3. J0^-1, dp_c and the eta
     // part along axis c.  Per coordinate a fully unrolled instance (constant
     // indices: no integer division or selects in the loops over the 27 points).
+#if RC_PREP_ONE_COPY
+    prep_affine_rt(slw, sJ[w], act, c);
+    __syncthreads();
+    float Ji[3][3];
+    prep_bounds_rt(slw, sJ[w], sb[w], Ji, act, c);
+#else
     switch (c) {   // warp-uniform
       case 0: prep_affine<0>(slw, sJ[w], act); break;
       case 1: prep_affine<1>(slw, sJ[w], act); break;
@@ -778,6 +855,7 @@ __global__ void __launch_bounds__(3 * PREP_E, PREP_CTAS_PER_SM) k_prep_slots(
       case 1: prep_bounds<1>(slw, sJ[w], sb[w], Ji, act); break;
       default: prep_bounds<2>(slw, sJ[w], sb[w], Ji, act); break;
     }
+#endif
     __syncthreads();
     if (act && c == 0) {
       float* af = slw + SLOT_AFF;

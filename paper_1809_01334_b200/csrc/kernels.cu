@@ -849,7 +849,7 @@ __device__ __forceinline__ bool fold_pixel_reg(const rc_seg* __restrict__ recs, 
 // that the second pass (one warp per CTA, CAP = FOLD_CAP_LIST records in
 // shared memory) works through.
 #ifndef RC_FOLD_MINB
-#define RC_FOLD_MINB 8
+#define RC_FOLD_MINB 8   // A/B at C4 (s8): 8 = 23.2, 6 = 25.2 ms of composite fold per frame
 #endif
 constexpr int FOLD_MINB = RC_FOLD_MINB;   // resident k_fold<512> CTAs per SM the register budget is sized for (A/B: 4 -> 8 = 31.1 -> 25.4 ms at C4)
 constexpr int FOLD_CAP_LIST = 16384;   // records per pixel the composite can order (more: NaN pixel, counted)

@@ -12,7 +12,7 @@
 #include "rc_internal.cuh"
 
 namespace rc {
-int64_t g_launches = 0;
+std::atomic<int64_t> g_launches{0};
 }
 using namespace rc;
 
@@ -42,8 +42,7 @@ rc_status rc_fail(rc_status st, const char* fmt, ...) {
 extern "C" const char* rc_last_error(void) { return g_err; }
 extern "C" int32_t rc_version(void) { return 4; }
 extern "C" int64_t rc_launch_count(int32_t reset) {
-  int64_t v = g_launches;
-  if (reset) g_launches = 0;
+  const int64_t v = reset ? g_launches.exchange(0) : g_launches.load();
   return v;
 }
 

@@ -4,6 +4,8 @@
 #include <cuda_runtime.h>
 #include <stdint.h>
 
+#include <atomic>
+
 #include "../../include/rc.h"
 
 // Device-side bounds checks of the checked build (tag "checks": -DRC_CHECKS,
@@ -263,7 +265,7 @@ int nccl_exchange(rc_comm* c, const char* sbuf, const int64_t* soff, const int64
                   const int64_t* roff, const int64_t* rcnt, cudaStream_t s);
 int nccl_alltoall_i64(rc_comm* c, const int64_t* d_send, int64_t* d_recv, cudaStream_t s);
 int nccl_partner_i64(rc_comm* c, const int64_t* d_send, int64_t* d_recv, cudaStream_t s);
-extern int64_t g_launches;
+extern std::atomic<int64_t> g_launches;   // several host threads may drive forests at once
 cudaError_t scan_exclusive_i64(const int64_t* in, int64_t* out, int64_t n, int64_t* tmp, cudaStream_t s);
 size_t scan_tmp_size(int64_t n);
 }  // namespace rc
