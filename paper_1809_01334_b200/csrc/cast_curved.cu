@@ -443,9 +443,15 @@ __device__ __noinline__ int face_roots_subdiv(const Patch& root, float tol, int 
 //    the paper's coarsening done on chip.
 //    Without folding every segment is a record keyed by its leaf.
 // ---------------------------------------------------------------------------
-constexpr int CWARPS = 4;   // warps per CTA
+#ifndef RC_CWARPS
+#define RC_CWARPS 4
+#endif
+#ifndef RC_CAST_CTAS
+#define RC_CAST_CTAS 3
+#endif
+constexpr int CWARPS = RC_CWARPS;   // warps per CTA
 constexpr float FAST_Q = 0.7f;       // contraction bound below which a face root takes the certified fast path
-constexpr int CAST_CTAS_PER_SM = 3;  // resident CTAs per SM (launch bounds: 168 registers, ~72 KB shared memory)
+constexpr int CAST_CTAS_PER_SM = RC_CAST_CTAS;  // resident CTAs per SM (launch bounds: 168 registers, ~72 KB shared memory)
 constexpr int MAXR = 8;                                   // face roots per (element, pixel) pair
 constexpr int ITEM_CAP = (MAXR / 2) * RC_CHUNK * RC_UNIT_CHUNKS;   // <= MAXR/2 segments per pair
 constexpr int MAXT = 6 * RC_CHUNK;                        // face tasks of one chunk
@@ -552,70 +558,9 @@ __device__ __forceinline__ void fence_proxy_async_smem() { asm volatile("fence.p
 //     J0^-1 coordinates and the part of eta (sup |dE/dxi|) along axis c;
 //  then the slots are written out coalesced.
 // Stages 2-3 of k_prep_slots for coordinate C (one warp per coordinate).
-template <int C>
-__device__ __forceinline__ void prep_affine(const float* __restrict__ slw, float* sJw, bool act) {
-  constexpr float wq[3] = {0.25f, 0.5f, 0.25f}, dq[3] = {-1.0f, 0.0f, 1.0f};
-  if (act) {
-    float xc = 0.f, j0 = 0.f, j1 = 0.f, j2 = 0.f;
-#pragma unroll
-    for (int m = 0; m < 27; ++m) {
-      const int a1 = m % 3, a2 = (m / 3) % 3, a3 = m / 9;
-      const float b = slw[GI(m) + C];
-      xc = fmaf(wq[a1] * wq[a2] * wq[a3], b, xc);
-      j0 = fmaf(dq[a1] * wq[a2] * wq[a3], b, j0);
-      j1 = fmaf(wq[a1] * dq[a2] * wq[a3], b, j1);
-      j2 = fmaf(wq[a1] * wq[a2] * dq[a3], b, j2);
-    }
-    sJw[C] = xc;
-    sJw[3 + 3 * C] = j0;
-    sJw[4 + 3 * C] = j1;
-    sJw[5 + 3 * C] = j2;
-  }
-}
-template <int C>
-__device__ __forceinline__ void prep_bounds(const float* __restrict__ slw, const float* sJw, float (*sbw)[3],
-                                            float (&Ji)[3][3], bool act) {
-  if (!act) return;
-  float J[3][3];
-#pragma unroll
-  for (int i = 0; i < 3; ++i)
-#pragma unroll
-    for (int a = 0; a < 3; ++a) J[i][a] = sJw[3 + 3 * i + a];
-  const float Xc[3] = {sJw[0], sJw[1], sJw[2]};
-  if (!inv3(J, Ji)) {
-#pragma unroll
-    for (int i = 0; i < 3; ++i)
-#pragma unroll
-      for (int a = 0; a < 3; ++a) Ji[i][a] = 0.0f;
-  }
-  float dpc = 0.0f, eta = 0.0f;
-  constexpr int str[3] = {1, 3, 9};
-#pragma unroll
-  for (int m = 0; m < 27; ++m) {
-    const int mmv[3] = {m % 3, (m / 3) % 3, m / 9};
-    const float* b = slw + GI(m);
-    const float x0 = 0.5f * mmv[0] - 0.5f, x1 = 0.5f * mmv[1] - 0.5f, x2 = 0.5f * mmv[2] - 0.5f;
-    const float r0 = b[0] - (Xc[0] + J[0][0] * x0 + J[0][1] * x1 + J[0][2] * x2);
-    const float r1 = b[1] - (Xc[1] + J[1][0] * x0 + J[1][1] * x1 + J[1][2] * x2);
-    const float r2 = b[2] - (Xc[2] + J[2][0] * x0 + J[2][1] * x1 + J[2][2] * x2);
-    dpc = fmaxf(dpc, fabsf(Ji[C][0] * r0 + Ji[C][1] * r1 + Ji[C][2] * r2));
-    // eta: Bernstein coefficients of dE/dxi_C = 2 J0^-1 (B_{m+e_C} - B_m) - e_C (inf-norm)
-    if (mmv[C] < 2) {
-      const float* b2 = slw + GI(m + str[C]);
-      const float e0 = 2.0f * (b2[0] - b[0]), e1 = 2.0f * (b2[1] - b[1]), e2 = 2.0f * (b2[2] - b[2]);
-      const float t0 = Ji[0][0] * e0 + Ji[0][1] * e1 + Ji[0][2] * e2 - (C == 0 ? 1.0f : 0.0f);
-      const float t1 = Ji[1][0] * e0 + Ji[1][1] * e1 + Ji[1][2] * e2 - (C == 1 ? 1.0f : 0.0f);
-      const float t2 = Ji[2][0] * e0 + Ji[2][1] * e1 + Ji[2][2] * e2 - (C == 2 ? 1.0f : 0.0f);
-      eta = fmaxf(eta, fmaxf(fabsf(t0), fmaxf(fabsf(t1), fabsf(t2))));
-    }
-  }
-  sbw[0][C] = dpc;
-  sbw[1][C] = eta;
-}
-
 // One instance for the three coordinate warps (runtime, warp-uniform C): a
-// third of the code of the per-coordinate instances (the prep kernel's top
-// stall is instruction fetch).  Same arithmetic in the same order.
+// third of the code of per-coordinate template instances (the prep kernel's
+// top stall is instruction fetch; A/B at C4, s10: 38.6 -> 36.4 ms per frame).
 __device__ __forceinline__ void prep_affine_rt(const float* __restrict__ slw, float* sJw, bool act, int C) {
   constexpr float wq[3] = {0.25f, 0.5f, 0.25f}, dq[3] = {-1.0f, 0.0f, 1.0f};
   if (act) {
@@ -682,9 +627,6 @@ __device__ __forceinline__ void prep_bounds_rt(const float* __restrict__ slw, co
 }
 
 constexpr int PREP_E = 32;
-#ifndef RC_PREP_ONE_COPY
-#define RC_PREP_ONE_COPY 0
-#endif
 #ifndef RC_PREP_CTAS
 #define RC_PREP_CTAS 4   // A/B at C4 (s8): 4 = 38.6, 5 = 40.1, 6 = 41.2 ms of prep per frame
 #endif
@@ -837,25 +779,10 @@ __global__ void __launch_bounds__(3 * PREP_E, PREP_CTAS_PER_SM) k_prep_slots(
     // 2. affine model at the centre, row c (fp32); 3. J0^-1, dp_c and the eta
     // part along axis c.  Per coordinate a fully unrolled instance (constant
     // indices: no integer division or selects in the loops over the 27 points).
-#if RC_PREP_ONE_COPY
     prep_affine_rt(slw, sJ[w], act, c);
     __syncthreads();
     float Ji[3][3];
     prep_bounds_rt(slw, sJ[w], sb[w], Ji, act, c);
-#else
-    switch (c) {   // warp-uniform
-      case 0: prep_affine<0>(slw, sJ[w], act); break;
-      case 1: prep_affine<1>(slw, sJ[w], act); break;
-      default: prep_affine<2>(slw, sJ[w], act); break;
-    }
-    __syncthreads();
-    float Ji[3][3];
-    switch (c) {
-      case 0: prep_bounds<0>(slw, sJ[w], sb[w], Ji, act); break;
-      case 1: prep_bounds<1>(slw, sJ[w], sb[w], Ji, act); break;
-      default: prep_bounds<2>(slw, sJ[w], sb[w], Ji, act); break;
-    }
-#endif
     __syncthreads();
     if (act && c == 0) {
       float* af = slw + SLOT_AFF;

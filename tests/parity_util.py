@@ -179,3 +179,53 @@ def gpu_fold0_chunked(scene, pixels, nchunks, device_copy=False):
         torch.cuda.empty_cache()
     return dict(visible=np.concatenate(vis), keys=np.unique(np.concatenate(keys)),
                 hits_per_pixel=hpp.cpu().numpy(), **stats)
+
+
+def linear_field_shell(base, cvec, d0):
+    """The scene `base` (R = 2 shell) with P = 2 nodal values of the world-linear
+    field f(x) = cvec.x + d0 at every element's GLL nodes, mapped through the
+    tree's R = 2 Lagrange map J_k (textbook Lagrange basis on {0, 1/2, 1}
+    evaluated here, not the oracle's or the GPU's code): f o X_E is then
+    triquadratic and the nodal interpolation exact (pin P16).  inv_F = 1."""
+    import dataclasses
+    ctrl = np.asarray(base.tree_ctrl)                 # [K][3][3][3][3], [k][m3][m2][m1][xyz]
+    g = np.array([0.0, 0.5, 1.0])
+
+    def lag(t):
+        return np.array([(t - g[1]) * (t - g[2]) / ((g[0] - g[1]) * (g[0] - g[2])),
+                         (t - g[0]) * (t - g[2]) / ((g[1] - g[0]) * (g[1] - g[2])),
+                         (t - g[0]) * (t - g[1]) / ((g[2] - g[0]) * (g[2] - g[1]))])
+
+    anc = np.asarray(base.leaf_anchor, np.float64) / (1 << 18)
+    hE = np.ldexp(1.0, -np.asarray(base.leaf_level, np.int64))
+    fld = np.zeros((base.num_leaves, 27), np.float32)
+    for e in range(base.num_leaves):
+        C = ctrl[int(base.leaf_tree[e])]
+        for k3 in range(3):
+            for k2 in range(3):
+                for k1 in range(3):
+                    t = anc[e] + hE[e] * g[[k1, k2, k3]]
+                    x = np.einsum("a,b,c,abcx->x", lag(t[2]), lag(t[1]), lag(t[0]), C)
+                    fld[e, (k3 * 3 + k2) * 3 + k1] = np.asarray(cvec) @ x + d0
+    return dataclasses.replace(base, leaf_field=fld, inv_F=1.0)
+
+
+def linear_field_segment(ro, rd, an, af, cvec, d0, kappa0):
+    """Closed-form A and quadrature B of one segment [an, af] of the ray
+    ro + alpha rd in the world-linear field (kappa = kappa0 f^2, q = ((1+f)/2,
+    (1-f)/2, 1/2)); s measured from the near end (Eq. ABgeneral)."""
+    import math
+    from numpy.polynomial import polynomial as Pn
+    from scipy.integrate import quad
+    nr = float(np.linalg.norm(rd))
+    fa = np.array([np.dot(cvec, ro) + d0, np.dot(cvec, rd)])
+    ik = Pn.polyint(kappa0 * Pn.polymul(fa, fa) * nr)
+    A = math.exp(-(Pn.polyval(af, ik) - Pn.polyval(an, ik)))
+    B = []
+    for c in range(3):
+        def qf(a_, c=c):
+            f = fa[0] + fa[1] * a_
+            return ((1 + f) / 2, (1 - f) / 2, 0.5)[c] * math.exp(-(Pn.polyval(a_, ik) - Pn.polyval(an, ik))) * nr
+        B.append(quad(qf, an, af, epsabs=1e-14, epsrel=1e-12)[0])
+    return A, np.array(B)
+

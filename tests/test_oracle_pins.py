@@ -804,40 +804,19 @@ def test_curved_pairs_linear_world_field_P16():
     """Per-pair (a, b) on curved R=2 elements with a NON-constant field
     (closes the "parity unpinned" gap of DESIGN §3): nodal values of
     f(x) = c.x + d at the element's GLL nodes mapped through the tree's R=2
-    Lagrange map J_k (evaluated here with a textbook Lagrange basis, not the
-    oracle), so f o X_E is triquadratic and the P = 2 interpolation is exact.
-    Along a ray f is linear in alpha, kappa = kappa0 f^2 quadratic: A =
-    exp(-int kappa ds) is a polynomial integral (numpy, exact) and
-    B = int q(s) exp(-int_0^s kappa) ds (s from the near end, the orientation
-    pinned by test_exact_vs_scipy_ode_orientation) a scipy quadrature in world
-    coordinates.  A wrong inverse map, interpolation or quadrature in the
-    oracle's per-pair path changes (a, b)."""
-    import dataclasses
-    from numpy.polynomial import polynomial as Pn
-    from scipy.integrate import quad
-    base = sg.shell_uniform(2, 24, 4, gl_points=6)
-    ctrl = np.asarray(base.tree_ctrl)                 # [K][3][3][3][3], [k][m3][m2][m1][xyz]
+    Lagrange map J_k (evaluated in tests/parity_util.py with a textbook
+    Lagrange basis, not the oracle), so f o X_E is triquadratic and the P = 2
+    interpolation is exact.  Along a ray f is linear in alpha, kappa = kappa0 f^2
+    quadratic: A = exp(-int kappa ds) is a polynomial integral (numpy, exact)
+    and B = int q(s) exp(-int_0^s kappa) ds (s from the near end, the
+    orientation pinned by test_exact_vs_scipy_ode_orientation) a scipy
+    quadrature in world coordinates.  A wrong inverse map, interpolation or
+    quadrature in the oracle's per-pair path changes (a, b)."""
+    import sys
+    sys.path.insert(0, os.path.dirname(os.path.abspath(__file__)))
+    from parity_util import linear_field_segment, linear_field_shell
     cvec, d0 = np.array([0.21, 0.11, -0.17]), 0.05
-    g = np.array([0.0, 0.5, 1.0])
-
-    def lag(t):   # Lagrange basis on {0, 1/2, 1}
-        return np.array([(t - g[1]) * (t - g[2]) / ((g[0] - g[1]) * (g[0] - g[2])),
-                         (t - g[0]) * (t - g[2]) / ((g[1] - g[0]) * (g[1] - g[2])),
-                         (t - g[0]) * (t - g[1]) / ((g[2] - g[0]) * (g[2] - g[1]))])
-
-    anc = np.asarray(base.leaf_anchor, np.float64) / (1 << 18)
-    hE = np.ldexp(1.0, -np.asarray(base.leaf_level, np.int64))
-    fld = np.zeros((base.num_leaves, 27), np.float32)
-    for e in range(base.num_leaves):
-        C = ctrl[int(base.leaf_tree[e])]
-        for k3 in range(3):
-            for k2 in range(3):
-                for k1 in range(3):
-                    t = anc[e] + hE[e] * g[[k1, k2, k3]]
-                    l1, l2, l3 = lag(t[0]), lag(t[1]), lag(t[2])
-                    x = np.einsum("a,b,c,abcx->x", l3, l2, l1, C)
-                    fld[e, (k3 * 3 + k2) * 3 + k1] = cvec @ x + d0
-    sc = dataclasses.replace(base, leaf_field=fld, inv_F=1.0)
+    sc = linear_field_shell(sg.shell_uniform(2, 24, 4, gl_points=6), cvec, d0)
     kap0 = float(np.float32(sc.kappa0))
     o = oracle.OracleScene(sc)
     W = sc.camera.width
@@ -846,25 +825,13 @@ def test_curved_pairs_linear_world_field_P16():
     nchk = 0
     for q_i, p in enumerate(res["pixels"]):
         ro, rd = o.ray(int(p) % W, int(p) // W)
-        nr = float(np.linalg.norm(rd))
-        fa = np.array([cvec @ ro + d0, cvec @ rd])            # f(alpha) coefficients
-        kap = kap0 * Pn.polymul(fa, fa) * nr                    # kappa per unit alpha
-        ik = Pn.polyint(kap)
         for h in res["hits"][q_i][:int(res["nhits"][q_i])]:
             if h["elem"] < 0 or not (h["flags"] & oracle.HIT) or (h["flags"] & oracle.AMBIGUOUS):
                 continue
             an, af = float(h["alpha_near"]), float(h["alpha_far"])
             if af - an < 1e-6:
                 continue
-            A = math.exp(-(Pn.polyval(af, ik) - Pn.polyval(an, ik)))
-            tau = lambda a_: Pn.polyval(a_, ik) - Pn.polyval(an, ik)
-            B = []
-            for c in range(3):
-                def qf(a_, c=c):
-                    f = fa[0] + fa[1] * a_
-                    qc = ((1 + f) / 2, (1 - f) / 2, 0.5)[c]
-                    return qc * math.exp(-tau(a_)) * nr
-                B.append(quad(qf, an, af, epsabs=1e-14, epsrel=1e-12)[0])
+            A, B = linear_field_segment(ro, rd, an, af, cvec, d0, kap0)
             # bound: the nodal values are fp32 (relative 6e-8), so tau is off by <= 1.2e-7 tau
             np.testing.assert_allclose(h["a"], A, rtol=5e-7, atol=1e-12)
             np.testing.assert_allclose(h["b"], B, rtol=5e-7, atol=1e-10)
