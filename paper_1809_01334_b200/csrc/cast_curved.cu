@@ -444,14 +444,14 @@ __device__ __noinline__ int face_roots_subdiv(const Patch& root, float tol, int 
 //    Without folding every segment is a record keyed by its leaf.
 // ---------------------------------------------------------------------------
 #ifndef RC_CWARPS
-#define RC_CWARPS 4
+#define RC_CWARPS 6   // A/B at C4 (s11): 4 x 3 CTAs 559.3 ms, 6 x 2 CTAs 552.6 ms, 12 x 1 CTA 605.3 ms
 #endif
 #ifndef RC_CAST_CTAS
-#define RC_CAST_CTAS 3
+#define RC_CAST_CTAS 2
 #endif
 constexpr int CWARPS = RC_CWARPS;   // warps per CTA
 constexpr float FAST_Q = 0.7f;       // contraction bound below which a face root takes the certified fast path
-constexpr int CAST_CTAS_PER_SM = RC_CAST_CTAS;  // resident CTAs per SM (launch bounds: 168 registers, ~72 KB shared memory)
+constexpr int CAST_CTAS_PER_SM = RC_CAST_CTAS;  // resident CTAs per SM (launch bounds: 168 registers)
 constexpr int MAXR = 8;                                   // face roots per (element, pixel) pair
 constexpr int ITEM_CAP = (MAXR / 2) * RC_CHUNK * RC_UNIT_CHUNKS;   // <= MAXR/2 segments per pair
 constexpr int MAXT = 6 * RC_CHUNK;                        // face tasks of one chunk

@@ -18,3 +18,13 @@ timeout 900 $CMD > $OUT/plain.log 2>&1 && \
   timeout 1200 ncu --metrics gpu__time_duration.sum --clock-control none -k regex:'k_|rc::' --csv \
     --log-file $OUT/launches_c4.csv $CMD > $OUT/ncu_launches.log 2>&1
 echo "launches exit $?" >> $OUT/status
+TCMD="python tools/profile_frame.py --config 4 --frames 1"
+timeout 600 $TCMD > $OUT/plain_traffic.log 2>&1 && \
+  timeout 900 ncu --metrics dram__bytes_read.sum,dram__bytes_write.sum,gpu__time_duration.sum --clock-control none \
+    -k regex:'k_cast_curved|k_prep_slots' --csv --log-file $OUT/traffic_c4.csv $TCMD > $OUT/ncu_traffic.log 2>&1
+echo "traffic exit $?" >> $OUT/status
+PCMD="python tools/profile_frame.py --config 45 --frames 1"
+timeout 300 $PCMD > $OUT/plain_pf.log 2>&1 && \
+  timeout 1200 ncu --set full --clock-control none --import-source on -k regex:'k_cast_curved' -c 1 \
+    -o $OUT/prof $PCMD > $OUT/ncu_full.log 2>&1
+echo "ncu full exit $?" >> $OUT/status
