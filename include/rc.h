@@ -59,7 +59,7 @@ typedef struct {      /* surface transfer of the corner-interpolated value v (su
   float k;
 } rc_surface;
 
-enum { RC_HOST_COPY = 0, RC_DEVICE_COPY = 1, RC_HOST_COPY_TRUSTED = 2 };
+enum { RC_HOST_COPY = 0, RC_DEVICE_COPY = 1, RC_HOST_COPY_TRUSTED = 2, RC_DEVICE_BORROW = 3 };
 
 typedef struct {
   int32_t num_trees;          /* K >= 1                                                  */
@@ -78,7 +78,10 @@ typedef struct {
                                  RC_HOST_COPY_TRUSTED: host pointers, the caller
                                  guarantees SFC order (no host-side check; pinned
                                  memory gives asynchronous DMA);
-                                 RC_DEVICE_COPY: leaf arrays are device pointers        */
+                                 RC_DEVICE_COPY: leaf arrays are device pointers;
+                                 RC_DEVICE_BORROW: device pointers used in place (anchor,
+                                 tree, field; the 1-byte levels are copied), owned by the
+                                 caller and alive until rc_forest_destroy returns        */
   rc_transfer transfer;
   /* surface forests (§2.8, App. A.1):
    * dim = 2 makes the leaves quadtree leaves (leaf_anchor[3e+2] == 0) of

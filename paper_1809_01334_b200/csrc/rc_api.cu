@@ -81,7 +81,8 @@ extern "C" rc_status rc_forest_create(const rc_forest_desc* d, void* stream, rc_
   if (d->num_leaves < 1 || d->num_leaves > (int64_t)INT32_MAX) return fail(RC_ERR_INVALID_ARG, "num_leaves out of range");
   if (!d->tree_ctrl || !d->leaf_anchor || !d->leaf_tree || !d->leaf_level)
     return fail(RC_ERR_INVALID_ARG, "rc_forest_create: null array");
-  if (d->memory != RC_HOST_COPY && d->memory != RC_DEVICE_COPY && d->memory != RC_HOST_COPY_TRUSTED)
+  if (d->memory != RC_HOST_COPY && d->memory != RC_DEVICE_COPY && d->memory != RC_HOST_COPY_TRUSTED &&
+      d->memory != RC_DEVICE_BORROW)
     return fail(RC_ERR_INVALID_ARG, "bad memory mode");
   if (d->first_global_leaf < 0 || d->first_global_leaf + d->num_leaves > (int64_t)UINT32_MAX)
     return fail(RC_ERR_INVALID_ARG, "global leaf index must fit 32 bits");
@@ -125,6 +126,8 @@ extern "C" rc_status rc_forest_create(const rc_forest_desc* d, void* stream, rc_
   f->first_global = d->first_global_leaf;
   f->transfer = d->transfer;
   f->has_field = d->leaf_field != nullptr;
+  f->borrowed = d->memory == RC_DEVICE_BORROW;
+  f->last_stream = s;
   f->surface = surface;
   if (surface) f->surf = d->surface;
   f->h_trees = new TreeConst[f->K];
@@ -138,10 +141,17 @@ extern "C" rc_status rc_forest_create(const rc_forest_desc* d, void* stream, rc_
 #define ALLOC(ptr, bytes)                                        \
   if ((e = dmalloc((void**)&(ptr), (bytes), s)) != cudaSuccess) \
     return cleanup(RC_ERR_OUT_OF_MEMORY, "cudaMalloc " #ptr);
-  ALLOC(f->d_anchor, sizeof(int32_t) * 3 * n);
-  ALLOC(f->d_tree, sizeof(int32_t) * n);
-  ALLOC(f->d_level, sizeof(int8_t) * ((n + 3) & ~(int64_t)3));   // whole words: k_prep_slots stages the level bytes with 4-byte copies
-  if (f->has_field) ALLOC(f->d_field, sizeof(float) * NF * n);
+  if (f->borrowed) {   // the caller's device arrays in place (they outlive the forest)
+    f->d_anchor = const_cast<int32_t*>(d->leaf_anchor);
+    f->d_tree = const_cast<int32_t*>(d->leaf_tree);
+    f->d_field = const_cast<float*>(d->leaf_field);
+  } else {
+    ALLOC(f->d_anchor, sizeof(int32_t) * 3 * n);
+    ALLOC(f->d_tree, sizeof(int32_t) * n);
+    if (f->has_field) ALLOC(f->d_field, sizeof(float) * NF * n);
+  }
+  // the 1-byte levels are always copied: k_prep_slots stages them in whole 4-byte words
+  ALLOC(f->d_level, sizeof(int8_t) * ((n + 3) & ~(int64_t)3));
   ALLOC(f->d_flag, sizeof(int32_t) * n);
   ALLOC(f->d_rect_all, sizeof(Rect16) * n);
   ALLOC(f->d_scan, sizeof(int64_t) * (n + 1));
@@ -154,11 +164,12 @@ extern "C" rc_status rc_forest_create(const rc_forest_desc* d, void* stream, rc_
   f->scan_tmp_cap = std::max<int64_t>((int64_t)scan_tmp_size(n + 1) + 64, 256);
   ALLOC(f->d_scan_tmp, sizeof(int64_t) * f->scan_tmp_cap);
 #undef ALLOC
-  cudaMemcpyKind kind = d->memory == RC_DEVICE_COPY ? cudaMemcpyDeviceToDevice : cudaMemcpyHostToDevice;
-  if ((e = cudaMemcpyAsync(f->d_anchor, d->leaf_anchor, sizeof(int32_t) * 3 * n, kind, s)) ||
-      (e = cudaMemcpyAsync(f->d_tree, d->leaf_tree, sizeof(int32_t) * n, kind, s)) ||
+  cudaMemcpyKind kind = (d->memory == RC_DEVICE_COPY || f->borrowed) ? cudaMemcpyDeviceToDevice : cudaMemcpyHostToDevice;
+  if ((!f->borrowed && (e = cudaMemcpyAsync(f->d_anchor, d->leaf_anchor, sizeof(int32_t) * 3 * n, kind, s))) ||
+      (!f->borrowed && (e = cudaMemcpyAsync(f->d_tree, d->leaf_tree, sizeof(int32_t) * n, kind, s))) ||
       (e = cudaMemcpyAsync(f->d_level, d->leaf_level, sizeof(int8_t) * n, kind, s)) ||
-      (f->has_field && (e = cudaMemcpyAsync(f->d_field, d->leaf_field, sizeof(float) * NF * n, kind, s))) ||
+      (!f->borrowed && f->has_field &&
+       (e = cudaMemcpyAsync(f->d_field, d->leaf_field, sizeof(float) * NF * n, kind, s))) ||
       (e = cudaMemsetAsync(f->d_counters, 0, sizeof(int64_t) * CNT_TOTAL, s)))
     return cleanup(RC_ERR_CUDA, "cudaMemcpyAsync leaves");
   // host copy of the tree control points for rc_camera_set
@@ -175,7 +186,11 @@ extern "C" rc_status rc_forest_create(const rc_forest_desc* d, void* stream, rc_
 
 extern "C" rc_status rc_forest_destroy(rc_forest* f) {
   if (!f) return RC_OK;
-  cudaDeviceSynchronize();   // blocks go back to the caching pool: no kernel may still use them
+  // blocks go back to the caching pool: no kernel may still use them.  One forest is driven from
+  // one stream at a time (rc.h), so its last stream holds all its pending work.
+  if (f->last_stream) cudaStreamSynchronize(f->last_stream);
+  else cudaDeviceSynchronize();
+  if (f->borrowed) f->d_anchor = f->d_tree = nullptr, f->d_field = nullptr;   // the caller's
   void* ptrs[] = {f->d_anchor, f->d_tree, f->d_level, f->d_field, f->d_flag, f->d_rect_all, f->d_scan,
                   f->d_vis, f->d_vis_rect, f->d_chunk_off, f->d_counters, f->d_trees, f->d_cam,
                   f->d_scan_tmp, f->d_chunk_elem, f->d_segs, f->d_hits_pp, f->d_pix_cnt, f->d_pix_off,
@@ -277,6 +292,7 @@ static void mat3_inv(const double A[9], double inv[9], double* det_out) {
 
 extern "C" rc_status rc_camera_set(rc_forest* f, const rc_camera* cam, void* stream) {
   RC_NVTX("rc_camera_set");
+  if (f) f->last_stream = (cudaStream_t)stream;
   if (!f || !cam) return fail(RC_ERR_INVALID_ARG, "rc_camera_set: null argument");
   auto dot = [](const double* a, const double* b) { return a[0] * b[0] + a[1] * b[1] + a[2] * b[2]; };
   double n = sqrt(dot(cam->view, cam->view));
@@ -493,6 +509,7 @@ extern "C" rc_status rc_cull(rc_forest* f, void* stream, int64_t* d_num_visible)
 }
 
 extern "C" rc_status rc_leaf_weights(rc_forest* f, int64_t* d_w, int64_t capacity, void* stream) {
+  if (f) f->last_stream = (cudaStream_t)stream;
   if (!f || !d_w) return fail(RC_ERR_INVALID_ARG, "rc_leaf_weights: null argument");
   if (!f->have_cull) return fail(RC_ERR_STATE, "rc_leaf_weights before rc_cull");
   if (capacity < f->n) return fail(RC_ERR_CAPACITY, "rc_leaf_weights: capacity %lld < %lld leaves",
@@ -502,6 +519,7 @@ extern "C" rc_status rc_leaf_weights(rc_forest* f, int64_t* d_w, int64_t capacit
 }
 
 extern "C" rc_status rc_cull_result(rc_forest* f, int32_t* d_visible, int64_t capacity, int64_t* count, void* stream) {
+  if (f) f->last_stream = (cudaStream_t)stream;
   if (!f || !count) return fail(RC_ERR_INVALID_ARG, "rc_cull_result: null argument");
   if (!f->have_cull) return fail(RC_ERR_STATE, "rc_cull_result before rc_cull");
   cudaStream_t s = (cudaStream_t)stream;
@@ -533,6 +551,7 @@ static rc_status aggregate_to(rc_forest* f, int level, cudaStream_t s);
 
 extern "C" rc_status rc_cast_segments(rc_forest* f, int32_t fold_levels, void* stream) {
   RC_NVTX("rc_cast_segments");
+  if (f) f->last_stream = (cudaStream_t)stream;
   if (!f) return fail(RC_ERR_INVALID_ARG, "rc_cast_segments: null forest");
   if (!f->have_cull) return fail(RC_ERR_STATE, "rc_cast_segments before rc_cull");
   if (!f->has_field) return fail(RC_ERR_STATE, "rc_cast_segments on a forest without a field (keys only)");
@@ -754,6 +773,7 @@ extern "C" float rc_last_phase_ms(rc_forest* f, int32_t phase) {
 }
 
 extern "C" rc_status rc_segments_get(rc_forest* f, rc_segments* out, void* stream) {
+  if (f) f->last_stream = (cudaStream_t)stream;
   if (!f || !out) return fail(RC_ERR_INVALID_ARG, "rc_segments_get: null argument");
   if (!f->have_cast) return fail(RC_ERR_STATE, "rc_segments_get before rc_cast_segments");
   cudaStream_t s = (cudaStream_t)stream;
@@ -816,6 +836,7 @@ static rc_status pack_device(rc_forest* f, const rc_tiling* t, cudaStream_t s) {
 
 extern "C" rc_status rc_pack_tiles(rc_forest* f, const rc_tiling* t, int64_t* h_send_counts, const rc_seg** d_send,
                                    void* stream) {
+  if (f) f->last_stream = (cudaStream_t)stream;
   if (!f || !h_send_counts || !d_send) return fail(RC_ERR_INVALID_ARG, "rc_pack_tiles: null argument");
   if (!f->have_cast) return fail(RC_ERR_STATE, "rc_pack_tiles before rc_cast_segments");
   rc_status st = check_tiling(f, t);
@@ -833,6 +854,7 @@ extern "C" rc_status rc_composite_records(rc_forest* f, const rc_tiling* t, cons
                                           const float background[3], float* d_rgba, int64_t capacity_floats,
                                           void* stream) {
   RC_NVTX("rc_composite_records");
+  if (f) f->last_stream = (cudaStream_t)stream;
   if (!f || !d_rgba) return fail(RC_ERR_INVALID_ARG, "rc_composite_records: null argument");
   if (!f->have_camera) return fail(RC_ERR_STATE, "rc_composite_records before rc_camera_set");
   if (nrecv < 0 || (nrecv > 0 && !d_recv)) return fail(RC_ERR_INVALID_ARG, "rc_composite_records: bad records");
@@ -931,6 +953,7 @@ extern "C" rc_status rc_composite_records(rc_forest* f, const rc_tiling* t, cons
 extern "C" rc_status rc_composite_tiles(rc_forest* f, const rc_tiling* t, rc_comm* comm, const float background[3],
                                         float* d_rgba, int64_t capacity_floats, void* stream) {
   RC_NVTX("rc_composite_tiles");
+  if (f) f->last_stream = (cudaStream_t)stream;
   if (!f || !t) return fail(RC_ERR_INVALID_ARG, "rc_composite_tiles: null argument");
   if (!comm) return rc_composite_records(f, t, nullptr, 0, background, d_rgba, capacity_floats, stream);
   if (!f->have_cast) return fail(RC_ERR_STATE, "rc_composite_tiles before rc_cast_segments");
@@ -987,6 +1010,7 @@ extern "C" rc_status rc_composite_tiles(rc_forest* f, const rc_tiling* t, rc_com
 
 extern "C" rc_status rc_composite(rc_forest* f, const float background[3], float* d_rgba, int64_t capacity_floats,
                                   void* stream) {
+  if (f) f->last_stream = (cudaStream_t)stream;
   if (!f) return fail(RC_ERR_INVALID_ARG, "rc_composite: null forest");
   rc_tiling t{1, 1, 1, 0};
   return rc_composite_records(f, &t, nullptr, 0, background, d_rgba, capacity_floats, stream);
@@ -1057,6 +1081,7 @@ static rc_status aggregate_to(rc_forest* f, int level, cudaStream_t s) {
 
 extern "C" rc_status rc_aggregate(rc_forest* f, int32_t cycles, void* stream) {
   RC_NVTX("rc_aggregate");
+  if (f) f->last_stream = (cudaStream_t)stream;
   if (!f) return fail(RC_ERR_INVALID_ARG, "rc_aggregate: null forest");
   if (cycles < 0) return fail(RC_ERR_INVALID_ARG, "cycles must be >= 0");
   if (cycles == 0) return RC_OK;
@@ -1069,6 +1094,7 @@ extern "C" rc_status rc_aggregate(rc_forest* f, int32_t cycles, void* stream) {
 
 extern "C" rc_status rc_segments_set(rc_forest* f, const rc_seg* d_recs, int64_t n, int32_t level, void* stream) {
   RC_NVTX("rc_segments_set");
+  if (f) f->last_stream = (cudaStream_t)stream;
   if (!f || (n > 0 && !d_recs) || n < 0) return fail(RC_ERR_INVALID_ARG, "rc_segments_set: bad arguments");
   if (!f->have_camera) return fail(RC_ERR_STATE, "rc_segments_set before rc_camera_set");
   if (level < 0 || level > RC_NODE_LEVELS) return fail(RC_ERR_INVALID_ARG, "level must be in [0, %d]", RC_NODE_LEVELS);
@@ -1086,6 +1112,7 @@ extern "C" rc_status rc_segments_set(rc_forest* f, const rc_seg* d_recs, int64_t
 
 extern "C" rc_status rc_debug_pair(rc_forest* f, int64_t local_leaf, int32_t i, int32_t j, rc_pair_result* out,
                                    void* stream) {
+  if (f) f->last_stream = (cudaStream_t)stream;
   if (!f || !out) return fail(RC_ERR_INVALID_ARG, "rc_debug_pair: null argument");
   if (!f->have_camera) return fail(RC_ERR_STATE, "rc_debug_pair before rc_camera_set");
   if (local_leaf < 0 || local_leaf >= f->n || i < 0 || j < 0 || i >= f->cc.W || j >= f->cc.H)
@@ -1165,6 +1192,7 @@ extern "C" rc_status rc_debug_pair(rc_forest* f, int64_t local_leaf, int32_t i, 
 
 extern "C" rc_status rc_node_table(rc_forest* f, int32_t level, int32_t* d_first, int64_t capacity, int64_t* count,
                                    void* stream) {
+  if (f) f->last_stream = (cudaStream_t)stream;
   if (!f || !count) return fail(RC_ERR_INVALID_ARG, "rc_node_table: null argument");
   if (level < 1 || level > RC_NODE_LEVELS) return fail(RC_ERR_INVALID_ARG, "level must be in [1, %d]", RC_NODE_LEVELS);
   *count = f->n_nodes[level];
@@ -1220,6 +1248,7 @@ static rc_status enqueue_affine_frame(rc_forest* f, const float bg[3], float* d_
 
 extern "C" rc_status rc_frame_capture(rc_forest* f, const rc_camera* cam, const float background[3], float* d_rgba,
                                       int64_t capacity_floats, void* stream) {
+  if (f) f->last_stream = (cudaStream_t)stream;
   if (!f || !cam || !d_rgba) return fail(RC_ERR_INVALID_ARG, "rc_frame_capture: null argument");
   cudaStream_t s = (cudaStream_t)stream;
   rc_status st = rc_render_frame(f, cam, 0, 0, background, d_rgba, capacity_floats, nullptr, stream);
@@ -1240,7 +1269,9 @@ extern "C" rc_status rc_frame_capture(rc_forest* f, const rc_camera* cam, const 
   if (!f->cap_stream) CU(cudaStreamCreateWithFlags(&f->cap_stream, cudaStreamNonBlocking));
   cudaStream_t cs = f->cap_stream;
   CU(cudaStreamBeginCapture(cs, cudaStreamCaptureModeThreadLocal));
+  const int64_t k0 = g_launches.load();
   st = enqueue_affine_frame(f, bg, d_rgba, cs);
+  f->graph_kernels = g_launches.load() - k0;   // kernel nodes of the graph (counted again per replay)
   cudaGraph_t g = nullptr;
   cudaError_t e = cudaStreamEndCapture(cs, &g);
   if (st) {
@@ -1256,9 +1287,11 @@ extern "C" rc_status rc_frame_capture(rc_forest* f, const rc_camera* cam, const 
 
 extern "C" rc_status rc_frame_replay(rc_forest* f, void* stream) {
   RC_NVTX("rc_frame_replay");
+  if (f) f->last_stream = (cudaStream_t)stream;
   if (!f) return fail(RC_ERR_INVALID_ARG, "rc_frame_replay: null forest");
   if (!f->graph_exec) return fail(RC_ERR_STATE, "rc_frame_replay before rc_frame_capture");
   CU(cudaGraphLaunch(f->graph_exec, (cudaStream_t)stream));
+  g_launches += f->graph_kernels;
   return RC_OK;
 }
 
@@ -1266,6 +1299,7 @@ extern "C" rc_status rc_render_frame(rc_forest* f, const rc_camera* cam, int32_t
                                      const float background[3], float* d_rgba, int64_t capacity_floats,
                                      int64_t* hit_pairs, void* stream) {
   RC_NVTX("rc_render_frame");
+  if (f) f->last_stream = (cudaStream_t)stream;
   rc_status st;
   if ((st = rc_camera_set(f, cam, stream))) return st;
   if ((st = rc_cull(f, stream, nullptr))) return st;

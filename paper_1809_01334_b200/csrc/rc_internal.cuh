@@ -121,6 +121,8 @@ struct rc_forest {
   int K, R, P;
   int64_t n, first_global;
   bool has_field = true;           // false: keys-only forest (aggregation / partition bookkeeping)
+  bool borrowed = false;           // RC_DEVICE_BORROW: d_anchor / d_tree / d_field are the caller's
+  cudaStream_t last_stream = nullptr;   // stream of the last call (one forest per stream at a time)
   bool surface = false;            // dim = 2: quadtree leaves on bilinear patches (surface.cu)
   rc_surface surf{};
   rc_transfer transfer;
@@ -168,6 +170,7 @@ struct rc_forest {
   int64_t* h_xcnt = nullptr;       // pinned copy
   TreeConst* h_trees_pin = nullptr; // graph frames: pinned camera constants of the captured frame
   cudaGraphExec_t graph_exec = nullptr;
+  int64_t graph_kernels = 0;       // kernel launches one replay of graph_exec makes
   cudaStream_t cap_stream = nullptr;
   // scan scratch
   int64_t* d_scan_tmp = nullptr;

@@ -65,6 +65,7 @@ unsigned blocks(int64_t n) { return (unsigned)((n + 255) / 256); }
 }  // namespace
 
 extern "C" rc_status rc_visible_area_add(rc_forest* f, int64_t* d_w, int64_t capacity, void* stream) {
+  if (f) f->last_stream = (cudaStream_t)stream;
   if (!f || !d_w) return rc_fail(RC_ERR_INVALID_ARG, "rc_visible_area_add: null argument");
   if (!f->have_cull) return rc_fail(RC_ERR_STATE, "rc_visible_area_add before rc_cull");
   if (capacity < f->n)
@@ -158,6 +159,7 @@ extern "C" rc_status rc_vforest_create(rc_forest* f, const int64_t* d_w, int64_t
 
 extern "C" rc_status rc_forest_leaves(rc_forest* f, int32_t* d_anchor, int32_t* d_tree, int8_t* d_level,
                                       float* d_field, int64_t capacity, void* stream) {
+  if (f) f->last_stream = (cudaStream_t)stream;
   if (!f) return rc_fail(RC_ERR_INVALID_ARG, "rc_forest_leaves: null forest");
   if (capacity < f->n)
     return rc_fail(RC_ERR_CAPACITY, "rc_forest_leaves: capacity %lld < %lld leaves", (long long)capacity,

@@ -17,7 +17,7 @@ RC_ERR_CAPACITY = -6
 STATUS_NAMES = {0: "RC_OK", -1: "RC_ERR_INVALID_ARG", -2: "RC_ERR_NOT_SFC_SORTED", -3: "RC_ERR_OUT_OF_MEMORY",
                 -4: "RC_ERR_CUDA", -5: "RC_ERR_NCCL", -6: "RC_ERR_CAPACITY", -7: "RC_ERR_STATE",
                 -8: "RC_ERR_NUMERIC"}
-RC_HOST_COPY, RC_DEVICE_COPY, RC_HOST_COPY_TRUSTED = 0, 1, 2
+RC_HOST_COPY, RC_DEVICE_COPY, RC_HOST_COPY_TRUSTED, RC_DEVICE_BORROW = 0, 1, 2, 3
 RC_PERSPECTIVE, RC_ORTHOGRAPHIC = 0, 1
 SCHEMES = {"gl": 0, "euler": 1, "heun2": 2, "heun3": 3, "rk4": 4, "gauss2": 5, "simpson": 6}   # RC_SCHEME_*
 
@@ -195,7 +195,8 @@ class Forest:
     (device copy); they are copied by rc_forest_create."""
 
     def __init__(self, tree_ctrl, geom_degree, field_degree, leaf_anchor, leaf_tree, leaf_level, leaf_field,
-                 kappa0, inv_F, q0, first_global_leaf=0, stream=None, trusted=False, dim=3, surface=None):
+                 kappa0, inv_F, q0, first_global_leaf=0, stream=None, trusted=False, dim=3, surface=None,
+                 borrow=False):
         import torch
         L = lib()
         ctrl = np.ascontiguousarray(tree_ctrl if isinstance(tree_ctrl, np.ndarray) else tree_ctrl.cpu().numpy(),
@@ -207,7 +208,7 @@ class Forest:
                     leaf_level.contiguous().to(torch.int8),
                     None if leaf_field is None else leaf_field.contiguous().to(torch.float32)]
             ptrs = [0 if t is None else t.data_ptr() for t in keep]
-            mem = RC_DEVICE_COPY
+            mem = RC_DEVICE_BORROW if borrow else RC_DEVICE_COPY
         else:
             def npy(a, dt):
                 a = a.cpu().numpy() if isinstance(a, torch.Tensor) else a
@@ -232,25 +233,29 @@ class Forest:
         h = C.c_void_p()
         _check(L.rc_forest_create(C.byref(desc), _stream(stream), C.byref(h)))
         self.h = h
+        self._borrowed = keep if (on_dev and borrow) else None   # RC_DEVICE_BORROW: alive as long as the forest
         self.cam = None
 
     @classmethod
-    def from_scene(cls, scene, first=0, count=None, device_copy=False, stream=None):
-        """Build from a scenegen.Scene-like object (attributes only, duck typed)."""
+    def from_scene(cls, scene, first=0, count=None, device_copy=False, stream=None, borrow=False):
+        """Build from a scenegen.Scene-like object (attributes only, duck typed).
+        borrow: the leaves go to the device once and the forest uses them in
+        place (RC_DEVICE_BORROW)."""
         import torch
         hi = scene.num_leaves if count is None else first + count
         arrs = [scene.leaf_anchor[first:hi], scene.leaf_tree[first:hi], scene.leaf_level[first:hi],
                 scene.leaf_field[first:hi]]
-        if device_copy:
+        if device_copy or borrow:
             arrs = [torch.as_tensor(np.ascontiguousarray(a) if isinstance(a, np.ndarray) else a).cuda() for a in arrs]
         return cls(scene.tree_ctrl, scene.geom_degree, scene.field_degree, *arrs, scene.kappa0, scene.inv_F,
                    scene.q0, first_global_leaf=first, stream=stream, dim=getattr(scene, "dim", 3),
-                   surface=getattr(scene, "surface", None))
+                   surface=getattr(scene, "surface", None), borrow=borrow)
 
     def close(self):
         if getattr(self, "h", None):
             lib().rc_forest_destroy(self.h)
             self.h = None
+        self._borrowed = None
 
     def __del__(self):
         try:

@@ -222,3 +222,24 @@ def test_graph_frame_replay_equals_frame(which):
     ores = o.render(mode="exact", with_hits=False)
     clean = ores["namb"] == 0
     assert np.abs(img.cpu().numpy().reshape(-1, 4)[clean] - ores["rgba"][clean]).max() < 1e-4
+
+
+def test_device_borrow_equals_copy():
+    """RC_DEVICE_BORROW: the forest renders from the caller's
+    device arrays in place (levels copied) and gives the copy forest's image
+    and records bit for bit; the binding keeps the arrays alive."""
+    import gc
+    import torch
+    from paper_1809_01334_b200 import rc
+    for sc, fold in ((sg.config2(width=64, maxlevel=5), 0), (sg.shell_uniform(2, 48, 8, gl_points=6), 2)):
+        fb = rc.Forest.from_scene(sc, borrow=True)
+        gc.collect()
+        fc = rc.Forest.from_scene(sc, device_copy=True)
+        ib, hb = fb.render_frame(sc.camera, fold_levels=fold)
+        ic, hc = fc.render_frame(sc.camera, fold_levels=fold)
+        torch.cuda.synchronize()
+        assert hb == hc and torch.equal(ib, ic)
+        rb, rcp = fb.segments()["raw"], fc.segments()["raw"]
+        assert torch.equal(rb[:, 0].sort().values, rcp[:, 0].sort().values)
+        fb.close()
+        fc.close()
