@@ -857,7 +857,8 @@ template <int CAP, bool FROM_LIST, int NW>
 __global__ void __launch_bounds__(NW * 32, CAP <= 512 ? FOLD_MINB : 1) k_fold(
     const rc_seg* __restrict__ recs, const uint32_t* __restrict__ perm, const int64_t* __restrict__ off, int W,
     int H, int tw, int th, const int32_t* __restrict__ my_tiles, int tiles_x, int64_t npix_out, float bg0, float bg1,
-    float bg2, float tau, float* __restrict__ rgba, int32_t* __restrict__ defer, int64_t* __restrict__ counters) {
+    float bg2, float tau, float* __restrict__ rgba, int32_t* __restrict__ defer, int64_t* __restrict__ counters,
+    int pps) {
   extern __shared__ unsigned char smem_raw[];
   const int warp = threadIdx.x >> 5;
   const unsigned lane = threadIdx.x & 31;
@@ -873,17 +874,17 @@ __global__ void __launch_bounds__(NW * 32, CAP <= 512 ? FOLD_MINB : 1) k_fold(
     const int tx = tile % tiles_x, ty = tile / tiles_x;
     return (int64_t)(ty * th + rem / tw) * W + (tx * tw + rem % tw);
   };
-  // 32 output pixels per warp step: a lane finishes its pixel alone when it
-  // has at most one record (no ordering needed); the others are folded one
-  // at a time by the whole warp below
-  const int64_t nsteps = FROM_LIST ? nq : (nq + 31) / 32;
+  // pps (32, or 1 for small images) output pixels per warp step: a lane
+  // finishes its pixel alone when it has at most one record (no ordering
+  // needed); the others are folded one at a time by the whole warp below
+  const int64_t nsteps = FROM_LIST ? nq : (nq + pps - 1) / pps;
   for (int64_t st = (int64_t)blockIdx.x * NW + warp; st < nsteps; st += (int64_t)gridDim.x * NW) {
     unsigned todo = 1u;
     int64_t my_q = 0, my_pix = 0, my_base = 0;
     int my_n = 0;
     if (!FROM_LIST) {
-      my_q = st * 32 + lane;
-      if (my_q < nq) {
+      my_q = st * pps + lane;
+      if ((int)lane < pps && my_q < nq) {
         my_pix = locate(my_q);
         my_base = off[my_pix];
         my_n = (int)(off[my_pix + 1] - my_base);
@@ -898,7 +899,7 @@ __global__ void __launch_bounds__(NW * 32, CAP <= 512 ? FOLD_MINB : 1) k_fold(
                           (float)(1.0 - a1.A));
         }
       }
-      todo = __ballot_sync(0xffffffffu, my_q < nq && my_n > 1);
+      todo = __ballot_sync(0xffffffffu, (int)lane < pps && my_q < nq && my_n > 1);
     }
   while (todo) {
     const int src = __ffs(todo) - 1;
@@ -1598,7 +1599,8 @@ cudaError_t launch_coarsen(const rc_seg* recs, int64_t nrec, int64_t nleaf, cons
 template <int CAP, bool FROM_LIST, int NW>
 static cudaError_t fold_pass(const rc_seg* recs, const uint32_t* perm, const int64_t* off, int W, int H, int tw,
                              int th, const int32_t* my_tiles, int tiles_x, int64_t npix_out, const float bg[3],
-                             float tau, float* rgba, int32_t* defer, int64_t* counters, int grid, cudaStream_t s) {
+                             float tau, float* rgba, int32_t* defer, int64_t* counters, int grid, int pps,
+                             cudaStream_t s) {
   static bool attr = false;
   const size_t smem = (size_t)NW * CAP * (sizeof(uint64_t) + sizeof(uint16_t));
   if (!attr) {
@@ -1608,7 +1610,7 @@ static cudaError_t fold_pass(const rc_seg* recs, const uint32_t* perm, const int
     attr = true;
   }
   k_fold<CAP, FROM_LIST, NW><<<grid, NW * 32, smem, s>>>(recs, perm, off, W, H, tw, th, my_tiles, tiles_x, npix_out,
-                                                         bg[0], bg[1], bg[2], tau, rgba, defer, counters);
+                                                         bg[0], bg[1], bg[2], tau, rgba, defer, counters, pps);
   ++g_launches;
   return cudaGetLastError();
 }
@@ -1616,15 +1618,19 @@ static cudaError_t fold_pass(const rc_seg* recs, const uint32_t* perm, const int
 cudaError_t launch_fold(const rc_seg* recs, const uint32_t* perm, const int64_t* off, int W, int H, int tw, int th,
                         const int32_t* my_tiles, int tiles_x, int64_t npix_out, const float bg[3], float tau,
                         float* rgba, int32_t* defer, int64_t* counters, int max_grid, cudaStream_t s) {
-  const int grid = (int)std::min<int64_t>((npix_out + FOLD_WARPS - 1) / FOLD_WARPS, (int64_t)max_grid);
+  // small images (C1: 4096 pixels) get one pixel per warp step, so that every
+  // pixel's fold runs in its own warp (32 per step left most of the GPU idle)
+  const int pps = npix_out < ((int64_t)1 << 17) ? 1 : 32;
+  const int grid = (int)std::min<int64_t>((npix_out + (int64_t)FOLD_WARPS * pps - 1) / ((int64_t)FOLD_WARPS * pps),
+                                          (int64_t)max_grid);
   cudaError_t e = cudaMemsetAsync(counters + CNT_DEFER, 0, sizeof(int64_t), s);
   if (e != cudaSuccess) return e;
   e = fold_pass<512, false, FOLD_WARPS>(recs, perm, off, W, H, tw, th, my_tiles, tiles_x, npix_out, bg, tau, rgba,
-                                        defer, counters, grid, s);
+                                        defer, counters, grid, pps, s);
   if (e != cudaSuccess) return e;
   // the deferred pixels (n > 512): a fixed grid reading the list length on the device
   return fold_pass<FOLD_CAP_LIST, true, 1>(recs, perm, off, W, H, tw, th, my_tiles, tiles_x, npix_out, bg, tau, rgba,
-                                           defer, counters, std::min(grid, 296), s);
+                                           defer, counters, std::min(grid, 296), 1, s);
 }
 
 }  // namespace rc
