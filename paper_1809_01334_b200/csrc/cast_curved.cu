@@ -449,9 +449,6 @@ __device__ __noinline__ int face_roots_subdiv(const Patch& root, float tol, int 
 #ifndef RC_CAST_CTAS
 #define RC_CAST_CTAS 2
 #endif
-#ifndef RC_EARLY2
-#define RC_EARLY2 0
-#endif
 constexpr int CWARPS = RC_CWARPS;   // warps per CTA
 constexpr float FAST_Q = 0.7f;       // contraction bound below which a face root takes the certified fast path
 constexpr int CAST_CTAS_PER_SM = RC_CAST_CTAS;  // resident CTAs per SM (launch bounds: 168 registers)
@@ -510,9 +507,7 @@ struct CastCtl {
   int64_t unit;
   int64_t ubeg, uend;          // this launch's unit range (the batch's units)
   int next_chunk;
-  int nitems;                  // items reserved (phase 1)
-  int written;                 // items written (RC_EARLY2: integration may start before the barrier)
-  int next_group;              // phase 2: next group of 32 items
+  int nitems;
   unsigned long long base;
   int warp_sum[CWARPS];
   int bb[4];                   // unit pixel bounding rectangle: -i0, i1, -j0, j1 (atomicMax)
@@ -982,7 +977,7 @@ __device__ __forceinline__ bool prefilter_f32(const CastSmem& S, const CamConst&
 }
 
 __device__ __forceinline__ void isect_chunk(WarpIsect& W, CastSmem& S, const CamConst& cc, int nvis, int vfirst,
-                                            int g, float4* __restrict__ items, int* s_nitems, int* s_written,
+                                            int g, float4* __restrict__ items, int* s_nitems,
                                             int32_t* __restrict__ hits_pp, int& local_hits, int& face_fail) {
   const unsigned lane = threadIdx.x & 31;
   const float tol = cc.newton_tol;
@@ -1228,16 +1223,6 @@ __device__ __forceinline__ void isect_chunk(WarpIsect& W, CastSmem& S, const Cam
     ++slot;
   }
   __syncwarp();   // W is reused by the warp's next chunk
-#if RC_EARLY2
-  // release: this chunk's items are written (warps that ran out of chunks may integrate them)
-  const int tot = __reduce_add_sync(0xffffffffu, nseg);
-  if (lane == 0 && tot > 0) {
-    __threadfence_block();
-    atomicAdd(s_written, tot);
-  }
-#else
-  (void)s_written;
-#endif
 }
 
 // ---- phase 2 with the paper's integrators (rc_camera.scheme, Alg. 1) ---------
@@ -1319,7 +1304,7 @@ template <int P, int N, bool ADAPT>
 __device__ __forceinline__ void integ_item(const float* __restrict__ gs, const CamConst& cc, float4 i0, float4 i1,
                                            float4 i2, float* __restrict__ scr, int& fails, int& capped, float& a_out,
                                            float b_out[3]) {
-  constexpr int ST = RC_EARLY2 ? 32 : CWARPS * 32;   // RC_EARLY2: per-warp node values
+  constexpr int ST = CWARPS * 32;
   const float tol = cc.newton_tol;
   const int max_it = cc.newton_max;
   const float* fs = gs + SLOT_FIELD;
@@ -1653,8 +1638,6 @@ __global__ void __launch_bounds__(CWARPS * 32, CAST_CTAS_PER_SM) k_cast_curved(C
       ctl.unit = ctl.ubeg + (int64_t)atomicAdd((unsigned long long*)&counters[CNT_UNITS], 1ull);
       ctl.next_chunk = 0;
       ctl.nitems = 0;
-      ctl.written = 0;
-      ctl.next_group = 0;
     }
     __syncthreads();
     const int64_t u = ctl.unit;
@@ -1763,8 +1746,7 @@ __global__ void __launch_bounds__(CWARPS * 32, CAST_CTAS_PER_SM) k_cast_curved(C
           if (32 + (int)lane < qn) W.queue[lane] = rest;
           qn = qn > 32 ? qn - 32 : 0;
           __syncwarp();
-          isect_chunk(W, S, cc, U.nvis, U.vfirst, gq, items, &ctl.nitems, &ctl.written, hits_pp, local_hits,
-                      face_fail);
+          isect_chunk(W, S, cc, U.nvis, U.vfirst, gq, items, &ctl.nitems, hits_pp, local_hits, face_fail);
         } else if (drained) {
           break;
         }
@@ -1774,81 +1756,6 @@ __global__ void __launch_bounds__(CWARPS * 32, CAST_CTAS_PER_SM) k_cast_curved(C
         n_fallback += W.stats[1];
       }
     }
-#if RC_EARLY2
-    // ---- phase 2: integration ---------------------------------------------------
-    // pass 0 (before the barrier): a warp out of chunks integrates full groups
-    // of 32 items whose writes are released (written == reserved, read in that
-    // order); pass 1 (after it): the remaining groups, claimed from the same counter.
-    // Node values live in the warp's own (dead) root scratch.
-    const int ubi0 = -ctl.bb[0], ubj0 = -ctl.bb[2];
-    int nitems = ITEM_CAP;
-    for (int pass = 0; pass < 2; ++pass) {
-      if (pass == 1) {
-        __syncthreads();
-        nitems = min(ctl.nitems, ITEM_CAP);
-      }
-      for (;;) {
-        int g = -1;
-        if (lane == 0) {
-          if (pass == 0) {
-            const int wr = atomicAdd(&ctl.written, 0);
-            __threadfence_block();
-            const int rs = atomicAdd(&ctl.nitems, 0);
-            if (wr == rs) {
-              const int avail = min(rs, ITEM_CAP) >> 5;
-              int cur = *(volatile int*)&ctl.next_group;
-              while (cur < avail) {
-                const int old = atomicCAS(&ctl.next_group, cur, cur + 1);
-                if (old == cur) {
-                  g = cur;
-                  break;
-                }
-                cur = old;
-              }
-            }
-            __threadfence_block();
-          } else {
-            g = atomicAdd(&ctl.next_group, 1);
-          }
-        }
-        g = __shfl_sync(0xffffffffu, g, 0);
-        __syncwarp();
-        if (g < 0 || g * 32 >= nitems) break;
-        const int idx = g * 32 + (int)lane;
-        const bool act = idx < nitems;
-        float a = 1.0f, bb[3] = {0.f, 0.f, 0.f};
-        uint32_t pix = 0;
-        float an = 0.f, afar = 0.f;
-        int v = 0;
-        if (act) {
-          const float4* it = items + 4 * idx;
-          const float4 i0 = it[0], i1 = it[1], i2 = it[2], i3 = it[3];
-          v = __float_as_int(i3.w);
-          const uint32_t ij = __float_as_uint(i3.z);
-          // fold: pixel packed relative to the unit's rectangle; else global j W + i
-          pix = fold > 0 ? ((((ij >> 16) - (uint32_t)ubj0) << 16) | ((ij & 0xffffu) - (uint32_t)ubi0))
-                         : (ij >> 16) * (uint32_t)cc.W + (ij & 0xffffu);
-          an = i3.x;
-          afar = i3.y;
-          integ_item<P, N, ADAPT>(S.u.p.slot[v - U.vfirst], cc, i0, i1, i2, &S.u.p.ph.isect[warp].roots[0][0][0] + lane,
-                                  fails, capped, a, bb);
-        }
-        if (fold > 0) {
-          if (act) {
-            store_seg(segs + idx, pix, an, afar, a, bb, (uint32_t)v);   // key field: visible leaf (fold tie-break)
-          }
-        } else {
-          const int64_t slot = warp_append(&counters[CNT_SEGS], act ? 1 : 0);
-          if (act) {
-            if (slot < out_cap) store_seg_cs(out + slot, pix, an, afar, a, bb, key_base + (uint32_t)vis[v]);
-            else atomicAdd((unsigned long long*)&counters[CNT_OVERFLOW], 1ull);
-          }
-        }
-      }
-    }
-    raw_local += (tid == 0) ? nitems : 0;
-    prev_items = nitems;
-#else
     __syncthreads();
     const int nitems = min(ctl.nitems, ITEM_CAP);
     raw_local += (tid == 0) ? nitems : 0;
@@ -1889,7 +1796,6 @@ __global__ void __launch_bounds__(CWARPS * 32, CAST_CTAS_PER_SM) k_cast_curved(C
         }
       }
     }
-#endif
     if (fold == 0) continue;   // next unit (the loop head synchronises first)
     __syncthreads();
     // ---- phase 3: fold -----------------------------------------------------------
