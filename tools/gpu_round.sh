@@ -1,13 +1,13 @@
 #!/bin/bash
 # smoke + GPU tests + A/B bench of build variants + ncu full of the segment kernel at C3.
-# Usage: bash tools/gpu_round.sh TAG "variants" [pytest-args]
+# Usage: [PYTARGET="test files"] bash tools/gpu_round.sh TAG "variants" [pytest-args]
 set -u
 TAG=$1; VARIANTS=${2:-default}; PYARGS=${3:-}
 OUT=gpurun_out/$TAG
 mkdir -p $OUT
 python -c "import __graft_entry__ as g; g.smoke()" > $OUT/smoke.log 2>&1; echo "smoke exit $?" >> $OUT/status
 if [ "$PYARGS" != "skip" ]; then
-  timeout 1500 python -m pytest tests -m gpu -x -q -rA $PYARGS > $OUT/pytest_gpu.log 2>&1; echo "pytest exit $?" >> $OUT/status
+  timeout 1500 python -m pytest ${PYTARGET:-tests} -m gpu -x -q -rA $PYARGS > $OUT/pytest_gpu.log 2>&1; echo "pytest exit $?" >> $OUT/status
 fi
 for v in $VARIANTS; do
   if [ "$v" = default ]; then LIB=""; else LIB=$PWD/paper_1809_01334_b200/librc_$v.so; fi
