@@ -1083,13 +1083,8 @@ __device__ __forceinline__ void isect_chunk(WarpIsect& W, CastSmem& S, const Cam
       const float* sB = S.u.p.slot[W.pw[pl]];   // the task's element
       const float* af = sB + SLOT_AFF;
       const float eta2 = 2.0f * af[15];
-      const float tP0[3] = {W.ps[0][pl], W.ps[1][pl], W.ps[2][pl]};
-      const float trf[3] = {W.ps[3][pl], W.ps[4][pl], W.ps[5][pl]};
-      const float txl0[3] = {W.ps[6][pl], W.ps[7][pl], W.ps[8][pl]};
-      const float tdl[3] = {W.ps[9][pl], W.ps[10][pl], W.ps[11][pl]};
-      const float trr = W.ps[13][pl];
       const int fk = f >> 1, fside = f & 1;
-      const int fa = (fk + 1) % 3, fb = (fk + 2) % 3;
+      const int fa = fk == 2 ? 0 : fk + 1, fb = fk == 0 ? 2 : fk - 1;
       bool done = false;
       {
         // Certified fast path.  In xi~ coordinates the face is
@@ -1097,36 +1092,41 @@ __device__ __forceinline__ void isect_chunk(WarpIsect& W, CastSmem& S, const Cam
         // x = (s_a, s_b, beta) solves x = x0 - M0^-1 E(s) with M0 = [e_a, e_b, -dl];
         // the map contracts with q = ||M0^-1|| 2 eta < FAST_Q < 1 (uniqueness +
         // convergence; the exclusion was proven in 1a).
-        const float dk = tdl[fk];
+        // The axes (k, a, b) are per lane: their components are read from
+        // shared memory at computed addresses (rows of J0^-1, the pixel's ray
+        // state), never by indexing register arrays (local memory).
+        const float dk = W.ps[9 + fk][pl], dla = W.ps[9 + fa][pl], dlb = W.ps[9 + fb][pl];
+        const float xlk = W.ps[6 + fk][pl], xla = W.ps[6 + fa][pl], xlb = W.ps[6 + fb][pl];
         const float rk = 1.0f / dk;
-        const float mnorm = fmaxf(fabsf(rk), 1.0f + fabsf(tdl[fa] * rk) + fabsf(tdl[fb] * rk));
+        const float mnorm = fmaxf(fabsf(rk), 1.0f + fabsf(dla * rk) + fabsf(dlb * rk));
         const float qf = mnorm * eta2;
         if (qf < FAST_Q) {
-          const float b0 = ((float)fside - txl0[fk]) * rk;
-          const float sa0 = txl0[fa] + b0 * tdl[fa], sb0 = txl0[fb] + b0 * tdl[fb];
+          const float side = (float)fside;
+          const float b0 = (side - xlk) * rk;
+          const float sa0 = xla + b0 * dla, sb0 = xlb + b0 * dlb;
           const float qfac = qf / (1.0f - qf) * 1.01f;
           float sa = sa0, sb = sb0, bt = b0;
-          const int pstr[3] = {3, 12, 36};   // padded float stride of m1, m2, m3
-          const int fbase = 2 * fside * pstr[fk], fsa = pstr[fa], fsb = pstr[fb];
+          // padded float strides of m1, m2, m3: 3, 12, 36
+          const int pk = fk == 0 ? 3 : (fk == 1 ? 12 : 36);
+          const int fsa = fk == 0 ? 12 : (fk == 1 ? 36 : 3), fsb = fk == 0 ? 36 : (fk == 1 ? 3 : 12);
+          const int fbase = 2 * fside * pk;
+          const float* jk = af + 3 + 3 * fk;   // rows k, a, b of J0^-1
+          const float* ja = af + 3 + 3 * fa;
+          const float* jb = af + 3 + 3 * fb;
 #pragma unroll 1
           for (int it = 0; it < max_it; ++it) {
-            float xi[3];
-            xi[fk] = (float)fside;
-            xi[fa] = sa;
-            xi[fb] = sb;
             float X[3];
             eval_face(sB, fbase, fsa, fsb, sa, sb, X);
-            // E(s) = J0^-1 (X - Xc) + 1/2 - xi
+            // E(s) = J0^-1 (X - Xc) + 1/2 - xi, components k, a, b (xi = side, s_a, s_b)
             const float y0 = X[0] - af[0], y1 = X[1] - af[1], y2 = X[2] - af[2];
-            float Ev[3];
-            Ev[0] = af[3] * y0 + af[4] * y1 + af[5] * y2 + 0.5f - xi[0];
-            Ev[1] = af[6] * y0 + af[7] * y1 + af[8] * y2 + 0.5f - xi[1];
-            Ev[2] = af[9] * y0 + af[10] * y1 + af[11] * y2 + 0.5f - xi[2];
+            const float Ek = jk[0] * y0 + jk[1] * y1 + jk[2] * y2 + 0.5f - side;
+            const float Ea = ja[0] * y0 + ja[1] * y1 + ja[2] * y2 + 0.5f - sa;
+            const float Eb = jb[0] * y0 + jb[1] * y1 + jb[2] * y2 + 0.5f - sb;
             // M0^-1 y: beta = -y_k/dl_k, s_a = y_a + beta dl_a, s_b = y_b + beta dl_b
-            const float db = -Ev[fk] * rk;
+            const float db = -Ek * rk;
             const float nbt = b0 - db;
-            const float nsa = sa0 - (Ev[fa] + db * tdl[fa]);
-            const float nsb = sb0 - (Ev[fb] + db * tdl[fb]);
+            const float nsa = sa0 - (Ea + db * dla);
+            const float nsb = sb0 - (Eb + db * dlb);
             const float step = fmaxf(fabsf(nsa - sa), fmaxf(fabsf(nsb - sb), fabsf((nbt - bt) * dk)));
             sa = nsa;
             sb = nsb;
@@ -1138,16 +1138,23 @@ __device__ __forceinline__ void isect_chunk(WarpIsect& W, CastSmem& S, const Cam
             }
           }
           if (done && sa >= -FACE_TOL && sa <= 1.0f + FACE_TOL && sb >= -FACE_TOL && sb <= 1.0f + FACE_TOL) {
-            float xi[3];
-            xi[fk] = (float)fside;
-            xi[fa] = fminf(fmaxf(sa, 0.0f), 1.0f);
-            xi[fb] = fminf(fmaxf(sb, 0.0f), 1.0f);
-            push_root(W, pl, bt, xi, face_fail);
+            const int k = atomicAdd(&W.nroots[pl], 1);   // push_root with the components placed by axis
+            if (k >= MAXR) {
+              ++face_fail;
+            } else {
+              W.roots[k][0][pl] = bt;
+              W.roots[k][1 + fk][pl] = side;
+              W.roots[k][1 + fa][pl] = fminf(fmaxf(sa, 0.0f), 1.0f);
+              W.roots[k][1 + fb][pl] = fminf(fmaxf(sb, 0.0f), 1.0f);
+            }
           }
         }
       }
       if (!done) {
         ++nfallback;
+        const float tP0[3] = {W.ps[0][pl], W.ps[1][pl], W.ps[2][pl]};
+        const float trf[3] = {W.ps[3][pl], W.ps[4][pl], W.ps[5][pl]};
+        const float trr = W.ps[13][pl];
         face_2d(W, sB, pl, f, tP0, trf, trr, tol, max_it, face_fail);
       }
     }
